@@ -1,0 +1,197 @@
+/*
+ * hsd_synth.h — counter-based synthetic workload generators for the HeiSD
+ * retrieval-side hot path (SURVEY.md §8(d) "Synthetic inputs").
+ *
+ * Every value is a pure function of (seed, stream tag, counter) and is built
+ * from integer hashing plus IEEE operations that are correctly rounded on both
+ * the host and the device (integer ops, +, *, /, sqrt; no libm transcendentals,
+ * no FMA-contractible expressions).  The CUDA generator kernels and the CPU
+ * oracle therefore produce bit-identical inputs without shipping 16 GB of keys
+ * across PCIe.
+ *
+ * Two key families:
+ *   HSD_SYNTH_EXACT : key = ((h mod 17) - 8) / 16.  Exact in bf16/TF32/fp32;
+ *                     every dot product of two such vectors is exact in fp32 in
+ *                     any summation order (|sum| <= 1024 in units of 2^-8), so
+ *                     scores tie often and the (score desc, id asc) rule of
+ *                     store.cpp:67-70 is exercised.  Every 997th row duplicates
+ *                     its predecessor (forced exact ties).
+ *   HSD_SYNTH_REAL  : Irwin-Hall(4) integer vector, L2-normalised exactly:
+ *                     sum of squares in int64 (order-independent), sqrt and the
+ *                     divide in fp64, then rounded once to fp32.
+ *
+ * This header is plain C99 and compiles as CUDA (__host__ __device__).
+ */
+#ifndef HSD_SYNTH_H
+#define HSD_SYNTH_H
+
+#include <stdint.h>
+#include <math.h>
+
+#if defined(__CUDACC__)
+#define HSD_HD __host__ __device__ __forceinline__
+#else
+#define HSD_HD static inline
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HSD_SYNTH_EXACT = 0,
+  HSD_SYNTH_REAL = 1,
+};
+
+/* stream tags */
+enum {
+  HSD_TAG_KEYS = 1,
+  HSD_TAG_QUERY = 2,
+  HSD_TAG_LOGITS = 3,
+  HSD_TAG_TRAJ = 4,
+  HSD_TAG_FEAT = 5,
+  HSD_TAG_ACTIONS = 6,
+  HSD_TAG_QNOISE = 7,
+  HSD_TAG_QPICK = 8,
+};
+
+HSD_HD uint64_t hsd_splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+/* Base of one (seed, tag) counter stream. */
+HSD_HD uint64_t hsd_stream_base(uint64_t seed, uint32_t tag) {
+  return hsd_splitmix64(seed * 0xD1342543DE82EF95ull + (uint64_t)tag * 0x2545F4914F6CDD1Dull);
+}
+
+HSD_HD uint64_t hsd_hash_at(uint64_t base, uint64_t idx) { return hsd_splitmix64(base ^ (idx * 0x9E3779B97F4A7C15ull)); }
+
+/* Row that a DB row's key is generated from (duplicate rows, EXACT family). */
+HSD_HD int64_t hsd_key_src_row(int kind, int64_t row) {
+  if (kind == HSD_SYNTH_EXACT && row > 0 && (row % 997) == 996) return row - 1;
+  return row;
+}
+
+/* Irwin-Hall(4) centred integer in [-131070, 131070]. */
+HSD_HD int32_t hsd_ih4(uint64_t h) {
+  int32_t s = (int32_t)(h & 0xFFFFu) + (int32_t)((h >> 16) & 0xFFFFu) + (int32_t)((h >> 32) & 0xFFFFu) +
+              (int32_t)((h >> 48) & 0xFFFFu);
+  return s - 131070;
+}
+
+/* EXACT-family element value. */
+HSD_HD float hsd_exact_val(uint64_t h) { return (float)((int32_t)(h % 17u) - 8) * 0.0625f; }
+
+/* REAL-family raw (un-normalised) integer of key (row, col). */
+HSD_HD int32_t hsd_key_raw(uint64_t kbase, int64_t src_row, int dim, int col) {
+  return hsd_ih4(hsd_hash_at(kbase, (uint64_t)src_row * (uint64_t)dim + (uint64_t)col));
+}
+
+/* Exactly-rounded normalisation of one raw element given the int64 sum of squares. */
+HSD_HD float hsd_norm_val(int64_t raw, int64_t sumsq) {
+  double n = sqrt((double)sumsq);
+  return (float)((double)raw / n);
+}
+
+/* ---- queries -------------------------------------------------------------
+ * Query q of a batch is one of:
+ *   EXACT: 25% an exact copy of DB row r (r hashed), else a fresh EXACT vector.
+ *   REAL : 50% near-duplicate 3*raw_key(r) + noise (top-1 cosine ~0.95, in line
+ *          with PAPER.md:852), else pure noise (random unit vector).
+ * hsd_query_mode() returns the picked row for copy/near-dup queries, -1 else. */
+HSD_HD int64_t hsd_query_row(uint64_t seed, int kind, int64_t q, int64_t n_rows) {
+  uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_QPICK), (uint64_t)q);
+  uint32_t sel = (uint32_t)(h & 0xFFu);
+  int hit = (kind == HSD_SYNTH_EXACT) ? (sel < 64u) : (sel < 128u);
+  if (!hit || n_rows <= 0) return -1;
+  return (int64_t)((h >> 8) % (uint64_t)n_rows);
+}
+
+/* REAL-family raw query element (needs the picked row). */
+HSD_HD int64_t hsd_query_raw(uint64_t seed, uint64_t db_seed, int64_t q, int64_t row, int dim, int col) {
+  int64_t noise = hsd_ih4(hsd_hash_at(hsd_stream_base(seed, HSD_TAG_QNOISE), (uint64_t)q * (uint64_t)dim + col));
+  if (row < 0) return noise;
+  int64_t k = hsd_key_raw(hsd_stream_base(db_seed, HSD_TAG_KEYS), hsd_key_src_row(HSD_SYNTH_REAL, row), dim, col);
+  return 3 * k + noise;
+}
+
+/* EXACT-family query element. */
+HSD_HD float hsd_query_exact(uint64_t seed, uint64_t db_seed, int64_t q, int64_t row, int dim, int col) {
+  if (row >= 0)
+    return hsd_exact_val(hsd_hash_at(hsd_stream_base(db_seed, HSD_TAG_KEYS),
+                                     (uint64_t)hsd_key_src_row(HSD_SYNTH_EXACT, row) * (uint64_t)dim + col));
+  return hsd_exact_val(hsd_hash_at(hsd_stream_base(seed, HSD_TAG_QNOISE), (uint64_t)q * (uint64_t)dim + col));
+}
+
+/* ---- payload actions (Payload::next_actions, store.hpp:31) ---------------
+ * next_actions[s][j] for record `row`: uniform in [-1, 1) with ~1.2% of values
+ * forced to the boundary (1.0) or outside the bounds (1.5, -1.25) so that the
+ * clamp of actions.cpp:42 is exercised.  Exact doubles. */
+HSD_HD double hsd_action_val(uint64_t seed, int64_t row, int s, int j) {
+  uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_ACTIONS), (uint64_t)row * 21u + (uint64_t)(s * 7 + j));
+  uint32_t sel = (uint32_t)(h & 0xFFu);
+  if (sel == 0u) return 1.0;
+  if (sel == 1u) return 1.5;
+  if (sel == 2u) return -1.25;
+  return (double)(h >> 11) * (1.0 / 9007199254740992.0) * 2.0 - 1.0;
+}
+
+/* ---- verifier logits ------------------------------------------------------
+ * logits[e][p][b] (fp32).  Background: multiples of 1/64 in [-2, 2).  The
+ * greedy bin is draft_bin + delta with delta = 0 (50%), |delta| <= 15 (30%),
+ * |delta| in [16, 64] (20%), clamped to [0, 255]; it gets 8.0.  1% of positions
+ * get a second bin at exactly 8.0 (argmax tie -> lowest index wins). */
+HSD_HD int hsd_logit_greedy_bin(uint64_t seed, int64_t e, int p, int draft_bin) {
+  uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_LOGITS), ((uint64_t)e << 8) ^ (uint64_t)(0xF000u + p));
+  uint32_t sel = (uint32_t)(h % 100u);
+  int delta = 0;
+  if (sel < 50u) {
+    delta = 0;
+  } else if (sel < 80u) {
+    delta = (int)((h >> 8) % 31u) - 15;
+  } else {
+    int mag = 16 + (int)((h >> 8) % 49u);
+    delta = ((h >> 20) & 1u) ? mag : -mag;
+  }
+  int g = draft_bin + delta;
+  if (g < 0) g = 0;
+  if (g > 255) g = 255;
+  return g;
+}
+
+HSD_HD int hsd_logit_tie_bin(uint64_t seed, int64_t e, int p) {
+  uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_LOGITS), ((uint64_t)e << 8) ^ (uint64_t)(0xE000u + p));
+  if ((h % 100u) != 0u) return -1;
+  return (int)((h >> 8) & 0xFFu);
+}
+
+HSD_HD float hsd_logit_background(uint64_t seed, int64_t e, int p, int b) {
+  uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_LOGITS), ((uint64_t)e * 64u + (uint64_t)p) * 256u + (uint64_t)b);
+  return (float)((int32_t)(h & 0xFFu) - 128) * 0.015625f;
+}
+
+/* ---- verifier features for the verify-skip check (Alg. 1) ----------------
+ * f_now = normalise(IH4 noise); f_prev = normalise(a * raw_now + noise) with the
+ * mixing weight a swept per episode in [1, 48] so cos(f_now, f_prev) straddles
+ * typical min_S values (0.7 .. 0.9998). */
+HSD_HD int32_t hsd_feat_mix(uint64_t seed, int64_t e) {
+  uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_FEAT), (uint64_t)e ^ 0xABCDEF0000000000ull);
+  return 1 + (int32_t)(h % 48u);
+}
+
+HSD_HD int64_t hsd_feat_raw(uint64_t seed, int64_t e, int which, int dim, int col) {
+  uint64_t base = hsd_stream_base(seed, HSD_TAG_FEAT);
+  int64_t now = hsd_ih4(hsd_hash_at(base, ((uint64_t)e * 2u) * (uint64_t)dim + (uint64_t)col));
+  if (which == 0) return now;
+  int64_t noise = hsd_ih4(hsd_hash_at(base, ((uint64_t)e * 2u + 1u) * (uint64_t)dim + (uint64_t)col));
+  return (int64_t)hsd_feat_mix(seed, e) * now + noise;
+}
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HSD_SYNTH_H */

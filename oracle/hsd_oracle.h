@@ -1,0 +1,159 @@
+/*
+ * hsd_oracle.h — CPU ORACLE (test infrastructure only).
+ *
+ * A plain-C restatement of the reference's algorithms on the HeiSD
+ * retrieval-side hot path, used ONLY by tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg as the checker.  The product
+ * (libhsd_gpu.so) never links, loads or calls anything in this directory.
+ *
+ * Parity anchors:
+ *   - search / quantize are pinned against the reference itself, compiled from
+ *     /root/reference/proj/src/{store,actions,hnsw}.cpp into oracle/_ref/
+ *     (oracle/Makefile) and driven through oracle/ref_shim.cpp;
+ *   - verification / drafting / decide_sd are spec-only in the reference
+ *      and are pinned by every SPEC golden vector
+ *     (tests/test_oracle_golden.py);
+ *   - kinematics.cpp needs Eigen, which is not vendored (proj/.gitignore:2), so
+ *     it is restated Eigen-free and pinned by the SPEC/PAPER fixtures at the
+ *     reference's stated tolerances.
+ */
+#ifndef HSD_ORACLE_H
+#define HSD_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes mirror errors.hpp:10-50 (and include/hsd/hsd_gpu.h) */
+enum { HSDO_OK = 0, HSDO_INVALID_INPUT = 1, HSDO_CONFIG = 2, HSDO_SCHEMA = 3, HSDO_CALIBRATION = 7 };
+
+/* ---------------------------------------------------------------- retrieval */
+/* cosine_similarity, store.cpp:29-34: sequential fp64 sum of a[i]*b[i]. */
+double hsdo_dot_f32(const float* a, const float* b, int dim);
+
+/* Collection::search_topk_exact, store.cpp:59-73, over fp32 keys widened to
+ * fp64.  Returns the hit count min(k, n) or -HSDO_INVALID_INPUT when k < 1. */
+int hsdo_search_topk_exact(const float* keys, int64_t n, int dim, const float* query, int k, double* scores,
+                           int64_t* ids);
+
+/* Same contract over a counter-generated DB (include/hsd/hsd_synth.h) that is
+ * never materialised: every row is generated once and scored against all B
+ * queries.  `threads` <= 0 uses all cores.  Results are independent of the
+ * thread count. */
+int hsdo_search_synth(int kind, uint64_t db_seed, int64_t n, int dim, const float* queries, int B, int k,
+                      double* scores, int64_t* ids, int threads);
+
+/* Generate rows [row0, row0+n) of a synthetic DB / a query batch (fp32). */
+void hsdo_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, float* out);
+void hsdo_gen_queries(int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B, int dim,
+                      float* out);
+
+/* ------------------------------------------------------------------ actions */
+/* quantize, actions.cpp:32-50 (uniform bounds lo/hi on all 7 dims).  Returns
+ * 0, or -HSDO_CONFIG / -HSDO_INVALID_INPUT. */
+int hsdo_quantize(const double* a7, const double* lo7, const double* hi7, int k_bins, int* bins7);
+/* Payload tokens of synthetic record `row`: quantize(next_actions[s]) for
+ * s = 0..2 with bounds [-1, 1], K = 256 -> 21 bins. */
+void hsdo_synth_tokens(uint64_t db_seed, int64_t row, uint8_t* tok21);
+
+/* ------------------------------------------------------------- verification */
+typedef struct {
+  int enabled;        /* relaxed acceptance on */
+  int bias_seq_max;   /* 30 (PAPER §4.2) */
+  int bias_token_max; /* 15 */
+} hsdo_accept_params;
+
+typedef struct {
+  double T;
+  double min_S;
+  int O_dist;
+  double delta;
+  int inverted; /* update_direction = inverted */
+} hsdo_skip_state;
+
+int hsdo_token_bias(int draft_bin, int verify_bin);
+/* accept_sequence.  is_gripper selects zero tolerance. */
+int hsdo_accept_sequence(const int* draft, const int* verify, int n, int is_gripper, const hsdo_accept_params* p);
+/* argmax over `nbins` logits, lowest index on ties (Eq. 2-1). */
+int hsdo_argmax(const float* logits, int nbins);
+
+/* Exactly-rounded (double-double) dot of two fp32 feature vectors. */
+double hsdo_feature_cos(const float* a, const float* b, int dim);
+/* should_skip, SPEC.md:458-466 (history = number of stored features). */
+int hsdo_should_skip(double cos_now_prev, const hsdo_skip_state* s, int gap_d, int history);
+
+typedef struct {
+  int accept_len;    /* accepted draft tokens (excludes the fallback token) */
+  int win_a;         /* winning chain: pos0 from candidate a ... */
+  int win_b;         /* ... everything after pos0 from candidate b */
+  int fallback;      /* empty prefix -> 1 greedy verifier token */
+  int calls;         /* verifier_calls (unique chains visited) */
+  int skipped;       /* verify-skip fired: whole rank-0 draft emitted */
+  int n_emit;        /* tokens emitted */
+  int tokens[64];    /* emitted tokens */
+} hsdo_outcome;
+
+/* One retrieval-mode decode round for one episode (CS-1):
+ *   drafts   : n_cand x L tokens (rank order, L = 7 or 21)
+ *   greedy   : L verifier greedy tokens (teacher-forced, context-free)
+ *   skip     : result of should_skip for this step
+ * chains = (a, b) label assignments, enumerated in DFS /
+ * lexicographic order, duplicates (identical token sequences) dropped, capped
+ * at `cap`.  Longest accepted prefix wins, earliest chain on ties. */
+void hsdo_verify_round(const int* drafts, int n_cand, int L, const int* greedy, int skip, int cap,
+                       const hsdo_accept_params* p, hsdo_outcome* out);
+
+/* Brute-force DFS enumerator used to pin the fast path above. */
+int hsdo_enumerate_chains(const int* drafts, int n_cand, int L, int cap, int* chains_out /* cap x L */,
+                          int* a_out, int* b_out);
+
+/* offline_calibrate_skip, SPEC.md:449-457 over a cosine matrix per trajectory.
+ * sims: n x n similarity matrix (row-major) of one trajectory; returns 0 and
+ * (min_S, O_dist) or -HSDO_CALIBRATION.  Multiple trajectories: call
+ * hsdo_calibrate_accumulate then hsdo_calibrate_finish. */
+typedef struct {
+  double min_S;
+  int O_dist;
+  int found;
+} hsdo_calib;
+void hsdo_calibrate_init(hsdo_calib* c);
+void hsdo_calibrate_accumulate(hsdo_calib* c, const double* sims, int n, double T);
+int hsdo_calibrate_finish(const hsdo_calib* c, double* min_S, int* O_dist);
+/* update_skip_state */
+void hsdo_update_skip_state(hsdo_skip_state* s, int success, double S_c, double min_S_h);
+
+/* --------------------------------------------------------------- kinematics */
+typedef struct {
+  double alpha;
+  int w;
+  double threshold;
+  double r_cap;
+} hsdo_metric_params;
+
+typedef struct {
+  double d_min, d_max95, r_min, r_max95;
+} hsdo_norm_bounds;
+
+/* project_window, kinematics.cpp:38-76. xyz: n x 3; uv: n x 2 */
+int hsdo_project_window(const double* xyz, int n, double* uv);
+/* fit_circle_center, kinematics.cpp:107-207 */
+int hsdo_fit_circle_center(const double* uv, int n, double* cu, double* cv, int* degenerate, int* iterations);
+/* curvature_radius, kinematics.cpp:209-218 */
+int hsdo_curvature_radius(const double* xyz, int n, double r_cap, double* R);
+/* cumulative_displacement, kinematics.cpp:220-230 */
+int hsdo_cumulative_displacement(const double* xyz, int n, double* D);
+double hsdo_normalize(double x, double lo, double hi95);                                /* :232-236 */
+int hsdo_percentile_bounds(const double* samples, int n, double* lo, double* p95);      /* :238-247 */
+double hsdo_fused_metric(double R, double D, const hsdo_metric_params* p, const hsdo_norm_bounds* b); /* :249-255 */
+int hsdo_classify(double F, double threshold); /* :257-259; 1 = retrieval_sd, 0 = drafter_sd */
+/* window_features, kinematics.cpp:261-273; decision = decide_sd
+ * with history >= w. */
+int hsdo_window_features(const double* xyz, int n, const hsdo_metric_params* p, const hsdo_norm_bounds* b, double* R,
+                         double* D, double* F, int* decision);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

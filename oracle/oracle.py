@@ -1,0 +1,338 @@
+"""CPU ORACLE bindings (test infrastructure only).
+
+ctypes access to
+  * oracle/_build/libhsd_oracle.so — the C restatement (hsd_oracle.c), and
+  * oracle/_ref/libhsdref.so      — the reference's own store/actions/hnsw
+                                   sources compiled in place (oracle/Makefile).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs import this
+module.  The product package (paper_2603_17573_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_build", "libhsd_oracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libhsdref.so")
+
+_lib = None
+_ref = None
+
+_f = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
+_d = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_i = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_l = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_u8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+
+
+def build() -> None:
+    """Build the oracle (and oracle/_ref when /root/reference is present)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+class AcceptParams(C.Structure):
+    _fields_ = [("enabled", C.c_int), ("bias_seq_max", C.c_int), ("bias_token_max", C.c_int)]
+
+
+class SkipState(C.Structure):
+    _fields_ = [("T", C.c_double), ("min_S", C.c_double), ("O_dist", C.c_int), ("delta", C.c_double),
+                ("inverted", C.c_int)]
+
+
+class Outcome(C.Structure):
+    _fields_ = [("accept_len", C.c_int), ("win_a", C.c_int), ("win_b", C.c_int), ("fallback", C.c_int),
+                ("calls", C.c_int), ("skipped", C.c_int), ("n_emit", C.c_int), ("tokens", C.c_int * 64)]
+
+
+class Calib(C.Structure):
+    _fields_ = [("min_S", C.c_double), ("O_dist", C.c_int), ("found", C.c_int)]
+
+
+class MetricParams(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("w", C.c_int), ("threshold", C.c_double), ("r_cap", C.c_double)]
+
+
+class NormBounds(C.Structure):
+    _fields_ = [("d_min", C.c_double), ("d_max95", C.c_double), ("r_min", C.c_double), ("r_max95", C.c_double)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        L.hsdo_dot_f32.restype = C.c_double
+        L.hsdo_dot_f32.argtypes = [_f, _f, C.c_int]
+        L.hsdo_search_topk_exact.argtypes = [_f, C.c_int64, C.c_int, _f, C.c_int, _d, _l]
+        L.hsdo_search_synth.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int, _f, C.c_int, C.c_int, _d, _l, C.c_int]
+        L.hsdo_gen_keys.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_int, _f]
+        L.hsdo_gen_queries.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, _f]
+        L.hsdo_quantize.argtypes = [_d, _d, _d, C.c_int, _i]
+        L.hsdo_synth_tokens.argtypes = [C.c_uint64, C.c_int64, _u8]
+        L.hsdo_token_bias.argtypes = [C.c_int, C.c_int]
+        L.hsdo_accept_sequence.argtypes = [_i, _i, C.c_int, C.c_int, C.POINTER(AcceptParams)]
+        L.hsdo_argmax.argtypes = [_f, C.c_int]
+        L.hsdo_feature_cos.restype = C.c_double
+        L.hsdo_feature_cos.argtypes = [_f, _f, C.c_int]
+        L.hsdo_should_skip.argtypes = [C.c_double, C.POINTER(SkipState), C.c_int, C.c_int]
+        L.hsdo_verify_round.argtypes = [_i, C.c_int, C.c_int, _i, C.c_int, C.c_int, C.POINTER(AcceptParams),
+                                        C.POINTER(Outcome)]
+        L.hsdo_enumerate_chains.argtypes = [_i, C.c_int, C.c_int, C.c_int, _i, _i, _i]
+        L.hsdo_calibrate_init.argtypes = [C.POINTER(Calib)]
+        L.hsdo_calibrate_accumulate.argtypes = [C.POINTER(Calib), _d, C.c_int, C.c_double]
+        L.hsdo_calibrate_finish.argtypes = [C.POINTER(Calib), C.POINTER(C.c_double), C.POINTER(C.c_int)]
+        L.hsdo_update_skip_state.argtypes = [C.POINTER(SkipState), C.c_int, C.c_double, C.c_double]
+        L.hsdo_project_window.argtypes = [_d, C.c_int, _d]
+        L.hsdo_fit_circle_center.argtypes = [_d, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                             C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.hsdo_curvature_radius.argtypes = [_d, C.c_int, C.c_double, C.POINTER(C.c_double)]
+        L.hsdo_cumulative_displacement.argtypes = [_d, C.c_int, C.POINTER(C.c_double)]
+        L.hsdo_normalize.restype = C.c_double
+        L.hsdo_normalize.argtypes = [C.c_double, C.c_double, C.c_double]
+        L.hsdo_percentile_bounds.argtypes = [_d, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.hsdo_fused_metric.restype = C.c_double
+        L.hsdo_fused_metric.argtypes = [C.c_double, C.c_double, C.POINTER(MetricParams), C.POINTER(NormBounds)]
+        L.hsdo_classify.argtypes = [C.c_double, C.c_double]
+        L.hsdo_window_features.argtypes = [_d, C.c_int, C.POINTER(MetricParams), C.POINTER(NormBounds),
+                                           C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                           C.POINTER(C.c_int)]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        R = C.CDLL(REF_PATH)
+        R.hsdref_collection_new.restype = C.c_void_p
+        R.hsdref_collection_new.argtypes = [C.c_int]
+        R.hsdref_collection_free.argtypes = [C.c_void_p]
+        R.hsdref_collection_size.restype = C.c_long
+        R.hsdref_collection_size.argtypes = [C.c_void_p]
+        R.hsdref_insert.argtypes = [C.c_void_p, _f, _d, C.c_int64, C.c_int, C.c_int]
+        R.hsdref_insert_synth.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_int]
+        R.hsdref_search.argtypes = [C.c_void_p, _d, C.c_int, C.c_int, _d, _i, C.c_void_p]
+        R.hsdref_search_batch.argtypes = [C.c_void_p, _f, C.c_int, C.c_int, C.c_int, C.c_int, _d, _i, C.c_void_p]
+        R.hsdref_quantize.argtypes = [_d, _d, _d, C.c_int, _i]
+        R.hsdref_dequantize.argtypes = [_i, _d, _d, C.c_int, _d]
+        R.hsdref_l2_normalize.argtypes = [_d, C.c_int, _d]
+        R.hsdref_cosine.restype = C.c_double
+        R.hsdref_cosine.argtypes = [_d, _d, C.c_int]
+        _ref = R
+    return _ref
+
+
+# ---------------------------------------------------------------- helpers
+EXACT, REAL = 0, 1
+
+
+def gen_keys(kind: int, db_seed: int, row0: int, n: int, dim: int) -> np.ndarray:
+    out = np.empty((n, dim), np.float32)
+    lib().hsdo_gen_keys(kind, db_seed, row0, n, dim, out)
+    return out
+
+
+def gen_queries(kind: int, q_seed: int, db_seed: int, n_rows: int, q0: int, B: int, dim: int) -> np.ndarray:
+    out = np.empty((B, dim), np.float32)
+    lib().hsdo_gen_queries(kind, q_seed, db_seed, n_rows, q0, B, dim, out)
+    return out
+
+
+def synth_tokens(db_seed: int, rows) -> np.ndarray:
+    rows = np.asarray(rows, np.int64).ravel()
+    out = np.empty((rows.size, 21), np.uint8)
+    t = np.empty(21, np.uint8)
+    for i, r in enumerate(rows):
+        lib().hsdo_synth_tokens(db_seed, int(r), t)
+        out[i] = t
+    return out
+
+
+def search_topk(keys: np.ndarray, queries: np.ndarray, k: int):
+    """Reference search semantics on materialised fp32 keys -> (scores f64, ids i64)."""
+    keys = np.ascontiguousarray(keys, np.float32)
+    queries = np.ascontiguousarray(np.atleast_2d(queries), np.float32)
+    n, dim = keys.shape
+    B = queries.shape[0]
+    kk = min(k, n) if n else 0
+    sc = np.zeros((B, max(k, 1)), np.float64)
+    ids = np.full((B, max(k, 1)), -1, np.int64)
+    for b in range(B):
+        s = np.zeros(max(k, 1), np.float64)
+        i = np.zeros(max(k, 1), np.int64)
+        rc = lib().hsdo_search_topk_exact(keys, n, dim, queries[b], k, s, i)
+        if rc < 0:
+            raise ValueError("k must be >= 1")
+        sc[b], ids[b] = s, i
+    return sc[:, :kk], ids[:, :kk]
+
+
+def search_synth(kind: int, db_seed: int, n: int, queries: np.ndarray, k: int, threads: int = 0):
+    queries = np.ascontiguousarray(np.atleast_2d(queries), np.float32)
+    B, dim = queries.shape
+    sc = np.zeros((B, k), np.float64)
+    ids = np.full((B, k), -1, np.int64)
+    rc = lib().hsdo_search_synth(kind, db_seed, n, dim, queries, B, k, sc, ids, threads)
+    if rc < 0:
+        raise ValueError("k must be >= 1")
+    kk = min(k, n)
+    return sc[:, :kk], ids[:, :kk]
+
+
+def quantize(a7, lo=-1.0, hi=1.0, k_bins=256):
+    a = np.ascontiguousarray(a7, np.float64)
+    lo7 = np.full(7, lo, np.float64) if np.isscalar(lo) else np.ascontiguousarray(lo, np.float64)
+    hi7 = np.full(7, hi, np.float64) if np.isscalar(hi) else np.ascontiguousarray(hi, np.float64)
+    out = np.zeros(7, np.int32)
+    rc = lib().hsdo_quantize(a, lo7, hi7, k_bins, out)
+    return rc, out
+
+
+def argmax(logits) -> int:
+    return lib().hsdo_argmax(np.ascontiguousarray(logits, np.float32), len(logits))
+
+
+def feature_cos(a, b) -> float:
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b, np.float32)
+    return lib().hsdo_feature_cos(a, b, a.size)
+
+
+def should_skip(cos: float, state: SkipState, gap_d: int, history: int) -> bool:
+    return bool(lib().hsdo_should_skip(cos, C.byref(state), gap_d, history))
+
+
+def accept_sequence(draft, verify, gripper=False, enabled=True, seq_max=30, tok_max=15) -> bool:
+    d = np.ascontiguousarray(draft, np.int32)
+    v = np.ascontiguousarray(verify, np.int32)
+    p = AcceptParams(int(enabled), seq_max, tok_max)
+    return bool(lib().hsdo_accept_sequence(d, v, d.size, int(gripper), C.byref(p)))
+
+
+def verify_round(drafts, greedy, skip=False, cap=64, enabled=True, seq_max=30, tok_max=15) -> Outcome:
+    drafts = np.ascontiguousarray(np.atleast_2d(drafts), np.int32)
+    greedy = np.ascontiguousarray(greedy, np.int32)
+    n_cand, L = drafts.shape
+    out = Outcome()
+    p = AcceptParams(int(enabled), seq_max, tok_max)
+    lib().hsdo_verify_round(drafts, n_cand, L, greedy, int(skip), cap, C.byref(p), C.byref(out))
+    return out
+
+
+def enumerate_chains(drafts, cap=64):
+    drafts = np.ascontiguousarray(np.atleast_2d(drafts), np.int32)
+    n_cand, L = drafts.shape
+    chains = np.zeros((cap, L), np.int32)
+    a = np.zeros(cap, np.int32)
+    b = np.zeros(cap, np.int32)
+    n = lib().hsdo_enumerate_chains(drafts, n_cand, L, cap, chains, a, b)
+    return chains[:n], a[:n], b[:n]
+
+
+def calibrate(sims_list, T):
+    c = Calib()
+    lib().hsdo_calibrate_init(C.byref(c))
+    for s in sims_list:
+        s = np.ascontiguousarray(s, np.float64)
+        lib().hsdo_calibrate_accumulate(C.byref(c), s, s.shape[0], T)
+    m = C.c_double()
+    o = C.c_int()
+    rc = lib().hsdo_calibrate_finish(C.byref(c), C.byref(m), C.byref(o))
+    if rc < 0:
+        return None
+    return m.value, o.value
+
+
+def update_skip_state(state: SkipState, success: bool, S_c: float, min_S_h: float) -> SkipState:
+    lib().hsdo_update_skip_state(C.byref(state), int(success), S_c, min_S_h)
+    return state
+
+
+def project_window(xyz):
+    xyz = np.ascontiguousarray(xyz, np.float64)
+    uv = np.zeros((xyz.shape[0], 2), np.float64)
+    rc = lib().hsdo_project_window(xyz, xyz.shape[0], uv)
+    if rc < 0:
+        raise ValueError(rc)
+    return uv
+
+
+def fit_circle_center(uv):
+    uv = np.ascontiguousarray(uv, np.float64)
+    cu, cv = C.c_double(), C.c_double()
+    deg, it = C.c_int(), C.c_int()
+    rc = lib().hsdo_fit_circle_center(uv, uv.shape[0], C.byref(cu), C.byref(cv), C.byref(deg), C.byref(it))
+    if rc < 0:
+        raise ValueError(rc)
+    return (cu.value, cv.value), bool(deg.value), it.value
+
+
+def curvature_radius(xyz, r_cap=1.0) -> float:
+    xyz = np.ascontiguousarray(xyz, np.float64)
+    R = C.c_double()
+    rc = lib().hsdo_curvature_radius(xyz, xyz.shape[0], r_cap, C.byref(R))
+    if rc < 0:
+        raise ValueError(rc)
+    return R.value
+
+
+def cumulative_displacement(xyz) -> float:
+    xyz = np.ascontiguousarray(xyz, np.float64)
+    D = C.c_double()
+    rc = lib().hsdo_cumulative_displacement(xyz, xyz.shape[0], C.byref(D))
+    if rc < 0:
+        raise ValueError(rc)
+    return D.value
+
+
+def normalize(x, lo, hi95) -> float:
+    return lib().hsdo_normalize(x, lo, hi95)
+
+
+def percentile_bounds(samples):
+    s = np.ascontiguousarray(samples, np.float64)
+    lo, hi = C.c_double(), C.c_double()
+    rc = lib().hsdo_percentile_bounds(s, s.size, C.byref(lo), C.byref(hi))
+    if rc < 0:
+        raise ValueError(rc)
+    return lo.value, hi.value
+
+
+def fused_metric(R, D, params: MetricParams, bounds: NormBounds) -> float:
+    return lib().hsdo_fused_metric(R, D, C.byref(params), C.byref(bounds))
+
+
+def window_features(xyz, params: MetricParams, bounds: NormBounds):
+    xyz = np.ascontiguousarray(xyz, np.float64)
+    R, D, F = C.c_double(), C.c_double(), C.c_double()
+    dec = C.c_int()
+    rc = lib().hsdo_window_features(xyz, xyz.shape[0], C.byref(params), C.byref(bounds), C.byref(R), C.byref(D),
+                                    C.byref(F), C.byref(dec))
+    if rc < 0:
+        raise ValueError(rc)
+    return R.value, D.value, F.value, dec.value
+
+
+def ref_search(col, queries: np.ndarray, k: int, threads: int = 1):
+    """Reference Collection::search_topk_exact over fp32 queries widened to fp64."""
+    q = np.ascontiguousarray(np.atleast_2d(queries), np.float32)
+    B, dim = q.shape
+    sc = np.zeros((B, k), np.float64)
+    ids = np.full((B, k), -1, np.int32)
+    tok = np.zeros((B, k, 21), np.uint8)
+    rc = ref().hsdref_search_batch(col, q, B, dim, k, threads, sc, ids, tok.ctypes.data)
+    if rc < 0:
+        raise RuntimeError(f"reference search failed: {rc}")
+    n = ref().hsdref_collection_size(col)
+    kk = min(k, n)
+    return sc[:, :kk], ids[:, :kk], tok[:, :kk]
