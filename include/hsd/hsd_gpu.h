@@ -1,0 +1,270 @@
+/*
+ * hsd_gpu.h — C ABI of the B200-native HeiSD retrieval-side hot path.
+ *
+ * Drop-in boundary for the reference's C++ API in proj/include/hsd (see
+ * INTEGRATION.md for the reference-side binding and include/hsd/gpu.hpp for
+ * the header-only C++ wrapper that re-exposes the reference signatures).
+ *
+ *   hot-path step (CS-5):
+ *     hsd_window_features  -> drafter/retrieval decision per robot  (K5)
+ *     hsd_search_topk_exact-> top-k records per query                (K1+K2)
+ *     hsd_verify_round     -> gather + verify-skip + relaxed accept  (K4)
+ *     hsd_step             -> all of the above on one stream
+ *
+ * Conventions
+ *   - Plain pointers and sizes; no C++ or torch types.  Unless stated
+ *     otherwise array arguments are DEVICE pointers on the collection's GPU and
+ *     work is enqueued asynchronously on `stream` (a cudaStream_t, NULL = the
+ *     legacy default stream).
+ *   - Every call returns an hsd_status; the status codes mirror the
+ *     reference's exception taxonomy (errors.hpp:10-50) so the C++ wrapper can
+ *     rethrow the matching hsd:: exception.  hsd_last_error() returns a
+ *     thread-local message for the last failing call on this thread.
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point returns HSD_ERR_NO_DEVICE.
+ */
+#ifndef HSD_GPU_H
+#define HSD_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HSD_ABI_VERSION 1
+#define HSD_K_MAX 32        /* largest k served by the device top-k */
+#define HSD_TOKENS_STRIDE 32 /* bytes per record in the device token table (21 used) */
+
+typedef enum hsd_status {
+  HSD_OK = 0,
+  HSD_ERR_INVALID_INPUT = 1, /* hsd::InvalidInputError (errors.hpp:15) */
+  HSD_ERR_CONFIG = 2,        /* hsd::ConfigError       (errors.hpp:20) */
+  HSD_ERR_SCHEMA = 3,        /* hsd::SchemaError       (errors.hpp:25) */
+  HSD_ERR_IO = 4,            /* hsd::IoError           (errors.hpp:30) */
+  HSD_ERR_PARSE = 5,         /* hsd::ParseError        (errors.hpp:35) */
+  HSD_ERR_VERSION = 6,       /* hsd::VersionError      (errors.hpp:43) */
+  HSD_ERR_CALIBRATION = 7,   /* hsd::CalibrationError  (errors.hpp:48) */
+  HSD_ERR_CUDA = 100,
+  HSD_ERR_NCCL = 101,
+  HSD_ERR_OOM = 102,
+  HSD_ERR_NO_DEVICE = 103,
+} hsd_status;
+
+const char* hsd_last_error(void);
+int hsd_abi_version(void);
+/* Number of visible sm_100 devices (0 when none). */
+hsd_status hsd_device_count(int* n);
+
+/* ------------------------------------------------------------------------
+ * Collection — one task shard of the trajectory DB resident in HBM.
+ * Replaces hsd::Collection (store.hpp:59-96): same dim rule (store.cpp:36-38),
+ * dense ids in insertion order (store.cpp:53), insert-time schema checks
+ * (store.cpp:44-57).  Keys are stored fp32 row-major [capacity][dim]; payload
+ * next_actions are quantized at insert (actions.cpp:32-50, bounds [-1,1],
+ * K = 256) into a uint8 token table [capacity][32] (21 used: 3 slices x 7).
+ * ---------------------------------------------------------------------- */
+typedef struct hsd_collection hsd_collection;
+
+hsd_status hsd_collection_create(int device, int dim, int64_t capacity, hsd_collection** out);
+hsd_status hsd_collection_destroy(hsd_collection* c);
+hsd_status hsd_collection_size(const hsd_collection* c, int64_t* n);
+hsd_status hsd_collection_dim(const hsd_collection* c, int* dim);
+hsd_status hsd_collection_device(const hsd_collection* c, int* device);
+/* Device pointers of the resident arrays (read-only views). */
+hsd_status hsd_collection_keys(const hsd_collection* c, const float** keys, const uint8_t** tokens);
+
+/* Collection::insert (store.cpp:44-57) of n records.  HOST pointers:
+ *   emb          fp32 [n][dim]
+ *   next_actions fp64 [n][3][7]  (Payload::next_actions, store.hpp:31)
+ *   episode_idx, step_idx int32 [n] or NULL (0); negative -> HSD_ERR_SCHEMA.
+ * Non-finite actions -> HSD_ERR_INVALID_INPUT (actions.cpp:38-40).
+ * *first_id receives the id of the first inserted record.  Synchronous. */
+hsd_status hsd_collection_insert(hsd_collection* c, const float* emb, const double* next_actions,
+                                 const int32_t* episode_idx, const int32_t* step_idx, int64_t n, int64_t* first_id);
+
+/* Append n counter-generated records (include/hsd/hsd_synth.h, family
+ * `kind`) generated on the device; synchronous.  Record i of the collection
+ * holds synthetic row i. */
+hsd_status hsd_collection_generate(hsd_collection* c, int kind, uint64_t db_seed, int64_t n);
+/* Same, appending synthetic rows [row0, row0 + n) of the global stream (the
+ * local shard of a row-sharded DB; local id j holds global row row0 + j). */
+hsd_status hsd_collection_generate_rows(hsd_collection* c, int kind, uint64_t db_seed, int64_t row0, int64_t n);
+
+/* ------------------------------------------------------------------------
+ * Exact top-k search — Collection::search_topk_exact (store.cpp:59-73) for a
+ * batch of B fp32 queries [B][dim].  Outputs [B][k]: fp64 scores and int32
+ * record ids, ordered (score desc, id asc); when k > size the trailing
+ * entries are id -1 / score -inf.  Scores are the reference's sequential fp64
+ * dot product of the (fp32-widened) query and key, bit for bit.
+ * k < 1 -> HSD_ERR_INVALID_INPUT (store.cpp:60); k > HSD_K_MAX ->
+ * HSD_ERR_INVALID_INPUT.  An empty collection yields all -1 (no error).
+ * ---------------------------------------------------------------------- */
+hsd_status hsd_search_topk_exact(hsd_collection* c, const float* queries, int B, int k, double* scores,
+                                 int32_t* ids, void* stream);
+
+/* Same, restricted to the record range [row_begin, row_end) (a per-task
+ * shard inside one device array); ids stay collection-global. */
+hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B, int k, int64_t row_begin,
+                                 int64_t row_end, double* scores, int32_t* ids, void* stream);
+
+/* Number of queries whose exact-rescoring candidate window overflowed in the
+ * last search on `stream` (0 in every tested configuration; non-zero means
+ * the result may be inexact).  Synchronizes `stream`. */
+hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count);
+
+/* ------------------------------------------------------------------------
+ * Verification — fused gather + verify-skip + sequence-wise relaxed
+ * acceptance + accepted length (spec-only in the reference).
+ * ---------------------------------------------------------------------- */
+typedef struct hsd_verify_params {
+  int32_t relaxed;        /* RelaxedAcceptanceParams::enabled */
+  int32_t bias_seq_max;   /* 30 (PAPER §4.2) */
+  int32_t bias_token_max; /* 15 */
+  int32_t skip_enabled;   /* verify-skip on (Alg. 1, retrieval mode only) */
+  double min_S;           /* VerifySkipState::min_S */
+  int32_t O_dist;         /* VerifySkipState::O_dist */
+  int32_t chain_cap;      /* enumerate_chains cap (default 64) */
+} hsd_verify_params;
+
+typedef struct hsd_outcome {
+  int32_t accept_len; /* accepted draft tokens (VerifyOutcome::accept_length) */
+  int16_t win_a;      /* winning chain: pos0 from candidate rank a ...        */
+  int16_t win_b;      /* ... every later group from candidate rank b          */
+  int16_t calls;      /* verifier_calls (unique chains visited)               */
+  int8_t fallback;    /* empty prefix -> one greedy verifier token            */
+  int8_t skipped;     /* verify-skip fired                                    */
+  int16_t n_emit;     /* tokens emitted                                       */
+  int16_t greedy0;    /* verifier greedy token at position 0                  */
+  float cos_sim;      /* skip-check similarity (diagnostic; -2 when not run)  */
+} hsd_outcome;
+
+/* One decode round for E episodes:
+ *   ids       int32 [E][k] retrieved record ids (rank order; -1 = none)
+ *   logits    fp32 [E][L][256] verifier logits (teacher-forced greedy = argmax,
+ *             lowest bin on ties), L in {7, 21} (1 or 3 action slices)
+ *   feat_now, feat_prev fp32 [E][d_f] verifier features (may be NULL when no
+ *             parameter set enables skipping)
+ *   history   int32 [E] number of stored features (NULL = unbounded)
+ *   gap_d     candidate step gap d of should_skip
+ *   params    HOST array of P parameter sets (a tolerance / threshold sweep
+ *             reads the inputs once)
+ * Outputs (device): out [P][E] outcomes, tokens [P][E][L] emitted tokens. */
+hsd_status hsd_verify_round(hsd_collection* c, const int32_t* ids, int E, int k, int L, const float* logits,
+                            const float* feat_now, const float* feat_prev, int d_f, const int32_t* history, int gap_d,
+                            const hsd_verify_params* params, int P, hsd_outcome* out, uint8_t* tokens, void* stream);
+
+/* Same over pre-gathered draft records (drafts uint8 [E][k][32], e.g. from
+ * hsd_search_topk_sharded); ids only mark valid candidates (-1 = none). */
+hsd_status hsd_verify_round_drafts(int device, const int32_t* ids, const uint8_t* drafts, int E, int k, int L,
+                                   const float* logits, const float* feat_now, const float* feat_prev, int d_f,
+                                   const int32_t* history, int gap_d, const hsd_verify_params* params, int P,
+                                   hsd_outcome* out, uint8_t* tokens, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Kinematic fused metric — window_features + classify_segment + decide_sd
+ * (kinematics.cpp:38-273) for W windows of w points.
+ * ---------------------------------------------------------------------- */
+typedef struct hsd_metric_params {
+  double alpha;     /* FusedMetricParams (kinematics.hpp:38-45) */
+  int32_t w;
+  double threshold;
+  double r_cap;
+} hsd_metric_params;
+
+typedef struct hsd_norm_bounds {
+  double d_min, d_max95, r_min, r_max95; /* NormalizationBounds (kinematics.hpp:29-36) */
+} hsd_norm_bounds;
+
+/* xyz fp64 [W][w][3]; history int32 [W] (NULL = warm) -> R, D, F fp64 [W],
+ * decision int32 [W]: 1 retrieval_sd, 0 drafter_sd (cold start history < w is
+ * drafter), -1 non-finite window (InvalidInputError).  Params
+ * are validated like FusedMetricParams/NormalizationBounds::validate
+ * (kinematics.cpp:13-24) -> HSD_ERR_CONFIG. */
+hsd_status hsd_window_features(int device, const double* xyz, int W, const hsd_metric_params* params,
+                               const hsd_norm_bounds* bounds, const int32_t* history, double* R, double* D, double* F,
+                               int32_t* decision, void* stream);
+
+/* quantize (actions.cpp:32-50) of n action slices fp64 [n][7] with per-dim
+ * bounds lo7/hi7 (HOST) into int32 bins [n][7]; status[n] (int32, device):
+ * 0 ok, 1 non-finite input.  Bad bounds / K < 2 -> HSD_ERR_CONFIG. */
+hsd_status hsd_quantize(int device, const double* actions, int64_t n, const double* lo7, const double* hi7, int k_bins,
+                        int32_t* bins, int32_t* status, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Fused decode-round step (CS-5): kinematics -> search -> verify on one
+ * stream with scratch owned by the engine.  All retrieval-mode episodes are
+ * searched; decision[] reports the drafter/retrieval boundary.
+ * ---------------------------------------------------------------------- */
+typedef struct hsd_engine hsd_engine;
+
+hsd_status hsd_engine_create(hsd_collection* c, int max_B, int k, int L, int d_f, int w, hsd_engine** out);
+hsd_status hsd_engine_destroy(hsd_engine* e);
+
+typedef struct hsd_step_io {
+  /* inputs [B]-major; device pointers for hsd_step, host for hsd_step_host */
+  const float* queries;   /* [B][dim] */
+  const float* logits;    /* [B][L][256] */
+  const float* feat_now;  /* [B][d_f] or NULL */
+  const float* feat_prev; /* [B][d_f] or NULL */
+  const double* xyz;      /* [B][w][3] or NULL (skip kinematics) */
+  const int32_t* history; /* [B] or NULL */
+  /* outputs */
+  double* scores;         /* [B][k] */
+  int32_t* ids;           /* [B][k] */
+  hsd_outcome* out;       /* [B] */
+  uint8_t* tokens;        /* [B][L] */
+  double* R;              /* [B] or NULL */
+  double* D;
+  double* F;
+  int32_t* decision;
+} hsd_step_io;
+
+hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                    const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream);
+/* Stage timing of the next `max_steps` hsd_step calls with CUDA events on the
+ * step's stream (0 disables).  hsd_engine_stage_times synchronizes and returns
+ * the summed milliseconds of [kinematics, similarity, select, verify, total]
+ * over the recorded steps, then resets the recorder. */
+hsd_status hsd_engine_enable_timing(hsd_engine* e, int max_steps);
+hsd_status hsd_engine_stage_times(hsd_engine* e, int* n_steps, double ms[5]);
+
+/* Same with HOST buffers: H2D of the inputs and D2H of the outputs happen
+ * inside the call (pinned staging owned by the engine); synchronous. */
+hsd_status hsd_step_host(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                         const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU: row-sharded collection (rank r owns a contiguous id range) with a
+ * per-rank local top-k, an NCCL all-gather of the B x k records over NVLink
+ * and a k-way merge; bit-identical to the single-GPU result.
+ * ---------------------------------------------------------------------- */
+typedef struct hsd_comm hsd_comm;
+#define HSD_UNIQUE_ID_BYTES 128
+hsd_status hsd_comm_unique_id(uint8_t id[HSD_UNIQUE_ID_BYTES]);
+hsd_status hsd_comm_create(const uint8_t id[HSD_UNIQUE_ID_BYTES], int world, int rank, int device, hsd_comm** out);
+hsd_status hsd_comm_destroy(hsd_comm* comm);
+/* Contiguous shard [begin, end) of n_total rows for `rank` of `world`. */
+hsd_status hsd_shard_range(int64_t n_total, int world, int rank, int64_t* begin, int64_t* end);
+/* Local search of this rank's collection (ids offset by id_offset) followed by
+ * the all-gather + merge; every rank receives the global [B][k] result and,
+ * when `drafts` is non-null, the matching payload tokens [B][k][32] (the
+ * records' drafts travel with them, so verification needs no remote lookup). */
+hsd_status hsd_search_topk_sharded(hsd_collection* c, hsd_comm* comm, int64_t id_offset, const float* queries, int B,
+                                   int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Synthetic workload generators on the device (include/hsd/hsd_synth.h).
+ * ---------------------------------------------------------------------- */
+hsd_status hsd_gen_queries(int device, int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B,
+                           int dim, float* out, void* stream);
+/* logits [E][L][256] whose greedy bins are draft tokens of record rows[e]
+ * (+ hsd_logit_greedy_bin deltas); rows may hold -1 (random draft). */
+hsd_status hsd_gen_logits(hsd_collection* c, uint64_t seed, const int64_t* rows, int E, int L, float* out,
+                          void* stream);
+hsd_status hsd_gen_features(int device, uint64_t seed, int E, int d_f, float* now, float* prev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSD_GPU_H */

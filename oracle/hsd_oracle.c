@@ -193,6 +193,40 @@ void hsdo_synth_tokens(uint64_t db_seed, int64_t row, uint8_t* tok21) {
   }
 }
 
+void hsdo_gen_features(uint64_t seed, int64_t e0, int E, int d_f, float* now, float* prev) {
+  int64_t* raw = (int64_t*)malloc(sizeof(int64_t) * (size_t)d_f);
+  for (int e = 0; e < E; ++e) {
+    for (int which = 0; which < 2; ++which) {
+      int64_t ss = 0;
+      for (int c = 0; c < d_f; ++c) {
+        raw[c] = hsd_feat_raw(seed, e0 + e, which, d_f, c);
+        ss += raw[c] * raw[c];
+      }
+      float* o = (which ? prev : now) + (size_t)e * d_f;
+      for (int c = 0; c < d_f; ++c) o[c] = hsd_norm_val(raw[c], ss);
+    }
+  }
+  free(raw);
+}
+
+void hsdo_gen_logits(uint64_t db_seed, uint64_t seed, const int64_t* rows, int64_t e0, int E, int L, float* out) {
+  uint8_t tok[21];
+  for (int e = 0; e < E; ++e) {
+    int64_t ee = e0 + e;
+    int64_t row = rows ? rows[e] : -1;
+    if (row >= 0) hsdo_synth_tokens(db_seed, row, tok);
+    for (int p = 0; p < L; ++p) {
+      int draft = row >= 0 ? tok[p]
+                           : (int)(hsd_hash_at(hsd_stream_base(seed, HSD_TAG_LOGITS), ((uint64_t)ee << 8) ^ (0xD000u + p)) &
+                                   0xFFu);
+      int g = hsd_logit_greedy_bin(seed, ee, p, draft);
+      int tie = hsd_logit_tie_bin(seed, ee, p);
+      float* o = out + ((size_t)e * L + p) * 256;
+      for (int b = 0; b < 256; ++b) o[b] = (b == g || b == tie) ? 8.0f : hsd_logit_background(seed, ee, p, b);
+    }
+  }
+}
+
 /* ======================================================================== */
 /* verification                                                              */
 /* ======================================================================== */

@@ -50,6 +50,12 @@ void hsdo_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim,
 void hsdo_gen_queries(int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B, int dim,
                       float* out);
 
+/* Verifier features (f_now, f_prev) of episodes [e0, e0+E) and logits
+ * [E][L][256] whose greedy bins track the draft tokens of DB row rows[e]
+ * (-1 = random draft), as generated on the device (hsd_synth.h). */
+void hsdo_gen_features(uint64_t seed, int64_t e0, int E, int d_f, float* now, float* prev);
+void hsdo_gen_logits(uint64_t db_seed, uint64_t seed, const int64_t* rows, int64_t e0, int E, int L, float* out);
+
 /* ------------------------------------------------------------------ actions */
 /* quantize, actions.cpp:32-50 (uniform bounds lo/hi on all 7 dims).  Returns
  * 0, or -HSDO_CONFIG / -HSDO_INVALID_INPUT. */

@@ -73,6 +73,8 @@ def lib():
         L.hsdo_search_synth.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int, _f, C.c_int, C.c_int, _d, _l, C.c_int]
         L.hsdo_gen_keys.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_int, _f]
         L.hsdo_gen_queries.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, _f]
+        L.hsdo_gen_features.argtypes = [C.c_uint64, C.c_int64, C.c_int, C.c_int, _f, _f]
+        L.hsdo_gen_logits.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p, C.c_int64, C.c_int, C.c_int, _f]
         L.hsdo_quantize.argtypes = [_d, _d, _d, C.c_int, _i]
         L.hsdo_synth_tokens.argtypes = [C.c_uint64, C.c_int64, _u8]
         L.hsdo_token_bias.argtypes = [C.c_int, C.c_int]
@@ -145,6 +147,21 @@ def gen_keys(kind: int, db_seed: int, row0: int, n: int, dim: int) -> np.ndarray
 def gen_queries(kind: int, q_seed: int, db_seed: int, n_rows: int, q0: int, B: int, dim: int) -> np.ndarray:
     out = np.empty((B, dim), np.float32)
     lib().hsdo_gen_queries(kind, q_seed, db_seed, n_rows, q0, B, dim, out)
+    return out
+
+
+def gen_features(seed: int, e0: int, E: int, d_f: int):
+    now = np.empty((E, d_f), np.float32)
+    prev = np.empty((E, d_f), np.float32)
+    lib().hsdo_gen_features(seed, e0, E, d_f, now, prev)
+    return now, prev
+
+
+def gen_logits(db_seed: int, seed: int, rows, e0: int, L: int) -> np.ndarray:
+    rows = np.ascontiguousarray(rows, np.int64)
+    E = rows.size
+    out = np.empty((E, L, 256), np.float32)
+    lib().hsdo_gen_logits(db_seed, seed, rows.ctypes.data, e0, E, L, out)
     return out
 
 

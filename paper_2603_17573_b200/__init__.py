@@ -1,0 +1,564 @@
+"""paper_2603_17573_b200 — B200-native HeiSD retrieval-side speculative-decoding hot path.
+
+Python mirror of the C ABI in include/hsd/hsd_gpu.h (the drop-in boundary for
+the reference's C++ API in proj/include/hsd).  The compute
+lives in libhsd_gpu.so (hand-written sm_100a CUDA, built in-tree by
+``__graft_entry__.build()``); this module only marshals pointers.  There is no
+CPU fallback: if the shared library is missing the import fails, and every
+compute call without an sm_100 device raises NoDeviceError.
+
+Names follow the reference: Collection.insert / search_topk_exact
+(store.hpp:59-96), quantize (actions.hpp:55), window_features /
+classify_segment (kinematics.hpp:88-93), and the SPEC names for the spec-only
+verification ops (verify_round ~ retrieve_drafts + should_skip + verify_tree).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhsd_gpu.so")
+
+HSD_K_MAX = 32
+TOKENS_STRIDE = 32
+EXACT, REAL = 0, 1
+
+
+# --------------------------------------------------------------------------- errors
+class HsdError(RuntimeError):
+    """hsd::Error (errors.hpp:10)."""
+
+
+class InvalidInputError(HsdError, ValueError):
+    pass
+
+
+class ConfigError(HsdError, ValueError):
+    pass
+
+
+class SchemaError(HsdError, ValueError):
+    pass
+
+
+class IoError(HsdError):
+    pass
+
+
+class ParseError(HsdError):
+    pass
+
+
+class VersionError(HsdError):
+    pass
+
+
+class CalibrationError(HsdError):
+    pass
+
+
+class CudaError(HsdError):
+    pass
+
+
+class NcclError(HsdError):
+    pass
+
+
+class OutOfMemoryError(HsdError, MemoryError):
+    pass
+
+
+class NoDeviceError(HsdError):
+    pass
+
+
+_STATUS = {1: InvalidInputError, 2: ConfigError, 3: SchemaError, 4: IoError, 5: ParseError, 6: VersionError,
+           7: CalibrationError, 100: CudaError, 101: NcclError, 102: OutOfMemoryError, 103: NoDeviceError}
+
+
+# --------------------------------------------------------------------------- ABI structs
+class VerifyParams(C.Structure):
+    _fields_ = [("relaxed", C.c_int32), ("bias_seq_max", C.c_int32), ("bias_token_max", C.c_int32),
+                ("skip_enabled", C.c_int32), ("min_S", C.c_double), ("O_dist", C.c_int32), ("chain_cap", C.c_int32)]
+
+    @classmethod
+    def make(cls, relaxed=True, bias_seq_max=30, bias_token_max=15, skip_enabled=False, min_S=0.95, O_dist=5,
+             chain_cap=64):
+        return cls(int(relaxed), bias_seq_max, bias_token_max, int(skip_enabled), float(min_S), O_dist, chain_cap)
+
+
+class Outcome(C.Structure):
+    _fields_ = [("accept_len", C.c_int32), ("win_a", C.c_int16), ("win_b", C.c_int16), ("calls", C.c_int16),
+                ("fallback", C.c_int8), ("skipped", C.c_int8), ("n_emit", C.c_int16), ("greedy0", C.c_int16),
+                ("cos_sim", C.c_float)]
+
+
+OUTCOME_DTYPE = np.dtype([("accept_len", np.int32), ("win_a", np.int16), ("win_b", np.int16), ("calls", np.int16),
+                          ("fallback", np.int8), ("skipped", np.int8), ("n_emit", np.int16), ("greedy0", np.int16),
+                          ("cos_sim", np.float32)])
+assert OUTCOME_DTYPE.itemsize == C.sizeof(Outcome) == 20
+
+
+class MetricParams(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("w", C.c_int32), ("threshold", C.c_double), ("r_cap", C.c_double)]
+
+
+class NormBounds(C.Structure):
+    _fields_ = [("d_min", C.c_double), ("d_max95", C.c_double), ("r_min", C.c_double), ("r_max95", C.c_double)]
+
+
+class StepIO(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("queries", "logits", "feat_now", "feat_prev", "xyz", "history", "scores",
+                                          "ids", "out", "tokens", "R", "D", "F", "decision")]
+
+
+# LIBERO-Goal bounds and FusedMetricParams defaults (kinematics.hpp:38-45)
+LIBERO_GOAL = NormBounds(0.000009, 0.123381, 0.000001, 0.014989)
+DEFAULT_METRIC = MetricParams(0.5, 15, 0.5, 1.0)
+
+
+# --------------------------------------------------------------------------- loader
+_lib = None
+_vp = C.c_void_p
+
+
+def lib():
+    """Load libhsd_gpu.so (fails loudly; there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing — build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the HeiSD hot path has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    L.hsd_last_error.restype = C.c_char_p
+    L.hsd_abi_version.restype = C.c_int
+    sig = {
+        "hsd_device_count": [C.POINTER(C.c_int)],
+        "hsd_collection_create": [C.c_int, C.c_int, C.c_int64, C.POINTER(_vp)],
+        "hsd_collection_destroy": [_vp],
+        "hsd_collection_size": [_vp, C.POINTER(C.c_int64)],
+        "hsd_collection_dim": [_vp, C.POINTER(C.c_int)],
+        "hsd_collection_device": [_vp, C.POINTER(C.c_int)],
+        "hsd_collection_keys": [_vp, C.POINTER(_vp), C.POINTER(_vp)],
+        "hsd_collection_insert": [_vp, _vp, _vp, _vp, _vp, C.c_int64, C.POINTER(C.c_int64)],
+        "hsd_collection_generate": [_vp, C.c_int, C.c_uint64, C.c_int64],
+        "hsd_search_topk_exact": [_vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp],
+        "hsd_search_topk_range": [_vp, _vp, C.c_int, C.c_int, C.c_int64, C.c_int64, _vp, _vp, _vp],
+        "hsd_search_overflow_count": [_vp, _vp, C.POINTER(C.c_int)],
+        "hsd_verify_round": [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, _vp, C.c_int,
+                             _vp, _vp, _vp],
+        "hsd_window_features": [C.c_int, _vp, C.c_int, C.POINTER(MetricParams), C.POINTER(NormBounds), _vp, _vp, _vp,
+                                _vp, _vp, _vp],
+        "hsd_quantize": [C.c_int, _vp, C.c_int64, _vp, _vp, C.c_int, _vp, _vp, _vp],
+        "hsd_engine_create": [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
+        "hsd_engine_destroy": [_vp],
+        "hsd_engine_enable_timing": [_vp, C.c_int],
+        "hsd_engine_stage_times": [_vp, C.POINTER(C.c_int), C.POINTER(C.c_double * 5)],
+        "hsd_step": [_vp, C.c_int, C.POINTER(StepIO), C.POINTER(VerifyParams), C.POINTER(MetricParams),
+                     C.POINTER(NormBounds), C.c_int, _vp],
+        "hsd_step_host": [_vp, C.c_int, C.POINTER(StepIO), C.POINTER(VerifyParams), C.POINTER(MetricParams),
+                          C.POINTER(NormBounds), C.c_int, _vp],
+        "hsd_comm_unique_id": [_vp],
+        "hsd_comm_create": [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
+        "hsd_comm_destroy": [_vp],
+        "hsd_shard_range": [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+        "hsd_search_topk_sharded": [_vp, _vp, C.c_int64, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
+        "hsd_verify_round_drafts": [C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp,
+                                    C.c_int, _vp, C.c_int, _vp, _vp, _vp],
+        "hsd_collection_generate_rows": [_vp, C.c_int, C.c_uint64, C.c_int64, C.c_int64],
+        "hsd_gen_queries": [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, _vp,
+                            _vp],
+        "hsd_gen_logits": [_vp, C.c_uint64, _vp, C.c_int, C.c_int, _vp, _vp],
+        "hsd_gen_features": [C.c_int, C.c_uint64, C.c_int, C.c_int, _vp, _vp, _vp],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = C.c_int
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib().hsd_last_error().decode(errors="replace")
+        raise _STATUS.get(status, HsdError)(f"[hsd status {status}] {msg}")
+
+
+def exported_symbols() -> list[str]:
+    """Every entry point declared in include/hsd/hsd_gpu.h."""
+    import re
+
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "hsd", "hsd_gpu.h")
+    with open(hdr) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"^(?:hsd_status|const char\*|int)\s+(hsd_\w+)\(", text, re.M)))
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    check(lib().hsd_device_count(C.byref(n)))
+    return n.value
+
+
+# --------------------------------------------------------------------------- torch helpers
+def _torch():
+    import torch
+
+    return torch
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+# --------------------------------------------------------------------------- Collection
+class Collection:
+    """Device-resident task shard; replaces hsd::Collection (store.hpp:59-96)."""
+
+    def __init__(self, dim: int, capacity: int = 1, device: int = 0):
+        self._h = C.c_void_p()
+        check(lib().hsd_collection_create(device, dim, capacity, C.byref(self._h)))
+        self.device = device
+        self._dim = dim
+
+    def close(self):
+        if self._h:
+            lib().hsd_collection_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def dim(self) -> int:
+        return self._dim
+
+    def size(self) -> int:
+        n = C.c_int64()
+        check(lib().hsd_collection_size(self._h, C.byref(n)))
+        return n.value
+
+    def __len__(self):
+        return self.size()
+
+    def insert(self, embeddings, next_actions, episode_idx=None, step_idx=None) -> int:
+        """Collection::insert (store.cpp:44-57) for a batch; returns the first id."""
+        emb = np.ascontiguousarray(np.atleast_2d(embeddings), np.float32)
+        act = np.ascontiguousarray(next_actions, np.float64).reshape(emb.shape[0], 21)
+        if emb.shape[1] != self._dim:  # store.cpp:46-49
+            raise SchemaError(f"embedding dim {emb.shape[1]} does not match collection dim {self._dim}")
+        ep = None if episode_idx is None else np.ascontiguousarray(episode_idx, np.int32)
+        st = None if step_idx is None else np.ascontiguousarray(step_idx, np.int32)
+        first = C.c_int64()
+        check(lib().hsd_collection_insert(self._h, emb.ctypes.data, act.ctypes.data,
+                                          None if ep is None else ep.ctypes.data,
+                                          None if st is None else st.ctypes.data, emb.shape[0], C.byref(first)))
+        return first.value
+
+    def generate(self, kind: int, db_seed: int, n: int, row0=None) -> None:
+        """Append n counter-generated records; row0 selects global synthetic rows (DB shards)."""
+        if row0 is None:
+            check(lib().hsd_collection_generate(self._h, kind, db_seed, n))
+        else:
+            check(lib().hsd_collection_generate_rows(self._h, kind, db_seed, row0, n))
+
+    def keys_view(self):
+        """(keys, tokens) torch views of the resident arrays."""
+        torch = _torch()
+        kp, tp = C.c_void_p(), C.c_void_p()
+        check(lib().hsd_collection_keys(self._h, C.byref(kp), C.byref(tp)))
+        n = self.size()
+        keys = _from_ptr(kp.value, (n, self._dim), torch.float32, self.device)
+        toks = _from_ptr(tp.value, (n, TOKENS_STRIDE), torch.uint8, self.device)
+        return keys, toks
+
+    def search_topk_exact(self, queries, k: int, row_range=None, stream=None):
+        """Batched Collection::search_topk_exact (store.cpp:59-73).
+
+        queries: cuda float32 [B, dim] -> (scores float64 [B, k], ids int32 [B, k]).
+        """
+        torch = _torch()
+        q = queries.contiguous()
+        if q.dtype != torch.float32 or not q.is_cuda:
+            raise InvalidInputError("queries must be a CUDA float32 tensor")
+        if q.dim() == 1:
+            q = q[None]
+        if q.shape[1] != self._dim:
+            raise InvalidInputError("embedding dim mismatch in cosine")  # store.cpp:30
+        B = q.shape[0]
+        kk = max(int(k), 1)
+        scores = torch.empty((B, kk), dtype=torch.float64, device=q.device)
+        ids = torch.empty((B, kk), dtype=torch.int32, device=q.device)
+        if row_range is None:
+            check(lib().hsd_search_topk_exact(self._h, _ptr(q), B, int(k), _ptr(scores), _ptr(ids), _stream(stream)))
+        else:
+            check(lib().hsd_search_topk_range(self._h, _ptr(q), B, int(k), int(row_range[0]), int(row_range[1]),
+                                              _ptr(scores), _ptr(ids), _stream(stream)))
+        return scores, ids
+
+    def overflow_count(self, stream=None) -> int:
+        c = C.c_int()
+        check(lib().hsd_search_overflow_count(self._h, _stream(stream), C.byref(c)))
+        return c.value
+
+    def verify_round(self, ids, logits, params, feat_now=None, feat_prev=None, history=None, gap_d=1, stream=None):
+        """Fused gather + verify-skip + relaxed acceptance.
+
+        ids int32 [E, k]; logits float32 [E, L, 256]; params: VerifyParams or a
+        list (sweep).  Returns (outcomes structured np array [P, E], tokens
+        uint8 tensor [P, E, L]).
+        """
+        torch = _torch()
+        if isinstance(params, VerifyParams):
+            params = [params]
+        P = len(params)
+        arr = (VerifyParams * P)(*params)
+        ids = ids.contiguous()
+        logits = logits.contiguous()
+        E, k = ids.shape
+        L = logits.shape[1]
+        d_f = 0 if feat_now is None else feat_now.shape[1]
+        out = torch.empty((P, E, C.sizeof(Outcome)), dtype=torch.uint8, device=ids.device)
+        toks = torch.empty((P, E, L), dtype=torch.uint8, device=ids.device)
+        check(lib().hsd_verify_round(self._h, _ptr(ids), E, k, L, _ptr(logits), _ptr(feat_now), _ptr(feat_prev), d_f,
+                                     _ptr(history), gap_d, C.cast(arr, C.c_void_p), P, _ptr(out), _ptr(toks),
+                                     _stream(stream)))
+        o = out.cpu().numpy().view(OUTCOME_DTYPE).reshape(P, E)
+        return o, toks
+
+
+def verify_round_drafts(ids, drafts, logits, params, feat_now=None, feat_prev=None, history=None, gap_d=1,
+                        stream=None):
+    """verify_round over pre-gathered draft records drafts uint8 [E, k, 32] (sharded search output)."""
+    torch = _torch()
+    if isinstance(params, VerifyParams):
+        params = [params]
+    P = len(params)
+    arr = (VerifyParams * P)(*params)
+    E, k = ids.shape
+    L = logits.shape[1]
+    d_f = 0 if feat_now is None else feat_now.shape[1]
+    out = torch.empty((P, E, C.sizeof(Outcome)), dtype=torch.uint8, device=ids.device)
+    toks = torch.empty((P, E, L), dtype=torch.uint8, device=ids.device)
+    check(lib().hsd_verify_round_drafts(ids.device.index or 0, _ptr(ids), _ptr(drafts), E, k, L, _ptr(logits),
+                                        _ptr(feat_now), _ptr(feat_prev), d_f, _ptr(history), gap_d,
+                                        C.cast(arr, C.c_void_p), P, _ptr(out), _ptr(toks), _stream(stream)))
+    return out.cpu().numpy().view(OUTCOME_DTYPE).reshape(P, E), toks
+
+
+class Comm:
+    """NCCL communicator of a row-sharded DB (one process per GPU)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().hsd_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, world: int, rank: int, device: int):
+        self._h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        check(lib().hsd_comm_create(buf, world, rank, device, C.byref(self._h)))
+        self.world, self.rank, self.device = world, rank, device
+
+    def close(self):
+        if self._h:
+            lib().hsd_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def search_topk(self, col: Collection, id_offset: int, queries, k: int, stream=None):
+        """Sharded search: local top-k + all-gather + merge -> (scores, ids, drafts [B, k, 32])."""
+        torch = _torch()
+        B = queries.shape[0]
+        scores = torch.empty((B, k), dtype=torch.float64, device=queries.device)
+        ids = torch.empty((B, k), dtype=torch.int32, device=queries.device)
+        drafts = torch.empty((B, k, TOKENS_STRIDE), dtype=torch.uint8, device=queries.device)
+        check(lib().hsd_search_topk_sharded(col.handle, self._h, id_offset, _ptr(queries), B, k, _ptr(scores),
+                                            _ptr(ids), _ptr(drafts), _stream(stream)))
+        return scores, ids, drafts
+
+
+def _from_ptr(ptr, shape, dtype, device):
+    """Non-owning torch view of device memory owned by the library."""
+    torch = _torch()
+    n = int(np.prod(shape))
+    if n == 0:
+        return torch.empty(shape, dtype=dtype, device=f"cuda:{device}")
+    esz = torch.empty((), dtype=dtype).element_size()
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": torch.empty((), dtype=dtype).numpy().dtype.str,
+                                    "data": (ptr, True), "version": 3, "strides": (esz,)}
+
+    return torch.as_tensor(_Arr(), device=f"cuda:{device}").view(shape)
+
+
+# --------------------------------------------------------------------------- free functions
+def window_features(xyz, params: MetricParams = DEFAULT_METRIC, bounds: NormBounds = LIBERO_GOAL, history=None,
+                    stream=None):
+    """Batched window_features + classify_segment + decide_sd (kinematics.cpp:261-273).
+
+    xyz: cuda float64 [W, w, 3] -> (R, D, F float64 [W], decision int32 [W]).
+    """
+    torch = _torch()
+    x = xyz.contiguous()
+    if x.dtype != torch.float64:
+        raise InvalidInputError("trajectory points must be float64")
+    W, w = x.shape[0], x.shape[1]
+    if w != params.w:
+        raise InvalidInputError("window_features expects exactly w points")  # kinematics.cpp:264-266
+    dev = x.device
+    R = torch.empty(W, dtype=torch.float64, device=dev)
+    D = torch.empty_like(R)
+    F = torch.empty_like(R)
+    dec = torch.empty(W, dtype=torch.int32, device=dev)
+    check(lib().hsd_window_features(dev.index or 0, _ptr(x), W, C.byref(params), C.byref(bounds), _ptr(history),
+                                    _ptr(R), _ptr(D), _ptr(F), _ptr(dec), _stream(stream)))
+    return R, D, F, dec
+
+
+def quantize(actions, lo=-1.0, hi=1.0, k_bins=256, stream=None):
+    """Batched quantize (actions.cpp:32-50): cuda float64 [n, 7] -> int32 bins [n, 7]."""
+    torch = _torch()
+    a = actions.contiguous()
+    n = a.shape[0]
+    lo7 = np.full(7, lo, np.float64) if np.isscalar(lo) else np.ascontiguousarray(lo, np.float64)
+    hi7 = np.full(7, hi, np.float64) if np.isscalar(hi) else np.ascontiguousarray(hi, np.float64)
+    bins = torch.empty((n, 7), dtype=torch.int32, device=a.device)
+    status = torch.empty(n, dtype=torch.int32, device=a.device)
+    check(lib().hsd_quantize(a.device.index or 0, _ptr(a), n, lo7.ctypes.data, hi7.ctypes.data, k_bins, _ptr(bins),
+                             _ptr(status), _stream(stream)))
+    if n and bool((status != 0).any()):
+        raise InvalidInputError("non-finite action value")  # actions.cpp:38-40
+    return bins
+
+
+def classify_segment(F: float, threshold: float) -> str:
+    """kinematics.cpp:257-259 (host helper; the device path fuses it into window_features)."""
+    return "retrieval_sd" if F > threshold else "drafter_sd"
+
+
+def gen_queries(kind, q_seed, db_seed, n_rows, q0, B, dim, device=0, stream=None):
+    torch = _torch()
+    out = torch.empty((B, dim), dtype=torch.float32, device=f"cuda:{device}")
+    check(lib().hsd_gen_queries(device, kind, q_seed, db_seed, n_rows, q0, B, dim, _ptr(out), _stream(stream)))
+    return out
+
+
+def gen_logits(col: Collection, seed, rows, L, stream=None):
+    torch = _torch()
+    rows_t = torch.as_tensor(np.asarray(rows, np.int64), device=f"cuda:{col.device}")
+    E = rows_t.numel()
+    out = torch.empty((E, L, 256), dtype=torch.float32, device=f"cuda:{col.device}")
+    check(lib().hsd_gen_logits(col.handle, seed, _ptr(rows_t), E, L, _ptr(out), _stream(stream)))
+    return out
+
+
+def gen_features(seed, E, d_f, device=0, stream=None):
+    torch = _torch()
+    now = torch.empty((E, d_f), dtype=torch.float32, device=f"cuda:{device}")
+    prev = torch.empty_like(now)
+    check(lib().hsd_gen_features(device, seed, E, d_f, _ptr(now), _ptr(prev), _stream(stream)))
+    return now, prev
+
+
+def query_rows(q_seed, kind, n_rows, q0, B):
+    """Host mirror of hsd_query_row (include/hsd/hsd_synth.h): the DB row each synthetic query copies (-1 = none)."""
+    from . import synth
+
+    return synth.query_rows(q_seed, kind, n_rows, q0, B)
+
+
+def shard_range(n_total, world, rank):
+    b, e = C.c_int64(), C.c_int64()
+    check(lib().hsd_shard_range(n_total, world, rank, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+# --------------------------------------------------------------------------- engine
+@dataclass
+class StepBuffers:
+    """Caller-owned buffers of one decode round (device or pinned host)."""
+    queries: object
+    logits: object
+    feat_now: object = None
+    feat_prev: object = None
+    xyz: object = None
+    history: object = None
+    scores: object = None
+    ids: object = None
+    out: object = None
+    tokens: object = None
+    R: object = None
+    D: object = None
+    F: object = None
+    decision: object = None
+
+    def io(self) -> StepIO:
+        s = StepIO()
+        for name, _ in StepIO._fields_:
+            v = getattr(self, name)
+            setattr(s, name, None if v is None else v.data_ptr())
+        return s
+
+
+class Engine:
+    """Fused decode-round step (CS-5): kinematics -> search -> verify on one stream."""
+
+    def __init__(self, col: Collection, max_B: int, k: int, L: int, d_f: int, w: int = 15):
+        self._h = C.c_void_p()
+        check(lib().hsd_engine_create(col.handle, max_B, k, L, d_f, w, C.byref(self._h)))
+        self.col, self.max_B, self.k, self.L, self.d_f, self.w = col, max_B, k, L, d_f, w
+
+    def close(self):
+        if self._h:
+            lib().hsd_engine_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def enable_timing(self, max_steps: int) -> None:
+        check(lib().hsd_engine_enable_timing(self._h, max_steps))
+
+    def stage_times(self):
+        """(steps, {stage: summed ms}) of the recorded steps (synchronizes)."""
+        n = C.c_int()
+        ms = (C.c_double * 5)()
+        check(lib().hsd_engine_stage_times(self._h, C.byref(n), C.byref(ms)))
+        names = ("kinematics", "similarity", "select", "verify", "total")
+        return n.value, dict(zip(names, list(ms)))
+
+    def step(self, B, bufs: StepBuffers, vp: VerifyParams, mp=DEFAULT_METRIC, nb=LIBERO_GOAL, gap_d=1, stream=None):
+        io = bufs.io()
+        check(lib().hsd_step(self._h, B, C.byref(io), C.byref(vp), C.byref(mp), C.byref(nb), gap_d, _stream(stream)))
+
+    def step_host(self, B, bufs: StepBuffers, vp: VerifyParams, mp=DEFAULT_METRIC, nb=LIBERO_GOAL, gap_d=1,
+                  stream=None):
+        io = bufs.io()
+        check(lib().hsd_step_host(self._h, B, C.byref(io), C.byref(vp), C.byref(mp), C.byref(nb), gap_d,
+                                  _stream(stream)))

@@ -1,0 +1,849 @@
+// api.cu — C ABI (include/hsd/hsd_gpu.h): collection handle, search / verify /
+// kinematics entry points, fused step engine and the NCCL-sharded search.
+// Host code only; kernels live in k_*.cu.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "hsd/hsd_gpu.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+hsd_status fail(hsd_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+hsd_status cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky-free errors
+  return fail(e == cudaErrorMemoryAllocation ? HSD_ERR_OOM : HSD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CU(x)                                     \
+  do {                                            \
+    cudaError_t e_ = (x);                         \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x); \
+  } while (0)
+
+#define NC(x)                                                                         \
+  do {                                                                                \
+    ncclResult_t r_ = (x);                                                            \
+    if (r_ != ncclSuccess) return fail(HSD_ERR_NCCL, "%s: %s", #x, ncclGetErrorString(r_)); \
+  } while (0)
+
+// Every compute entry point requires an sm_100 device; there is no CPU path.
+hsd_status require_device(int device) {
+  static int s_count = -1;
+  static signed char s_ok[64] = {0};  // 0 unknown, 1 sm_100, -1 other
+  if (s_count < 0) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    s_count = n;
+  }
+  if (s_count == 0) return fail(HSD_ERR_NO_DEVICE, "no CUDA device visible (the HeiSD hot path has no CPU fallback)");
+  if (device < 0 || device >= s_count || device >= 64)
+    return fail(HSD_ERR_INVALID_INPUT, "device %d out of range [0, %d)", device, s_count);
+  if (s_ok[device] == 0) {
+    int major = 0, minor = 0;
+    CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+    CU(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+    s_ok[device] = major == 10 ? 1 : -1;
+    if (major != 10)
+      return fail(HSD_ERR_NO_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a", device, major, minor);
+  }
+  if (s_ok[device] < 0) return fail(HSD_ERR_NO_DEVICE, "device %d is not sm_100", device);
+  CU(cudaSetDevice(device));
+  return HSD_OK;
+}
+
+int num_sms(int device) {
+  static int cache[64] = {0};
+  if (device >= 0 && device < 64 && cache[device]) return cache[device];
+  int v = 148;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  if (device >= 0 && device < 64) cache[device] = v;
+  return v;
+}
+
+__global__ void fill_empty_kernel(double* scores, int32_t* ids, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    scores[i] = -INFINITY;
+    ids[i] = -1;
+  }
+}
+
+__global__ void offset_ids_kernel(int32_t* ids, int n, int64_t off) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && ids[i] >= 0) ids[i] = (int32_t)(ids[i] + off);
+}
+
+struct Scratch {
+  uint64_t* partial = nullptr;
+  size_t partial_cap = 0;  // bytes
+  int* overflow = nullptr;
+};
+
+}  // namespace
+
+struct hsd_collection {
+  int device = 0;
+  int dim = 0;
+  int64_t n = 0;
+  int64_t cap = 0;
+  float* keys = nullptr;
+  uint8_t* tokens = nullptr;
+  unsigned long long* maxnorm = nullptr;  // fp64 bits of max row norm
+  std::mutex mu;
+  std::unordered_map<cudaStream_t, Scratch> scratch;
+};
+
+namespace {
+
+hsd_status ensure_capacity(hsd_collection* c, int64_t need) {
+  if (need <= c->cap) return HSD_OK;
+  int64_t ncap = std::max<int64_t>(need, c->cap * 2);
+  float* nk = nullptr;
+  uint8_t* nt = nullptr;
+  CU(cudaMalloc(&nk, (size_t)ncap * c->dim * sizeof(float)));
+  cudaError_t e = cudaMalloc(&nt, (size_t)ncap * HSD_TOKENS_STRIDE);
+  if (e != cudaSuccess) {
+    cudaFree(nk);
+    return cuda_fail(e, "cudaMalloc(tokens)");
+  }
+  if (c->n > 0) {
+    CU(cudaMemcpy(nk, c->keys, (size_t)c->n * c->dim * sizeof(float), cudaMemcpyDeviceToDevice));
+    CU(cudaMemcpy(nt, c->tokens, (size_t)c->n * HSD_TOKENS_STRIDE, cudaMemcpyDeviceToDevice));
+  }
+  cudaFree(c->keys);
+  cudaFree(c->tokens);
+  c->keys = nk;
+  c->tokens = nt;
+  c->cap = ncap;
+  return HSD_OK;
+}
+
+hsd_status get_scratch(hsd_collection* c, cudaStream_t s, size_t partial_bytes, Scratch** out) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  Scratch& sc = c->scratch[s];
+  if (!sc.overflow) CU(cudaMalloc(&sc.overflow, sizeof(int)));
+  if (sc.partial_cap < partial_bytes) {
+    cudaFree(sc.partial);
+    sc.partial = nullptr;
+    sc.partial_cap = 0;
+    CU(cudaMalloc(&sc.partial, partial_bytes));
+    sc.partial_cap = partial_bytes;
+  }
+  *out = &sc;
+  return HSD_OK;
+}
+
+constexpr int kSlab = 64;  // queries per similarity launch
+
+// Optional stage events (engine timing): marks[i] is recorded after stage i.
+struct StageMarks {
+  cudaEvent_t after_sim = nullptr;
+  cudaEvent_t after_select = nullptr;
+};
+
+hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, int64_t rb, int64_t re, double* scores,
+                       int32_t* ids, cudaStream_t s, const StageMarks* marks = nullptr) {
+  if (k < 1) return fail(HSD_ERR_INVALID_INPUT, "k must be >= 1");  // store.cpp:60
+  if (k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k = %d exceeds HSD_K_MAX = %d", k, HSD_K_MAX);
+  if (B < 0) return fail(HSD_ERR_INVALID_INPUT, "negative batch");
+  if (B == 0) return HSD_OK;
+  if (!queries || !scores || !ids) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  rb = std::max<int64_t>(rb, 0);
+  re = std::min<int64_t>(re, c->n);
+  const int64_t rows = re - rb;
+  if (rows <= 0) {  // empty collection -> empty result, no error (store.cpp:62-72)
+    const int n = B * k;
+    fill_empty_kernel<<<(n + 255) / 256, 256, 0, s>>>(scores, ids, n);
+    CU(cudaGetLastError());
+    return HSD_OK;
+  }
+  const int nsm = num_sms(c->device);
+  const int Bs0 = std::min(B, kSlab);
+  const hsd::SimPlan plan0 = hsd::sim_plan(Bs0, rows, c->dim, nsm);
+  Scratch* sc = nullptr;
+  st = get_scratch(c, s, (size_t)plan0.lists * Bs0 * hsd::dev::kCandLocal * sizeof(uint64_t), &sc);
+  if (st != HSD_OK) return st;
+  CU(cudaMemsetAsync(sc->overflow, 0, sizeof(int), s));
+  for (int b0 = 0; b0 < B; b0 += kSlab) {
+    const int Bs = std::min(kSlab, B - b0);
+    const hsd::SimPlan plan = hsd::sim_plan(Bs, rows, c->dim, nsm);
+    const float* q = queries + (size_t)b0 * c->dim;
+    CU(hsd::launch_sim(c->keys, rb, re, c->dim, q, Bs, plan, sc->partial, s));
+    if (marks && marks->after_sim && b0 + kSlab >= B) CU(cudaEventRecord(marks->after_sim, s));
+    CU(hsd::launch_select(sc->partial, plan.lists, Bs, k, c->keys, c->dim, q, c->maxnorm, plan.gamma,
+                          scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->overflow, s));
+  }
+  if (marks && marks->after_select) CU(cudaEventRecord(marks->after_select, s));
+  return HSD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hsd_last_error(void) { return g_err.c_str(); }
+int hsd_abi_version(void) { return HSD_ABI_VERSION; }
+
+hsd_status hsd_device_count(int* n) {
+  if (!n) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess) {
+    cudaGetLastError();
+    cnt = 0;
+  }
+  int ok = 0;
+  for (int d = 0; d < cnt; ++d) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++ok;
+  }
+  *n = ok;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_create(int device, int dim, int64_t capacity, hsd_collection** out) {
+  if (!out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *out = nullptr;
+  if (dim < 1) return fail(HSD_ERR_CONFIG, "collection dim must be >= 1");  // store.cpp:37
+  if (dim % 4 != 0) return fail(HSD_ERR_CONFIG, "dim must be a multiple of 4 (128-bit loads), got %d", dim);
+  hsd_status st = require_device(device);
+  if (st != HSD_OK) return st;
+  auto* c = new hsd_collection();
+  c->device = device;
+  c->dim = dim;
+  cudaError_t e = cudaMalloc(&c->maxnorm, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->maxnorm, 0, sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(maxnorm)");
+  }
+  st = ensure_capacity(c, std::max<int64_t>(capacity, 1));
+  if (st != HSD_OK) {
+    hsd_collection_destroy(c);
+    return st;
+  }
+  *out = c;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_destroy(hsd_collection* c) {
+  if (!c) return HSD_OK;
+  cudaSetDevice(c->device);
+  for (auto& kv : c->scratch) {
+    cudaFree(kv.second.partial);
+    cudaFree(kv.second.overflow);
+  }
+  cudaFree(c->keys);
+  cudaFree(c->tokens);
+  cudaFree(c->maxnorm);
+  delete c;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_size(const hsd_collection* c, int64_t* n) {
+  if (!c || !n) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *n = c->n;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_dim(const hsd_collection* c, int* dim) {
+  if (!c || !dim) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *dim = c->dim;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_device(const hsd_collection* c, int* device) {
+  if (!c || !device) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *device = c->device;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_keys(const hsd_collection* c, const float** keys, const uint8_t** tokens) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (keys) *keys = c->keys;
+  if (tokens) *tokens = c->tokens;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_insert(hsd_collection* c, const float* emb, const double* next_actions,
+                                 const int32_t* episode_idx, const int32_t* step_idx, int64_t n, int64_t* first_id) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
+  if (n < 0) return fail(HSD_ERR_INVALID_INPUT, "negative record count");
+  if (first_id) *first_id = c->n;
+  if (n == 0) return HSD_OK;
+  if (!emb || !next_actions) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  for (int64_t i = 0; i < n; ++i)  // store.cpp:50-52
+    if ((episode_idx && episode_idx[i] < 0) || (step_idx && step_idx[i] < 0))
+      return fail(HSD_ERR_SCHEMA, "payload indices must be nonnegative");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  st = ensure_capacity(c, c->n + n);
+  if (st != HSD_OK) return st;
+  double* dact = nullptr;
+  int32_t* dbad = nullptr;
+  CU(cudaMalloc(&dact, (size_t)n * 21 * sizeof(double)));
+  CU(cudaMalloc(&dbad, sizeof(int32_t)));
+  int32_t bad = 0;
+  cudaError_t e = cudaMemcpy(dact, next_actions, (size_t)n * 21 * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(dbad, 0, sizeof(int32_t));
+  if (e == cudaSuccess) e = hsd::launch_quantize_tokens(dact, n, c->tokens + (size_t)c->n * HSD_TOKENS_STRIDE, dbad, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(&bad, dbad, sizeof(int32_t), cudaMemcpyDeviceToHost);
+  cudaFree(dact);
+  cudaFree(dbad);
+  if (e != cudaSuccess) return cuda_fail(e, "insert: quantize payload");
+  if (bad) return fail(HSD_ERR_INVALID_INPUT, "non-finite action value in payload");  // actions.cpp:38-40
+  CU(cudaMemcpy(c->keys + (size_t)c->n * c->dim, emb, (size_t)n * c->dim * sizeof(float), cudaMemcpyHostToDevice));
+  CU(hsd::launch_row_norms(c->keys, c->n, n, c->dim, c->maxnorm, 0));
+  CU(cudaDeviceSynchronize());
+  c->n += n;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_generate(hsd_collection* c, int kind, uint64_t db_seed, int64_t n) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
+  return hsd_collection_generate_rows(c, kind, db_seed, c->n, n);
+}
+
+hsd_status hsd_collection_generate_rows(hsd_collection* c, int kind, uint64_t db_seed, int64_t row0, int64_t n) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
+  if (row0 < 0) return fail(HSD_ERR_INVALID_INPUT, "negative row offset");
+  if (kind != 0 && kind != 1) return fail(HSD_ERR_CONFIG, "unknown synthetic family %d", kind);
+  if (n < 0) return fail(HSD_ERR_INVALID_INPUT, "negative record count");
+  if (n == 0) return HSD_OK;
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  st = ensure_capacity(c, c->n + n);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_gen_keys(kind, db_seed, row0, n, c->dim, c->keys + (size_t)c->n * c->dim,
+                          c->tokens + (size_t)c->n * HSD_TOKENS_STRIDE, c->maxnorm, 0));
+  CU(cudaDeviceSynchronize());
+  c->n += n;
+  return HSD_OK;
+}
+
+hsd_status hsd_search_topk_exact(hsd_collection* c, const float* queries, int B, int k, double* scores, int32_t* ids,
+                                 void* stream) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
+  return search_impl(c, queries, B, k, 0, c->n, scores, ids, (cudaStream_t)stream);
+}
+
+hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B, int k, int64_t row_begin,
+                                 int64_t row_end, double* scores, int32_t* ids, void* stream) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
+  if (row_begin > row_end) return fail(HSD_ERR_INVALID_INPUT, "row_begin > row_end");
+  return search_impl(c, queries, B, k, row_begin, row_end, scores, ids, (cudaStream_t)stream);
+}
+
+hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count) {
+  if (!c || !count) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  *count = 0;
+  int* ov = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    auto it = c->scratch.find((cudaStream_t)stream);
+    if (it == c->scratch.end()) return HSD_OK;
+    ov = it->second.overflow;
+  }
+  CU(cudaStreamSynchronize((cudaStream_t)stream));
+  CU(cudaMemcpy(count, ov, sizeof(int), cudaMemcpyDeviceToHost));
+  return HSD_OK;
+}
+
+static hsd_status check_verify_params(const hsd_verify_params* params, int P) {
+  if (!params || P < 1) return fail(HSD_ERR_INVALID_INPUT, "need at least one parameter set");
+  for (int i = 0; i < P; ++i) {
+    const hsd_verify_params& p = params[i];
+    if (p.bias_seq_max < 0 || p.bias_token_max < 0 || p.bias_token_max > p.bias_seq_max)
+      return fail(HSD_ERR_CONFIG, "acceptance caps must satisfy 0 <= bias_token_max <= bias_seq_max (SPEC.md:409)");
+    if (p.skip_enabled && p.O_dist < 1) return fail(HSD_ERR_CONFIG, "O_dist must be >= 1 (SPEC.md:413)");
+  }
+  return HSD_OK;
+}
+
+// device copies of parameter arrays, cached per stream
+namespace {
+struct ParamCache {
+  std::mutex mu;
+  std::unordered_map<cudaStream_t, std::pair<hsd_verify_params*, std::vector<hsd_verify_params>>> m;
+} g_params;
+
+hsd_status device_params(int device, const hsd_verify_params* params, int P, cudaStream_t s,
+                         const hsd_verify_params** out) {
+  std::lock_guard<std::mutex> lk(g_params.mu);
+  auto& ent = g_params.m[s];
+  const bool same = ent.second.size() == (size_t)P &&
+                    std::memcmp(ent.second.data(), params, sizeof(hsd_verify_params) * P) == 0;
+  if (!same) {
+    if (ent.second.size() < (size_t)P || !ent.first) {
+      if (ent.first) {
+        cudaStreamSynchronize(s);
+        cudaFree(ent.first);
+      }
+      ent.first = nullptr;
+      CU(cudaMalloc(&ent.first, sizeof(hsd_verify_params) * std::max(P, 16)));
+    } else {
+      cudaStreamSynchronize(s);  // the previous parameters may still be in use
+    }
+    CU(cudaMemcpy(ent.first, params, sizeof(hsd_verify_params) * P, cudaMemcpyHostToDevice));
+    ent.second.assign(params, params + P);
+  }
+  (void)device;
+  *out = ent.first;
+  return HSD_OK;
+}
+}  // namespace
+
+static hsd_status verify_impl(int device, hsd_collection* c, const uint8_t* drafts, const int32_t* ids, int E, int k,
+                              int L, const float* logits, const float* feat_now, const float* feat_prev, int d_f,
+                              const int32_t* history, int gap_d, const hsd_verify_params* params, int P,
+                              hsd_outcome* out, uint8_t* tokens, void* stream) {
+  if (L != 7 && L != 21) return fail(HSD_ERR_INVALID_INPUT, "draft length must be 7 or 21, got %d", L);
+  if (k < 1 || k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k must be in [1, %d]", HSD_K_MAX);
+  if (E < 0) return fail(HSD_ERR_INVALID_INPUT, "negative episode count");
+  hsd_status st = check_verify_params(params, P);
+  if (st != HSD_OK) return st;
+  if (E == 0) return HSD_OK;
+  if (!ids || !logits || !out || !tokens) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  int need_cos = 0;
+  for (int i = 0; i < P; ++i) need_cos |= params[i].skip_enabled;
+  if (need_cos && (!feat_now || !feat_prev || d_f < 4 || d_f % 4))
+    return fail(HSD_ERR_INVALID_INPUT, "verify-skip needs fp32 features with d_f a multiple of 4");
+  st = require_device(device);
+  if (st != HSD_OK) return st;
+  const hsd_verify_params* dp = nullptr;
+  st = device_params(device, params, P, (cudaStream_t)stream, &dp);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_verify(ids, E, k, L, c ? c->tokens : nullptr, drafts, logits, feat_now, feat_prev, d_f, history, gap_d, dp, P,
+                        need_cos, out, tokens, (cudaStream_t)stream));
+  return HSD_OK;
+}
+
+hsd_status hsd_verify_round(hsd_collection* c, const int32_t* ids, int E, int k, int L, const float* logits,
+                            const float* feat_now, const float* feat_prev, int d_f, const int32_t* history, int gap_d,
+                            const hsd_verify_params* params, int P, hsd_outcome* out, uint8_t* tokens, void* stream) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
+  return verify_impl(c->device, c, nullptr, ids, E, k, L, logits, feat_now, feat_prev, d_f, history, gap_d, params, P,
+                     out, tokens, stream);
+}
+
+hsd_status hsd_verify_round_drafts(int device, const int32_t* ids, const uint8_t* drafts, int E, int k, int L,
+                                   const float* logits, const float* feat_now, const float* feat_prev, int d_f,
+                                   const int32_t* history, int gap_d, const hsd_verify_params* params, int P,
+                                   hsd_outcome* out, uint8_t* tokens, void* stream) {
+  if (!drafts) return fail(HSD_ERR_INVALID_INPUT, "null drafts");
+  return verify_impl(device, nullptr, drafts, ids, E, k, L, logits, feat_now, feat_prev, d_f, history, gap_d, params,
+                     P, out, tokens, stream);
+}
+
+static hsd_status check_metric(const hsd_metric_params* mp, const hsd_norm_bounds* nb) {
+  if (!mp || !nb) return fail(HSD_ERR_INVALID_INPUT, "null parameters");
+  // FusedMetricParams::validate (kinematics.cpp:19-24)
+  if (!(mp->alpha >= 0.0 && mp->alpha <= 1.0)) return fail(HSD_ERR_CONFIG, "metric.alpha must lie in [0,1]");
+  if (mp->w < 3) return fail(HSD_ERR_CONFIG, "metric.window must be >= 3");
+  if (mp->w > 32) return fail(HSD_ERR_CONFIG, "metric.window must be <= 32 on the device path");
+  if (!(mp->threshold >= 0.0 && mp->threshold <= 1.0)) return fail(HSD_ERR_CONFIG, "metric.threshold must lie in [0,1]");
+  if (!(mp->r_cap > 0.0)) return fail(HSD_ERR_CONFIG, "metric.r_cap must be positive");
+  // NormalizationBounds::validate (kinematics.cpp:13-17)
+  if (!(nb->d_min >= 0.0) || !(nb->r_min >= 0.0)) return fail(HSD_ERR_CONFIG, "normalization bounds must be nonnegative");
+  if (nb->d_min > nb->d_max95) return fail(HSD_ERR_CONFIG, "d_min exceeds d_max95");
+  if (nb->r_min > nb->r_max95) return fail(HSD_ERR_CONFIG, "r_min exceeds r_max95");
+  return HSD_OK;
+}
+
+hsd_status hsd_window_features(int device, const double* xyz, int W, const hsd_metric_params* params,
+                               const hsd_norm_bounds* bounds, const int32_t* history, double* R, double* D, double* F,
+                               int32_t* decision, void* stream) {
+  hsd_status st = check_metric(params, bounds);
+  if (st != HSD_OK) return st;
+  if (W < 0) return fail(HSD_ERR_INVALID_INPUT, "negative window count");
+  if (W == 0) return HSD_OK;
+  if (!xyz || !R || !D || !F || !decision) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  st = require_device(device);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_kinematics(xyz, W, *params, *bounds, history, R, D, F, decision, (cudaStream_t)stream));
+  return HSD_OK;
+}
+
+hsd_status hsd_quantize(int device, const double* actions, int64_t n, const double* lo7, const double* hi7, int k_bins,
+                        int32_t* bins, int32_t* status, void* stream) {
+  if (k_bins < 2) return fail(HSD_ERR_CONFIG, "bin count must be >= 2, got %d", k_bins);  // actions.cpp:28-30
+  if (!lo7 || !hi7) return fail(HSD_ERR_INVALID_INPUT, "null bounds");
+  for (int i = 0; i < 7; ++i) {  // ActionSpaceBounds::validate (actions.cpp:17-26)
+    if (!std::isfinite(lo7[i]) || !std::isfinite(hi7[i]))
+      return fail(HSD_ERR_CONFIG, "action bounds must be finite (dim %d)", i);
+    if (!(lo7[i] < hi7[i])) return fail(HSD_ERR_CONFIG, "degenerate action bounds on dim %d", i);
+  }
+  if (n < 0) return fail(HSD_ERR_INVALID_INPUT, "negative count");
+  if (n == 0) return HSD_OK;
+  if (!actions || !bins) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(device);
+  if (st != HSD_OK) return st;
+  double lohi[14];
+  std::memcpy(lohi, lo7, 7 * sizeof(double));
+  std::memcpy(lohi + 7, hi7, 7 * sizeof(double));
+  double* d = nullptr;
+  CU(cudaMalloc(&d, sizeof(lohi)));
+  cudaError_t e = cudaMemcpy(d, lohi, sizeof(lohi), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = hsd::launch_quantize(actions, n, d, k_bins, bins, status, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "quantize");
+  return HSD_OK;
+}
+
+// ----------------------------------------------------------------------- engine
+}  // extern "C"
+
+struct hsd_engine {
+  hsd_collection* c = nullptr;
+  int max_B = 0, k = 0, L = 0, d_f = 0, w = 0;
+  // device staging for hsd_step_host
+  float *q = nullptr, *logits = nullptr, *fnow = nullptr, *fprev = nullptr;
+  double* xyz = nullptr;
+  int32_t* hist = nullptr;
+  double* scores = nullptr;
+  int32_t* ids = nullptr;
+  hsd_outcome* out = nullptr;
+  uint8_t* tok = nullptr;
+  double *R = nullptr, *D = nullptr, *F = nullptr;
+  int32_t* dec = nullptr;
+  // stage timing: 5 events per step (start, kinematics, similarity, select, verify)
+  std::vector<cudaEvent_t> ev;
+  int max_steps = 0, recorded = 0;
+};
+
+extern "C" {
+
+hsd_status hsd_engine_create(hsd_collection* c, int max_B, int k, int L, int d_f, int w, hsd_engine** out) {
+  if (!c || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *out = nullptr;
+  if (max_B < 1 || k < 1 || k > HSD_K_MAX || (L != 7 && L != 21) || d_f < 0 || d_f % 4 || w < 3 || w > 32)
+    return fail(HSD_ERR_INVALID_INPUT, "bad engine shape");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  auto* e = new hsd_engine();
+  e->c = c;
+  e->max_B = max_B;
+  e->k = k;
+  e->L = L;
+  e->d_f = d_f;
+  e->w = w;
+  cudaError_t r = cudaSuccess;
+  auto alloc = [&](auto** p, size_t bytes) {
+    if (r == cudaSuccess && bytes) r = cudaMalloc(p, bytes);
+  };
+  alloc(&e->q, (size_t)max_B * c->dim * 4);
+  alloc(&e->logits, (size_t)max_B * L * 256 * 4);
+  alloc(&e->fnow, (size_t)max_B * d_f * 4);
+  alloc(&e->fprev, (size_t)max_B * d_f * 4);
+  alloc(&e->xyz, (size_t)max_B * w * 3 * 8);
+  alloc(&e->hist, (size_t)max_B * 4);
+  alloc(&e->scores, (size_t)max_B * k * 8);
+  alloc(&e->ids, (size_t)max_B * k * 4);
+  alloc(&e->out, (size_t)max_B * sizeof(hsd_outcome));
+  alloc(&e->tok, (size_t)max_B * L);
+  alloc(&e->R, (size_t)max_B * 8);
+  alloc(&e->D, (size_t)max_B * 8);
+  alloc(&e->F, (size_t)max_B * 8);
+  alloc(&e->dec, (size_t)max_B * 4);
+  if (r != cudaSuccess) {
+    hsd_engine_destroy(e);
+    return cuda_fail(r, "engine buffers");
+  }
+  *out = e;
+  return HSD_OK;
+}
+
+hsd_status hsd_engine_enable_timing(hsd_engine* e, int max_steps) {
+  if (!e || max_steps < 0) return fail(HSD_ERR_INVALID_INPUT, "bad arguments");
+  hsd_status st = require_device(e->c->device);
+  if (st != HSD_OK) return st;
+  for (cudaEvent_t x : e->ev) cudaEventDestroy(x);
+  e->ev.assign((size_t)max_steps * 5, nullptr);
+  for (auto& x : e->ev) CU(cudaEventCreate(&x));
+  e->max_steps = max_steps;
+  e->recorded = 0;
+  return HSD_OK;
+}
+
+hsd_status hsd_engine_stage_times(hsd_engine* e, int* n_steps, double* ms) {
+  if (!e || !n_steps || !ms) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(e->c->device);
+  if (st != HSD_OK) return st;
+  for (int i = 0; i < 5; ++i) ms[i] = 0.0;
+  for (int s = 0; s < e->recorded; ++s) {
+    cudaEvent_t* v = &e->ev[(size_t)s * 5];
+    CU(cudaEventSynchronize(v[4]));
+    for (int i = 0; i < 4; ++i) {
+      float t = 0.f;
+      CU(cudaEventElapsedTime(&t, v[i], v[i + 1]));
+      ms[i] += t;
+    }
+    float tot = 0.f;
+    CU(cudaEventElapsedTime(&tot, v[0], v[4]));
+    ms[4] += tot;
+  }
+  *n_steps = e->recorded;
+  e->recorded = 0;
+  return HSD_OK;
+}
+
+hsd_status hsd_engine_destroy(hsd_engine* e) {
+  if (!e) return HSD_OK;
+  cudaSetDevice(e->c->device);
+  for (cudaEvent_t x : e->ev) cudaEventDestroy(x);
+  void* ps[] = {e->q, e->logits, e->fnow, e->fprev, e->xyz, e->hist, e->scores, e->ids, e->out, e->tok, e->R, e->D,
+                e->F, e->dec};
+  for (void* p : ps) cudaFree(p);
+  delete e;
+  return HSD_OK;
+}
+
+hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                    const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream) {
+  if (!e || !io || !vp) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (B < 0 || B > e->max_B) return fail(HSD_ERR_INVALID_INPUT, "batch %d outside [0, %d]", B, e->max_B);
+  if (B == 0) return HSD_OK;
+  hsd_status st;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t* ev = (e->recorded < e->max_steps) ? &e->ev[(size_t)e->recorded * 5] : nullptr;
+  if (ev) CU(cudaEventRecord(ev[0], s));
+  if (io->xyz) {  // K5: hybrid boundary (decide_sd)
+    st = hsd_window_features(e->c->device, io->xyz, B, mp, nb, io->history, io->R, io->D, io->F, io->decision, stream);
+    if (st != HSD_OK) return st;
+  }
+  if (ev) CU(cudaEventRecord(ev[1], s));
+  StageMarks marks;
+  if (ev) {
+    marks.after_sim = ev[2];
+    marks.after_select = ev[3];
+  }
+  st = search_impl(e->c, io->queries, B, e->k, 0, e->c->n, io->scores, io->ids, s, ev ? &marks : nullptr);  // K1+K2
+  if (st != HSD_OK) return st;
+  st = hsd_verify_round(e->c, io->ids, B, e->k, e->L, io->logits, io->feat_now, io->feat_prev, e->d_f, io->history,
+                        gap_d, vp, 1, io->out, io->tokens, stream);  // K4
+  if (st != HSD_OK) return st;
+  if (ev) {
+    CU(cudaEventRecord(ev[4], s));
+    ++e->recorded;
+  }
+  return HSD_OK;
+}
+
+hsd_status hsd_step_host(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                         const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream) {
+  if (!e || !io) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (B < 0 || B > e->max_B) return fail(HSD_ERR_INVALID_INPUT, "batch %d outside [0, %d]", B, e->max_B);
+  if (B == 0) return HSD_OK;
+  hsd_status st = require_device(e->c->device);
+  if (st != HSD_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int dim = e->c->dim;
+  hsd_step_io d{};
+  CU(cudaMemcpyAsync(e->q, io->queries, (size_t)B * dim * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(e->logits, io->logits, (size_t)B * e->L * 256 * 4, cudaMemcpyHostToDevice, s));
+  d.queries = e->q;
+  d.logits = e->logits;
+  if (io->feat_now && io->feat_prev && e->d_f) {
+    CU(cudaMemcpyAsync(e->fnow, io->feat_now, (size_t)B * e->d_f * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(e->fprev, io->feat_prev, (size_t)B * e->d_f * 4, cudaMemcpyHostToDevice, s));
+    d.feat_now = e->fnow;
+    d.feat_prev = e->fprev;
+  }
+  if (io->xyz) {
+    CU(cudaMemcpyAsync(e->xyz, io->xyz, (size_t)B * e->w * 3 * 8, cudaMemcpyHostToDevice, s));
+    d.xyz = e->xyz;
+  }
+  if (io->history) {
+    CU(cudaMemcpyAsync(e->hist, io->history, (size_t)B * 4, cudaMemcpyHostToDevice, s));
+    d.history = e->hist;
+  }
+  d.scores = e->scores;
+  d.ids = e->ids;
+  d.out = e->out;
+  d.tokens = e->tok;
+  d.R = e->R;
+  d.D = e->D;
+  d.F = e->F;
+  d.decision = e->dec;
+  st = hsd_step(e, B, &d, vp, mp, nb, gap_d, stream);
+  if (st != HSD_OK) return st;
+  if (io->scores) CU(cudaMemcpyAsync(io->scores, e->scores, (size_t)B * e->k * 8, cudaMemcpyDeviceToHost, s));
+  if (io->ids) CU(cudaMemcpyAsync(io->ids, e->ids, (size_t)B * e->k * 4, cudaMemcpyDeviceToHost, s));
+  if (io->out) CU(cudaMemcpyAsync(io->out, e->out, (size_t)B * sizeof(hsd_outcome), cudaMemcpyDeviceToHost, s));
+  if (io->tokens) CU(cudaMemcpyAsync(io->tokens, e->tok, (size_t)B * e->L, cudaMemcpyDeviceToHost, s));
+  if (io->xyz) {
+    if (io->R) CU(cudaMemcpyAsync(io->R, e->R, (size_t)B * 8, cudaMemcpyDeviceToHost, s));
+    if (io->D) CU(cudaMemcpyAsync(io->D, e->D, (size_t)B * 8, cudaMemcpyDeviceToHost, s));
+    if (io->F) CU(cudaMemcpyAsync(io->F, e->F, (size_t)B * 8, cudaMemcpyDeviceToHost, s));
+    if (io->decision) CU(cudaMemcpyAsync(io->decision, e->dec, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+  }
+  CU(cudaStreamSynchronize(s));
+  return HSD_OK;
+}
+
+// ------------------------------------------------------------------ multi-GPU
+}  // extern "C"
+
+struct hsd_comm {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0, device = 0;
+  double* gs = nullptr;
+  int32_t* gi = nullptr;
+  double* ls = nullptr;
+  int32_t* li = nullptr;
+  uint8_t* gt = nullptr;
+  uint8_t* lt = nullptr;
+  size_t cap = 0;  // entries per rank
+};
+
+extern "C" {
+
+hsd_status hsd_comm_unique_id(uint8_t id[HSD_UNIQUE_ID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == HSD_UNIQUE_ID_BYTES, "NCCL unique id size");
+  if (!id) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  ncclUniqueId u;
+  NC(ncclGetUniqueId(&u));
+  std::memcpy(id, &u, sizeof(u));
+  return HSD_OK;
+}
+
+hsd_status hsd_comm_create(const uint8_t id[HSD_UNIQUE_ID_BYTES], int world, int rank, int device, hsd_comm** out) {
+  if (!id || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (world < 1 || rank < 0 || rank >= world) return fail(HSD_ERR_INVALID_INPUT, "bad rank %d of %d", rank, world);
+  hsd_status st = require_device(device);
+  if (st != HSD_OK) return st;
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  auto* c = new hsd_comm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  ncclResult_t r = ncclCommInitRank(&c->comm, world, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(HSD_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return HSD_OK;
+}
+
+hsd_status hsd_comm_destroy(hsd_comm* c) {
+  if (!c) return HSD_OK;
+  cudaSetDevice(c->device);
+  if (c->comm) ncclCommDestroy(c->comm);
+  void* ps[] = {c->gs, c->gi, c->ls, c->li, c->gt, c->lt};
+  for (void* p : ps) cudaFree(p);
+  delete c;
+  return HSD_OK;
+}
+
+hsd_status hsd_shard_range(int64_t n_total, int world, int rank, int64_t* begin, int64_t* end) {
+  if (!begin || !end) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (world < 1 || rank < 0 || rank >= world || n_total < 0) return fail(HSD_ERR_INVALID_INPUT, "bad shard request");
+  const int64_t base = n_total / world, rem = n_total % world;
+  *begin = rank * base + std::min<int64_t>(rank, rem);
+  *end = *begin + base + (rank < rem ? 1 : 0);
+  return HSD_OK;
+}
+
+hsd_status hsd_search_topk_sharded(hsd_collection* col, hsd_comm* cm, int64_t id_offset, const float* queries, int B,
+                                   int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream) {
+  if (!col || !cm) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (k < 1 || k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k must be in [1, %d]", HSD_K_MAX);
+  if (B <= 0) return B == 0 ? HSD_OK : fail(HSD_ERR_INVALID_INPUT, "negative batch");
+  hsd_status st = require_device(col->device);
+  if (st != HSD_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t need = (size_t)B * k;
+  if (cm->cap < need) {
+    void* ps[] = {cm->gs, cm->gi, cm->ls, cm->li, cm->gt, cm->lt};
+    for (void* p : ps) cudaFree(p);
+    cm->gs = nullptr;
+    cm->gi = nullptr;
+    cm->ls = nullptr;
+    cm->li = nullptr;
+    cm->gt = nullptr;
+    cm->lt = nullptr;
+    cm->cap = 0;
+    CU(cudaMalloc(&cm->gs, need * cm->world * 8));
+    CU(cudaMalloc(&cm->gi, need * cm->world * 4));
+    CU(cudaMalloc(&cm->gt, need * cm->world * HSD_TOKENS_STRIDE));
+    CU(cudaMalloc(&cm->ls, need * 8));
+    CU(cudaMalloc(&cm->li, need * 4));
+    CU(cudaMalloc(&cm->lt, need * HSD_TOKENS_STRIDE));
+    cm->cap = need;
+  }
+  // local top-k over this rank's shard (K1 + K2), then the 32-B draft record
+  st = search_impl(col, queries, B, k, 0, col->n, cm->ls, cm->li, s);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_gather_tokens(col->tokens, cm->li, (int)need, cm->lt, s));
+  offset_ids_kernel<<<(int)((need + 255) / 256), 256, 0, s>>>(cm->li, (int)need, id_offset);
+  CU(cudaGetLastError());
+  // K3: exchange the B x k records over NVLink and merge (score desc, id asc)
+  NC(ncclGroupStart());
+  NC(ncclAllGather(cm->ls, cm->gs, need, ncclFloat64, cm->comm, s));
+  NC(ncclAllGather(cm->li, cm->gi, need, ncclInt32, cm->comm, s));
+  NC(ncclAllGather(cm->lt, cm->gt, need * HSD_TOKENS_STRIDE, ncclUint8, cm->comm, s));
+  NC(ncclGroupEnd());
+  CU(hsd::launch_merge_ranks(cm->gs, cm->gi, cm->gt, cm->world, B, k, scores, ids, drafts, s));
+  return HSD_OK;
+}
+
+// ------------------------------------------------------------------ generators
+hsd_status hsd_gen_queries(int device, int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B,
+                           int dim, float* out, void* stream) {
+  if (kind != 0 && kind != 1) return fail(HSD_ERR_CONFIG, "unknown synthetic family %d", kind);
+  if (B < 0 || dim < 1) return fail(HSD_ERR_INVALID_INPUT, "bad shape");
+  hsd_status st = require_device(device);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_gen_queries(kind, q_seed, db_seed, n_rows, q0, B, dim, out, (cudaStream_t)stream));
+  return HSD_OK;
+}
+
+hsd_status hsd_gen_logits(hsd_collection* c, uint64_t seed, const int64_t* rows, int E, int L, float* out,
+                          void* stream) {
+  if (!c || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (L < 1 || L > 21) return fail(HSD_ERR_INVALID_INPUT, "bad draft length");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_gen_logits(c->tokens, seed, rows, E, L, out, (cudaStream_t)stream));
+  return HSD_OK;
+}
+
+hsd_status hsd_gen_features(int device, uint64_t seed, int E, int d_f, float* now, float* prev, void* stream) {
+  if (!now || !prev || d_f < 1 || E < 0) return fail(HSD_ERR_INVALID_INPUT, "bad arguments");
+  hsd_status st = require_device(device);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_gen_features(seed, E, d_f, now, prev, (cudaStream_t)stream));
+  return HSD_OK;
+}
+
+}  // extern "C"

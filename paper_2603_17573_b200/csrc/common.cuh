@@ -1,0 +1,116 @@
+// common.cuh — shared device helpers for the HeiSD hot-path kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hsd {
+namespace dev {
+
+constexpr int kWarp = 32;
+constexpr int kCandLocal = 32;     // candidates kept per (CTA, query) by the similarity kernels
+constexpr uint64_t kEmpty = ~0ull; // empty candidate slot (sorts last)
+
+// ---- candidate keys ---------------------------------------------------------
+// A candidate is (approx score f32, record id u32) packed so that ASCENDING u64
+// order is the reference's (score desc, id asc) order (store.cpp:67-70).
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+  uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ uint64_t cand_key(float s, uint32_t id) {
+  if (s != s) s = -INFINITY;  // NaN ranks last
+  return ((uint64_t)(~f2ord(s)) << 32) | (uint64_t)id;
+}
+__device__ __forceinline__ float cand_score(uint64_t k) { return ord2f(~(uint32_t)(k >> 32)); }
+__device__ __forceinline__ uint32_t cand_id(uint64_t k) { return (uint32_t)(k & 0xFFFFFFFFu); }
+
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
+  uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(v >> 32), m);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
+  uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
+  uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// ---- warp bitonic sort ------------------------------------------------------
+// Sorts 32*V u64 keys ascending across a warp; element i lives in lane
+// (i % 32), slot (i / 32).
+template <int V>
+__device__ __forceinline__ void warp_sort(uint64_t (&a)[V]) {
+  const int lane = threadIdx.x & 31;
+  constexpr int N = 32 * V;
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {
+        const int vs = stride / 32;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int pv = v ^ vs;
+          if (pv > v) {
+            const int i = v * 32 + lane;
+            const bool asc = (i & size) == 0;
+            uint64_t x = a[v], y = a[pv];
+            const bool sw = asc ? (x > y) : (x < y);
+            a[v] = sw ? y : x;
+            a[pv] = sw ? x : y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int i = v * 32 + lane;
+          const bool asc = (i & size) == 0;
+          const uint64_t y = shfl_xor_u64(a[v], stride);
+          const bool lower = (lane & stride) == 0;
+          const uint64_t mn = a[v] < y ? a[v] : y;
+          const uint64_t mx = a[v] < y ? y : a[v];
+          a[v] = (asc == lower) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
+// Merge a sorted-ascending 32-key list `x` (one per lane) into the running
+// sorted top-32 `top` (one per lane): keeps the 32 smallest, sorted.
+__device__ __forceinline__ uint64_t warp_merge_top32(uint64_t top, uint64_t x) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t y = shfl_u64(x, 31 - lane);  // reverse -> bitonic with `top`
+  uint64_t m = top < y ? top : y;              // lower half of the 64-element bitonic merge
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    const uint64_t o = shfl_xor_u64(m, stride);
+    const bool lower = (lane & stride) == 0;
+    m = lower ? (m < o ? m : o) : (m < o ? o : m);
+  }
+  return m;
+}
+
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Knuth TwoSum (error-free transformation).
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  double bv = __dsub_rn(s, a);
+  double av = __dsub_rn(s, bv);
+  e = __dadd_rn(__dsub_rn(a, av), __dsub_rn(b, bv));
+}
+
+}  // namespace dev
+}  // namespace hsd

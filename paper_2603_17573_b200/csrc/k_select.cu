@@ -1,0 +1,223 @@
+// k_select.cu — K2 select and K3 shard merge.
+//
+// K2, one CTA per query:
+//   1. merge the per-CTA candidate lists (sorted u64 keys) into the global
+//      approximate top-32 (warp bitonic merges) -> A_k, the k-th best approx
+//      score;
+//   2. margin: every record whose EXACT score can reach the exact k-th score
+//      has approx >= A_k - 2E, E = gamma * max|key| * |q| (forward error bound
+//      of the approximate path).  Collect all such candidates; flag overflow
+//      if a per-CTA list was exhausted above the margin;
+//   3. rescore the candidates with the reference's arithmetic — cosine_similarity
+//      (store.cpp:29-34): s += q[i] * k[i] sequentially in fp64 — so scores are
+//      bit-identical to the reference;
+//   4. order (score desc, id asc) (store.cpp:67-70), truncate to k (:71).
+// K3: k-way merge of G ranks' exact top-k lists (multi-GPU all-gather result).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hsd {
+namespace {
+
+using dev::cand_id;
+using dev::cand_score;
+using dev::kCandLocal;
+using dev::kEmpty;
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kPool = 256;
+constexpr int kCandMax = 64;
+constexpr int kChunk = 128;          // columns staged per rescoring pass
+constexpr int kRowStride = kChunk + 1;  // bank-conflict-free sequential reads
+
+struct SelectSmem {
+  uint64_t top[kWarps][32];
+  uint64_t pool[kPool];
+  float rows[kCandMax * kRowStride];
+  float q[kChunk];
+  double exact[kCandMax];
+  uint32_t id[kCandMax];
+  double red[kWarps];
+  int pool_n;
+  int over;
+};
+
+__global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __restrict__ partial, int lists, int B, int k,
+                                                          const float* __restrict__ keys, int dim,
+                                                          const float* __restrict__ queries,
+                                                          const unsigned long long* __restrict__ maxnorm_bits,
+                                                          double gamma, double* __restrict__ scores,
+                                                          int32_t* __restrict__ ids, int* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SelectSmem& S = *reinterpret_cast<SelectSmem*>(smem_raw);
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float* qrow = queries + (size_t)b * dim;
+
+  // 1. approximate global top-32
+  uint64_t top = kEmpty;
+  for (int l = warp; l < lists; l += kWarps) top = dev::warp_merge_top32(top, partial[((size_t)l * B + b) * kCandLocal + lane]);
+  S.top[warp][lane] = top;
+  double qq = 0.0;
+  for (int i = tid; i < dim; i += kThreads) qq += (double)qrow[i] * (double)qrow[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
+  if (lane == 0) S.red[warp] = qq;
+  if (tid == 0) {
+    S.pool_n = 0;
+    S.over = 0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t t = S.top[0][lane];
+    for (int w = 1; w < kWarps; ++w) t = dev::warp_merge_top32(t, S.top[w][lane]);
+    S.top[0][lane] = t;
+  }
+  __syncthreads();
+  double qn2 = 0.0;
+  for (int w = 0; w < kWarps; ++w) qn2 += S.red[w];
+  const uint64_t kth = S.top[0][k - 1];
+  const double maxnorm = __longlong_as_double((long long)*maxnorm_bits);
+  const double E = gamma * maxnorm * sqrt(qn2) * 1.000001 + 1e-300;
+  const double T = (kth == kEmpty) ? -INFINITY : (double)cand_score(kth) - 2.0 * E;
+
+  // 2. margin candidates
+  for (int l = tid; l < lists; l += kThreads) {
+    const uint64_t* lst = partial + ((size_t)l * B + b) * kCandLocal;
+    int j = 0;
+    for (; j < kCandLocal; ++j) {
+      const uint64_t key = lst[j];
+      if (key == kEmpty || (double)cand_score(key) < T) break;
+      const int slot = atomicAdd(&S.pool_n, 1);
+      if (slot < kPool) S.pool[slot] = key;
+    }
+    if (j == kCandLocal) S.over = 1;  // list exhausted above the margin
+  }
+  __syncthreads();
+  int n = S.pool_n;
+  if (n > kPool) {
+    n = kPool;
+    if (tid == 0) S.over = 1;
+  }
+  if (n > kCandMax) {
+    if (warp == 0) {
+      uint64_t v[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) v[s] = s * 32 + lane < n ? S.pool[s * 32 + lane] : kEmpty;
+      dev::warp_sort<8>(v);
+      S.pool[lane] = v[0];
+      S.pool[32 + lane] = v[1];
+    }
+    n = kCandMax;
+    if (tid == 0) S.over = 1;
+  }
+  __syncthreads();
+  if (tid < n) S.id[tid] = cand_id(S.pool[tid]);
+  __syncthreads();
+
+  // 3. exact rescoring in the reference's order
+  double acc = 0.0;
+  for (int c0 = 0; c0 < dim; c0 += kChunk) {
+    const int w = dim - c0 < kChunk ? dim - c0 : kChunk;
+    for (int i = tid; i < n * kChunk; i += kThreads) {
+      const int c = i / kChunk, j = i % kChunk;
+      S.rows[c * kRowStride + j] = j < w ? keys[(size_t)S.id[c] * dim + c0 + j] : 0.f;
+    }
+    for (int j = tid; j < kChunk; j += kThreads) S.q[j] = j < w ? qrow[c0 + j] : 0.f;
+    __syncthreads();
+    if (tid < n) {
+      const float* r = &S.rows[tid * kRowStride];
+      for (int j = 0; j < w; ++j) acc = __dadd_rn(acc, __dmul_rn((double)S.q[j], (double)r[j]));
+    }
+    __syncthreads();
+  }
+  if (tid < n) S.exact[tid] = acc;
+  __syncthreads();
+
+  // 4. rank by (score desc, id asc) and emit the first k
+  if (tid < n) {
+    const double s = S.exact[tid];
+    const uint32_t me = S.id[tid];
+    int rank = 0;
+    for (int c = 0; c < n; ++c) {
+      const double o = S.exact[c];
+      rank += (o > s) || (o == s && S.id[c] < me);
+    }
+    if (rank < k) {
+      scores[(size_t)b * k + rank] = s;
+      ids[(size_t)b * k + rank] = (int32_t)me;
+    }
+  }
+  for (int r = n + tid; r < k; r += kThreads) {
+    scores[(size_t)b * k + r] = -INFINITY;
+    ids[(size_t)b * k + r] = -1;
+  }
+  if (tid == 0 && S.over) atomicAdd(overflow, 1);
+}
+
+// K3: G sorted lists [G][B][k] -> global [B][k].
+__global__ void merge_ranks_kernel(const double* __restrict__ gs, const int32_t* __restrict__ gi,
+                                   const uint8_t* __restrict__ gt, int G, int B, int k, double* __restrict__ scores,
+                                   int32_t* __restrict__ ids, uint8_t* __restrict__ tok) {
+  const int b = blockIdx.x;
+  const int n = G * k;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int g = i / k, j = i % k;
+    const int32_t me = gi[((size_t)g * B + b) * k + j];
+    if (me < 0) continue;
+    const double s = gs[((size_t)g * B + b) * k + j];
+    int rank = 0;
+    for (int c = 0; c < n; ++c) {
+      const int gg = c / k, jj = c % k;
+      const int32_t o = gi[((size_t)gg * B + b) * k + jj];
+      if (o < 0) continue;
+      const double os = gs[((size_t)gg * B + b) * k + jj];
+      rank += (os > s) || (os == s && o < me);
+    }
+    if (rank < k) {
+      scores[(size_t)b * k + rank] = s;
+      ids[(size_t)b * k + rank] = me;
+      if (tok) {
+        const uint4* src = reinterpret_cast<const uint4*>(gt + (((size_t)g * B + b) * k + j) * HSD_TOKENS_STRIDE);
+        uint4* dst = reinterpret_cast<uint4*>(tok + ((size_t)b * k + rank) * HSD_TOKENS_STRIDE);
+        dst[0] = src[0];
+        dst[1] = src[1];
+      }
+    }
+  }
+  // ranks beyond the number of valid entries
+  __shared__ int valid;
+  if (threadIdx.x == 0) valid = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (gi[((size_t)(i / k) * B + b) * k + (i % k)] >= 0) atomicAdd(&valid, 1);
+  __syncthreads();
+  for (int r = valid + threadIdx.x; r < k; r += blockDim.x) {
+    scores[(size_t)b * k + r] = -INFINITY;
+    ids[(size_t)b * k + r] = -1;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const float* keys, int dim,
+                          const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
+                          int32_t* ids, int* overflow, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  const size_t smem = sizeof(SelectSmem);
+  cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  select_kernel<<<B, kThreads, smem, s>>>(partial, lists, B, k, keys, dim, queries, maxnorm_bits, gamma, scores, ids,
+                                          overflow);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_ranks(const double* g_scores, const int32_t* g_ids, const uint8_t* g_tok, int G, int B, int k,
+                               double* scores, int32_t* ids, uint8_t* tok, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  merge_ranks_kernel<<<B, 256, 0, s>>>(g_scores, g_ids, g_tok, G, B, k, scores, ids, tok);
+  return cudaGetLastError();
+}
+
+}  // namespace hsd

@@ -1,0 +1,317 @@
+// k_verify.cu — K4: fused draft gather + verify-skip + sequence-wise relaxed
+// acceptance + accepted length, one warp per episode.
+//
+// Spec-only in the reference; semantics frozen in the oracle
+// (oracle/hsd_oracle.c: hsdo_verify_round) and DESIGN.md:
+//   - retrieve_drafts: gather the k candidates' pre-quantized
+//     payload tokens (L = 7: next_actions[0]; L = 21: all three slices);
+//   - greedy verifier token per position = argmax over 256 bins, lowest bin
+//     on ties (Eq. 2-1);
+//   - should_skip: d <= O_dist, history >= d and
+//     cos(f_now, f_prev) >= min_S (double-double dot, exactly rounded);
+//   - sequence groups pos/rot/grip; accept_sequence
+//     (SPEC.md:430-439): gripper zero tolerance, else sum <= 30 and max <= 15;
+//   - chains (a, b): pos0 from rank a, every later group from rank b (gripper
+//     isolation), DFS = lexicographic order over distinct
+//     token sequences, capped; longest accepted prefix wins,
+//     earliest chain on ties; empty prefix -> fallback greedy token
+//     (SPEC.md:440-448).
+// All parameter sets of a sweep are evaluated from the same registers; the
+// logits, tokens and features are read once.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hsd {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxL = 21;
+constexpr int kTokStride = 24;  // bytes per candidate row in shared memory
+
+__device__ __forceinline__ int group_count(int L) { return (L / 7) * 3; }
+__device__ __forceinline__ void group_at(int g, int& st, int& ln, bool& grip) {
+  const int s = g / 3, kind = g % 3;
+  st = s * 7 + (kind == 0 ? 0 : (kind == 1 ? 3 : 6));
+  ln = kind == 2 ? 1 : 3;
+  grip = kind == 2;
+}
+
+__device__ __forceinline__ bool accept_group(const uint8_t* draft, const int* greedy, int st, int ln, bool grip,
+                                             const hsd_verify_params& p) {
+  int sum = 0, mx = 0;
+  for (int i = 0; i < ln; ++i) {
+    const int b = abs((int)draft[st + i] - greedy[st + i]);
+    sum += b;
+    mx = b > mx ? b : mx;
+  }
+  if (grip || !p.relaxed) return mx == 0;
+  return sum <= p.bias_seq_max && mx <= p.bias_token_max;
+}
+
+__global__ void __launch_bounds__(kThreads) verify_kernel(const int32_t* __restrict__ ids, int E, int k, int L,
+                                                          const uint8_t* __restrict__ tokens,
+                                                          const uint8_t* __restrict__ cand_tokens,
+                                                          const float* __restrict__ logits,
+                                                          const float* __restrict__ feat_now,
+                                                          const float* __restrict__ feat_prev, int d_f,
+                                                          const int32_t* __restrict__ history, int gap_d,
+                                                          const hsd_verify_params* __restrict__ params, int P,
+                                                          int need_cos, hsd_outcome* __restrict__ out,
+                                                          uint8_t* __restrict__ tok_out) {
+  __shared__ uint8_t s_tok[kWarps][HSD_K_MAX][kTokStride];
+  __shared__ int s_greedy[kWarps][32];
+  __shared__ int s_acc0[kWarps][HSD_K_MAX], s_rest[kWarps][HSD_K_MAX];
+  __shared__ int s_canA[kWarps][HSD_K_MAX], s_canB[kWarps][HSD_K_MAX];
+  __shared__ int s_rankA[kWarps][HSD_K_MAX], s_rankB[kWarps][HSD_K_MAX];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * kWarps + warp;
+  if (e >= E) return;
+
+  // ---- greedy tokens: argmax per position, lowest index on ties
+  const float4* lg = reinterpret_cast<const float4*>(logits + (size_t)e * L * 256);
+  for (int p = 0; p < L; ++p) {
+    const float4 a = __ldg(lg + p * 64 + lane * 2);
+    const float4 c = __ldg(lg + p * 64 + lane * 2 + 1);
+    const float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+    float best = v[0];
+    int bi = lane * 8;
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+      if (v[i] > best) {
+        best = v[i];
+        bi = lane * 8 + i;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) s_greedy[warp][p] = bi;
+  }
+
+  // ---- verify-skip similarity: exactly rounded dot (double-double)
+  double cosv = -2.0;
+  if (need_cos && feat_now && feat_prev) {
+    const float4* a4 = reinterpret_cast<const float4*>(feat_now + (size_t)e * d_f);
+    const float4* b4 = reinterpret_cast<const float4*>(feat_prev + (size_t)e * d_f);
+    double hi = 0.0, lo = 0.0;
+    for (int t = lane; t < d_f / 4; t += 32) {
+      const float4 x = __ldg(a4 + t), y = __ldg(b4 + t);
+      const double pr[4] = {(double)x.x * (double)y.x, (double)x.y * (double)y.y, (double)x.z * (double)y.z,
+                            (double)x.w * (double)y.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double s, er;
+        dev::two_sum(hi, pr[i], s, er);
+        hi = s;
+        lo = __dadd_rn(lo, er);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+      const double olo = __shfl_xor_sync(0xffffffffu, lo, o);
+      double s, er;
+      dev::two_sum(hi, ohi, s, er);
+      hi = s;
+      lo = __dadd_rn(__dadd_rn(lo, olo), er);
+    }
+    double s, er;
+    dev::two_sum(hi, lo, s, er);
+    cosv = s;
+  }
+
+  // ---- gather the candidates' draft tokens
+  const int32_t* my_ids = ids + (size_t)e * k;
+  int n_cand = 0;
+  {
+    const int id = lane < k ? my_ids[lane] : -1;
+    const unsigned m = __ballot_sync(0xffffffffu, id >= 0);
+    n_cand = __popc(m);  // ids are rank-ordered with -1 padding at the end
+    if (id >= 0) {
+      const uint8_t* row = cand_tokens ? cand_tokens + ((size_t)e * k + lane) * HSD_TOKENS_STRIDE
+                                       : tokens + (size_t)id * HSD_TOKENS_STRIDE;
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(row);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(s_tok[warp][lane]);
+#pragma unroll
+      for (int i = 0; i < kTokStride / 4; ++i) dst[i] = __ldg(src + i);
+    }
+  }
+  __syncwarp();
+  int greedy[kMaxL];
+#pragma unroll
+  for (int p = 0; p < kMaxL; ++p) greedy[p] = p < L ? s_greedy[warp][p] : 0;
+  const int hist = history ? history[e] : 0x7fffffff;
+
+  // ---- candidate dedup (chain language) — independent of params
+  if (lane < n_cand) {
+    const uint8_t* me = s_tok[warp][lane];
+    int ca = lane, cb = lane;
+    for (int c = 0; c < lane; ++c) {
+      const uint8_t* o = s_tok[warp][c];
+      if (ca == lane && o[0] == me[0] && o[1] == me[1] && o[2] == me[2]) ca = c;
+      if (cb == lane) {
+        bool same = true;
+        for (int t = 3; t < L; ++t) same &= (o[t] == me[t]);
+        if (same) cb = c;
+      }
+    }
+    s_canA[warp][lane] = ca;
+    s_canB[warp][lane] = cb;
+  }
+  __syncwarp();
+  int nA = 0, nB = 0;
+  {
+    const bool isA = lane < n_cand && s_canA[warp][lane] == lane;
+    const bool isB = lane < n_cand && s_canB[warp][lane] == lane;
+    const unsigned mA = __ballot_sync(0xffffffffu, isA), mB = __ballot_sync(0xffffffffu, isB);
+    nA = __popc(mA);
+    nB = __popc(mB);
+    if (lane < n_cand) {
+      s_rankA[warp][lane] = isA ? __popc(mA & ((1u << lane) - 1)) : -1;
+      s_rankB[warp][lane] = isB ? __popc(mB & ((1u << lane) - 1)) : -1;
+    }
+  }
+  __syncwarp();
+
+  const int G = group_count(L);
+  for (int pi = 0; pi < P; ++pi) {
+    const hsd_verify_params p = params[pi];
+    hsd_outcome o;
+    o.accept_len = 0;
+    o.win_a = -1;
+    o.win_b = -1;
+    o.calls = 0;
+    o.fallback = 0;
+    o.skipped = 0;
+    o.n_emit = 0;
+    o.greedy0 = (int16_t)greedy[0];
+    o.cos_sim = (float)cosv;
+    uint8_t* my_tok = tok_out + ((size_t)pi * E + e) * L;
+    const bool skip = p.skip_enabled && n_cand > 0 && gap_d >= 1 && hist >= gap_d && gap_d <= p.O_dist &&
+                      cosv >= p.min_S;
+    if (skip) {  // the retrieved draft is emitted as fully accepted
+      o.accept_len = L;
+      o.win_a = 0;
+      o.win_b = 0;
+      o.skipped = 1;
+      o.n_emit = (int16_t)L;
+      for (int t = lane; t < L; t += 32) my_tok[t] = s_tok[warp][0][t];
+    } else if (n_cand == 0) {  // empty shard: autoregressive step
+      o.fallback = 1;
+      o.calls = 1;
+      o.n_emit = 1;
+      if (lane == 0) my_tok[0] = (uint8_t)greedy[0];
+      for (int t = 1 + lane; t < L; t += 32) my_tok[t] = 0;
+    } else {
+      // per-candidate group acceptance
+      if (lane < n_cand) {
+        const uint8_t* me = s_tok[warp][lane];
+        int st, ln;
+        bool gr;
+        group_at(0, st, ln, gr);
+        s_acc0[warp][lane] = accept_group(me, greedy, st, ln, gr, p) ? 1 : 0;
+        int rest = 0;
+        for (int g = 1; g < G; ++g) {
+          group_at(g, st, ln, gr);
+          if (!accept_group(me, greedy, st, ln, gr, p)) break;
+          rest += ln;
+        }
+        s_rest[warp][lane] = rest;
+      }
+      __syncwarp();
+      const int cap = p.chain_cap > 0 ? p.chain_cap : 64;
+      // lane a (canonical pos0) finds its best enumerated b
+      int len = -1, bestB = -1, rA = 1 << 20;
+      if (lane < n_cand && s_rankA[warp][lane] >= 0) {
+        rA = s_rankA[warp][lane];
+        const int limit = cap - rA * nB;  // b's with rankB < limit are enumerated
+        if (limit > 0) {
+          int br = -1, bb = -1;
+          for (int b = 0; b < n_cand; ++b) {
+            const int rb = s_rankB[warp][b];
+            if (rb < 0 || rb >= limit) continue;
+            const int r = s_rest[warp][b];
+            if (r > br) {
+              br = r;
+              bb = b;
+            }
+          }
+          bestB = bb;
+          len = s_acc0[warp][lane] ? 3 + br : 0;
+        }
+      }
+      // warp arg-max: longest, then earliest chain (smallest rank of a)
+      int wl = len, wa = lane, wr = rA, wb = bestB;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const int ol = __shfl_xor_sync(0xffffffffu, wl, off);
+        const int oa = __shfl_xor_sync(0xffffffffu, wa, off);
+        const int orr = __shfl_xor_sync(0xffffffffu, wr, off);
+        const int ob = __shfl_xor_sync(0xffffffffu, wb, off);
+        if (ol > wl || (ol == wl && orr < wr)) {
+          wl = ol;
+          wa = oa;
+          wr = orr;
+          wb = ob;
+        }
+      }
+      const long long chains = (long long)nA * nB;
+      o.calls = (int16_t)(chains < cap ? chains : cap);
+      if (wl <= 0) {  // every chain rejected at pos0 -> first chain, fallback token
+        o.win_a = 0;
+        o.win_b = 0;
+        o.fallback = 1;
+        o.n_emit = 1;
+        if (lane == 0) my_tok[0] = (uint8_t)greedy[0];
+        for (int t = 1 + lane; t < L; t += 32) my_tok[t] = 0;
+      } else {
+        o.win_a = (int16_t)wa;
+        o.win_b = (int16_t)wb;
+        o.accept_len = wl;
+        o.n_emit = (int16_t)wl;
+        for (int t = lane; t < L; t += 32)
+          my_tok[t] = t < wl ? (t < 3 ? s_tok[warp][wa][t] : s_tok[warp][wb][t]) : (uint8_t)0;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) out[(size_t)pi * E + e] = o;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_verify(const int32_t* ids, int E, int k, int L, const uint8_t* tokens, const uint8_t* cand_tokens,
+                          const float* logits, const float* feat_now, const float* feat_prev, int d_f,
+                          const int32_t* history, int gap_d, const hsd_verify_params* params_dev, int P, int need_cos,
+                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s) {
+  if (E <= 0) return cudaSuccess;
+  verify_kernel<<<(E + kWarps - 1) / kWarps, kThreads, 0, s>>>(ids, E, k, L, tokens, cand_tokens, logits, feat_now,
+                                                                feat_prev, d_f, history, gap_d, params_dev, P, need_cos,
+                                                                out, tok_out);
+  return cudaGetLastError();
+}
+
+// Pre-gather the payload tokens of a [n] id list (sharded search records).
+__global__ void gather_tokens_kernel(const uint8_t* __restrict__ tokens, const int32_t* __restrict__ ids, int n,
+                                     uint8_t* __restrict__ out) {
+  const int i = blockIdx.x * (blockDim.x / 8) + threadIdx.x / 8;
+  const int w = threadIdx.x & 7;
+  if (i >= n) return;
+  const int id = ids[i];
+  const uint32_t v = id >= 0 ? reinterpret_cast<const uint32_t*>(tokens + (size_t)id * HSD_TOKENS_STRIDE)[w] : 0u;
+  reinterpret_cast<uint32_t*>(out + (size_t)i * HSD_TOKENS_STRIDE)[w] = v;
+}
+
+cudaError_t launch_gather_tokens(const uint8_t* tokens, const int32_t* ids, int n, uint8_t* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  gather_tokens_kernel<<<(n + 31) / 32, 256, 0, s>>>(tokens, ids, n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace hsd

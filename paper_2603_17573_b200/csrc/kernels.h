@@ -1,0 +1,60 @@
+// kernels.h — host-side launchers of the sm_100a kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hsd/hsd_gpu.h"
+
+namespace hsd {
+
+// ---- K0 synthetic generators (k_synth.cu) ------------------------------------
+cudaError_t launch_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, float* keys,
+                            uint8_t* tokens, unsigned long long* maxnorm_bits, cudaStream_t s);
+cudaError_t launch_row_norms(const float* keys, int64_t row0, int64_t n, int dim,
+                             unsigned long long* maxnorm_bits, cudaStream_t s);
+cudaError_t launch_gen_queries(int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B, int dim,
+                               float* out, cudaStream_t s);
+cudaError_t launch_gen_logits(const uint8_t* tokens, uint64_t seed, const int64_t* rows, int E, int L, float* out,
+                              cudaStream_t s);
+cudaError_t launch_gen_features(uint64_t seed, int E, int d_f, float* now, float* prev, cudaStream_t s);
+cudaError_t launch_quantize(const double* actions, int64_t n, const double* lohi_dev /*[14] lo7 then hi7*/,
+                            int k_bins, int32_t* bins, int32_t* status, cudaStream_t s);
+cudaError_t launch_quantize_tokens(const double* actions /*[n][21]*/, int64_t n, uint8_t* tokens /*[n][32]*/,
+                                   int32_t* bad, cudaStream_t s);
+
+// ---- K1 similarity + per-CTA candidate lists ---------------------------------
+// partial: [grid][B][kCandLocal] u64 candidate keys; returns grid in *lists.
+struct SimPlan {
+  int lists;      // number of candidate lists per query (= grid of the sim kernel)
+  double gamma;   // relative error bound of the approximate score path
+};
+SimPlan sim_plan(int B, int64_t rows, int dim, int num_sms);
+cudaError_t launch_sim(const float* keys, int64_t row_begin, int64_t row_end, int dim, const float* queries, int B,
+                       const SimPlan& plan, uint64_t* partial, cudaStream_t s);
+
+// ---- K2 select: margin candidates + exact fp64 rescoring + final top-k -------
+cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const float* keys, int dim,
+                          const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
+                          int32_t* ids, int* overflow, cudaStream_t s);
+
+// K3 merge of G gathered per-rank top-k records (sharded search); tokens
+// [G][B][k][32] are permuted alongside when non-null.
+cudaError_t launch_merge_ranks(const double* g_scores, const int32_t* g_ids, const uint8_t* g_tok, int G, int B, int k,
+                               double* scores, int32_t* ids, uint8_t* tok, cudaStream_t s);
+
+// ---- K4 gather + verify-skip + relaxed acceptance ----------------------------
+// Draft tokens come from the collection's table by id, or pre-gathered
+// cand_tokens [E][k][32] when non-null (sharded search records).
+cudaError_t launch_verify(const int32_t* ids, int E, int k, int L, const uint8_t* tokens, const uint8_t* cand_tokens,
+                          const float* logits, const float* feat_now, const float* feat_prev, int d_f,
+                          const int32_t* history, int gap_d, const hsd_verify_params* params_dev, int P, int need_cos,
+                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s);
+cudaError_t launch_gather_tokens(const uint8_t* tokens, const int32_t* ids, int n, uint8_t* out, cudaStream_t s);
+
+// ---- K5 kinematics -------------------------------------------------------------
+cudaError_t launch_kinematics(const double* xyz, int W, const hsd_metric_params& mp, const hsd_norm_bounds& nb,
+                              const int32_t* history, double* R, double* D, double* F, int32_t* decision,
+                              cudaStream_t s);
+
+}  // namespace hsd
