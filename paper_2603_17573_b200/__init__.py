@@ -172,6 +172,8 @@ def lib():
         "hsd_verify_round_drafts": [C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp,
                                     C.c_int, _vp, C.c_int, _vp, _vp, _vp],
         "hsd_collection_generate_rows": [_vp, C.c_int, C.c_uint64, C.c_int64, C.c_int64],
+        "hsd_debug_sim_scores": [_vp, _vp, C.c_int, _vp, _vp],
+        "hsd_set_sim_path": [C.c_int],
         "hsd_gen_queries": [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, _vp,
                             _vp],
         "hsd_gen_logits": [_vp, C.c_uint64, _vp, C.c_int, C.c_int, _vp, _vp],
@@ -317,6 +319,14 @@ class Collection:
                                               _ptr(scores), _ptr(ids), _stream(stream)))
         return scores, ids
 
+    def debug_sim_scores(self, queries, stream=None):
+        """Approximate tcgen05 filter scores float32 [B, size] (diagnostics)."""
+        torch = _torch()
+        q = queries.contiguous()
+        out = torch.empty((q.shape[0], self.size()), dtype=torch.float32, device=q.device)
+        check(lib().hsd_debug_sim_scores(self._h, _ptr(q), q.shape[0], _ptr(out), _stream(stream)))
+        return out
+
     def overflow_count(self, stream=None) -> int:
         c = C.c_int()
         check(lib().hsd_search_overflow_count(self._h, _stream(stream), C.byref(c)))
@@ -409,7 +419,7 @@ def _from_ptr(ptr, shape, dtype, device):
 
     class _Arr:
         __cuda_array_interface__ = {"shape": (n,), "typestr": torch.empty((), dtype=dtype).numpy().dtype.str,
-                                    "data": (ptr, True), "version": 3, "strides": (esz,)}
+                                    "data": (ptr, False), "version": 3, "strides": (esz,)}
 
     return torch.as_tensor(_Arr(), device=f"cuda:{device}").view(shape)
 
@@ -452,6 +462,14 @@ def quantize(actions, lo=-1.0, hi=1.0, k_bins=256, stream=None):
     if n and bool((status != 0).any()):
         raise InvalidInputError("non-finite action value")  # actions.cpp:38-40
     return bins
+
+
+SIM_PATHS = {"auto": 0, "rows": 1, "tile": 2, "tc": 3}
+
+
+def set_sim_path(name: str) -> None:
+    """Similarity kernel override (ablations / tests): auto | rows | tile | tc."""
+    check(lib().hsd_set_sim_path(SIM_PATHS[name]))
 
 
 def classify_segment(F: float, threshold: float) -> str:

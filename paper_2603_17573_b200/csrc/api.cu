@@ -100,6 +100,8 @@ __global__ void offset_ids_kernel(int32_t* ids, int n, int64_t off) {
 struct Scratch {
   uint64_t* partial = nullptr;
   size_t partial_cap = 0;  // bytes
+  float* qsplit = nullptr;  // Qh | Ql of the tcgen05 path
+  size_t qsplit_cap = 0;
   int* overflow = nullptr;
 };
 
@@ -142,7 +144,7 @@ hsd_status ensure_capacity(hsd_collection* c, int64_t need) {
   return HSD_OK;
 }
 
-hsd_status get_scratch(hsd_collection* c, cudaStream_t s, size_t partial_bytes, Scratch** out) {
+hsd_status get_scratch(hsd_collection* c, cudaStream_t s, size_t partial_bytes, size_t qsplit_bytes, Scratch** out) {
   std::lock_guard<std::mutex> lk(c->mu);
   Scratch& sc = c->scratch[s];
   if (!sc.overflow) CU(cudaMalloc(&sc.overflow, sizeof(int)));
@@ -153,11 +155,40 @@ hsd_status get_scratch(hsd_collection* c, cudaStream_t s, size_t partial_bytes, 
     CU(cudaMalloc(&sc.partial, partial_bytes));
     sc.partial_cap = partial_bytes;
   }
+  if (sc.qsplit_cap < qsplit_bytes) {
+    cudaFree(sc.qsplit);
+    sc.qsplit = nullptr;
+    sc.qsplit_cap = 0;
+    CU(cudaMalloc(&sc.qsplit, qsplit_bytes));
+    sc.qsplit_cap = qsplit_bytes;
+  }
   *out = &sc;
   return HSD_OK;
 }
 
 constexpr int kSlab = 64;  // queries per similarity launch
+
+// Similarity path per query slab: SIMT GEMV for tiny batches (HBM-bound on
+// CUDA cores), tcgen05 3xTF32 otherwise.  HSD_SIM_PATH=rows|tile|tc overrides
+// (tests and ablations).
+enum { kPathAuto = 0, kPathRows = 1, kPathTile = 2, kPathTc = 3 };
+int g_path = -1;
+int path_override() {
+  int& v = g_path;
+  if (v < 0) {
+    const char* e = getenv("HSD_SIM_PATH");
+    v = !e ? kPathAuto
+           : (!strcmp(e, "rows") ? kPathRows : (!strcmp(e, "tile") ? kPathTile : (!strcmp(e, "tc") ? kPathTc : 0)));
+  }
+  return v;
+}
+int choose_path(int Bs) {
+  const int o = path_override();
+  if (o == kPathRows) return Bs <= 8 ? kPathRows : kPathTile;
+  if (o == kPathTile) return Bs <= 8 ? kPathRows : kPathTile;  // launch_sim picks rows for B <= 8
+  if (o == kPathTc) return kPathTc;
+  return Bs <= 4 ? kPathRows : kPathTc;
+}
 
 // Optional stage events (engine timing): marks[i] is recorded after stage i.
 struct StageMarks {
@@ -185,16 +216,25 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   }
   const int nsm = num_sms(c->device);
   const int Bs0 = std::min(B, kSlab);
-  const hsd::SimPlan plan0 = hsd::sim_plan(Bs0, rows, c->dim, nsm);
+  const int path0 = choose_path(Bs0);
+  const int lists0 = path0 == kPathTc ? hsd::sim_tc_lists(rows, nsm) : hsd::sim_plan(Bs0, rows, c->dim, nsm).lists;
   Scratch* sc = nullptr;
-  st = get_scratch(c, s, (size_t)plan0.lists * Bs0 * hsd::dev::kCandLocal * sizeof(uint64_t), &sc);
+  st = get_scratch(c, s, (size_t)std::max(lists0, 4 * nsm) * Bs0 * hsd::dev::kCandLocal * sizeof(uint64_t),
+                   path0 == kPathTc ? hsd::sim_tc_scratch_bytes(c->dim) : 0, &sc);
   if (st != HSD_OK) return st;
   CU(cudaMemsetAsync(sc->overflow, 0, sizeof(int), s));
   for (int b0 = 0; b0 < B; b0 += kSlab) {
     const int Bs = std::min(kSlab, B - b0);
-    const hsd::SimPlan plan = hsd::sim_plan(Bs, rows, c->dim, nsm);
+    const int path = choose_path(Bs);
+    hsd::SimPlan plan = hsd::sim_plan(Bs, rows, c->dim, nsm);
     const float* q = queries + (size_t)b0 * c->dim;
-    CU(hsd::launch_sim(c->keys, rb, re, c->dim, q, Bs, plan, sc->partial, s));
+    if (path == kPathTc) {
+      plan.lists = hsd::sim_tc_lists(rows, nsm);
+      plan.gamma = hsd::sim_tc_gamma(c->dim);
+      CU(hsd::launch_sim_tc(c->keys, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial, nullptr, s));
+    } else {
+      CU(hsd::launch_sim(c->keys, rb, re, c->dim, q, Bs, plan, sc->partial, s));
+    }
     if (marks && marks->after_sim && b0 + kSlab >= B) CU(cudaEventRecord(marks->after_sim, s));
     CU(hsd::launch_select(sc->partial, plan.lists, Bs, k, c->keys, c->dim, q, c->maxnorm, plan.gamma,
                           scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->overflow, s));
@@ -256,6 +296,7 @@ hsd_status hsd_collection_destroy(hsd_collection* c) {
   cudaSetDevice(c->device);
   for (auto& kv : c->scratch) {
     cudaFree(kv.second.partial);
+    cudaFree(kv.second.qsplit);
     cudaFree(kv.second.overflow);
   }
   cudaFree(c->keys);
@@ -357,6 +398,28 @@ hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B,
   if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
   if (row_begin > row_end) return fail(HSD_ERR_INVALID_INPUT, "row_begin > row_end");
   return search_impl(c, queries, B, k, row_begin, row_end, scores, ids, (cudaStream_t)stream);
+}
+
+hsd_status hsd_set_sim_path(int path) {
+  if (path < 0 || path > 3) return fail(HSD_ERR_INVALID_INPUT, "path must be 0 auto, 1 rows, 2 tile, 3 tc");
+  g_path = path;
+  return HSD_OK;
+}
+
+hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, float* out, void* stream) {
+  if (!c || !queries || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (B < 1 || B > kSlab) return fail(HSD_ERR_INVALID_INPUT, "debug dump supports 1 <= B <= %d", kSlab);
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  if (c->n == 0) return HSD_OK;
+  const int lists = hsd::sim_tc_lists(c->n, num_sms(c->device));
+  Scratch* sc = nullptr;
+  st = get_scratch(c, (cudaStream_t)stream, (size_t)lists * B * hsd::dev::kCandLocal * 8, hsd::sim_tc_scratch_bytes(c->dim),
+                   &sc);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_sim_tc(c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial, out,
+                        (cudaStream_t)stream));
+  return HSD_OK;
 }
 
 hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count) {

@@ -1,0 +1,495 @@
+// k_sim_tc.cu — K1' (tensor cores): 3xTF32 similarity on tcgen05 + TMA,
+// fused with the per-CTA top-32 candidate filter.
+//
+// S = K·Q^T for 128-key blocks against a 64-query slab, split-precision so the
+// filter scores carry ~fp32 accuracy (error bound in sim_plan_tc):
+//     K = Kh + Kl,  Q = Qh + Ql      (h = TF32-truncated, l = exact remainder)
+//     S ~= Kh·Qh + (Kh·Ql + Kl·Qh)
+//   MMA1 (SS): A = raw key tile (smem, TMA SWIZZLE_128B, read as TF32 = Kh),
+//              B = [Qh | Ql] (N = 128)  -> TMEM cols [0,64) Kh·Qh, [64,128) Kh·Ql
+//   MMA2 (TS): A = Kl (TMEM, written by the split warps with tcgen05.st),
+//              B = Qh (N = 64)          -> accumulates into cols [64,128)
+// Both products share one pass of the key tile through shared memory; Kl never
+// touches shared memory.  Three accumulators (3 x 128 key rows) live in TMEM
+// so each query chunk staged in smem is reused for 3 key tiles.
+//
+// Warp roles (384 threads, 1 CTA per SM, persistent over a contiguous range of
+// key blocks):
+//   warp 0      TMA producer (keys ring, query ring)
+//   warp 1      tcgen05.mma issuer (single elected lane)
+//   warp 2      TMEM allocator
+//   warps 4-7   split: Kl = K - trunc_tf32(K) -> TMEM (tcgen05.st)
+//   warps 8-11  epilogue: tcgen05.ld scores -> per-query candidate filter
+// Every synchronisation is an mbarrier (TMA complete_tx, tcgen05.commit,
+// thread arrivals); the epilogue warpgroup uses a named barrier.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace hsd {
+namespace {
+
+using dev::cand_key;
+using dev::kCandLocal;
+using dev::kEmpty;
+
+constexpr int kBM = 128;       // keys per block (UMMA M)
+constexpr int kBQ = 64;        // queries per slab
+constexpr int kBK = 32;        // fp32 per k-chunk (one 128-B swizzle atom)
+constexpr int kGB = 3;         // key blocks per group (accumulators in TMEM)
+constexpr int kKStages = 5;    // key ring (16 KB per stage)
+constexpr int kQStages = 3;    // query ring (16 KB per stage: Qh rows 0-63, Ql rows 64-127)
+constexpr int kLStages = 4;    // Kl stages in TMEM (32 columns each)
+constexpr int kAccCols = 128;  // per key block
+constexpr int kKlCol0 = kGB * kAccCols;  // 384
+constexpr int kTmemCols = 512;
+constexpr int kThreads = 384;
+constexpr int kTileBytes = kBM * kBK * 4;  // 16 KB
+constexpr int kCBuf = kCandLocal + kBM;     // 160 slots per query
+
+struct __align__(1024) TcSmem {
+  float kbuf[kKStages][kBM * kBK];
+  float qbuf[kQStages][128 * kBK];
+  uint64_t cbuf[kBQ][kCBuf];
+  uint64_t thr[kBQ];
+  int cnt[kBQ];
+  uint64_t k_full[kKStages], k_empty[kKStages];
+  uint64_t q_full[kQStages], q_empty[kQStages];
+  uint64_t l_full[kLStages], l_empty[kLStages];
+  uint64_t acc_full, acc_empty;
+  uint32_t tmem_base;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "@p bra.uni DONE;\n\t"
+      "bra.uni LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
+               : "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+#define TMEM_LD32(addr, r)                                                                                        \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"   \
+               "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                         \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),  \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),       \
+                 "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),     \
+                 "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),     \
+                 "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                           \
+               : "r"(addr))
+
+#define TMEM_ST32(addr, r)                                                                                        \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"     \
+               "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),           \
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), \
+               "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),    \
+               "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),   \
+               "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])               \
+               : "memory")
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// K-major, SWIZZLE_128B shared-memory matrix descriptor (8-row atoms of
+// 1024 B; SBO = 1024 B; LBO unused for a single atom along K; version 1).
+__device__ __forceinline__ uint64_t sw128_desc(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  return ((addr >> 4) & 0x3FFFull) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, K-major, M x N.
+__host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------------ kernel
+template <bool kDump>
+__global__ void __launch_bounds__(kThreads, 1)
+    sim_tc_kernel(const __grid_constant__ CUtensorMap keys_map, const __grid_constant__ CUtensorMap qh_map,
+                  const __grid_constant__ CUtensorMap ql_map, int64_t row_begin, int64_t row_end, int dim, int B,
+                  int64_t blocks_per_cta, uint64_t* __restrict__ partial, float* __restrict__ dump) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
+  const int64_t blk0 = (int64_t)blockIdx.x * blocks_per_cta;
+  const int64_t blk1 = std::min<int64_t>(blk0 + blocks_per_cta, n_blocks);
+  const int nk = (dim + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kKStages; ++i) {
+      mbar_init(&S.k_full[i], 1);
+      mbar_init(&S.k_empty[i], 1 + 4);  // MMA commit + 4 split warps
+    }
+    for (int i = 0; i < kQStages; ++i) {
+      mbar_init(&S.q_full[i], 1);
+      mbar_init(&S.q_empty[i], 1);
+    }
+    for (int i = 0; i < kLStages; ++i) {
+      mbar_init(&S.l_full[i], 4);
+      mbar_init(&S.l_empty[i], 1);
+    }
+    mbar_init(&S.acc_full, 1);
+    mbar_init(&S.acc_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < kBQ; i += kThreads) {
+    S.thr[i] = kEmpty;
+    S.cnt[i] = 0;
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    // ======================= TMA producer
+    if (lane == 0 && blk0 < blk1) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&keys_map) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&qh_map) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&ql_map) : "memory");
+      const uint64_t pol_k = policy_evict_first(), pol_q = policy_evict_last();
+      int ks = 0, qs = 0;
+      uint32_t kph = 0, qph = 0;
+      for (int64_t g0 = blk0; g0 < blk1; g0 += kGB) {
+        const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
+        for (int kc = 0; kc < nk; ++kc) {
+          mbar_wait(&S.q_empty[qs], qph ^ 1);
+          mbar_expect_tx(&S.q_full[qs], kTileBytes);
+          tma_load_2d(&S.qbuf[qs][0], &qh_map, &S.q_full[qs], kc * kBK, 0, pol_q);
+          tma_load_2d(&S.qbuf[qs][64 * kBK], &ql_map, &S.q_full[qs], kc * kBK, 0, pol_q);
+          if (++qs == kQStages) {
+            qs = 0;
+            qph ^= 1;
+          }
+          for (int m = 0; m < gb; ++m) {
+            mbar_wait(&S.k_empty[ks], kph ^ 1);
+            mbar_expect_tx(&S.k_full[ks], kTileBytes);
+            tma_load_2d(&S.kbuf[ks][0], &keys_map, &S.k_full[ks], kc * kBK, (int)(row_begin + (g0 + m) * kBM), pol_k);
+            if (++ks == kKStages) {
+              ks = 0;
+              kph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer
+    constexpr uint32_t idesc1 = tf32_idesc(128, 128);
+    constexpr uint32_t idesc2 = tf32_idesc(128, 64);
+    int ks = 0, qs = 0, ls = 0;
+    uint32_t kph = 0, qph = 0, lph = 0;
+    int gi = 0;
+    for (int64_t g0 = blk0; g0 < blk1; g0 += kGB, ++gi) {
+      const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
+      if (gi > 0) {
+        mbar_wait(&S.acc_empty, (gi - 1) & 1);
+        tc_fence_after();
+      }
+      for (int kc = 0; kc < nk; ++kc) {
+        mbar_wait(&S.q_full[qs], qph);
+        const uint64_t bdesc = sw128_desc(&S.qbuf[qs][0]);
+        for (int m = 0; m < gb; ++m) {
+          mbar_wait(&S.k_full[ks], kph);
+          mbar_wait(&S.l_full[ls], lph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint64_t adesc = sw128_desc(&S.kbuf[ks][0]);
+            const uint32_t d = tmem + m * kAccCols;
+            const uint32_t kl = tmem + kKlCol0 + ls * kBK;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 8; ++kk) {
+              // +32 B per K-step of 8 tf32 (descriptor address field is in 16-B units)
+              mma_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc1, (kc > 0 || kk > 0) ? 1u : 0u);
+              mma_ts(d + 64, kl + 8 * kk, bdesc + 2 * kk, idesc2, 1u);
+            }
+            tc_commit(&S.k_empty[ks]);
+            tc_commit(&S.l_empty[ls]);
+          }
+          __syncwarp();
+          if (++ks == kKStages) {
+            ks = 0;
+            kph ^= 1;
+          }
+          if (++ls == kLStages) {
+            ls = 0;
+            lph ^= 1;
+          }
+        }
+        if (lane == 0) tc_commit(&S.q_empty[qs]);
+        __syncwarp();
+        if (++qs == kQStages) {
+          qs = 0;
+          qph ^= 1;
+        }
+      }
+      if (lane == 0) tc_commit(&S.acc_full);
+      __syncwarp();
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ======================= split: Kl = K - trunc_tf32(K) -> TMEM
+    const int r = (warp - 4) * 32 + lane;  // key row within the tile == TMEM lane
+    const uint32_t lane_addr = (uint32_t)((warp - 4) * 32) << 16;
+    int ks = 0, ls = 0;
+    uint32_t kph = 0, lph = 0;
+    for (int64_t g0 = blk0; g0 < blk1; g0 += kGB) {
+      const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
+      for (int kc = 0; kc < nk; ++kc) {
+        for (int m = 0; m < gb; ++m) {
+          mbar_wait(&S.k_full[ks], kph);
+          mbar_wait(&S.l_empty[ls], lph ^ 1);
+          tc_fence_after();
+          const unsigned char* row = reinterpret_cast<const unsigned char*>(&S.kbuf[ks][0]) + r * 128;
+          uint32_t lo[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 4));
+            const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float h = __uint_as_float(__float_as_uint(x[j]) & 0xFFFFE000u);
+              lo[c * 4 + j] = __float_as_uint(x[j] - h);
+            }
+          }
+          TMEM_ST32(tmem + lane_addr + kKlCol0 + ls * kBK, lo);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&S.l_full[ls]);
+            mbar_arrive(&S.k_empty[ks]);
+          }
+          if (++ks == kKStages) {
+            ks = 0;
+            kph ^= 1;
+          }
+          if (++ls == kLStages) {
+            ls = 0;
+            lph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ======================= epilogue: scores -> candidate filter
+    const int ew = warp - 8;
+    const int r = ew * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(ew * 32) << 16;
+    int gi = 0;
+    for (int64_t g0 = blk0; g0 < blk1; g0 += kGB, ++gi) {
+      const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
+      mbar_wait(&S.acc_full, gi & 1);
+      tc_fence_after();
+      for (int m = 0; m < gb; ++m) {
+        const int64_t row = row_begin + (g0 + m) * kBM + r;
+        const bool valid = row < row_end;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t hi[32], cr[32];
+          TMEM_LD32(tmem + lane_addr + m * kAccCols + half * 32, hi);
+          TMEM_LD32(tmem + lane_addr + m * kAccCols + 64 + half * 32, cr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int q = half * 32 + j;
+            const float s = __uint_as_float(hi[j]) + __uint_as_float(cr[j]);
+            if (kDump) {
+              if (valid && q < B) dump[(size_t)q * (row_end - row_begin) + (row - row_begin)] = s;
+            } else if (valid && q < B) {
+              const uint64_t key = cand_key(s, (uint32_t)row);
+              if (key < S.thr[q]) {
+                const int slot = atomicAdd(&S.cnt[q], 1);
+                S.cbuf[q][slot] = key;
+              }
+            }
+          }
+        }
+        if (!kDump) {
+          named_sync(1, 128);
+          for (int q = ew; q < B; q += 4) {
+            const int c = S.cnt[q];
+            if (c > kCandLocal) {
+              uint64_t v[8];
+#pragma unroll
+              for (int s = 0; s < 8; ++s) {
+                const int i = s * 32 + lane;
+                v[s] = i < c ? S.cbuf[q][i] : kEmpty;
+              }
+              dev::warp_sort<8>(v);
+              __syncwarp();
+              S.cbuf[q][lane] = v[0];
+              if (lane == 31) S.thr[q] = v[0];
+              if (lane == 0) S.cnt[q] = kCandLocal;
+            }
+          }
+          named_sync(1, 128);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.acc_empty);
+    }
+    if (!kDump) {
+      for (int q = ew; q < B; q += 4) {
+        const int c = S.cnt[q];
+        uint64_t v[1];
+        v[0] = lane < c ? S.cbuf[q][lane] : kEmpty;
+        dev::warp_sort<1>(v);
+        partial[((size_t)blockIdx.x * B + q) * kCandLocal + lane] = v[0];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// Q [B][dim] -> Qh = trunc_tf32(Q), Ql = Q - Qh, zero-padded to 64 rows.
+__global__ void split_queries_kernel(const float* __restrict__ q, int B, int dim, float* __restrict__ qh,
+                                     float* __restrict__ ql) {
+  const int row = blockIdx.x;
+  for (int c = threadIdx.x; c < dim; c += blockDim.x) {
+    const float x = row < B ? q[(size_t)row * dim + c] : 0.f;
+    const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    qh[(size_t)row * dim + c] = h;
+    ql[(size_t)row * dim + c] = x - h;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t dim, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t gdim[2] = {dim, rows};
+  const cuuint64_t gstride[1] = {dim * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstride, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+size_t sim_tc_scratch_bytes(int dim) { return 2ull * kBQ * dim * sizeof(float); }
+
+double sim_tc_gamma(int dim) {
+  // |S - S~| <= gamma * sum|k_i q_i|:  split/representation error 3 * 2^-20
+  // (|Kl|,|Ql| < 2^-10 |.|, TF32 rounding of the remainders, dropped Kl*Ql)
+  // plus fp32 accumulation of 3 * dim products at <= 2^-23 relative each.
+  return 3.0 / 1048576.0 + (3.0 * dim + 16.0) / 8388608.0;
+}
+
+int sim_tc_lists(int64_t rows, int num_sms) {
+  const int64_t blocks = (rows + kBM - 1) / kBM;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, num_sms));
+}
+
+cudaError_t launch_sim_tc(const float* keys, int64_t n_keys_total, int64_t row_begin, int64_t row_end, int dim,
+                          const float* queries, int B, int lists, float* scratch, uint64_t* partial, float* dump,
+                          cudaStream_t s) {
+  if (B < 1 || B > kBQ) return cudaErrorInvalidValue;
+  float* qh = scratch;
+  float* ql = scratch + (size_t)kBQ * dim;
+  split_queries_kernel<<<kBQ, 256, 0, s>>>(queries, B, dim, qh, ql);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  CUtensorMap km, qhm, qlm;
+  if (!make_map(&km, keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) || !make_map(&qhm, qh, kBQ, dim, kBQ) ||
+      !make_map(&qlm, ql, kBQ, dim, kBQ))
+    return cudaErrorInvalidValue;
+  const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
+  const int64_t per = (n_blocks + lists - 1) / lists;
+  const size_t smem = sizeof(TcSmem) + 1024;
+  if (dump) {
+    e = cudaFuncSetAttribute(sim_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    sim_tc_kernel<true><<<lists, kThreads, smem, s>>>(km, qhm, qlm, row_begin, row_end, dim, B, per, partial, dump);
+  } else {
+    e = cudaFuncSetAttribute(sim_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    sim_tc_kernel<false><<<lists, kThreads, smem, s>>>(km, qhm, qlm, row_begin, row_end, dim, B, per, partial, dump);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hsd

@@ -33,6 +33,16 @@ SimPlan sim_plan(int B, int64_t rows, int dim, int num_sms);
 cudaError_t launch_sim(const float* keys, int64_t row_begin, int64_t row_end, int dim, const float* queries, int B,
                        const SimPlan& plan, uint64_t* partial, cudaStream_t s);
 
+// K1' tcgen05 3xTF32 path (k_sim_tc.cu): B <= 64 queries per launch, one
+// persistent CTA per SM.  scratch: sim_tc_scratch_bytes(dim) (Qh/Ql split).
+// dump != nullptr -> debug mode writing every approximate score [B][rows].
+size_t sim_tc_scratch_bytes(int dim);
+double sim_tc_gamma(int dim);
+int sim_tc_lists(int64_t rows, int num_sms);
+cudaError_t launch_sim_tc(const float* keys, int64_t n_keys_total, int64_t row_begin, int64_t row_end, int dim,
+                          const float* queries, int B, int lists, float* scratch, uint64_t* partial, float* dump,
+                          cudaStream_t s);
+
 // ---- K2 select: margin candidates + exact fp64 rescoring + final top-k -------
 cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const float* keys, int dim,
                           const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
