@@ -26,9 +26,9 @@ using dev::kEmpty;
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kPool = 256;
-constexpr int kCandMax = 64;
-constexpr int kChunk = 128;          // columns staged per rescoring pass
+constexpr int kPool = 512;
+constexpr int kCandMax = 256;           // rescored candidates (one thread each)
+constexpr int kChunk = 32;              // columns staged per rescoring pass
 constexpr int kRowStride = kChunk + 1;  // bank-conflict-free sequential reads
 
 struct SelectSmem {
@@ -100,14 +100,14 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
     n = kPool;
     if (tid == 0) S.over = 1;
   }
-  if (n > kCandMax) {
+  if (n > kCandMax) {  // keep the best kCandMax by approximate score
     if (warp == 0) {
-      uint64_t v[8];
+      uint64_t v[16];
 #pragma unroll
-      for (int s = 0; s < 8; ++s) v[s] = s * 32 + lane < n ? S.pool[s * 32 + lane] : kEmpty;
-      dev::warp_sort<8>(v);
-      S.pool[lane] = v[0];
-      S.pool[32 + lane] = v[1];
+      for (int s = 0; s < 16; ++s) v[s] = s * 32 + lane < n ? S.pool[s * 32 + lane] : kEmpty;
+      dev::warp_sort<16>(v);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) S.pool[s * 32 + lane] = v[s];
     }
     n = kCandMax;
     if (tid == 0) S.over = 1;

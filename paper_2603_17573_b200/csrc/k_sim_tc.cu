@@ -43,14 +43,19 @@ constexpr int kBQ = 64;        // queries per slab
 constexpr int kBK = 32;        // fp32 per k-chunk (one 128-B swizzle atom)
 constexpr int kGB = 3;         // key blocks per group (accumulators in TMEM)
 constexpr int kKStages = 5;    // key ring (16 KB per stage)
-constexpr int kQStages = 3;    // query ring (16 KB per stage: Qh rows 0-63, Ql rows 64-127)
+constexpr int kQStages = 2;    // query ring (16 KB per stage: Qh rows 0-63, Ql rows 64-127)
 constexpr int kLStages = 4;    // Kl stages in TMEM (32 columns each)
 constexpr int kAccCols = 128;  // per key block
 constexpr int kKlCol0 = kGB * kAccCols;  // 384
 constexpr int kTmemCols = 512;
 constexpr int kThreads = 384;
 constexpr int kTileBytes = kBM * kBK * 4;  // 16 KB
-constexpr int kCBuf = kCandLocal + kBM;     // 160 slots per query
+// Lazy compaction: a query's buffer is sorted down to its best 32 only when it
+// holds more than kCTrig entries, so after the first few blocks (insert rate
+// ~32/n at the n-th block) a query compacts O(log n) times, not once per block.
+// The threshold stays conservative between compactions (it only tightens).
+constexpr int kCTrig = 64;
+constexpr int kCBuf = kCTrig + kBM;  // 192 slots per query
 
 struct __align__(1024) TcSmem {
   float kbuf[kKStages][kBM * kBK];
@@ -81,7 +86,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@p bra.uni DONE;\n\t"
       "bra.uni LAB_WAIT;\n\t"
       "DONE:\n\t}" ::"r"(smem_u32(b)),
@@ -168,7 +173,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const __grid_constant__ CUtensorMap ql_map, int64_t row_begin, int64_t row_end, int dim, int B,
                   int64_t blocks_per_cta, uint64_t* __restrict__ partial, float* __restrict__ dump) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // keep the pointer derived from the __shared__ array so accesses stay LDS/STS
+  TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
   const int64_t blk0 = (int64_t)blockIdx.x * blocks_per_cta;
@@ -373,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           named_sync(1, 128);
           for (int q = ew; q < B; q += 4) {
             const int c = S.cnt[q];
-            if (c > kCandLocal) {
+            if (c > kCTrig) {
               uint64_t v[8];
 #pragma unroll
               for (int s = 0; s < 8; ++s) {
@@ -397,9 +403,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!kDump) {
       for (int q = ew; q < B; q += 4) {
         const int c = S.cnt[q];
-        uint64_t v[1];
-        v[0] = lane < c ? S.cbuf[q][lane] : kEmpty;
-        dev::warp_sort<1>(v);
+        uint64_t v[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const int i = s * 32 + lane;
+          v[s] = i < c ? S.cbuf[q][i] : kEmpty;
+        }
+        dev::warp_sort<8>(v);
         partial[((size_t)blockIdx.x * B + q) * kCandLocal + lane] = v[0];
       }
     }
