@@ -42,7 +42,7 @@ constexpr int kBM = 128;       // keys per block (UMMA M)
 constexpr int kBQ = 64;        // queries per slab
 constexpr int kBK = 32;        // fp32 per k-chunk (one 128-B swizzle atom)
 constexpr int kGB = 3;         // key blocks per group (accumulators in TMEM)
-constexpr int kKStages = 5;    // key ring (16 KB per stage)
+constexpr int kKStages = 9;    // key ring (16 KB per stage): 144 KB of HBM reads in flight per SM
 constexpr int kQStages = 2;    // query ring (16 KB per stage: Qh rows 0-63, Ql rows 64-127)
 constexpr int kLStages = 4;    // Kl stages in TMEM (32 columns each)
 constexpr int kAccCols = 128;  // per key block
@@ -50,19 +50,18 @@ constexpr int kKlCol0 = kGB * kAccCols;  // 384
 constexpr int kTmemCols = 512;
 constexpr int kThreads = 384;
 constexpr int kTileBytes = kBM * kBK * 4;  // 16 KB
-// Lazy compaction: a query's buffer is sorted down to its best 32 only when it
-// holds more than kCTrig entries, so after the first few blocks (insert rate
-// ~32/n at the n-th block) a query compacts O(log n) times, not once per block.
-// The threshold stays conservative between compactions (it only tightens).
-constexpr int kCTrig = 64;
-constexpr int kCBuf = kCTrig + kBM;  // 192 slots per query
+constexpr int kStg = kBQ + 1;              // padded row of the score staging tile
 
+// Candidate filter: the 4 epilogue warps own queries q % 4 == w; each keeps the
+// running sorted top-32 of each of its queries in registers (one key per
+// lane).  Per 128-key block the scores are staged through shared memory
+// (row-major, padded: conflict-free), each warp tests its queries' 128 keys
+// against the lane-31 threshold with one ballot, and inserts the (rare, ~32/n
+// at the n-th block) survivors one by one with a shuffle shift.
 struct __align__(1024) TcSmem {
   float kbuf[kKStages][kBM * kBK];
   float qbuf[kQStages][128 * kBK];
-  uint64_t cbuf[kBQ][kCBuf];
-  uint64_t thr[kBQ];
-  int cnt[kBQ];
+  float stg[kBM * kStg];
   uint64_t k_full[kKStages], k_empty[kKStages];
   uint64_t q_full[kQStages], q_empty[kQStages];
   uint64_t l_full[kLStages], l_empty[kLStages];
@@ -197,10 +196,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&S.acc_full, 1);
     mbar_init(&S.acc_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = threadIdx.x; i < kBQ; i += kThreads) {
-    S.thr[i] = kEmpty;
-    S.cnt[i] = 0;
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
@@ -346,14 +341,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 8;
     const int r = ew * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(ew * 32) << 16;
+    constexpr int kMyQ = kBQ / 4;  // queries owned by this warp: q = ew + 4 i
+    uint64_t top[kMyQ];
+#pragma unroll
+    for (int i = 0; i < kMyQ; ++i) top[i] = kEmpty;
     int gi = 0;
     for (int64_t g0 = blk0; g0 < blk1; g0 += kGB, ++gi) {
       const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
       mbar_wait(&S.acc_full, gi & 1);
       tc_fence_after();
       for (int m = 0; m < gb; ++m) {
-        const int64_t row = row_begin + (g0 + m) * kBM + r;
-        const bool valid = row < row_end;
+        const int64_t base = row_begin + (g0 + m) * kBM;
+        // 1. TMEM -> registers -> staging tile (S~ = hi*hi + corrections)
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           uint32_t hi[32], cr[32];
@@ -362,55 +361,57 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const int q = half * 32 + j;
             const float s = __uint_as_float(hi[j]) + __uint_as_float(cr[j]);
             if (kDump) {
-              if (valid && q < B) dump[(size_t)q * (row_end - row_begin) + (row - row_begin)] = s;
-            } else if (valid && q < B) {
-              const uint64_t key = cand_key(s, (uint32_t)row);
-              if (key < S.thr[q]) {
-                const int slot = atomicAdd(&S.cnt[q], 1);
-                S.cbuf[q][slot] = key;
-              }
+              const int q = half * 32 + j;
+              if (base + r < row_end && q < B) dump[(size_t)q * (row_end - row_begin) + (base + r - row_begin)] = s;
+            } else {
+              S.stg[r * kStg + half * 32 + j] = s;
             }
           }
         }
-        if (!kDump) {
-          named_sync(1, 128);
-          for (int q = ew; q < B; q += 4) {
-            const int c = S.cnt[q];
-            if (c > kCTrig) {
-              uint64_t v[8];
+        if (m == gb - 1) {  // accumulators drained: the next group's MMAs may start
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.acc_empty);
+        }
+        if (kDump) continue;
+        named_sync(1, 128);
+        // 2. filter: one ballot per (query, 32 keys); rare survivors inserted by shuffle shift
 #pragma unroll
-              for (int s = 0; s < 8; ++s) {
-                const int i = s * 32 + lane;
-                v[s] = i < c ? S.cbuf[q][i] : kEmpty;
+        for (int i = 0; i < kMyQ; ++i) {
+          const int q = ew + 4 * i;
+          if (q < B) {
+            uint64_t key[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int rr = lane + 32 * j;
+              key[j] = base + rr < row_end ? cand_key(S.stg[rr * kStg + q], (uint32_t)(base + rr)) : kEmpty;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t mask = __ballot_sync(0xffffffffu, key[j] < dev::shfl_u64(top[i], 31));
+              while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const uint64_t x = dev::shfl_u64(key[j], src);
+                const int pos = __popc(__ballot_sync(0xffffffffu, top[i] < x));
+                if (pos < 32) {
+                  const uint64_t up = dev::shfl_u64(top[i], (lane + 31) & 31);
+                  top[i] = lane < pos ? top[i] : (lane == pos ? x : up);
+                }
               }
-              dev::warp_sort<8>(v);
-              __syncwarp();
-              S.cbuf[q][lane] = v[0];
-              if (lane == 31) S.thr[q] = v[0];
-              if (lane == 0) S.cnt[q] = kCandLocal;
             }
           }
-          named_sync(1, 128);
         }
+        named_sync(1, 128);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.acc_empty);
     }
     if (!kDump) {
-      for (int q = ew; q < B; q += 4) {
-        const int c = S.cnt[q];
-        uint64_t v[8];
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
-          const int i = s * 32 + lane;
-          v[s] = i < c ? S.cbuf[q][i] : kEmpty;
-        }
-        dev::warp_sort<8>(v);
-        partial[((size_t)blockIdx.x * B + q) * kCandLocal + lane] = v[0];
+      for (int i = 0; i < kMyQ; ++i) {
+        const int q = ew + 4 * i;
+        if (q < B) partial[((size_t)blockIdx.x * B + q) * kCandLocal + lane] = top[i];
       }
     }
   }
