@@ -112,22 +112,28 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// The MMA-side helpers are executed by the whole (converged) warp with
+// warp-uniform operands; one lane is elected inside the asm.  Issuing them
+// under `if (lane == 0)` instead makes ptxas wrap every instruction in an
+// ELECT/R2UR.BROADCAST waterfall loop, which was the issue-rate bottleneck.
 __device__ __forceinline__ void tc_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b))
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(b))
+      : "memory");
 }
 // D[tmem] (+)= A[smem] * B[smem]
 __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 // D[tmem] (+)= A[tmem] * B[smem]
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
@@ -207,17 +213,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
 
-  if (warp == 0) {
-    // ======================= TMA producer
+  if (warp == 3) {
+    // ======================= TMA producer: query chunks (L2-resident, reused by gb key tiles)
     if (lane == 0 && blk0 < blk1) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&keys_map) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&qh_map) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&ql_map) : "memory");
-      const uint64_t pol_k = policy_evict_first(), pol_q = policy_evict_last();
-      int ks = 0, qs = 0;
-      uint32_t kph = 0, qph = 0;
+      const uint64_t pol_q = policy_evict_last();
+      int qs = 0;
+      uint32_t qph = 0;
       for (int64_t g0 = blk0; g0 < blk1; g0 += kGB) {
-        const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
         for (int kc = 0; kc < nk; ++kc) {
           mbar_wait(&S.q_empty[qs], qph ^ 1);
           mbar_expect_tx(&S.q_full[qs], kTileBytes);
@@ -227,6 +231,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             qs = 0;
             qph ^= 1;
           }
+        }
+      }
+    }
+  } else if (warp == 0) {
+    // ======================= TMA producer: key tiles (HBM stream, runs kKStages ahead)
+    if (lane == 0 && blk0 < blk1) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&keys_map) : "memory");
+      const uint64_t pol_k = policy_evict_first();
+      int ks = 0;
+      uint32_t kph = 0;
+      for (int64_t g0 = blk0; g0 < blk1; g0 += kGB) {
+        const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
+        for (int kc = 0; kc < nk; ++kc) {
           for (int m = 0; m < gb; ++m) {
             mbar_wait(&S.k_empty[ks], kph ^ 1);
             mbar_expect_tx(&S.k_full[ks], kTileBytes);
@@ -246,6 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int ks = 0, qs = 0, ls = 0;
     uint32_t kph = 0, qph = 0, lph = 0;
     int gi = 0;
+    // stage s of a 16-KB ring sits 16384 B = 1024 descriptor units further
+    const uint64_t adesc0 = sw128_desc(&S.kbuf[0][0]);
+    const uint64_t bdesc0 = sw128_desc(&S.qbuf[0][0]);
     for (int64_t g0 = blk0; g0 < blk1; g0 += kGB, ++gi) {
       const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
       if (gi > 0) {
@@ -254,25 +274,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       for (int kc = 0; kc < nk; ++kc) {
         mbar_wait(&S.q_full[qs], qph);
-        const uint64_t bdesc = sw128_desc(&S.qbuf[qs][0]);
+        const uint64_t bdesc = bdesc0 + (uint64_t)(qs * (kTileBytes >> 4));
         for (int m = 0; m < gb; ++m) {
           mbar_wait(&S.k_full[ks], kph);
           mbar_wait(&S.l_full[ls], lph);
           tc_fence_after();
-          if (lane == 0) {
-            const uint64_t adesc = sw128_desc(&S.kbuf[ks][0]);
-            const uint32_t d = tmem + m * kAccCols;
-            const uint32_t kl = tmem + kKlCol0 + ls * kBK;
+          const uint64_t adesc = adesc0 + (uint64_t)(ks * (kTileBytes >> 4));
+          const uint32_t d = tmem + m * kAccCols;
+          const uint32_t kl = tmem + kKlCol0 + ls * kBK;
 #pragma unroll
-            for (int kk = 0; kk < kBK / 8; ++kk) {
-              // +32 B per K-step of 8 tf32 (descriptor address field is in 16-B units)
-              mma_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc1, (kc > 0 || kk > 0) ? 1u : 0u);
-              mma_ts(d + 64, kl + 8 * kk, bdesc + 2 * kk, idesc2, 1u);
-            }
-            tc_commit(&S.k_empty[ks]);
-            tc_commit(&S.l_empty[ls]);
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            // +32 B per K-step of 8 tf32 (descriptor address field is in 16-B units)
+            mma_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc1, (kc > 0 || kk > 0) ? 1u : 0u);
+            mma_ts(d + 64, kl + 8 * kk, bdesc + 2 * kk, idesc2, 1u);
           }
-          __syncwarp();
+          tc_commit(&S.k_empty[ks]);
+          tc_commit(&S.l_empty[ls]);
           if (++ks == kKStages) {
             ks = 0;
             kph ^= 1;
@@ -282,15 +299,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             lph ^= 1;
           }
         }
-        if (lane == 0) tc_commit(&S.q_empty[qs]);
-        __syncwarp();
+        tc_commit(&S.q_empty[qs]);
         if (++qs == kQStages) {
           qs = 0;
           qph ^= 1;
         }
       }
-      if (lane == 0) tc_commit(&S.acc_full);
-      __syncwarp();
+      tc_commit(&S.acc_full);
     }
   } else if (warp >= 4 && warp < 8) {
     // ======================= split: Kl = K - trunc_tf32(K) -> TMEM
