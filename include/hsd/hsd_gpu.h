@@ -201,9 +201,10 @@ hsd_status hsd_quantize(int device, const double* actions, int64_t n, const doub
                         int32_t* bins, int32_t* status, void* stream);
 
 /* ------------------------------------------------------------------------
- * Fused decode-round step (CS-5): kinematics -> search -> verify on one
- * stream with scratch owned by the engine.  All retrieval-mode episodes are
- * searched; decision[] reports the drafter/retrieval boundary.
+ * Fused decode-round step (CS-5): kinematics + search -> verify, ordered on
+ * `stream` (the kinematic metric runs on an engine-owned side stream forked
+ * from and joined back into `stream`, overlapping the DB scan).  All episodes
+ * are searched; decision[] reports the drafter/retrieval boundary.
  * ---------------------------------------------------------------------- */
 typedef struct hsd_engine hsd_engine;
 

@@ -197,7 +197,7 @@ struct StageMarks {
 };
 
 hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, int64_t rb, int64_t re, double* scores,
-                       int32_t* ids, cudaStream_t s, const StageMarks* marks = nullptr) {
+                       int32_t* ids, cudaStream_t s, const StageMarks* marks = nullptr, int reserve_sms = 0) {
   if (k < 1) return fail(HSD_ERR_INVALID_INPUT, "k must be >= 1");  // store.cpp:60
   if (k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k = %d exceeds HSD_K_MAX = %d", k, HSD_K_MAX);
   if (B < 0) return fail(HSD_ERR_INVALID_INPUT, "negative batch");
@@ -214,7 +214,10 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
     CU(cudaGetLastError());
     return HSD_OK;
   }
-  const int nsm = num_sms(c->device);
+  // reserve_sms: SMs left free for work running concurrently on another stream
+  // (the engine's kinematics); the persistent tcgen05 kernel sizes its grid to
+  // the rest so neither waits for the other's CTAs to retire.
+  const int nsm = std::max(1, num_sms(c->device) - std::max(0, reserve_sms));
   const int Bs0 = std::min(B, kSlab);
   const int path0 = choose_path(Bs0);
   const int lists0 = path0 == kPathTc ? hsd::sim_tc_lists(rows, nsm) : hsd::sim_plan(Bs0, rows, c->dim, nsm).lists;
@@ -597,10 +600,15 @@ struct hsd_engine {
   uint8_t* tok = nullptr;
   double *R = nullptr, *D = nullptr, *F = nullptr;
   int32_t* dec = nullptr;
-  // stage timing: 5 events per step (start, kinematics, similarity, select, verify)
+  // stage timing, kStepEvents per step: [0] start, [1] after similarity,
+  // [2] after select, [3] end (verify + join), [4]/[5] kinematics on the side stream
   std::vector<cudaEvent_t> ev;
   int max_steps = 0, recorded = 0;
+  cudaStream_t side = nullptr;  // K5 runs concurrently with K1
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
+
+static constexpr int kStepEvents = 6;
 
 extern "C" {
 
@@ -649,7 +657,7 @@ hsd_status hsd_engine_enable_timing(hsd_engine* e, int max_steps) {
   hsd_status st = require_device(e->c->device);
   if (st != HSD_OK) return st;
   for (cudaEvent_t x : e->ev) cudaEventDestroy(x);
-  e->ev.assign((size_t)max_steps * 5, nullptr);
+  e->ev.assign((size_t)max_steps * kStepEvents, nullptr);
   for (auto& x : e->ev) CU(cudaEventCreate(&x));
   e->max_steps = max_steps;
   e->recorded = 0;
@@ -662,16 +670,19 @@ hsd_status hsd_engine_stage_times(hsd_engine* e, int* n_steps, double* ms) {
   if (st != HSD_OK) return st;
   for (int i = 0; i < 5; ++i) ms[i] = 0.0;
   for (int s = 0; s < e->recorded; ++s) {
-    cudaEvent_t* v = &e->ev[(size_t)s * 5];
-    CU(cudaEventSynchronize(v[4]));
-    for (int i = 0; i < 4; ++i) {
-      float t = 0.f;
-      CU(cudaEventElapsedTime(&t, v[i], v[i + 1]));
-      ms[i] += t;
-    }
-    float tot = 0.f;
-    CU(cudaEventElapsedTime(&tot, v[0], v[4]));
-    ms[4] += tot;
+    cudaEvent_t* v = &e->ev[(size_t)s * kStepEvents];
+    CU(cudaEventSynchronize(v[3]));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, v[4], v[5]));  // kinematics (side stream, overlapped)
+    ms[0] += t;
+    CU(cudaEventElapsedTime(&t, v[0], v[1]));  // similarity
+    ms[1] += t;
+    CU(cudaEventElapsedTime(&t, v[1], v[2]));  // select
+    ms[2] += t;
+    CU(cudaEventElapsedTime(&t, v[2], v[3]));  // verify (+ join of the side stream)
+    ms[3] += t;
+    CU(cudaEventElapsedTime(&t, v[0], v[3]));  // step total
+    ms[4] += t;
   }
   *n_steps = e->recorded;
   e->recorded = 0;
@@ -682,6 +693,12 @@ hsd_status hsd_engine_destroy(hsd_engine* e) {
   if (!e) return HSD_OK;
   cudaSetDevice(e->c->device);
   for (cudaEvent_t x : e->ev) cudaEventDestroy(x);
+  if (e->side) {
+    cudaStreamSynchronize(e->side);
+    cudaStreamDestroy(e->side);
+    cudaEventDestroy(e->fork);
+    cudaEventDestroy(e->join);
+  }
   void* ps[] = {e->q, e->logits, e->fnow, e->fprev, e->xyz, e->hist, e->scores, e->ids, e->out, e->tok, e->R, e->D,
                 e->F, e->dec};
   for (void* p : ps) cudaFree(p);
@@ -694,27 +711,47 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
   if (!e || !io || !vp) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   if (B < 0 || B > e->max_B) return fail(HSD_ERR_INVALID_INPUT, "batch %d outside [0, %d]", B, e->max_B);
   if (B == 0) return HSD_OK;
-  hsd_status st;
+  hsd_status st = require_device(e->c->device);
+  if (st != HSD_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  cudaEvent_t* ev = (e->recorded < e->max_steps) ? &e->ev[(size_t)e->recorded * 5] : nullptr;
+  cudaEvent_t* ev = (e->recorded < e->max_steps) ? &e->ev[(size_t)e->recorded * kStepEvents] : nullptr;
   if (ev) CU(cudaEventRecord(ev[0], s));
-  if (io->xyz) {  // K5: hybrid boundary (decide_sd)
-    st = hsd_window_features(e->c->device, io->xyz, B, mp, nb, io->history, io->R, io->D, io->F, io->decision, stream);
+  if (io->xyz) {
+    // K5 (hybrid boundary, decide_sd) is independent of the retrieval: run it on
+    // a side stream so its latency-bound Gauss-Newton loop hides under K1.
+    if (!e->side) {
+      CU(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&e->join, cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(e->fork, s));
+    CU(cudaStreamWaitEvent(e->side, e->fork, 0));
+    if (ev) CU(cudaEventRecord(ev[4], e->side));
+    st = hsd_window_features(e->c->device, io->xyz, B, mp, nb, io->history, io->R, io->D, io->F, io->decision,
+                             e->side);
     if (st != HSD_OK) return st;
+    if (ev) CU(cudaEventRecord(ev[5], e->side));
+    CU(cudaEventRecord(e->join, e->side));
   }
-  if (ev) CU(cudaEventRecord(ev[1], s));
   StageMarks marks;
   if (ev) {
-    marks.after_sim = ev[2];
-    marks.after_select = ev[3];
+    marks.after_sim = ev[1];
+    marks.after_select = ev[2];
   }
-  st = search_impl(e->c, io->queries, B, e->k, 0, e->c->n, io->scores, io->ids, s, ev ? &marks : nullptr);  // K1+K2
+  const int k5_blocks = io->xyz ? (B + 15) / 16 : 0;  // K5 runs 16 windows per CTA
+  st = search_impl(e->c, io->queries, B, e->k, 0, e->c->n, io->scores, io->ids, s, ev ? &marks : nullptr,
+                   k5_blocks);  // K1+K2
   if (st != HSD_OK) return st;
   st = hsd_verify_round(e->c, io->ids, B, e->k, e->L, io->logits, io->feat_now, io->feat_prev, e->d_f, io->history,
                         gap_d, vp, 1, io->out, io->tokens, stream);  // K4
   if (st != HSD_OK) return st;
+  if (io->xyz) CU(cudaStreamWaitEvent(s, e->join, 0));
   if (ev) {
-    CU(cudaEventRecord(ev[4], s));
+    if (!io->xyz) {
+      CU(cudaEventRecord(ev[4], s));
+      CU(cudaEventRecord(ev[5], s));
+    }
+    CU(cudaEventRecord(ev[3], s));
     ++e->recorded;
   }
   return HSD_OK;

@@ -19,7 +19,9 @@
 namespace hsd {
 namespace {
 
-constexpr int kThreads = 128;
+// 16 windows per block: a decode round's windows occupy few SMs, which the
+// engine keeps free of the similarity kernel so K5 overlaps K1 (api.cu).
+constexpr int kThreads = 512;
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll

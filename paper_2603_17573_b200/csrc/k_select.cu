@@ -27,15 +27,19 @@ using dev::kEmpty;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kPool = 512;
-constexpr int kCandMax = 256;           // rescored candidates (one thread each)
-constexpr int kChunk = 32;              // columns staged per rescoring pass
-constexpr int kRowStride = kChunk + 1;  // bank-conflict-free sequential reads
+constexpr int kCandMax = 256;  // rescored candidates (one thread each)
+// Rescoring staging ring: 2 buffers of n rows x (W + 4) floats (16-B aligned
+// rows for cp.async, +4 floats spreads rows over banks), W = 512 for n <= 32,
+// 64 for n <= 256.
+constexpr int kRowsFloats = 2 * 256 * (64 + 4);  // >= 2 * 32 * (512 + 4)
+static_assert(kRowsFloats >= 2 * 32 * (512 + 4), "staging ring too small");
+constexpr int kMaxW = 512;
 
 struct SelectSmem {
   uint64_t top[kWarps][32];
   uint64_t pool[kPool];
-  float rows[kCandMax * kRowStride];
-  float q[kChunk];
+  __align__(16) float rows[kRowsFloats];
+  __align__(16) double q[2][kMaxW];
   double exact[kCandMax];
   uint32_t id[kCandMax];
   double red[kWarps];
@@ -55,9 +59,18 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* qrow = queries + (size_t)b * dim;
 
-  // 1. approximate global top-32
+  // 1. approximate global top-32 (4 list loads in flight per warp)
   uint64_t top = kEmpty;
-  for (int l = warp; l < lists; l += kWarps) top = dev::warp_merge_top32(top, partial[((size_t)l * B + b) * kCandLocal + lane]);
+  for (int l0 = warp; l0 < lists; l0 += 4 * kWarps) {
+    uint64_t x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int l = l0 + u * kWarps;
+      x[u] = l < lists ? partial[((size_t)l * B + b) * kCandLocal + lane] : kEmpty;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) top = dev::warp_merge_top32(top, x[u]);
+  }
   S.top[warp][lane] = top;
   double qq = 0.0;
   for (int i = tid; i < dim; i += kThreads) qq += (double)qrow[i] * (double)qrow[i];
@@ -116,19 +129,47 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
   if (tid < n) S.id[tid] = cand_id(S.pool[tid]);
   __syncthreads();
 
-  // 3. exact rescoring in the reference's order
-  double acc = 0.0;
-  for (int c0 = 0; c0 < dim; c0 += kChunk) {
-    const int w = dim - c0 < kChunk ? dim - c0 : kChunk;
-    for (int i = tid; i < n * kChunk; i += kThreads) {
-      const int c = i / kChunk, j = i % kChunk;
-      S.rows[c * kRowStride + j] = j < w ? keys[(size_t)S.id[c] * dim + c0 + j] : 0.f;
+  // 3. exact rescoring in the reference's order.  Candidate rows stream
+  //    through a double-buffered cp.async ring of wide column chunks (the
+  //    next chunk lands while this one is consumed); each thread then runs
+  //    the sequential fp64 chain of its candidate out of shared memory.
+  const int W = n <= 32 ? kMaxW : 64;
+  const int stride = W + 4;
+  const int nchunk = (dim + W - 1) / W;
+  const int v4 = W / 4;  // 16-B copies per row chunk
+  auto issue = [&](int ch) {
+    float* dst = S.rows + (ch & 1) * n * stride;
+    const int c0 = ch * W;
+    for (int i = tid; i < n * v4; i += kThreads) {
+      const int c = i / v4, j4 = i - c * v4;
+      const int col = c0 + j4 * 4;
+      const float* src = keys + (size_t)S.id[c] * dim + col;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + c * stride + j4 * 4);
+      const int bytes = col < dim ? 16 : 0;  // dim % 4 == 0; zero-fill past the end
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
     }
-    for (int j = tid; j < kChunk; j += kThreads) S.q[j] = j < w ? qrow[c0 + j] : 0.f;
+    for (int j = tid; j < W; j += kThreads) S.q[ch & 1][j] = c0 + j < dim ? (double)qrow[c0 + j] : 0.0;
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc = 0.0;
+  issue(0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    if (ch + 1 < nchunk) {
+      issue(ch + 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
+    const int w = dim - ch * W < W ? dim - ch * W : W;
     if (tid < n) {
-      const float* r = &S.rows[tid * kRowStride];
-      for (int j = 0; j < w; ++j) acc = __dadd_rn(acc, __dmul_rn((double)S.q[j], (double)r[j]));
+      // acc = fl(acc + fl(q*k)) of store.cpp:32; the fp32 x fp32 product is
+      // exact in fp64, so the fused form fl(acc + q*k) is bit-identical and
+      // leaves one dependent op per element on the chain.
+      const float* r = S.rows + (ch & 1) * n * stride + tid * stride;
+      const double* qc = S.q[ch & 1];
+#pragma unroll 16
+      for (int j = 0; j < w; ++j) acc = __fma_rn(qc[j], (double)r[j], acc);
     }
     __syncthreads();
   }
