@@ -113,13 +113,15 @@ hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B,
  * the result may be inexact).  Synchronizes `stream`. */
 hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count);
 
-/* Diagnostics: the tcgen05 similarity kernel's approximate (filter) scores of
- * B <= 64 queries against every record, fp32 [B][size] (device).  Used by the
- * tests to check the 3xTF32 error bound the exact rescoring relies on. */
-hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, float* out, void* stream);
+/* Diagnostics: a tcgen05 similarity kernel's approximate (filter) scores of
+ * B <= 64 queries against every record, fp32 [B][size] (device); variant 1 =
+ * TF32 filter (default path), 3 = 3xTF32 filter.  Used by the tests to check
+ * the error bounds the exact rescoring relies on. */
+hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
+                                void* stream);
 /* Similarity-path override for ablations/tests: 0 auto (SIMT for B <= 4,
- * tcgen05 otherwise), 1 SIMT rows/tile, 2 SIMT tile, 3 tcgen05 always.
- * Process-wide; also settable with HSD_SIM_PATH=rows|tile|tc. */
+ * tcgen05 TF32 otherwise), 1 SIMT rows/tile, 2 SIMT tile, 3 tcgen05 TF32,
+ * 4 tcgen05 3xTF32.  Process-wide; also HSD_SIM_PATH=rows|tile|tc|tc3. */
 hsd_status hsd_set_sim_path(int path);
 
 /* ------------------------------------------------------------------------

@@ -172,7 +172,7 @@ def lib():
         "hsd_verify_round_drafts": [C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp,
                                     C.c_int, _vp, C.c_int, _vp, _vp, _vp],
         "hsd_collection_generate_rows": [_vp, C.c_int, C.c_uint64, C.c_int64, C.c_int64],
-        "hsd_debug_sim_scores": [_vp, _vp, C.c_int, _vp, _vp],
+        "hsd_debug_sim_scores": [_vp, _vp, C.c_int, C.c_int, _vp, _vp],
         "hsd_set_sim_path": [C.c_int],
         "hsd_gen_queries": [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, _vp,
                             _vp],
@@ -319,12 +319,12 @@ class Collection:
                                               _ptr(scores), _ptr(ids), _stream(stream)))
         return scores, ids
 
-    def debug_sim_scores(self, queries, stream=None):
-        """Approximate tcgen05 filter scores float32 [B, size] (diagnostics)."""
+    def debug_sim_scores(self, queries, variant=1, stream=None):
+        """Approximate tcgen05 filter scores float32 [B, size] (diagnostics; variant 1 TF32, 3 3xTF32)."""
         torch = _torch()
         q = queries.contiguous()
         out = torch.empty((q.shape[0], self.size()), dtype=torch.float32, device=q.device)
-        check(lib().hsd_debug_sim_scores(self._h, _ptr(q), q.shape[0], _ptr(out), _stream(stream)))
+        check(lib().hsd_debug_sim_scores(self._h, _ptr(q), q.shape[0], variant, _ptr(out), _stream(stream)))
         return out
 
     def overflow_count(self, stream=None) -> int:
@@ -464,11 +464,11 @@ def quantize(actions, lo=-1.0, hi=1.0, k_bins=256, stream=None):
     return bins
 
 
-SIM_PATHS = {"auto": 0, "rows": 1, "tile": 2, "tc": 3}
+SIM_PATHS = {"auto": 0, "rows": 1, "tile": 2, "tc": 3, "tc3": 4}
 
 
 def set_sim_path(name: str) -> None:
-    """Similarity kernel override (ablations / tests): auto | rows | tile | tc."""
+    """Similarity kernel override (ablations / tests): auto | rows | tile | tc | tc3."""
     check(lib().hsd_set_sim_path(SIM_PATHS[name]))
 
 

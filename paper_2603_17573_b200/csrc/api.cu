@@ -169,16 +169,19 @@ hsd_status get_scratch(hsd_collection* c, cudaStream_t s, size_t partial_bytes, 
 constexpr int kSlab = 64;  // queries per similarity launch
 
 // Similarity path per query slab: SIMT GEMV for tiny batches (HBM-bound on
-// CUDA cores), tcgen05 3xTF32 otherwise.  HSD_SIM_PATH=rows|tile|tc overrides
-// (tests and ablations).
-enum { kPathAuto = 0, kPathRows = 1, kPathTile = 2, kPathTc = 3 };
+// CUDA cores), the tcgen05 TF32 filter otherwise.  HSD_SIM_PATH=rows|tile|tc|tc3
+// or hsd_set_sim_path override it (tests and ablations; tc3 = 3xTF32 filter).
+enum { kPathAuto = 0, kPathRows = 1, kPathTile = 2, kPathTc = 3, kPathTc3 = 4 };
 int g_path = -1;
 int path_override() {
   int& v = g_path;
   if (v < 0) {
     const char* e = getenv("HSD_SIM_PATH");
-    v = !e ? kPathAuto
-           : (!strcmp(e, "rows") ? kPathRows : (!strcmp(e, "tile") ? kPathTile : (!strcmp(e, "tc") ? kPathTc : 0)));
+    v = kPathAuto;
+    if (e && !strcmp(e, "rows")) v = kPathRows;
+    if (e && !strcmp(e, "tile")) v = kPathTile;
+    if (e && !strcmp(e, "tc")) v = kPathTc;
+    if (e && !strcmp(e, "tc3")) v = kPathTc3;
   }
   return v;
 }
@@ -186,9 +189,10 @@ int choose_path(int Bs) {
   const int o = path_override();
   if (o == kPathRows) return Bs <= 8 ? kPathRows : kPathTile;
   if (o == kPathTile) return Bs <= 8 ? kPathRows : kPathTile;  // launch_sim picks rows for B <= 8
-  if (o == kPathTc) return kPathTc;
+  if (o == kPathTc || o == kPathTc3) return o;
   return Bs <= 4 ? kPathRows : kPathTc;
 }
+bool is_tc(int p) { return p == kPathTc || p == kPathTc3; }
 
 // Optional stage events (engine timing): marks[i] is recorded after stage i.
 struct StageMarks {
@@ -220,10 +224,10 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   const int nsm = std::max(1, num_sms(c->device) - std::max(0, reserve_sms));
   const int Bs0 = std::min(B, kSlab);
   const int path0 = choose_path(Bs0);
-  const int lists0 = path0 == kPathTc ? hsd::sim_tc_lists(rows, nsm) : hsd::sim_plan(Bs0, rows, c->dim, nsm).lists;
+  const int lists0 = is_tc(path0) ? hsd::sim_tc_lists(rows, nsm) : hsd::sim_plan(Bs0, rows, c->dim, nsm).lists;
   Scratch* sc = nullptr;
   st = get_scratch(c, s, (size_t)std::max(lists0, 4 * nsm) * Bs0 * hsd::dev::kCandLocal * sizeof(uint64_t),
-                   path0 == kPathTc ? hsd::sim_tc_scratch_bytes(c->dim) : 0, &sc);
+                   is_tc(path0) ? hsd::sim_tc_scratch_bytes(c->dim) : 0, &sc);
   if (st != HSD_OK) return st;
   CU(cudaMemsetAsync(sc->overflow, 0, sizeof(int), s));
   for (int b0 = 0; b0 < B; b0 += kSlab) {
@@ -232,6 +236,10 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
     hsd::SimPlan plan = hsd::sim_plan(Bs, rows, c->dim, nsm);
     const float* q = queries + (size_t)b0 * c->dim;
     if (path == kPathTc) {
+      plan.lists = hsd::sim_tc_lists(rows, nsm);
+      plan.gamma = hsd::sim_tc1_gamma(c->dim);
+      CU(hsd::launch_sim_tc1(c->keys, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial, nullptr, s));
+    } else if (path == kPathTc3) {
       plan.lists = hsd::sim_tc_lists(rows, nsm);
       plan.gamma = hsd::sim_tc_gamma(c->dim);
       CU(hsd::launch_sim_tc(c->keys, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial, nullptr, s));
@@ -404,14 +412,17 @@ hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B,
 }
 
 hsd_status hsd_set_sim_path(int path) {
-  if (path < 0 || path > 3) return fail(HSD_ERR_INVALID_INPUT, "path must be 0 auto, 1 rows, 2 tile, 3 tc");
+  if (path < 0 || path > 4)
+    return fail(HSD_ERR_INVALID_INPUT, "path must be 0 auto, 1 rows, 2 tile, 3 tc (TF32), 4 tc3 (3xTF32)");
   g_path = path;
   return HSD_OK;
 }
 
-hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, float* out, void* stream) {
+hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
+                                void* stream) {
   if (!c || !queries || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   if (B < 1 || B > kSlab) return fail(HSD_ERR_INVALID_INPUT, "debug dump supports 1 <= B <= %d", kSlab);
+  if (variant != 1 && variant != 3) return fail(HSD_ERR_INVALID_INPUT, "variant must be 1 (TF32) or 3 (3xTF32)");
   hsd_status st = require_device(c->device);
   if (st != HSD_OK) return st;
   if (c->n == 0) return HSD_OK;
@@ -420,8 +431,12 @@ hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, 
   st = get_scratch(c, (cudaStream_t)stream, (size_t)lists * B * hsd::dev::kCandLocal * 8, hsd::sim_tc_scratch_bytes(c->dim),
                    &sc);
   if (st != HSD_OK) return st;
-  CU(hsd::launch_sim_tc(c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial, out,
-                        (cudaStream_t)stream));
+  if (variant == 3)
+    CU(hsd::launch_sim_tc(c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial, out,
+                          (cudaStream_t)stream));
+  else
+    CU(hsd::launch_sim_tc1(c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial, out,
+                           (cudaStream_t)stream));
   return HSD_OK;
 }
 

@@ -43,6 +43,14 @@ cudaError_t launch_sim_tc(const float* keys, int64_t n_keys_total, int64_t row_b
                           const float* queries, int B, int lists, float* scratch, uint64_t* partial, float* dump,
                           cudaStream_t s);
 
+// K1 tcgen05 TF32 filter path (k_sim_tc1.cu, default for B > 4): same
+// contract; scratch sim_tc1_scratch_bytes(dim) (64-row padded query slab).
+double sim_tc1_gamma(int dim);
+size_t sim_tc1_scratch_bytes(int dim);
+cudaError_t launch_sim_tc1(const float* keys, int64_t n_keys_total, int64_t row_begin, int64_t row_end, int dim,
+                           const float* queries, int B, int lists, float* scratch, uint64_t* partial, float* dump,
+                           cudaStream_t s);
+
 // ---- K2 select: margin candidates + exact fp64 rescoring + final top-k -------
 cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const float* keys, int dim,
                           const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
