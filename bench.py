@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=20.0)
     p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--force-sharded", action="store_true",
+                   help="use the sharded (NCCL all-gather + merge) step even at world size 1")
     return p.parse_args()
 
 
@@ -102,7 +104,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
+                                          "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -286,7 +288,7 @@ def run_ours(args):
     hist = torch.full((B,), 100, dtype=torch.int32, device=dev)
     vp = H.VerifyParams.make(relaxed=True, bias_seq_max=30, bias_token_max=15, skip_enabled=True, min_S=0.95, O_dist=5)
 
-    if world == 1:
+    if world == 1 and not args.force_sharded:
         eng = H.Engine(col, B, k, L, d_f, 15)
         outs = dict(scores=torch.empty((B, k), dtype=torch.float64, device=dev),
                     ids=torch.empty((B, k), dtype=torch.int32, device=dev),
@@ -372,7 +374,7 @@ def run_ours(args):
     overflow = col.overflow_count(stream)
     if rank == 0:
         cb = None
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and not args.force_sharded:
             cb, _ = cpu_baseline(args, seconds_budget=args.cpu_seconds)
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
@@ -401,6 +403,8 @@ def gen_logits_global(H, args, rows, local, col, b0, b1):
 
 
 def setup_comm(H, dist, world, rank, local):
+    if world == 1:
+        return H.Comm(H.Comm.unique_id(), 1, 0, local)
     obj = [H.Comm.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     return H.Comm(obj[0], world, rank, local)

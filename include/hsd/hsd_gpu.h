@@ -265,6 +265,14 @@ hsd_status hsd_shard_range(int64_t n_total, int world, int rank, int64_t* begin,
 hsd_status hsd_search_topk_sharded(hsd_collection* c, hsd_comm* comm, int64_t id_offset, const float* queries, int B,
                                    int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream);
 
+/* K3 merge on the device: G per-shard exact top-k lists (g_scores fp64 /
+ * g_ids int32 [G][B][k], ids already global; optional g_drafts uint8
+ * [G][B][k][32]) -> the global [B][k] in (score desc, id asc) order.  Used by
+ * hsd_search_topk_sharded after the all-gather, and directly for task shards
+ * searched separately on one GPU. */
+hsd_status hsd_merge_topk(int device, const double* g_scores, const int32_t* g_ids, const uint8_t* g_drafts, int G,
+                          int B, int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream);
+
 /* ------------------------------------------------------------------------
  * Synthetic workload generators on the device (include/hsd/hsd_synth.h).
  * ---------------------------------------------------------------------- */

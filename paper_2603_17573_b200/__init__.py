@@ -174,6 +174,7 @@ def lib():
         "hsd_collection_generate_rows": [_vp, C.c_int, C.c_uint64, C.c_int64, C.c_int64],
         "hsd_debug_sim_scores": [_vp, _vp, C.c_int, C.c_int, _vp, _vp],
         "hsd_set_sim_path": [C.c_int],
+        "hsd_merge_topk": [C.c_int, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
         "hsd_gen_queries": [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, _vp,
                             _vp],
         "hsd_gen_logits": [_vp, C.c_uint64, _vp, C.c_int, C.c_int, _vp, _vp],
@@ -407,6 +408,19 @@ class Comm:
         check(lib().hsd_search_topk_sharded(col.handle, self._h, id_offset, _ptr(queries), B, k, _ptr(scores),
                                             _ptr(ids), _ptr(drafts), _stream(stream)))
         return scores, ids, drafts
+
+
+def merge_topk(g_scores, g_ids, g_drafts=None, stream=None):
+    """K3 device merge of G shard lists [G, B, k] (global ids) -> (scores, ids[, drafts]) [B, k]."""
+    torch = _torch()
+    G, B, k = g_ids.shape
+    scores = torch.empty((B, k), dtype=torch.float64, device=g_ids.device)
+    ids = torch.empty((B, k), dtype=torch.int32, device=g_ids.device)
+    drafts = None if g_drafts is None else torch.empty((B, k, TOKENS_STRIDE), dtype=torch.uint8, device=g_ids.device)
+    check(lib().hsd_merge_topk(g_ids.device.index or 0, _ptr(g_scores.contiguous()), _ptr(g_ids.contiguous()),
+                               _ptr(None if g_drafts is None else g_drafts.contiguous()), G, B, k, _ptr(scores),
+                               _ptr(ids), _ptr(drafts), _stream(stream)))
+    return (scores, ids) if drafts is None else (scores, ids, drafts)
 
 
 def _from_ptr(ptr, shape, dtype, device):

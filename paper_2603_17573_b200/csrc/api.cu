@@ -932,6 +932,18 @@ hsd_status hsd_search_topk_sharded(hsd_collection* col, hsd_comm* cm, int64_t id
   return HSD_OK;
 }
 
+hsd_status hsd_merge_topk(int device, const double* g_scores, const int32_t* g_ids, const uint8_t* g_drafts, int G,
+                          int B, int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream) {
+  if (G < 1 || B < 0 || k < 1 || k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "bad merge shape");
+  if (!g_scores || !g_ids || !scores || !ids || (drafts && !g_drafts)) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (B == 0) return HSD_OK;
+  hsd_status st = require_device(device);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_merge_ranks(g_scores, g_ids, drafts ? g_drafts : nullptr, G, B, k, scores, ids, drafts,
+                             (cudaStream_t)stream));
+  return HSD_OK;
+}
+
 // ------------------------------------------------------------------ generators
 hsd_status hsd_gen_queries(int device, int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B,
                            int dim, float* out, void* stream) {

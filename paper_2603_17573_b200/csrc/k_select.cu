@@ -133,7 +133,11 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
   //    through a double-buffered cp.async ring of wide column chunks (the
   //    next chunk lands while this one is consumed); each thread then runs
   //    the sequential fp64 chain of its candidate out of shared memory.
-  const int W = n <= 32 ? kMaxW : 64;
+  // widest chunk whose double buffer fits: fewer chunk rounds (syncs, waits)
+  const int W = 2 * n * (kMaxW + 4) <= kRowsFloats ? kMaxW
+                : 2 * n * (256 + 4) <= kRowsFloats ? 256
+                : 2 * n * (128 + 4) <= kRowsFloats ? 128
+                                                   : 64;
   const int stride = W + 4;
   const int nchunk = (dim + W - 1) / W;
   const int v4 = W / 4;  // 16-B copies per row chunk

@@ -1,0 +1,161 @@
+// dropin_test.cpp — the reference's own C++ API next to the drop-in.
+//
+// Builds a reference hsd::Collection (store.cpp, compiled in place into
+// oracle/_ref/libhsdref.so), uploads it with hsd::gpu::Collection::from, and
+// checks that search_topk_exact returns identical SearchHits (score bits,
+// record ids, payloads), that hsd::gpu::quantize matches hsd::quantize, that
+// hsd::gpu::window_features matches the oracle restatement within 1e-5, and
+// that errors surface as the reference's exception types.
+// Built by tests/cpp/Makefile (needs /root/reference headers), run on the GPU
+// box by tests/test_cpp_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "hsd/gpu.hpp"
+
+extern "C" {
+#include "hsd_oracle.h"
+}
+#include "hsd_synth.h"
+
+static int failures = 0;
+#define CHECK(cond, ...)              \
+  do {                                \
+    if (!(cond)) {                    \
+      std::printf("FAIL: " __VA_ARGS__); \
+      std::printf("\n");              \
+      ++failures;                     \
+    }                                 \
+  } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+int main() {
+  const int dim = 256, n = 5000, B = 40, k = 8;
+  // ---- reference collection with synthetic records
+  hsd::Collection ref("dropin", dim);
+  std::vector<float> row((size_t)dim);
+  for (int r = 0; r < n; ++r) {
+    hsdo_gen_keys(HSD_SYNTH_REAL, 77, r, 1, dim, row.data());
+    hsd::Payload p;
+    p.dataset_name = "synthetic";
+    p.episode_idx = r / 100;
+    p.step_idx = r % 100;
+    for (int s = 0; s < 3; ++s)
+      for (int j = 0; j < 7; ++j) p.next_actions[(size_t)s][(size_t)j] = hsd_action_val(77, r, s, j);
+    ref.insert(hsd::Embedding(row.begin(), row.end()), p);
+  }
+  hsd::gpu::Collection gpu = hsd::gpu::Collection::from(ref, 0);
+  CHECK(gpu.size() == ref.size(), "size");
+
+  // ---- search parity (single and batched)
+  std::vector<float> q((size_t)B * dim);
+  hsdo_gen_queries(HSD_SYNTH_REAL, 78, 77, n, 0, B, dim, q.data());
+  std::vector<hsd::Embedding> queries;
+  for (int b = 0; b < B; ++b) queries.emplace_back(q.begin() + (size_t)b * dim, q.begin() + (size_t)(b + 1) * dim);
+  auto batch = gpu.search_topk_exact_batch(queries, k);
+  for (int b = 0; b < B; ++b) {
+    auto want = ref.search_topk_exact(queries[(size_t)b], k);
+    auto got = b % 7 == 0 ? gpu.search_topk_exact(queries[(size_t)b], k) : batch[(size_t)b];
+    CHECK(got.size() == want.size(), "hit count q=%d", b);
+    for (size_t i = 0; i < std::min(got.size(), want.size()); ++i) {
+      CHECK(got[i].record_id == want[i].record_id, "id q=%d rank=%zu", b, i);
+      CHECK(std::memcmp(&got[i].score, &want[i].score, sizeof(double)) == 0, "score bits q=%d rank=%zu", b, i);
+      CHECK(got[i].payload == want[i].payload, "payload q=%d rank=%zu", b, i);
+    }
+  }
+  CHECK(gpu.search_topk(queries[0], HSD_K_MAX).size() == HSD_K_MAX, "k = HSD_K_MAX");
+  CHECK(throws<hsd::InvalidInputError>([&] { gpu.search_topk(queries[0], HSD_K_MAX + 1); }),
+        "k > HSD_K_MAX -> InvalidInputError (documented device limit, no CPU fallback)");
+  CHECK(throws<hsd::InvalidInputError>([&] { gpu.search_topk_exact(queries[0], 0); }), "k < 1 -> InvalidInputError");
+  CHECK(throws<hsd::SchemaError>([&] { gpu.insert(hsd::Embedding(3, 0.0), hsd::Payload{}); }), "dim -> SchemaError");
+  hsd::gpu::Collection empty("e", dim);
+  CHECK(empty.search_topk_exact(queries[0], 5).empty(), "empty collection -> empty result");
+  CHECK(throws<hsd::ConfigError>([&] { hsd::gpu::Collection bad("b", 0); }), "dim 0 -> ConfigError");
+
+  // ---- quantize parity against the reference
+  std::mt19937_64 rng(5);
+  std::uniform_real_distribution<double> U(-1.4, 1.4);
+  std::vector<hsd::ActionSlice> acts(3000);
+  for (auto& a : acts)
+    for (int j = 0; j < 7; ++j) a[j] = U(rng);
+  acts[0] = hsd::ActionSlice{{-1, 1, 0, 1, -1, 0.5, 1}};
+  const auto bounds = hsd::ActionSpaceBounds::uniform(-1.0, 1.0);
+  auto got = hsd::gpu::quantize_batch(acts, bounds, 256);
+  for (size_t i = 0; i < acts.size(); ++i) CHECK(got[i] == hsd::quantize(acts[i], bounds, 256), "quantize %zu", i);
+  hsd::ActionSlice nan_a;
+  nan_a[2] = NAN;
+  CHECK(throws<hsd::InvalidInputError>([&] { hsd::gpu::quantize(nan_a, bounds, 256); }), "nan -> InvalidInputError");
+
+  // ---- window_features vs the oracle restatement (reference needs Eigen)
+  hsd::FusedMetricParams mp;  // alpha .5, w 15, theta .5, r_cap 1 (kinematics.hpp:39-42)
+  hsd::NormalizationBounds nb{0.000009, 0.123381, 0.000001, 0.014989};
+  std::vector<std::vector<hsd::TrajectoryPoint>> wins;
+  std::normal_distribution<double> N(0.0, 0.004);
+  for (int w = 0; w < 200; ++w) {
+    std::vector<hsd::TrajectoryPoint> pts;
+    double x = 0, y = 0, z = 0;
+    for (int i = 0; i < 15; ++i) {
+      if (w % 3 == 0) {
+        const double th = 0.3 * i;
+        x = 0.05 * std::cos(th) + 0.1 * w / 200.0;
+        y = 0.05 * std::sin(th);
+        z = 0.001 * i;
+      } else {
+        x += N(rng);
+        y += N(rng);
+        z += N(rng);
+      }
+      pts.push_back({x, y, z, i});
+    }
+    wins.push_back(pts);
+  }
+  std::vector<hsd::SdKind> dec;
+  auto feats = hsd::gpu::window_features_batch(wins, mp, nb, &dec);
+  hsdo_metric_params omp{mp.alpha, mp.w, mp.threshold, mp.r_cap};
+  hsdo_norm_bounds onb{nb.d_min, nb.d_max95, nb.r_min, nb.r_max95};
+  for (size_t w = 0; w < wins.size(); ++w) {
+    double xyz[45], R, D, F;
+    int d;
+    for (int i = 0; i < 15; ++i) {
+      xyz[3 * i] = wins[w][(size_t)i].x;
+      xyz[3 * i + 1] = wins[w][(size_t)i].y;
+      xyz[3 * i + 2] = wins[w][(size_t)i].z;
+    }
+    hsdo_window_features(xyz, 15, &omp, &onb, &R, &D, &F, &d);
+    CHECK(std::fabs(feats[w].R - R) <= 1e-5 * std::max(1e-12, std::fabs(R)) + 1e-15, "R w=%zu %g %g", w, feats[w].R, R);
+    CHECK(std::fabs(feats[w].D - D) <= 1e-5 * D + 1e-15, "D w=%zu", w);
+    CHECK(std::fabs(feats[w].F - F) <= 1e-5, "F w=%zu", w);
+    if (std::fabs(F - mp.threshold) > 1e-9)
+      CHECK((dec[w] == hsd::SdKind::retrieval_sd) == (d == 1), "decision w=%zu", w);
+  }
+  auto one = hsd::gpu::window_features(std::span<const hsd::TrajectoryPoint>(wins[1]), mp, nb);
+  CHECK(one.R == feats[1].R && one.w == 15, "single window");
+  CHECK(throws<hsd::InvalidInputError>([&] {
+          hsd::gpu::window_features(std::span<const hsd::TrajectoryPoint>(wins[0].data(), 14), mp, nb);
+        }),
+        "w mismatch -> InvalidInputError");
+  hsd::FusedMetricParams badp;
+  badp.alpha = 1.5;
+  CHECK(throws<hsd::ConfigError>([&] { hsd::gpu::window_features_batch({wins[0]}, badp, nb); }), "alpha -> ConfigError");
+
+  if (failures) {
+    std::printf("DROPIN FAILED (%d)\n", failures);
+    return 1;
+  }
+  std::printf("DROPIN OK: %d queries, %zu quantize, %zu windows\n", B, acts.size(), wins.size());
+  return 0;
+}

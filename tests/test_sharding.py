@@ -1,0 +1,123 @@
+"""Row-sharded DB: rank r of G owns the contiguous id range
+hsd_shard_range(N, G, r); each rank's exact local top-k is exchanged (NCCL
+all-gather on the GPU path) and k-way merged in (score desc, id asc) order,
+which makes the result bit-identical to the single-collection search.
+
+CPU (gloo, world_size 2): the host-side protocol — shard ranges from the C ABI,
+per-shard oracle top-k with global ids, all-gather, merge — equals the
+unsharded oracle search.
+GPU: the device merge kernel (K3) over virtual shards of one GPU, and
+hsd_search_topk_sharded through a real 1-rank NCCL communicator."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2603_17573_b200 as H
+from oracle import oracle as O
+
+N, DIM, B, K, SEED = 6000, 64, 12, 8, 31
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def merge_lists(lists, k):
+    """(score desc, id asc) merge of per-shard (scores, ids) lists."""
+    out_s, out_i = [], []
+    for b in range(lists[0][0].shape[0]):
+        cand = [(s, i) for sc, ids in lists for s, i in zip(sc[b], ids[b]) if i >= 0]
+        cand.sort(key=lambda t: (-t[0], t[1]))
+        out_s.append([c[0] for c in cand[:k]])
+        out_i.append([c[1] for c in cand[:k]])
+    return np.array(out_s), np.array(out_i)
+
+
+def _worker(rank, world, port, q, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    b, e = H.shard_range(N, world, rank)
+    keys = O.gen_keys(O.REAL, SEED, b, e - b, DIM)
+    sc, ids = O.search_topk(keys, q, K)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (sc, ids + b))
+    ms, mi = merge_lists(gathered, K)
+    ret[rank] = (ms, mi)
+    dist.destroy_process_group()
+
+
+def test_gloo_two_rank_sharded_protocol():
+    q = O.gen_queries(O.REAL, 32, SEED, N, 0, B, DIM)
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    ret = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, ret)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    full_s, full_i = O.search_synth(O.REAL, SEED, N, q, K)
+    for r in range(2):
+        ms, mi = ret[r]
+        np.testing.assert_array_equal(mi, full_i)
+        np.testing.assert_array_equal(ms, full_s)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_device_merge_of_virtual_shards(G):
+    col = H.Collection(DIM, capacity=N)
+    col.generate(O.EXACT, SEED, N)  # heavy ties: merge order must follow ids
+    q = H.gen_queries(O.EXACT, 32, SEED, N, 0, B, DIM)
+    full_s, full_i = col.search_topk_exact(q, K)
+    gs, gi = [], []
+    for r in range(G):
+        b, e = H.shard_range(N, G, r)
+        s, i = col.search_topk_exact(q, K, row_range=(b, e))
+        gs.append(s)
+        gi.append(i)
+    _, toks = col.keys_view()
+    gi_t = torch.stack(gi)
+    gd = torch.where(gi_t[..., None] >= 0, toks[gi_t.clamp(min=0).long()], torch.zeros_like(toks[:1][None]))
+    ms, mi, md = H.merge_topk(torch.stack(gs), gi_t, gd)
+    np.testing.assert_array_equal(mi.cpu().numpy(), full_i.cpu().numpy())
+    np.testing.assert_array_equal(ms.cpu().numpy(), full_s.cpu().numpy())
+    np.testing.assert_array_equal(md.cpu().numpy(), toks[full_i.long()].cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_nccl_sharded_search_single_rank():
+    """hsd_search_topk_sharded through a real NCCL communicator (world 1 on
+    one GPU): local search + all-gather + merge + draft records; then the
+    verify kernel on the pre-gathered drafts equals verify on the collection."""
+    col = H.Collection(DIM, capacity=N)
+    col.generate(O.REAL, SEED, N)
+    q = H.gen_queries(O.REAL, 32, SEED, N, 0, B, DIM)
+    comm = H.Comm(H.Comm.unique_id(), 1, 0, 0)
+    try:
+        s, i, d = comm.search_topk(col, 0, q, K)
+    finally:
+        comm.close()
+    full_s, full_i = col.search_topk_exact(q, K)
+    np.testing.assert_array_equal(i.cpu().numpy(), full_i.cpu().numpy())
+    np.testing.assert_array_equal(s.cpu().numpy(), full_s.cpu().numpy())
+    _, toks = col.keys_view()
+    np.testing.assert_array_equal(d.cpu().numpy(), toks[full_i.long()].cpu().numpy())
+    rows = H.query_rows(32, O.REAL, N, 0, B)
+    lg = H.gen_logits(col, 3, rows, 7)
+    vp = H.VerifyParams.make()
+    o1, t1 = col.verify_round(i, lg, vp)
+    o2, t2 = H.verify_round_drafts(i, d, lg, vp)
+    assert (o1 == o2).all()
+    np.testing.assert_array_equal(t1.cpu().numpy(), t2.cpu().numpy())
