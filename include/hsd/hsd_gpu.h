@@ -51,6 +51,12 @@ typedef enum hsd_status {
   HSD_ERR_NO_DEVICE = 103,
 } hsd_status;
 
+/* Key storage type of a collection. */
+typedef enum hsd_dtype {
+  HSD_DTYPE_F32 = 0,  /* fp32 keys (the reference's fp64 embeddings rounded once to fp32) */
+  HSD_DTYPE_BF16 = 1, /* bf16 keys (RN-even from fp32): half the HBM bytes per scan */
+} hsd_dtype;
+
 const char* hsd_last_error(void);
 int hsd_abi_version(void);
 /* Number of visible sm_100 devices (0 when none). */
@@ -67,12 +73,22 @@ hsd_status hsd_device_count(int* n);
 typedef struct hsd_collection hsd_collection;
 
 hsd_status hsd_collection_create(int device, int dim, int64_t capacity, hsd_collection** out);
+/* Same with an explicit key storage type (hsd_dtype).  bf16 collections round
+ * keys once to bf16 (RN-even) at insert/generate; searches over them are exact
+ * (bit-identical to the reference's fp64 dot) with respect to the STORED bf16
+ * keys, and their recall against an fp32 DB is what the bf16 mode reports.
+ * bf16 needs dim % 8 == 0 -> HSD_ERR_CONFIG otherwise. */
+hsd_status hsd_collection_create_ex(int device, int dim, int64_t capacity, int dtype, hsd_collection** out);
 hsd_status hsd_collection_destroy(hsd_collection* c);
 hsd_status hsd_collection_size(const hsd_collection* c, int64_t* n);
 hsd_status hsd_collection_dim(const hsd_collection* c, int* dim);
 hsd_status hsd_collection_device(const hsd_collection* c, int* device);
-/* Device pointers of the resident arrays (read-only views). */
+/* Device pointers of the resident arrays (read-only views); the fp32 key view
+ * fails with HSD_ERR_INVALID_INPUT on a bf16 collection. */
 hsd_status hsd_collection_keys(const hsd_collection* c, const float** keys, const uint8_t** tokens);
+hsd_status hsd_collection_dtype(const hsd_collection* c, int* dtype);
+/* Untyped key view (fp32 or bf16 bits per hsd_collection_dtype). */
+hsd_status hsd_collection_data(const hsd_collection* c, const void** keys, const uint8_t** tokens);
 
 /* Collection::insert (store.cpp:44-57) of n records.  HOST pointers:
  *   emb          fp32 [n][dim]
@@ -114,14 +130,17 @@ hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B,
 hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count);
 
 /* Diagnostics: a tcgen05 similarity kernel's approximate (filter) scores of
- * B <= 64 queries against every record, fp32 [B][size] (device); variant 1 =
- * TF32 filter (default path), 3 = 3xTF32 filter.  Used by the tests to check
- * the error bounds the exact rescoring relies on. */
+ * B queries against every record, fp32 [B][size] (device); variant 1 = the
+ * wide filter of the default path (TF32 over fp32 keys, bf16 over bf16 keys;
+ * B <= 256), 2 = 64-query TF32 kernel, 3 = 3xTF32 filter (B <= 64).  Used by
+ * the tests to check the error bounds the exact rescoring relies on. */
 hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
                                 void* stream);
-/* Similarity-path override for ablations/tests: 0 auto (SIMT for B <= 4,
- * tcgen05 TF32 otherwise), 1 SIMT rows/tile, 2 SIMT tile, 3 tcgen05 TF32,
- * 4 tcgen05 3xTF32.  Process-wide; also HSD_SIM_PATH=rows|tile|tc|tc3. */
+/* Similarity-path override for ablations/tests (fp32 collections): 0 auto
+ * (SIMT for B <= 4, wide tcgen05 TF32 otherwise), 1 SIMT rows/tile, 2 SIMT
+ * tile, 3 wide tcgen05 TF32 (256 queries per pass), 4 tcgen05 3xTF32, 5
+ * 64-query tcgen05 TF32.  Process-wide; also HSD_SIM_PATH=rows|tile|tc|tc3|tc1.
+ * bf16 collections always use the wide kernel. */
 hsd_status hsd_set_sim_path(int path);
 
 /* ------------------------------------------------------------------------

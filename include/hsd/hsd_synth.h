@@ -96,6 +96,29 @@ HSD_HD float hsd_norm_val(int64_t raw, int64_t sumsq) {
   return (float)((double)raw / n);
 }
 
+/* ---- bf16 key storage (bf16 collections) ----------------------------------
+ * fp32 -> bf16 round-to-nearest-even on the bit pattern (finite inputs; the
+ * generators and insert reject non-finite values), identical on host and
+ * device, and the exact widening back to fp32. */
+HSD_HD uint16_t hsd_bf16_bits(float f) {
+  union {
+    float f;
+    uint32_t u;
+  } v;
+  v.f = f;
+  uint32_t u = v.u;
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+HSD_HD float hsd_bf16_val(uint16_t b) {
+  union {
+    float f;
+    uint32_t u;
+  } v;
+  v.u = (uint32_t)b << 16;
+  return v.f;
+}
+
 /* ---- queries -------------------------------------------------------------
  * Query q of a batch is one of:
  *   EXACT: 25% an exact copy of DB row r (r hashed), else a fresh EXACT vector.

@@ -61,18 +61,24 @@ int hsdo_search_topk_exact(const float* keys, int64_t n, int dim, const float* q
   return len;
 }
 
+/* `kind` may carry HSDO_KEYS_BF16: the stored key is the bf16 rounding
+ * (RN-even) of the fp32 key, widened back to fp32 (bf16 collections). */
 static void gen_key_row(int kind, uint64_t kbase, int64_t row, int dim, float* out, int32_t* scratch) {
+  const int bf16 = (kind & HSDO_KEYS_BF16) != 0;
+  kind &= ~HSDO_KEYS_BF16;
   int64_t src = hsd_key_src_row(kind, row);
   if (kind == HSD_SYNTH_EXACT) {
     for (int c = 0; c < dim; ++c) out[c] = hsd_exact_val(hsd_hash_at(kbase, (uint64_t)src * (uint64_t)dim + c));
-    return;
+  } else {
+    int64_t ss = 0;
+    for (int c = 0; c < dim; ++c) {
+      scratch[c] = hsd_key_raw(kbase, src, dim, c);
+      ss += (int64_t)scratch[c] * scratch[c];
+    }
+    for (int c = 0; c < dim; ++c) out[c] = hsd_norm_val(scratch[c], ss);
   }
-  int64_t ss = 0;
-  for (int c = 0; c < dim; ++c) {
-    scratch[c] = hsd_key_raw(kbase, src, dim, c);
-    ss += (int64_t)scratch[c] * scratch[c];
-  }
-  for (int c = 0; c < dim; ++c) out[c] = hsd_norm_val(scratch[c], ss);
+  if (bf16)
+    for (int c = 0; c < dim; ++c) out[c] = hsd_bf16_val(hsd_bf16_bits(out[c]));
 }
 
 void hsdo_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, float* out) {

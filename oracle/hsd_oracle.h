@@ -45,6 +45,11 @@ int hsdo_search_topk_exact(const float* keys, int64_t n, int dim, const float* q
 int hsdo_search_synth(int kind, uint64_t db_seed, int64_t n, int dim, const float* queries, int B, int k,
                       double* scores, int64_t* ids, int threads);
 
+/* Key-storage flag OR-ed into `kind` of hsdo_search_synth / hsdo_gen_keys:
+ * the DB stores bf16 keys (RN-even rounding of the fp32 synthetic key), as a
+ * bf16 collection does (include/hsd/hsd_synth.h hsd_bf16_bits). */
+#define HSDO_KEYS_BF16 0x100
+
 /* Generate rows [row0, row0+n) of a synthetic DB / a query batch (fp32). */
 void hsdo_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, float* out);
 void hsdo_gen_queries(int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B, int dim,

@@ -136,6 +136,7 @@ def ref():
 
 # ---------------------------------------------------------------- helpers
 EXACT, REAL = 0, 1
+KEYS_BF16 = 0x100  # OR into `kind`: the DB stores bf16-rounded keys (hsd_oracle.h HSDO_KEYS_BF16)
 
 
 def gen_keys(kind: int, db_seed: int, row0: int, n: int, dim: int) -> np.ndarray:

@@ -26,6 +26,8 @@ LIB_PATH = os.path.join(_HERE, "libhsd_gpu.so")
 HSD_K_MAX = 32
 TOKENS_STRIDE = 32
 EXACT, REAL = 0, 1
+F32, BF16 = 0, 1  # hsd_dtype (key storage)
+_DTYPES = {"f32": F32, "fp32": F32, "float32": F32, F32: F32, "bf16": BF16, "bfloat16": BF16, BF16: BF16}
 
 
 # --------------------------------------------------------------------------- errors
@@ -141,6 +143,9 @@ def lib():
     sig = {
         "hsd_device_count": [C.POINTER(C.c_int)],
         "hsd_collection_create": [C.c_int, C.c_int, C.c_int64, C.POINTER(_vp)],
+        "hsd_collection_create_ex": [C.c_int, C.c_int, C.c_int64, C.c_int, C.POINTER(_vp)],
+        "hsd_collection_dtype": [_vp, C.POINTER(C.c_int)],
+        "hsd_collection_data": [_vp, C.POINTER(_vp), C.POINTER(_vp)],
         "hsd_collection_destroy": [_vp],
         "hsd_collection_size": [_vp, C.POINTER(C.c_int64)],
         "hsd_collection_dim": [_vp, C.POINTER(C.c_int)],
@@ -233,9 +238,13 @@ def _stream(stream=None):
 class Collection:
     """Device-resident task shard; replaces hsd::Collection (store.hpp:59-96)."""
 
-    def __init__(self, dim: int, capacity: int = 1, device: int = 0):
+    def __init__(self, dim: int, capacity: int = 1, device: int = 0, dtype="f32"):
+        """dtype: key storage, "f32" (default) or "bf16" (keys rounded once to bf16)."""
         self._h = C.c_void_p()
-        check(lib().hsd_collection_create(device, dim, capacity, C.byref(self._h)))
+        if dtype not in _DTYPES:
+            raise ConfigError(f"unknown key dtype {dtype!r}")
+        self.dtype = _DTYPES[dtype]
+        check(lib().hsd_collection_create_ex(device, dim, capacity, self.dtype, C.byref(self._h)))
         self.device = device
         self._dim = dim
 
@@ -287,12 +296,13 @@ class Collection:
             check(lib().hsd_collection_generate_rows(self._h, kind, db_seed, row0, n))
 
     def keys_view(self):
-        """(keys, tokens) torch views of the resident arrays."""
+        """(keys, tokens) torch views of the resident arrays (keys float32 or bfloat16)."""
         torch = _torch()
         kp, tp = C.c_void_p(), C.c_void_p()
-        check(lib().hsd_collection_keys(self._h, C.byref(kp), C.byref(tp)))
+        check(lib().hsd_collection_data(self._h, C.byref(kp), C.byref(tp)))
         n = self.size()
-        keys = _from_ptr(kp.value, (n, self._dim), torch.float32, self.device)
+        kt = torch.bfloat16 if self.dtype == BF16 else torch.float32
+        keys = _from_ptr(kp.value, (n, self._dim), kt, self.device)
         toks = _from_ptr(tp.value, (n, TOKENS_STRIDE), torch.uint8, self.device)
         return keys, toks
 
@@ -321,7 +331,8 @@ class Collection:
         return scores, ids
 
     def debug_sim_scores(self, queries, variant=1, stream=None):
-        """Approximate tcgen05 filter scores float32 [B, size] (diagnostics; variant 1 TF32, 3 3xTF32)."""
+        """Approximate tcgen05 filter scores float32 [B, size] (diagnostics; variant 1 = wide TF32/bf16
+        filter of the default path, 2 = 64-query TF32, 3 = 3xTF32)."""
         torch = _torch()
         q = queries.contiguous()
         out = torch.empty((q.shape[0], self.size()), dtype=torch.float32, device=q.device)
@@ -429,13 +440,16 @@ def _from_ptr(ptr, shape, dtype, device):
     n = int(np.prod(shape))
     if n == 0:
         return torch.empty(shape, dtype=dtype, device=f"cuda:{device}")
+    view_as = dtype
+    if dtype == torch.bfloat16:  # numpy has no bf16: map as int16, reinterpret in torch
+        dtype = torch.int16
     esz = torch.empty((), dtype=dtype).element_size()
 
     class _Arr:
         __cuda_array_interface__ = {"shape": (n,), "typestr": torch.empty((), dtype=dtype).numpy().dtype.str,
                                     "data": (ptr, False), "version": 3, "strides": (esz,)}
 
-    return torch.as_tensor(_Arr(), device=f"cuda:{device}").view(shape)
+    return torch.as_tensor(_Arr(), device=f"cuda:{device}").view(view_as).view(shape)
 
 
 # --------------------------------------------------------------------------- free functions
@@ -478,11 +492,12 @@ def quantize(actions, lo=-1.0, hi=1.0, k_bins=256, stream=None):
     return bins
 
 
-SIM_PATHS = {"auto": 0, "rows": 1, "tile": 2, "tc": 3, "tc3": 4}
+SIM_PATHS = {"auto": 0, "rows": 1, "tile": 2, "tc": 3, "tc3": 4, "tc1": 5}
 
 
 def set_sim_path(name: str) -> None:
-    """Similarity kernel override (ablations / tests): auto | rows | tile | tc | tc3."""
+    """Similarity kernel override (ablations / tests): auto | rows | tile | tc (wide TF32, default) | tc1 (64-query
+    TF32) | tc3 (3xTF32)."""
     check(lib().hsd_set_sim_path(SIM_PATHS[name]))
 
 

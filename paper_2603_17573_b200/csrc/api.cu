@@ -110,9 +110,10 @@ struct Scratch {
 struct hsd_collection {
   int device = 0;
   int dim = 0;
+  int dtype = HSD_DTYPE_F32;
   int64_t n = 0;
   int64_t cap = 0;
-  float* keys = nullptr;
+  void* keys = nullptr;  // fp32 or bf16 [cap][dim]
   uint8_t* tokens = nullptr;
   unsigned long long* maxnorm = nullptr;  // fp64 bits of max row norm
   std::mutex mu;
@@ -121,19 +122,21 @@ struct hsd_collection {
 
 namespace {
 
+size_t key_bytes(const hsd_collection* c) { return c->dtype == HSD_DTYPE_BF16 ? 2 : 4; }
+
 hsd_status ensure_capacity(hsd_collection* c, int64_t need) {
   if (need <= c->cap) return HSD_OK;
   int64_t ncap = std::max<int64_t>(need, c->cap * 2);
-  float* nk = nullptr;
+  void* nk = nullptr;
   uint8_t* nt = nullptr;
-  CU(cudaMalloc(&nk, (size_t)ncap * c->dim * sizeof(float)));
+  CU(cudaMalloc(&nk, (size_t)ncap * c->dim * key_bytes(c)));
   cudaError_t e = cudaMalloc(&nt, (size_t)ncap * HSD_TOKENS_STRIDE);
   if (e != cudaSuccess) {
     cudaFree(nk);
     return cuda_fail(e, "cudaMalloc(tokens)");
   }
   if (c->n > 0) {
-    CU(cudaMemcpy(nk, c->keys, (size_t)c->n * c->dim * sizeof(float), cudaMemcpyDeviceToDevice));
+    CU(cudaMemcpy(nk, c->keys, (size_t)c->n * c->dim * key_bytes(c), cudaMemcpyDeviceToDevice));
     CU(cudaMemcpy(nt, c->tokens, (size_t)c->n * HSD_TOKENS_STRIDE, cudaMemcpyDeviceToDevice));
   }
   cudaFree(c->keys);
@@ -166,12 +169,14 @@ hsd_status get_scratch(hsd_collection* c, cudaStream_t s, size_t partial_bytes, 
   return HSD_OK;
 }
 
-constexpr int kSlab = 64;  // queries per similarity launch
+constexpr int kSlab = 64;  // queries per similarity launch of the 64-wide paths
 
-// Similarity path per query slab: SIMT GEMV for tiny batches (HBM-bound on
-// CUDA cores), the tcgen05 TF32 filter otherwise.  HSD_SIM_PATH=rows|tile|tc|tc3
-// or hsd_set_sim_path override it (tests and ablations; tc3 = 3xTF32 filter).
-enum { kPathAuto = 0, kPathRows = 1, kPathTile = 2, kPathTc = 3, kPathTc3 = 4 };
+// Similarity path per query pass: SIMT GEMV for tiny batches on fp32
+// collections (HBM-bound on CUDA cores), the wide tcgen05 filter otherwise
+// (TF32 over fp32 keys, bf16 over bf16 keys; up to 256 queries per pass).
+// HSD_SIM_PATH=rows|tile|tc|tc1|tc3 or hsd_set_sim_path override it for fp32
+// collections (tests and ablations: tc1 = 64-query TF32 kernel, tc3 = 3xTF32).
+enum { kPathAuto = 0, kPathRows = 1, kPathTile = 2, kPathTc = 3, kPathTc3 = 4, kPathTc1 = 5 };
 int g_path = -1;
 int path_override() {
   int& v = g_path;
@@ -182,17 +187,20 @@ int path_override() {
     if (e && !strcmp(e, "tile")) v = kPathTile;
     if (e && !strcmp(e, "tc")) v = kPathTc;
     if (e && !strcmp(e, "tc3")) v = kPathTc3;
+    if (e && !strcmp(e, "tc1")) v = kPathTc1;
   }
   return v;
 }
-int choose_path(int Bs) {
+int choose_path(int B, int dtype) {
+  if (dtype == HSD_DTYPE_BF16) return kPathTc;  // the only bf16 similarity kernel
   const int o = path_override();
-  if (o == kPathRows) return Bs <= 8 ? kPathRows : kPathTile;
-  if (o == kPathTile) return Bs <= 8 ? kPathRows : kPathTile;  // launch_sim picks rows for B <= 8
-  if (o == kPathTc || o == kPathTc3) return o;
-  return Bs <= 4 ? kPathRows : kPathTc;
+  if (o == kPathRows) return B <= 8 ? kPathRows : kPathTile;
+  if (o == kPathTile) return B <= 8 ? kPathRows : kPathTile;  // launch_sim picks rows for B <= 8
+  if (o == kPathTc || o == kPathTc3 || o == kPathTc1) return o;
+  return B <= 4 ? kPathRows : kPathTc;
 }
-bool is_tc(int p) { return p == kPathTc || p == kPathTc3; }
+bool is_tc(int p) { return p == kPathTc || p == kPathTc3 || p == kPathTc1; }
+int pass_width(int p) { return p == kPathTc ? hsd::sim_wide_max_batch() : kSlab; }
 
 // Optional stage events (engine timing): marks[i] is recorded after stage i.
 struct StageMarks {
@@ -222,32 +230,45 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   // (the engine's kinematics); the persistent tcgen05 kernel sizes its grid to
   // the rest so neither waits for the other's CTAs to retire.
   const int nsm = std::max(1, num_sms(c->device) - std::max(0, reserve_sms));
-  const int Bs0 = std::min(B, kSlab);
-  const int path0 = choose_path(Bs0);
-  const int lists0 = is_tc(path0) ? hsd::sim_tc_lists(rows, nsm) : hsd::sim_plan(Bs0, rows, c->dim, nsm).lists;
+  const int path = choose_path(B, c->dtype);
+  const int W = pass_width(path);
+  const int Bs0 = std::min(B, W);
+  const int lists0 = is_tc(path) ? hsd::sim_tc_lists(rows, nsm) : hsd::sim_plan(Bs0, rows, c->dim, nsm).lists;
+  const size_t qscratch = path == kPathTc    ? hsd::sim_wide_scratch_bytes(c->dim)
+                          : path == kPathTc1 ? hsd::sim_tc1_scratch_bytes(c->dim)
+                          : path == kPathTc3 ? hsd::sim_tc_scratch_bytes(c->dim)
+                                             : 0;
   Scratch* sc = nullptr;
-  st = get_scratch(c, s, (size_t)std::max(lists0, 4 * nsm) * Bs0 * hsd::dev::kCandLocal * sizeof(uint64_t),
-                   is_tc(path0) ? hsd::sim_tc_scratch_bytes(c->dim) : 0, &sc);
+  st = get_scratch(c, s, (size_t)std::max(lists0, 4 * nsm) * Bs0 * hsd::dev::kCandLocal * sizeof(uint64_t), qscratch,
+                   &sc);
   if (st != HSD_OK) return st;
   CU(cudaMemsetAsync(sc->overflow, 0, sizeof(int), s));
-  for (int b0 = 0; b0 < B; b0 += kSlab) {
-    const int Bs = std::min(kSlab, B - b0);
-    const int path = choose_path(Bs);
+  for (int b0 = 0; b0 < B; b0 += W) {
+    const int Bs = std::min(W, B - b0);
+    // the SIMT paths pick rows vs tile per pass; the tcgen05 paths are fixed
+    const int p = is_tc(path) ? path : choose_path(Bs, c->dtype);
     hsd::SimPlan plan = hsd::sim_plan(Bs, rows, c->dim, nsm);
     const float* q = queries + (size_t)b0 * c->dim;
-    if (path == kPathTc) {
+    if (p == kPathTc) {
+      plan.lists = hsd::sim_tc_lists(rows, nsm);
+      plan.gamma = hsd::sim_wide_gamma(c->dim, c->dtype);
+      CU(hsd::launch_sim_wide(c->keys, c->dtype, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial,
+                              nullptr, s));
+    } else if (p == kPathTc1) {
       plan.lists = hsd::sim_tc_lists(rows, nsm);
       plan.gamma = hsd::sim_tc1_gamma(c->dim);
-      CU(hsd::launch_sim_tc1(c->keys, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial, nullptr, s));
-    } else if (path == kPathTc3) {
+      CU(hsd::launch_sim_tc1((const float*)c->keys, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial,
+                             nullptr, s));
+    } else if (p == kPathTc3) {
       plan.lists = hsd::sim_tc_lists(rows, nsm);
       plan.gamma = hsd::sim_tc_gamma(c->dim);
-      CU(hsd::launch_sim_tc(c->keys, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial, nullptr, s));
+      CU(hsd::launch_sim_tc((const float*)c->keys, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial,
+                            nullptr, s));
     } else {
-      CU(hsd::launch_sim(c->keys, rb, re, c->dim, q, Bs, plan, sc->partial, s));
+      CU(hsd::launch_sim((const float*)c->keys, rb, re, c->dim, q, Bs, plan, sc->partial, s));
     }
-    if (marks && marks->after_sim && b0 + kSlab >= B) CU(cudaEventRecord(marks->after_sim, s));
-    CU(hsd::launch_select(sc->partial, plan.lists, Bs, k, c->keys, c->dim, q, c->maxnorm, plan.gamma,
+    if (marks && marks->after_sim && b0 + W >= B) CU(cudaEventRecord(marks->after_sim, s));
+    CU(hsd::launch_select(sc->partial, plan.lists, Bs, k, c->keys, c->dtype, c->dim, q, c->maxnorm, plan.gamma,
                           scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->overflow, s));
   }
   if (marks && marks->after_select) CU(cudaEventRecord(marks->after_select, s));
@@ -278,15 +299,23 @@ hsd_status hsd_device_count(int* n) {
 }
 
 hsd_status hsd_collection_create(int device, int dim, int64_t capacity, hsd_collection** out) {
+  return hsd_collection_create_ex(device, dim, capacity, HSD_DTYPE_F32, out);
+}
+
+hsd_status hsd_collection_create_ex(int device, int dim, int64_t capacity, int dtype, hsd_collection** out) {
   if (!out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   *out = nullptr;
   if (dim < 1) return fail(HSD_ERR_CONFIG, "collection dim must be >= 1");  // store.cpp:37
+  if (dtype != HSD_DTYPE_F32 && dtype != HSD_DTYPE_BF16) return fail(HSD_ERR_CONFIG, "unknown key dtype %d", dtype);
   if (dim % 4 != 0) return fail(HSD_ERR_CONFIG, "dim must be a multiple of 4 (128-bit loads), got %d", dim);
+  if (dtype == HSD_DTYPE_BF16 && dim % 8 != 0)
+    return fail(HSD_ERR_CONFIG, "bf16 collections need dim a multiple of 8 (16-B rows), got %d", dim);
   hsd_status st = require_device(device);
   if (st != HSD_OK) return st;
   auto* c = new hsd_collection();
   c->device = device;
   c->dim = dim;
+  c->dtype = dtype;
   cudaError_t e = cudaMalloc(&c->maxnorm, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->maxnorm, 0, sizeof(unsigned long long));
   if (e != cudaSuccess) {
@@ -337,6 +366,20 @@ hsd_status hsd_collection_device(const hsd_collection* c, int* device) {
 
 hsd_status hsd_collection_keys(const hsd_collection* c, const float** keys, const uint8_t** tokens) {
   if (!c) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (keys && c->dtype != HSD_DTYPE_F32) return fail(HSD_ERR_INVALID_INPUT, "fp32 key view of a bf16 collection");
+  if (keys) *keys = (const float*)c->keys;
+  if (tokens) *tokens = c->tokens;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_dtype(const hsd_collection* c, int* dtype) {
+  if (!c || !dtype) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *dtype = c->dtype;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_data(const hsd_collection* c, const void** keys, const uint8_t** tokens) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   if (keys) *keys = c->keys;
   if (tokens) *tokens = c->tokens;
   return HSD_OK;
@@ -369,8 +412,20 @@ hsd_status hsd_collection_insert(hsd_collection* c, const float* emb, const doub
   cudaFree(dbad);
   if (e != cudaSuccess) return cuda_fail(e, "insert: quantize payload");
   if (bad) return fail(HSD_ERR_INVALID_INPUT, "non-finite action value in payload");  // actions.cpp:38-40
-  CU(cudaMemcpy(c->keys + (size_t)c->n * c->dim, emb, (size_t)n * c->dim * sizeof(float), cudaMemcpyHostToDevice));
-  CU(hsd::launch_row_norms(c->keys, c->n, n, c->dim, c->maxnorm, 0));
+  if (c->dtype == HSD_DTYPE_BF16) {
+    float* tmp = nullptr;
+    CU(cudaMalloc(&tmp, (size_t)n * c->dim * sizeof(float)));
+    e = cudaMemcpy(tmp, emb, (size_t)n * c->dim * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = hsd::launch_to_bf16(tmp, n * c->dim, (uint16_t*)c->keys + (size_t)c->n * c->dim, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaFree(tmp);
+    if (e != cudaSuccess) return cuda_fail(e, "insert: bf16 keys");
+  } else {
+    CU(cudaMemcpy((float*)c->keys + (size_t)c->n * c->dim, emb, (size_t)n * c->dim * sizeof(float),
+                  cudaMemcpyHostToDevice));
+  }
+  CU(hsd::launch_row_norms(c->keys, c->dtype, c->n, n, c->dim, c->maxnorm, 0));
   CU(cudaDeviceSynchronize());
   c->n += n;
   return HSD_OK;
@@ -391,8 +446,8 @@ hsd_status hsd_collection_generate_rows(hsd_collection* c, int kind, uint64_t db
   if (st != HSD_OK) return st;
   st = ensure_capacity(c, c->n + n);
   if (st != HSD_OK) return st;
-  CU(hsd::launch_gen_keys(kind, db_seed, row0, n, c->dim, c->keys + (size_t)c->n * c->dim,
-                          c->tokens + (size_t)c->n * HSD_TOKENS_STRIDE, c->maxnorm, 0));
+  CU(hsd::launch_gen_keys(kind, db_seed, row0, n, c->dim, (uint8_t*)c->keys + (size_t)c->n * c->dim * key_bytes(c),
+                          c->dtype, c->tokens + (size_t)c->n * HSD_TOKENS_STRIDE, c->maxnorm, 0));
   CU(cudaDeviceSynchronize());
   c->n += n;
   return HSD_OK;
@@ -412,8 +467,9 @@ hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B,
 }
 
 hsd_status hsd_set_sim_path(int path) {
-  if (path < 0 || path > 4)
-    return fail(HSD_ERR_INVALID_INPUT, "path must be 0 auto, 1 rows, 2 tile, 3 tc (TF32), 4 tc3 (3xTF32)");
+  if (path < 0 || path > 5)
+    return fail(HSD_ERR_INVALID_INPUT,
+                "path must be 0 auto, 1 rows, 2 tile, 3 tc (wide TF32), 4 tc3 (3xTF32), 5 tc1 (64-query TF32)");
   g_path = path;
   return HSD_OK;
 }
@@ -421,22 +477,28 @@ hsd_status hsd_set_sim_path(int path) {
 hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
                                 void* stream) {
   if (!c || !queries || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
-  if (B < 1 || B > kSlab) return fail(HSD_ERR_INVALID_INPUT, "debug dump supports 1 <= B <= %d", kSlab);
-  if (variant != 1 && variant != 3) return fail(HSD_ERR_INVALID_INPUT, "variant must be 1 (TF32) or 3 (3xTF32)");
+  if (variant != 1 && variant != 2 && variant != 3)
+    return fail(HSD_ERR_INVALID_INPUT, "variant must be 1 (wide TF32/bf16), 2 (64-query TF32) or 3 (3xTF32)");
+  const int maxB = variant == 1 ? hsd::sim_wide_max_batch() : kSlab;
+  if (B < 1 || B > maxB) return fail(HSD_ERR_INVALID_INPUT, "debug dump supports 1 <= B <= %d", maxB);
+  if (variant != 1 && c->dtype != HSD_DTYPE_F32) return fail(HSD_ERR_INVALID_INPUT, "variant needs fp32 keys");
   hsd_status st = require_device(c->device);
   if (st != HSD_OK) return st;
   if (c->n == 0) return HSD_OK;
   const int lists = hsd::sim_tc_lists(c->n, num_sms(c->device));
   Scratch* sc = nullptr;
-  st = get_scratch(c, (cudaStream_t)stream, (size_t)lists * B * hsd::dev::kCandLocal * 8, hsd::sim_tc_scratch_bytes(c->dim),
-                   &sc);
+  st = get_scratch(c, (cudaStream_t)stream, (size_t)lists * B * hsd::dev::kCandLocal * 8,
+                   std::max(hsd::sim_tc_scratch_bytes(c->dim), hsd::sim_wide_scratch_bytes(c->dim)), &sc);
   if (st != HSD_OK) return st;
   if (variant == 3)
-    CU(hsd::launch_sim_tc(c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial, out,
-                          (cudaStream_t)stream));
+    CU(hsd::launch_sim_tc((const float*)c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial,
+                          out, (cudaStream_t)stream));
+  else if (variant == 2)
+    CU(hsd::launch_sim_tc1((const float*)c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial,
+                           out, (cudaStream_t)stream));
   else
-    CU(hsd::launch_sim_tc1(c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial, out,
-                           (cudaStream_t)stream));
+    CU(hsd::launch_sim_wide(c->keys, c->dtype, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial, out,
+                            (cudaStream_t)stream));
   return HSD_OK;
 }
 

@@ -14,6 +14,7 @@
 //   4. order (score desc, id asc) (store.cpp:67-70), truncate to k (:71).
 // K3: k-way merge of G ranks' exact top-k lists (multi-GPU all-gather result).
 #include "common.cuh"
+#include "hsd/hsd_synth.h"
 #include "kernels.h"
 
 namespace hsd {
@@ -35,10 +36,13 @@ constexpr int kRowsFloats = 2 * 256 * (64 + 4);  // >= 2 * 32 * (512 + 4)
 static_assert(kRowsFloats >= 2 * 32 * (512 + 4), "staging ring too small");
 constexpr int kMaxW = 512;
 
+__device__ __forceinline__ double widen(float x) { return (double)x; }
+__device__ __forceinline__ double widen(uint16_t b) { return (double)hsd_bf16_val(b); }  // bf16 key -> exact fp64
+
 struct SelectSmem {
   uint64_t top[kWarps][32];
   uint64_t pool[kPool];
-  __align__(16) float rows[kRowsFloats];
+  __align__(16) float rows[kRowsFloats];  // staging ring, reinterpreted as KT
   __align__(16) double q[2][kMaxW];
   double exact[kCandMax];
   uint32_t id[kCandMax];
@@ -47,8 +51,9 @@ struct SelectSmem {
   int over;
 };
 
+template <typename KT>  // float (fp32 collection) or uint16_t (bf16 bits)
 __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __restrict__ partial, int lists, int B, int k,
-                                                          const float* __restrict__ keys, int dim,
+                                                          const KT* __restrict__ keys, int dim,
                                                           const float* __restrict__ queries,
                                                           const unsigned long long* __restrict__ maxnorm_bits,
                                                           double gamma, double* __restrict__ scores,
@@ -133,23 +138,27 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
   //    through a double-buffered cp.async ring of wide column chunks (the
   //    next chunk lands while this one is consumed); each thread then runs
   //    the sequential fp64 chain of its candidate out of shared memory.
-  // widest chunk whose double buffer fits: fewer chunk rounds (syncs, waits)
-  const int W = 2 * n * (kMaxW + 4) <= kRowsFloats ? kMaxW
-                : 2 * n * (256 + 4) <= kRowsFloats ? 256
-                : 2 * n * (128 + 4) <= kRowsFloats ? 128
-                                                   : 64;
-  const int stride = W + 4;
+  // widest chunk (in elements) whose double buffer fits; rows are padded by
+  // 16 B (spreads them over banks, keeps cp.async destinations aligned)
+  constexpr int kPad = 16 / (int)sizeof(KT);
+  constexpr int kRingElems = kRowsFloats * 4 / (int)sizeof(KT);
+  const int W = 2 * n * (kMaxW + kPad) <= kRingElems ? kMaxW
+                : 2 * n * (256 + kPad) <= kRingElems ? 256
+                : 2 * n * (128 + kPad) <= kRingElems ? 128
+                                                     : 64;
+  const int stride = W + kPad;
   const int nchunk = (dim + W - 1) / W;
-  const int v4 = W / 4;  // 16-B copies per row chunk
+  const int v16 = W / kPad;  // 16-B copies per row chunk
+  KT* ring = reinterpret_cast<KT*>(S.rows);
   auto issue = [&](int ch) {
-    float* dst = S.rows + (ch & 1) * n * stride;
+    KT* dst = ring + (ch & 1) * n * stride;
     const int c0 = ch * W;
-    for (int i = tid; i < n * v4; i += kThreads) {
-      const int c = i / v4, j4 = i - c * v4;
-      const int col = c0 + j4 * 4;
-      const float* src = keys + (size_t)S.id[c] * dim + col;
-      const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + c * stride + j4 * 4);
-      const int bytes = col < dim ? 16 : 0;  // dim % 4 == 0; zero-fill past the end
+    for (int i = tid; i < n * v16; i += kThreads) {
+      const int c = i / v16, j16 = i - c * v16;
+      const int col = c0 + j16 * kPad;
+      const KT* src = keys + (size_t)S.id[c] * dim + col;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + c * stride + j16 * kPad);
+      const int bytes = col < dim ? 16 : 0;  // dim is a multiple of kPad; zero-fill past the end
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
     }
     for (int j = tid; j < W; j += kThreads) S.q[ch & 1][j] = c0 + j < dim ? (double)qrow[c0 + j] : 0.0;
@@ -167,13 +176,13 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
     __syncthreads();
     const int w = dim - ch * W < W ? dim - ch * W : W;
     if (tid < n) {
-      // acc = fl(acc + fl(q*k)) of store.cpp:32; the fp32 x fp32 product is
-      // exact in fp64, so the fused form fl(acc + q*k) is bit-identical and
-      // leaves one dependent op per element on the chain.
-      const float* r = S.rows + (ch & 1) * n * stride + tid * stride;
+      // acc = fl(acc + fl(q*k)) of store.cpp:32; the fp32 x fp32 (or fp32 x
+      // bf16) product is exact in fp64, so the fused form fl(acc + q*k) is
+      // bit-identical and leaves one dependent op per element on the chain.
+      const KT* r = ring + (ch & 1) * n * stride + tid * stride;
       const double* qc = S.q[ch & 1];
 #pragma unroll 16
-      for (int j = 0; j < w; ++j) acc = __fma_rn(qc[j], (double)r[j], acc);
+      for (int j = 0; j < w; ++j) acc = __fma_rn(qc[j], widen(r[j]), acc);
     }
     __syncthreads();
   }
@@ -246,15 +255,23 @@ __global__ void merge_ranks_kernel(const double* __restrict__ gs, const int32_t*
 
 }  // namespace
 
-cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const float* keys, int dim,
+cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const void* keys, int key_dtype, int dim,
                           const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
                           int32_t* ids, int* overflow, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   const size_t smem = sizeof(SelectSmem);
-  cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  select_kernel<<<B, kThreads, smem, s>>>(partial, lists, B, k, keys, dim, queries, maxnorm_bits, gamma, scores, ids,
-                                          overflow);
+  if (key_dtype == HSD_DTYPE_BF16) {
+    if (dim % 8) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(select_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    select_kernel<uint16_t><<<B, kThreads, smem, s>>>(partial, lists, B, k, (const uint16_t*)keys, dim, queries,
+                                                      maxnorm_bits, gamma, scores, ids, overflow);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(select_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    select_kernel<float><<<B, kThreads, smem, s>>>(partial, lists, B, k, (const float*)keys, dim, queries,
+                                                   maxnorm_bits, gamma, scores, ids, overflow);
+  }
   return cudaGetLastError();
 }
 

@@ -1,0 +1,410 @@
+// k_sim_wide.cu — K1 (tensor cores, default path for B > 4): similarity FILTER
+// on tcgen05 + TMA for up to 256 queries per pass, fused with the per-CTA
+// top-32 candidate filter.  Two operand types share the kernel:
+//
+//   TF32  fp32 collections: keys and queries are read as TF32 straight from
+//         the fp32 tiles (kind::tf32, 32 fp32 = one 128-B atom per k-chunk);
+//   BF16  bf16 collections: keys are stored bf16, queries rounded to bf16 at
+//         padding time (kind::f16, 64 bf16 per k-chunk).
+//
+// Either way the tensor cores only FILTER: |S - S~| <= gamma * sum|k_i q_i|
+// (sim_wide_gamma) and the select kernel (k_select.cu) rescores every record
+// within 2E of the k-th best with the reference's sequential fp64 dot
+// (store.cpp:29-34) against the STORED keys, so ids and scores are
+// bit-identical to the reference over the stored (fp32 or bf16) DB.
+//
+// Query batch width: NS slabs of 64 queries form one UMMA N = 64*NS (<= 256)
+// so a key tile is read from HBM once per pass for up to 256 queries:
+//
+//   NS  N    key blocks per accumulator   TMEM columns per buffer
+//   1   64   4                            256
+//   2   128  2                            256
+//   4   256  1                            256
+//
+// Per SM (persistent CTA over a contiguous range of 128-key blocks):
+//   warp 0      TMA producer: key tiles 128 rows x 128 B (16 KB, SWIZZLE_128B)
+//   warp 3      TMA producer: query tiles 64*NS rows x 128 B (L2-resident)
+//   warp 1      tcgen05.mma issuer: per key tile 4 x (M128 N64NS K) into the
+//               accumulator of its key block
+//   warp 2      TMEM allocator (512 columns = 2 buffers x 256)
+//   warps 4-11  epilogue: tcgen05.ld (x16) -> staging tile of 32 queries ->
+//               ballot filter against the register-resident per-query top-32
+// Accumulators are double-buffered, so the epilogue of group g overlaps the
+// MMAs of group g+1.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+#include "hsd/hsd_synth.h"
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace hsd {
+namespace {
+
+using namespace sm100;
+using dev::cand_key;
+using dev::kCandLocal;
+using dev::kEmpty;
+
+constexpr int kBM = 128;              // keys per block (UMMA M)
+constexpr int kKeyTile = kBM * 128;   // 16 KB: 128 rows x one 128-B swizzle atom
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 32 * (4 + kEpiWarps);
+constexpr int kTmemCols = 512;
+constexpr int kStgQ = 32;             // queries staged per epilogue round
+constexpr int kStg = kStgQ + 1;
+
+template <int NS, int GB>
+struct WideCfg {
+  static constexpr int kBQ = 64 * NS;                 // UMMA N
+  static constexpr int kGB = GB;                      // key blocks per accumulator buffer (query-tile reuse)
+  static constexpr int kBufCols = GB * kBQ;           // TMEM columns per accumulator buffer
+  static constexpr int kBufs = kTmemCols / kBufCols;  // 2 = double-buffered, 1 = single
+  static_assert(kBufs == 1 || kBufs == 2, "accumulators must fill 256 or 512 TMEM columns");
+  static constexpr int kQTile = kBQ * 128;            // bytes per query k-chunk tile
+  static constexpr int kKStages = NS == 4 ? 7 : 9;
+  static constexpr int kQStages = NS == 1 ? 4 : 3;
+  static constexpr int kMyQ = kBQ / kEpiWarps;        // queries owned per epilogue lane-group
+};
+
+template <int NS, int GB>
+struct __align__(1024) WideSmem {
+  using Cfg = WideCfg<NS, GB>;
+  uint8_t kbuf[Cfg::kKStages][kKeyTile];
+  uint8_t qbuf[Cfg::kQStages][Cfg::kQTile];
+  float stg[kBM * kStg];
+  uint64_t k_full[Cfg::kKStages], k_empty[Cfg::kKStages];
+  uint64_t q_full[Cfg::kQStages], q_empty[Cfg::kQStages];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+};
+
+template <bool kBf16, int NS, int GB, bool kDump>
+__global__ void __launch_bounds__(kThreads, 1)
+    sim_wide_kernel(const __grid_constant__ CUtensorMap keys_map, const __grid_constant__ CUtensorMap q_map,
+                    int64_t row_begin, int64_t row_end, int dim, int B, int64_t blocks_per_cta,
+                    uint64_t* __restrict__ partial, float* __restrict__ dump) {
+  using Cfg = WideCfg<NS, GB>;
+  constexpr int kBQ = Cfg::kBQ, kGB = Cfg::kGB, kKS = Cfg::kKStages, kQS = Cfg::kQStages;
+  constexpr int kBufCols = Cfg::kBufCols, kBufs = Cfg::kBufs;
+  constexpr int kBK = kBf16 ? 64 : 32;  // elements per 128-B k-chunk
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  WideSmem<NS, GB>& S = *reinterpret_cast<WideSmem<NS, GB>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
+  const int64_t blk0 = (int64_t)blockIdx.x * blocks_per_cta;
+  const int64_t blk1 = std::min<int64_t>(blk0 + blocks_per_cta, n_blocks);
+  const int nk = (dim + kBK - 1) / kBK;
+  // Each CTA walks the k-chunks starting at its own offset, so the 148 CTAs do
+  // not all request the same (L2-resident) query tile at the same moment; the
+  // filter's error bound does not depend on the accumulation order.
+  const int kc0 = (int)(((int64_t)blockIdx.x * nk) / gridDim.x);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kKS; ++i) {
+      mbar_init(&S.k_full[i], 1);
+      mbar_init(&S.k_empty[i], 1);
+    }
+    for (int i = 0; i < kQS; ++i) {
+      mbar_init(&S.q_full[i], 1);
+      mbar_init(&S.q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S.acc_full[i], 1);
+      mbar_init(&S.acc_empty[i], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    // ======================= key stream (HBM)
+    if (lane == 0 && blk0 < blk1) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&keys_map) : "memory");
+      const uint64_t pol = policy_evict_first();
+      int ks = 0;
+      uint32_t kph = 0;
+      for (int64_t g0 = blk0; g0 < blk1; g0 += kGB) {
+        const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
+        for (int kc = 0; kc < nk; ++kc)
+          for (int m = 0; m < gb; ++m) {
+            mbar_wait(&S.k_empty[ks], kph ^ 1);
+            mbar_expect_tx(&S.k_full[ks], kKeyTile);
+            const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
+            tma_load_2d(&S.kbuf[ks][0], &keys_map, &S.k_full[ks], c * kBK, (int)(row_begin + (g0 + m) * kBM), pol);
+            if (++ks == kKS) {
+              ks = 0;
+              kph ^= 1;
+            }
+          }
+      }
+    }
+  } else if (warp == 3) {
+    // ======================= query tiles (L2-resident, reused by gb key tiles)
+    if (lane == 0 && blk0 < blk1) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&q_map) : "memory");
+      const uint64_t pol = policy_evict_last();
+      int qs = 0;
+      uint32_t qph = 0;
+      for (int64_t g0 = blk0; g0 < blk1; g0 += kGB)
+        for (int kc = 0; kc < nk; ++kc) {
+          mbar_wait(&S.q_empty[qs], qph ^ 1);
+          mbar_expect_tx(&S.q_full[qs], Cfg::kQTile);
+          const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
+          tma_load_2d(&S.qbuf[qs][0], &q_map, &S.q_full[qs], c * kBK, 0, pol);
+          if (++qs == kQS) {
+            qs = 0;
+            qph ^= 1;
+          }
+        }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (whole warp; one lane elected in the asm)
+    constexpr uint32_t idesc = kBf16 ? bf16_idesc(kBM, kBQ) : tf32_idesc(kBM, kBQ);
+    const uint64_t adesc0 = sw128_desc(&S.kbuf[0][0]);
+    const uint64_t bdesc0 = sw128_desc(&S.qbuf[0][0]);
+    int ks = 0, qs = 0;
+    uint32_t kph = 0, qph = 0;
+    int gi = 0;
+    for (int64_t g0 = blk0; g0 < blk1; g0 += kGB, ++gi) {
+      const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
+      const int buf = gi % kBufs;
+      if (gi >= kBufs) {  // the epilogue must have drained this buffer
+        mbar_wait(&S.acc_empty[buf], ((gi / kBufs) - 1) & 1);
+        tc_fence_after();
+      }
+      for (int kc = 0; kc < nk; ++kc) {
+        mbar_wait(&S.q_full[qs], qph);
+        const uint64_t bdesc = bdesc0 + (uint64_t)(qs * (Cfg::kQTile >> 4));
+        for (int m = 0; m < gb; ++m) {
+          mbar_wait(&S.k_full[ks], kph);
+          tc_fence_after();
+          const uint64_t adesc = adesc0 + (uint64_t)(ks * (kKeyTile >> 4));
+          const uint32_t d = tmem + buf * kBufCols + m * kBQ;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {  // +32 B per UMMA K-step (8 tf32 / 16 bf16)
+            if (kBf16)
+              mma_ss_f16(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
+            else
+              mma_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&S.k_empty[ks]);
+          if (++ks == kKS) {
+            ks = 0;
+            kph ^= 1;
+          }
+        }
+        tc_commit(&S.q_empty[qs]);
+        if (++qs == kQS) {
+          qs = 0;
+          qph ^= 1;
+        }
+      }
+      tc_commit(&S.acc_full[buf]);
+    }
+  } else if (warp >= 4) {
+    // ======================= epilogue (8 warps)
+    const int ew = warp - 4;        // 0..7
+    const int quad = warp & 3;      // TMEM lane quadrant this warp may access
+    const int half = ew >> 2;       // which 16 of the 32 staged columns it loads
+    const int r = quad * 32 + lane; // key row of the block this thread loads
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    // query q = j * 32 + ew * 4 + i  (j: staging round, i < 4) -> top[j * 4 + i]
+    uint64_t top[Cfg::kMyQ];
+#pragma unroll
+    for (int i = 0; i < Cfg::kMyQ; ++i) top[i] = kEmpty;
+    int gi = 0;
+    for (int64_t g0 = blk0; g0 < blk1; g0 += kGB, ++gi) {
+      const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
+      const int buf = gi % kBufs;
+      mbar_wait(&S.acc_full[buf], (gi / kBufs) & 1);
+      tc_fence_after();
+      for (int m = 0; m < gb; ++m) {
+        const int64_t base = row_begin + (g0 + m) * kBM;
+#pragma unroll
+        for (int j = 0; j < kBQ / kStgQ; ++j) {
+          uint32_t acc[16];
+          TMEM_LD16(tmem + lane_addr + buf * kBufCols + m * kBQ + j * kStgQ + half * 16, acc);
+          tmem_ld_wait();
+          if (m == gb - 1 && j == kBQ / kStgQ - 1) {  // buffer drained: MMAs of group gi+kBufs may reuse it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.acc_empty[buf]);
+          }
+          if constexpr (kDump) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              const int q = j * kStgQ + half * 16 + t;
+              if (base + r < row_end && q < B)
+                dump[(size_t)q * (row_end - row_begin) + (base + r - row_begin)] = __uint_as_float(acc[t]);
+            }
+          } else {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) S.stg[r * kStg + half * 16 + t] = __uint_as_float(acc[t]);
+            named_sync(1, 32 * kEpiWarps);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int ql = ew * 4 + i;
+              if (j * kStgQ + ql < B) {
+                uint64_t& tp = top[j * 4 + i];
+                uint64_t key[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int rr = lane + 32 * u;
+                  key[u] = base + rr < row_end ? cand_key(S.stg[rr * kStg + ql], (uint32_t)(base + rr)) : kEmpty;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  uint32_t mask = __ballot_sync(0xffffffffu, key[u] < dev::shfl_u64(tp, 31));
+                  while (mask) {
+                    const int src = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const uint64_t x = dev::shfl_u64(key[u], src);
+                    const int pos = __popc(__ballot_sync(0xffffffffu, tp < x));
+                    if (pos < 32) {
+                      const uint64_t up = dev::shfl_u64(tp, (lane + 31) & 31);
+                      tp = lane < pos ? tp : (lane == pos ? x : up);
+                    }
+                  }
+                }
+              }
+            }
+            named_sync(1, 32 * kEpiWarps);
+          }
+        }
+      }
+    }
+    if (!kDump) {
+#pragma unroll
+      for (int j = 0; j < kBQ / kStgQ; ++j)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int q = j * kStgQ + ew * 4 + i;
+          if (q < B) partial[((size_t)blockIdx.x * B + q) * kCandLocal + lane] = top[j * 4 + i];
+        }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// Zero-padded copy of the query slab to `rows` rows (the TMA box); bf16 mode
+// rounds to bf16 (RN-even, hsd_bf16_bits) on the way.
+__global__ void pad_queries_f32_kernel(const float* __restrict__ q, int B, int dim, float* __restrict__ out) {
+  const int row = blockIdx.x;
+  for (int c = threadIdx.x; c < dim; c += blockDim.x) out[(size_t)row * dim + c] = row < B ? q[(size_t)row * dim + c] : 0.f;
+}
+__global__ void pad_queries_bf16_kernel(const float* __restrict__ q, int B, int dim, uint16_t* __restrict__ out) {
+  const int row = blockIdx.x;
+  for (int c = threadIdx.x; c < dim; c += blockDim.x)
+    out[(size_t)row * dim + c] = row < B ? hsd_bf16_bits(q[(size_t)row * dim + c]) : (uint16_t)0;
+}
+
+template <bool kBf16, int NS, int GB, bool kDump>
+cudaError_t launch_ns(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, int64_t re, int dim, int B,
+                      int lists, int64_t per, uint64_t* partial, float* dump, cudaStream_t s) {
+  const size_t smem = sizeof(WideSmem<NS, GB>) + 1024;
+  auto kern = sim_wide_kernel<kBf16, NS, GB, kDump>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<lists, kThreads, smem, s>>>(km, qm, rb, re, dim, B, per, partial, dump);
+  return cudaGetLastError();
+}
+
+// Accumulator layout per NS: "db" = double-buffered (256 columns per buffer;
+// the epilogue of one group overlaps the MMAs of the next), "max" = one
+// 512-column buffer holding twice the key blocks (each query tile feeds twice
+// as many key tiles; the MMAs wait for the epilogue once per group).
+// HSD_WIDE_ACC=db|max overrides the default for ablations.
+int wide_acc_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HSD_WIDE_ACC");
+    v = (e && !strcmp(e, "max")) ? 1 : 0;  // default: double-buffered (measured faster at NS = 2 and 4)
+  }
+  return v;
+}
+
+template <bool kBf16, bool kDump>
+cudaError_t launch_dispatch(int NS, const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, int64_t re, int dim,
+                            int B, int lists, int64_t per, uint64_t* partial, float* dump, cudaStream_t s) {
+  const int mode = wide_acc_mode();
+  if (NS == 1) return launch_ns<kBf16, 1, 4, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
+  if (NS == 2) {
+    if (mode == 1 && !kDump) return launch_ns<kBf16, 2, 4, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
+    return launch_ns<kBf16, 2, 2, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
+  }
+  if (mode == 1 && !kDump) return launch_ns<kBf16, 4, 2, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
+  return launch_ns<kBf16, 4, 1, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
+}
+
+}  // namespace
+
+int sim_wide_max_batch() { return 256; }
+
+double sim_wide_gamma(int dim, int key_dtype) {
+  // Accumulation: fp32 tensor-core accumulator (not round-to-nearest) over dim
+  // products, <= (dim + 16) 2^-23 relative to sum|k_i q_i| (as for TF32).
+  const double acc = (dim + 16.0) / 8388608.0;
+  if (key_dtype == HSD_DTYPE_BF16) {
+    // bf16 keys are exact; queries rounded to bf16 (RN): |q - bf16(q)| <= 2^-9 |q|;
+    // bf16 x bf16 products are exact in fp32.
+    return 1.0 / 512.0 * 1.0001 + acc;
+  }
+  // TF32 operands: |x - tf32(x)| <= 2^-10 |x| (truncation), so
+  // |kq - k'q'| <= (2^-10 + 2^-10 (1 + 2^-10)) |k||q| per product.
+  return (2.0 + 1.0 / 1024.0) / 1024.0 * 1.0001 + acc;
+}
+
+size_t sim_wide_scratch_bytes(int dim) { return (size_t)256 * dim * sizeof(float); }
+
+cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin, int64_t row_end,
+                            int dim, const float* queries, int B, int lists, void* scratch, uint64_t* partial,
+                            float* dump, cudaStream_t s) {
+  if (B < 1 || B > 256) return cudaErrorInvalidValue;
+  const int NS = B <= 64 ? 1 : (B <= 128 ? 2 : 4);
+  const int rows = 64 * NS;
+  const bool bf16 = key_dtype == HSD_DTYPE_BF16;
+  if (bf16 && dim % 8) return cudaErrorInvalidValue;  // TMA row stride must be a multiple of 16 B
+  CUtensorMap km, qm;
+  if (bf16) {
+    pad_queries_bf16_kernel<<<rows, 256, 0, s>>>(queries, B, dim, (uint16_t*)scratch);
+    if (!tc_make_map_bf16(&km, keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
+        !tc_make_map_bf16(&qm, scratch, (uint64_t)rows, (uint64_t)dim, (uint32_t)rows))
+      return cudaErrorInvalidValue;
+  } else {
+    pad_queries_f32_kernel<<<rows, 256, 0, s>>>(queries, B, dim, (float*)scratch);
+    if (!tc_make_map(&km, (const float*)keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
+        !tc_make_map(&qm, (const float*)scratch, (uint64_t)rows, (uint64_t)dim, (uint32_t)rows))
+      return cudaErrorInvalidValue;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
+  const int64_t per = (n_blocks + lists - 1) / lists;
+  if (bf16)
+    return dump ? launch_dispatch<true, true>(NS, km, qm, row_begin, row_end, dim, B, lists, per, partial, dump, s)
+                : launch_dispatch<true, false>(NS, km, qm, row_begin, row_end, dim, B, lists, per, partial, dump, s);
+  return dump ? launch_dispatch<false, true>(NS, km, qm, row_begin, row_end, dim, B, lists, per, partial, dump, s)
+              : launch_dispatch<false, false>(NS, km, qm, row_begin, row_end, dim, B, lists, per, partial, dump, s);
+}
+
+}  // namespace hsd

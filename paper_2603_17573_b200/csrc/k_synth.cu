@@ -4,6 +4,8 @@
 // per-row norm pass feeding the top-k error bound.
 #include <cub/block/block_reduce.cuh>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "hsd/hsd_synth.h"
 #include "kernels.h"
@@ -27,10 +29,22 @@ __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* bits, doub
   atomicMax(bits, (unsigned long long)__double_as_longlong(v));
 }
 
-// One CTA per DB row: key row (EXACT or exactly-normalised REAL), its norm,
-// and the 21 payload tokens quantize(next_actions[s]).
+// Stored key element: fp32 as generated, or bf16 (RN-even) for bf16 collections.
+__device__ __forceinline__ float store_key(float* p, float v) {
+  *p = v;
+  return v;
+}
+__device__ __forceinline__ float store_key(uint16_t* p, float v) {
+  const uint16_t b = hsd_bf16_bits(v);
+  *p = b;
+  return hsd_bf16_val(b);
+}
+
+// One CTA per DB row: key row (EXACT or exactly-normalised REAL), the norm of
+// the stored row, and the 21 payload tokens quantize(next_actions[s]).
+template <typename KT>
 __global__ void __launch_bounds__(kGenThreads) gen_keys_kernel(int kind, uint64_t db_seed, int64_t row0, int dim,
-                                                               float* __restrict__ keys, uint8_t* __restrict__ tokens,
+                                                               KT* __restrict__ keys, uint8_t* __restrict__ tokens,
                                                                unsigned long long* maxnorm_bits) {
   using BR = cub::BlockReduce<long long, kGenThreads>;
   using BRD = cub::BlockReduce<double, kGenThreads>;
@@ -42,12 +56,11 @@ __global__ void __launch_bounds__(kGenThreads) gen_keys_kernel(int kind, uint64_
   const int64_t row = row0 + blockIdx.x;
   const int64_t src = hsd_key_src_row(kind, row);
   const uint64_t kbase = hsd_stream_base(db_seed, HSD_TAG_KEYS);
-  float* out = keys + (size_t)blockIdx.x * (size_t)dim;
+  KT* out = keys + (size_t)blockIdx.x * (size_t)dim;
   double nrm2 = 0.0;
   if (kind == HSD_SYNTH_EXACT) {
     for (int c = threadIdx.x; c < dim; c += kGenThreads) {
-      float v = hsd_exact_val(hsd_hash_at(kbase, (uint64_t)src * (uint64_t)dim + c));
-      out[c] = v;
+      const float v = store_key(out + c, hsd_exact_val(hsd_hash_at(kbase, (uint64_t)src * (uint64_t)dim + c)));
       nrm2 += (double)v * (double)v;
     }
   } else {
@@ -61,8 +74,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_keys_kernel(int kind, uint64_
     __syncthreads();
     ss = s_ss;
     for (int c = threadIdx.x; c < dim; c += kGenThreads) {
-      float v = hsd_norm_val(hsd_key_raw(kbase, src, dim, c), ss);
-      out[c] = v;
+      const float v = store_key(out + c, hsd_norm_val(hsd_key_raw(kbase, src, dim, c), ss));
       nrm2 += (double)v * (double)v;
     }
     __syncthreads();
@@ -79,13 +91,17 @@ __global__ void __launch_bounds__(kGenThreads) gen_keys_kernel(int kind, uint64_
   }
 }
 
-__global__ void __launch_bounds__(kGenThreads) row_norm_kernel(const float* __restrict__ keys, int dim,
+__device__ __forceinline__ double key_val(float x) { return (double)x; }
+__device__ __forceinline__ double key_val(uint16_t b) { return (double)hsd_bf16_val(b); }
+
+template <typename KT>
+__global__ void __launch_bounds__(kGenThreads) row_norm_kernel(const KT* __restrict__ keys, int dim,
                                                                unsigned long long* maxnorm_bits) {
   using BRD = cub::BlockReduce<double, kGenThreads>;
   __shared__ typename BRD::TempStorage tmp;
-  const float* r = keys + (size_t)blockIdx.x * (size_t)dim;
+  const KT* r = keys + (size_t)blockIdx.x * (size_t)dim;
   double s = 0.0;
-  for (int c = threadIdx.x; c < dim; c += kGenThreads) s += (double)r[c] * (double)r[c];
+  for (int c = threadIdx.x; c < dim; c += kGenThreads) s += key_val(r[c]) * key_val(r[c]);
   s = BRD(tmp).Sum(s);
   if (threadIdx.x == 0) atomic_max_nonneg(maxnorm_bits, sqrt(s));
 }
@@ -189,24 +205,48 @@ __global__ void quantize_tokens_kernel(const double* __restrict__ a, int64_t n, 
 
 }  // namespace
 
-cudaError_t launch_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, float* keys,
+cudaError_t launch_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, void* keys, int key_dtype,
                             uint8_t* tokens, unsigned long long* maxnorm_bits, cudaStream_t s) {
   constexpr int64_t kChunk = 1 << 20;
   for (int64_t r = 0; r < n; r += kChunk) {
     const int64_t m = n - r < kChunk ? n - r : kChunk;
-    gen_keys_kernel<<<(unsigned)m, kGenThreads, 0, s>>>(kind, db_seed, row0 + r, dim, keys + (size_t)r * dim,
-                                                        tokens + (size_t)r * HSD_TOKENS_STRIDE, maxnorm_bits);
+    if (key_dtype == HSD_DTYPE_BF16)
+      gen_keys_kernel<uint16_t><<<(unsigned)m, kGenThreads, 0, s>>>(
+          kind, db_seed, row0 + r, dim, (uint16_t*)keys + (size_t)r * dim, tokens + (size_t)r * HSD_TOKENS_STRIDE,
+          maxnorm_bits);
+    else
+      gen_keys_kernel<float><<<(unsigned)m, kGenThreads, 0, s>>>(
+          kind, db_seed, row0 + r, dim, (float*)keys + (size_t)r * dim, tokens + (size_t)r * HSD_TOKENS_STRIDE,
+          maxnorm_bits);
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_row_norms(const float* keys, int64_t row0, int64_t n, int dim, unsigned long long* maxnorm_bits,
-                             cudaStream_t s) {
+cudaError_t launch_row_norms(const void* keys, int key_dtype, int64_t row0, int64_t n, int dim,
+                             unsigned long long* maxnorm_bits, cudaStream_t s) {
   constexpr int64_t kChunk = 1 << 20;
   for (int64_t r = 0; r < n; r += kChunk) {
     const int64_t m = n - r < kChunk ? n - r : kChunk;
-    row_norm_kernel<<<(unsigned)m, kGenThreads, 0, s>>>(keys + (size_t)(row0 + r) * dim, dim, maxnorm_bits);
+    if (key_dtype == HSD_DTYPE_BF16)
+      row_norm_kernel<uint16_t><<<(unsigned)m, kGenThreads, 0, s>>>((const uint16_t*)keys + (size_t)(row0 + r) * dim,
+                                                                   dim, maxnorm_bits);
+    else
+      row_norm_kernel<float><<<(unsigned)m, kGenThreads, 0, s>>>((const float*)keys + (size_t)(row0 + r) * dim, dim,
+                                                                maxnorm_bits);
   }
+  return cudaGetLastError();
+}
+
+// fp32 -> bf16 (RN-even, hsd_bf16_bits) of n elements (bf16 collection insert).
+__global__ void to_bf16_kernel(const float* __restrict__ in, int64_t n, uint16_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = hsd_bf16_bits(in[i]);
+}
+
+cudaError_t launch_to_bf16(const float* in, int64_t n, uint16_t* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  to_bf16_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, n, out);
   return cudaGetLastError();
 }
 

@@ -9,10 +9,12 @@
 namespace hsd {
 
 // ---- K0 synthetic generators (k_synth.cu) ------------------------------------
-cudaError_t launch_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, float* keys,
+// keys: fp32 or bf16 (key_dtype = HSD_DTYPE_*) row-major [n][dim]
+cudaError_t launch_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, void* keys, int key_dtype,
                             uint8_t* tokens, unsigned long long* maxnorm_bits, cudaStream_t s);
-cudaError_t launch_row_norms(const float* keys, int64_t row0, int64_t n, int dim,
+cudaError_t launch_row_norms(const void* keys, int key_dtype, int64_t row0, int64_t n, int dim,
                              unsigned long long* maxnorm_bits, cudaStream_t s);
+cudaError_t launch_to_bf16(const float* in, int64_t n, uint16_t* out, cudaStream_t s);
 cudaError_t launch_gen_queries(int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B, int dim,
                                float* out, cudaStream_t s);
 cudaError_t launch_gen_logits(const uint8_t* tokens, uint64_t seed, const int64_t* rows, int E, int L, float* out,
@@ -51,8 +53,18 @@ cudaError_t launch_sim_tc1(const float* keys, int64_t n_keys_total, int64_t row_
                            const float* queries, int B, int lists, float* scratch, uint64_t* partial, float* dump,
                            cudaStream_t s);
 
+// K1 wide tcgen05 filter (k_sim_wide.cu): up to 256 queries per pass (UMMA
+// N = 64/128/256), fp32 keys read as TF32 or bf16 keys (kind::f16); same
+// partial-list contract.  scratch: sim_wide_scratch_bytes(dim).
+int sim_wide_max_batch();
+double sim_wide_gamma(int dim, int key_dtype);
+size_t sim_wide_scratch_bytes(int dim);
+cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin, int64_t row_end,
+                            int dim, const float* queries, int B, int lists, void* scratch, uint64_t* partial,
+                            float* dump, cudaStream_t s);
+
 // ---- K2 select: margin candidates + exact fp64 rescoring + final top-k -------
-cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const float* keys, int dim,
+cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const void* keys, int key_dtype, int dim,
                           const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
                           int32_t* ids, int* overflow, cudaStream_t s);
 

@@ -23,7 +23,7 @@ def gamma_tc(dim, variant):
     return (2.0 + 1.0 / 1024) / 1024 * 1.0001 + (dim + 16.0) / 2**23  # TF32 (k_sim_tc1.cu)
 
 
-@pytest.mark.parametrize("variant", [1, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3])
 @pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
 @pytest.mark.parametrize("dim,n,B", [(64, 3000, 64), (4096, 3000, 64), (4096, 1000, 13), (256, 777, 1)])
 def test_tc_scores_within_bound(torch, kind, dim, n, B, variant):
@@ -49,7 +49,7 @@ def test_tc_scores_within_bound(torch, kind, dim, n, B, variant):
         assert np.array_equal(approx, exact)
 
 
-@pytest.mark.parametrize("path", ["rows", "tile", "tc", "tc3"])
+@pytest.mark.parametrize("path", ["rows", "tile", "tc", "tc1", "tc3"])
 @pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
 def test_paths_bit_identical(torch, path, kind):
     try:
@@ -68,7 +68,7 @@ def test_paths_bit_identical(torch, path, kind):
         H.set_sim_path("auto")
 
 
-@pytest.mark.parametrize("path", ["tc", "tc3"])
+@pytest.mark.parametrize("path", ["tc", "tc1", "tc3"])
 def test_tc_ragged_tail_and_range(torch, path):
     """Row counts that are not multiples of the 128-key block, and sub-ranges."""
     H.set_sim_path(path)
@@ -86,3 +86,91 @@ def test_tc_ragged_tail_and_range(torch, path):
             np.testing.assert_array_equal(sc.cpu().numpy()[:, :kk], osc)
     finally:
         H.set_sim_path("auto")
+
+
+# ----------------------------------------------------------------------------- wide kernel (k_sim_wide.cu)
+def gamma_wide(dim, bf16):
+    acc = (dim + 16.0) / 2**23
+    return (1.0 / 512 * 1.0001 + acc) if bf16 else ((2.0 + 1.0 / 1024) / 1024 * 1.0001 + acc)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
+@pytest.mark.parametrize("dim,n,B", [(64, 2000, 256), (4096, 1500, 200), (4096, 900, 128), (256, 777, 65),
+                                     (4352, 600, 7)])
+def test_wide_scores_within_bound(torch, kind, dim, n, B, dtype):
+    """The wide filter (N = 64/128/256 queries per UMMA) stays inside gamma * sum|k q|."""
+    bf16 = dtype == "bf16"
+    col = H.Collection(dim, capacity=n, dtype=dtype)
+    col.generate(kind, 5, n)
+    q = H.gen_queries(kind, 6, 5, n, 0, B, dim)
+    approx = col.debug_sim_scores(q, variant=1).cpu().numpy().astype(np.float64)
+    keys = O.gen_keys(kind | (O.KEYS_BF16 if bf16 else 0), 5, 0, n, dim).astype(np.float64)
+    qq = q.cpu().numpy().astype(np.float64)
+    exact = qq @ keys.T
+    bound = gamma_wide(dim, bf16) * (np.abs(qq) @ np.abs(keys).T)
+    err = np.abs(approx - exact)
+    assert np.all(err <= bound), float((err / np.maximum(bound, 1e-300)).max())
+    if kind == O.EXACT:  # k/16 values are exact in TF32 and bf16 -> exact scores
+        assert np.array_equal(approx, exact)
+
+
+@pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
+def test_wide_batches_bit_identical(torch, kind):
+    """One pass serves up to 256 queries; B > 256 takes several passes."""
+    for dim, n in ((64, 4000), (4096, 1800)):
+        col = H.Collection(dim, capacity=n)
+        col.generate(kind, 21, n)
+        for B in (5, 65, 127, 128, 129, 200, 256, 300):
+            q = H.gen_queries(kind, 22, 21, n, 1, B, dim)
+            sc, ids = col.search_topk_exact(q, 8)
+            osc, oid = O.search_synth(kind, 21, n, q.cpu().numpy(), 8)
+            np.testing.assert_array_equal(ids.cpu().numpy(), oid, err_msg=f"dim={dim} B={B}")
+            np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+        assert col.overflow_count() == 0
+
+
+@pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
+def test_bf16_collection_exact_over_stored_keys(torch, kind):
+    """bf16 collections: ids and fp64 scores bit-identical to the reference's
+    search over the bf16-rounded keys (store.cpp:59-73 on the stored DB)."""
+    for dim, n in ((64, 3000), (4096, 1500), (4352, 700)):
+        col = H.Collection(dim, capacity=n, dtype="bf16")
+        col.generate(kind, 31, n)
+        keys, _ = col.keys_view()
+        assert keys.dtype == torch.bfloat16
+        ok = O.gen_keys(kind | O.KEYS_BF16, 31, 0, n, dim)
+        np.testing.assert_array_equal(keys.float().cpu().numpy(), ok)
+        for B, k in ((1, 8), (3, 1), (64, 8), (100, 32), (256, 8)):
+            q = H.gen_queries(kind, 32, 31, n, 0, B, dim)
+            sc, ids = col.search_topk_exact(q, k)
+            osc, oid = O.search_synth(kind | O.KEYS_BF16, 31, n, q.cpu().numpy(), k)
+            np.testing.assert_array_equal(ids.cpu().numpy(), oid, err_msg=f"dim={dim} B={B}")
+            np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+        assert col.overflow_count() == 0
+
+
+def test_bf16_insert_and_range(torch):
+    rng = np.random.default_rng(3)
+    n, dim = 1300, 128
+    emb = rng.standard_normal((n, dim)).astype(np.float32)
+    acts = rng.uniform(-1, 1, (n, 3, 7))
+    col = H.Collection(dim, capacity=16, dtype="bf16")
+    col.insert(emb, acts)
+    stored = torch.as_tensor(emb).to(torch.bfloat16).float().numpy()  # RN-even, as hsd_bf16_bits
+    keys, _ = col.keys_view()
+    np.testing.assert_array_equal(keys.float().cpu().numpy(), stored)
+    q = torch.as_tensor(rng.standard_normal((40, dim)).astype(np.float32), device="cuda")
+    for rg in ((0, n), (17, 900), (n - 3, n)):
+        sc, ids = col.search_topk_exact(q, 6, row_range=rg)
+        osc, oid = O.search_topk(stored[rg[0]:rg[1]], q.cpu().numpy(), 6)
+        kk = oid.shape[1]
+        np.testing.assert_array_equal(ids.cpu().numpy()[:, :kk], oid + rg[0])
+        np.testing.assert_array_equal(sc.cpu().numpy()[:, :kk], osc)
+
+
+def test_bf16_config_errors(torch):
+    with pytest.raises(H.ConfigError):
+        H.Collection(36, capacity=4, dtype="bf16")  # dim % 8
+    with pytest.raises(H.ConfigError):
+        H.Collection(64, capacity=4, dtype="fp8")

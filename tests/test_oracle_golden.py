@@ -300,3 +300,16 @@ def test_decide_sd_fixtures():
     fast = np.stack([np.arange(15) * 0.02, np.arange(15) * 0.01, np.zeros(15)], axis=1)
     R, D, F, dec = O.window_features(fast, p, b)
     assert dec == 1 and F == 1.0
+
+
+def test_bf16_key_rounding_matches_torch_rn_even():
+    """hsd_bf16_bits (bf16 collections, oracle KEYS_BF16) is IEEE RN-even."""
+    import torch
+
+    for kind in (O.EXACT, O.REAL):
+        k32 = O.gen_keys(kind, 11, 0, 64, 4096)
+        kb = O.gen_keys(kind | O.KEYS_BF16, 11, 0, 64, 4096)
+        ref = torch.as_tensor(k32).to(torch.bfloat16).float().numpy()
+        np.testing.assert_array_equal(kb, ref)
+        if kind == O.EXACT:  # k/16 values are exact in bf16
+            np.testing.assert_array_equal(kb, k32)
