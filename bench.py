@@ -24,6 +24,13 @@ records with an NCCL all-gather and merges them; verification of the 64
 episodes is split across ranks.
 
 --impl reference: the reference CPU path alone (see cpu_reference_step).
+
+--config selects the workload (default c2, the BASELINE.json headline):
+  c2    configs[1]: 1M x 4096 fp32, B = 64 (the north-star metric)
+  c4    configs[3]: 10M x 4096 fp32, B = 256 (row-sharded over --gpus N)
+  bf16  the C2 workload on a bf16 DB (kind::f16 filter + exact rescoring over
+        the stored bf16 keys), reported with recall@k against the fp32 DB
+  c3    configs[2]: verify/accept sweep, 4096 episodes x P parameter sets
 """
 from __future__ import annotations
 
@@ -62,7 +69,19 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--force-sharded", action="store_true",
                    help="use the sharded (NCCL all-gather + merge) step even at world size 1")
-    return p.parse_args()
+    p.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "bf16"])
+    p.add_argument("--dtype", default=None, choices=["f32", "bf16"], help="key storage (default per config)")
+    p.add_argument("--episodes", type=int, default=4096, help="C3 episodes per round")
+    a = p.parse_args()
+    given = {x.split("=")[0] for x in sys.argv[1:] if x.startswith("--")}
+    if a.config == "c4":
+        if "--n" not in given:
+            a.n = 10_000_000
+        if "--batch" not in given:
+            a.batch = 256
+    if a.dtype is None:
+        a.dtype = "bf16" if a.config == "bf16" else "f32"
+    return a
 
 
 def env_rank():
@@ -194,10 +213,15 @@ def cpu_reference_step(args, state, n_sample, threads):
         O.verify_round(tok[e, :, :args.L], greedy, skip=skip)
 
 
+def cpu_sample_rows(args):
+    """Rows of the DB sample the CPU arm searches: ~1-2 s of CPU work per pass
+    (1/16 of the 1M DB; capped so a 10M DB does not need 20 GB of host fp64)."""
+    return max(1000, min(args.n, args.n // 16, 62_500))
+
+
 def cpu_baseline(args, seconds_budget=20.0, steps=None, warmup=0):
     threads = os.cpu_count() or 1
-    # size the sample so one pass is ~1-2 s of CPU work: ~1/16 of the 1M DB
-    n_sample = max(1000, min(args.n, args.n // 16))
+    n_sample = cpu_sample_rows(args)
     state = cpu_reference_setup(args, n_sample)
     for _ in range(warmup):
         cpu_reference_step(args, state, n_sample, threads)
@@ -230,7 +254,7 @@ def run_reference(args):
     if rank != 0:
         return
     cb, times = cpu_baseline(args, steps=args.steps, warmup=args.warmup)
-    t = statistics.mean(times) * (args.n / max(1000, min(args.n, args.n // 16)))
+    t = statistics.mean(times) * (args.n / cpu_sample_rows(args))
     line = {
         "metric": METRIC, "value": cb["value"], "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * t, "higher_is_better": True,
@@ -243,14 +267,25 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def metric_of(args):
+    if args.config == "c2" and args.dtype == "f32":
+        return METRIC
+    return (f"retrieved+verified draft steps/sec at {args.n / 1e6:g}M-entry {args.dtype} DB, batch {args.batch} "
+            f"({args.config.upper()}); HBM GB/s vs 8 TB/s peak")
+
+
 def config_of(args, world):
+    tag = {"c2": "C2", "c4": "C4", "bf16": "C2-bf16"}.get(args.config, args.config)
     return {
-        "workload": (f"C2: {args.n}-entry x {args.dim}-d fp32 trajectory DB, batch {args.batch} queries, k={args.k}, "
-                     f"draft len {args.L}, 7x256 verifier logits, {args.d_f}-d skip features, 15-pt windows"),
+        "workload": (f"{tag}: {args.n}-entry x {args.dim}-d {args.dtype} trajectory DB, batch {args.batch} queries, "
+                     f"k={args.k}, draft len {args.L}, 7x256 verifier logits, {args.d_f}-d skip features, "
+                     f"15-pt windows"),
+        "key_dtype": args.dtype,
         "n_rows": args.n, "dim": args.dim, "batch": args.batch, "k": args.k, "draft_len": args.L, "d_f": args.d_f,
         "synthetic_family": "REAL" if args.kind == 1 else "EXACT",
         "parallelism": f"db-shard{world}" if world > 1 else "single",
-        "l2": "inputs larger than L2 (16.4 GB of keys streamed per pass)",
+        "l2": f"inputs larger than L2 ({args.n * args.dim * (2 if args.dtype == 'bf16' else 4) / 1e9:.1f} GB of keys "
+              f"streamed per pass)",
         "verify": "relaxed 30/15, verify-skip min_S=0.95 O_dist=5 d=1, chain cap 64",
     }
 
@@ -270,7 +305,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     B, k, L, d_f, dim = args.batch, args.k, args.L, args.d_f, args.dim
     b0, b1 = H.shard_range(args.n, world, rank)
-    col = H.Collection(dim, capacity=b1 - b0, device=local)
+    col = H.Collection(dim, capacity=b1 - b0, device=local, dtype=args.dtype)
     col.generate(args.kind, 2026, b1 - b0, row0=b0)
     stream = torch.cuda.current_stream()
 
@@ -358,13 +393,24 @@ def run_ours(args):
         n_rec, st = eng.stage_times()
         stages = {kname: v / max(n_rec, 1) for kname, v in st.items()}
         sim_ms = stages["similarity"]
-        alg_bytes = (b1 - b0) * dim * 4 + B * dim * 4
+        esz = 2 if args.dtype == "bf16" else 4
+        passes = (B + 255) // 256
+        alg_bytes = passes * (b1 - b0) * dim * esz + B * dim * 4
         peak, peak_kind = load_peaks()
         achieved = alg_bytes / (sim_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic("similarity"), "kernel": "similarity (K1)",
+                "traffic": load_traffic("similarity" if args.config == "c2" else f"similarity_{args.config}"),
+                "kernel": f"similarity (K1, {'kind::f16' if args.dtype == 'bf16' else 'kind::tf32'} filter)",
                 "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": sim_ms, "peak_source": peak_kind,
                 "share_of_step": sim_ms / stages["total"]}
+        # tensor-pipe side of the same kernel (the filter's MMA work)
+        tflops = 2.0 * B * (b1 - b0) * dim / (sim_ms / 1e3) / 1e12
+        bf16_peak = load_peak_key("bf16_tflops")
+        if bf16_peak:
+            tpk = bf16_peak if args.dtype == "bf16" else bf16_peak / 2.0
+            roof["tensor"] = {"achieved_tflops": tflops, "peak_tflops": tpk, "frac": tflops / tpk,
+                              "peak_source": "measured bf16" if args.dtype == "bf16"
+                              else "measured bf16 / 2 (nominal TF32:BF16 dense ratio)"}
 
     # ---- e2e through the public host-buffer API (N=1: hsd_step_host)
     e2e = None
@@ -372,18 +418,23 @@ def run_ours(args):
         e2e = run_e2e(H, torch, eng, args, qs, lg, feats, xyz_np, vp, stream)
 
     overflow = col.overflow_count(stream)
+    recall = None
+    if args.dtype == "bf16" and world == 1 and args.n <= 4_000_000:
+        recall = bf16_recall(H, torch, args, col, qs, local)
     if rank == 0:
         cb = None
         if world == 1 and not args.no_cpu_baseline and not args.force_sharded:
             cb, _ = cpu_baseline(args, seconds_budget=args.cpu_seconds)
         line = {
-            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+            "metric": metric_of(args), "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (counter-generated DB/queries/logits/features)",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (counter-generated DB/queries/logits/features)",
             "config": config_of(args, world), "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "stages_ms": stages,
             "search_overflow": overflow,
         }
+        if recall is not None:
+            line["recall_at_k"] = recall
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -440,10 +491,185 @@ def run_e2e(H, torch, eng, args, qs, lg, feats, xyz_np, vp, stream):
             "api": "hsd_step_host (C ABI), pinned host buffers, wall clock", "passes": n}
 
 
+def load_peak_key(key):
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)[key])
+    except Exception:
+        return None
+
+
+def bf16_recall(H, torch, args, col_bf16, qs, local):
+    """recall@k of the bf16 DB's exact top-k against the fp32 DB's exact top-k
+    (same synthetic rows before rounding), over every resident query batch."""
+    col32 = H.Collection(args.dim, capacity=args.n, device=local)
+    col32.generate(args.kind, 2026, args.n)
+    hits = total = 0
+    same_top1 = 0
+    for q in qs:
+        _, ib = col_bf16.search_topk_exact(q, args.k)
+        _, i32 = col32.search_topk_exact(q, args.k)
+        ib, i32 = ib.cpu().numpy(), i32.cpu().numpy()
+        for a, b in zip(ib, i32):
+            hits += len(set(a.tolist()) & set(b.tolist()))
+            total += args.k
+            same_top1 += int(a[0] == b[0])
+    col32.close()
+    torch.cuda.empty_cache()
+    return {"k": args.k, "recall": hits / total, "top1_agreement": same_top1 / (len(qs) * args.batch),
+            "queries": len(qs) * args.batch, "against": "exact fp32 search of the same synthetic DB"}
+
+
+# ------------------------------------------------------------------------------ C3: verify/accept sweep
+C3_SWEEP = [  # (relaxed, bias_seq_max, bias_token_max, skip_enabled, min_S): tolerance x skip-threshold grid
+    (r, sm, tm, sk, ms)
+    for (r, sm, tm) in ((False, 0, 0), (True, 10, 5), (True, 30, 15), (True, 60, 30))
+    for (sk, ms) in ((False, 0.95), (True, 0.9), (True, 0.95))
+]
+
+
+def c3_params(H):
+    return [H.VerifyParams.make(relaxed=r, bias_seq_max=sm, bias_token_max=tm, skip_enabled=sk, min_S=ms, O_dist=5)
+            for (r, sm, tm, sk, ms) in C3_SWEEP]
+
+
+def run_c3(args):
+    """configs[2]: one ROUND verifies E episodes (argmax of 7x256 logits, skip
+    test on 4096-d features, gather of k = 8 drafts, relaxed acceptance) under
+    every parameter set of the sweep in one K4 launch."""
+    import torch
+
+    import paper_2603_17573_b200 as H
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    E, k, L, d_f = args.episodes, args.k, args.L, args.d_f
+    n_db = 1_000_000
+    col = H.Collection(8, capacity=n_db, device=local)  # token table (payload drafts); keys unused here
+    col.generate(H.REAL, 2026, n_db)
+    params = c3_params(H)
+    P = len(params)
+    S = 2  # two resident input sets (2 x 164 MB > L2)
+    g = torch.Generator(device="cpu").manual_seed(11)
+    ids = [torch.randint(0, n_db, (E, k), generator=g, dtype=torch.int32).to(dev) for _ in range(S)]
+    lg = [H.gen_logits(col, 3 + s, ids[s][:, 0].cpu().numpy().astype(np.int64), L) for s in range(S)]
+    feats = [H.gen_features(5 + s, E, d_f, device=local) for s in range(S)]
+    hist = torch.full((E,), 100, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    arr = (H.VerifyParams * P)(*params)
+    out = torch.empty((P, E, 20), dtype=torch.uint8, device=dev)
+    toks = torch.empty((P, E, L), dtype=torch.uint8, device=dev)
+
+    def launch(s, o=out, t=toks):
+        H.check(H.lib().hsd_verify_round(col.handle, H._ptr(ids[s]), E, k, L, H._ptr(lg[s]), H._ptr(feats[s][0]),
+                                         H._ptr(feats[s][1]), d_f, H._ptr(hist), 1, H.C.cast(arr, H.C.c_void_p), P,
+                                         H._ptr(o), H._ptr(t), H._stream(stream)))
+
+    for i in range(args.warmup):
+        launch(i % S)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(args.steps):
+            launch(i % S)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    value = E / (ms / 1e3)
+    in_bytes = E * (L * 256 * 4 + 2 * d_f * 4 + k * 4 + k * HSD_TOK_ROW + 4)
+    out_bytes = P * E * (20 + L)
+    peak, peak_kind = load_peaks()
+    achieved = (in_bytes + out_bytes) / (ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": load_traffic("verify_c3"), "kernel": "verify (K4: gather + skip + relaxed accept, P sets)",
+            "algorithmic_bytes_per_launch": in_bytes + out_bytes, "avg_launch_ms": ms, "peak_source": peak_kind,
+            "share_of_step": 1.0}
+
+    # e2e through the public verify entry point with host buffers: H2D of the
+    # round's inputs, K4, D2H of the P x E outcomes + emitted tokens
+    pin = lambda t: t.cpu().pin_memory()
+    h_in = [dict(ids=pin(ids[s]), lg=pin(lg[s]), fn=pin(feats[s][0]), fp=pin(feats[s][1])) for s in range(S)]
+    h_out, h_tok = torch.empty_like(out, device="cpu").pin_memory(), torch.empty_like(toks, device="cpu").pin_memory()
+    d_ids, d_lg = torch.empty_like(ids[0]), torch.empty_like(lg[0])
+    d_fn, d_fp = torch.empty_like(feats[0][0]), torch.empty_like(feats[0][1])
+    h2d = sum(v.numel() * v.element_size() for v in h_in[0].values())
+    d2h = h_out.numel() + h_tok.numel()
+    import time as _t
+    n_e2e = max(3, args.e2e_steps)
+    for i in range(n_e2e + 2):
+        if i == 2:
+            torch.cuda.synchronize()
+            t0 = _t.perf_counter()
+        hi = h_in[i % S]
+        d_ids.copy_(hi["ids"], non_blocking=True)
+        d_lg.copy_(hi["lg"], non_blocking=True)
+        d_fn.copy_(hi["fn"], non_blocking=True)
+        d_fp.copy_(hi["fp"], non_blocking=True)
+        H.check(H.lib().hsd_verify_round(col.handle, H._ptr(d_ids), E, k, L, H._ptr(d_lg), H._ptr(d_fn), H._ptr(d_fp),
+                                         d_f, H._ptr(hist), 1, H.C.cast(arr, H.C.c_void_p), P, H._ptr(out),
+                                         H._ptr(toks), H._stream(stream)))
+        h_out.copy_(out, non_blocking=True)
+        h_tok.copy_(toks, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_v = E * n_e2e / (_t.perf_counter() - t0)
+    e2e = {"value": e2e_v, "unit": "episode-rounds/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "api": "hsd_verify_round (C ABI) with pinned host buffers, wall clock", "passes": n_e2e}
+
+    cb = None
+    if not args.no_cpu_baseline:
+        cb = c3_cpu_baseline(args, ids[0].cpu().numpy(), lg[0].cpu().numpy(), feats[0][0].cpu().numpy(),
+                             feats[0][1].cpu().numpy(), col)
+    line = {
+        "metric": "verified episode-rounds/sec (each under every parameter set of the sweep), 4096 concurrent "
+                  "episodes, 7x256 logits (C3)",
+        "value": value, "unit": "episode-rounds/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (counter-generated logits/features/drafts)",
+        "config": {"workload": f"C3: {E} episodes x {P} parameter sets (acceptance tolerance x skip threshold), "
+                               f"k={k}, L={L}, d_f={d_f}", "episodes": E, "param_sets": P, "sweep": C3_SWEEP,
+                   "l2": "two resident input sets of 164 MB alternate (> L2)"},
+        "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+HSD_TOK_ROW = 32
+
+
+def c3_cpu_baseline(args, ids, lg, fn, fp, col):
+    """Oracle port of the same round (argmax, skip, verify_tree per parameter
+    set) on a sample of episodes, 1 thread."""
+    from oracle import oracle as O
+
+    _, tok = col.keys_view()
+    tok = tok.cpu().numpy()
+    P = len(C3_SWEEP)
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < min(args.cpu_seconds, 10.0) and n < ids.shape[0]:
+        e = n
+        greedy = np.array([O.argmax(lg[e, p]) for p in range(args.L)], np.int32)
+        cos = O.feature_cos(fn[e], fp[e])
+        drafts = tok[ids[e], :args.L].astype(np.int32)
+        for (r, sm, tm, sk, ms) in C3_SWEEP:
+            skip = sk and O.should_skip(cos, O.SkipState(0.0, ms, 5, 0.0, 0), 1, 100)
+            O.verify_round(drafts, greedy, skip=skip, enabled=r, seq_max=sm, tok_max=tm)
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "episode-rounds/s", "cores": 1, "kind": "port",
+            "sample": f"{n} episodes x {P} parameter sets through the oracle port (spec-only in the reference), "
+                      f"1 thread, {dt:.1f} s"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c3":
+        run_c3(args)
     else:
         run_ours(args)
 
