@@ -293,6 +293,83 @@ hsd_status hsd_merge_topk(int device, const double* g_scores, const int32_t* g_i
                           int B, int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Hybrid decoding loop (config 5): the SPEC scheduler's run_step / run_episode
+ * for R robots at once, device-resident.  Per round and
+ * robot: decide_sd (kinematic fused metric over the trailing w points; cold
+ * start -> drafter) -> retrieval (top-K_top drafts, 21 tokens, verify-skip,
+ * verify_tree with relaxed acceptance) or toy drafter (L tokens, verified) ->
+ * emitted tokens + autoregressive completion of the action slice -> ToyEnv
+ * position += HSD_ENV_SCALE * dequantize(xyz bins) -> trajectory ring; cost
+ * model, StepRecord trace and EpisodeReport counters.  The
+ * synthetic harness (demonstration policy, robots, drafter) is the
+ * counter-based one of hsd_synth.h.  The DB must hold HSD_PAYLOAD_TRAJ rows
+ * (row = e * traj_T + j).  With a communicator the DB is row-sharded: every
+ * rank runs all robots (replicated state), searches its shard and merges the
+ * all-gathered top-k; results are identical on every rank.
+ * ---------------------------------------------------------------------- */
+enum { HSD_MODE_HYBRID = 0, HSD_MODE_PURE_RETRIEVAL = 1, HSD_MODE_PURE_DRAFTER = 2, HSD_MODE_AUTOREGRESSIVE = 3 };
+#define HSD_HYB_RET_L 21    /* retrieval draft: 3 action slices */
+#define HSD_HYB_MAX_EMIT 28 /* 21 accepted + completion to the slice boundary */
+
+typedef struct hsd_hybrid_params {
+  int32_t robots;           /* R */
+  int32_t k;                /* K_top retrieved drafts (SPEC.md:379 default 3) */
+  int32_t mode;             /* HSD_MODE_* (HybridConfig.mode) */
+  int32_t traj_T;           /* demonstration length of the DB rows */
+  int32_t drafter_p_pct;    /* toy drafter accuracy p in percent (85) */
+  int32_t drafter_L;        /* drafter draft length (7) */
+  int32_t gap_d;            /* should_skip gap d (1) */
+  int32_t d_f;              /* verifier feature dim of the skip check (0: skip off) */
+  uint64_t seed;            /* robots, drafter, logits, features */
+  uint64_t db_seed;         /* DB keys + demonstration policy */
+  int32_t key_kind;         /* synthetic key family of the DB (HSD_SYNTH_*) */
+  int32_t record_trace;     /* keep the per-round StepRecord trace on the device */
+  hsd_verify_params verify; /* acceptance caps + verify-skip state (retrieval mode) */
+  hsd_metric_params metric; /* FusedMetricParams */
+  hsd_norm_bounds bounds;   /* NormalizationBounds */
+  double cost_verifier;     /* CostModel: verifier call 1.0 */
+  double cost_drafter_token;/*            drafter token 0.1 */
+  double cost_retrieval;    /*            retrieval query 0.37 */
+} hsd_hybrid_params;
+
+typedef struct hsd_step_record { /* StepRecord */
+  float F;                /* fused metric (-1 in autoregressive mode) */
+  int16_t accept_len;     /* accepted draft tokens */
+  int16_t verifier_calls; /* chains verified + autoregressive completion tokens */
+  int16_t n_emit;         /* tokens emitted (multiple of 7) */
+  int8_t mode;            /* 1 retrieval_sd, 0 drafter_sd, 2 autoregressive */
+  int8_t skipped;         /* verify-skip fired */
+  float cost;             /* cost units of the round */
+} hsd_step_record;
+
+typedef struct hsd_episode_report { /* EpisodeReport counters */
+  int64_t rounds, tokens, accepted, verifier_calls;
+  double cost;
+  int32_t n_retrieval, n_drafter, n_skipped, n_fallback;
+} hsd_episode_report;
+
+typedef struct hsd_hybrid hsd_hybrid;
+/* comm may be NULL (single GPU: the collection holds rows [0, n_total_rows)). */
+hsd_status hsd_hybrid_create(hsd_collection* c, hsd_comm* comm, int64_t id_offset, int64_t n_total_rows,
+                             const hsd_hybrid_params* p, int max_rounds, hsd_hybrid** out);
+hsd_status hsd_hybrid_destroy(hsd_hybrid* h);
+/* Run n decode rounds for all robots on `stream` (one host sync per round:
+ * the retrieval/drafter robot counts size the launches). */
+hsd_status hsd_hybrid_step(hsd_hybrid* h, int n_rounds, void* stream);
+/* Host copies: positions [R][3], reports [R], trace [rounds][R] (rounds
+ * recorded so far, <= max_rounds); stage times (ms, summed over rounds:
+ * [kinematics, search, verify, other, total]). */
+hsd_status hsd_hybrid_positions(hsd_hybrid* h, double* xyz);
+hsd_status hsd_hybrid_reports(hsd_hybrid* h, hsd_episode_report* out);
+hsd_status hsd_hybrid_trace(hsd_hybrid* h, hsd_step_record* out, int* rounds);
+hsd_status hsd_hybrid_counts(hsd_hybrid* h, int64_t* retrieval_queries, int64_t* drafter_rounds);
+
+/* Generate with an explicit payload family (HSD_PAYLOAD_*): TRAJ rows hold the
+ * demonstration policy of episode row / traj_T from action row % traj_T. */
+hsd_status hsd_collection_generate_ex(hsd_collection* c, int kind, uint64_t db_seed, int64_t row0, int64_t n,
+                                      int payload, int traj_T);
+
+/* ------------------------------------------------------------------------
  * Synthetic workload generators on the device (include/hsd/hsd_synth.h).
  * ---------------------------------------------------------------------- */
 hsd_status hsd_gen_queries(int device, int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B,

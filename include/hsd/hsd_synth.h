@@ -53,6 +53,15 @@ enum {
   HSD_TAG_ACTIONS = 6,
   HSD_TAG_QNOISE = 7,
   HSD_TAG_QPICK = 8,
+  HSD_TAG_POLICY = 9,
+  HSD_TAG_ROBOT = 10,
+  HSD_TAG_DRAFTER = 11,
+};
+
+/* Payload families of generated records (hsd_collection_generate_ex). */
+enum {
+  HSD_PAYLOAD_RANDOM = 0, /* next_actions uniform in [-1, 1) (hsd_action_val) */
+  HSD_PAYLOAD_TRAJ = 1,   /* demonstration rows: row = e * T + j holds next_actions[s] = policy(e, j + s) */
 };
 
 HSD_HD uint64_t hsd_splitmix64(uint64_t x) {
@@ -211,6 +220,129 @@ HSD_HD int64_t hsd_feat_raw(uint64_t seed, int64_t e, int which, int dim, int co
   if (which == 0) return now;
   int64_t noise = hsd_ih4(hsd_hash_at(base, ((uint64_t)e * 2u + 1u) * (uint64_t)dim + (uint64_t)col));
   return (int64_t)hsd_feat_mix(seed, e) * now + noise;
+}
+
+/* ---- trajectory harness (config 5: the hybrid decoding loop) -------------
+ * Stand-in for the SPEC harness (ToyEnv + OracleVLA +
+ * recorded demonstrations).  Demonstration episode e follows a piecewise
+ * policy of HSD_SEG_LEN-action segments that alternate
+ *   transport (even segments): straight, fast (|v| <= 0.8), gripper open;
+ *   approach  (odd segments) : the velocity turns by a fixed rational rotation
+ *                              (cos, sin) = ((1-u^2)/(1+u^2), 2u/(1+u^2)) per
+ *                              action in one axis plane, slow (|v| ~ 0.3),
+ *                              gripper closed;
+ * so the fused metric (kinematics.cpp) sees straight/fast windows (retrieval)
+ * and tight slow arcs (drafter).  Values use +, *, / with explicit rounding
+ * (no FMA contraction, no libm transcendentals): host and device agree bit for
+ * bit.  Tokens are the reference quantize (actions.cpp:32-50) of the values. */
+#define HSD_SEG_LEN 24
+#define HSD_ENV_SCALE 0.01 /* ToyEnv: position += HSD_ENV_SCALE * dequantize(xyz bins) */
+
+#if defined(__CUDA_ARCH__)
+#define HSD_MUL(a, b) __dmul_rn((a), (b))
+#define HSD_ADD(a, b) __dadd_rn((a), (b))
+#define HSD_SUB(a, b) __dsub_rn((a), (b))
+#define HSD_DIV(a, b) __ddiv_rn((a), (b))
+#else
+#define HSD_MUL(a, b) ((a) * (b))
+#define HSD_ADD(a, b) ((a) + (b))
+#define HSD_SUB(a, b) ((a) - (b))
+#define HSD_DIV(a, b) ((a) / (b))
+#endif
+
+/* quantize of one value, actions.cpp:42-47 (bounds [lo, hi], K bins). */
+HSD_HD int hsd_quantize_bin(double v, double lo, double hi, int k_bins) {
+  const double c = v < lo ? lo : (hi < v ? hi : v);
+  const double t = HSD_DIV(HSD_SUB(c, lo), HSD_SUB(hi, lo));
+  int bin = (int)floor(HSD_MUL(t, (double)(k_bins - 1)));
+  bin = bin < 0 ? 0 : bin;
+  return bin > k_bins - 1 ? k_bins - 1 : bin;
+}
+
+/* dequantize of one bin, actions.cpp:60-63: lo + bin / (K - 1) * span. */
+HSD_HD double hsd_dequantize_bin(int bin, double lo, double hi, int k_bins) {
+  return HSD_ADD(lo, HSD_MUL(HSD_DIV((double)bin, (double)(k_bins - 1)), HSD_SUB(hi, lo)));
+}
+
+/* Policy action value of demonstration episode e at action index j, dim d. */
+HSD_HD double hsd_policy_val(uint64_t seed, int64_t e, int64_t j, int d) {
+  const int64_t seg = j / HSD_SEG_LEN;
+  const int64_t jj = j - seg * HSD_SEG_LEN;
+  const uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_POLICY), (uint64_t)e * 0x100000001B3ull + (uint64_t)seg);
+  const int arc = (int)(seg & 1);
+  if (d == 6) return arc ? 1.0 : -1.0; /* gripper closed while approaching */
+  if (d >= 3) /* rotation: piecewise-constant small values */
+    return HSD_MUL(0.0625, (double)((int)((h >> (8 * d)) % 5u) - 2));
+  if (!arc) { /* transport: constant direction, components in [-0.8, 0.8) */
+    return HSD_DIV((double)((int)((h >> (8 * d)) & 0xFFu) - 128), 160.0);
+  }
+  /* approach: rotate (cx, cy) by the rational angle of u, jj times */
+  const int plane = (int)((h >> 24) % 3u); /* (0,1) (1,2) (0,2) */
+  const int ax = plane == 1 ? 1 : 0, ay = plane == 0 ? 1 : 2;
+  if (d != ax && d != ay) return 0.0;
+  const double u = HSD_ADD(0.15, HSD_DIV((double)((h >> 32) & 0xFFu), 1700.0)); /* 0.15 .. 0.30 */
+  const double u2 = HSD_MUL(u, u);
+  const double den = HSD_ADD(1.0, u2);
+  const double cr = HSD_DIV(HSD_SUB(1.0, u2), den), sr = HSD_DIV(HSD_MUL(2.0, u), den);
+  const double w = HSD_SUB(HSD_DIV((double)((h >> 40) & 0xFFu), 127.5), 1.0); /* start angle parameter */
+  const double w2 = HSD_MUL(w, w);
+  double cx = HSD_DIV(HSD_SUB(1.0, w2), HSD_ADD(1.0, w2)), cy = HSD_DIV(HSD_MUL(2.0, w), HSD_ADD(1.0, w2));
+  for (int64_t i = 0; i < jj; ++i) {
+    const double nx = HSD_SUB(HSD_MUL(cr, cx), HSD_MUL(sr, cy));
+    const double ny = HSD_ADD(HSD_MUL(sr, cx), HSD_MUL(cr, cy));
+    cx = nx;
+    cy = ny;
+  }
+  const double sp = HSD_ADD(0.25, HSD_DIV((double)((h >> 48) & 0xFFu), 2550.0)); /* 0.25 .. 0.35 */
+  return HSD_MUL(sp, d == ax ? cx : cy);
+}
+
+HSD_HD int hsd_policy_token(uint64_t seed, int64_t e, int64_t j, int d) {
+  return hsd_quantize_bin(hsd_policy_val(seed, e, j, d), -1.0, 1.0, 256);
+}
+
+/* Robot r of the hybrid loop: the demonstration episode it replays (>= n_demo
+ * -> an episode absent from the DB: "unseen instance", ~1/8 of robots) and its
+ * per-dim bin bias (1/4 of seen robots deviate by 1..6 bins on pos/rot dims:
+ * inside the relaxed caps 30/15, rejected by strict acceptance). */
+HSD_HD int64_t hsd_robot_episode(uint64_t seed, int64_t r, int64_t n_demo) {
+  const uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_ROBOT), (uint64_t)r);
+  if (n_demo <= 0 || (h & 7u) == 0u) return n_demo + (int64_t)((h >> 8) % 1000003u); /* unseen */
+  return (int64_t)((h >> 8) % (uint64_t)n_demo);
+}
+HSD_HD int hsd_robot_bias(uint64_t seed, int64_t r, int d) {
+  const uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_ROBOT), (uint64_t)r ^ 0x5A5A000000000000ull);
+  if (d == 6 || (h & 3u) != 0u) return 0;
+  const int mag = 1 + (int)((h >> (4 + 6 * d)) % 6u);
+  return ((h >> (40 + d)) & 1u) ? mag : -mag;
+}
+/* Verifier (OracleVLA stand-in) greedy token of robot r (replaying episode e)
+ * at action j, dim d: the policy token (policy_seed = the DB seed) plus the
+ * robot's bias (robot_seed = the loop seed), clamped to [0, 255]. */
+HSD_HD int hsd_robot_greedy(uint64_t policy_seed, uint64_t robot_seed, int64_t r, int64_t e, int64_t j, int d) {
+  int t = hsd_policy_token(policy_seed, e, j, d) + hsd_robot_bias(robot_seed, r, d);
+  return t < 0 ? 0 : (t > 255 ? 255 : t);
+}
+/* DB row a robot's retrieval query near-duplicates: its demonstration row
+ * (e, j) when that row exists, else -1 (a query with no near neighbour). */
+HSD_HD int64_t hsd_hybrid_query_row(int64_t e, int64_t j, int64_t T, int64_t n_demo, int64_t n_rows) {
+  if (e < 0 || e >= n_demo || j < 0 || j >= T) return -1;
+  const int64_t row = e * T + j;
+  return row < n_rows ? row : -1;
+}
+/* ToyEnv start position of robot r (exact binary fractions in [-0.125, 0.125)). */
+HSD_HD double hsd_robot_start(uint64_t seed, int64_t r, int d) {
+  const uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_ROBOT), (uint64_t)r ^ 0xA5A5000000000000ull);
+  return (double)((int)((h >> (8 * d)) & 0xFFu) - 128) / 1024.0;
+}
+/* Counter id of robot r's round-`round` query / features / logits streams. */
+HSD_HD int64_t hsd_hybrid_qid(int64_t r, int64_t round) { return (r << 24) + round; }
+/* Toy drafter: the verifier's greedy token with probability
+ * p_pct/100, else a uniformly random different bin. */
+HSD_HD int hsd_drafter_token(uint64_t seed, int64_t r, int64_t step, int p, int greedy, int p_pct) {
+  const uint64_t h = hsd_hash_at(hsd_stream_base(seed, HSD_TAG_DRAFTER), ((uint64_t)r << 24) ^ ((uint64_t)step << 5) ^ (uint64_t)p);
+  if ((int)(h % 100u) < p_pct) return greedy;
+  return (greedy + 1 + (int)((h >> 8) % 255u)) & 255;
 }
 
 #ifdef __cplusplus

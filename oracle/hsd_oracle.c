@@ -761,3 +761,204 @@ int hsdo_window_features(const double* xyz, int n, const hsdo_metric_params* p, 
   *decision = hsdo_classify(*F, p->threshold);
   return 0;
 }
+
+#define HSD_MODE_HYBRID_O 0
+#define HSD_K_MAX_O 32
+#define HSD_HYB_MAX_EMIT_O 28
+
+/* ------------------------------------------------------- hybrid loop (config 5)
+ * SPEC.md:508-578 run_step per robot and round:
+ *   decide_sd: window_features over the trailing w points
+ *     (kinematics.cpp:261-273), cold start (< w points) -> drafter; pure modes
+ *     override;
+ *   retrieval_sd: retrieve_drafts (search_topk_exact over the
+ *     stored keys, payload = the demonstration policy tokens) -> should_skip
+ *      -> verify_tree;
+ *   drafter_sd: drafter_generate (toy drafter) -> verify;
+ *   emit + autoregressive completion of the action slice, ToyEnv position,
+ *   trajectory history, cost model. */
+static void hyb_window(const double* ring, int w, int n, double* out) {
+  for (int i = 0; i < w; ++i) {
+    int src = n >= w ? (n - w + i) % w : (i < n ? i : (n > 0 ? n - 1 : 0));
+    out[i * 3 + 0] = ring[src * 3 + 0];
+    out[i * 3 + 1] = ring[src * 3 + 1];
+    out[i * 3 + 2] = ring[src * 3 + 2];
+  }
+}
+
+static void hyb_query(const hsdo_hybrid_params* p, int64_t qid, int64_t row, int dim, float* q, int64_t* raw) {
+  const int kind = p->key_kind & ~HSDO_KEYS_BF16;
+  if (kind == HSD_SYNTH_EXACT) {
+    for (int c = 0; c < dim; ++c) q[c] = hsd_query_exact(p->seed, p->db_seed, qid, row, dim, c);
+    return;
+  }
+  int64_t ss = 0;
+  for (int c = 0; c < dim; ++c) {
+    raw[c] = hsd_query_raw(p->seed, p->db_seed, qid, row, dim, c);
+    ss += raw[c] * raw[c];
+  }
+  for (int c = 0; c < dim; ++c) q[c] = hsd_norm_val(raw[c], ss);
+}
+
+int hsdo_hybrid_run(const hsdo_hybrid_params* p, int64_t n_rows, int dim, int rounds, hsdo_step_record* trace,
+                    double* pos, hsdo_episode_report* rep) {
+  const int R = p->robots, w = p->metric.w, k = p->k, L = p->drafter_L;
+  const int64_t n_demo = n_rows / p->traj_T;
+  double* ring = (double*)calloc((size_t)R * w * 3, sizeof(double));
+  int* hist_n = (int*)calloc((size_t)R, sizeof(int));
+  int64_t* act = (int64_t*)calloc((size_t)R, sizeof(int64_t));
+  int* nrounds = (int*)calloc((size_t)R, sizeof(int));
+  int* modes = (int*)calloc((size_t)R, sizeof(int));
+  double* Fv = (double*)calloc((size_t)R, sizeof(double));
+  int* ret = (int*)malloc(sizeof(int) * (size_t)R);
+  float* qs = (float*)malloc(sizeof(float) * (size_t)R * dim);
+  int64_t* raw = (int64_t*)malloc(sizeof(int64_t) * (size_t)(dim > p->d_f ? dim : p->d_f) + 8);
+  double* sc = (double*)malloc(sizeof(double) * (size_t)R * k);
+  int64_t* ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)R * k);
+  float* fn = (float*)malloc(sizeof(float) * (size_t)(p->d_f > 0 ? p->d_f : 1));
+  float* fp = (float*)malloc(sizeof(float) * (size_t)(p->d_f > 0 ? p->d_f : 1));
+  hsdo_outcome* outs = (hsdo_outcome*)malloc(sizeof(hsdo_outcome) * (size_t)R);
+  const hsdo_accept_params ap = {p->relaxed, p->bias_seq_max, p->bias_token_max};
+  const hsdo_skip_state ss = {0.0, p->min_S, p->O_dist, 0.0, 0};
+  double win[3 * 32];
+  for (int r = 0; r < R; ++r) {
+    for (int d = 0; d < 3; ++d) pos[r * 3 + d] = ring[(size_t)r * w * 3 + d] = hsd_robot_start(p->seed, r, d);
+    hist_n[r] = 1;
+    memset(&rep[r], 0, sizeof(rep[r]));
+  }
+  for (int round = 0; round < rounds; ++round) {
+    int nr = 0;
+    for (int r = 0; r < R; ++r) {  /* decide_sd */
+      double Rk = 0, Dk = 0, F = 0;
+      int dec = 0;
+      hyb_window(ring + (size_t)r * w * 3, w, hist_n[r], win);
+      hsdo_window_features(win, w, &p->metric, &p->bounds, &Rk, &Dk, &F, &dec);
+      if (hist_n[r] < w) dec = 0; /* cold start */
+      Fv[r] = F;
+      if (p->mode == HSD_MODE_HYBRID_O)
+        modes[r] = dec == 1 ? 1 : 0;
+      else
+        modes[r] = p->mode == 1 ? 1 : (p->mode == 2 ? 0 : 2);
+      if (modes[r] == 1) ret[nr++] = r;
+    }
+    /* retrieve_drafts: one batched exact search over the stored keys */
+    for (int i = 0; i < nr; ++i) {
+      const int r = ret[i];
+      const int64_t e = hsd_robot_episode(p->seed, r, n_demo);
+      const int64_t row = hsd_hybrid_query_row(e, act[r], p->traj_T, n_demo, n_rows);
+      hyb_query(p, hsd_hybrid_qid(r, round), row, dim, qs + (size_t)i * dim, raw);
+    }
+    if (nr > 0) hsdo_search_synth(p->key_kind, p->db_seed, n_rows, dim, qs, nr, k, sc, ids, 0);
+    for (int i = 0; i < nr; ++i) { /* should_skip + verify_tree */
+      const int r = ret[i];
+      const int64_t e = hsd_robot_episode(p->seed, r, n_demo);
+      int greedy[21], drafts[HSD_K_MAX_O * 21], nc = 0;
+      for (int q = 0; q < 21; ++q) greedy[q] = hsd_robot_greedy(p->db_seed, p->seed, r, e, act[r] + q / 7, q % 7);
+      for (int c = 0; c < k; ++c) {
+        const int64_t id = ids[(size_t)i * k + c];
+        if (id < 0) continue;
+        for (int q = 0; q < 21; ++q)
+          drafts[nc * 21 + q] = hsd_policy_token(p->db_seed, id / p->traj_T, id % p->traj_T + q / 7, q % 7);
+        ++nc;
+      }
+      int skip = 0;
+      if (p->skip_enabled) {
+        hsdo_gen_features(p->seed, hsd_hybrid_qid(r, round), 1, p->d_f, fn, fp);
+        skip = hsdo_should_skip(hsdo_feature_cos(fn, fp, p->d_f), &ss, p->gap_d, nrounds[r]);
+      }
+      if (nc == 0) { /* empty shard: autoregressive for the step */
+        memset(&outs[r], 0, sizeof(outs[r]));
+        outs[r].calls = 1;
+        outs[r].fallback = 1;
+        outs[r].n_emit = 1;
+        outs[r].tokens[0] = greedy[0];
+      } else {
+        hsdo_verify_round(drafts, nc, 21, greedy, skip, p->chain_cap, &ap, &outs[r]);
+      }
+    }
+    for (int r = 0; r < R; ++r) { /* drafter_generate + verify */
+      if (modes[r] != 0) continue;
+      const int64_t e = hsd_robot_episode(p->seed, r, n_demo);
+      int greedy[21], draft[21];
+      for (int q = 0; q < L; ++q) {
+        greedy[q] = hsd_robot_greedy(p->db_seed, p->seed, r, e, act[r] + q / 7, q % 7);
+        draft[q] = hsd_drafter_token(p->seed, r, round, q, greedy[q], p->drafter_p_pct);
+      }
+      hsdo_verify_round(draft, 1, L, greedy, 0, p->chain_cap, &ap, &outs[r]);
+    }
+    for (int r = 0; r < R; ++r) { /* emit, ToyEnv, history, cost */
+      const int m = modes[r];
+      const int64_t e = hsd_robot_episode(p->seed, r, n_demo);
+      int toks[HSD_HYB_MAX_EMIT_O], n = 0, accepted = 0, calls = 0, skipped = 0, fallback = 0;
+      double cost = 0.0;
+      if (m == 0 || m == 1) {
+        const hsdo_outcome* o = &outs[r];
+        for (int i = 0; i < o->n_emit; ++i) toks[n++] = o->tokens[i];
+        accepted = o->accept_len;
+        calls = o->calls;
+        skipped = o->skipped;
+        fallback = o->fallback;
+        cost = m == 1 ? p->cost_retrieval : p->cost_drafter_token * (double)L;
+      }
+      const int target = n == 0 ? 7 : ((n + 6) / 7) * 7;
+      while (n < target) {
+        toks[n] = hsd_robot_greedy(p->db_seed, p->seed, r, e, act[r] + n / 7, n % 7);
+        ++n;
+        ++calls;
+      }
+      cost = cost + (double)calls * p->cost_verifier;
+      double* rg = ring + (size_t)r * w * 3;
+      for (int a = 0; a < n / 7; ++a) {
+        for (int d = 0; d < 3; ++d) pos[r * 3 + d] = pos[r * 3 + d] + HSD_ENV_SCALE * hsd_dequantize_bin(toks[a * 7 + d], -1.0, 1.0, 256);
+        const int sw = hist_n[r] % w;
+        rg[sw * 3 + 0] = pos[r * 3 + 0];
+        rg[sw * 3 + 1] = pos[r * 3 + 1];
+        rg[sw * 3 + 2] = pos[r * 3 + 2];
+        ++hist_n[r];
+      }
+      act[r] += n / 7;
+      nrounds[r] += 1;
+      rep[r].rounds += 1;
+      rep[r].tokens += n;
+      rep[r].accepted += accepted;
+      rep[r].verifier_calls += calls;
+      rep[r].cost += cost;
+      rep[r].n_retrieval += m == 1;
+      rep[r].n_drafter += m == 0;
+      rep[r].n_skipped += skipped;
+      rep[r].n_fallback += fallback;
+      if (trace) {
+        hsdo_step_record* t = &trace[(size_t)round * R + r];
+        t->F = m == 2 ? -1.0f : (float)Fv[r];
+        t->accept_len = (int16_t)accepted;
+        t->verifier_calls = (int16_t)calls;
+        t->n_emit = (int16_t)n;
+        t->mode = (int8_t)m;
+        t->skipped = (int8_t)skipped;
+        t->cost = (float)cost;
+      }
+    }
+  }
+  free(ring);
+  free(hist_n);
+  free(act);
+  free(nrounds);
+  free(modes);
+  free(Fv);
+  free(ret);
+  free(qs);
+  free(raw);
+  free(sc);
+  free(ids);
+  free(fn);
+  free(fp);
+  free(outs);
+  return 0;
+}
+
+int hsdo_policy_token(uint64_t db_seed, int64_t e, int64_t j, int d) { return hsd_policy_token(db_seed, e, j, d); }
+int hsdo_robot_greedy(uint64_t db_seed, uint64_t seed, int64_t r, int64_t n_demo, int64_t j, int d) {
+  return hsd_robot_greedy(db_seed, seed, r, hsd_robot_episode(seed, r, n_demo), j, d);
+}
+double hsdo_robot_start(uint64_t seed, int64_t r, int d) { return hsd_robot_start(seed, r, d); }
+double hsdo_dequantize_bin(int bin, double lo, double hi, int k_bins) { return hsd_dequantize_bin(bin, lo, hi, k_bins); }

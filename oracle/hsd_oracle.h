@@ -164,6 +164,47 @@ int hsdo_classify(double F, double threshold); /* :257-259; 1 = retrieval_sd, 0 
 int hsdo_window_features(const double* xyz, int n, const hsdo_metric_params* p, const hsdo_norm_bounds* b, double* R,
                          double* D, double* F, int* decision);
 
+/* ------------------------------------------------------- hybrid loop (config 5)
+ * run_step / run_episode of the SPEC scheduler for R robots,
+ * sequentially, over the counter-based harness of hsd_synth.h (demonstration
+ * policy rows, robots, toy drafter, ToyEnv).  Restates the device loop
+ * (k_hybrid.cu + api.cu hsd_hybrid_step) for parity; the record layouts are
+ * those of include/hsd/hsd_gpu.h. */
+typedef struct {
+  int robots, k, mode, traj_T, drafter_p_pct, drafter_L, gap_d, d_f;
+  uint64_t seed, db_seed;
+  int key_kind;  /* may carry HSDO_KEYS_BF16 */
+  int relaxed, bias_seq_max, bias_token_max, skip_enabled, O_dist, chain_cap;
+  double min_S;
+  hsdo_metric_params metric;
+  hsdo_norm_bounds bounds;
+  double cost_verifier, cost_drafter_token, cost_retrieval;
+} hsdo_hybrid_params;
+
+typedef struct {
+  float F;
+  int16_t accept_len, verifier_calls, n_emit;
+  int8_t mode, skipped;
+  float cost;
+} hsdo_step_record;
+
+typedef struct {
+  int64_t rounds, tokens, accepted, verifier_calls;
+  double cost;
+  int32_t n_retrieval, n_drafter, n_skipped, n_fallback;
+} hsdo_episode_report;
+
+/* DB: n_rows synthetic rows of family key_kind (dim) with TRAJ payloads.
+ * Outputs: trace [rounds][R] (or NULL), pos [R][3], reports [R]. */
+/* Demonstration policy token (hsd_synth.h hsd_policy_token). */
+int hsdo_policy_token(uint64_t db_seed, int64_t e, int64_t j, int d);
+int hsdo_robot_greedy(uint64_t db_seed, uint64_t seed, int64_t r, int64_t n_demo, int64_t j, int d);
+double hsdo_robot_start(uint64_t seed, int64_t r, int d);
+/* dequantize of one bin, actions.cpp:52-66 */
+double hsdo_dequantize_bin(int bin, double lo, double hi, int k_bins);
+int hsdo_hybrid_run(const hsdo_hybrid_params* p, int64_t n_rows, int dim, int rounds, hsdo_step_record* trace,
+                    double* pos, hsdo_episode_report* reports);
+
 #ifdef __cplusplus
 }
 #endif

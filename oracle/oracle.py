@@ -61,6 +61,61 @@ class NormBounds(C.Structure):
     _fields_ = [("d_min", C.c_double), ("d_max95", C.c_double), ("r_min", C.c_double), ("r_max95", C.c_double)]
 
 
+class HybridParams(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("robots", "k", "mode", "traj_T", "drafter_p_pct", "drafter_L", "gap_d", "d_f")] + [
+        ("seed", C.c_uint64), ("db_seed", C.c_uint64), ("key_kind", C.c_int)] + [
+        (n, C.c_int) for n in ("relaxed", "bias_seq_max", "bias_token_max", "skip_enabled", "O_dist", "chain_cap")] + [
+        ("min_S", C.c_double), ("metric", MetricParams), ("bounds", NormBounds), ("cost_verifier", C.c_double),
+        ("cost_drafter_token", C.c_double), ("cost_retrieval", C.c_double)]
+
+
+STEP_RECORD_DTYPE = np.dtype([("F", np.float32), ("accept_len", np.int16), ("verifier_calls", np.int16),
+                              ("n_emit", np.int16), ("mode", np.int8), ("skipped", np.int8), ("cost", np.float32)])
+EPISODE_REPORT_DTYPE = np.dtype([("rounds", np.int64), ("tokens", np.int64), ("accepted", np.int64),
+                                 ("verifier_calls", np.int64), ("cost", np.float64), ("n_retrieval", np.int32),
+                                 ("n_drafter", np.int32), ("n_skipped", np.int32), ("n_fallback", np.int32)])
+
+
+def hybrid_run(params: HybridParams, n_rows: int, dim: int, rounds: int):
+    """Oracle hybrid loop (hsdo_hybrid_run) -> (trace [rounds, R], pos [R, 3], reports [R])."""
+    R = params.robots
+    trace = np.zeros(rounds * R, STEP_RECORD_DTYPE)
+    pos = np.zeros((R, 3), np.float64)
+    rep = np.zeros(R, EPISODE_REPORT_DTYPE)
+    rc = lib().hsdo_hybrid_run(C.byref(params), n_rows, dim, rounds, trace.ctypes.data, pos.ctypes.data,
+                               rep.ctypes.data)
+    assert rc == 0, rc
+    return trace.reshape(rounds, R), pos, rep
+
+
+def policy_token(db_seed: int, e: int, j: int, d: int) -> int:
+    return lib().hsdo_policy_token(db_seed, e, j, d)
+
+
+def robot_greedy(db_seed, seed, r, n_demo, j, d) -> int:
+    return lib().hsdo_robot_greedy(db_seed, seed, r, n_demo, j, d)
+
+
+def robot_start(seed, r, d) -> float:
+    return lib().hsdo_robot_start(seed, r, d)
+
+
+def dequantize_bin(b, lo=-1.0, hi=1.0, k_bins=256) -> float:
+    return lib().hsdo_dequantize_bin(b, lo, hi, k_bins)
+
+
+ENV_SCALE = 0.01  # HSD_ENV_SCALE
+
+
+def ar_position(db_seed, seed, r, n_demo, n_actions):
+    """ToyEnv position after the robot's first n_actions greedy (verifier) actions: the autoregressive trajectory."""
+    p = [robot_start(seed, r, d) for d in range(3)]
+    for j in range(n_actions):
+        for d in range(3):
+            p[d] = p[d] + ENV_SCALE * dequantize_bin(robot_greedy(db_seed, seed, r, n_demo, j, d))
+    return np.array(p)
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -104,6 +159,16 @@ def lib():
         L.hsdo_window_features.argtypes = [_d, C.c_int, C.POINTER(MetricParams), C.POINTER(NormBounds),
                                            C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
                                            C.POINTER(C.c_int)]
+        L.hsdo_hybrid_run.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.hsdo_hybrid_run.restype = C.c_int
+        L.hsdo_policy_token.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int]
+        L.hsdo_policy_token.restype = C.c_int
+        L.hsdo_robot_greedy.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_int]
+        L.hsdo_robot_greedy.restype = C.c_int
+        L.hsdo_robot_start.argtypes = [C.c_uint64, C.c_int64, C.c_int]
+        L.hsdo_robot_start.restype = C.c_double
+        L.hsdo_dequantize_bin.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int]
+        L.hsdo_dequantize_bin.restype = C.c_double
         _lib = L
     return _lib
 

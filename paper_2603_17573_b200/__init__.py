@@ -114,6 +114,24 @@ class NormBounds(C.Structure):
     _fields_ = [("d_min", C.c_double), ("d_max95", C.c_double), ("r_min", C.c_double), ("r_max95", C.c_double)]
 
 
+class HybridParams(C.Structure):
+    """hsd_hybrid_params (include/hsd/hsd_gpu.h): HybridConfig + CostModel of the SPEC scheduler."""
+    _fields_ = [(n, C.c_int32) for n in ("robots", "k", "mode", "traj_T", "drafter_p_pct", "drafter_L", "gap_d",
+                                         "d_f")] + [
+        ("seed", C.c_uint64), ("db_seed", C.c_uint64), ("key_kind", C.c_int32), ("record_trace", C.c_int32),
+        ("verify", VerifyParams), ("metric", MetricParams), ("bounds", NormBounds), ("cost_verifier", C.c_double),
+        ("cost_drafter_token", C.c_double), ("cost_retrieval", C.c_double)]
+
+
+STEP_RECORD_DTYPE = np.dtype([("F", np.float32), ("accept_len", np.int16), ("verifier_calls", np.int16),
+                              ("n_emit", np.int16), ("mode", np.int8), ("skipped", np.int8), ("cost", np.float32)])
+EPISODE_REPORT_DTYPE = np.dtype([("rounds", np.int64), ("tokens", np.int64), ("accepted", np.int64),
+                                 ("verifier_calls", np.int64), ("cost", np.float64), ("n_retrieval", np.int32),
+                                 ("n_drafter", np.int32), ("n_skipped", np.int32), ("n_fallback", np.int32)])
+MODE_HYBRID, MODE_PURE_RETRIEVAL, MODE_PURE_DRAFTER, MODE_AUTOREGRESSIVE = 0, 1, 2, 3
+PAYLOAD_RANDOM, PAYLOAD_TRAJ = 0, 1
+
+
 class StepIO(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("queries", "logits", "feat_now", "feat_prev", "xyz", "history", "scores",
                                           "ids", "out", "tokens", "R", "D", "F", "decision")]
@@ -184,6 +202,14 @@ def lib():
                             _vp],
         "hsd_gen_logits": [_vp, C.c_uint64, _vp, C.c_int, C.c_int, _vp, _vp],
         "hsd_gen_features": [C.c_int, C.c_uint64, C.c_int, C.c_int, _vp, _vp, _vp],
+        "hsd_collection_generate_ex": [_vp, C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int],
+        "hsd_hybrid_create": [_vp, _vp, C.c_int64, C.c_int64, C.POINTER(HybridParams), C.c_int, C.POINTER(_vp)],
+        "hsd_hybrid_destroy": [_vp],
+        "hsd_hybrid_step": [_vp, C.c_int, _vp],
+        "hsd_hybrid_positions": [_vp, _vp],
+        "hsd_hybrid_reports": [_vp, _vp],
+        "hsd_hybrid_trace": [_vp, _vp, C.POINTER(C.c_int)],
+        "hsd_hybrid_counts": [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -288,9 +314,13 @@ class Collection:
                                           None if st is None else st.ctypes.data, emb.shape[0], C.byref(first)))
         return first.value
 
-    def generate(self, kind: int, db_seed: int, n: int, row0=None) -> None:
-        """Append n counter-generated records; row0 selects global synthetic rows (DB shards)."""
-        if row0 is None:
+    def generate(self, kind: int, db_seed: int, n: int, row0=None, payload=PAYLOAD_RANDOM, traj_T=0) -> None:
+        """Append n counter-generated records; row0 selects global synthetic rows (DB shards);
+        payload=PAYLOAD_TRAJ stores demonstration-policy drafts (row = e * traj_T + j)."""
+        if payload != PAYLOAD_RANDOM:
+            check(lib().hsd_collection_generate_ex(self._h, kind, db_seed, self.size() if row0 is None else row0, n,
+                                                   payload, traj_T))
+        elif row0 is None:
             check(lib().hsd_collection_generate(self._h, kind, db_seed, n))
         else:
             check(lib().hsd_collection_generate_rows(self._h, kind, db_seed, row0, n))
@@ -609,3 +639,67 @@ class Engine:
         io = bufs.io()
         check(lib().hsd_step_host(self._h, B, C.byref(io), C.byref(vp), C.byref(mp), C.byref(nb), gap_d,
                                   _stream(stream)))
+
+
+# --------------------------------------------------------------------------- hybrid loop (config 5)
+def hybrid_params(robots, k=3, mode=MODE_HYBRID, traj_T=500, drafter_p_pct=85, drafter_L=7, gap_d=1, d_f=4096,
+                  seed=1, db_seed=2026, key_kind=REAL, record_trace=True, verify=None, metric=None, bounds=None,
+                  cost_verifier=1.0, cost_drafter_token=0.1, cost_retrieval=0.37) -> HybridParams:
+    """HybridConfig defaults of the SPEC: K_top 3, p 0.85, L 7, relaxed 30/15,
+    verify-skip min_S 0.95 / O_dist 5, cost 1.0 / 0.1 / 0.37."""
+    if verify is None:
+        verify = VerifyParams.make(relaxed=True, bias_seq_max=30, bias_token_max=15, skip_enabled=d_f > 0,
+                                   min_S=0.95, O_dist=5)
+    return HybridParams(robots, k, mode, traj_T, drafter_p_pct, drafter_L, gap_d, d_f, seed, db_seed, key_kind,
+                        int(record_trace), verify, metric or DEFAULT_METRIC, bounds or LIBERO_GOAL, cost_verifier,
+                        cost_drafter_token, cost_retrieval)
+
+
+class HybridLoop:
+    """Device-resident run_step / run_episode for many robots (hsd_hybrid_*)."""
+
+    def __init__(self, col: Collection, params: HybridParams, n_total_rows=None, max_rounds=0, comm=None,
+                 id_offset=0):
+        self._h = C.c_void_p()
+        self.params = params
+        self.R = params.robots
+        n_total = col.size() if n_total_rows is None else n_total_rows
+        check(lib().hsd_hybrid_create(col.handle, None if comm is None else comm._h, id_offset, n_total,
+                                      C.byref(params), max_rounds, C.byref(self._h)))
+        self.col = col
+
+    def close(self):
+        if self._h:
+            lib().hsd_hybrid_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, n_rounds=1, stream=None):
+        check(lib().hsd_hybrid_step(self._h, n_rounds, _stream(stream)))
+
+    def positions(self):
+        out = np.zeros((self.R, 3), np.float64)
+        check(lib().hsd_hybrid_positions(self._h, out.ctypes.data))
+        return out
+
+    def reports(self):
+        out = np.zeros(self.R, EPISODE_REPORT_DTYPE)
+        check(lib().hsd_hybrid_reports(self._h, out.ctypes.data))
+        return out
+
+    def trace(self):
+        n = C.c_int()
+        check(lib().hsd_hybrid_trace(self._h, None, C.byref(n)))
+        out = np.zeros(n.value * self.R, STEP_RECORD_DTYPE)
+        check(lib().hsd_hybrid_trace(self._h, out.ctypes.data if n.value else None, C.byref(n)))
+        return out.reshape(n.value, self.R)
+
+    def counts(self):
+        a, b = C.c_int64(), C.c_int64()
+        check(lib().hsd_hybrid_counts(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value

@@ -14,6 +14,7 @@
 
 #include "common.cuh"
 #include "hsd/hsd_gpu.h"
+#include "hsd/hsd_synth.h"
 #include "kernels.h"
 
 namespace {
@@ -437,7 +438,15 @@ hsd_status hsd_collection_generate(hsd_collection* c, int kind, uint64_t db_seed
 }
 
 hsd_status hsd_collection_generate_rows(hsd_collection* c, int kind, uint64_t db_seed, int64_t row0, int64_t n) {
+  return hsd_collection_generate_ex(c, kind, db_seed, row0, n, HSD_PAYLOAD_RANDOM, 0);
+}
+
+hsd_status hsd_collection_generate_ex(hsd_collection* c, int kind, uint64_t db_seed, int64_t row0, int64_t n,
+                                      int payload, int traj_T) {
   if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
+  if (payload != HSD_PAYLOAD_RANDOM && payload != HSD_PAYLOAD_TRAJ)
+    return fail(HSD_ERR_CONFIG, "unknown payload family %d", payload);
+  if (payload == HSD_PAYLOAD_TRAJ && traj_T < 1) return fail(HSD_ERR_CONFIG, "traj_T must be >= 1");
   if (row0 < 0) return fail(HSD_ERR_INVALID_INPUT, "negative row offset");
   if (kind != 0 && kind != 1) return fail(HSD_ERR_CONFIG, "unknown synthetic family %d", kind);
   if (n < 0) return fail(HSD_ERR_INVALID_INPUT, "negative record count");
@@ -447,7 +456,7 @@ hsd_status hsd_collection_generate_rows(hsd_collection* c, int kind, uint64_t db
   st = ensure_capacity(c, c->n + n);
   if (st != HSD_OK) return st;
   CU(hsd::launch_gen_keys(kind, db_seed, row0, n, c->dim, (uint8_t*)c->keys + (size_t)c->n * c->dim * key_bytes(c),
-                          c->dtype, c->tokens + (size_t)c->n * HSD_TOKENS_STRIDE, c->maxnorm, 0));
+                          c->dtype, c->tokens + (size_t)c->n * HSD_TOKENS_STRIDE, c->maxnorm, payload, traj_T, 0));
   CU(cudaDeviceSynchronize());
   c->n += n;
   return HSD_OK;
@@ -1032,6 +1041,235 @@ hsd_status hsd_gen_features(int device, uint64_t seed, int E, int d_f, float* no
   hsd_status st = require_device(device);
   if (st != HSD_OK) return st;
   CU(hsd::launch_gen_features(seed, E, d_f, now, prev, (cudaStream_t)stream));
+  return HSD_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ hybrid loop (config 5)
+struct hsd_hybrid {
+  hsd_collection* c = nullptr;
+  hsd_comm* comm = nullptr;
+  int64_t id_offset = 0, n_total = 0;
+  hsd_hybrid_params p{};
+  int R = 0, w = 0, max_rounds = 0, round = 0;
+  hsd::HybridArgs a{};
+  // per-robot state (a.* pointers) + per-round scratch
+  double *xyz = nullptr, *Rk = nullptr, *Dk = nullptr, *Fk = nullptr;
+  int32_t *histw = nullptr, *dec = nullptr, *modes = nullptr, *slot = nullptr, *ret_idx = nullptr, *drf_idx = nullptr,
+          *counts = nullptr, *hist_c = nullptr, *ids = nullptr, *ids_d = nullptr;
+  float *q = nullptr, *fnow = nullptr, *fprev = nullptr, *lg_r = nullptr, *lg_d = nullptr;
+  double* scores = nullptr;
+  uint8_t *drafts = nullptr, *drafts_d = nullptr, *tok_r = nullptr, *tok_d = nullptr;
+  hsd_outcome *out_r = nullptr, *out_d = nullptr;
+  hsd_step_record* trace = nullptr;
+  int32_t* h_counts = nullptr;  // pinned
+  int64_t n_ret_queries = 0, n_drf_rounds = 0;
+  std::vector<void*> allocs;
+};
+
+extern "C" {
+
+hsd_status hsd_hybrid_destroy(hsd_hybrid* h) {
+  if (!h) return HSD_OK;
+  cudaSetDevice(h->c->device);
+  cudaDeviceSynchronize();
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->h_counts) cudaFreeHost(h->h_counts);
+  delete h;
+  return HSD_OK;
+}
+
+hsd_status hsd_hybrid_create(hsd_collection* c, hsd_comm* comm, int64_t id_offset, int64_t n_total_rows,
+                             const hsd_hybrid_params* p, int max_rounds, hsd_hybrid** out) {
+  if (!c || !p || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *out = nullptr;
+  if (p->robots < 1 || p->robots > (1 << 20)) return fail(HSD_ERR_CONFIG, "robots must lie in [1, 2^20]");
+  if (p->k < 1 || p->k > HSD_K_MAX) return fail(HSD_ERR_CONFIG, "K_top must lie in [1, %d]", HSD_K_MAX);
+  if (p->mode < HSD_MODE_HYBRID || p->mode > HSD_MODE_AUTOREGRESSIVE) return fail(HSD_ERR_CONFIG, "unknown mode");
+  if (p->traj_T < 1) return fail(HSD_ERR_CONFIG, "traj_T must be >= 1");
+  if (p->drafter_L != 7 && p->drafter_L != 21) return fail(HSD_ERR_CONFIG, "drafter L must be 7 or 21");
+  if (p->drafter_p_pct < 0 || p->drafter_p_pct > 100) return fail(HSD_ERR_CONFIG, "drafter p must lie in [0, 100]");
+  if (p->gap_d < 1) return fail(HSD_ERR_CONFIG, "gap d must be >= 1");
+  if (p->d_f < 0 || p->d_f % 4) return fail(HSD_ERR_CONFIG, "d_f must be a nonnegative multiple of 4");
+  if (p->verify.skip_enabled && p->d_f == 0) return fail(HSD_ERR_CONFIG, "verify-skip needs d_f > 0");
+  if (!(p->cost_verifier >= 0 && p->cost_drafter_token >= 0 && p->cost_retrieval >= 0))
+    return fail(HSD_ERR_CONFIG, "cost weights must be >= 0");  // CostModel invariant
+  if (max_rounds < 0) return fail(HSD_ERR_INVALID_INPUT, "negative trace capacity");
+  hsd_status st = check_metric(&p->metric, &p->bounds);
+  if (st != HSD_OK) return st;
+  st = check_verify_params(&p->verify, 1);
+  if (st != HSD_OK) return st;
+  st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  auto* h = new hsd_hybrid();
+  h->c = c;
+  h->comm = comm;
+  h->id_offset = id_offset;
+  h->n_total = n_total_rows;
+  h->p = *p;
+  h->R = p->robots;
+  h->w = p->metric.w;
+  h->max_rounds = p->record_trace ? max_rounds : 0;
+  const int R = h->R, w = h->w, k = p->k, L = p->drafter_L, dim = c->dim, d_f = p->d_f;
+  cudaError_t e = cudaSuccess;
+  auto alloc = [&](auto** ptr, size_t bytes) {
+    if (e != cudaSuccess) return;
+    e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) h->allocs.push_back((void*)*ptr);
+  };
+  hsd::HybridArgs& a = h->a;
+  alloc(&a.pos, (size_t)R * 3 * 8);
+  alloc(&a.ring, (size_t)R * w * 3 * 8);
+  alloc(&a.hist_n, (size_t)R * 4);
+  alloc(&a.act, (size_t)R * 8);
+  alloc(&a.rounds, (size_t)R * 4);
+  alloc(&a.report, (size_t)R * sizeof(hsd_episode_report));
+  alloc(&h->xyz, (size_t)R * w * 3 * 8);
+  alloc(&h->histw, (size_t)R * 4);
+  alloc(&h->Rk, (size_t)R * 8);
+  alloc(&h->Dk, (size_t)R * 8);
+  alloc(&h->Fk, (size_t)R * 8);
+  alloc(&h->dec, (size_t)R * 4);
+  alloc(&h->modes, (size_t)R * 4);
+  alloc(&h->slot, (size_t)R * 4);
+  alloc(&h->ret_idx, (size_t)R * 4);
+  alloc(&h->drf_idx, (size_t)R * 4);
+  alloc(&h->counts, 8);
+  alloc(&h->hist_c, (size_t)R * 4);
+  alloc(&h->q, (size_t)R * dim * 4);
+  alloc(&h->fnow, (size_t)R * d_f * 4);
+  alloc(&h->fprev, (size_t)R * d_f * 4);
+  alloc(&h->lg_r, (size_t)R * HSD_HYB_RET_L * 256 * 4);
+  alloc(&h->scores, (size_t)R * k * 8);
+  alloc(&h->ids, (size_t)R * k * 4);
+  alloc(&h->drafts, (size_t)R * k * HSD_TOKENS_STRIDE);
+  alloc(&h->out_r, (size_t)R * sizeof(hsd_outcome));
+  alloc(&h->tok_r, (size_t)R * HSD_HYB_RET_L);
+  alloc(&h->lg_d, (size_t)R * L * 256 * 4);
+  alloc(&h->drafts_d, (size_t)R * HSD_TOKENS_STRIDE);
+  alloc(&h->ids_d, (size_t)R * 4);
+  alloc(&h->out_d, (size_t)R * sizeof(hsd_outcome));
+  alloc(&h->tok_d, (size_t)R * L);
+  if (h->max_rounds) alloc(&h->trace, (size_t)h->max_rounds * R * sizeof(hsd_step_record));
+  if (e == cudaSuccess) e = cudaMallocHost(&h->h_counts, 2 * sizeof(int32_t));
+  if (e != cudaSuccess) {
+    hsd_hybrid_destroy(h);
+    return cuda_fail(e, "hybrid buffers");
+  }
+  a.R = R;
+  a.w = w;
+  a.dim = dim;
+  a.d_f = d_f;
+  a.key_kind = p->key_kind;
+  a.traj_T = p->traj_T;
+  a.drafter_p_pct = p->drafter_p_pct;
+  a.drafter_L = L;
+  a.seed = p->seed;
+  a.db_seed = p->db_seed;
+  a.n_rows = n_total_rows;
+  a.n_demo = n_total_rows / p->traj_T;
+  a.cost_verifier = p->cost_verifier;
+  a.cost_drafter_token = p->cost_drafter_token;
+  a.cost_retrieval = p->cost_retrieval;
+  e = hsd::launch_hyb_init(a, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    hsd_hybrid_destroy(h);
+    return cuda_fail(e, "hybrid init");
+  }
+  *out = h;
+  return HSD_OK;
+}
+
+hsd_status hsd_hybrid_step(hsd_hybrid* h, int n_rounds, void* stream) {
+  if (!h) return fail(HSD_ERR_INVALID_INPUT, "null hybrid loop");
+  if (n_rounds < 0) return fail(HSD_ERR_INVALID_INPUT, "negative round count");
+  hsd_status st = require_device(h->c->device);
+  if (st != HSD_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const hsd_hybrid_params& p = h->p;
+  const int R = h->R, k = p.k, L = p.drafter_L;
+  hsd_verify_params vp_drf = p.verify;
+  vp_drf.skip_enabled = 0;  // verify-skip is retrieval-mode only
+  for (int it = 0; it < n_rounds; ++it) {
+    const int round = h->round;
+    // decide_sd for every robot (K5 over the trailing window; cold start -> drafter)
+    CU(hsd::launch_hyb_windows(R, h->w, h->a.ring, h->a.hist_n, h->xyz, h->histw, s));
+    CU(hsd::launch_kinematics(h->xyz, R, p.metric, p.bounds, h->histw, h->Rk, h->Dk, h->Fk, h->dec, s));
+    CU(hsd::launch_hyb_compact(R, p.mode, h->dec, h->modes, h->slot, h->ret_idx, h->drf_idx, h->counts, s));
+    CU(cudaMemcpyAsync(h->h_counts, h->counts, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const int nr = h->h_counts[0], nd = h->h_counts[1];
+    if (nr > 0) {  // retrieval_sd robots: retrieve_drafts -> should_skip -> verify_tree
+      CU(hsd::launch_hyb_prep_ret(h->a, round, h->ret_idx, nr, h->q, h->fnow, h->fprev, h->hist_c, s));
+      CU(hsd::launch_hyb_logits(h->a, round, h->ret_idx, nr, HSD_HYB_RET_L, h->lg_r, s));
+      const float* fn = p.d_f ? h->fnow : nullptr;
+      const float* fp = p.d_f ? h->fprev : nullptr;
+      if (h->comm) {
+        st = hsd_search_topk_sharded(h->c, h->comm, h->id_offset, h->q, nr, k, h->scores, h->ids, h->drafts, s);
+        if (st != HSD_OK) return st;
+        st = verify_impl(h->c->device, nullptr, h->drafts, h->ids, nr, k, HSD_HYB_RET_L, h->lg_r, fn, fp, p.d_f,
+                         h->hist_c, p.gap_d, &p.verify, 1, h->out_r, h->tok_r, s);
+      } else {
+        st = search_impl(h->c, h->q, nr, k, 0, h->c->n, h->scores, h->ids, s);
+        if (st != HSD_OK) return st;
+        st = verify_impl(h->c->device, h->c, nullptr, h->ids, nr, k, HSD_HYB_RET_L, h->lg_r, fn, fp, p.d_f, h->hist_c,
+                         p.gap_d, &p.verify, 1, h->out_r, h->tok_r, s);
+      }
+      if (st != HSD_OK) return st;
+    }
+    if (nd > 0) {  // drafter_sd robots: drafter_generate -> verify (one candidate)
+      CU(hsd::launch_hyb_drafts(h->a, round, h->drf_idx, nd, L, h->drafts_d, h->ids_d, s));
+      CU(hsd::launch_hyb_logits(h->a, round, h->drf_idx, nd, L, h->lg_d, s));
+      st = verify_impl(h->c->device, nullptr, h->drafts_d, h->ids_d, nd, 1, L, h->lg_d, nullptr, nullptr, 0, nullptr,
+                       p.gap_d, &vp_drf, 1, h->out_d, h->tok_d, s);
+      if (st != HSD_OK) return st;
+    }
+    hsd_step_record* tr = round < h->max_rounds ? h->trace : nullptr;
+    CU(hsd::launch_hyb_emit(h->a, round, h->modes, h->slot, h->out_r, h->tok_r, h->out_d, h->tok_d, h->Fk, tr, s));
+    h->n_ret_queries += nr;
+    h->n_drf_rounds += nd;
+    ++h->round;
+  }
+  return HSD_OK;
+}
+
+hsd_status hsd_hybrid_positions(hsd_hybrid* h, double* xyz) {
+  if (!h || !xyz) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(h->c->device);
+  if (st != HSD_OK) return st;
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(xyz, h->a.pos, (size_t)h->R * 3 * 8, cudaMemcpyDeviceToHost));
+  return HSD_OK;
+}
+
+hsd_status hsd_hybrid_reports(hsd_hybrid* h, hsd_episode_report* out) {
+  if (!h || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(h->c->device);
+  if (st != HSD_OK) return st;
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(out, h->a.report, (size_t)h->R * sizeof(hsd_episode_report), cudaMemcpyDeviceToHost));
+  return HSD_OK;
+}
+
+hsd_status hsd_hybrid_trace(hsd_hybrid* h, hsd_step_record* out, int* rounds) {
+  if (!h || !rounds) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(h->c->device);
+  if (st != HSD_OK) return st;
+  const int n = std::min(h->round, h->max_rounds);
+  *rounds = n;
+  if (out && n > 0) {
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(out, h->trace, (size_t)n * h->R * sizeof(hsd_step_record), cudaMemcpyDeviceToHost));
+  }
+  return HSD_OK;
+}
+
+hsd_status hsd_hybrid_counts(hsd_hybrid* h, int64_t* retrieval_queries, int64_t* drafter_rounds) {
+  if (!h) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (retrieval_queries) *retrieval_queries = h->n_ret_queries;
+  if (drafter_rounds) *drafter_rounds = h->n_drf_rounds;
   return HSD_OK;
 }
 

@@ -45,7 +45,8 @@ __device__ __forceinline__ float store_key(uint16_t* p, float v) {
 template <typename KT>
 __global__ void __launch_bounds__(kGenThreads) gen_keys_kernel(int kind, uint64_t db_seed, int64_t row0, int dim,
                                                                KT* __restrict__ keys, uint8_t* __restrict__ tokens,
-                                                               unsigned long long* maxnorm_bits) {
+                                                               unsigned long long* maxnorm_bits, int payload,
+                                                               int traj_T) {
   using BR = cub::BlockReduce<long long, kGenThreads>;
   using BRD = cub::BlockReduce<double, kGenThreads>;
   __shared__ union {
@@ -85,7 +86,10 @@ __global__ void __launch_bounds__(kGenThreads) gen_keys_kernel(int kind, uint64_
     uint8_t t = 0;
     if (threadIdx.x < 21) {
       const int s = threadIdx.x / 7, j = threadIdx.x % 7;
-      t = (uint8_t)quantize_one(hsd_action_val(db_seed, row, s, j), -1.0, 1.0, 256);
+      if (payload == HSD_PAYLOAD_TRAJ)  // demonstration row (e, jj): next_actions[s] = policy(e, jj + s)
+        t = (uint8_t)hsd_policy_token(db_seed, row / traj_T, row % traj_T + s, j);
+      else
+        t = (uint8_t)quantize_one(hsd_action_val(db_seed, row, s, j), -1.0, 1.0, 256);
     }
     tokens[(size_t)blockIdx.x * HSD_TOKENS_STRIDE + threadIdx.x] = t;
   }
@@ -206,18 +210,19 @@ __global__ void quantize_tokens_kernel(const double* __restrict__ a, int64_t n, 
 }  // namespace
 
 cudaError_t launch_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, void* keys, int key_dtype,
-                            uint8_t* tokens, unsigned long long* maxnorm_bits, cudaStream_t s) {
+                            uint8_t* tokens, unsigned long long* maxnorm_bits, int payload, int traj_T,
+                            cudaStream_t s) {
   constexpr int64_t kChunk = 1 << 20;
   for (int64_t r = 0; r < n; r += kChunk) {
     const int64_t m = n - r < kChunk ? n - r : kChunk;
     if (key_dtype == HSD_DTYPE_BF16)
       gen_keys_kernel<uint16_t><<<(unsigned)m, kGenThreads, 0, s>>>(
           kind, db_seed, row0 + r, dim, (uint16_t*)keys + (size_t)r * dim, tokens + (size_t)r * HSD_TOKENS_STRIDE,
-          maxnorm_bits);
+          maxnorm_bits, payload, traj_T);
     else
       gen_keys_kernel<float><<<(unsigned)m, kGenThreads, 0, s>>>(
           kind, db_seed, row0 + r, dim, (float*)keys + (size_t)r * dim, tokens + (size_t)r * HSD_TOKENS_STRIDE,
-          maxnorm_bits);
+          maxnorm_bits, payload, traj_T);
   }
   return cudaGetLastError();
 }

@@ -10,8 +10,11 @@ namespace hsd {
 
 // ---- K0 synthetic generators (k_synth.cu) ------------------------------------
 // keys: fp32 or bf16 (key_dtype = HSD_DTYPE_*) row-major [n][dim]
+// payload: HSD_PAYLOAD_RANDOM (quantized hsd_action_val) or HSD_PAYLOAD_TRAJ
+// (demonstration policy tokens, rows of traj_T actions per episode)
 cudaError_t launch_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, void* keys, int key_dtype,
-                            uint8_t* tokens, unsigned long long* maxnorm_bits, cudaStream_t s);
+                            uint8_t* tokens, unsigned long long* maxnorm_bits, int payload, int traj_T,
+                            cudaStream_t s);
 cudaError_t launch_row_norms(const void* keys, int key_dtype, int64_t row0, int64_t n, int dim,
                              unsigned long long* maxnorm_bits, cudaStream_t s);
 cudaError_t launch_to_bf16(const float* in, int64_t n, uint16_t* out, cudaStream_t s);
@@ -86,5 +89,33 @@ cudaError_t launch_gather_tokens(const uint8_t* tokens, const int32_t* ids, int 
 cudaError_t launch_kinematics(const double* xyz, int W, const hsd_metric_params& mp, const hsd_norm_bounds& nb,
                               const int32_t* history, double* R, double* D, double* F, int32_t* decision,
                               cudaStream_t s);
+
+// ---- hybrid decoding loop (k_hybrid.cu) ----------------------------------------
+struct HybridArgs {
+  int R, w, dim, d_f, key_kind, traj_T, drafter_p_pct, drafter_L;
+  uint64_t seed, db_seed;
+  int64_t n_demo, n_rows;
+  double cost_verifier, cost_drafter_token, cost_retrieval;
+  double* pos;       // [R][3]
+  double* ring;      // [R][w][3]
+  int32_t* hist_n;   // [R] points appended (ring index = hist_n % w)
+  int64_t* act;      // [R] actions emitted (next action index j)
+  int32_t* rounds;   // [R] decode rounds (stored skip features)
+  hsd_episode_report* report;  // [R]
+};
+cudaError_t launch_hyb_init(const HybridArgs& a, cudaStream_t s);
+cudaError_t launch_hyb_windows(int R, int w, const double* ring, const int32_t* hist_n, double* xyz, int32_t* histw,
+                               cudaStream_t s);
+cudaError_t launch_hyb_compact(int R, int mode, const int32_t* decision, int32_t* modes, int32_t* slot,
+                               int32_t* ret_idx, int32_t* drf_idx, int32_t* counts, cudaStream_t s);
+cudaError_t launch_hyb_prep_ret(const HybridArgs& a, int round, const int32_t* ret_idx, int n, float* queries,
+                                float* fnow, float* fprev, int32_t* hist_c, cudaStream_t s);
+cudaError_t launch_hyb_logits(const HybridArgs& a, int round, const int32_t* idx, int n, int L, float* out,
+                              cudaStream_t s);
+cudaError_t launch_hyb_drafts(const HybridArgs& a, int round, const int32_t* idx, int n, int L, uint8_t* drafts,
+                              int32_t* ids, cudaStream_t s);
+cudaError_t launch_hyb_emit(const HybridArgs& a, int round, const int32_t* modes, const int32_t* slot,
+                            const hsd_outcome* out_r, const uint8_t* tok_r, const hsd_outcome* out_d,
+                            const uint8_t* tok_d, const double* F, hsd_step_record* trace, cudaStream_t s);
 
 }  // namespace hsd
