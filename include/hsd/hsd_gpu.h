@@ -357,12 +357,15 @@ hsd_status hsd_hybrid_destroy(hsd_hybrid* h);
  * the retrieval/drafter robot counts size the launches). */
 hsd_status hsd_hybrid_step(hsd_hybrid* h, int n_rounds, void* stream);
 /* Host copies: positions [R][3], reports [R], trace [rounds][R] (rounds
- * recorded so far, <= max_rounds); stage times (ms, summed over rounds:
- * [kinematics, search, verify, other, total]). */
+ * recorded so far, <= max_rounds), retrieval queries / drafter rounds so far. */
 hsd_status hsd_hybrid_positions(hsd_hybrid* h, double* xyz);
 hsd_status hsd_hybrid_reports(hsd_hybrid* h, hsd_episode_report* out);
 hsd_status hsd_hybrid_trace(hsd_hybrid* h, hsd_step_record* out, int* rounds);
 hsd_status hsd_hybrid_counts(hsd_hybrid* h, int64_t* retrieval_queries, int64_t* drafter_rounds);
+/* CUDA-event stage times summed over the rounds since the last call (ms):
+ * [decide (windows + K5 + compaction), search (queries, logits, K1+K2[+K3]),
+ *  verify (K4 retrieval + drafter), emit, total]; synchronizes. */
+hsd_status hsd_hybrid_stage_times(hsd_hybrid* h, int* rounds, double ms[5]);
 
 /* Generate with an explicit payload family (HSD_PAYLOAD_*): TRAJ rows hold the
  * demonstration policy of episode row / traj_T from action row % traj_T. */

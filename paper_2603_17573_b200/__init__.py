@@ -210,6 +210,7 @@ def lib():
         "hsd_hybrid_reports": [_vp, _vp],
         "hsd_hybrid_trace": [_vp, _vp, C.POINTER(C.c_int)],
         "hsd_hybrid_counts": [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+        "hsd_hybrid_stage_times": [_vp, C.POINTER(C.c_int), C.POINTER(C.c_double * 5)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -703,3 +704,10 @@ class HybridLoop:
         a, b = C.c_int64(), C.c_int64()
         check(lib().hsd_hybrid_counts(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def stage_times(self):
+        """{decide, search, verify, emit, total} ms per round (CUDA events) since the last call."""
+        n, ms = C.c_int(), (C.c_double * 5)()
+        check(lib().hsd_hybrid_stage_times(self._h, C.byref(n), C.byref(ms)))
+        names = ("decide", "search", "verify", "emit", "total")
+        return n.value, {k: v / max(n.value, 1) for k, v in zip(names, ms)}

@@ -1066,7 +1066,23 @@ struct hsd_hybrid {
   int32_t* h_counts = nullptr;  // pinned
   int64_t n_ret_queries = 0, n_drf_rounds = 0;
   std::vector<void*> allocs;
+  // stage timing: two alternating event sets [start, decided, searched, verified, emitted]
+  cudaEvent_t ev[2][5] = {};
+  bool pending[2] = {false, false};
+  double stage_ms[5] = {0, 0, 0, 0, 0};
+  int timed_rounds = 0;
 };
+
+static void hybrid_collect(hsd_hybrid* h, int set) {
+  if (!h->pending[set]) return;
+  float t;
+  cudaEvent_t* e = h->ev[set];
+  for (int i = 0; i < 4; ++i)
+    if (cudaEventElapsedTime(&t, e[i], e[i + 1]) == cudaSuccess) h->stage_ms[i] += t;
+  if (cudaEventElapsedTime(&t, e[0], e[4]) == cudaSuccess) h->stage_ms[4] += t;
+  h->pending[set] = false;
+  ++h->timed_rounds;
+}
 
 extern "C" {
 
@@ -1076,6 +1092,9 @@ hsd_status hsd_hybrid_destroy(hsd_hybrid* h) {
   cudaDeviceSynchronize();
   for (void* p : h->allocs) cudaFree(p);
   if (h->h_counts) cudaFreeHost(h->h_counts);
+  for (auto& set : h->ev)
+    for (cudaEvent_t e : set)
+      if (e) cudaEventDestroy(e);
   delete h;
   return HSD_OK;
 }
@@ -1172,7 +1191,10 @@ hsd_status hsd_hybrid_create(hsd_collection* c, hsd_comm* comm, int64_t id_offse
   a.cost_verifier = p->cost_verifier;
   a.cost_drafter_token = p->cost_drafter_token;
   a.cost_retrieval = p->cost_retrieval;
-  e = hsd::launch_hyb_init(a, 0);
+  for (auto& set : h->ev)
+    for (cudaEvent_t& ev : set)
+      if (e == cudaSuccess) e = cudaEventCreate(&ev);
+  if (e == cudaSuccess) e = hsd::launch_hyb_init(a, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     hsd_hybrid_destroy(h);
@@ -1194,13 +1216,19 @@ hsd_status hsd_hybrid_step(hsd_hybrid* h, int n_rounds, void* stream) {
   vp_drf.skip_enabled = 0;  // verify-skip is retrieval-mode only
   for (int it = 0; it < n_rounds; ++it) {
     const int round = h->round;
+    const int set = round & 1;
+    cudaEvent_t* ev = h->ev[set];
+    CU(cudaEventRecord(ev[0], s));
     // decide_sd for every robot (K5 over the trailing window; cold start -> drafter)
     CU(hsd::launch_hyb_windows(R, h->w, h->a.ring, h->a.hist_n, h->xyz, h->histw, s));
     CU(hsd::launch_kinematics(h->xyz, R, p.metric, p.bounds, h->histw, h->Rk, h->Dk, h->Fk, h->dec, s));
     CU(hsd::launch_hyb_compact(R, p.mode, h->dec, h->modes, h->slot, h->ret_idx, h->drf_idx, h->counts, s));
     CU(cudaMemcpyAsync(h->h_counts, h->counts, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CU(cudaEventRecord(ev[1], s));
     CU(cudaStreamSynchronize(s));
+    hybrid_collect(h, set ^ 1);  // the previous round has completed
     const int nr = h->h_counts[0], nd = h->h_counts[1];
+    if (nr == 0) CU(cudaEventRecord(ev[2], s));
     if (nr > 0) {  // retrieval_sd robots: retrieve_drafts -> should_skip -> verify_tree
       CU(hsd::launch_hyb_prep_ret(h->a, round, h->ret_idx, nr, h->q, h->fnow, h->fprev, h->hist_c, s));
       CU(hsd::launch_hyb_logits(h->a, round, h->ret_idx, nr, HSD_HYB_RET_L, h->lg_r, s));
@@ -1209,11 +1237,13 @@ hsd_status hsd_hybrid_step(hsd_hybrid* h, int n_rounds, void* stream) {
       if (h->comm) {
         st = hsd_search_topk_sharded(h->c, h->comm, h->id_offset, h->q, nr, k, h->scores, h->ids, h->drafts, s);
         if (st != HSD_OK) return st;
+        CU(cudaEventRecord(ev[2], s));
         st = verify_impl(h->c->device, nullptr, h->drafts, h->ids, nr, k, HSD_HYB_RET_L, h->lg_r, fn, fp, p.d_f,
                          h->hist_c, p.gap_d, &p.verify, 1, h->out_r, h->tok_r, s);
       } else {
         st = search_impl(h->c, h->q, nr, k, 0, h->c->n, h->scores, h->ids, s);
         if (st != HSD_OK) return st;
+        CU(cudaEventRecord(ev[2], s));
         st = verify_impl(h->c->device, h->c, nullptr, h->ids, nr, k, HSD_HYB_RET_L, h->lg_r, fn, fp, p.d_f, h->hist_c,
                          p.gap_d, &p.verify, 1, h->out_r, h->tok_r, s);
       }
@@ -1226,12 +1256,31 @@ hsd_status hsd_hybrid_step(hsd_hybrid* h, int n_rounds, void* stream) {
                        p.gap_d, &vp_drf, 1, h->out_d, h->tok_d, s);
       if (st != HSD_OK) return st;
     }
+    CU(cudaEventRecord(ev[3], s));
     hsd_step_record* tr = round < h->max_rounds ? h->trace : nullptr;
     CU(hsd::launch_hyb_emit(h->a, round, h->modes, h->slot, h->out_r, h->tok_r, h->out_d, h->tok_d, h->Fk, tr, s));
+    CU(cudaEventRecord(ev[4], s));
+    h->pending[set] = true;
     h->n_ret_queries += nr;
     h->n_drf_rounds += nd;
     ++h->round;
   }
+  return HSD_OK;
+}
+
+hsd_status hsd_hybrid_stage_times(hsd_hybrid* h, int* rounds, double* ms) {
+  if (!h || !rounds || !ms) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(h->c->device);
+  if (st != HSD_OK) return st;
+  CU(cudaDeviceSynchronize());
+  hybrid_collect(h, 0);
+  hybrid_collect(h, 1);
+  for (int i = 0; i < 5; ++i) {
+    ms[i] = h->stage_ms[i];
+    h->stage_ms[i] = 0;
+  }
+  *rounds = h->timed_rounds;
+  h->timed_rounds = 0;
   return HSD_OK;
 }
 
