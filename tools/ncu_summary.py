@@ -1,8 +1,13 @@
 """Summarise ncu outputs into profiles/ (committed evidence).
 
   python tools/ncu_summary.py launches gpurun_out/launches.csv profiles/r01_launches.md
-  python tools/ncu_summary.py full gpurun_out/prof_full.ncu-rep profiles/r01_ncu_full.md [--traffic profiles/traffic.json]
+  python tools/ncu_summary.py full gpurun_out/prof_full.ncu-rep profiles/r01_ncu_full.md \
+      [--traffic profiles/traffic.json --key similarity --match sim_wide]
+
+--traffic merges dram read+write bytes of the first kernel whose name contains
+--match into the json under --key (bench.py reads it as roofline.traffic).
 """
+import re
 import collections
 import csv
 import io
@@ -47,7 +52,7 @@ def launches(src, dst):
     print(open(dst).read())
 
 
-def full(src, dst, traffic=None):
+def full(src, dst, traffic=None, key="similarity", match="sim_wide"):
     raw = subprocess.run(["ncu", "-i", src, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, units = rows[0], rows[1]
@@ -64,23 +69,31 @@ def full(src, dst, traffic=None):
             u = units[h.index(m)] if m in h else ""
             vals.append(f"{v} {u}".strip())
         out.append(f"| `{name}` | " + " | ".join(vals) + " |")
-        if "sim_tc1" in name and "dram__bytes_read.sum" in d:
+        if re.search(match, name) and key not in tr and "dram__bytes_read.sum" in d:
             def to_bytes(m):
                 v = float(d[m].replace(",", ""))
                 u = units[h.index(m)]
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-            tr["similarity"] = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
+            tr[key] = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
     with open(dst, "w") as f:
         f.write("\n".join(out) + "\n")
     print("\n".join(out))
     if traffic and tr:
+        try:
+            with open(traffic) as f:
+                old = json.load(f)
+        except Exception:
+            old = {}
+        old.update(tr)
         with open(traffic, "w") as f:
-            json.dump(tr, f, indent=1)
-        print(traffic, tr)
+            json.dump(old, f, indent=1)
+        print(traffic, old)
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
-        full(sys.argv[2], sys.argv[3], sys.argv[5] if len(sys.argv) > 5 and sys.argv[4] == "--traffic" else None)
+        opt = {sys.argv[i]: sys.argv[i + 1] for i in range(4, len(sys.argv) - 1, 2)}
+        full(sys.argv[2], sys.argv[3], opt.get("--traffic"), opt.get("--key", "similarity"),
+             opt.get("--match", "sim_wide"))
