@@ -58,6 +58,9 @@ typedef enum hsd_dtype {
 } hsd_dtype;
 
 const char* hsd_last_error(void);
+/* 1-based line of the last HSD_ERR_PARSE from a file reader (hsd::ParseError
+ * line_number, errors.hpp:35-40); 0 when not applicable. */
+long hsd_last_error_line(void);
 int hsd_abi_version(void);
 /* Number of visible sm_100 devices (0 when none). */
 hsd_status hsd_device_count(int* n);
@@ -291,6 +294,36 @@ hsd_status hsd_search_topk_sharded(hsd_collection* c, hsd_comm* comm, int64_t id
  * searched separately on one GPU. */
 hsd_status hsd_merge_topk(int device, const double* g_scores, const int32_t* g_ids, const uint8_t* g_drafts, int G,
                           int B, int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream);
+
+/* ------------------------------------------------------------------------
+ * DB ingest: load_collection (store.cpp:152-191) of the
+ * reference's JSONL v1 file, parsed natively (strict JSON, multi-threaded by
+ * line) into a host columnar image, then uploaded like hsd_collection_insert.
+ * Errors follow store.cpp: HSD_ERR_IO (cannot open), HSD_ERR_PARSE with
+ * hsd_last_error_line() (missing / malformed header, no integer version,
+ * metric != "cosine", malformed record, missing or mis-sized embedding,
+ * missing payload, bad payload fields, negative indices), HSD_ERR_VERSION
+ * (version != 1), HSD_ERR_CONFIG (dim < 1).  Additions: features of one file
+ * must share one length (HSD_ERR_SCHEMA with the line).
+ * ---------------------------------------------------------------------- */
+typedef struct hsd_jsonl_db hsd_jsonl_db;
+/* Host-only (no device needed).  threads <= 0: all cores. */
+hsd_status hsd_jsonl_read(const char* path, int threads, hsd_jsonl_db** out);
+hsd_status hsd_jsonl_free(hsd_jsonl_db* db);
+hsd_status hsd_jsonl_info(const hsd_jsonl_db* db, int64_t* n, int* dim, int* d_f, const char** name);
+/* Host views: emb fp32 [n][dim] (fp32 rounding of the file's doubles),
+ * next_actions fp64 [n][21], episode/step idx int32 [n], features fp32
+ * [n][d_f] (NULL when no record has one; zeros where absent), has_feature [n]. */
+hsd_status hsd_jsonl_data(const hsd_jsonl_db* db, const float** emb, const double** next_actions,
+                          const int32_t** episode_idx, const int32_t** step_idx, const float** features,
+                          const uint8_t** has_feature);
+hsd_status hsd_collection_from_jsonl(const hsd_jsonl_db* db, int device, int dtype, hsd_collection** out);
+hsd_status hsd_collection_load_jsonl(const char* path, int device, int dtype, hsd_collection** out);
+/* Binary columnar device image (keys as stored, quantized tokens, max row
+ * norm) for fast reload of a shard; synchronous, streamed through pinned 64 MB
+ * chunks.  Bad magic / truncated -> HSD_ERR_PARSE, version -> HSD_ERR_VERSION. */
+hsd_status hsd_collection_save_image(hsd_collection* c, const char* path);
+hsd_status hsd_collection_load_image(const char* path, int device, hsd_collection** out);
 
 /* ------------------------------------------------------------------------
  * Hybrid decoding loop (config 5): the SPEC scheduler's run_step / run_episode

@@ -195,8 +195,39 @@ def ref():
         R.hsdref_l2_normalize.argtypes = [_d, C.c_int, _d]
         R.hsdref_cosine.restype = C.c_double
         R.hsdref_cosine.argtypes = [_d, _d, C.c_int]
+        R.hsdref_load.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_long)]
+        R.hsdref_save.argtypes = [C.c_void_p, C.c_char_p]
+        R.hsdref_dim.argtypes = [C.c_void_p]
+        R.hsdref_record.argtypes = [C.c_void_p, C.c_long, _d, _d, C.POINTER(C.c_int), C.POINTER(C.c_int), _d, C.c_int]
         _ref = R
     return _ref
+
+
+def ref_load(path: str):
+    """The reference's own load_collection (store.cpp:152-191): (status, line, dict | None).
+    status: 0 ok, -5 ParseError, -6 VersionError, -2 ConfigError, -4 IoError, -99 a non-hsd exception."""
+    R = ref()
+    h, line = C.c_void_p(), C.c_long()
+    st = R.hsdref_load(os.fsencode(path), C.byref(h), C.byref(line))
+    if st != 0:
+        return st, line.value, None
+    n, dim = R.hsdref_collection_size(h), R.hsdref_dim(h)
+    out = {"n": n, "dim": dim, "embedding": np.zeros((n, dim)), "next_actions": np.zeros((n, 3, 7)),
+           "episode_idx": np.zeros(n, np.int32), "step_idx": np.zeros(n, np.int32), "features": []}
+    e, nx, fb = np.zeros(max(dim, 1)), np.zeros(21), np.zeros(1 << 16)
+    ep, stp = C.c_int(), C.c_int()
+    for r in range(n):
+        nf = R.hsdref_record(h, r, e, nx, C.byref(ep), C.byref(stp), fb, fb.size)
+        out["embedding"][r] = e[:dim]
+        out["next_actions"][r] = nx.reshape(3, 7)
+        out["episode_idx"][r], out["step_idx"][r] = ep.value, stp.value
+        out["features"].append(None if nf < 0 else fb[:nf].copy())
+    out["_handle"] = h
+    return 0, 0, out
+
+
+def ref_save(loaded: dict, path: str) -> int:
+    return ref().hsdref_save(loaded["_handle"], os.fsencode(path))
 
 
 # ---------------------------------------------------------------- helpers

@@ -191,4 +191,48 @@ double hsdref_cosine(const double* a, const double* b, int n) {
   return hsd::cosine_similarity(std::vector<double>(a, a + n), std::vector<double>(b, b + n));
 }
 
+// ---- persistence (store.cpp:138-191), the reference's own JSONL v1 path ----
+// hsdref_load: load_collection(path); returns 0 or the negative status of the
+// thrown hsd:: exception (-99 for a non-hsd exception, e.g. nlohmann's), with
+// ParseError's line number in *line.  On success *out holds the Collection.
+int hsdref_load(const char* path, void** out, long* line) {
+  *out = nullptr;
+  *line = 0;
+  try {
+    *out = new hsd::Collection(hsd::load_collection(path));
+    return 0;
+  } catch (const hsd::ParseError& e) {
+    *line = e.line_number;
+    return -5;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int hsdref_save(void* c, const char* path) {
+  try {
+    hsd::save_collection(*static_cast<hsd::Collection*>(c), path);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+int hsdref_dim(void* c) { return static_cast<hsd::Collection*>(c)->dim(); }
+
+// Record r of a loaded collection: embedding [dim], next_actions [21],
+// episode/step idx, feature length (-1 = none) and up to feat_cap values.
+int hsdref_record(void* c, long r, double* emb, double* next21, int* ep, int* st, double* feat, int feat_cap) {
+  const auto& rec = static_cast<hsd::Collection*>(c)->records().at(static_cast<size_t>(r));
+  std::memcpy(emb, rec.embedding.data(), rec.embedding.size() * sizeof(double));
+  for (int s = 0; s < 3; ++s)
+    for (int j = 0; j < 7; ++j) next21[s * 7 + j] = rec.payload.next_actions[static_cast<size_t>(s)][static_cast<size_t>(j)];
+  *ep = rec.payload.episode_idx;
+  *st = rec.payload.step_idx;
+  if (!rec.feature) return -1;
+  const int n = static_cast<int>(rec.feature->size());
+  for (int i = 0; i < n && i < feat_cap; ++i) feat[i] = (*rec.feature)[static_cast<size_t>(i)];
+  return n;
+}
+
 }  // extern "C"

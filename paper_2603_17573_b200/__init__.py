@@ -157,6 +157,7 @@ def lib():
                           "(the HeiSD hot path has no CPU fallback)")
     L = C.CDLL(LIB_PATH)
     L.hsd_last_error.restype = C.c_char_p
+    L.hsd_last_error_line.restype = C.c_long
     L.hsd_abi_version.restype = C.c_int
     sig = {
         "hsd_device_count": [C.POINTER(C.c_int)],
@@ -211,6 +212,14 @@ def lib():
         "hsd_hybrid_trace": [_vp, _vp, C.POINTER(C.c_int)],
         "hsd_hybrid_counts": [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
         "hsd_hybrid_stage_times": [_vp, C.POINTER(C.c_int), C.POINTER(C.c_double * 5)],
+        "hsd_jsonl_read": [C.c_char_p, C.c_int, C.POINTER(_vp)],
+        "hsd_jsonl_free": [_vp],
+        "hsd_jsonl_info": [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_char_p)],
+        "hsd_jsonl_data": [_vp] + [C.POINTER(_vp)] * 6,
+        "hsd_collection_from_jsonl": [_vp, C.c_int, C.c_int, C.POINTER(_vp)],
+        "hsd_collection_load_jsonl": [C.c_char_p, C.c_int, C.c_int, C.POINTER(_vp)],
+        "hsd_collection_save_image": [_vp, C.c_char_p],
+        "hsd_collection_load_image": [C.c_char_p, C.c_int, C.POINTER(_vp)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -223,7 +232,10 @@ def lib():
 def check(status: int) -> None:
     if status != 0:
         msg = lib().hsd_last_error().decode(errors="replace")
-        raise _STATUS.get(status, HsdError)(f"[hsd status {status}] {msg}")
+        err = _STATUS.get(status, HsdError)(f"[hsd status {status}] {msg}")
+        if status == 5:  # hsd::ParseError carries its line (errors.hpp:35-40)
+            err.line_number = lib().hsd_last_error_line()
+        raise err
 
 
 def exported_symbols() -> list[str]:
@@ -233,7 +245,7 @@ def exported_symbols() -> list[str]:
     hdr = os.path.join(os.path.dirname(_HERE), "include", "hsd", "hsd_gpu.h")
     with open(hdr) as f:
         text = f.read()
-    return sorted(set(re.findall(r"^(?:hsd_status|const char\*|int)\s+(hsd_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^(?:hsd_status|const char\*|int|long)\s+(hsd_\w+)\(", text, re.M)))
 
 
 def device_count() -> int:
@@ -369,6 +381,10 @@ class Collection:
         out = torch.empty((q.shape[0], self.size()), dtype=torch.float32, device=q.device)
         check(lib().hsd_debug_sim_scores(self._h, _ptr(q), q.shape[0], variant, _ptr(out), _stream(stream)))
         return out
+
+    def save_image(self, path: str) -> None:
+        """Binary columnar device image (hsd_collection_save_image)."""
+        check(lib().hsd_collection_save_image(self._h, os.fsencode(path)))
 
     def overflow_count(self, stream=None) -> int:
         c = C.c_int()
@@ -711,3 +727,56 @@ class HybridLoop:
         check(lib().hsd_hybrid_stage_times(self._h, C.byref(n), C.byref(ms)))
         names = ("decide", "search", "verify", "emit", "total")
         return n.value, {k: v / max(n.value, 1) for k, v in zip(names, ms)}
+
+
+# --------------------------------------------------------------------------- DB ingest (JSONL v1)
+def jsonl_read(path: str, threads: int = 0) -> dict:
+    """Host-side native parse of a reference JSONL v1 DB file (load_collection, store.cpp:152-191)."""
+    h = C.c_void_p()
+    check(lib().hsd_jsonl_read(os.fsencode(path), threads, C.byref(h)))
+    try:
+        n, dim, d_f, name = C.c_int64(), C.c_int(), C.c_int(), C.c_char_p()
+        check(lib().hsd_jsonl_info(h, C.byref(n), C.byref(dim), C.byref(d_f), C.byref(name)))
+        ptrs = [C.c_void_p() for _ in range(6)]
+        check(lib().hsd_jsonl_data(h, *[C.byref(p) for p in ptrs]))
+        n, dim, d_f = n.value, dim.value, d_f.value
+
+        def arr(p, ct, shape):
+            cnt = int(np.prod(shape))
+            if not p.value or cnt == 0:
+                return np.zeros(shape, np.dtype(ct))
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), (cnt,)).reshape(shape).copy()
+
+        out = {"name": (name.value or b"").decode(), "n": n, "dim": dim, "d_f": d_f,
+               "embedding": arr(ptrs[0], C.c_float, (n, dim)), "next_actions": arr(ptrs[1], C.c_double, (n, 3, 7)),
+               "episode_idx": arr(ptrs[2], C.c_int32, (n,)), "step_idx": arr(ptrs[3], C.c_int32, (n,)),
+               "feature": arr(ptrs[4], C.c_float, (n, d_f)) if d_f else None,
+               "has_feature": arr(ptrs[5], C.c_uint8, (n,))}
+        return out
+    finally:
+        lib().hsd_jsonl_free(h)
+
+
+def _wrap_handle(h, device) -> Collection:
+    col = Collection.__new__(Collection)
+    col._h = h
+    col.device = device
+    d, t = C.c_int(), C.c_int()
+    check(lib().hsd_collection_dim(h, C.byref(d)))
+    check(lib().hsd_collection_dtype(h, C.byref(t)))
+    col._dim, col.dtype = d.value, t.value
+    return col
+
+
+def load_jsonl(path: str, device: int = 0, dtype="f32") -> Collection:
+    """load_collection (store.cpp:152-191) straight into HBM."""
+    h = C.c_void_p()
+    check(lib().hsd_collection_load_jsonl(os.fsencode(path), device, _DTYPES[dtype], C.byref(h)))
+    return _wrap_handle(h, device)
+
+
+def load_image(path: str, device: int = 0) -> Collection:
+    """Reload a binary device image written by Collection.save_image."""
+    h = C.c_void_p()
+    check(lib().hsd_collection_load_image(os.fsencode(path), device, C.byref(h)))
+    return _wrap_handle(h, device)

@@ -20,8 +20,10 @@
 namespace {
 
 thread_local std::string g_err;
+thread_local long g_err_line = 0;
 
 hsd_status fail(hsd_status st, const char* fmt, ...) {
+  g_err_line = 0;
   char buf[512];
   va_list ap;
   va_start(ap, fmt);
@@ -281,6 +283,7 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
 extern "C" {
 
 const char* hsd_last_error(void) { return g_err.c_str(); }
+long hsd_last_error_line(void) { return g_err_line; }
 int hsd_abi_version(void) { return HSD_ABI_VERSION; }
 
 hsd_status hsd_device_count(int* n) {
@@ -1319,6 +1322,131 @@ hsd_status hsd_hybrid_counts(hsd_hybrid* h, int64_t* retrieval_queries, int64_t*
   if (!h) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   if (retrieval_queries) *retrieval_queries = h->n_ret_queries;
   if (drafter_rounds) *drafter_rounds = h->n_drf_rounds;
+  return HSD_OK;
+}
+
+}  // extern "C"
+
+// Error plumbing for the host-only translation units (ingest.cpp): ParseError
+// carries its 1-based line (errors.hpp:35-40) in the message and in
+// hsd_last_error_line().
+hsd_status hsd_internal_fail(hsd_status st, const char* msg, long line) {
+  if (line > 0)
+    fail(st, "%s (line %ld)", msg, line);
+  else
+    fail(st, "%s", msg);
+  g_err_line = line;
+  return st;
+}
+
+// ------------------------------------------------------------------ binary device image
+// Columnar image of a collection for fast reload:
+//   "HSDIMG01" | u32 version=1 | i32 dim | i32 dtype | i32 pad | i64 n | u64 maxnorm bits
+//   | keys [n][dim] (fp32 or bf16) | tokens [n][32]
+// Streamed through a pinned staging buffer in 64 MB chunks.
+namespace {
+constexpr char kImgMagic[8] = {'H', 'S', 'D', 'I', 'M', 'G', '0', '1'};
+constexpr size_t kImgChunk = 64u << 20;
+
+struct ImgHeader {
+  char magic[8];
+  uint32_t version;
+  int32_t dim, dtype, pad;
+  int64_t n;
+  unsigned long long maxnorm;
+};
+static_assert(sizeof(ImgHeader) == 40, "image header layout");
+
+hsd_status img_copy(FILE* f, void* dev, size_t bytes, bool to_file, void* pin) {
+  for (size_t off = 0; off < bytes; off += kImgChunk) {
+    const size_t m = std::min(kImgChunk, bytes - off);
+    if (to_file) {
+      CU(cudaMemcpy(pin, (uint8_t*)dev + off, m, cudaMemcpyDeviceToHost));
+      if (fwrite(pin, 1, m, f) != m) return fail(HSD_ERR_IO, "image write failed");
+    } else {
+      if (fread(pin, 1, m, f) != m) return fail(HSD_ERR_PARSE, "truncated image");
+      CU(cudaMemcpy((uint8_t*)dev + off, pin, m, cudaMemcpyHostToDevice));
+    }
+  }
+  return HSD_OK;
+}
+}  // namespace
+
+extern "C" {
+
+hsd_status hsd_collection_save_image(hsd_collection* c, const char* path) {
+  if (!c || !path) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  ImgHeader h{};
+  std::memcpy(h.magic, kImgMagic, 8);
+  h.version = 1;
+  h.dim = c->dim;
+  h.dtype = c->dtype;
+  h.n = c->n;
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(&h.maxnorm, c->maxnorm, 8, cudaMemcpyDeviceToHost));
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(HSD_ERR_IO, "cannot open for writing: %s", path);
+  void* pin = nullptr;
+  cudaError_t e = cudaMallocHost(&pin, kImgChunk);
+  if (e != cudaSuccess) {
+    fclose(f);
+    return cuda_fail(e, "pinned staging");
+  }
+  st = fwrite(&h, sizeof h, 1, f) == 1 ? HSD_OK : fail(HSD_ERR_IO, "image write failed");
+  if (st == HSD_OK) st = img_copy(f, c->keys, (size_t)c->n * c->dim * key_bytes(c), true, pin);
+  if (st == HSD_OK) st = img_copy(f, c->tokens, (size_t)c->n * HSD_TOKENS_STRIDE, true, pin);
+  cudaFreeHost(pin);
+  if (fclose(f) != 0 && st == HSD_OK) st = fail(HSD_ERR_IO, "image close failed");
+  return st;
+}
+
+hsd_status hsd_collection_load_image(const char* path, int device, hsd_collection** out) {
+  if (!path || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *out = nullptr;
+  FILE* f = fopen(path, "rb");
+  if (!f) return fail(HSD_ERR_IO, "cannot open for reading: %s", path);
+  ImgHeader h{};
+  if (fread(&h, sizeof h, 1, f) != 1 || std::memcmp(h.magic, kImgMagic, 8) != 0) {
+    fclose(f);
+    return fail(HSD_ERR_PARSE, "not an hsd device image: %s", path);
+  }
+  if (h.version != 1) {
+    fclose(f);
+    return fail(HSD_ERR_VERSION, "unsupported device image version %u", h.version);
+  }
+  if (h.n < 0) {
+    fclose(f);
+    return fail(HSD_ERR_PARSE, "corrupt image header");
+  }
+  hsd_collection* c = nullptr;
+  hsd_status st = hsd_collection_create_ex(device, h.dim, std::max<int64_t>(h.n, 1), h.dtype, &c);
+  if (st != HSD_OK) {
+    fclose(f);
+    return st;
+  }
+  void* pin = nullptr;
+  cudaError_t e = cudaMallocHost(&pin, kImgChunk);
+  if (e != cudaSuccess) {
+    fclose(f);
+    hsd_collection_destroy(c);
+    return cuda_fail(e, "pinned staging");
+  }
+  st = img_copy(f, c->keys, (size_t)h.n * h.dim * key_bytes(c), false, pin);
+  if (st == HSD_OK) st = img_copy(f, c->tokens, (size_t)h.n * HSD_TOKENS_STRIDE, false, pin);
+  cudaFreeHost(pin);
+  fclose(f);
+  if (st == HSD_OK) {
+    cudaError_t e2 = cudaMemcpy(c->maxnorm, &h.maxnorm, 8, cudaMemcpyHostToDevice);
+    if (e2 != cudaSuccess) st = cuda_fail(e2, "maxnorm");
+  }
+  if (st != HSD_OK) {
+    hsd_collection_destroy(c);
+    return st;
+  }
+  c->n = h.n;
+  *out = c;
   return HSD_OK;
 }
 

@@ -28,6 +28,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxL = 21;
 constexpr int kTokStride = 24;  // bytes per candidate row in shared memory
+constexpr int kFeatUnroll = 4;  // feature float4 pairs loaded per lane before accumulation
 
 __device__ __forceinline__ int group_count(int L) { return (L / 7) * 3; }
 __device__ __forceinline__ void group_at(int g, int& st, int& ln, bool& grip) {
@@ -49,7 +50,7 @@ __device__ __forceinline__ bool accept_group(const uint8_t* draft, const int* gr
   return sum <= p.bias_seq_max && mx <= p.bias_token_max;
 }
 
-__global__ void __launch_bounds__(kThreads) verify_kernel(const int32_t* __restrict__ ids, int E, int k, int L,
+__global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __restrict__ ids, int E, int k, int L,
                                                           const uint8_t* __restrict__ tokens,
                                                           const uint8_t* __restrict__ cand_tokens,
                                                           const float* __restrict__ logits,
@@ -68,48 +69,69 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(const int32_t* __restr
   const int e = blockIdx.x * kWarps + warp;
   if (e >= E) return;
 
-  // ---- greedy tokens: argmax per position, lowest index on ties
+  // ---- greedy tokens: argmax per position, lowest index on ties.  The 7
+  //      positions of an action slice are loaded before any is reduced (7 KB
+  //      in flight per warp) — the kernel is HBM-bound at C3's 4096 episodes.
   const float4* lg = reinterpret_cast<const float4*>(logits + (size_t)e * L * 256);
-  for (int p = 0; p < L; ++p) {
-    const float4 a = __ldg(lg + p * 64 + lane * 2);
-    const float4 c = __ldg(lg + p * 64 + lane * 2 + 1);
-    const float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-    float best = v[0];
-    int bi = lane * 8;
+  for (int p0 = 0; p0 < L; p0 += 7) {
+    float4 a[7], c[7];
 #pragma unroll
-    for (int i = 1; i < 8; ++i)
-      if (v[i] > best) {
-        best = v[i];
-        bi = lane * 8 + i;
-      }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) {
-        best = ob;
-        bi = oi;
-      }
+    for (int u = 0; u < 7; ++u) {
+      a[u] = __ldg(lg + (p0 + u) * 64 + lane * 2);
+      c[u] = __ldg(lg + (p0 + u) * 64 + lane * 2 + 1);
     }
-    if (lane == 0) s_greedy[warp][p] = bi;
+#pragma unroll
+    for (int u = 0; u < 7; ++u) {
+      const float v[8] = {a[u].x, a[u].y, a[u].z, a[u].w, c[u].x, c[u].y, c[u].z, c[u].w};
+      float best = v[0];
+      int bi = lane * 8;
+#pragma unroll
+      for (int i = 1; i < 8; ++i)
+        if (v[i] > best) {
+          best = v[i];
+          bi = lane * 8 + i;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (lane == 0) s_greedy[warp][p0 + u] = bi;
+    }
   }
 
-  // ---- verify-skip similarity: exactly rounded dot (double-double)
+  // ---- verify-skip similarity: exactly rounded dot (double-double; the
+  //      result is the exact sum rounded once, so the order is free and
+  //      kFeatUnroll float4 pairs per lane are loaded before they are accumulated)
   double cosv = -2.0;
   if (need_cos && feat_now && feat_prev) {
     const float4* a4 = reinterpret_cast<const float4*>(feat_now + (size_t)e * d_f);
     const float4* b4 = reinterpret_cast<const float4*>(feat_prev + (size_t)e * d_f);
+    const int n4 = d_f / 4;
     double hi = 0.0, lo = 0.0;
-    for (int t = lane; t < d_f / 4; t += 32) {
-      const float4 x = __ldg(a4 + t), y = __ldg(b4 + t);
-      const double pr[4] = {(double)x.x * (double)y.x, (double)x.y * (double)y.y, (double)x.z * (double)y.z,
-                            (double)x.w * (double)y.w};
+    for (int t0 = lane; t0 < n4; t0 += 32 * kFeatUnroll) {
+      float4 xa[kFeatUnroll], yb[kFeatUnroll];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        double s, er;
-        dev::two_sum(hi, pr[i], s, er);
-        hi = s;
-        lo = __dadd_rn(lo, er);
+      for (int u = 0; u < kFeatUnroll; ++u) {
+        const int t = t0 + 32 * u;
+        xa[u] = t < n4 ? __ldg(a4 + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+        yb[u] = t < n4 ? __ldg(b4 + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kFeatUnroll; ++u) {
+        const double pr[4] = {(double)xa[u].x * (double)yb[u].x, (double)xa[u].y * (double)yb[u].y,
+                              (double)xa[u].z * (double)yb[u].z, (double)xa[u].w * (double)yb[u].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          double s, er;
+          dev::two_sum(hi, pr[i], s, er);
+          hi = s;
+          lo = __dadd_rn(lo, er);
+        }
       }
     }
 #pragma unroll
