@@ -326,6 +326,30 @@ hsd_status hsd_collection_save_image(hsd_collection* c, const char* path);
 hsd_status hsd_collection_load_image(const char* path, int device, hsd_collection** out);
 
 /* ------------------------------------------------------------------------
+ * Verify-skip lifecycle (Alg. 1).
+ * ---------------------------------------------------------------------- */
+typedef struct hsd_skip_state { /* VerifySkipState */
+  double T;         /* pre-sampled similarity boundary */
+  double min_S;
+  int32_t O_dist;
+  double delta;     /* feedback step */
+  int32_t inverted; /* update_direction = inverted */
+} hsd_skip_state;
+
+/* offline_calibrate_skip over n_traj trajectories: rows [offsets[t],
+ * offsets[t+1]) of the DEVICE feature matrix fp32 [n][d_f] (offsets: HOST
+ * int64 [n_traj + 1]).  S(i, i+d) is the exactly rounded feature dot (the
+ * similarity should_skip uses); the minimum S > T wins, ties to the first pair
+ * in (trajectory, i, d) order.  Batched per-trajectory Gram tiles on the fp64
+ * pipe (double-double, bit-exact).  No pair above T -> HSD_ERR_CALIBRATION
+ * (skipping stays disabled).  Synchronizes `stream`. */
+hsd_status hsd_calibrate_skip(int device, const float* features, int d_f, const int64_t* offsets, int n_traj,
+                              double T, double* min_S, int* O_dist, void* stream);
+/* update_skip_state: host arithmetic, literal Alg. 1
+ * directions, optional inversion, min_S clamped to [T, 1], O_dist >= 1. */
+hsd_status hsd_update_skip_state(hsd_skip_state* s, int success, double S_c, double min_S_h);
+
+/* ------------------------------------------------------------------------
  * Hybrid decoding loop (config 5): the SPEC scheduler's run_step / run_episode
  * for R robots at once, device-resident.  Per round and
  * robot: decide_sd (kinematic fused metric over the trailing w points; cold

@@ -132,6 +132,12 @@ MODE_HYBRID, MODE_PURE_RETRIEVAL, MODE_PURE_DRAFTER, MODE_AUTOREGRESSIVE = 0, 1,
 PAYLOAD_RANDOM, PAYLOAD_TRAJ = 0, 1
 
 
+class SkipState(C.Structure):
+    """hsd_skip_state: VerifySkipState (SPEC.md:411-414)."""
+    _fields_ = [("T", C.c_double), ("min_S", C.c_double), ("O_dist", C.c_int32), ("delta", C.c_double),
+                ("inverted", C.c_int32)]
+
+
 class StepIO(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("queries", "logits", "feat_now", "feat_prev", "xyz", "history", "scores",
                                           "ids", "out", "tokens", "R", "D", "F", "decision")]
@@ -219,6 +225,9 @@ def lib():
         "hsd_collection_from_jsonl": [_vp, C.c_int, C.c_int, C.POINTER(_vp)],
         "hsd_collection_load_jsonl": [C.c_char_p, C.c_int, C.c_int, C.POINTER(_vp)],
         "hsd_collection_save_image": [_vp, C.c_char_p],
+        "hsd_calibrate_skip": [C.c_int, _vp, C.c_int, _vp, C.c_int, C.c_double, C.POINTER(C.c_double),
+                               C.POINTER(C.c_int), _vp],
+        "hsd_update_skip_state": [C.POINTER(SkipState), C.c_int, C.c_double, C.c_double],
         "hsd_collection_load_image": [C.c_char_p, C.c_int, C.POINTER(_vp)],
     }
     for name, args in sig.items():
@@ -780,3 +789,30 @@ def load_image(path: str, device: int = 0) -> Collection:
     h = C.c_void_p()
     check(lib().hsd_collection_load_image(os.fsencode(path), device, C.byref(h)))
     return _wrap_handle(h, device)
+
+
+# --------------------------------------------------------------------------- verify-skip lifecycle (Alg. 1)
+def calibrate_skip(features, offsets, T=0.9, stream=None):
+    """offline_calibrate_skip: features cuda float32 [n, d_f], offsets int [n_traj + 1]
+    (trajectory t = rows offsets[t]:offsets[t+1]) -> (min_S, O_dist); CalibrationError when no pair exceeds T."""
+    f = features.contiguous()
+    off = np.ascontiguousarray(offsets, np.int64)
+    ms, od = C.c_double(), C.c_int()
+    check(lib().hsd_calibrate_skip(f.device.index or 0, _ptr(f), f.shape[1], off.ctypes.data, off.size - 1,
+                                   float(T), C.byref(ms), C.byref(od), _stream(stream)))
+    return ms.value, od.value
+
+
+def update_skip_state(state: SkipState, success: bool, S_c: float, min_S_h: float) -> SkipState:
+    """update_skip_state, in place; returns the state."""
+    check(lib().hsd_update_skip_state(C.byref(state), int(success), float(S_c), float(min_S_h)))
+    return state
+
+
+def trajectory_offsets(episode_idx) -> np.ndarray:
+    """Offsets of maximal runs of equal episode_idx (per-episode feature lists in DB order)."""
+    e = np.asarray(episode_idx)
+    if e.size == 0:
+        return np.zeros(1, np.int64)
+    cuts = np.flatnonzero(np.diff(e) != 0) + 1
+    return np.concatenate([[0], cuts, [e.size]]).astype(np.int64)

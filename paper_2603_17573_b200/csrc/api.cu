@@ -1451,3 +1451,60 @@ hsd_status hsd_collection_load_image(const char* path, int device, hsd_collectio
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ verify-skip calibration (Alg. 1)
+extern "C" {
+
+hsd_status hsd_calibrate_skip(int device, const float* features, int d_f, const int64_t* offsets, int n_traj,
+                              double T, double* min_S, int* O_dist, void* stream) {
+  if (!features || !offsets || !min_S || !O_dist) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (n_traj < 1) return fail(HSD_ERR_INVALID_INPUT, "need at least one trajectory (SPEC.md:453)");
+  if (d_f < 1) return fail(HSD_ERR_INVALID_INPUT, "feature dim must be >= 1");
+  if (!std::isfinite(T)) return fail(HSD_ERR_CONFIG, "similarity boundary T must be finite");
+  int64_t max_len = 0;
+  for (int t = 0; t < n_traj; ++t) {
+    if (offsets[t + 1] < offsets[t] || offsets[t] < 0)
+      return fail(HSD_ERR_INVALID_INPUT, "trajectory offsets must be nondecreasing");
+    max_len = std::max<int64_t>(max_len, offsets[t + 1] - offsets[t]);
+  }
+  if (max_len >= (1 << 20)) return fail(HSD_ERR_INVALID_INPUT, "trajectories longer than 2^20 points");
+  if (n_traj > 65535) return fail(HSD_ERR_INVALID_INPUT, "at most 65535 trajectories per call");
+  hsd_status st = require_device(device);
+  if (st != HSD_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nt = (int)((max_len + 31) / 32);
+  const int max_tiles = nt * (nt + 1) / 2;
+  int64_t* doff = nullptr;
+  void* scratch = nullptr;
+  CU(cudaMalloc(&doff, (size_t)(n_traj + 1) * sizeof(int64_t)));
+  cudaError_t e = cudaMalloc(&scratch, hsd::calib_scratch_bytes(n_traj, std::max(max_tiles, 1)));
+  int found = 0;
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(doff, offsets, (size_t)(n_traj + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = hsd::launch_calibrate(features, d_f, doff, n_traj, (int)max_len, T, scratch, min_S, O_dist, &found, s);
+  cudaFree(doff);
+  cudaFree(scratch);
+  if (e != cudaSuccess) return cuda_fail(e, "calibrate");
+  if (!found)  // no pair exceeds T -> calibration failed, skipping stays disabled
+    return fail(HSD_ERR_CALIBRATION, "no feature pair exceeds the similarity boundary T = %.17g", T);
+  return HSD_OK;
+}
+
+hsd_status hsd_update_skip_state(hsd_skip_state* s, int success, double S_c, double min_S_h) {
+  if (!s) return fail(HSD_ERR_INVALID_INPUT, "null state");
+  // literal Alg. 1 feedback, optional inversion, clamp [T, 1]
+  const double adj = s->delta * std::fabs(S_c - min_S_h);
+  double sign = success ? 1.0 : -1.0;
+  if (s->inverted) sign = -sign;
+  s->min_S += sign * adj;
+  if (success)
+    s->O_dist += 1;
+  else
+    s->O_dist = s->O_dist - 1 < 1 ? 1 : s->O_dist - 1;
+  if (s->min_S < s->T) s->min_S = s->T;
+  if (s->min_S > 1.0) s->min_S = 1.0;
+  return HSD_OK;
+}
+
+}  // extern "C"

@@ -90,6 +90,11 @@ cudaError_t launch_kinematics(const double* xyz, int W, const hsd_metric_params&
                               const int32_t* history, double* R, double* D, double* F, int32_t* decision,
                               cudaStream_t s);
 
+// ---- verify-skip offline calibration (k_calib.cu) --------------------------------
+size_t calib_scratch_bytes(int n_traj, int max_tiles);
+cudaError_t launch_calibrate(const float* feat, int d_f, const int64_t* off_dev, int n_traj, int max_len, double T,
+                             void* scratch, double* min_S_out, int* O_dist_out, int* found_out, cudaStream_t s);
+
 // ---- hybrid decoding loop (k_hybrid.cu) ----------------------------------------
 struct HybridArgs {
   int R, w, dim, d_f, key_kind, traj_T, drafter_p_pct, drafter_L;
