@@ -218,6 +218,15 @@ hsd_status hsd_window_features(int device, const double* xyz, int W, const hsd_m
                                const hsd_norm_bounds* bounds, const int32_t* history, double* R, double* D, double* F,
                                int32_t* decision, void* stream);
 
+/* Same, plus the windowed finite-difference kinematics of each window in the
+ * same pass: vaj fp64 [W][3] (may be NULL) = mean |velocity|, mean
+ * |acceleration|, mean |jerk| per action step (v_i = P_{i+1} - P_i,
+ * a_i = v_{i+1} - v_i, j_i = a_{i+1} - a_i; 0 when the window is too short).
+ * Diagnostics named by the north star; the reference's decision uses R/D/F. */
+hsd_status hsd_window_features_ex(int device, const double* xyz, int W, const hsd_metric_params* params,
+                                  const hsd_norm_bounds* bounds, const int32_t* history, double* R, double* D,
+                                  double* F, int32_t* decision, double* vaj, void* stream);
+
 /* quantize (actions.cpp:32-50) of n action slices fp64 [n][7] with per-dim
  * bounds lo7/hi7 (HOST) into int32 bins [n][7]; status[n] (int32, device):
  * 0 ok, 1 non-finite input.  Bad bounds / K < 2 -> HSD_ERR_CONFIG. */

@@ -962,3 +962,32 @@ int hsdo_robot_greedy(uint64_t db_seed, uint64_t seed, int64_t r, int64_t n_demo
 }
 double hsdo_robot_start(uint64_t seed, int64_t r, int d) { return hsd_robot_start(seed, r, d); }
 double hsdo_dequantize_bin(int bin, double lo, double hi, int k_bins) { return hsd_dequantize_bin(bin, lo, hi, k_bins); }
+
+/* Windowed finite-difference kinematics (diagnostics beside R/D/F): mean
+ * |v|, |a|, |j| per step, v_i = P_{i+1} - P_i, a_i = v_{i+1} - v_i, j_i = a_{i+1} - a_i. */
+void hsdo_window_derivatives(const double* xyz, int n, double* out3) {
+  double sv = 0, sa = 0, sj = 0;
+  for (int i = 0; i + 1 < n; ++i) {
+    double v[3], a[3], j[3];
+    for (int d = 0; d < 3; ++d) v[d] = xyz[(i + 1) * 3 + d] - xyz[i * 3 + d];
+    sv += sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    if (i + 2 < n) {
+      for (int d = 0; d < 3; ++d) {
+        double v1 = xyz[(i + 2) * 3 + d] - xyz[(i + 1) * 3 + d];
+        a[d] = v1 - v[d];
+      }
+      sa += sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+      if (i + 3 < n) {
+        for (int d = 0; d < 3; ++d) {
+          double v1 = xyz[(i + 2) * 3 + d] - xyz[(i + 1) * 3 + d];
+          double v2 = xyz[(i + 3) * 3 + d] - xyz[(i + 2) * 3 + d];
+          j[d] = (v2 - v1) - a[d];
+        }
+        sj += sqrt(j[0] * j[0] + j[1] * j[1] + j[2] * j[2]);
+      }
+    }
+  }
+  out3[0] = n > 1 ? sv / (double)(n - 1) : 0.0;
+  out3[1] = n > 2 ? sa / (double)(n - 2) : 0.0;
+  out3[2] = n > 3 ? sj / (double)(n - 3) : 0.0;
+}

@@ -164,6 +164,9 @@ int hsdo_classify(double F, double threshold); /* :257-259; 1 = retrieval_sd, 0 
 int hsdo_window_features(const double* xyz, int n, const hsdo_metric_params* p, const hsdo_norm_bounds* b, double* R,
                          double* D, double* F, int* decision);
 
+/* Windowed finite-difference kinematics: mean |v|, |a|, |j| per step (out3). */
+void hsdo_window_derivatives(const double* xyz, int n, double* out3);
+
 /* ------------------------------------------------------- hybrid loop (config 5)
  * run_step / run_episode of the SPEC scheduler for R robots,
  * sequentially, over the counter-based harness of hsd_synth.h (demonstration

@@ -450,3 +450,11 @@ def ref_search(col, queries: np.ndarray, k: int, threads: int = 1):
     n = ref().hsdref_collection_size(col)
     kk = min(k, n)
     return sc[:, :kk], ids[:, :kk], tok[:, :kk]
+
+
+def window_derivatives(xyz) -> np.ndarray:
+    """Mean |velocity|, |acceleration|, |jerk| per step of one window (hsdo_window_derivatives)."""
+    x = np.ascontiguousarray(xyz, np.float64)
+    out = np.zeros(3, np.float64)
+    lib().hsdo_window_derivatives(x.ctypes.data_as(C.c_void_p), x.shape[0], out.ctypes.data_as(C.c_void_p))
+    return out

@@ -186,6 +186,8 @@ def lib():
         "hsd_window_features": [C.c_int, _vp, C.c_int, C.POINTER(MetricParams), C.POINTER(NormBounds), _vp, _vp, _vp,
                                 _vp, _vp, _vp],
         "hsd_quantize": [C.c_int, _vp, C.c_int64, _vp, _vp, C.c_int, _vp, _vp, _vp],
+        "hsd_window_features_ex": [C.c_int, _vp, C.c_int, C.POINTER(MetricParams), C.POINTER(NormBounds), _vp, _vp,
+                                   _vp, _vp, _vp, _vp, _vp],
         "hsd_engine_create": [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
         "hsd_engine_destroy": [_vp],
         "hsd_engine_enable_timing": [_vp, C.c_int],
@@ -510,10 +512,11 @@ def _from_ptr(ptr, shape, dtype, device):
 
 # --------------------------------------------------------------------------- free functions
 def window_features(xyz, params: MetricParams = DEFAULT_METRIC, bounds: NormBounds = LIBERO_GOAL, history=None,
-                    stream=None):
+                    stream=None, derivatives=False):
     """Batched window_features + classify_segment + decide_sd (kinematics.cpp:261-273).
 
-    xyz: cuda float64 [W, w, 3] -> (R, D, F float64 [W], decision int32 [W]).
+    xyz: cuda float64 [W, w, 3] -> (R, D, F float64 [W], decision int32 [W]); with derivatives=True also
+    vaj float64 [W, 3] = mean |velocity|, |acceleration|, |jerk| per step, computed in the same kernel.
     """
     torch = _torch()
     x = xyz.contiguous()
@@ -527,6 +530,12 @@ def window_features(xyz, params: MetricParams = DEFAULT_METRIC, bounds: NormBoun
     D = torch.empty_like(R)
     F = torch.empty_like(R)
     dec = torch.empty(W, dtype=torch.int32, device=dev)
+    if derivatives:
+        vaj = torch.empty((W, 3), dtype=torch.float64, device=dev)
+        check(lib().hsd_window_features_ex(dev.index or 0, _ptr(x), W, C.byref(params), C.byref(bounds),
+                                           _ptr(history), _ptr(R), _ptr(D), _ptr(F), _ptr(dec), _ptr(vaj),
+                                           _stream(stream)))
+        return R, D, F, dec, vaj
     check(lib().hsd_window_features(dev.index or 0, _ptr(x), W, C.byref(params), C.byref(bounds), _ptr(history),
                                     _ptr(R), _ptr(D), _ptr(F), _ptr(dec), _stream(stream)))
     return R, D, F, dec

@@ -646,6 +646,20 @@ hsd_status hsd_window_features(int device, const double* xyz, int W, const hsd_m
   return HSD_OK;
 }
 
+hsd_status hsd_window_features_ex(int device, const double* xyz, int W, const hsd_metric_params* params,
+                                  const hsd_norm_bounds* bounds, const int32_t* history, double* R, double* D,
+                                  double* F, int32_t* decision, double* vaj, void* stream) {
+  hsd_status st = check_metric(params, bounds);
+  if (st != HSD_OK) return st;
+  if (W < 0) return fail(HSD_ERR_INVALID_INPUT, "negative window count");
+  if (W == 0) return HSD_OK;
+  if (!xyz || !R || !D || !F || !decision) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  st = require_device(device);
+  if (st != HSD_OK) return st;
+  CU(hsd::launch_kinematics(xyz, W, *params, *bounds, history, R, D, F, decision, (cudaStream_t)stream, vaj));
+  return HSD_OK;
+}
+
 hsd_status hsd_quantize(int device, const double* actions, int64_t n, const double* lo7, const double* hi7, int k_bins,
                         int32_t* bins, int32_t* status, void* stream) {
   if (k_bins < 2) return fail(HSD_ERR_CONFIG, "bin count must be >= 2, got %d", k_bins);  // actions.cpp:28-30

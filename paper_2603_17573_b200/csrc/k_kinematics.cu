@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(kThreads) kinematics_kernel(const double* __re
                                                               hsd_metric_params mp, hsd_norm_bounds nb,
                                                               const int32_t* __restrict__ history,
                                                               double* __restrict__ Rout, double* __restrict__ Dout,
-                                                              double* __restrict__ Fout, int32_t* __restrict__ dec) {
+                                                              double* __restrict__ Fout, int32_t* __restrict__ dec,
+                                                              double* __restrict__ vaj) {
   const int lane = threadIdx.x & 31;
   const int win = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   if (win >= W) return;
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__(kThreads) kinematics_kernel(const double* __re
       Dout[win] = 0.0;
       Fout[win] = 0.0;
       dec[win] = -1;
+      if (vaj) vaj[(size_t)win * 3 + 0] = vaj[(size_t)win * 3 + 1] = vaj[(size_t)win * 3 + 2] = 0.0;
     }
     return;
   }
@@ -124,6 +126,26 @@ __global__ void __launch_bounds__(kThreads) kinematics_kernel(const double* __re
     seg = sqrt(dx * dx + dy * dy + dz * dz);
   }
   const double D = wsum(seg);
+
+  // ---- windowed finite-difference kinematics (north-star diagnostics; the
+  //      reference pins only R / D / F): mean |velocity|, |acceleration|,
+  //      |jerk| per action step, v_i = P_{i+1} - P_i, a_i = v_{i+1} - v_i,
+  //      j_i = a_{i+1} - a_i.
+  if (vaj) {
+    const double vx = nx - x, vy = ny - y, vz = nz - z;  // valid on lanes < n - 1
+    const double ax_ = __shfl_down_sync(0xffffffffu, vx, 1) - vx, ay_ = __shfl_down_sync(0xffffffffu, vy, 1) - vy,
+                 az_ = __shfl_down_sync(0xffffffffu, vz, 1) - vz;  // lanes < n - 2
+    const double jx = __shfl_down_sync(0xffffffffu, ax_, 1) - ax_, jy = __shfl_down_sync(0xffffffffu, ay_, 1) - ay_,
+                 jz = __shfl_down_sync(0xffffffffu, az_, 1) - az_;  // lanes < n - 3
+    const double sv = wsum(lane + 1 < n ? sqrt(__dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz))) : 0.0);
+    const double sa = wsum(lane + 2 < n ? sqrt(__dadd_rn(__dadd_rn(__dmul_rn(ax_, ax_), __dmul_rn(ay_, ay_)), __dmul_rn(az_, az_))) : 0.0);
+    const double sj = wsum(lane + 3 < n ? sqrt(__dadd_rn(__dadd_rn(__dmul_rn(jx, jx), __dmul_rn(jy, jy)), __dmul_rn(jz, jz))) : 0.0);
+    if (lane == 0) {
+      vaj[(size_t)win * 3 + 0] = n > 1 ? sv / (double)(n - 1) : 0.0;
+      vaj[(size_t)win * 3 + 1] = n > 2 ? sa / (double)(n - 2) : 0.0;
+      vaj[(size_t)win * 3 + 2] = n > 3 ? sj / (double)(n - 3) : 0.0;
+    }
+  }
 
   // ---- project_window
   const double mx = wsum(x) * inv_n, my = wsum(y) * inv_n, mz = wsum(z) * inv_n;
@@ -246,10 +268,10 @@ __global__ void __launch_bounds__(kThreads) kinematics_kernel(const double* __re
 
 cudaError_t launch_kinematics(const double* xyz, int W, const hsd_metric_params& mp, const hsd_norm_bounds& nb,
                               const int32_t* history, double* R, double* D, double* F, int32_t* decision,
-                              cudaStream_t s) {
+                              cudaStream_t s, double* vaj) {
   if (W <= 0) return cudaSuccess;
   const int wpb = kThreads / 32;
-  kinematics_kernel<<<(W + wpb - 1) / wpb, kThreads, 0, s>>>(xyz, W, mp.w, mp, nb, history, R, D, F, decision);
+  kinematics_kernel<<<(W + wpb - 1) / wpb, kThreads, 0, s>>>(xyz, W, mp.w, mp, nb, history, R, D, F, decision, vaj);
   return cudaGetLastError();
 }
 

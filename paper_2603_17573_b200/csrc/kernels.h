@@ -86,9 +86,10 @@ cudaError_t launch_verify(const int32_t* ids, int E, int k, int L, const uint8_t
 cudaError_t launch_gather_tokens(const uint8_t* tokens, const int32_t* ids, int n, uint8_t* out, cudaStream_t s);
 
 // ---- K5 kinematics -------------------------------------------------------------
+// vaj (optional) [W][3]: mean |velocity|, |acceleration|, |jerk| per step over the window
 cudaError_t launch_kinematics(const double* xyz, int W, const hsd_metric_params& mp, const hsd_norm_bounds& nb,
                               const int32_t* history, double* R, double* D, double* F, int32_t* decision,
-                              cudaStream_t s);
+                              cudaStream_t s, double* vaj = nullptr);
 
 // ---- verify-skip offline calibration (k_calib.cu) --------------------------------
 size_t calib_scratch_bytes(int n_traj, int max_tiles);

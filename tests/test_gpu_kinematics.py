@@ -74,3 +74,23 @@ def test_kinematics_fixtures_on_device(torch):
     assert dec2[3] == 1 and dec2[0] == 0  # 14 points of history -> drafter (:533)
     with pytest.raises(H.InvalidInputError):
         H.window_features(x[:, :14].contiguous(), mp, H.LIBERO_GOAL)
+
+
+def test_velocity_acceleration_jerk_diagnostics(torch):
+    """K5's windowed finite-difference kinematics (north-star diagnostics) match
+    the oracle's sequential restatement; R/D/F/decisions are unchanged."""
+    from paper_2603_17573_b200 import synth
+
+    xyz, _ = synth.trajectory_windows(300, 15, seed=11)
+    x = torch.as_tensor(xyz, device="cuda")
+    R0, D0, F0, d0 = H.window_features(x)
+    R, D, F, dec, vaj = H.window_features(x, derivatives=True)
+    assert torch.equal(R, R0) and torch.equal(D, D0) and torch.equal(F, F0) and torch.equal(dec, d0)
+    got = vaj.cpu().numpy()
+    for i in range(xyz.shape[0]):
+        exp = O.window_derivatives(xyz[i])
+        np.testing.assert_allclose(got[i], exp, rtol=1e-12, atol=1e-300)
+    # a straight constant-speed window: |a| = |j| = 0 up to rounding, |v| = the step
+    line = np.stack([np.linspace(0, 0.14, 15), np.zeros(15), np.zeros(15)], 1)[None]
+    _, _, _, _, v = H.window_features(torch.as_tensor(line, device="cuda"), derivatives=True)
+    assert abs(v[0, 0].item() - 0.01) < 1e-12 and v[0, 1].item() < 1e-12 and v[0, 2].item() < 1e-12
