@@ -273,9 +273,17 @@ hsd_status hsd_engine_enable_timing(hsd_engine* e, int max_steps);
 hsd_status hsd_engine_stage_times(hsd_engine* e, int* n_steps, double ms[5]);
 
 /* Same with HOST buffers: H2D of the inputs and D2H of the outputs happen
- * inside the call (pinned staging owned by the engine); synchronous. */
+ * inside the call (device staging owned by the engine); synchronous. */
 hsd_status hsd_step_host(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
                          const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream);
+/* Asynchronous hsd_step_host: enqueue and return.  Two steps may be in flight
+ * (double-buffered device staging): the uploads of step i+1 and the downloads
+ * of step i-1 run on engine copy streams under step i's kernels.  Host buffers
+ * should be pinned, must stay valid and unmodified until hsd_engine_sync, and
+ * the outputs are complete after it returns. */
+hsd_status hsd_step_host_async(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                               const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream);
+hsd_status hsd_engine_sync(hsd_engine* e);
 
 /* ------------------------------------------------------------------------
  * Multi-GPU: row-sharded collection (rank r owns a contiguous id range) with a

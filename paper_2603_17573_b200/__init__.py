@@ -196,6 +196,9 @@ def lib():
                      C.POINTER(NormBounds), C.c_int, _vp],
         "hsd_step_host": [_vp, C.c_int, C.POINTER(StepIO), C.POINTER(VerifyParams), C.POINTER(MetricParams),
                           C.POINTER(NormBounds), C.c_int, _vp],
+        "hsd_step_host_async": [_vp, C.c_int, C.POINTER(StepIO), C.POINTER(VerifyParams), C.POINTER(MetricParams),
+                                C.POINTER(NormBounds), C.c_int, _vp],
+        "hsd_engine_sync": [_vp],
         "hsd_comm_unique_id": [_vp],
         "hsd_comm_create": [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
         "hsd_comm_destroy": [_vp],
@@ -674,6 +677,16 @@ class Engine:
         io = bufs.io()
         check(lib().hsd_step_host(self._h, B, C.byref(io), C.byref(vp), C.byref(mp), C.byref(nb), gap_d,
                                   _stream(stream)))
+
+    def step_host_async(self, B, bufs: StepBuffers, vp: VerifyParams, mp=DEFAULT_METRIC, nb=LIBERO_GOAL, gap_d=1,
+                        stream=None):
+        """Enqueue one host-buffer step (pinned buffers; complete after sync())."""
+        io = bufs.io()
+        check(lib().hsd_step_host_async(self._h, B, C.byref(io), C.byref(vp), C.byref(mp), C.byref(nb), gap_d,
+                                        _stream(stream)))
+
+    def sync(self):
+        check(lib().hsd_engine_sync(self._h))
 
 
 # --------------------------------------------------------------------------- hybrid loop (config 5)

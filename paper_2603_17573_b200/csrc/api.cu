@@ -690,10 +690,9 @@ hsd_status hsd_quantize(int device, const double* actions, int64_t n, const doub
 // ----------------------------------------------------------------------- engine
 }  // extern "C"
 
-struct hsd_engine {
-  hsd_collection* c = nullptr;
-  int max_B = 0, k = 0, L = 0, d_f = 0, w = 0;
-  // device staging for hsd_step_host
+// Device staging of one host-buffer step (hsd_step_host[_async]); two slots
+// let step i+1's uploads and step i-1's downloads overlap step i's kernels.
+struct StageSlot {
   float *q = nullptr, *logits = nullptr, *fnow = nullptr, *fprev = nullptr;
   double* xyz = nullptr;
   int32_t* hist = nullptr;
@@ -703,6 +702,16 @@ struct hsd_engine {
   uint8_t* tok = nullptr;
   double *R = nullptr, *D = nullptr, *F = nullptr;
   int32_t* dec = nullptr;
+  cudaEvent_t uploaded = nullptr, computed = nullptr, downloaded = nullptr;
+  bool used = false;
+};
+
+struct hsd_engine {
+  hsd_collection* c = nullptr;
+  int max_B = 0, k = 0, L = 0, d_f = 0, w = 0;
+  StageSlot slot[2];
+  int next_slot = 0;
+  cudaStream_t up = nullptr, down = nullptr;  // H2D / D2H copy streams
   // stage timing, kStepEvents per step: [0] start, [1] after similarity,
   // [2] after select, [3] end (verify + join), [4]/[5] kinematics on the side stream
   std::vector<cudaEvent_t> ev;
@@ -733,20 +742,26 @@ hsd_status hsd_engine_create(hsd_collection* c, int max_B, int k, int L, int d_f
   auto alloc = [&](auto** p, size_t bytes) {
     if (r == cudaSuccess && bytes) r = cudaMalloc(p, bytes);
   };
-  alloc(&e->q, (size_t)max_B * c->dim * 4);
-  alloc(&e->logits, (size_t)max_B * L * 256 * 4);
-  alloc(&e->fnow, (size_t)max_B * d_f * 4);
-  alloc(&e->fprev, (size_t)max_B * d_f * 4);
-  alloc(&e->xyz, (size_t)max_B * w * 3 * 8);
-  alloc(&e->hist, (size_t)max_B * 4);
-  alloc(&e->scores, (size_t)max_B * k * 8);
-  alloc(&e->ids, (size_t)max_B * k * 4);
-  alloc(&e->out, (size_t)max_B * sizeof(hsd_outcome));
-  alloc(&e->tok, (size_t)max_B * L);
-  alloc(&e->R, (size_t)max_B * 8);
-  alloc(&e->D, (size_t)max_B * 8);
-  alloc(&e->F, (size_t)max_B * 8);
-  alloc(&e->dec, (size_t)max_B * 4);
+  for (StageSlot& S : e->slot) {
+    alloc(&S.q, (size_t)max_B * c->dim * 4);
+    alloc(&S.logits, (size_t)max_B * L * 256 * 4);
+    alloc(&S.fnow, (size_t)max_B * d_f * 4);
+    alloc(&S.fprev, (size_t)max_B * d_f * 4);
+    alloc(&S.xyz, (size_t)max_B * w * 3 * 8);
+    alloc(&S.hist, (size_t)max_B * 4);
+    alloc(&S.scores, (size_t)max_B * k * 8);
+    alloc(&S.ids, (size_t)max_B * k * 4);
+    alloc(&S.out, (size_t)max_B * sizeof(hsd_outcome));
+    alloc(&S.tok, (size_t)max_B * L);
+    alloc(&S.R, (size_t)max_B * 8);
+    alloc(&S.D, (size_t)max_B * 8);
+    alloc(&S.F, (size_t)max_B * 8);
+    alloc(&S.dec, (size_t)max_B * 4);
+    for (cudaEvent_t* ev : {&S.uploaded, &S.computed, &S.downloaded})
+      if (r == cudaSuccess) r = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  }
+  if (r == cudaSuccess) r = cudaStreamCreateWithFlags(&e->up, cudaStreamNonBlocking);
+  if (r == cudaSuccess) r = cudaStreamCreateWithFlags(&e->down, cudaStreamNonBlocking);
   if (r != cudaSuccess) {
     hsd_engine_destroy(e);
     return cuda_fail(r, "engine buffers");
@@ -802,9 +817,16 @@ hsd_status hsd_engine_destroy(hsd_engine* e) {
     cudaEventDestroy(e->fork);
     cudaEventDestroy(e->join);
   }
-  void* ps[] = {e->q, e->logits, e->fnow, e->fprev, e->xyz, e->hist, e->scores, e->ids, e->out, e->tok, e->R, e->D,
-                e->F, e->dec};
-  for (void* p : ps) cudaFree(p);
+  if (e->up) cudaStreamSynchronize(e->up);
+  if (e->down) cudaStreamSynchronize(e->down);
+  for (StageSlot& S : e->slot) {
+    void* ps[] = {S.q, S.logits, S.fnow, S.fprev, S.xyz, S.hist, S.scores, S.ids, S.out, S.tok, S.R, S.D, S.F, S.dec};
+    for (void* p : ps) cudaFree(p);
+    for (cudaEvent_t ev : {S.uploaded, S.computed, S.downloaded})
+      if (ev) cudaEventDestroy(ev);
+  }
+  if (e->up) cudaStreamDestroy(e->up);
+  if (e->down) cudaStreamDestroy(e->down);
   delete e;
   return HSD_OK;
 }
@@ -860,56 +882,84 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
   return HSD_OK;
 }
 
-hsd_status hsd_step_host(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
-                         const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream) {
+hsd_status hsd_step_host_async(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                               const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream) {
   if (!e || !io) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   if (B < 0 || B > e->max_B) return fail(HSD_ERR_INVALID_INPUT, "batch %d outside [0, %d]", B, e->max_B);
   if (B == 0) return HSD_OK;
   hsd_status st = require_device(e->c->device);
   if (st != HSD_OK) return st;
-  cudaStream_t s = (cudaStream_t)stream;
+  cudaStream_t s = (cudaStream_t)stream, up = e->up, down = e->down;
+  StageSlot& S = e->slot[e->next_slot];
+  e->next_slot ^= 1;
   const int dim = e->c->dim;
+  // uploads: the slot's inputs were last read by the kernels of step i-2
+  if (S.used) CU(cudaStreamWaitEvent(up, S.computed, 0));
   hsd_step_io d{};
-  CU(cudaMemcpyAsync(e->q, io->queries, (size_t)B * dim * 4, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(e->logits, io->logits, (size_t)B * e->L * 256 * 4, cudaMemcpyHostToDevice, s));
-  d.queries = e->q;
-  d.logits = e->logits;
+  CU(cudaMemcpyAsync(S.q, io->queries, (size_t)B * dim * 4, cudaMemcpyHostToDevice, up));
+  CU(cudaMemcpyAsync(S.logits, io->logits, (size_t)B * e->L * 256 * 4, cudaMemcpyHostToDevice, up));
+  d.queries = S.q;
+  d.logits = S.logits;
   if (io->feat_now && io->feat_prev && e->d_f) {
-    CU(cudaMemcpyAsync(e->fnow, io->feat_now, (size_t)B * e->d_f * 4, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(e->fprev, io->feat_prev, (size_t)B * e->d_f * 4, cudaMemcpyHostToDevice, s));
-    d.feat_now = e->fnow;
-    d.feat_prev = e->fprev;
+    CU(cudaMemcpyAsync(S.fnow, io->feat_now, (size_t)B * e->d_f * 4, cudaMemcpyHostToDevice, up));
+    CU(cudaMemcpyAsync(S.fprev, io->feat_prev, (size_t)B * e->d_f * 4, cudaMemcpyHostToDevice, up));
+    d.feat_now = S.fnow;
+    d.feat_prev = S.fprev;
   }
   if (io->xyz) {
-    CU(cudaMemcpyAsync(e->xyz, io->xyz, (size_t)B * e->w * 3 * 8, cudaMemcpyHostToDevice, s));
-    d.xyz = e->xyz;
+    CU(cudaMemcpyAsync(S.xyz, io->xyz, (size_t)B * e->w * 3 * 8, cudaMemcpyHostToDevice, up));
+    d.xyz = S.xyz;
   }
   if (io->history) {
-    CU(cudaMemcpyAsync(e->hist, io->history, (size_t)B * 4, cudaMemcpyHostToDevice, s));
-    d.history = e->hist;
+    CU(cudaMemcpyAsync(S.hist, io->history, (size_t)B * 4, cudaMemcpyHostToDevice, up));
+    d.history = S.hist;
   }
-  d.scores = e->scores;
-  d.ids = e->ids;
-  d.out = e->out;
-  d.tokens = e->tok;
-  d.R = e->R;
-  d.D = e->D;
-  d.F = e->F;
-  d.decision = e->dec;
+  CU(cudaEventRecord(S.uploaded, up));
+  d.scores = S.scores;
+  d.ids = S.ids;
+  d.out = S.out;
+  d.tokens = S.tok;
+  d.R = S.R;
+  d.D = S.D;
+  d.F = S.F;
+  d.decision = S.dec;
+  // kernels: after this step's uploads and after step i-2's downloads of the slot's outputs
+  CU(cudaStreamWaitEvent(s, S.uploaded, 0));
+  if (S.used) CU(cudaStreamWaitEvent(s, S.downloaded, 0));
   st = hsd_step(e, B, &d, vp, mp, nb, gap_d, stream);
   if (st != HSD_OK) return st;
-  if (io->scores) CU(cudaMemcpyAsync(io->scores, e->scores, (size_t)B * e->k * 8, cudaMemcpyDeviceToHost, s));
-  if (io->ids) CU(cudaMemcpyAsync(io->ids, e->ids, (size_t)B * e->k * 4, cudaMemcpyDeviceToHost, s));
-  if (io->out) CU(cudaMemcpyAsync(io->out, e->out, (size_t)B * sizeof(hsd_outcome), cudaMemcpyDeviceToHost, s));
-  if (io->tokens) CU(cudaMemcpyAsync(io->tokens, e->tok, (size_t)B * e->L, cudaMemcpyDeviceToHost, s));
+  CU(cudaEventRecord(S.computed, s));
+  // downloads overlap the next step's kernels
+  CU(cudaStreamWaitEvent(down, S.computed, 0));
+  if (io->scores) CU(cudaMemcpyAsync(io->scores, S.scores, (size_t)B * e->k * 8, cudaMemcpyDeviceToHost, down));
+  if (io->ids) CU(cudaMemcpyAsync(io->ids, S.ids, (size_t)B * e->k * 4, cudaMemcpyDeviceToHost, down));
+  if (io->out) CU(cudaMemcpyAsync(io->out, S.out, (size_t)B * sizeof(hsd_outcome), cudaMemcpyDeviceToHost, down));
+  if (io->tokens) CU(cudaMemcpyAsync(io->tokens, S.tok, (size_t)B * e->L, cudaMemcpyDeviceToHost, down));
   if (io->xyz) {
-    if (io->R) CU(cudaMemcpyAsync(io->R, e->R, (size_t)B * 8, cudaMemcpyDeviceToHost, s));
-    if (io->D) CU(cudaMemcpyAsync(io->D, e->D, (size_t)B * 8, cudaMemcpyDeviceToHost, s));
-    if (io->F) CU(cudaMemcpyAsync(io->F, e->F, (size_t)B * 8, cudaMemcpyDeviceToHost, s));
-    if (io->decision) CU(cudaMemcpyAsync(io->decision, e->dec, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+    if (io->R) CU(cudaMemcpyAsync(io->R, S.R, (size_t)B * 8, cudaMemcpyDeviceToHost, down));
+    if (io->D) CU(cudaMemcpyAsync(io->D, S.D, (size_t)B * 8, cudaMemcpyDeviceToHost, down));
+    if (io->F) CU(cudaMemcpyAsync(io->F, S.F, (size_t)B * 8, cudaMemcpyDeviceToHost, down));
+    if (io->decision) CU(cudaMemcpyAsync(io->decision, S.dec, (size_t)B * 4, cudaMemcpyDeviceToHost, down));
   }
-  CU(cudaStreamSynchronize(s));
+  CU(cudaEventRecord(S.downloaded, down));
+  S.used = true;
   return HSD_OK;
+}
+
+hsd_status hsd_engine_sync(hsd_engine* e) {
+  if (!e) return fail(HSD_ERR_INVALID_INPUT, "null engine");
+  hsd_status st = require_device(e->c->device);
+  if (st != HSD_OK) return st;
+  CU(cudaStreamSynchronize(e->down));  // the last download waits for every earlier step
+  CU(cudaStreamSynchronize(e->up));
+  return HSD_OK;
+}
+
+hsd_status hsd_step_host(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                         const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream) {
+  hsd_status st = hsd_step_host_async(e, B, io, vp, mp, nb, gap_d, stream);
+  if (st != HSD_OK) return st;
+  return hsd_engine_sync(e);
 }
 
 // ------------------------------------------------------------------ multi-GPU

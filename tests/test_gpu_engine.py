@@ -1,0 +1,67 @@
+"""The fused decode-round engine (hsd_step / hsd_step_host / hsd_step_host_async):
+host-buffer steps equal device-buffer steps, and the double-buffered async path
+keeps every in-flight step's inputs and outputs separate."""
+import numpy as np
+import pytest
+
+import paper_2603_17573_b200 as H
+from paper_2603_17573_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    return torch
+
+
+def make_inputs(torch, col, n, dim, B, L, d_f, s):
+    q = H.gen_queries(H.REAL, 7 + s, 5, n, 0, B, dim)
+    rows = H.query_rows(7 + s, H.REAL, n, 0, B)
+    lg = H.gen_logits(col, 3 + s, rows, L)
+    fn, fp = H.gen_features(5 + s, B, d_f)
+    xyz = torch.as_tensor(synth.trajectory_windows(B, 15, seed=4 + s)[0], device="cuda")
+    hist = torch.full((B,), 100, dtype=torch.int32, device="cuda")
+    return dict(queries=q, logits=lg, feat_now=fn, feat_prev=fp, xyz=xyz, history=hist)
+
+
+def outputs(torch, B, k, L, device):
+    pin = device == "cpu"
+    mk = lambda shape, dt: (torch.empty(shape, dtype=dt, device=device).pin_memory() if pin  # noqa: E731
+                            else torch.empty(shape, dtype=dt, device=device))
+    return dict(scores=mk((B, k), torch.float64), ids=mk((B, k), torch.int32), out=mk((B, 20), torch.uint8),
+                tokens=mk((B, L), torch.uint8), R=mk((B,), torch.float64), D=mk((B,), torch.float64),
+                F=mk((B,), torch.float64), decision=mk((B,), torch.int32))
+
+
+def test_host_and_async_steps_match_device_steps(torch):
+    n, dim, B, k, L, d_f = 20000, 256, 48, 8, 7, 256
+    col = H.Collection(dim, capacity=n)
+    col.generate(H.REAL, 5, n)
+    eng = H.Engine(col, B, k, L, d_f, 15)
+    vp = H.VerifyParams.make(skip_enabled=True, min_S=0.95, O_dist=5)
+    S = 5
+    ins = [make_inputs(torch, col, n, dim, B, L, d_f, s) for s in range(S)]
+    ref = []
+    for s in range(S):
+        o = outputs(torch, B, k, L, "cuda")
+        eng.step(B, H.StepBuffers(**ins[s], **o), vp)
+        torch.cuda.synchronize()
+        ref.append({kk: v.cpu() for kk, v in o.items()})
+    h_in = [{kk: v.cpu().pin_memory() for kk, v in d.items()} for d in ins]
+    # synchronous host-buffer step
+    o = outputs(torch, B, k, L, "cpu")
+    eng.step_host(B, H.StepBuffers(**h_in[2], **o), vp)
+    for kk in o:
+        assert torch.equal(o[kk], ref[2][kk]), kk
+    # async: all S steps in flight through the two staging slots, distinct host outputs
+    outs = [outputs(torch, B, k, L, "cpu") for _ in range(S)]
+    for rep in range(2):
+        for s in range(S):
+            eng.step_host_async(B, H.StepBuffers(**h_in[s], **outs[s]), vp)
+        eng.sync()
+        for s in range(S):
+            for kk in outs[s]:
+                assert torch.equal(outs[s][kk], ref[s][kk]), (rep, s, kk)
