@@ -236,14 +236,17 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   const int path = choose_path(B, c->dtype);
   const int W = pass_width(path);
   const int Bs0 = std::min(B, W);
-  const int lists0 = is_tc(path) ? hsd::sim_tc_lists(rows, nsm) : hsd::sim_plan(Bs0, rows, c->dim, nsm).lists;
+  const int lists0 = path == kPathTc ? hsd::sim_wide_lists(Bs0, rows, nsm)
+                     : is_tc(path)    ? hsd::sim_tc_lists(rows, nsm)
+                                      : hsd::sim_plan(Bs0, rows, c->dim, nsm).lists;
   const size_t qscratch = path == kPathTc    ? hsd::sim_wide_scratch_bytes(c->dim)
                           : path == kPathTc1 ? hsd::sim_tc1_scratch_bytes(c->dim)
                           : path == kPathTc3 ? hsd::sim_tc_scratch_bytes(c->dim)
                                              : 0;
   Scratch* sc = nullptr;
-  st = get_scratch(c, s, (size_t)std::max(lists0, 4 * nsm) * Bs0 * hsd::dev::kCandLocal * sizeof(uint64_t), qscratch,
-                   &sc);
+  // partial lists: the tcgen05 paths write exactly lists0 per pass; the SIMT plan may use up to 4 per SM
+  const size_t n_lists = is_tc(path) ? (size_t)lists0 : (size_t)std::max(lists0, 4 * nsm);
+  st = get_scratch(c, s, n_lists * Bs0 * hsd::dev::kCandLocal * sizeof(uint64_t), qscratch, &sc);
   if (st != HSD_OK) return st;
   CU(cudaMemsetAsync(sc->overflow, 0, sizeof(int), s));
   for (int b0 = 0; b0 < B; b0 += W) {
@@ -253,7 +256,7 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
     hsd::SimPlan plan = hsd::sim_plan(Bs, rows, c->dim, nsm);
     const float* q = queries + (size_t)b0 * c->dim;
     if (p == kPathTc) {
-      plan.lists = hsd::sim_tc_lists(rows, nsm);
+      plan.lists = hsd::sim_wide_lists(Bs, rows, nsm);
       plan.gamma = hsd::sim_wide_gamma(c->dim, c->dtype);
       CU(hsd::launch_sim_wide(c->keys, c->dtype, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial,
                               nullptr, s));
@@ -497,6 +500,7 @@ hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, 
   hsd_status st = require_device(c->device);
   if (st != HSD_OK) return st;
   if (c->n == 0) return HSD_OK;
+  if (variant == 1 && B > 256) return fail(HSD_ERR_INVALID_INPUT, "debug dump supports B <= 256");
   const int lists = hsd::sim_tc_lists(c->n, num_sms(c->device));
   Scratch* sc = nullptr;
   st = get_scratch(c, (cudaStream_t)stream, (size_t)lists * B * hsd::dev::kCandLocal * 8,

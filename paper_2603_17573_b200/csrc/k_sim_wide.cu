@@ -85,7 +85,12 @@ struct __align__(1024) WideSmem {
   uint32_t tmem_base;
 };
 
-template <bool kBf16, int NS, int GB, bool kDump>
+// kMC > 1: a cluster of kMC CTAs shares one key range; CTA rank r holds query
+// group r (256 queries each) and issues every kMC-th key tile with a TMA
+// multicast into all kMC CTAs, so the keys cross HBM once for up to 1024
+// queries.  A ring slot is refilled only after every CTA's MMAs released it
+// (multicast commits into each CTA's k_empty, count kMC).
+template <bool kBf16, int NS, int GB, bool kDump, int kMC = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     sim_wide_kernel(const __grid_constant__ CUtensorMap keys_map, const __grid_constant__ CUtensorMap q_map,
                     int64_t row_begin, int64_t row_end, int dim, int B, int64_t blocks_per_cta,
@@ -98,18 +103,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   WideSmem<NS, GB>& S = *reinterpret_cast<WideSmem<NS, GB>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
-  const int64_t blk0 = (int64_t)blockIdx.x * blocks_per_cta;
+  const int unit = kMC > 1 ? (int)cluster_id_x() : (int)blockIdx.x;  // key-range owner
+  const int n_units = kMC > 1 ? (int)n_clusters_x() : (int)gridDim.x;
+  const int rank = kMC > 1 ? (int)cluster_ctarank() : 0;             // query group
+  const int q_base = rank * kBQ;
+  const int64_t blk0 = (int64_t)unit * blocks_per_cta;
   const int64_t blk1 = std::min<int64_t>(blk0 + blocks_per_cta, n_blocks);
   const int nk = (dim + kBK - 1) / kBK;
   // Each CTA walks the k-chunks starting at its own offset, so the 148 CTAs do
   // not all request the same (L2-resident) query tile at the same moment; the
   // filter's error bound does not depend on the accumulation order.
-  const int kc0 = (int)(((int64_t)blockIdx.x * nk) / gridDim.x);
+  const int kc0 = (int)(((int64_t)unit * nk) / n_units);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kKS; ++i) {
       mbar_init(&S.k_full[i], 1);
-      mbar_init(&S.k_empty[i], 1);
+      mbar_init(&S.k_empty[i], kMC);
     }
     for (int i = 0; i < kQS; ++i) {
       mbar_init(&S.q_full[i], 1);
@@ -128,6 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kMC > 1) cluster_sync_all();  // peers' barriers exist before any multicast / remote arrive
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
 
@@ -138,14 +148,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol = policy_evict_first();
       int ks = 0;
       uint32_t kph = 0;
+      uint32_t tile = 0;
       for (int64_t g0 = blk0; g0 < blk1; g0 += kGB) {
         const int gb = (int)std::min<int64_t>(kGB, blk1 - g0);
         for (int kc = 0; kc < nk; ++kc)
-          for (int m = 0; m < gb; ++m) {
+          for (int m = 0; m < gb; ++m, ++tile) {
             mbar_wait(&S.k_empty[ks], kph ^ 1);
             mbar_expect_tx(&S.k_full[ks], kKeyTile);
             const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
-            tma_load_2d(&S.kbuf[ks][0], &keys_map, &S.k_full[ks], c * kBK, (int)(row_begin + (g0 + m) * kBM), pol);
+            if constexpr (kMC > 1) {
+              if ((int)(tile % kMC) == rank)
+                tma_load_2d_mc(&S.kbuf[ks][0], &keys_map, &S.k_full[ks], c * kBK,
+                               (int)(row_begin + (g0 + m) * kBM), (uint16_t)((1u << kMC) - 1), pol);
+            } else {
+              tma_load_2d(&S.kbuf[ks][0], &keys_map, &S.k_full[ks], c * kBK, (int)(row_begin + (g0 + m) * kBM),
+                          pol);
+            }
             if (++ks == kKS) {
               ks = 0;
               kph ^= 1;
@@ -165,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&S.q_empty[qs], qph ^ 1);
           mbar_expect_tx(&S.q_full[qs], Cfg::kQTile);
           const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
-          tma_load_2d(&S.qbuf[qs][0], &q_map, &S.q_full[qs], c * kBK, 0, pol);
+          tma_load_2d(&S.qbuf[qs][0], &q_map, &S.q_full[qs], c * kBK, q_base, pol);
           if (++qs == kQS) {
             qs = 0;
             qph ^= 1;
@@ -202,7 +220,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
               mma_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
           }
-          tc_commit(&S.k_empty[ks]);
+          if constexpr (kMC > 1)
+            tc_commit_mc(&S.k_empty[ks], (uint16_t)((1u << kMC) - 1));
+          else
+            tc_commit(&S.k_empty[ks]);
           if (++ks == kKS) {
             ks = 0;
             kph ^= 1;
@@ -249,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
               const int q = j * kStgQ + half * 16 + t;
-              if (base + r < row_end && q < B)
+              if (base + r < row_end && q_base + q < B)
                 dump[(size_t)q * (row_end - row_begin) + (base + r - row_begin)] = __uint_as_float(acc[t]);
             }
           } else {
@@ -259,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int ql = ew * 4 + i;
-              if (j * kStgQ + ql < B) {
+              if (q_base + j * kStgQ + ql < B) {
                 uint64_t& tp = top[j * 4 + i];
                 uint64_t key[4];
 #pragma unroll
@@ -294,12 +315,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int q = j * kStgQ + ew * 4 + i;
-          if (q < B) partial[((size_t)blockIdx.x * B + q) * kCandLocal + lane] = top[j * 4 + i];
+          if (q_base + q < B) partial[((size_t)unit * B + q_base + q) * kCandLocal + lane] = top[j * 4 + i];
         }
     }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kMC > 1) cluster_sync_all();  // no CTA leaves while peers may still multicast into it
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
@@ -318,14 +340,31 @@ __global__ void pad_queries_bf16_kernel(const float* __restrict__ q, int B, int 
     out[(size_t)row * dim + c] = row < B ? hsd_bf16_bits(q[(size_t)row * dim + c]) : (uint16_t)0;
 }
 
-template <bool kBf16, int NS, int GB, bool kDump>
+template <bool kBf16, int NS, int GB, bool kDump, int kMC = 1>
 cudaError_t launch_ns(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, int64_t re, int dim, int B,
                       int lists, int64_t per, uint64_t* partial, float* dump, cudaStream_t s) {
   const size_t smem = sizeof(WideSmem<NS, GB>) + 1024;
-  auto kern = sim_wide_kernel<kBf16, NS, GB, kDump>;
+  auto kern = sim_wide_kernel<kBf16, NS, GB, kDump, kMC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<lists, kThreads, smem, s>>>(km, qm, rb, re, dim, B, per, partial, dump);
+  if constexpr (kMC == 1) {
+    kern<<<lists, kThreads, smem, s>>>(km, qm, rb, re, dim, B, per, partial, dump);
+  } else {  // `lists` clusters of kMC CTAs
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(lists * kMC));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kMC;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, km, qm, rb, re, dim, B, per, partial, dump);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
@@ -358,7 +397,62 @@ cudaError_t launch_dispatch(int NS, const CUtensorMap& km, const CUtensorMap& qm
 
 }  // namespace
 
-int sim_wide_max_batch() { return 256; }
+int sim_wide_max_batch() { return 1024; }
+
+// Query groups (cluster size) of one pass: B <= 256 -> 1 CTA per key range;
+// more -> ceil(B / 256) CTAs per cluster sharing each key tile by multicast.
+static int wide_groups(int B) { return B <= 256 ? 1 : (B + 255) / 256; }
+
+// Clusters of G CTAs that fit on the device at once (GPC packing leaves some
+// SMs unused for G = 3, 4); a persistent grid larger than this would run a
+// second wave.  Cached per G (same kernel resources for both dtypes).
+static int max_active_clusters(int G, int num_sms) {
+  static int cache[5] = {0, 0, 0, 0, 0};
+  if (G <= 1) return num_sms;
+  if (cache[G]) return cache[G];
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(G * (num_sms / G)));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = sizeof(WideSmem<4, 1>) + 1024;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  cudaError_t e = cudaSuccess;
+  switch (G) {
+    case 2:
+      e = cudaFuncSetAttribute(sim_wide_kernel<false, 4, 1, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)cfg.dynamicSmemBytes);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&n, sim_wide_kernel<false, 4, 1, false, 2>, &cfg);
+      break;
+    case 3:
+      e = cudaFuncSetAttribute(sim_wide_kernel<false, 4, 1, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)cfg.dynamicSmemBytes);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&n, sim_wide_kernel<false, 4, 1, false, 3>, &cfg);
+      break;
+    default:
+      e = cudaFuncSetAttribute(sim_wide_kernel<false, 4, 1, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)cfg.dynamicSmemBytes);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&n, sim_wide_kernel<false, 4, 1, false, 4>, &cfg);
+      break;
+  }
+  if (e != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = num_sms / G;
+  }
+  cache[G] = std::min(n, num_sms / G);
+  return cache[G];
+}
+
+int sim_wide_lists(int B, int64_t rows, int num_sms) {
+  const int g = wide_groups(B);
+  const int64_t blocks = (rows + kBM - 1) / kBM;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, max_active_clusters(g, num_sms)));
+}
 
 double sim_wide_gamma(int dim, int key_dtype) {
   // Accumulation: fp32 tensor-core accumulator (not round-to-nearest) over dim
@@ -374,32 +468,48 @@ double sim_wide_gamma(int dim, int key_dtype) {
   return (2.0 + 1.0 / 1024.0) / 1024.0 * 1.0001 + acc;
 }
 
-size_t sim_wide_scratch_bytes(int dim) { return (size_t)256 * dim * sizeof(float); }
+size_t sim_wide_scratch_bytes(int dim) { return (size_t)1024 * dim * sizeof(float); }
 
 cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin, int64_t row_end,
                             int dim, const float* queries, int B, int lists, void* scratch, uint64_t* partial,
                             float* dump, cudaStream_t s) {
-  if (B < 1 || B > 256) return cudaErrorInvalidValue;
-  const int NS = B <= 64 ? 1 : (B <= 128 ? 2 : 4);
-  const int rows = 64 * NS;
+  if (B < 1 || B > 1024) return cudaErrorInvalidValue;
+  const int groups = wide_groups(B);
+  const int NS = groups > 1 ? 4 : (B <= 64 ? 1 : (B <= 128 ? 2 : 4));
+  const int box = 64 * NS;          // query rows per CTA
+  const int rows = box * groups;    // padded query slab
   const bool bf16 = key_dtype == HSD_DTYPE_BF16;
   if (bf16 && dim % 8) return cudaErrorInvalidValue;  // TMA row stride must be a multiple of 16 B
   CUtensorMap km, qm;
   if (bf16) {
     pad_queries_bf16_kernel<<<rows, 256, 0, s>>>(queries, B, dim, (uint16_t*)scratch);
     if (!tc_make_map_bf16(&km, keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
-        !tc_make_map_bf16(&qm, scratch, (uint64_t)rows, (uint64_t)dim, (uint32_t)rows))
+        !tc_make_map_bf16(&qm, scratch, (uint64_t)rows, (uint64_t)dim, (uint32_t)box))
       return cudaErrorInvalidValue;
   } else {
     pad_queries_f32_kernel<<<rows, 256, 0, s>>>(queries, B, dim, (float*)scratch);
     if (!tc_make_map(&km, (const float*)keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
-        !tc_make_map(&qm, (const float*)scratch, (uint64_t)rows, (uint64_t)dim, (uint32_t)rows))
+        !tc_make_map(&qm, (const float*)scratch, (uint64_t)rows, (uint64_t)dim, (uint32_t)box))
       return cudaErrorInvalidValue;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
   const int64_t per = (n_blocks + lists - 1) / lists;
+  if (groups > 1) {
+    if (dump) return cudaErrorInvalidValue;  // the debug dump covers single-group passes
+    switch (groups) {
+#define HSD_WIDE_MC(G)                                                                                            \
+  case G:                                                                                                         \
+    return bf16 ? launch_ns<true, 4, 1, false, G>(km, qm, row_begin, row_end, dim, B, lists, per, partial, dump, s) \
+                : launch_ns<false, 4, 1, false, G>(km, qm, row_begin, row_end, dim, B, lists, per, partial, dump, s);
+      HSD_WIDE_MC(2)
+      HSD_WIDE_MC(3)
+      HSD_WIDE_MC(4)
+#undef HSD_WIDE_MC
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (bf16)
     return dump ? launch_dispatch<true, true>(NS, km, qm, row_begin, row_end, dim, B, lists, per, partial, dump, s)
                 : launch_dispatch<true, false>(NS, km, qm, row_begin, row_end, dim, B, lists, per, partial, dump, s);

@@ -121,7 +121,7 @@ def test_wide_batches_bit_identical(torch, kind):
     for dim, n in ((64, 4000), (4096, 1800)):
         col = H.Collection(dim, capacity=n)
         col.generate(kind, 21, n)
-        for B in (5, 65, 127, 128, 129, 200, 256, 300):
+        for B in (5, 65, 127, 128, 129, 200, 256, 300, 513, 700, 1024, 1100):
             q = H.gen_queries(kind, 22, 21, n, 1, B, dim)
             sc, ids = col.search_topk_exact(q, 8)
             osc, oid = O.search_synth(kind, 21, n, q.cpu().numpy(), 8)
@@ -141,7 +141,7 @@ def test_bf16_collection_exact_over_stored_keys(torch, kind):
         assert keys.dtype == torch.bfloat16
         ok = O.gen_keys(kind | O.KEYS_BF16, 31, 0, n, dim)
         np.testing.assert_array_equal(keys.float().cpu().numpy(), ok)
-        for B, k in ((1, 8), (3, 1), (64, 8), (100, 32), (256, 8)):
+        for B, k in ((1, 8), (3, 1), (64, 8), (100, 32), (256, 8), (683, 3), (1024, 8)):
             q = H.gen_queries(kind, 32, 31, n, 0, B, dim)
             sc, ids = col.search_topk_exact(q, k)
             osc, oid = O.search_synth(kind | O.KEYS_BF16, 31, n, q.cpu().numpy(), k)

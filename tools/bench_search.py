@@ -49,7 +49,7 @@ def main():
                 e1.record(s)
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / a.iters
-                gbs = a.n * a.dim * esz * ((B + 255) // 256 if path == "tc" else (B + 63) // 64) / (ms / 1e3) / 1e9
+                gbs = a.n * a.dim * esz * ((B + 1023) // 1024 if path == "tc" else (B + 63) // 64) / (ms / 1e3) / 1e9
                 print(json.dumps({"dtype": dt, "path": path, "B": B, "n": a.n, "dim": a.dim, "ms": ms,
                                   "queries_per_s": B / (ms / 1e3), "key_stream_GBps": gbs,
                                   "overflow": col.overflow_count()}), flush=True)
