@@ -90,6 +90,15 @@ hsd_status hsd_collection_device(const hsd_collection* c, int* device);
  * fails with HSD_ERR_INVALID_INPUT on a bf16 collection. */
 hsd_status hsd_collection_keys(const hsd_collection* c, const float** keys, const uint8_t** tokens);
 hsd_status hsd_collection_dtype(const hsd_collection* c, int* dtype);
+
+/* Filter mode of an fp32 collection.  HSD_FILTER_BF16_COPY keeps a bf16 copy
+ * of the keys resident (+50% HBM) that the tensor-core filter streams at half
+ * the bytes per scan; the exact fp64 rescoring still reads the fp32 keys, so
+ * ids and scores stay bit-identical to the reference (the filter margin widens
+ * to the bf16 x bf16 error bound).  Kept current by insert / generate. */
+enum { HSD_FILTER_NATIVE = 0, HSD_FILTER_BF16_COPY = 1 };
+hsd_status hsd_collection_set_filter(hsd_collection* c, int filter);
+hsd_status hsd_collection_get_filter(const hsd_collection* c, int* filter);
 /* Untyped key view (fp32 or bf16 bits per hsd_collection_dtype). */
 hsd_status hsd_collection_data(const hsd_collection* c, const void** keys, const uint8_t** tokens);
 
@@ -135,7 +144,8 @@ hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count
 /* Diagnostics: a tcgen05 similarity kernel's approximate (filter) scores of
  * B queries against every record, fp32 [B][size] (device); variant 1 = the
  * wide filter of the default path (TF32 over fp32 keys, bf16 over bf16 keys;
- * B <= 256), 2 = 64-query TF32 kernel, 3 = 3xTF32 filter (B <= 64).  Used by
+ * B <= 256), 2 = 64-query TF32 kernel, 3 = 3xTF32 filter (B <= 64), 4 = the
+ * bf16 filter copy of an fp32 collection (B <= 256).  Used by
  * the tests to check the error bounds the exact rescoring relies on. */
 hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
                                 void* stream);

@@ -170,6 +170,8 @@ def lib():
         "hsd_collection_create": [C.c_int, C.c_int, C.c_int64, C.POINTER(_vp)],
         "hsd_collection_create_ex": [C.c_int, C.c_int, C.c_int64, C.c_int, C.POINTER(_vp)],
         "hsd_collection_dtype": [_vp, C.POINTER(C.c_int)],
+        "hsd_collection_set_filter": [_vp, C.c_int],
+        "hsd_collection_get_filter": [_vp, C.POINTER(C.c_int)],
         "hsd_collection_data": [_vp, C.POINTER(_vp), C.POINTER(_vp)],
         "hsd_collection_destroy": [_vp],
         "hsd_collection_size": [_vp, C.POINTER(C.c_int64)],
@@ -389,12 +391,22 @@ class Collection:
 
     def debug_sim_scores(self, queries, variant=1, stream=None):
         """Approximate tcgen05 filter scores float32 [B, size] (diagnostics; variant 1 = wide TF32/bf16
-        filter of the default path, 2 = 64-query TF32, 3 = 3xTF32)."""
+        filter of the default path, 2 = 64-query TF32, 3 = 3xTF32, 4 = the bf16 filter copy)."""
         torch = _torch()
         q = queries.contiguous()
         out = torch.empty((q.shape[0], self.size()), dtype=torch.float32, device=q.device)
         check(lib().hsd_debug_sim_scores(self._h, _ptr(q), q.shape[0], variant, _ptr(out), _stream(stream)))
         return out
+
+    def set_filter(self, filter) -> None:
+        """"native" (default) or "bf16_copy": keep a bf16 filter copy of fp32 keys (half the scan bytes; results
+        stay bit-identical: the exact rescoring reads the fp32 keys)."""
+        check(lib().hsd_collection_set_filter(self._h, {"native": 0, "bf16_copy": 1}.get(filter, filter)))
+
+    def filter(self) -> str:
+        f = C.c_int()
+        check(lib().hsd_collection_get_filter(self._h, C.byref(f)))
+        return "bf16_copy" if f.value == 1 else "native"
 
     def save_image(self, path: str) -> None:
         """Binary columnar device image (hsd_collection_save_image)."""

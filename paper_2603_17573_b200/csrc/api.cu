@@ -103,6 +103,8 @@ __global__ void offset_ids_kernel(int32_t* ids, int n, int64_t off) {
 struct Scratch {
   uint64_t* partial = nullptr;
   size_t partial_cap = 0;  // bytes
+  void* sel = nullptr;     // K2 per-query candidate / exact-score scratch
+  size_t sel_cap = 0;
   float* qsplit = nullptr;  // Qh | Ql of the tcgen05 path
   size_t qsplit_cap = 0;
   int* overflow = nullptr;
@@ -117,6 +119,10 @@ struct hsd_collection {
   int64_t n = 0;
   int64_t cap = 0;
   void* keys = nullptr;  // fp32 or bf16 [cap][dim]
+  // Optional bf16 filter copy of an fp32 collection ([cap][dim], RN-even):
+  // the tensor-core filter streams it (half the HBM bytes); the exact fp64
+  // rescoring still reads the fp32 keys, so results are unchanged.
+  uint16_t* shadow = nullptr;
   uint8_t* tokens = nullptr;
   unsigned long long* maxnorm = nullptr;  // fp64 bits of max row norm
   std::mutex mu;
@@ -142,11 +148,31 @@ hsd_status ensure_capacity(hsd_collection* c, int64_t need) {
     CU(cudaMemcpy(nk, c->keys, (size_t)c->n * c->dim * key_bytes(c), cudaMemcpyDeviceToDevice));
     CU(cudaMemcpy(nt, c->tokens, (size_t)c->n * HSD_TOKENS_STRIDE, cudaMemcpyDeviceToDevice));
   }
+  if (c->shadow) {
+    uint16_t* ns = nullptr;
+    cudaError_t e2 = cudaMalloc(&ns, (size_t)ncap * c->dim * 2);
+    if (e2 != cudaSuccess) {
+      cudaFree(nk);
+      cudaFree(nt);
+      return cuda_fail(e2, "cudaMalloc(filter shadow)");
+    }
+    if (c->n > 0) CU(cudaMemcpy(ns, c->shadow, (size_t)c->n * c->dim * 2, cudaMemcpyDeviceToDevice));
+    cudaFree(c->shadow);
+    c->shadow = ns;
+  }
   cudaFree(c->keys);
   cudaFree(c->tokens);
   c->keys = nk;
   c->tokens = nt;
   c->cap = ncap;
+  return HSD_OK;
+}
+
+// bf16 filter copy of rows [row0, row0 + n) of an fp32 collection.
+hsd_status refresh_shadow(hsd_collection* c, int64_t row0, int64_t n) {
+  if (!c->shadow || n <= 0) return HSD_OK;
+  CU(hsd::launch_to_bf16((const float*)c->keys + (size_t)row0 * c->dim, n * c->dim,
+                         c->shadow + (size_t)row0 * c->dim, 0));
   return HSD_OK;
 }
 
@@ -160,6 +186,14 @@ hsd_status get_scratch(hsd_collection* c, cudaStream_t s, size_t partial_bytes, 
     sc.partial_cap = 0;
     CU(cudaMalloc(&sc.partial, partial_bytes));
     sc.partial_cap = partial_bytes;
+  }
+  const size_t sel_bytes = hsd::select_scratch_bytes(1024);
+  if (sc.sel_cap < sel_bytes) {
+    cudaFree(sc.sel);
+    sc.sel = nullptr;
+    sc.sel_cap = 0;
+    CU(cudaMalloc(&sc.sel, sel_bytes));
+    sc.sel_cap = sel_bytes;
   }
   if (sc.qsplit_cap < qsplit_bytes) {
     cudaFree(sc.qsplit);
@@ -194,8 +228,11 @@ int path_override() {
   }
   return v;
 }
-int choose_path(int B, int dtype) {
+constexpr int kShadowGamma = 0x100;  // sim_wide_gamma flag: bf16-rounded keys (filter shadow)
+
+int choose_path(int B, int dtype, bool shadow = false) {
   if (dtype == HSD_DTYPE_BF16) return kPathTc;  // the only bf16 similarity kernel
+  if (shadow && path_override() == kPathAuto) return kPathTc;  // the bf16 copy halves the scan for every B
   const int o = path_override();
   if (o == kPathRows) return B <= 8 ? kPathRows : kPathTile;
   if (o == kPathTile) return B <= 8 ? kPathRows : kPathTile;  // launch_sim picks rows for B <= 8
@@ -233,7 +270,7 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   // (the engine's kinematics); the persistent tcgen05 kernel sizes its grid to
   // the rest so neither waits for the other's CTAs to retire.
   const int nsm = std::max(1, num_sms(c->device) - std::max(0, reserve_sms));
-  const int path = choose_path(B, c->dtype);
+  const int path = choose_path(B, c->dtype, c->shadow != nullptr);
   const int W = pass_width(path);
   const int Bs0 = std::min(B, W);
   const int lists0 = path == kPathTc ? hsd::sim_wide_lists(Bs0, rows, nsm)
@@ -252,14 +289,20 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   for (int b0 = 0; b0 < B; b0 += W) {
     const int Bs = std::min(W, B - b0);
     // the SIMT paths pick rows vs tile per pass; the tcgen05 paths are fixed
-    const int p = is_tc(path) ? path : choose_path(Bs, c->dtype);
+    const int p = is_tc(path) ? path : choose_path(Bs, c->dtype, c->shadow != nullptr);
     hsd::SimPlan plan = hsd::sim_plan(Bs, rows, c->dim, nsm);
     const float* q = queries + (size_t)b0 * c->dim;
     if (p == kPathTc) {
       plan.lists = hsd::sim_wide_lists(Bs, rows, nsm);
-      plan.gamma = hsd::sim_wide_gamma(c->dim, c->dtype);
-      CU(hsd::launch_sim_wide(c->keys, c->dtype, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial,
-                              nullptr, s));
+      if (c->shadow) {  // bf16 filter copy of fp32 keys: both operands rounded
+        plan.gamma = hsd::sim_wide_gamma(c->dim, HSD_DTYPE_BF16 | kShadowGamma);
+        CU(hsd::launch_sim_wide(c->shadow, HSD_DTYPE_BF16, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit,
+                                sc->partial, nullptr, s));
+      } else {
+        plan.gamma = hsd::sim_wide_gamma(c->dim, c->dtype);
+        CU(hsd::launch_sim_wide(c->keys, c->dtype, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial,
+                                nullptr, s));
+      }
     } else if (p == kPathTc1) {
       plan.lists = hsd::sim_tc_lists(rows, nsm);
       plan.gamma = hsd::sim_tc1_gamma(c->dim);
@@ -275,7 +318,7 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
     }
     if (marks && marks->after_sim && b0 + W >= B) CU(cudaEventRecord(marks->after_sim, s));
     CU(hsd::launch_select(sc->partial, plan.lists, Bs, k, c->keys, c->dtype, c->dim, q, c->maxnorm, plan.gamma,
-                          scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->overflow, s));
+                          scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->overflow, sc->sel, s));
   }
   if (marks && marks->after_select) CU(cudaEventRecord(marks->after_select, s));
   return HSD_OK;
@@ -343,11 +386,13 @@ hsd_status hsd_collection_destroy(hsd_collection* c) {
   cudaSetDevice(c->device);
   for (auto& kv : c->scratch) {
     cudaFree(kv.second.partial);
+    cudaFree(kv.second.sel);
     cudaFree(kv.second.qsplit);
     cudaFree(kv.second.overflow);
   }
   cudaFree(c->keys);
   cudaFree(c->tokens);
+  cudaFree(c->shadow);
   cudaFree(c->maxnorm);
   delete c;
   return HSD_OK;
@@ -376,6 +421,34 @@ hsd_status hsd_collection_keys(const hsd_collection* c, const float** keys, cons
   if (keys && c->dtype != HSD_DTYPE_F32) return fail(HSD_ERR_INVALID_INPUT, "fp32 key view of a bf16 collection");
   if (keys) *keys = (const float*)c->keys;
   if (tokens) *tokens = c->tokens;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_set_filter(hsd_collection* c, int filter) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
+  if (filter != HSD_FILTER_NATIVE && filter != HSD_FILTER_BF16_COPY)
+    return fail(HSD_ERR_CONFIG, "unknown filter mode %d", filter);
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  if (filter == HSD_FILTER_NATIVE) {
+    CU(cudaDeviceSynchronize());
+    cudaFree(c->shadow);
+    c->shadow = nullptr;
+    return HSD_OK;
+  }
+  if (c->dtype != HSD_DTYPE_F32) return fail(HSD_ERR_CONFIG, "the bf16 filter copy applies to fp32 collections");
+  if (c->dim % 8) return fail(HSD_ERR_CONFIG, "the bf16 filter copy needs dim % 8 == 0");
+  if (c->shadow) return HSD_OK;
+  CU(cudaMalloc(&c->shadow, (size_t)c->cap * c->dim * 2));
+  st = refresh_shadow(c, 0, c->n);
+  if (st != HSD_OK) return st;
+  CU(cudaDeviceSynchronize());
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_get_filter(const hsd_collection* c, int* filter) {
+  if (!c || !filter) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *filter = c->shadow ? HSD_FILTER_BF16_COPY : HSD_FILTER_NATIVE;
   return HSD_OK;
 }
 
@@ -433,6 +506,8 @@ hsd_status hsd_collection_insert(hsd_collection* c, const float* emb, const doub
                   cudaMemcpyHostToDevice));
   }
   CU(hsd::launch_row_norms(c->keys, c->dtype, c->n, n, c->dim, c->maxnorm, 0));
+  st = refresh_shadow(c, c->n, n);
+  if (st != HSD_OK) return st;
   CU(cudaDeviceSynchronize());
   c->n += n;
   return HSD_OK;
@@ -463,6 +538,8 @@ hsd_status hsd_collection_generate_ex(hsd_collection* c, int kind, uint64_t db_s
   if (st != HSD_OK) return st;
   CU(hsd::launch_gen_keys(kind, db_seed, row0, n, c->dim, (uint8_t*)c->keys + (size_t)c->n * c->dim * key_bytes(c),
                           c->dtype, c->tokens + (size_t)c->n * HSD_TOKENS_STRIDE, c->maxnorm, payload, traj_T, 0));
+  st = refresh_shadow(c, c->n, n);
+  if (st != HSD_OK) return st;
   CU(cudaDeviceSynchronize());
   c->n += n;
   return HSD_OK;
@@ -492,11 +569,14 @@ hsd_status hsd_set_sim_path(int path) {
 hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
                                 void* stream) {
   if (!c || !queries || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
-  if (variant != 1 && variant != 2 && variant != 3)
-    return fail(HSD_ERR_INVALID_INPUT, "variant must be 1 (wide TF32/bf16), 2 (64-query TF32) or 3 (3xTF32)");
-  const int maxB = variant == 1 ? hsd::sim_wide_max_batch() : kSlab;
+  if (variant < 1 || variant > 4)
+    return fail(HSD_ERR_INVALID_INPUT,
+                "variant must be 1 (wide TF32/bf16), 2 (64-query TF32), 3 (3xTF32) or 4 (bf16 filter copy)");
+  if (variant == 4 && !c->shadow) return fail(HSD_ERR_INVALID_INPUT, "collection has no bf16 filter copy");
+  const int maxB = (variant == 1 || variant == 4) ? 256 : kSlab;
   if (B < 1 || B > maxB) return fail(HSD_ERR_INVALID_INPUT, "debug dump supports 1 <= B <= %d", maxB);
-  if (variant != 1 && c->dtype != HSD_DTYPE_F32) return fail(HSD_ERR_INVALID_INPUT, "variant needs fp32 keys");
+  if (variant != 1 && variant != 4 && c->dtype != HSD_DTYPE_F32)
+    return fail(HSD_ERR_INVALID_INPUT, "variant needs fp32 keys");
   hsd_status st = require_device(c->device);
   if (st != HSD_OK) return st;
   if (c->n == 0) return HSD_OK;
@@ -512,6 +592,9 @@ hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, 
   else if (variant == 2)
     CU(hsd::launch_sim_tc1((const float*)c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial,
                            out, (cudaStream_t)stream));
+  else if (variant == 4)
+    CU(hsd::launch_sim_wide(c->shadow, HSD_DTYPE_BF16, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit,
+                            sc->partial, out, (cudaStream_t)stream));
   else
     CU(hsd::launch_sim_wide(c->keys, c->dtype, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial, out,
                             (cudaStream_t)stream));

@@ -28,44 +28,45 @@ using dev::kEmpty;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kPool = 512;
-constexpr int kCandMax = 256;  // rescored candidates (one thread each)
-// Rescoring staging ring: 2 buffers of n rows x (W + 4) floats (16-B aligned
-// rows for cp.async, +4 floats spreads rows over banks), W = 512 for n <= 32,
-// 64 for n <= 256.
-constexpr int kRowsFloats = 2 * 256 * (64 + 4);  // >= 2 * 32 * (512 + 4)
-static_assert(kRowsFloats >= 2 * 32 * (512 + 4), "staging ring too small");
-constexpr int kMaxW = 512;
+constexpr int kCandMax = 256;   // rescored candidates per query
+constexpr int kPer = 8;         // candidates rescored per CTA of the rescoring kernel
+constexpr int kRThreads = 128;  // rescoring CTA: all threads stage rows, kPer run the fp64 chains
+constexpr int kW = 512;         // row chunk (elements) per staging buffer
 
 __device__ __forceinline__ double widen(float x) { return (double)x; }
 __device__ __forceinline__ double widen(uint16_t b) { return (double)hsd_bf16_val(b); }  // bf16 key -> exact fp64
 
-struct SelectSmem {
+// Per-query scratch between the three K2 kernels.
+struct SelScratch {
+  uint32_t id[kCandMax];
+  double exact[kCandMax];
+  int n;
+  int over;
+};
+
+struct CandSmem {
   uint64_t top[kWarps][32];
   uint64_t pool[kPool];
-  __align__(16) float rows[kRowsFloats];  // staging ring, reinterpreted as KT
-  __align__(16) double q[2][kMaxW];
-  double exact[kCandMax];
-  uint32_t id[kCandMax];
   double red[kWarps];
   int pool_n;
   int over;
 };
 
-template <typename KT>  // float (fp32 collection) or uint16_t (bf16 bits)
-__global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __restrict__ partial, int lists, int B, int k,
-                                                          const KT* __restrict__ keys, int dim,
-                                                          const float* __restrict__ queries,
-                                                          const unsigned long long* __restrict__ maxnorm_bits,
-                                                          double gamma, double* __restrict__ scores,
-                                                          int32_t* __restrict__ ids, int* __restrict__ overflow) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  SelectSmem& S = *reinterpret_cast<SelectSmem*>(smem_raw);
+// K2a, one CTA per query: approximate global top-32 of the per-CTA lists ->
+// A_k; every record whose exact score can reach the exact k-th has approx >=
+// A_k - 2E (E = gamma * max|key| * |q|): collect them (best kCandMax by
+// approximate score), flag an overflow if a per-CTA list ran out above the
+// margin.
+__global__ void __launch_bounds__(kThreads) select_cand_kernel(const uint64_t* __restrict__ partial, int lists, int B,
+                                                               int k, int dim, const float* __restrict__ queries,
+                                                               const unsigned long long* __restrict__ maxnorm_bits,
+                                                               double gamma, SelScratch* __restrict__ scr) {
+  __shared__ CandSmem S;
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* qrow = queries + (size_t)b * dim;
 
-  // 1. approximate global top-32 (4 list loads in flight per warp)
-  uint64_t top = kEmpty;
+  uint64_t top = kEmpty;  // 4 list loads in flight per warp
   for (int l0 = warp; l0 < lists; l0 += 4 * kWarps) {
     uint64_t x[4];
 #pragma unroll
@@ -100,7 +101,6 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
   const double E = gamma * maxnorm * sqrt(qn2) * 1.000001 + 1e-300;
   const double T = (kth == kEmpty) ? -INFINITY : (double)cand_score(kth) - 2.0 * E;
 
-  // 2. margin candidates
   for (int l = tid; l < lists; l += kThreads) {
     const uint64_t* lst = partial + ((size_t)l * B + b) * kCandLocal;
     int j = 0;
@@ -131,37 +131,50 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
     if (tid == 0) S.over = 1;
   }
   __syncthreads();
-  if (tid < n) S.id[tid] = cand_id(S.pool[tid]);
-  __syncthreads();
+  SelScratch& o = scr[b];
+  if (tid < n) o.id[tid] = cand_id(S.pool[tid]);
+  if (tid == 0) {
+    o.n = n;
+    o.over = S.over;
+  }
+}
 
-  // 3. exact rescoring in the reference's order.  Candidate rows stream
-  //    through a double-buffered cp.async ring of wide column chunks (the
-  //    next chunk lands while this one is consumed); each thread then runs
-  //    the sequential fp64 chain of its candidate out of shared memory.
-  // widest chunk (in elements) whose double buffer fits; rows are padded by
-  // 16 B (spreads them over banks, keeps cp.async destinations aligned)
+// K2b, one CTA per (query, kPer candidates): exact rescoring in the
+// reference's order (store.cpp:32).  Rows stream through a double-buffered
+// cp.async ring of kW-element chunks (all 128 threads copy); kPer threads run
+// the sequential fp64 chain acc = fma(q_i, k_i, acc), i = 0..dim-1 — the fp32
+// (or bf16) x fp32 product is exact in fp64, so the fused form is
+// bit-identical to s += a[i]*b[i].
+template <typename KT>
+__global__ void __launch_bounds__(kRThreads) rescore_kernel(const KT* __restrict__ keys, int dim,
+                                                            const float* __restrict__ queries,
+                                                            SelScratch* __restrict__ scr) {
   constexpr int kPad = 16 / (int)sizeof(KT);
-  constexpr int kRingElems = kRowsFloats * 4 / (int)sizeof(KT);
-  const int W = 2 * n * (kMaxW + kPad) <= kRingElems ? kMaxW
-                : 2 * n * (256 + kPad) <= kRingElems ? 256
-                : 2 * n * (128 + kPad) <= kRingElems ? 128
-                                                     : 64;
-  const int stride = W + kPad;
-  const int nchunk = (dim + W - 1) / W;
-  const int v16 = W / kPad;  // 16-B copies per row chunk
-  KT* ring = reinterpret_cast<KT*>(S.rows);
+  constexpr int kStride = kW + kPad;
+  __shared__ __align__(16) KT rows[2][kPer][kStride];
+  __shared__ double qs[2][kW];
+  __shared__ uint32_t ids[kPer];
+  const int b = blockIdx.x, c0 = blockIdx.y * kPer;
+  SelScratch& o = scr[b];
+  const int n = min(o.n - c0, kPer);
+  if (n <= 0) return;
+  const int tid = threadIdx.x;
+  if (tid < n) ids[tid] = o.id[c0 + tid];
+  __syncthreads();
+  const float* qrow = queries + (size_t)b * dim;
+  const int nchunk = (dim + kW - 1) / kW;
+  constexpr int v16 = kW / kPad;  // 16-B copies per row chunk
   auto issue = [&](int ch) {
-    KT* dst = ring + (ch & 1) * n * stride;
-    const int c0 = ch * W;
-    for (int i = tid; i < n * v16; i += kThreads) {
+    const int cbase = ch * kW;
+    for (int i = tid; i < n * v16; i += kRThreads) {
       const int c = i / v16, j16 = i - c * v16;
-      const int col = c0 + j16 * kPad;
-      const KT* src = keys + (size_t)S.id[c] * dim + col;
-      const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + c * stride + j16 * kPad);
+      const int col = cbase + j16 * kPad;
+      const KT* src = keys + (size_t)ids[c] * dim + col;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&rows[ch & 1][c][j16 * kPad]);
       const int bytes = col < dim ? 16 : 0;  // dim is a multiple of kPad; zero-fill past the end
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
     }
-    for (int j = tid; j < W; j += kThreads) S.q[ch & 1][j] = c0 + j < dim ? (double)qrow[c0 + j] : 0.0;
+    for (int j = tid; j < kW; j += kRThreads) qs[ch & 1][j] = cbase + j < dim ? (double)qrow[cbase + j] : 0.0;
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   double acc = 0.0;
@@ -174,29 +187,40 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    const int w = dim - ch * W < W ? dim - ch * W : W;
+    const int w = dim - ch * kW < kW ? dim - ch * kW : kW;
     if (tid < n) {
-      // acc = fl(acc + fl(q*k)) of store.cpp:32; the fp32 x fp32 (or fp32 x
-      // bf16) product is exact in fp64, so the fused form fl(acc + q*k) is
-      // bit-identical and leaves one dependent op per element on the chain.
-      const KT* r = ring + (ch & 1) * n * stride + tid * stride;
-      const double* qc = S.q[ch & 1];
+      const KT* r = rows[ch & 1][tid];
+      const double* qc = qs[ch & 1];
 #pragma unroll 16
       for (int j = 0; j < w; ++j) acc = __fma_rn(qc[j], widen(r[j]), acc);
     }
     __syncthreads();
   }
-  if (tid < n) S.exact[tid] = acc;
-  __syncthreads();
+  if (tid < n) o.exact[c0 + tid] = acc;
+}
 
-  // 4. rank by (score desc, id asc) and emit the first k
+// K2c, one CTA per query: rank by (score desc, id asc) and emit the first k
+// (store.cpp:67-71).
+__global__ void __launch_bounds__(kThreads) rank_kernel(const SelScratch* __restrict__ scr, int k,
+                                                        double* __restrict__ scores, int32_t* __restrict__ ids,
+                                                        int* __restrict__ overflow) {
+  __shared__ double ex[kCandMax];
+  __shared__ uint32_t id[kCandMax];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const SelScratch& o = scr[b];
+  const int n = o.n;
   if (tid < n) {
-    const double s = S.exact[tid];
-    const uint32_t me = S.id[tid];
+    ex[tid] = o.exact[tid];
+    id[tid] = o.id[tid];
+  }
+  __syncthreads();
+  if (tid < n) {
+    const double s = ex[tid];
+    const uint32_t me = id[tid];
     int rank = 0;
     for (int c = 0; c < n; ++c) {
-      const double o = S.exact[c];
-      rank += (o > s) || (o == s && S.id[c] < me);
+      const double x = ex[c];
+      rank += (x > s) || (x == s && id[c] < me);
     }
     if (rank < k) {
       scores[(size_t)b * k + rank] = s;
@@ -207,7 +231,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const uint64_t* __rest
     scores[(size_t)b * k + r] = -INFINITY;
     ids[(size_t)b * k + r] = -1;
   }
-  if (tid == 0 && S.over) atomicAdd(overflow, 1);
+  if (tid == 0 && o.over) atomicAdd(overflow, 1);
 }
 
 // K3: G sorted lists [G][B][k] -> global [B][k].
@@ -255,23 +279,25 @@ __global__ void merge_ranks_kernel(const double* __restrict__ gs, const int32_t*
 
 }  // namespace
 
+size_t select_scratch_bytes(int B) { return (size_t)B * sizeof(SelScratch); }
+
 cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const void* keys, int key_dtype, int dim,
                           const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
-                          int32_t* ids, int* overflow, cudaStream_t s) {
+                          int32_t* ids, int* overflow, void* scratch, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
-  const size_t smem = sizeof(SelectSmem);
-  if (key_dtype == HSD_DTYPE_BF16) {
-    if (dim % 8) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(select_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    select_kernel<uint16_t><<<B, kThreads, smem, s>>>(partial, lists, B, k, (const uint16_t*)keys, dim, queries,
-                                                      maxnorm_bits, gamma, scores, ids, overflow);
-  } else {
-    cudaError_t e = cudaFuncSetAttribute(select_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    select_kernel<float><<<B, kThreads, smem, s>>>(partial, lists, B, k, (const float*)keys, dim, queries,
-                                                   maxnorm_bits, gamma, scores, ids, overflow);
-  }
+  if (key_dtype == HSD_DTYPE_BF16 && dim % 8) return cudaErrorInvalidValue;
+  SelScratch* scr = reinterpret_cast<SelScratch*>(scratch);
+  select_cand_kernel<<<B, kThreads, 0, s>>>(partial, lists, B, k, dim, queries, maxnorm_bits, gamma, scr);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const dim3 grid(B, kCandMax / kPer);
+  if (key_dtype == HSD_DTYPE_BF16)
+    rescore_kernel<uint16_t><<<grid, kRThreads, 0, s>>>((const uint16_t*)keys, dim, queries, scr);
+  else
+    rescore_kernel<float><<<grid, kRThreads, 0, s>>>((const float*)keys, dim, queries, scr);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  rank_kernel<<<B, kThreads, 0, s>>>(scr, k, scores, ids, overflow);
   return cudaGetLastError();
 }
 

@@ -458,6 +458,11 @@ double sim_wide_gamma(int dim, int key_dtype) {
   // Accumulation: fp32 tensor-core accumulator (not round-to-nearest) over dim
   // products, <= (dim + 16) 2^-23 relative to sum|k_i q_i| (as for TF32).
   const double acc = (dim + 16.0) / 8388608.0;
+  if (key_dtype & 0x100) {
+    // bf16 filter copy of fp32 keys: both operands rounded (RN, 2^-9 each):
+    // |kq - k'q'| <= (2^-9 + 2^-9 + 2^-18) |k||q| per product.
+    return (1.0 / 256.0 + 1.0 / 262144.0) * 1.0001 + acc;
+  }
   if (key_dtype == HSD_DTYPE_BF16) {
     // bf16 keys are exact; queries rounded to bf16 (RN): |q - bf16(q)| <= 2^-9 |q|;
     // bf16 x bf16 products are exact in fp32.

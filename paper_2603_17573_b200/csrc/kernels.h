@@ -69,9 +69,12 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
                             float* dump, cudaStream_t s);
 
 // ---- K2 select: margin candidates + exact fp64 rescoring + final top-k -------
+// Three launches (candidates, rescoring over (query, 8-candidate) CTAs, rank);
+// scratch: select_scratch_bytes(B).
+size_t select_scratch_bytes(int B);
 cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const void* keys, int key_dtype, int dim,
                           const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
-                          int32_t* ids, int* overflow, cudaStream_t s);
+                          int32_t* ids, int* overflow, void* scratch, cudaStream_t s);
 
 // K3 merge of G gathered per-rank top-k records (sharded search); tokens
 // [G][B][k][32] are permuted alongside when non-null.

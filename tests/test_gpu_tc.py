@@ -174,3 +174,60 @@ def test_bf16_config_errors(torch):
         H.Collection(36, capacity=4, dtype="bf16")  # dim % 8
     with pytest.raises(H.ConfigError):
         H.Collection(64, capacity=4, dtype="fp8")
+
+
+# ----------------------------------------------------------------------------- bf16 filter copy of fp32 keys
+GAMMA_COPY = lambda dim: (1.0 / 256 + 1.0 / 262144) * 1.0001 + (dim + 16.0) / 2**23  # noqa: E731
+
+
+@pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
+@pytest.mark.parametrize("dim,n,B", [(64, 2000, 256), (4096, 1200, 100), (4352, 600, 7)])
+def test_filter_copy_scores_within_bound(torch, kind, dim, n, B):
+    col = H.Collection(dim, capacity=n)
+    col.generate(kind, 5, n)
+    col.set_filter("bf16_copy")
+    q = H.gen_queries(kind, 6, 5, n, 0, B, dim)
+    approx = col.debug_sim_scores(q, variant=4).cpu().numpy().astype(np.float64)
+    keys = O.gen_keys(kind, 5, 0, n, dim).astype(np.float64)
+    qq = q.cpu().numpy().astype(np.float64)
+    err = np.abs(approx - qq @ keys.T)
+    bound = GAMMA_COPY(dim) * (np.abs(qq) @ np.abs(keys).T)
+    assert np.all(err <= bound), float((err / np.maximum(bound, 1e-300)).max())
+
+
+@pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
+def test_filter_copy_results_bit_identical(torch, kind):
+    """With the bf16 filter copy the ids and fp64 scores are still the reference's over the fp32 keys."""
+    for dim, n in ((64, 5000), (4096, 1500)):
+        col = H.Collection(dim, capacity=n // 2)
+        col.generate(kind, 41, n // 2)
+        col.set_filter("bf16_copy")
+        assert col.filter() == "bf16_copy"
+        col.generate(kind, 41, n - n // 2)  # appended rows refresh the copy (and grow it)
+        for B, k in ((1, 8), (4, 3), (5, 8), (64, 8), (300, 8), (1024, 32)):
+            q = H.gen_queries(kind, 42, 41, n, 2, B, dim)
+            sc, ids = col.search_topk_exact(q, k)
+            osc, oid = O.search_synth(kind, 41, n, q.cpu().numpy(), k)
+            np.testing.assert_array_equal(ids.cpu().numpy(), oid, err_msg=f"dim={dim} B={B}")
+            np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+        assert col.overflow_count() == 0
+        col.set_filter("native")
+        assert col.filter() == "native"
+
+
+def test_filter_copy_insert_and_range(torch):
+    rng = np.random.default_rng(9)
+    n, dim = 900, 128
+    emb = rng.standard_normal((n, dim)).astype(np.float32)
+    col = H.Collection(dim, capacity=8)
+    col.set_filter("bf16_copy")
+    col.insert(emb[:300], rng.uniform(-1, 1, (300, 3, 7)))
+    col.insert(emb[300:], rng.uniform(-1, 1, (n - 300, 3, 7)))
+    q = torch.as_tensor(rng.standard_normal((50, dim)).astype(np.float32), device="cuda")
+    for rg in ((0, n), (10, 777)):
+        sc, ids = col.search_topk_exact(q, 5, row_range=rg)
+        osc, oid = O.search_topk(emb[rg[0]:rg[1]], q.cpu().numpy(), 5)
+        np.testing.assert_array_equal(ids.cpu().numpy(), oid + rg[0])
+        np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+    with pytest.raises(H.ConfigError):
+        H.Collection(64, capacity=4, dtype="bf16").set_filter("bf16_copy")
