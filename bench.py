@@ -74,8 +74,9 @@ def parse():
     p.add_argument("--traj-T", type=int, default=500, help="C5 demonstration length (actions) per DB episode")
     p.add_argument("--k-top", type=int, default=3, help="C5 K_top (SPEC default 3)")
     p.add_argument("--dtype", default=None, choices=["f32", "bf16"], help="key storage (default per config)")
-    p.add_argument("--filter", default="native", choices=["native", "bf16_copy"],
-                   help="fp32 collections: tensor-core filter over the fp32 keys (TF32) or over a resident bf16 copy")
+    p.add_argument("--filter", default="bf16_copy", choices=["native", "bf16_copy"],
+                   help="fp32 collections: tensor-core filter over a resident bf16 copy of the keys (default; falls "
+                        "back to native when HBM cannot hold it) or over the fp32 keys themselves (TF32)")
     p.add_argument("--episodes", type=int, default=4096, help="C3 episodes per round")
     a = p.parse_args()
     given = {x.split("=")[0] for x in sys.argv[1:] if x.startswith("--")}
@@ -122,18 +123,53 @@ def load_traffic(kernel_tag):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled DURING the timed
+    region: NVML polled every ~1 ms from a thread (short regions still get
+    samples); nvidia-smi -lms 20 as the fallback when NVML is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device_index: int):
         self.dev = device_index
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, set(reasons))
+        self.nvml = None
+        self.stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.dev)
+            bits = {"hw_slowdown": N.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksEventReasonSwPowerCap}
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((float(sm), float(mx), {k for k, b in bits.items() if r & b}))
+                    except Exception:
+                        pass
+                    time.sleep(0.001)
+
+            self.nvml = N
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            while not self.samples:  # the first sample is in before the timed region starts
+                time.sleep(0.0005)
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "20"], stdout=subprocess.PIPE,
@@ -149,6 +185,13 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
+            try:
+                self.nvml.nvmlShutdown()
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -158,7 +201,10 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s_mhz, m_mhz, rs in self.samples:
+            sm.append(s_mhz)
+            mx = max(mx, m_mhz)
+            reasons |= rs
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 8:
@@ -168,12 +214,13 @@ class ClockSampler:
                 mx = max(mx, float(parts[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[4:8]):
+            for nm, v in zip(self.NAMES, parts[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 # ------------------------------------------------------------------------------ CPU reference arm
@@ -294,8 +341,10 @@ def config_of(args, world):
                      f"k={args.k}, draft len {args.L}, 7x256 verifier logits, {args.d_f}-d skip features, "
                      f"15-pt windows"),
         "key_dtype": args.dtype,
-        "filter": ("bf16 copy of the fp32 keys (+50% HBM); exact fp64 rescoring from the fp32 keys"
-                   if args.filter == "bf16_copy" and args.dtype == "f32" else "native"),
+        "filter": ("bf16 copy of the fp32 keys (+50% HBM) streamed by the tensor-core filter; exact fp64 rescoring "
+                   "from the fp32 keys (results bit-identical to the fp32 reference)"
+                   if args.filter == "bf16_copy" and args.dtype == "f32"
+                   else getattr(args, "filter_note", "native (filter reads the stored keys)")),
         "n_rows": args.n, "dim": args.dim, "batch": args.batch, "k": args.k, "draft_len": args.L, "d_f": args.d_f,
         "synthetic_family": "REAL" if args.kind == 1 else "EXACT",
         "parallelism": f"db-shard{world}" if world > 1 else "single",
@@ -323,7 +372,11 @@ def run_ours(args):
     col = H.Collection(dim, capacity=b1 - b0, device=local, dtype=args.dtype)
     col.generate(args.kind, 2026, b1 - b0, row0=b0)
     if args.filter == "bf16_copy" and args.dtype == "f32":
-        col.set_filter("bf16_copy")
+        try:
+            col.set_filter("bf16_copy")
+        except H.OutOfMemoryError:  # e.g. C4's 164 GB of fp32 keys on one GPU: no room for the copy
+            args.filter = "native"
+            args.filter_note = "bf16 copy does not fit next to the fp32 keys on this GPU; native TF32 filter"
     stream = torch.cuda.current_stream()
 
     # inputs resident in HBM: S distinct batches cycled through the steps
@@ -416,7 +469,7 @@ def run_ours(args):
         peak, peak_kind = load_peaks()
         achieved = alg_bytes / (sim_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic("similarity" if args.config == "c2" else f"similarity_{args.config}"),
+                "traffic": load_traffic(traffic_key(args)),
                 "kernel": f"similarity (K1, {'kind::tf32' if esz == 4 else 'kind::f16'} filter"
                           f"{' over the bf16 key copy' if args.filter == 'bf16_copy' else ''})",
                 "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": sim_ms, "peak_source": peak_kind,
@@ -516,6 +569,13 @@ def run_e2e(H, torch, eng, args, qs, lg, feats, xyz_np, vp, stream):
     return {"value": B * n / dt, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "api": "hsd_step_host_async + hsd_engine_sync (C ABI), pinned host buffers, wall clock",
             "passes": n, "sync_api_value": B * n / dt_sync}
+
+
+def traffic_key(args):
+    """profiles/traffic.json entry of this run's dominant kernel (ncu dram bytes per launch)."""
+    if args.config == "c2":
+        return "similarity" if args.filter == "bf16_copy" else "similarity_native"
+    return f"similarity_{args.config}"
 
 
 def load_peak_key(key):
