@@ -231,3 +231,34 @@ def test_filter_copy_insert_and_range(torch):
         np.testing.assert_array_equal(sc.cpu().numpy(), osc)
     with pytest.raises(H.ConfigError):
         H.Collection(64, capacity=4, dtype="bf16").set_filter("bf16_copy")
+
+
+@pytest.mark.parametrize("dtype,filt", [("f32", "native"), ("f32", "bf16_copy"), ("bf16", "native")])
+def test_edge_shapes_all_kernels(torch, dtype, filt):
+    """Dims that are not a multiple of the 128-B k-chunk (TMA zero fill), tiny
+    and partial key blocks, k > n, sub-ranges, and every pass width (one
+    CTA, 2-4 query groups per cluster, several passes)."""
+    rng = np.random.default_rng(77)
+    for dim in (8, 40, 72, 136):
+        if dtype == "bf16" and dim % 8:
+            continue
+        for n in (1, 5, 127, 129, 700):
+            emb = rng.standard_normal((n, dim)).astype(np.float32)
+            col = H.Collection(dim, capacity=n, dtype=dtype)
+            col.insert(emb, rng.uniform(-1, 1, (n, 3, 7)))
+            if filt == "bf16_copy":
+                col.set_filter("bf16_copy")
+            stored = emb if dtype == "f32" else torch.as_tensor(emb).bfloat16().float().numpy()
+            for B in (1, 3, 70, 300, 1030):
+                q = torch.as_tensor(rng.standard_normal((B, dim)).astype(np.float32), device="cuda")
+                for k, rg in ((1, (0, n)), (9, (0, n)), (4, (n // 3, n))):
+                    if rg[0] >= rg[1]:
+                        continue
+                    sc, ids = col.search_topk_exact(q, k, row_range=rg)
+                    osc, oid = O.search_topk(stored[rg[0]:rg[1]], q.cpu().numpy(), k)
+                    kk = oid.shape[1]
+                    np.testing.assert_array_equal(ids.cpu().numpy()[:, :kk], oid + rg[0],
+                                                  err_msg=f"dim={dim} n={n} B={B} k={k} rg={rg}")
+                    np.testing.assert_array_equal(sc.cpu().numpy()[:, :kk], osc)
+                    assert np.all(ids.cpu().numpy()[:, kk:] == -1)
+            assert col.overflow_count() == 0
