@@ -28,6 +28,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxL = 21;
 constexpr int kTokStride = 24;  // bytes per candidate row in shared memory
+constexpr int kPairs = 256;     // (parameter set, candidate) pairs per warp per chunk
 constexpr int kFeatUnroll = 4;  // feature float4 pairs loaded per lane before accumulation
 
 __device__ __forceinline__ int group_count(int L) { return (L / 7) * 3; }
@@ -62,7 +63,8 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
                                                           uint8_t* __restrict__ tok_out) {
   __shared__ uint8_t s_tok[kWarps][HSD_K_MAX][kTokStride];
   __shared__ int s_greedy[kWarps][32];
-  __shared__ int s_acc0[kWarps][HSD_K_MAX], s_rest[kWarps][HSD_K_MAX];
+  __shared__ uint8_t s_pair[kWarps][kPairs];  // per (set, candidate): rest | pos0-accepted << 7
+  __shared__ int8_t s_len[kWarps][kPairs], s_bb[kWarps][kPairs];
   __shared__ int s_canA[kWarps][HSD_K_MAX], s_canB[kWarps][HSD_K_MAX];
   __shared__ int s_rankA[kWarps][HSD_K_MAX], s_rankB[kWarps][HSD_K_MAX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -165,9 +167,7 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
     }
   }
   __syncwarp();
-  int greedy[kMaxL];
-#pragma unroll
-  for (int p = 0; p < kMaxL; ++p) greedy[p] = p < L ? s_greedy[warp][p] : 0;
+  const int* greedy = s_greedy[warp];  // positions < L (shared memory, no per-thread copy)
   const int hist = history ? history[e] : 0x7fffffff;
 
   // ---- candidate dedup (chain language) — independent of params
@@ -201,108 +201,124 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
   }
   __syncwarp();
 
+  // ---- per parameter set (a tolerance / threshold sweep): lane-parallel over
+  //      (set, candidate) pairs, processed in chunks of kPairs pairs.
+  //      A: group acceptance of every candidate (pos0 accepted?, length of the
+  //         accepted run of later groups);
+  //      B: for every canonical pos0 candidate a, the best later-group source b
+  //         among the enumerated chains (DFS order: rank_a * nB + rank_b < cap);
+  //      C: one lane per set: longest chain, earliest on ties -> outcome.
   const int G = group_count(L);
-  for (int pi = 0; pi < P; ++pi) {
-    const hsd_verify_params p = params[pi];
-    hsd_outcome o;
-    o.accept_len = 0;
-    o.win_a = -1;
-    o.win_b = -1;
-    o.calls = 0;
-    o.fallback = 0;
-    o.skipped = 0;
-    o.n_emit = 0;
-    o.greedy0 = (int16_t)greedy[0];
-    o.cos_sim = (float)cosv;
-    uint8_t* my_tok = tok_out + ((size_t)pi * E + e) * L;
-    const bool skip = p.skip_enabled && n_cand > 0 && gap_d >= 1 && hist >= gap_d && gap_d <= p.O_dist &&
-                      cosv >= p.min_S;
-    if (skip) {  // the retrieved draft is emitted as fully accepted
-      o.accept_len = L;
-      o.win_a = 0;
-      o.win_b = 0;
-      o.skipped = 1;
-      o.n_emit = (int16_t)L;
-      for (int t = lane; t < L; t += 32) my_tok[t] = s_tok[warp][0][t];
-    } else if (n_cand == 0) {  // empty shard: autoregressive step
-      o.fallback = 1;
-      o.calls = 1;
-      o.n_emit = 1;
-      if (lane == 0) my_tok[0] = (uint8_t)greedy[0];
-      for (int t = 1 + lane; t < L; t += 32) my_tok[t] = 0;
-    } else {
-      // per-candidate group acceptance
-      if (lane < n_cand) {
-        const uint8_t* me = s_tok[warp][lane];
-        int st, ln;
-        bool gr;
-        group_at(0, st, ln, gr);
-        s_acc0[warp][lane] = accept_group(me, greedy, st, ln, gr, p) ? 1 : 0;
-        int rest = 0;
-        for (int g = 1; g < G; ++g) {
-          group_at(g, st, ln, gr);
-          if (!accept_group(me, greedy, st, ln, gr, p)) break;
-          rest += ln;
-        }
-        s_rest[warp][lane] = rest;
+  const int hist_ok = gap_d >= 1 && hist >= gap_d;
+  const int nc = n_cand > 0 ? n_cand : 1;
+  const int chunk = kPairs / nc;  // sets per chunk (>= 1: n_cand <= 32)
+  for (int p0 = 0; p0 < P; p0 += chunk) {
+    const int pc = min(chunk, P - p0);
+    const int npairs = pc * n_cand;
+    for (int idx = lane; idx < npairs; idx += 32) {  // A
+      const int pi = p0 + idx / n_cand, c = idx % n_cand;
+      const hsd_verify_params& pp = params[pi];
+      const uint8_t* me = s_tok[warp][c];
+      int st, ln;
+      bool gr;
+      group_at(0, st, ln, gr);
+      const int a0 = accept_group(me, greedy, st, ln, gr, pp) ? 1 : 0;
+      int rest = 0;
+      for (int g = 1; g < G; ++g) {
+        group_at(g, st, ln, gr);
+        if (!accept_group(me, greedy, st, ln, gr, pp)) break;
+        rest += ln;
       }
-      __syncwarp();
-      const int cap = p.chain_cap > 0 ? p.chain_cap : 64;
-      // lane a (canonical pos0) finds its best enumerated b
-      int len = -1, bestB = -1, rA = 1 << 20;
-      if (lane < n_cand && s_rankA[warp][lane] >= 0) {
-        rA = s_rankA[warp][lane];
+      s_pair[warp][idx] = (uint8_t)(rest | (a0 << 7));
+    }
+    __syncwarp();
+    for (int idx = lane; idx < npairs; idx += 32) {  // B
+      const int pi = p0 + idx / n_cand, a = idx % n_cand, base = idx - a;
+      const int rA = s_rankA[warp][a];
+      int len = -1, bb = -1;
+      if (rA >= 0) {
+        const int cap = params[pi].chain_cap > 0 ? params[pi].chain_cap : 64;
         const int limit = cap - rA * nB;  // b's with rankB < limit are enumerated
         if (limit > 0) {
-          int br = -1, bb = -1;
+          int br = -1;
           for (int b = 0; b < n_cand; ++b) {
             const int rb = s_rankB[warp][b];
             if (rb < 0 || rb >= limit) continue;
-            const int r = s_rest[warp][b];
+            const int r = s_pair[warp][base + b] & 0x7F;
             if (r > br) {
               br = r;
               bb = b;
             }
           }
-          bestB = bb;
-          len = s_acc0[warp][lane] ? 3 + br : 0;
+          len = (s_pair[warp][idx] >> 7) ? 3 + br : 0;
         }
       }
-      // warp arg-max: longest, then earliest chain (smallest rank of a)
-      int wl = len, wa = lane, wr = rA, wb = bestB;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const int ol = __shfl_xor_sync(0xffffffffu, wl, off);
-        const int oa = __shfl_xor_sync(0xffffffffu, wa, off);
-        const int orr = __shfl_xor_sync(0xffffffffu, wr, off);
-        const int ob = __shfl_xor_sync(0xffffffffu, wb, off);
-        if (ol > wl || (ol == wl && orr < wr)) {
-          wl = ol;
-          wa = oa;
-          wr = orr;
-          wb = ob;
-        }
-      }
-      const long long chains = (long long)nA * nB;
-      o.calls = (int16_t)(chains < cap ? chains : cap);
-      if (wl <= 0) {  // every chain rejected at pos0 -> first chain, fallback token
+      s_len[warp][idx] = (int8_t)len;
+      s_bb[warp][idx] = (int8_t)bb;
+    }
+    __syncwarp();
+    for (int q = lane; q < pc; q += 32) {  // C
+      const int pi = p0 + q;
+      const hsd_verify_params& pp = params[pi];
+      hsd_outcome o;
+      o.accept_len = 0;
+      o.win_a = -1;
+      o.win_b = -1;
+      o.calls = 0;
+      o.fallback = 0;
+      o.skipped = 0;
+      o.n_emit = 0;
+      o.greedy0 = (int16_t)greedy[0];
+      o.cos_sim = (float)cosv;
+      uint8_t* my_tok = tok_out + ((size_t)pi * E + e) * L;
+      const bool skip = pp.skip_enabled && n_cand > 0 && hist_ok && gap_d <= pp.O_dist && cosv >= pp.min_S;
+      if (skip) {  // the retrieved draft is emitted as fully accepted
+        o.accept_len = L;
         o.win_a = 0;
         o.win_b = 0;
+        o.skipped = 1;
+        o.n_emit = (int16_t)L;
+        for (int t = 0; t < L; ++t) my_tok[t] = s_tok[warp][0][t];
+      } else if (n_cand == 0) {  // empty shard: autoregressive step
         o.fallback = 1;
+        o.calls = 1;
         o.n_emit = 1;
-        if (lane == 0) my_tok[0] = (uint8_t)greedy[0];
-        for (int t = 1 + lane; t < L; t += 32) my_tok[t] = 0;
+        my_tok[0] = (uint8_t)greedy[0];
+        for (int t = 1; t < L; ++t) my_tok[t] = 0;
       } else {
-        o.win_a = (int16_t)wa;
-        o.win_b = (int16_t)wb;
-        o.accept_len = wl;
-        o.n_emit = (int16_t)wl;
-        for (int t = lane; t < L; t += 32)
-          my_tok[t] = t < wl ? (t < 3 ? s_tok[warp][wa][t] : s_tok[warp][wb][t]) : (uint8_t)0;
+        const int cap = pp.chain_cap > 0 ? pp.chain_cap : 64;
+        int wl = -1, wa = 0, wr = 1 << 20, wb = -1;  // longest, then the earliest chain (smallest rank of a)
+        for (int a = 0; a < n_cand; ++a) {
+          const int l = s_len[warp][q * n_cand + a];
+          const int ra = s_rankA[warp][a] >= 0 ? s_rankA[warp][a] : (1 << 20);
+          if (l > wl || (l == wl && ra < wr)) {
+            wl = l;
+            wa = a;
+            wr = ra;
+            wb = s_bb[warp][q * n_cand + a];
+          }
+        }
+        const long long chains = (long long)nA * nB;
+        o.calls = (int16_t)(chains < cap ? chains : cap);
+        if (wl <= 0) {  // every chain rejected at pos0 -> first chain, fallback token
+          o.win_a = 0;
+          o.win_b = 0;
+          o.fallback = 1;
+          o.n_emit = 1;
+          my_tok[0] = (uint8_t)greedy[0];
+          for (int t = 1; t < L; ++t) my_tok[t] = 0;
+        } else {
+          o.win_a = (int16_t)wa;
+          o.win_b = (int16_t)wb;
+          o.accept_len = wl;
+          o.n_emit = (int16_t)wl;
+          for (int t = 0; t < L; ++t)
+            my_tok[t] = t < wl ? (t < 3 ? s_tok[warp][wa][t] : s_tok[warp][wb][t]) : (uint8_t)0;
+        }
       }
-      __syncwarp();
+      out[(size_t)pi * E + e] = o;
     }
-    if (lane == 0) out[(size_t)pi * E + e] = o;
+    __syncwarp();
   }
 }
 
