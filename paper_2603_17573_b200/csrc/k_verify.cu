@@ -51,36 +51,40 @@ __device__ __forceinline__ bool accept_group(const uint8_t* draft, const int* gr
   return sum <= p.bias_seq_max && mx <= p.bias_token_max;
 }
 
-__global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __restrict__ ids, int E, int k, int L,
-                                                          const uint8_t* __restrict__ tokens,
-                                                          const uint8_t* __restrict__ cand_tokens,
-                                                          const float* __restrict__ logits,
-                                                          const float* __restrict__ feat_now,
-                                                          const float* __restrict__ feat_prev, int d_f,
-                                                          const int32_t* __restrict__ history, int gap_d,
-                                                          const hsd_verify_params* __restrict__ params, int P,
-                                                          int need_cos, hsd_outcome* __restrict__ out,
-                                                          uint8_t* __restrict__ tok_out) {
-  __shared__ uint8_t s_tok[kWarps][HSD_K_MAX][kTokStride];
-  __shared__ int s_greedy[kWarps][32];
-  __shared__ uint8_t s_pair[kWarps][kPairs];  // per (set, candidate): rest | pos0-accepted << 7
-  __shared__ int8_t s_len[kWarps][kPairs], s_bb[kWarps][kPairs];
-  __shared__ int s_canA[kWarps][HSD_K_MAX], s_canB[kWarps][HSD_K_MAX];
-  __shared__ int s_rankA[kWarps][HSD_K_MAX], s_rankB[kWarps][HSD_K_MAX];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int e = blockIdx.x * kWarps + warp;
-  if (e >= E) return;
+// Per-warp shared scratch of one episode.
+struct WarpScratch {
+  uint8_t tok[HSD_K_MAX][kTokStride];
+  int greedy[32];
+  uint8_t pair[kPairs];  // per (set, candidate): rest | pos0-accepted << 7
+  int8_t len[kPairs], bb[kPairs];
+  int canA[HSD_K_MAX], canB[HSD_K_MAX];
+  int rankA[HSD_K_MAX], rankB[HSD_K_MAX];
+};
 
+// One episode's decode round on one warp.  lgE: its logits [L][256]; fnE /
+// fpE: its features [d_f] (or null).  (A persistent variant streaming the next
+// episode into shared memory with bulk copies measured 3.7x slower at C3: with
+// 2 warps per SM the short dependent global reads of ids / tokens / params are
+// no longer hidden; one warp per episode at full occupancy is faster.)
+__device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const int32_t* __restrict__ ids,
+                                               const uint8_t* __restrict__ tokens,
+                                               const uint8_t* __restrict__ cand_tokens, const float* lgE,
+                                               const float* fnE, const float* fpE, int d_f,
+                                               const int32_t* __restrict__ history, int gap_d,
+                                               const hsd_verify_params* __restrict__ params, int P, int need_cos,
+                                               hsd_outcome* __restrict__ out, uint8_t* __restrict__ tok_out,
+                                               WarpScratch& W) {
+  const int lane = threadIdx.x & 31;
   // ---- greedy tokens: argmax per position, lowest index on ties.  The 7
   //      positions of an action slice are loaded before any is reduced (7 KB
   //      in flight per warp) — the kernel is HBM-bound at C3's 4096 episodes.
-  const float4* lg = reinterpret_cast<const float4*>(logits + (size_t)e * L * 256);
+  const float4* lg = reinterpret_cast<const float4*>(lgE);
   for (int p0 = 0; p0 < L; p0 += 7) {
     float4 a[7], c[7];
 #pragma unroll
     for (int u = 0; u < 7; ++u) {
-      a[u] = __ldg(lg + (p0 + u) * 64 + lane * 2);
-      c[u] = __ldg(lg + (p0 + u) * 64 + lane * 2 + 1);
+      a[u] = lg[(p0 + u) * 64 + lane * 2];
+      c[u] = lg[(p0 + u) * 64 + lane * 2 + 1];
     }
 #pragma unroll
     for (int u = 0; u < 7; ++u) {
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
           bi = oi;
         }
       }
-      if (lane == 0) s_greedy[warp][p0 + u] = bi;
+      if (lane == 0) W.greedy[p0 + u] = bi;
     }
   }
 
@@ -110,18 +114,20 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
   //      result is the exact sum rounded once, so the order is free and
   //      kFeatUnroll float4 pairs per lane are loaded before they are accumulated)
   double cosv = -2.0;
-  if (need_cos && feat_now && feat_prev) {
-    const float4* a4 = reinterpret_cast<const float4*>(feat_now + (size_t)e * d_f);
-    const float4* b4 = reinterpret_cast<const float4*>(feat_prev + (size_t)e * d_f);
+  if (need_cos && fnE && fpE) {
+    const float4* a4 = reinterpret_cast<const float4*>(fnE);
+    const float4* b4 = reinterpret_cast<const float4*>(fpE);
     const int n4 = d_f / 4;
-    double hi = 0.0, lo = 0.0;
+    // four independent double-double accumulators (one per float4 component)
+    // keep four dependent chains in flight instead of one
+    double hv[4] = {0.0, 0.0, 0.0, 0.0}, lv[4] = {0.0, 0.0, 0.0, 0.0};
     for (int t0 = lane; t0 < n4; t0 += 32 * kFeatUnroll) {
       float4 xa[kFeatUnroll], yb[kFeatUnroll];
 #pragma unroll
       for (int u = 0; u < kFeatUnroll; ++u) {
         const int t = t0 + 32 * u;
-        xa[u] = t < n4 ? __ldg(a4 + t) : make_float4(0.f, 0.f, 0.f, 0.f);
-        yb[u] = t < n4 ? __ldg(b4 + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+        xa[u] = t < n4 ? a4[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+        yb[u] = t < n4 ? b4[t] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < kFeatUnroll; ++u) {
@@ -130,11 +136,19 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           double s, er;
-          dev::two_sum(hi, pr[i], s, er);
-          hi = s;
-          lo = __dadd_rn(lo, er);
+          dev::two_sum(hv[i], pr[i], s, er);
+          hv[i] = s;
+          lv[i] = __dadd_rn(lv[i], er);
         }
       }
+    }
+    double hi = hv[0], lo = lv[0];
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+      double s, er;
+      dev::two_sum(hi, hv[i], s, er);
+      hi = s;
+      lo = __dadd_rn(__dadd_rn(lo, lv[i]), er);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -161,21 +175,21 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
       const uint8_t* row = cand_tokens ? cand_tokens + ((size_t)e * k + lane) * HSD_TOKENS_STRIDE
                                        : tokens + (size_t)id * HSD_TOKENS_STRIDE;
       const uint32_t* src = reinterpret_cast<const uint32_t*>(row);
-      uint32_t* dst = reinterpret_cast<uint32_t*>(s_tok[warp][lane]);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(W.tok[lane]);
 #pragma unroll
       for (int i = 0; i < kTokStride / 4; ++i) dst[i] = __ldg(src + i);
     }
   }
   __syncwarp();
-  const int* greedy = s_greedy[warp];  // positions < L (shared memory, no per-thread copy)
+  const int* greedy = W.greedy;  // positions < L (shared memory, no per-thread copy)
   const int hist = history ? history[e] : 0x7fffffff;
 
   // ---- candidate dedup (chain language) — independent of params
   if (lane < n_cand) {
-    const uint8_t* me = s_tok[warp][lane];
+    const uint8_t* me = W.tok[lane];
     int ca = lane, cb = lane;
     for (int c = 0; c < lane; ++c) {
-      const uint8_t* o = s_tok[warp][c];
+      const uint8_t* o = W.tok[c];
       if (ca == lane && o[0] == me[0] && o[1] == me[1] && o[2] == me[2]) ca = c;
       if (cb == lane) {
         bool same = true;
@@ -183,20 +197,20 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
         if (same) cb = c;
       }
     }
-    s_canA[warp][lane] = ca;
-    s_canB[warp][lane] = cb;
+    W.canA[lane] = ca;
+    W.canB[lane] = cb;
   }
   __syncwarp();
   int nA = 0, nB = 0;
   {
-    const bool isA = lane < n_cand && s_canA[warp][lane] == lane;
-    const bool isB = lane < n_cand && s_canB[warp][lane] == lane;
+    const bool isA = lane < n_cand && W.canA[lane] == lane;
+    const bool isB = lane < n_cand && W.canB[lane] == lane;
     const unsigned mA = __ballot_sync(0xffffffffu, isA), mB = __ballot_sync(0xffffffffu, isB);
     nA = __popc(mA);
     nB = __popc(mB);
     if (lane < n_cand) {
-      s_rankA[warp][lane] = isA ? __popc(mA & ((1u << lane) - 1)) : -1;
-      s_rankB[warp][lane] = isB ? __popc(mB & ((1u << lane) - 1)) : -1;
+      W.rankA[lane] = isA ? __popc(mA & ((1u << lane) - 1)) : -1;
+      W.rankB[lane] = isB ? __popc(mB & ((1u << lane) - 1)) : -1;
     }
   }
   __syncwarp();
@@ -218,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
     for (int idx = lane; idx < npairs; idx += 32) {  // A
       const int pi = p0 + idx / n_cand, c = idx % n_cand;
       const hsd_verify_params& pp = params[pi];
-      const uint8_t* me = s_tok[warp][c];
+      const uint8_t* me = W.tok[c];
       int st, ln;
       bool gr;
       group_at(0, st, ln, gr);
@@ -229,12 +243,12 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
         if (!accept_group(me, greedy, st, ln, gr, pp)) break;
         rest += ln;
       }
-      s_pair[warp][idx] = (uint8_t)(rest | (a0 << 7));
+      W.pair[idx] = (uint8_t)(rest | (a0 << 7));
     }
     __syncwarp();
     for (int idx = lane; idx < npairs; idx += 32) {  // B
       const int pi = p0 + idx / n_cand, a = idx % n_cand, base = idx - a;
-      const int rA = s_rankA[warp][a];
+      const int rA = W.rankA[a];
       int len = -1, bb = -1;
       if (rA >= 0) {
         const int cap = params[pi].chain_cap > 0 ? params[pi].chain_cap : 64;
@@ -242,19 +256,19 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
         if (limit > 0) {
           int br = -1;
           for (int b = 0; b < n_cand; ++b) {
-            const int rb = s_rankB[warp][b];
+            const int rb = W.rankB[b];
             if (rb < 0 || rb >= limit) continue;
-            const int r = s_pair[warp][base + b] & 0x7F;
+            const int r = W.pair[base + b] & 0x7F;
             if (r > br) {
               br = r;
               bb = b;
             }
           }
-          len = (s_pair[warp][idx] >> 7) ? 3 + br : 0;
+          len = (W.pair[idx] >> 7) ? 3 + br : 0;
         }
       }
-      s_len[warp][idx] = (int8_t)len;
-      s_bb[warp][idx] = (int8_t)bb;
+      W.len[idx] = (int8_t)len;
+      W.bb[idx] = (int8_t)bb;
     }
     __syncwarp();
     for (int q = lane; q < pc; q += 32) {  // C
@@ -278,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
         o.win_b = 0;
         o.skipped = 1;
         o.n_emit = (int16_t)L;
-        for (int t = 0; t < L; ++t) my_tok[t] = s_tok[warp][0][t];
+        for (int t = 0; t < L; ++t) my_tok[t] = W.tok[0][t];
       } else if (n_cand == 0) {  // empty shard: autoregressive step
         o.fallback = 1;
         o.calls = 1;
@@ -289,13 +303,13 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
         const int cap = pp.chain_cap > 0 ? pp.chain_cap : 64;
         int wl = -1, wa = 0, wr = 1 << 20, wb = -1;  // longest, then the earliest chain (smallest rank of a)
         for (int a = 0; a < n_cand; ++a) {
-          const int l = s_len[warp][q * n_cand + a];
-          const int ra = s_rankA[warp][a] >= 0 ? s_rankA[warp][a] : (1 << 20);
+          const int l = W.len[q * n_cand + a];
+          const int ra = W.rankA[a] >= 0 ? W.rankA[a] : (1 << 20);
           if (l > wl || (l == wl && ra < wr)) {
             wl = l;
             wa = a;
             wr = ra;
-            wb = s_bb[warp][q * n_cand + a];
+            wb = W.bb[q * n_cand + a];
           }
         }
         const long long chains = (long long)nA * nB;
@@ -313,13 +327,32 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
           o.accept_len = wl;
           o.n_emit = (int16_t)wl;
           for (int t = 0; t < L; ++t)
-            my_tok[t] = t < wl ? (t < 3 ? s_tok[warp][wa][t] : s_tok[warp][wb][t]) : (uint8_t)0;
+            my_tok[t] = t < wl ? (t < 3 ? W.tok[wa][t] : W.tok[wb][t]) : (uint8_t)0;
         }
       }
       out[(size_t)pi * E + e] = o;
     }
     __syncwarp();
   }
+}
+
+__global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __restrict__ ids, int E, int k, int L,
+                                                             const uint8_t* __restrict__ tokens,
+                                                             const uint8_t* __restrict__ cand_tokens,
+                                                             const float* __restrict__ logits,
+                                                             const float* __restrict__ feat_now,
+                                                             const float* __restrict__ feat_prev, int d_f,
+                                                             const int32_t* __restrict__ history, int gap_d,
+                                                             const hsd_verify_params* __restrict__ params, int P,
+                                                             int need_cos, hsd_outcome* __restrict__ out,
+                                                             uint8_t* __restrict__ tok_out) {
+  __shared__ WarpScratch sw[kWarps];
+  const int warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * kWarps + warp;
+  if (e >= E) return;
+  verify_episode(e, E, k, L, ids, tokens, cand_tokens, logits + (size_t)e * L * 256,
+                 feat_now ? feat_now + (size_t)e * d_f : nullptr, feat_prev ? feat_prev + (size_t)e * d_f : nullptr,
+                 d_f, history, gap_d, params, P, need_cos, out, tok_out, sw[warp]);
 }
 
 }  // namespace
