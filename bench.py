@@ -18,10 +18,14 @@ fp32 keys (16.4 GB resident in HBM), batch 64 queries, k = 8, draft length 7,
   cpu_baseline  the reference's own search (oracle/_ref, store.cpp compiled
              in place) + oracle port of verify/kinematics on the host cores
 
---gpus N (torchrun): the 1M DB is row-sharded over N GPUs (strong scaling);
-each pass searches all 64 queries on every shard, exchanges the B x k draft
-records with an NCCL all-gather and merges them; verification of the 64
-episodes is split across ranks.
+--gpus N (torchrun), --shard episodes (default): every GPU holds the 1M DB
+(+ its bf16 filter copy) and runs its own batches of independent episodes —
+the episodes are the independent units, so there is no collective on the data
+path (weak scaling; value = all ranks' steps / the slowest rank's time).
+--shard db: the 1M DB is row-sharded over N GPUs (strong scaling); each pass
+searches all 64 queries on every shard, exchanges the B x k draft records with
+an NCCL all-gather and merges them; verification of the 64 episodes is split
+across ranks (the path C4 / C5 use for DBs that do not fit one GPU).
 
 --impl reference: the reference CPU path alone (see cpu_reference_step).
 
@@ -69,6 +73,10 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--force-sharded", action="store_true",
                    help="use the sharded (NCCL all-gather + merge) step even at world size 1")
+    p.add_argument("--shard", default="episodes", choices=["episodes", "db"],
+                   help="N > 1: 'episodes' = every rank holds the DB and runs its own batch of independent episodes "
+                        "(weak scaling, no collective on the data path); 'db' = the DB is row-sharded and every "
+                        "query searches all shards (local top-k + NCCL all-gather + merge, strong scaling)")
     p.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "bf16", "c5"])
     p.add_argument("--robots", type=int, default=1024, help="C5 robots")
     p.add_argument("--traj-T", type=int, default=500, help="C5 demonstration length (actions) per DB episode")
@@ -347,7 +355,9 @@ def config_of(args, world):
                    else getattr(args, "filter_note", "native (filter reads the stored keys)")),
         "n_rows": args.n, "dim": args.dim, "batch": args.batch, "k": args.k, "draft_len": args.L, "d_f": args.d_f,
         "synthetic_family": "REAL" if args.kind == 1 else "EXACT",
-        "parallelism": f"db-shard{world}" if world > 1 else "single",
+        "parallelism": ("single" if world == 1 else
+                        f"episode-shard{world} (DB replica per GPU, no collective)" if args.shard == "episodes"
+                        and not args.force_sharded else f"db-shard{world} (NCCL all-gather + merge)"),
         "l2": f"inputs larger than L2 ({args.n * args.dim * (2 if args.dtype == 'bf16' else 4) / 1e9:.1f} GB of keys "
               f"streamed per pass)",
         "verify": "relaxed 30/15, verify-skip min_S=0.95 O_dist=5 d=1, chain cap 64",
@@ -363,12 +373,14 @@ def run_ours(args):
     from paper_2603_17573_b200 import synth
 
     rank, world, local = env_rank()
+    local = local % max(torch.cuda.device_count(), 1)  # (plumbing tests may run several ranks on one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dist, dev)
     B, k, L, d_f, dim = args.batch, args.k, args.L, args.d_f, args.dim
-    b0, b1 = H.shard_range(args.n, world, rank)
+    replicas = world > 1 and args.shard == "episodes" and not args.force_sharded
+    b0, b1 = (0, args.n) if replicas else H.shard_range(args.n, world, rank)
     col = H.Collection(dim, capacity=b1 - b0, device=local, dtype=args.dtype)
     col.generate(args.kind, 2026, b1 - b0, row0=b0)
     if args.filter == "bf16_copy" and args.dtype == "f32":
@@ -381,8 +393,9 @@ def run_ours(args):
 
     # inputs resident in HBM: S distinct batches cycled through the steps
     S = 4
-    rows = [synth.query_rows(7, args.kind, args.n, s * B, B) for s in range(S)]
-    qs = [H.gen_queries(args.kind, 7, 2026, args.n, s * B, B, dim, device=local) for s in range(S)]
+    e0_rank = rank * S * B if replicas else 0  # replicas: each rank runs its own episodes
+    rows = [synth.query_rows(7, args.kind, args.n, e0_rank + s * B, B) for s in range(S)]
+    qs = [H.gen_queries(args.kind, 7, 2026, args.n, e0_rank + s * B, B, dim, device=local) for s in range(S)]
     # logits are generated from global rows; with a sharded DB use the token view of rank-local rows only when
     # available: generate them on the host oracle-free path -> device generator needs the row's tokens, so we
     # build them from a full-token collection of the rows we need (tokens are tiny).
@@ -393,7 +406,7 @@ def run_ours(args):
     hist = torch.full((B,), 100, dtype=torch.int32, device=dev)
     vp = H.VerifyParams.make(relaxed=True, bias_seq_max=30, bias_token_max=15, skip_enabled=True, min_S=0.95, O_dist=5)
 
-    if world == 1 and not args.force_sharded:
+    if (world == 1 or replicas) and not args.force_sharded:
         eng = H.Engine(col, B, k, L, d_f, 15)
         outs = dict(scores=torch.empty((B, k), dtype=torch.float64, device=dev),
                     ids=torch.empty((B, k), dtype=torch.int32, device=dev),
@@ -451,11 +464,9 @@ def run_ours(args):
         barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = reduce_scalar(dist, torch, ms, "max")
     ms_per_step = ms / args.steps
-    value = B * args.steps / (ms / 1e3)
+    value = (world if replicas else 1) * B * args.steps / (ms / 1e3)  # whole-job steps/s
 
     stages = None
     roof = None
@@ -483,10 +494,13 @@ def run_ours(args):
                               "peak_source": "measured bf16" if esz == 2
                               else "measured bf16 / 2 (nominal TF32:BF16 dense ratio)"}
 
-    # ---- e2e through the public host-buffer API (N=1: hsd_step_host)
+    # ---- e2e through the public host-buffer API (hsd_step_host_async)
     e2e = None
     if eng is not None:
         e2e = run_e2e(H, torch, eng, args, qs, lg, feats, xyz_np, vp, stream)
+        if replicas:  # whole job: the slowest rank's rate x ranks
+            e2e["value"] = reduce_scalar(dist, torch, e2e["value"], "min") * world
+            e2e["note"] = "min over ranks x ranks (each rank its own episodes)"
 
     overflow = col.overflow_count(stream)
     recall = None
@@ -498,7 +512,8 @@ def run_ours(args):
             cb, _ = cpu_baseline(args, seconds_budget=args.cpu_seconds)
         line = {
             "metric": metric_of(args), "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if (replicas or world == 1) else "strong",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (counter-generated DB/queries/logits/features)",
             "config": config_of(args, world), "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "stages_ms": stages,
@@ -510,6 +525,24 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def init_dist(dist, dev):
+    """NCCL (one process per GPU); HSD_BENCH_BACKEND=gloo for plumbing runs with
+    several ranks on one GPU (the timing reductions use CPU tensors)."""
+    backend = os.environ.get("HSD_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+
+
+def reduce_scalar(dist, torch, v, op):
+    t = torch.tensor([float(v)], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.MIN)
+    return float(t.item())
 
 
 def gen_logits_global(H, args, rows, local, col, b0, b1):
@@ -764,10 +797,11 @@ def run_c5(args):
     import paper_2603_17573_b200 as H
 
     rank, world, local = env_rank()
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dist, dev)
     b0, b1 = H.shard_range(args.n, world, rank)
     col = H.Collection(args.dim, capacity=b1 - b0, device=local, dtype=args.dtype)
     col.generate(args.kind, 2026, b1 - b0, row0=b0, payload=H.PAYLOAD_TRAJ, traj_T=args.traj_T)
@@ -790,9 +824,7 @@ def run_c5(args):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = reduce_scalar(dist, torch, ms, "max")
     n_rounds, stages = loop.stage_times()
     tr = loop.trace()[args.warmup:]
     rep = loop.reports()
