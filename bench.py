@@ -77,7 +77,8 @@ def parse():
                    help="N > 1: 'episodes' = every rank holds the DB and runs its own batch of independent episodes "
                         "(weak scaling, no collective on the data path); 'db' = the DB is row-sharded and every "
                         "query searches all shards (local top-k + NCCL all-gather + merge, strong scaling)")
-    p.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "bf16", "c5"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "bf16", "c5"])
+    p.add_argument("--graph", action="store_true", help="replay each decode round from a captured CUDA graph")
     p.add_argument("--robots", type=int, default=1024, help="C5 robots")
     p.add_argument("--traj-T", type=int, default=500, help="C5 demonstration length (actions) per DB episode")
     p.add_argument("--k-top", type=int, default=3, help="C5 K_top (SPEC default 3)")
@@ -93,6 +94,14 @@ def parse():
             a.n = 10_000_000
         if "--batch" not in given:
             a.batch = 256
+    if a.config == "c1":  # configs[0]: 10k-entry DB, batch 1, a 200-step episode; launch-bound -> CUDA graphs
+        if "--n" not in given:
+            a.n = 10_000
+        if "--batch" not in given:
+            a.batch = 1
+        if "--steps" not in given:
+            a.steps = 200
+        a.graph = True
     if a.config == "c5":
         world = int(os.environ.get("WORLD_SIZE", 1))
         if "--n" not in given:
@@ -283,7 +292,10 @@ def cpu_reference_step(args, state, n_sample, threads):
 
 def cpu_sample_rows(args):
     """Rows of the DB sample the CPU arm searches: ~1-2 s of CPU work per pass
-    (1/16 of the 1M DB; capped so a 10M DB does not need 20 GB of host fp64)."""
+    (1/16 of the 1M DB; capped so a 10M DB does not need 20 GB of host fp64;
+    config 1's 10k-row DB is searched whole)."""
+    if args.n <= 20_000:
+        return args.n
     return max(1000, min(args.n, args.n // 16, 62_500))
 
 
@@ -343,7 +355,7 @@ def metric_of(args):
 
 
 def config_of(args, world):
-    tag = {"c2": "C2", "c4": "C4", "bf16": "C2-bf16"}.get(args.config, args.config)
+    tag = {"c1": "C1", "c2": "C2", "c4": "C4", "bf16": "C2-bf16"}.get(args.config, args.config)
     return {
         "workload": (f"{tag}: {args.n}-entry x {args.dim}-d {args.dtype} trajectory DB, batch {args.batch} queries, "
                      f"k={args.k}, draft len {args.L}, 7x256 verifier logits, {args.d_f}-d skip features, "
@@ -358,7 +370,8 @@ def config_of(args, world):
         "parallelism": ("single" if world == 1 else
                         f"episode-shard{world} (DB replica per GPU, no collective)" if args.shard == "episodes"
                         and not args.force_sharded else f"db-shard{world} (NCCL all-gather + merge)"),
-        "l2": f"inputs larger than L2 ({args.n * args.dim * (2 if args.dtype == 'bf16' else 4) / 1e9:.1f} GB of keys "
+        "l2": getattr(args, "l2_note", None) or
+              f"inputs larger than L2 ({args.n * args.dim * (2 if args.dtype == 'bf16' or args.filter == 'bf16_copy' else 4) / 1e9:.1f} GB of keys "
               f"streamed per pass)",
         "verify": "relaxed 30/15, verify-skip min_S=0.95 O_dist=5 d=1, chain cap 64",
     }
@@ -389,6 +402,9 @@ def run_ours(args):
         except H.OutOfMemoryError:  # e.g. C4's 164 GB of fp32 keys on one GPU: no room for the copy
             args.filter = "native"
             args.filter_note = "bf16 copy does not fit next to the fp32 keys on this GPU; native TF32 filter"
+    if args.graph:  # graph capture needs a non-legacy stream
+        gstream = torch.cuda.Stream(device=dev)
+        torch.cuda.set_stream(gstream)
     stream = torch.cuda.current_stream()
 
     # inputs resident in HBM: S distinct batches cycled through the steps
@@ -419,8 +435,8 @@ def run_ours(args):
                               history=hist, **outs) for s in range(S)]
 
         def step(i):
-            eng.step(B, bufs[i % S], vp, gap_d=1, stream=stream)
-        launches_per_step = 4
+            eng.step(B, bufs[i % S], vp, gap_d=1, stream=stream, graph=args.graph)
+        launches_per_step = 7  # K5, pad queries, K1, K2 (3 kernels), K4 — eager or as the nodes of one graph launch
     else:
         comm = setup_comm(H, dist, world, rank, local)
         lo, hi = H.shard_range(B, world, rank)  # this rank's episodes
@@ -455,14 +471,29 @@ def run_ours(args):
         eng.enable_timing(args.steps)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    # A DB that fits in L2 (config 1: 82 MB scanned per step) would stay cached
+    # across steps: flush L2 between timed steps (a 512 MB write, outside the
+    # per-step CUDA-event brackets) and sum the per-step device times.
+    scanned = (b1 - b0) * dim * (2 if (args.dtype == "bf16" or args.filter == "bf16_copy") else 4)
+    flush = scanned < 2 * 126e6
+    if flush:
+        l2buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
         for i in range(args.steps):
+            if flush:
+                l2buf.fill_(i & 0xFF)
+                evs[i][0].record(stream)
             step(i)
+            if flush:
+                evs[i][1].record(stream)
         e1.record(stream)
         barrier()
-    ms = e0.elapsed_time(e1)
+    ms = e0.elapsed_time(e1) if not flush else sum(a.elapsed_time(b) for a, b in evs)
+    args.l2_note = ("L2 flushed between timed steps (512 MB write outside the per-step CUDA-event brackets; the "
+                    "per-step device times are summed)") if flush else None
     if world > 1:
         ms = reduce_scalar(dist, torch, ms, "max")
     ms_per_step = ms / args.steps
@@ -470,6 +501,12 @@ def run_ours(args):
 
     stages = None
     roof = None
+    if eng is not None and args.graph:  # graph replays carry no stage events: time eager rounds of the same shape
+        eng.stage_times()
+        eng.enable_timing(min(args.steps, 50))
+        for i in range(min(args.steps, 50)):
+            eng.step(B, bufs[i % S], vp, gap_d=1, stream=stream)
+        torch.cuda.synchronize()
     if eng is not None:
         n_rec, st = eng.stage_times()
         stages = {kname: v / max(n_rec, 1) for kname, v in st.items()}

@@ -275,6 +275,12 @@ typedef struct hsd_step_io {
 
 hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
                     const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream);
+/* hsd_step replayed from a CUDA graph: the first call with a given (B, io
+ * pointers, parameters, stream) runs eagerly and captures the round; later
+ * identical calls launch the graph (one launch instead of ~10: for small,
+ * launch-bound batches such as config 1's B = 1).  Needs a non-NULL stream. */
+hsd_status hsd_step_graph(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                          const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream);
 /* Stage timing of the next `max_steps` hsd_step calls with CUDA events on the
  * step's stream (0 disables).  hsd_engine_stage_times synchronizes and returns
  * the summed milliseconds of [kinematics, similarity, select, verify, total]

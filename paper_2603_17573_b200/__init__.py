@@ -200,6 +200,8 @@ def lib():
                           C.POINTER(NormBounds), C.c_int, _vp],
         "hsd_step_host_async": [_vp, C.c_int, C.POINTER(StepIO), C.POINTER(VerifyParams), C.POINTER(MetricParams),
                                 C.POINTER(NormBounds), C.c_int, _vp],
+        "hsd_step_graph": [_vp, C.c_int, C.POINTER(StepIO), C.POINTER(VerifyParams), C.POINTER(MetricParams),
+                           C.POINTER(NormBounds), C.c_int, _vp],
         "hsd_engine_sync": [_vp],
         "hsd_comm_unique_id": [_vp],
         "hsd_comm_create": [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
@@ -680,9 +682,13 @@ class Engine:
         names = ("kinematics", "similarity", "select", "verify", "total")
         return n.value, dict(zip(names, list(ms)))
 
-    def step(self, B, bufs: StepBuffers, vp: VerifyParams, mp=DEFAULT_METRIC, nb=LIBERO_GOAL, gap_d=1, stream=None):
+    def step(self, B, bufs: StepBuffers, vp: VerifyParams, mp=DEFAULT_METRIC, nb=LIBERO_GOAL, gap_d=1, stream=None,
+             graph=False):
+        """One decode round on device buffers; graph=True replays a captured CUDA graph of the round (needs a
+        non-default stream)."""
         io = bufs.io()
-        check(lib().hsd_step(self._h, B, C.byref(io), C.byref(vp), C.byref(mp), C.byref(nb), gap_d, _stream(stream)))
+        fn = lib().hsd_step_graph if graph else lib().hsd_step
+        check(fn(self._h, B, C.byref(io), C.byref(vp), C.byref(mp), C.byref(nb), gap_d, _stream(stream)))
 
     def step_host(self, B, bufs: StepBuffers, vp: VerifyParams, mp=DEFAULT_METRIC, nb=LIBERO_GOAL, gap_d=1,
                   stream=None):

@@ -793,9 +793,17 @@ struct StageSlot {
   bool used = false;
 };
 
+// A captured decode round (hsd_step_graph): the launch sequence of one
+// (shape, buffers, parameters, stream) combination replayed as one graph.
+struct StepGraph {
+  std::vector<uint8_t> key;
+  cudaGraphExec_t exec = nullptr;
+};
+
 struct hsd_engine {
   hsd_collection* c = nullptr;
   int max_B = 0, k = 0, L = 0, d_f = 0, w = 0;
+  std::vector<StepGraph> graphs;  // small LRU-less cache (cleared when full)
   StageSlot slot[2];
   int next_slot = 0;
   cudaStream_t up = nullptr, down = nullptr;  // H2D / D2H copy streams
@@ -914,6 +922,7 @@ hsd_status hsd_engine_destroy(hsd_engine* e) {
   }
   if (e->up) cudaStreamDestroy(e->up);
   if (e->down) cudaStreamDestroy(e->down);
+  for (StepGraph& g : e->graphs) cudaGraphExecDestroy(g.exec);
   delete e;
   return HSD_OK;
 }
@@ -967,6 +976,67 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
     ++e->recorded;
   }
   return HSD_OK;
+}
+
+hsd_status hsd_step_graph(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                          const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream) {
+  if (!e || !io || !vp) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (B < 0 || B > e->max_B) return fail(HSD_ERR_INVALID_INPUT, "batch %d outside [0, %d]", B, e->max_B);
+  if (B == 0) return HSD_OK;
+  hsd_status st = require_device(e->c->device);
+  if (st != HSD_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!s) return fail(HSD_ERR_INVALID_INPUT, "graph capture needs an explicit (non-legacy) stream");
+  // key: everything the captured launches depend on
+  std::vector<uint8_t> key;
+  auto put = [&](const void* p, size_t n) {
+    const uint8_t* b = (const uint8_t*)p;
+    key.insert(key.end(), b, b + n);
+  };
+  put(&B, sizeof B);
+  put(io, sizeof *io);
+  put(vp, sizeof *vp);
+  const hsd_metric_params mpz = mp ? *mp : hsd_metric_params{};
+  const hsd_norm_bounds nbz = nb ? *nb : hsd_norm_bounds{};
+  put(&mpz, sizeof mpz);
+  put(&nbz, sizeof nbz);
+  put(&gap_d, sizeof gap_d);
+  put(&s, sizeof s);
+  const int64_t n = e->c->n;
+  put(&n, sizeof n);
+  for (StepGraph& g : e->graphs)
+    if (g.key == key) {
+      CU(cudaGraphLaunch(g.exec, s));
+      return HSD_OK;
+    }
+  // miss: run the round eagerly (warms every per-stream cache), then capture
+  // the same launch sequence for the next calls
+  const int saved = e->max_steps;
+  e->max_steps = 0;  // no stage-timing events inside graphs
+  st = hsd_step(e, B, io, vp, mp, nb, gap_d, stream);
+  if (st == HSD_OK) {
+    cudaGraph_t g = nullptr;
+    CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    st = hsd_step(e, B, io, vp, mp, nb, gap_d, stream);
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (st == HSD_OK && ce != cudaSuccess) st = cuda_fail(ce, "cudaStreamEndCapture");
+    if (st == HSD_OK) {
+      cudaGraphExec_t x = nullptr;
+      ce = cudaGraphInstantiate(&x, g, 0);
+      if (ce != cudaSuccess) {
+        st = cuda_fail(ce, "cudaGraphInstantiate");
+      } else {
+        if (e->graphs.size() >= 16) {
+          for (StepGraph& old : e->graphs) cudaGraphExecDestroy(old.exec);
+          e->graphs.clear();
+        }
+        e->graphs.push_back({std::move(key), x});
+      }
+    }
+    if (g) cudaGraphDestroy(g);
+  }
+  e->max_steps = saved;
+  return st;
 }
 
 hsd_status hsd_step_host_async(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,

@@ -65,3 +65,32 @@ def test_host_and_async_steps_match_device_steps(torch):
         for s in range(S):
             for kk in outs[s]:
                 assert torch.equal(outs[s][kk], ref[s][kk]), (rep, s, kk)
+
+
+def test_graph_replay_matches_eager(torch):
+    """hsd_step_graph: the captured round replays to the eager results (B = 1, config-1 shape)."""
+    n, dim, B, k, L, d_f = 10000, 4096, 1, 8, 7, 4096
+    col = H.Collection(dim, capacity=n)
+    col.generate(H.REAL, 5, n)
+    col.set_filter("bf16_copy")
+    eng = H.Engine(col, B, k, L, d_f, 15)
+    vp = H.VerifyParams.make(skip_enabled=True, min_S=0.95, O_dist=5)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        ins = [make_inputs(torch, col, n, dim, B, L, d_f, s) for s in range(3)]
+        ref, got = [], []
+        for s in range(3):
+            o = outputs(torch, B, k, L, "cuda")
+            eng.step(B, H.StepBuffers(**ins[s], **o), vp, stream=st)
+            st.synchronize()
+            ref.append({kk: v.clone() for kk, v in o.items()})
+        bufs = [(outputs(torch, B, k, L, "cuda")) for _ in range(3)]
+        for rep in range(3):  # miss (eager + capture), then replays
+            for s in range(3):
+                for v in bufs[s].values():
+                    v.zero_()
+                eng.step(B, H.StepBuffers(**ins[s], **bufs[s]), vp, stream=st, graph=True)
+            st.synchronize()
+            for s in range(3):
+                for kk in bufs[s]:
+                    assert torch.equal(bufs[s][kk], ref[s][kk]), (rep, s, kk)
