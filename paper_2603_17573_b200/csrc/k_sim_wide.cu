@@ -267,11 +267,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) mbar_arrive(&S.acc_empty[buf]);
           }
           if constexpr (kDump) {
+            if (base + r < row_end) {
+              const size_t nrows = (size_t)(row_end - row_begin);
+              const int q0 = j * kStgQ + half * 16;
+              float* drow = dump + (size_t)q0 * nrows + (size_t)(base + r - row_begin);
+              const int tmax = min(16, B - q_base - q0);
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-              const int q = j * kStgQ + half * 16 + t;
-              if (base + r < row_end && q_base + q < B)
-                dump[(size_t)q * (row_end - row_begin) + (base + r - row_begin)] = __uint_as_float(acc[t]);
+              for (int t = 0; t < 16; ++t)
+                if (t < tmax) drow[(size_t)t * nrows] = __uint_as_float(acc[t]);
             }
           } else {
 #pragma unroll
@@ -387,11 +390,13 @@ cudaError_t launch_dispatch(int NS, const CUtensorMap& km, const CUtensorMap& qm
                             int B, int lists, int64_t per, uint64_t* partial, float* dump, cudaStream_t s) {
   const int mode = wide_acc_mode();
   if (NS == 1) return launch_ns<kBf16, 1, 4, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
-  if (NS == 2) {
-    if (mode == 1 && !kDump) return launch_ns<kBf16, 2, 4, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
-    return launch_ns<kBf16, 2, 2, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
+  if constexpr (!kDump) {  // the single-buffer ablation is not instantiated for the debug dump
+    if (mode == 1) {
+      if (NS == 2) return launch_ns<kBf16, 2, 4, false>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
+      return launch_ns<kBf16, 4, 2, false>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
+    }
   }
-  if (mode == 1 && !kDump) return launch_ns<kBf16, 4, 2, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
+  if (NS == 2) return launch_ns<kBf16, 2, 2, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
   return launch_ns<kBf16, 4, 1, kDump>(km, qm, rb, re, dim, B, lists, per, partial, dump, s);
 }
 

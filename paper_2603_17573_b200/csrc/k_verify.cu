@@ -26,7 +26,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxL = 21;
 constexpr int kTokStride = 24;  // bytes per candidate row in shared memory
 constexpr int kPairs = 256;     // (parameter set, candidate) pairs per warp per chunk
 constexpr int kFeatUnroll = 4;  // feature float4 pairs loaded per lane before accumulation
