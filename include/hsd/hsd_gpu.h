@@ -320,6 +320,22 @@ hsd_status hsd_shard_range(int64_t n_total, int world, int rank, int64_t* begin,
 hsd_status hsd_search_topk_sharded(hsd_collection* c, hsd_comm* comm, int64_t id_offset, const float* queries, int B,
                                    int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream);
 
+/* Peer-memory exchange instead of the NCCL all-gather: every rank exports the
+ * CUDA IPC handle of its receive window (sized for up to max_B queries and
+ * k_max), the caller all-gathers the world x HSD_IPC_HANDLE_BYTES handles (any
+ * transport) and imports them.  hsd_search_topk_sharded then publishes each
+ * rank's B x k records straight into every peer's window (stores over
+ * NVLink / NVSwitch + a system-scope release flag per epoch) and merges once
+ * all G flags of its own window arrived — results identical to the NCCL
+ * path.  A peer that never publishes is reported by hsd_comm_p2p_status
+ * (bounded wait, no hang). */
+#define HSD_IPC_HANDLE_BYTES 64
+/* A communicator for the peer-memory exchange only (no NCCL communicator). */
+hsd_status hsd_comm_create_p2p(int world, int rank, int device, hsd_comm** out);
+hsd_status hsd_comm_p2p_export(hsd_comm* comm, int max_B, int k_max, uint8_t handle[HSD_IPC_HANDLE_BYTES]);
+hsd_status hsd_comm_p2p_import(hsd_comm* comm, const uint8_t* handles /* [world][HSD_IPC_HANDLE_BYTES] */);
+hsd_status hsd_comm_p2p_status(hsd_comm* comm, int* peer_timeout);
+
 /* K3 merge on the device: G per-shard exact top-k lists (g_scores fp64 /
  * g_ids int32 [G][B][k], ids already global; optional g_drafts uint8
  * [G][B][k][32]) -> the global [B][k] in (score desc, id asc) order.  Used by

@@ -206,6 +206,10 @@ def lib():
         "hsd_comm_unique_id": [_vp],
         "hsd_comm_create": [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
         "hsd_comm_destroy": [_vp],
+        "hsd_comm_create_p2p": [C.c_int, C.c_int, C.c_int, C.POINTER(_vp)],
+        "hsd_comm_p2p_export": [_vp, C.c_int, C.c_int, _vp],
+        "hsd_comm_p2p_import": [_vp, _vp],
+        "hsd_comm_p2p_status": [_vp, C.POINTER(C.c_int)],
         "hsd_shard_range": [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
         "hsd_search_topk_sharded": [_vp, _vp, C.c_int64, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
         "hsd_verify_round_drafts": [C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp,
@@ -473,11 +477,33 @@ class Comm:
         check(lib().hsd_comm_unique_id(buf))
         return bytes(buf)
 
-    def __init__(self, uid: bytes, world: int, rank: int, device: int):
+    def __init__(self, uid, world: int, rank: int, device: int):
+        """uid: an NCCL unique id (bytes) for the all-gather exchange, or None for a peer-memory-only
+        communicator (call p2p_export / p2p_import before searching)."""
         self._h = C.c_void_p()
-        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
-        check(lib().hsd_comm_create(buf, world, rank, device, C.byref(self._h)))
+        if uid is None:
+            check(lib().hsd_comm_create_p2p(world, rank, device, C.byref(self._h)))
+        else:
+            buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+            check(lib().hsd_comm_create(buf, world, rank, device, C.byref(self._h)))
         self.world, self.rank, self.device = world, rank, device
+
+    def p2p_export(self, max_B: int, k_max: int) -> bytes:
+        """CUDA IPC handle of this rank's receive window (all-gather it, then p2p_import)."""
+        buf = (C.c_uint8 * 64)()
+        check(lib().hsd_comm_p2p_export(self._h, max_B, k_max, buf))
+        return bytes(buf)
+
+    def p2p_import(self, handles) -> None:
+        """handles: the world ranks' p2p_export() bytes, in rank order."""
+        blob = b"".join(handles)
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        check(lib().hsd_comm_p2p_import(self._h, buf))
+
+    def p2p_timed_out(self) -> bool:
+        v = C.c_int()
+        check(lib().hsd_comm_p2p_status(self._h, C.byref(v)))
+        return bool(v.value)
 
     def close(self):
         if self._h:

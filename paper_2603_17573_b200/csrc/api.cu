@@ -1132,6 +1132,12 @@ struct hsd_comm {
   uint8_t* gt = nullptr;
   uint8_t* lt = nullptr;
   size_t cap = 0;  // entries per rank
+  // peer-memory exchange (hsd_comm_p2p_*): receive window + mapped peers
+  void* window = nullptr;
+  hsd::P2PWindows win{};
+  bool p2p = false;
+  uint64_t epoch = 0;
+  int* err = nullptr;
 };
 
 extern "C" {
@@ -1168,10 +1174,76 @@ hsd_status hsd_comm_create(const uint8_t id[HSD_UNIQUE_ID_BYTES], int world, int
 hsd_status hsd_comm_destroy(hsd_comm* c) {
   if (!c) return HSD_OK;
   cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
   if (c->comm) ncclCommDestroy(c->comm);
-  void* ps[] = {c->gs, c->gi, c->ls, c->li, c->gt, c->lt};
+  for (int g = 0; g < c->world && g < hsd::kMaxP2P; ++g)
+    if (c->p2p && g != c->rank && c->win.base[g]) cudaIpcCloseMemHandle(c->win.base[g]);
+  void* ps[] = {c->gs, c->gi, c->ls, c->li, c->gt, c->lt, c->window, c->err};
   for (void* p : ps) cudaFree(p);
   delete c;
+  return HSD_OK;
+}
+
+hsd_status hsd_comm_create_p2p(int world, int rank, int device, hsd_comm** out) {
+  if (!out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (world < 1 || rank < 0 || rank >= world) return fail(HSD_ERR_INVALID_INPUT, "bad rank %d of %d", rank, world);
+  if (world > hsd::kMaxP2P) return fail(HSD_ERR_CONFIG, "peer exchange supports up to %d ranks", hsd::kMaxP2P);
+  hsd_status st = require_device(device);
+  if (st != HSD_OK) return st;
+  auto* c = new hsd_comm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  *out = c;
+  return HSD_OK;
+}
+
+hsd_status hsd_comm_p2p_export(hsd_comm* c, int max_B, int k_max, uint8_t handle[HSD_IPC_HANDLE_BYTES]) {
+  if (!c || !handle) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (c->world > hsd::kMaxP2P) return fail(HSD_ERR_CONFIG, "peer exchange supports up to %d ranks", hsd::kMaxP2P);
+  if (max_B < 1 || k_max < 1 || k_max > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "bad window shape");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  static_assert(sizeof(cudaIpcMemHandle_t) == HSD_IPC_HANDLE_BYTES, "IPC handle size");
+  if (!c->window) {
+    const size_t bytes = hsd::p2p_window_bytes(c->world, max_B, k_max, &c->win);
+    CU(cudaMalloc(&c->window, bytes));
+    CU(cudaMemset(c->window, 0, bytes));  // flags start at epoch 0
+    CU(cudaMalloc(&c->err, sizeof(int)));
+    CU(cudaMemset(c->err, 0, sizeof(int)));
+    c->win.base[c->rank] = c->window;
+  }
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, c->window));
+  std::memcpy(handle, &h, sizeof h);
+  return HSD_OK;
+}
+
+hsd_status hsd_comm_p2p_import(hsd_comm* c, const uint8_t* handles) {
+  if (!c || !handles) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (!c->window) return fail(HSD_ERR_INVALID_INPUT, "call hsd_comm_p2p_export first");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  for (int g = 0; g < c->world; ++g) {
+    if (g == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles + (size_t)g * HSD_IPC_HANDLE_BYTES, sizeof h);
+    void* p = nullptr;
+    CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->win.base[g] = p;
+  }
+  CU(cudaDeviceSynchronize());
+  c->p2p = true;
+  return HSD_OK;
+}
+
+hsd_status hsd_comm_p2p_status(hsd_comm* c, int* peer_timeout) {
+  if (!c || !peer_timeout) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *peer_timeout = 0;
+  if (!c->err) return HSD_OK;
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  CU(cudaMemcpy(peer_timeout, c->err, sizeof(int), cudaMemcpyDeviceToHost));
   return HSD_OK;
 }
 
@@ -1218,6 +1290,16 @@ hsd_status hsd_search_topk_sharded(hsd_collection* col, hsd_comm* cm, int64_t id
   offset_ids_kernel<<<(int)((need + 255) / 256), 256, 0, s>>>(cm->li, (int)need, id_offset);
   CU(cudaGetLastError());
   // K3: exchange the B x k records over NVLink and merge (score desc, id asc)
+  if (cm->p2p) {  // peer-memory stores + flags, no NCCL launch
+    if (B > cm->win.Bmax || k > cm->win.kmax)
+      return fail(HSD_ERR_INVALID_INPUT, "batch %d / k %d exceed the peer window (%d, %d)", B, k, cm->win.Bmax,
+                  cm->win.kmax);
+    ++cm->epoch;
+    CU(hsd::launch_p2p_exchange(cm->win, cm->rank, cm->world, B, k, cm->epoch, cm->ls, cm->li, cm->lt, scores, ids,
+                                drafts, cm->err, s));
+    return HSD_OK;
+  }
+  if (!cm->comm) return fail(HSD_ERR_INVALID_INPUT, "peer-memory communicator not imported (hsd_comm_p2p_import)");
   NC(ncclGroupStart());
   NC(ncclAllGather(cm->ls, cm->gs, need, ncclFloat64, cm->comm, s));
   NC(ncclAllGather(cm->li, cm->gi, need, ncclInt32, cm->comm, s));

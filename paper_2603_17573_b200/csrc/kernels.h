@@ -81,6 +81,21 @@ cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, cons
 cudaError_t launch_merge_ranks(const double* g_scores, const int32_t* g_ids, const uint8_t* g_tok, int G, int B, int k,
                                double* scores, int32_t* ids, uint8_t* tok, cudaStream_t s);
 
+// K3 over peer memory (k_p2p.cu): receive windows shared by CUDA IPC; publish
+// writes this rank's B x k records into every peer's window + a release flag,
+// merge waits for all G flags of its own window and merges.  err set on a
+// peer that never published (bounded spin, no hang).
+constexpr int kMaxP2P = 8;
+struct P2PWindows {
+  void* base[kMaxP2P];  // window of each rank as mapped in this process (own = local allocation)
+  size_t off_flags, off_scores, off_ids, off_toks;
+  int Bmax, kmax;
+};
+size_t p2p_window_bytes(int G, int Bmax, int kmax, P2PWindows* layout);
+cudaError_t launch_p2p_exchange(const P2PWindows& w, int rank, int G, int B, int k, uint64_t epoch,
+                                const double* ls, const int32_t* li, const uint8_t* lt, double* scores, int32_t* ids,
+                                uint8_t* tok, int* err, cudaStream_t s);
+
 // ---- K4 gather + verify-skip + relaxed acceptance ----------------------------
 // Draft tokens come from the collection's table by id, or pre-gathered
 // cand_tokens [E][k][32] when non-null (sharded search records).

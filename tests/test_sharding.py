@@ -121,3 +121,39 @@ def test_nccl_sharded_search_single_rank():
     o2, t2 = H.verify_round_drafts(i, d, lg, vp)
     assert (o1 == o2).all()
     np.testing.assert_array_equal(t1.cpu().numpy(), t2.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_p2p_sharded_search_single_rank():
+    """Peer-memory exchange (publish + flag-synchronised merge, k_p2p.cu) at world 1, several epochs."""
+    col = H.Collection(DIM, capacity=N)
+    col.generate(O.REAL, SEED, N)
+    comm = H.Comm(None, 1, 0, 0)
+    try:
+        comm.p2p_import([comm.p2p_export(B, K)])
+        for ep in range(5):
+            q = H.gen_queries(O.REAL, 40 + ep, SEED, N, 0, B - ep, DIM)
+            s, i, d = comm.search_topk(col, 0, q, K)
+            full_s, full_i = col.search_topk_exact(q, K)
+            np.testing.assert_array_equal(i.cpu().numpy(), full_i.cpu().numpy())
+            np.testing.assert_array_equal(s.cpu().numpy(), full_s.cpu().numpy())
+            _, toks = col.keys_view()
+            np.testing.assert_array_equal(d.cpu().numpy(), toks[full_i.long()].cpu().numpy())
+        assert not comm.p2p_timed_out()
+    finally:
+        comm.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_exchange_multi_process(world):
+    """G processes exchange their top-k records through each other's IPC-mapped windows (one GPU)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = 29600 + world
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "tests", "p2p_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root)
+    assert "P2P_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
