@@ -73,6 +73,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=20)
     p.add_argument("--force-sharded", action="store_true",
                    help="use the sharded (NCCL all-gather + merge) step even at world size 1")
+    p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                   help="row-sharded DB: top-k records exchanged through peer memory (default) or an NCCL all-gather")
     p.add_argument("--shard", default="episodes", choices=["episodes", "db"],
                    help="N > 1: 'episodes' = every rank holds the DB and runs its own batch of independent episodes "
                         "(weak scaling, no collective on the data path); 'db' = the DB is row-sharded and every "
@@ -369,7 +371,9 @@ def config_of(args, world):
         "synthetic_family": "REAL" if args.kind == 1 else "EXACT",
         "parallelism": ("single" if world == 1 else
                         f"episode-shard{world} (DB replica per GPU, no collective)" if args.shard == "episodes"
-                        and not args.force_sharded else f"db-shard{world} (NCCL all-gather + merge)"),
+                        and not args.force_sharded else
+                        f"db-shard{world} ({'peer-memory' if args.exchange == 'p2p' else 'NCCL all-gather'} exchange + "
+                        f"merge)"),
         "l2": getattr(args, "l2_note", None) or
               f"inputs larger than L2 ({args.n * args.dim * (2 if args.dtype == 'bf16' or args.filter == 'bf16_copy' else 4) / 1e9:.1f} GB of keys "
               f"streamed per pass)",
@@ -438,7 +442,7 @@ def run_ours(args):
             eng.step(B, bufs[i % S], vp, gap_d=1, stream=stream, graph=args.graph)
         launches_per_step = 7  # K5, pad queries, K1, K2 (3 kernels), K4 — eager or as the nodes of one graph launch
     else:
-        comm = setup_comm(H, dist, world, rank, local)
+        comm = setup_comm(H, dist, world, rank, local, args.exchange, max_B=B, k_max=k)
         lo, hi = H.shard_range(B, world, rank)  # this rank's episodes
         sc = torch.empty((B, k), dtype=torch.float64, device=dev)
         Bl = hi - lo
@@ -594,7 +598,19 @@ def gen_logits_global(H, args, rows, local, col, b0, b1):
     return H.gen_logits(col, 3, r, args.L)
 
 
-def setup_comm(H, dist, world, rank, local):
+def setup_comm(H, dist, world, rank, local, exchange="p2p", max_B=1024, k_max=32):
+    """Communicator of a row-sharded DB.  exchange="p2p": the B x k records go
+    straight into every peer's IPC-mapped receive window (k_p2p.cu, no NCCL
+    launch); "nccl": an NCCL all-gather."""
+    if exchange == "p2p":
+        comm = H.Comm(None, world, rank, local)
+        h = comm.p2p_export(max_B, k_max)
+        handles = [h]
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, h)
+        comm.p2p_import(handles)
+        return comm
     if world == 1:
         return H.Comm(H.Comm.unique_id(), 1, 0, local)
     obj = [H.Comm.unique_id() if rank == 0 else None]
@@ -842,7 +858,7 @@ def run_c5(args):
     b0, b1 = H.shard_range(args.n, world, rank)
     col = H.Collection(args.dim, capacity=b1 - b0, device=local, dtype=args.dtype)
     col.generate(args.kind, 2026, b1 - b0, row0=b0, payload=H.PAYLOAD_TRAJ, traj_T=args.traj_T)
-    comm = setup_comm(H, dist, world, rank, local) if world > 1 else None
+    comm = setup_comm(H, dist, world, rank, local, args.exchange, max_B=1024, k_max=args.k_top) if world > 1 else None
     total_rounds = args.warmup + args.steps
     hp = H.hybrid_params(args.robots, k=args.k_top, traj_T=args.traj_T, d_f=args.d_f, seed=1, db_seed=2026,
                          key_kind=args.kind)
