@@ -248,8 +248,12 @@ struct StageMarks {
   cudaEvent_t after_select = nullptr;
 };
 
+// pub != nullptr: sharded search over peer memory — the final per-query
+// top-k records are published into the peers' windows by K2 (scores / ids
+// are then scratch for an empty shard only).
 hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, int64_t rb, int64_t re, double* scores,
-                       int32_t* ids, cudaStream_t s, const StageMarks* marks = nullptr, int reserve_sms = 0) {
+                       int32_t* ids, cudaStream_t s, const StageMarks* marks = nullptr, int reserve_sms = 0,
+                       const hsd::P2PPublish* pub = nullptr) {
   if (k < 1) return fail(HSD_ERR_INVALID_INPUT, "k must be >= 1");  // store.cpp:60
   if (k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k = %d exceeds HSD_K_MAX = %d", k, HSD_K_MAX);
   if (B < 0) return fail(HSD_ERR_INVALID_INPUT, "negative batch");
@@ -264,6 +268,7 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
     const int n = B * k;
     fill_empty_kernel<<<(n + 255) / 256, 256, 0, s>>>(scores, ids, n);
     CU(cudaGetLastError());
+    if (pub) CU(hsd::launch_p2p_publish(pub->w, pub->rank, pub->G, B, k, pub->epoch, scores, ids, nullptr, s));
     return HSD_OK;
   }
   // reserve_sms: SMs left free for work running concurrently on another stream
@@ -317,8 +322,14 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
       CU(hsd::launch_sim((const float*)c->keys, rb, re, c->dim, q, Bs, plan, sc->partial, s));
     }
     if (marks && marks->after_sim && b0 + W >= B) CU(cudaEventRecord(marks->after_sim, s));
+    hsd::P2PPublish pb{};
+    if (pub) {
+      pb = *pub;
+      pb.q_offset = b0;
+    }
     CU(hsd::launch_select(sc->partial, plan.lists, Bs, k, c->keys, c->dtype, c->dim, q, c->maxnorm, plan.gamma,
-                          scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->overflow, sc->sel, s));
+                          scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->overflow, sc->sel, s,
+                          pub ? &pb : nullptr));
   }
   if (marks && marks->after_select) CU(cudaEventRecord(marks->after_select, s));
   return HSD_OK;
@@ -1283,6 +1294,23 @@ hsd_status hsd_search_topk_sharded(hsd_collection* col, hsd_comm* cm, int64_t id
     CU(cudaMalloc(&cm->lt, need * HSD_TOKENS_STRIDE));
     cm->cap = need;
   }
+  if (cm->p2p) {  // local top-k whose K2 epilogue publishes into every peer's window, then the merge
+    if (B > cm->win.Bmax || k > cm->win.kmax)
+      return fail(HSD_ERR_INVALID_INPUT, "batch %d / k %d exceed the peer window (%d, %d)", B, k, cm->win.Bmax,
+                  cm->win.kmax);
+    ++cm->epoch;
+    hsd::P2PPublish pub{};
+    pub.w = cm->win;
+    pub.rank = cm->rank;
+    pub.G = cm->world;
+    pub.epoch = cm->epoch;
+    pub.id_offset = id_offset;
+    pub.tokens = col->tokens;
+    st = search_impl(col, queries, B, k, 0, col->n, cm->ls, cm->li, s, nullptr, 0, &pub);
+    if (st != HSD_OK) return st;
+    CU(hsd::launch_p2p_merge(cm->win, cm->rank, cm->world, B, k, cm->epoch, scores, ids, drafts, cm->err, s));
+    return HSD_OK;
+  }
   // local top-k over this rank's shard (K1 + K2), then the 32-B draft record
   st = search_impl(col, queries, B, k, 0, col->n, cm->ls, cm->li, s);
   if (st != HSD_OK) return st;
@@ -1290,15 +1318,6 @@ hsd_status hsd_search_topk_sharded(hsd_collection* col, hsd_comm* cm, int64_t id
   offset_ids_kernel<<<(int)((need + 255) / 256), 256, 0, s>>>(cm->li, (int)need, id_offset);
   CU(cudaGetLastError());
   // K3: exchange the B x k records over NVLink and merge (score desc, id asc)
-  if (cm->p2p) {  // peer-memory stores + flags, no NCCL launch
-    if (B > cm->win.Bmax || k > cm->win.kmax)
-      return fail(HSD_ERR_INVALID_INPUT, "batch %d / k %d exceed the peer window (%d, %d)", B, k, cm->win.Bmax,
-                  cm->win.kmax);
-    ++cm->epoch;
-    CU(hsd::launch_p2p_exchange(cm->win, cm->rank, cm->world, B, k, cm->epoch, cm->ls, cm->li, cm->lt, scores, ids,
-                                drafts, cm->err, s));
-    return HSD_OK;
-  }
   if (!cm->comm) return fail(HSD_ERR_INVALID_INPUT, "peer-memory communicator not imported (hsd_comm_p2p_import)");
   NC(ncclGroupStart());
   NC(ncclAllGather(cm->ls, cm->gs, need, ncclFloat64, cm->comm, s));

@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "hsd/hsd_synth.h"
 #include "kernels.h"
+#include "p2p.cuh"
 
 namespace hsd {
 namespace {
@@ -201,9 +202,13 @@ __global__ void __launch_bounds__(kRThreads) rescore_kernel(const KT* __restrict
 
 // K2c, one CTA per query: rank by (score desc, id asc) and emit the first k
 // (store.cpp:67-71).
+// With a publish descriptor (sharded search over peer memory) the final
+// records go straight into every peer's receive window — global id, fp64
+// score and the 32-byte draft tokens — followed by the per-query flag: the
+// local top-k and the exchange are one kernel.
 __global__ void __launch_bounds__(kThreads) rank_kernel(const SelScratch* __restrict__ scr, int k,
                                                         double* __restrict__ scores, int32_t* __restrict__ ids,
-                                                        int* __restrict__ overflow) {
+                                                        int* __restrict__ overflow, P2PPublish pub, int publish) {
   __shared__ double ex[kCandMax];
   __shared__ uint32_t id[kCandMax];
   const int b = blockIdx.x, tid = threadIdx.x;
@@ -223,13 +228,29 @@ __global__ void __launch_bounds__(kThreads) rank_kernel(const SelScratch* __rest
       rank += (x > s) || (x == s && id[c] < me);
     }
     if (rank < k) {
-      scores[(size_t)b * k + rank] = s;
-      ids[(size_t)b * k + rank] = (int32_t)me;
+      if (publish) {
+        const int qb = pub.q_offset + b;
+        for (int g = 0; g < pub.G; ++g)
+          p2p_put_record(pub.w, g, pub.rank, pub.G, qb, rank, pub.epoch, s, (int32_t)(me + pub.id_offset),
+                         pub.tokens + (size_t)me * HSD_TOKENS_STRIDE);
+      } else {
+        scores[(size_t)b * k + rank] = s;
+        ids[(size_t)b * k + rank] = (int32_t)me;
+      }
     }
   }
   for (int r = n + tid; r < k; r += kThreads) {
-    scores[(size_t)b * k + r] = -INFINITY;
-    ids[(size_t)b * k + r] = -1;
+    if (publish) {
+      for (int g = 0; g < pub.G; ++g)
+        p2p_put_record(pub.w, g, pub.rank, pub.G, pub.q_offset + b, r, pub.epoch, -INFINITY, -1, nullptr);
+    } else {
+      scores[(size_t)b * k + r] = -INFINITY;
+      ids[(size_t)b * k + r] = -1;
+    }
+  }
+  if (publish) {
+    __syncthreads();
+    if (tid < pub.G) p2p_put_flag(pub.w, tid, pub.rank, pub.G, pub.q_offset + b, pub.epoch);
   }
   if (tid == 0 && o.over) atomicAdd(overflow, 1);
 }
@@ -283,7 +304,7 @@ size_t select_scratch_bytes(int B) { return (size_t)B * sizeof(SelScratch); }
 
 cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const void* keys, int key_dtype, int dim,
                           const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
-                          int32_t* ids, int* overflow, void* scratch, cudaStream_t s) {
+                          int32_t* ids, int* overflow, void* scratch, cudaStream_t s, const P2PPublish* pub) {
   if (B <= 0) return cudaSuccess;
   if (key_dtype == HSD_DTYPE_BF16 && dim % 8) return cudaErrorInvalidValue;
   SelScratch* scr = reinterpret_cast<SelScratch*>(scratch);
@@ -297,7 +318,9 @@ cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, cons
     rescore_kernel<float><<<grid, kRThreads, 0, s>>>((const float*)keys, dim, queries, scr);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  rank_kernel<<<B, kThreads, 0, s>>>(scr, k, scores, ids, overflow);
+  P2PPublish pb{};
+  if (pub) pb = *pub;
+  rank_kernel<<<B, kThreads, 0, s>>>(scr, k, scores, ids, overflow, pb, pub ? 1 : 0);
   return cudaGetLastError();
 }
 

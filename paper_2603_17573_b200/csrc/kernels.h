@@ -72,9 +72,12 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
 // Three launches (candidates, rescoring over (query, 8-candidate) CTAs, rank);
 // scratch: select_scratch_bytes(B).
 size_t select_scratch_bytes(int B);
+// pub != nullptr: the rank kernel publishes the top-k records (global ids +
+// draft tokens) into every peer's window instead of writing scores / ids.
+struct P2PPublish;
 cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const void* keys, int key_dtype, int dim,
                           const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
-                          int32_t* ids, int* overflow, void* scratch, cudaStream_t s);
+                          int32_t* ids, int* overflow, void* scratch, cudaStream_t s, const P2PPublish* pub = nullptr);
 
 // K3 merge of G gathered per-rank top-k records (sharded search); tokens
 // [G][B][k][32] are permuted alongside when non-null.
@@ -91,10 +94,22 @@ struct P2PWindows {
   size_t off_flags, off_scores, off_ids, off_toks;
   int Bmax, kmax;
 };
+// Fused publish (K2's rank kernel writes its final records straight into the
+// peers' windows): what the rank kernel needs to do it.
+struct P2PPublish {
+  P2PWindows w;
+  int rank, G;
+  uint64_t epoch;
+  int64_t id_offset;      // local id -> global id
+  int q_offset;           // query index of this pass's first query
+  const uint8_t* tokens;  // local token table [n][32] (drafts travel with the records)
+};
 size_t p2p_window_bytes(int G, int Bmax, int kmax, P2PWindows* layout);
-cudaError_t launch_p2p_exchange(const P2PWindows& w, int rank, int G, int B, int k, uint64_t epoch,
-                                const double* ls, const int32_t* li, const uint8_t* lt, double* scores, int32_t* ids,
-                                uint8_t* tok, int* err, cudaStream_t s);
+// Standalone publish from local buffers (empty shards) + the flag-synchronised merge.
+cudaError_t launch_p2p_publish(const P2PWindows& w, int rank, int G, int B, int k, uint64_t epoch, const double* ls,
+                               const int32_t* li, const uint8_t* lt, cudaStream_t s);
+cudaError_t launch_p2p_merge(const P2PWindows& w, int rank, int G, int B, int k, uint64_t epoch, double* scores,
+                             int32_t* ids, uint8_t* tok, int* err, cudaStream_t s);
 
 // ---- K4 gather + verify-skip + relaxed acceptance ----------------------------
 // Draft tokens come from the collection's table by id, or pre-gathered

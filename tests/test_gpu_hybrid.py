@@ -87,13 +87,18 @@ def test_hybrid_relaxed_off_exact_family_and_k8(torch):
     compare(loop, hp, H.EXACT, 40)
 
 
-def test_hybrid_sharded_world1_equals_single(torch):
-    """The sharded retrieval path (NCCL all-gather + merge, world 1) gives the same loop."""
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+def test_hybrid_sharded_world1_equals_single(torch, exchange):
+    """The sharded retrieval path (NCCL all-gather or peer-memory publish + merge, world 1) gives the same loop."""
     col = make_db("bf16")
     hp = H.hybrid_params(32, k=3, traj_T=T, d_f=64, seed=4, db_seed=7)
     single = H.HybridLoop(col, hp, max_rounds=30)
     single.step(30)
-    comm = H.Comm(H.Comm.unique_id(), 1, 0, 0)
+    if exchange == "nccl":
+        comm = H.Comm(H.Comm.unique_id(), 1, 0, 0)
+    else:
+        comm = H.Comm(None, 1, 0, 0)
+        comm.p2p_import([comm.p2p_export(1024, 32)])
     sharded = H.HybridLoop(col, hp, max_rounds=30, comm=comm, n_total_rows=col.size())
     sharded.step(30)
     np.testing.assert_array_equal(single.positions(), sharded.positions())
