@@ -30,9 +30,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kPool = 512;
 constexpr int kCandMax = 256;   // rescored candidates per query
-constexpr int kPer = 8;         // candidates rescored per CTA of the rescoring kernel
-constexpr int kRThreads = 128;  // rescoring CTA: all threads stage rows, kPer run the fp64 chains
-constexpr int kW = 512;         // row chunk (elements) per staging buffer
+constexpr int kPer = 32;        // candidates rescored per CTA of the rescoring kernel (lanes of warp 0)
+constexpr int kRThreads = 128;  // rescoring CTA: all threads stage rows, warp 0 runs the fp64 chains
 
 __device__ __forceinline__ double widen(float x) { return (double)x; }
 __device__ __forceinline__ double widen(uint16_t b) { return (double)hsd_bf16_val(b); }  // bf16 key -> exact fp64
@@ -141,19 +140,35 @@ __global__ void __launch_bounds__(kThreads) select_cand_kernel(const uint64_t* _
 }
 
 // K2b, one CTA per (query, kPer candidates): exact rescoring in the
-// reference's order (store.cpp:32).  Rows stream through a double-buffered
-// cp.async ring of kW-element chunks (all 128 threads copy); kPer threads run
-// the sequential fp64 chain acc = fma(q_i, k_i, acc), i = 0..dim-1 — the fp32
-// (or bf16) x fp32 product is exact in fp64, so the fused form is
-// bit-identical to s += a[i]*b[i].
+// reference's order (store.cpp:32): acc = fma(q_i, k_i, acc), i = 0..dim-1, in
+// fp64 — the fp32 (or bf16) x fp32 product is exact in fp64, so the fused form
+// is bit-identical to s += a[i]*b[i].
+// Rows and the query stream through a double-buffered cp.async ring of
+// kW-element chunks (all 128 threads copy); the query chunk is widened to fp64
+// once per chunk CTA-wide; lane c of warp 0 runs candidate c's chain with the
+// operands of the next kPipe steps loaded ahead of the current kPipe DFMAs.
+// Shape (tools/rescore_lab.cu, config-2 shape, L2 flushed): 32 chains per CTA
+// run at 52 us where 8 chains per CTA took 90-110 us — the chain's per-step
+// F2F widening and DFMA are issued per warp instruction, so full warps of
+// chains cost 4x fewer issue slots per SM than quarter-filled ones.
+constexpr int kW = 256;    // elements per chunk
+constexpr int kPipe = 8;   // chain steps whose operands are loaded ahead
+
+template <typename KT>
+constexpr size_t rescore_smem() {
+  return sizeof(KT) * 2 * kPer * (kW + 16 / sizeof(KT)) + sizeof(float) * 2 * kW + sizeof(double) * kW;
+}
+
 template <typename KT>
 __global__ void __launch_bounds__(kRThreads) rescore_kernel(const KT* __restrict__ keys, int dim,
                                                             const float* __restrict__ queries,
                                                             SelScratch* __restrict__ scr) {
   constexpr int kPad = 16 / (int)sizeof(KT);
   constexpr int kStride = kW + kPad;
-  __shared__ __align__(16) KT rows[2][kPer][kStride];
-  __shared__ double qs[2][kW];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  auto& rows = *reinterpret_cast<KT(*)[2][kPer][kStride]>(smem_raw);
+  auto& qs = *reinterpret_cast<float(*)[2][kW]>(smem_raw + sizeof(KT) * 2 * kPer * kStride);
+  auto& qd = *reinterpret_cast<double(*)[kW]>(smem_raw + sizeof(KT) * 2 * kPer * kStride + sizeof(float) * 2 * kW);
   __shared__ uint32_t ids[kPer];
   const int b = blockIdx.x, c0 = blockIdx.y * kPer;
   SelScratch& o = scr[b];
@@ -170,12 +185,18 @@ __global__ void __launch_bounds__(kRThreads) rescore_kernel(const KT* __restrict
     for (int i = tid; i < n * v16; i += kRThreads) {
       const int c = i / v16, j16 = i - c * v16;
       const int col = cbase + j16 * kPad;
-      const KT* src = keys + (size_t)ids[c] * dim + col;
       const uint32_t d = (uint32_t)__cvta_generic_to_shared(&rows[ch & 1][c][j16 * kPad]);
       const int bytes = col < dim ? 16 : 0;  // dim is a multiple of kPad; zero-fill past the end
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(keys + (size_t)ids[c] * dim + col),
+                   "r"(bytes)
+                   : "memory");
     }
-    for (int j = tid; j < kW; j += kRThreads) qs[ch & 1][j] = cbase + j < dim ? (double)qrow[cbase + j] : 0.0;
+    for (int j4 = tid; j4 < kW / 4; j4 += kRThreads) {
+      const int col = cbase + j4 * 4;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&qs[ch & 1][j4 * 4]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(qrow + col), "r"(col < dim ? 16 : 0)
+                   : "memory");
+    }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   double acc = 0.0;
@@ -188,12 +209,38 @@ __global__ void __launch_bounds__(kRThreads) rescore_kernel(const KT* __restrict
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
-    const int w = dim - ch * kW < kW ? dim - ch * kW : kW;
+    for (int j = tid; j < kW; j += kRThreads) qd[j] = (double)qs[ch & 1][j];
+    __syncthreads();
+    const int w = min(dim - ch * kW, kW);
     if (tid < n) {
       const KT* r = rows[ch & 1][tid];
-      const double* qc = qs[ch & 1];
+      if (w == kW) {
+        double qa[kPipe], ra[kPipe];
+#pragma unroll
+        for (int u = 0; u < kPipe; ++u) {
+          qa[u] = qd[u];
+          ra[u] = widen(r[u]);
+        }
+        for (int j = 0; j < kW; j += kPipe) {
+          double qb[kPipe], rb[kPipe];
+          const int jn = j + kPipe < kW ? j + kPipe : j;
+#pragma unroll
+          for (int u = 0; u < kPipe; ++u) {
+            qb[u] = qd[jn + u];
+            rb[u] = widen(r[jn + u]);
+          }
+#pragma unroll
+          for (int u = 0; u < kPipe; ++u) acc = __fma_rn(qa[u], ra[u], acc);
+#pragma unroll
+          for (int u = 0; u < kPipe; ++u) {
+            qa[u] = qb[u];
+            ra[u] = rb[u];
+          }
+        }
+      } else {
 #pragma unroll 16
-      for (int j = 0; j < w; ++j) acc = __fma_rn(qc[j], widen(r[j]), acc);
+        for (int j = 0; j < w; ++j) acc = __fma_rn(qd[j], widen(r[j]), acc);
+      }
     }
     __syncthreads();
   }
@@ -312,10 +359,20 @@ cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, cons
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const dim3 grid(B, kCandMax / kPer);
+  // the kernel's occupancy is set by shared memory: ask for the full carveout
+  const size_t sm16 = rescore_smem<uint16_t>(), sm32 = rescore_smem<float>();
+  static const bool carve = [&] {
+    cudaFuncSetAttribute(rescore_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm16);
+    cudaFuncSetAttribute(rescore_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32);
+    cudaFuncSetAttribute(rescore_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(rescore_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return true;
+  }();
+  (void)carve;
   if (key_dtype == HSD_DTYPE_BF16)
-    rescore_kernel<uint16_t><<<grid, kRThreads, 0, s>>>((const uint16_t*)keys, dim, queries, scr);
+    rescore_kernel<uint16_t><<<grid, kRThreads, sm16, s>>>((const uint16_t*)keys, dim, queries, scr);
   else
-    rescore_kernel<float><<<grid, kRThreads, 0, s>>>((const float*)keys, dim, queries, scr);
+    rescore_kernel<float><<<grid, kRThreads, sm32, s>>>((const float*)keys, dim, queries, scr);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   P2PPublish pb{};

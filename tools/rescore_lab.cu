@@ -1,0 +1,341 @@
+// Lab for K2's exact rescoring (k_select.cu rescore_kernel): the same
+// workload shape as config 2 (64 queries x ~84 margin candidates x 4096-d
+// fp32 rows gathered from a DB larger than L2), several kernel variants,
+// bit-equality checked against variant 0, device-timed with L2 flushed
+// between launches.  Build + run:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/rl tools/rescore_lab.cu && /tmp/rl
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+#include <random>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); exit(1); } } while (0)
+
+constexpr int kCandMax = 256;
+struct Scr { uint32_t id[kCandMax]; double exact[kCandMax]; int n; int over; };
+
+// ---- V0: two-stage cp.async ring, 8 chains per 128-thread CTA, all threads stage ----
+template <int kPer, int kW, int kPipe = 0, int kThr = 128, int kMode = 0>
+__global__ void __launch_bounds__(kThr) v_ring(const float* __restrict__ keys, int dim, const float* __restrict__ queries, Scr* scr) {
+  constexpr int kStride = kW + 4;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  auto& rows = *reinterpret_cast<float(*)[2][kPer][kStride]>(smem_raw);
+  auto& qs = *reinterpret_cast<float(*)[2][kW]>(smem_raw + 4 * 2 * kPer * kStride);
+  auto& qd = *reinterpret_cast<double(*)[kW]>(smem_raw + 4 * 2 * kPer * kStride + 4 * 2 * kW);
+  __shared__ uint32_t ids[kPer];
+  const int b = blockIdx.x, c0 = blockIdx.y * kPer;
+  Scr& o = scr[b];
+  const int n = min(o.n - c0, kPer);
+  if (n <= 0) return;
+  const int tid = threadIdx.x;
+  if (tid < n) ids[tid] = o.id[c0 + tid];
+  __syncthreads();
+  const float* qrow = queries + (size_t)b * dim;
+  const int nchunk = (dim + kW - 1) / kW;
+  constexpr int v16 = kW / 4;
+  auto issue = [&](int ch) {
+    const int cbase = ch * kW;
+    if (kMode == 1) { asm volatile("cp.async.commit_group;" ::: "memory"); return; }
+    for (int i = tid; i < n * v16; i += kThr) {
+      const int c = i / v16, j16 = i - c * v16;
+      const int col = cbase + j16 * 4;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&rows[ch & 1][c][j16 * 4]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(keys + (size_t)ids[c] * dim + col), "r"(col < dim ? 16 : 0) : "memory");
+    }
+    for (int j4 = tid; j4 < kW / 4; j4 += kThr) {
+      const int col = cbase + j4 * 4;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&qs[ch & 1][j4 * 4]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(qrow + col), "r"(col < dim ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc = 0.0;
+  issue(0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    if (ch + 1 < nchunk) { issue(ch + 1); asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    for (int j = tid; j < kW; j += kThr) qd[j] = (double)qs[ch & 1][j];
+    __syncthreads();
+    const int w = min(dim - ch * kW, kW);
+    if (kMode == 2) { if (tid < n) acc += rows[ch & 1][tid][ch]; }
+    else if (tid < n) {
+      const float* r = rows[ch & 1][tid];
+      if (kPipe > 0 && w == kW) {
+        constexpr int P = kPipe > 0 ? kPipe : 1;
+        double qa[P], ra[P];
+#pragma unroll
+        for (int u = 0; u < P; ++u) { qa[u] = qd[u]; ra[u] = (double)r[u]; }
+        for (int j = 0; j < kW; j += P) {
+          double qb[P], rb[P];
+          const int jn = j + P < kW ? j + P : j;
+#pragma unroll
+          for (int u = 0; u < P; ++u) { qb[u] = qd[jn + u]; rb[u] = (double)r[jn + u]; }
+#pragma unroll
+          for (int u = 0; u < P; ++u) acc = __fma_rn(qa[u], ra[u], acc);
+#pragma unroll
+          for (int u = 0; u < P; ++u) { qa[u] = qb[u]; ra[u] = rb[u]; }
+        }
+      } else {
+#pragma unroll 16
+        for (int j = 0; j < w; ++j) acc = __fma_rn(qd[j], (double)r[j], acc);
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < n) o.exact[c0 + tid] = acc;
+}
+
+// ---- V1: warp-specialised (warp 0 chains, others stage + widen), register-pipelined chain ----
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int kPer, int kThr, int kW, int kPipe, int kStages>
+__global__ void __launch_bounds__(kThr) v_ws(const float* __restrict__ keys, int dim, const float* __restrict__ queries, Scr* scr) {
+  constexpr int kStride = kW + 4;
+  constexpr int kRdStride = kW + 1;
+  constexpr int kProd = kThr - 32;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  auto& rd = *reinterpret_cast<double(*)[kStages][kPer][kRdStride]>(smem_raw);
+  auto& qd = *reinterpret_cast<double(*)[kStages][kW]>(smem_raw + 8 * kStages * kPer * kRdStride);
+  auto& rows = *reinterpret_cast<float(*)[2][kPer][kStride]>(smem_raw + 8 * kStages * (kPer * kRdStride + kW));
+  auto& qs = *reinterpret_cast<float(*)[2][kW]>(smem_raw + 8 * kStages * (kPer * kRdStride + kW) + 4 * 2 * kPer * kStride);
+  __shared__ uint32_t ids[kPer];
+  const int b = blockIdx.x, c0 = blockIdx.y * kPer;
+  Scr& o = scr[b];
+  const int n = min(o.n - c0, kPer);
+  if (n <= 0) return;
+  const int tid = threadIdx.x;
+  if (tid < n) ids[tid] = o.id[c0 + tid];
+  __syncthreads();
+  const int nchunk = (dim + kW - 1) / kW;
+  if (tid < 32) {
+    double acc = 0.0;
+    for (int ch = 0; ch < nchunk; ++ch) {
+      const int st = ch % kStages;
+      named_sync(2 + st, kThr);
+      const int w = min(dim - ch * kW, kW);
+      if (tid < n) {
+        const double* r = rd[st][tid];
+        const double* q = qd[st];
+        if (kPipe > 0 && w == kW) {
+          constexpr int P = kPipe > 0 ? kPipe : 1;
+          double qa[P], ra[P];
+#pragma unroll
+          for (int u = 0; u < P; ++u) { qa[u] = q[u]; ra[u] = r[u]; }
+          for (int j = 0; j < kW; j += P) {
+            double qb[P], rb[P];
+            const int jn = j + P < kW ? j + P : j;
+#pragma unroll
+            for (int u = 0; u < P; ++u) { qb[u] = q[jn + u]; rb[u] = r[jn + u]; }
+#pragma unroll
+            for (int u = 0; u < P; ++u) acc = __fma_rn(qa[u], ra[u], acc);
+#pragma unroll
+            for (int u = 0; u < P; ++u) { qa[u] = qb[u]; ra[u] = rb[u]; }
+          }
+        } else {
+#pragma unroll 16
+          for (int j = 0; j < w; ++j) acc = __fma_rn(q[j], r[j], acc);
+        }
+      }
+      if (ch + kStages < nchunk) named_arrive(2 + kStages + st, kThr);
+    }
+    if (tid < n) o.exact[c0 + tid] = acc;
+    return;
+  }
+  const int p = tid - 32;
+  const float* qrow = queries + (size_t)b * dim;
+  constexpr int v16 = kW / 4;
+  auto issue = [&](int ch) {
+    if (ch < nchunk) {
+      const int cbase = ch * kW;
+      for (int i = p; i < n * v16; i += kProd) {
+        const int c = i / v16, j16 = i - c * v16;
+        const int col = cbase + j16 * 4;
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(&rows[ch & 1][c][j16 * 4]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(keys + (size_t)ids[c] * dim + col), "r"(col < dim ? 16 : 0) : "memory");
+      }
+      for (int j4 = p; j4 < kW / 4; j4 += kProd) {
+        const int col = cbase + j4 * 4;
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(&qs[ch & 1][j4 * 4]);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(qrow + col), "r"(col < dim ? 16 : 0) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(0);
+  issue(1);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    const int st = ch % kStages, sg = ch & 1;
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    named_sync(1, kProd);
+    if (ch >= kStages) named_sync(2 + kStages + st, kThr);
+    constexpr int kV = kW / 4;
+    for (int i = p; i < (kPer + 1) * kV; i += kProd) {
+      const int c = i / kV, j = (i % kV) * 4;
+      if (c < kPer) {
+        if (c < n) {
+          const float4 f = *reinterpret_cast<const float4*>(&rows[sg][c][j]);
+          double* d = &rd[st][c][j];
+          d[0] = f.x; d[1] = f.y; d[2] = f.z; d[3] = f.w;
+        }
+      } else {
+        const float4 f = *reinterpret_cast<const float4*>(&qs[sg][j]);
+        double* d = &qd[st][j];
+        d[0] = f.x; d[1] = f.y; d[2] = f.z; d[3] = f.w;
+      }
+    }
+    named_sync(1, kProd);
+    issue(ch + 2);
+    named_arrive(2 + st, kThr);
+  }
+}
+
+// ---- V2: chain lanes read the float rows and widen with integer ops (no F2F on the chain) ----
+// exact float->double for normal numbers and zeros; denormal / inf / nan fall back to F2F
+__device__ __forceinline__ double widen_int(float x) {
+  const uint32_t u = __float_as_uint(x);
+  const uint32_t e = u & 0x7f800000u;
+  if (e == 0u || e == 0x7f800000u) return (double)x;
+  const uint32_t hi = (u & 0x80000000u) | (((u & 0x7fffffffu) >> 3) + 0x38000000u);
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+
+template <int kPer, int kW>
+__global__ void __launch_bounds__(128) v_int(const float* __restrict__ keys, int dim, const float* __restrict__ queries, Scr* scr) {
+  constexpr int kStride = kW + 4;
+  __shared__ __align__(16) float rows[2][kPer][kStride];
+  __shared__ __align__(16) float qs[2][kW];
+  __shared__ uint32_t ids[kPer];
+  const int b = blockIdx.x, c0 = blockIdx.y * kPer;
+  Scr& o = scr[b];
+  const int n = min(o.n - c0, kPer);
+  if (n <= 0) return;
+  const int tid = threadIdx.x;
+  if (tid < n) ids[tid] = o.id[c0 + tid];
+  __syncthreads();
+  const float* qrow = queries + (size_t)b * dim;
+  const int nchunk = (dim + kW - 1) / kW;
+  constexpr int v16 = kW / 4;
+  auto issue = [&](int ch) {
+    const int cbase = ch * kW;
+    for (int i = tid; i < n * v16; i += 128) {
+      const int c = i / v16, j16 = i - c * v16;
+      const int col = cbase + j16 * 4;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&rows[ch & 1][c][j16 * 4]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(keys + (size_t)ids[c] * dim + col), "r"(col < dim ? 16 : 0) : "memory");
+    }
+    for (int j4 = tid; j4 < kW / 4; j4 += 128) {
+      const int col = cbase + j4 * 4;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&qs[ch & 1][j4 * 4]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(qrow + col), "r"(col < dim ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc = 0.0;
+  issue(0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    if (ch + 1 < nchunk) { issue(ch + 1); asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const int w = min(dim - ch * kW, kW);
+    if (tid < n) {
+      const float* r = rows[ch & 1][tid];
+      const float* q = qs[ch & 1];
+#pragma unroll 16
+      for (int j = 0; j < w; ++j) acc = __fma_rn(widen_int(q[j]), widen_int(r[j]), acc);
+    }
+    __syncthreads();
+  }
+  if (tid < n) o.exact[c0 + tid] = acc;
+}
+
+__global__ void flush(float* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] += 1.f;
+}
+
+int main(int argc, char** argv) {
+  const int B = 64, dim = 4096;
+  const size_t N = 250000;  // 4.1 GB of fp32 rows
+  std::mt19937_64 rng(7);
+  std::vector<float> hk(N * dim);
+  std::normal_distribution<float> nd(0.f, 1.f);
+  for (size_t i = 0; i < hk.size(); i += 1) hk[i] = nd(rng);
+  std::vector<float> hq((size_t)B * dim);
+  for (auto& x : hq) x = nd(rng);
+  std::vector<Scr> hs(B);
+  std::uniform_int_distribution<int> nc(40, 163);
+  for (int b = 0; b < B; ++b) {
+    hs[b].n = nc(rng);
+    for (int c = 0; c < hs[b].n; ++c) hs[b].id[c] = (uint32_t)(rng() % N);
+  }
+  float *dk, *dq, *dfl;
+  Scr* ds;
+  CK(cudaMalloc(&dk, N * dim * 4));
+  CK(cudaMalloc(&dq, (size_t)B * dim * 4));
+  CK(cudaMalloc(&ds, B * sizeof(Scr)));
+  const size_t nfl = 64ull << 20;  // 256 MB
+  CK(cudaMalloc(&dfl, nfl * 4));
+  CK(cudaMemcpy(dk, hk.data(), N * dim * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dq, hq.data(), (size_t)B * dim * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ds, hs.data(), B * sizeof(Scr), cudaMemcpyHostToDevice));
+  std::vector<double> ref;
+  auto run = [&](const char* name, auto launch) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float tot = 0.f;
+    const int it = 20;
+    for (int i = 0; i < it + 3; ++i) {
+      flush<<<1184, 256>>>(dfl, nfl);
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (i >= 3) tot += ms;
+    }
+    CK(cudaGetLastError());
+    std::vector<Scr> out(B);
+    CK(cudaMemcpy(out.data(), ds, B * sizeof(Scr), cudaMemcpyDeviceToHost));
+    std::vector<double> v;
+    for (int b = 0; b < B; ++b) for (int c = 0; c < out[b].n; ++c) v.push_back(out[b].exact[c]);
+    bool same = true;
+    if (ref.empty()) ref = v; else for (size_t i = 0; i < v.size(); ++i) same &= (v[i] == ref[i]);
+    printf("%-40s %8.1f us  %s\n", name, 1000.f * tot / it, same ? "bit-equal" : "MISMATCH");
+  };
+#define RINGM(P, W, PIPE, T, M)                                                                        \
+  {                                                                                                      \
+    auto k = v_ring<P, W, PIPE, T, M>;                                                                   \
+    const int sm = 4 * 2 * P * (W + 4) + 4 * 2 * W + 8 * W;                                              \
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                        \
+    run("v_ring<" #P "," #W ",pipe" #PIPE ",thr" #T ",mode" #M ">", [&] { k<<<dim3(B, kCandMax / P), T, sm>>>(dk, dim, dq, ds); }); \
+  }
+#define RING(P, W, PIPE, T)                                                                           \
+  {                                                                                                      \
+    auto k = v_ring<P, W, PIPE, T>;                                                                      \
+    const int sm = 4 * 2 * P * (W + 4) + 4 * 2 * W + 8 * W;                                              \
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                        \
+    run("v_ring<" #P "," #W ",pipe" #PIPE ",thr" #T ">", [&] { k<<<dim3(B, kCandMax / P), T, sm>>>(dk, dim, dq, ds); }); \
+  }
+  RING(32, 256, 8, 128)
+  RINGM(32, 256, 8, 128, 1)
+  RINGM(32, 256, 8, 128, 2)
+  RINGM(8, 512, 0, 128, 1)
+  RINGM(8, 512, 0, 128, 2)
+  RING(24, 256, 8, 128)
+  RING(24, 256, 4, 128)
+  RING(24, 256, 4, 256)
+  run("v_int<32,128>", [&] { v_int<32, 128><<<dim3(B, kCandMax / 32), 128>>>(dk, dim, dq, ds); });
+#define WS(P, T, W, PIPE, S)                                                                                     \
+  {                                                                                                              \
+    auto k = v_ws<P, T, W, PIPE, S>;                                                                             \
+    const int sm = 8 * S * (P * (W + 1) + W) + 4 * 2 * P * (W + 4) + 4 * 2 * W;                                 \
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                                \
+    run("v_ws<" #P "," #T "," #W ",pipe" #PIPE ",st" #S ">", [&] { k<<<dim3(B, kCandMax / P), T, sm>>>(dk, dim, dq, ds); }); \
+  }
+
+  return 0;
+}
