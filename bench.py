@@ -440,7 +440,8 @@ def run_ours(args):
 
         def step(i):
             eng.step(B, bufs[i % S], vp, gap_d=1, stream=stream, graph=args.graph)
-        launches_per_step = 7  # K5, pad queries, K1, K2 (3 kernels), K4 — eager or as the nodes of one graph launch
+        # K5 + skip similarity (side stream), pad queries, K1, K2 (3 kernels), K4 — eager or as one graph's nodes
+        launches_per_step = 8
     else:
         comm = setup_comm(H, dist, world, rank, local, args.exchange, max_B=B, k_max=k)
         lo, hi = H.shard_range(B, world, rank)  # this rank's episodes

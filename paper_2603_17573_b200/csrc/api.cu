@@ -676,7 +676,7 @@ hsd_status device_params(int device, const hsd_verify_params* params, int P, cud
 static hsd_status verify_impl(int device, hsd_collection* c, const uint8_t* drafts, const int32_t* ids, int E, int k,
                               int L, const float* logits, const float* feat_now, const float* feat_prev, int d_f,
                               const int32_t* history, int gap_d, const hsd_verify_params* params, int P,
-                              hsd_outcome* out, uint8_t* tokens, void* stream) {
+                              hsd_outcome* out, uint8_t* tokens, void* stream, const double* cos_in = nullptr) {
   if (L != 7 && L != 21) return fail(HSD_ERR_INVALID_INPUT, "draft length must be 7 or 21, got %d", L);
   if (k < 1 || k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k must be in [1, %d]", HSD_K_MAX);
   if (E < 0) return fail(HSD_ERR_INVALID_INPUT, "negative episode count");
@@ -694,7 +694,7 @@ static hsd_status verify_impl(int device, hsd_collection* c, const uint8_t* draf
   st = device_params(device, params, P, (cudaStream_t)stream, &dp);
   if (st != HSD_OK) return st;
   CU(hsd::launch_verify(ids, E, k, L, c ? c->tokens : nullptr, drafts, logits, feat_now, feat_prev, d_f, history, gap_d, dp, P,
-                        need_cos, out, tokens, (cudaStream_t)stream));
+                        need_cos, out, tokens, (cudaStream_t)stream, cos_in));
   return HSD_OK;
 }
 
@@ -822,8 +822,9 @@ struct hsd_engine {
   // [2] after select, [3] end (verify + join), [4]/[5] kinematics on the side stream
   std::vector<cudaEvent_t> ev;
   int max_steps = 0, recorded = 0;
-  cudaStream_t side = nullptr;  // K5 runs concurrently with K1
+  cudaStream_t side = nullptr;  // K5 and the verify-skip similarity run concurrently with K1
   cudaEvent_t fork = nullptr, join = nullptr;
+  double* cos = nullptr;  // [max_B] should_skip similarity, computed on the side stream
 };
 
 static constexpr int kStepEvents = 6;
@@ -866,6 +867,7 @@ hsd_status hsd_engine_create(hsd_collection* c, int max_B, int k, int L, int d_f
     for (cudaEvent_t* ev : {&S.uploaded, &S.computed, &S.downloaded})
       if (r == cudaSuccess) r = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
   }
+  alloc(&e->cos, (size_t)max_B * 8);
   if (r == cudaSuccess) r = cudaStreamCreateWithFlags(&e->up, cudaStreamNonBlocking);
   if (r == cudaSuccess) r = cudaStreamCreateWithFlags(&e->down, cudaStreamNonBlocking);
   if (r != cudaSuccess) {
@@ -917,6 +919,7 @@ hsd_status hsd_engine_destroy(hsd_engine* e) {
   if (!e) return HSD_OK;
   cudaSetDevice(e->c->device);
   for (cudaEvent_t x : e->ev) cudaEventDestroy(x);
+  cudaFree(e->cos);
   if (e->side) {
     cudaStreamSynchronize(e->side);
     cudaStreamDestroy(e->side);
@@ -948,9 +951,13 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
   cudaStream_t s = (cudaStream_t)stream;
   cudaEvent_t* ev = (e->recorded < e->max_steps) ? &e->ev[(size_t)e->recorded * kStepEvents] : nullptr;
   if (ev) CU(cudaEventRecord(ev[0], s));
-  if (io->xyz) {
-    // K5 (hybrid boundary, decide_sd) is independent of the retrieval: run it on
-    // a side stream so its latency-bound Gauss-Newton loop hides under K1.
+  // K5 (hybrid boundary, decide_sd) and should_skip's similarity do not depend
+  // on the retrieval: run them on a side stream so they hide under K1 (K5's
+  // Gauss-Newton loop is latency-bound; the similarity would otherwise be a
+  // serial feature stream inside K4 after K2).
+  const bool cos_side = vp->skip_enabled && e->d_f > 0 && io->feat_now && io->feat_prev;
+  const bool use_side = io->xyz || cos_side;
+  if (use_side) {
     if (!e->side) {
       CU(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
       CU(cudaEventCreateWithFlags(&e->fork, cudaEventDisableTiming));
@@ -959,9 +966,12 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
     CU(cudaEventRecord(e->fork, s));
     CU(cudaStreamWaitEvent(e->side, e->fork, 0));
     if (ev) CU(cudaEventRecord(ev[4], e->side));
-    st = hsd_window_features(e->c->device, io->xyz, B, mp, nb, io->history, io->R, io->D, io->F, io->decision,
-                             e->side);
-    if (st != HSD_OK) return st;
+    if (cos_side) CU(hsd::launch_cos(io->feat_now, io->feat_prev, B, e->d_f, e->cos, e->side));
+    if (io->xyz) {
+      st = hsd_window_features(e->c->device, io->xyz, B, mp, nb, io->history, io->R, io->D, io->F, io->decision,
+                               e->side);
+      if (st != HSD_OK) return st;
+    }
     if (ev) CU(cudaEventRecord(ev[5], e->side));
     CU(cudaEventRecord(e->join, e->side));
   }
@@ -974,12 +984,13 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
   st = search_impl(e->c, io->queries, B, e->k, 0, e->c->n, io->scores, io->ids, s, ev ? &marks : nullptr,
                    k5_blocks);  // K1+K2
   if (st != HSD_OK) return st;
-  st = hsd_verify_round(e->c, io->ids, B, e->k, e->L, io->logits, io->feat_now, io->feat_prev, e->d_f, io->history,
-                        gap_d, vp, 1, io->out, io->tokens, stream);  // K4
+  if (use_side) CU(cudaStreamWaitEvent(s, e->join, 0));
+  st = verify_impl(e->c->device, e->c, nullptr, io->ids, B, e->k, e->L, io->logits, io->feat_now, io->feat_prev,
+                   e->d_f, io->history, gap_d, vp, 1, io->out, io->tokens, stream,
+                   cos_side ? e->cos : nullptr);  // K4
   if (st != HSD_OK) return st;
-  if (io->xyz) CU(cudaStreamWaitEvent(s, e->join, 0));
   if (ev) {
-    if (!io->xyz) {
+    if (!use_side) {
       CU(cudaEventRecord(ev[4], s));
       CU(cudaEventRecord(ev[5], s));
     }

@@ -16,6 +16,8 @@
 #include "common.cuh"
 #include "hsd/hsd_synth.h"
 #include "kernels.h"
+
+#include <atomic>
 #include "p2p.cuh"
 
 namespace hsd {
@@ -361,14 +363,21 @@ cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, cons
   const dim3 grid(B, kCandMax / kPer);
   // the kernel's occupancy is set by shared memory: ask for the full carveout
   const size_t sm16 = rescore_smem<uint16_t>(), sm32 = rescore_smem<float>();
-  static const bool carve = [&] {
-    cudaFuncSetAttribute(rescore_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm16);
-    cudaFuncSetAttribute(rescore_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32);
-    cudaFuncSetAttribute(rescore_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(rescore_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    return true;
-  }();
-  (void)carve;
+  // function attributes are per device: set them once for each device used
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !(configured.load() >> dev & 1)) {
+    e = cudaFuncSetAttribute(rescore_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm16);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(rescore_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(rescore_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(rescore_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    configured.fetch_or(1ull << dev);
+  }
   if (key_dtype == HSD_DTYPE_BF16)
     rescore_kernel<uint16_t><<<grid, kRThreads, sm16, s>>>((const uint16_t*)keys, dim, queries, scr);
   else

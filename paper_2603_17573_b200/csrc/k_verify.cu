@@ -24,7 +24,7 @@
 namespace hsd {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 64;  // 2 warps (episodes) per CTA: finer CTAs balance C3's 4096 episodes over 148 SMs
 constexpr int kWarps = kThreads / 32;
 constexpr int kTokStride = 24;  // bytes per candidate row in shared memory
 constexpr int kPairs = 256;     // (parameter set, candidate) pairs per warp per chunk
@@ -71,8 +71,8 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
                                                const float* fnE, const float* fpE, int d_f,
                                                const int32_t* __restrict__ history, int gap_d,
                                                const hsd_verify_params* __restrict__ params, int P, int need_cos,
-                                               hsd_outcome* __restrict__ out, uint8_t* __restrict__ tok_out,
-                                               WarpScratch& W) {
+                                               const double* __restrict__ cos_in, hsd_outcome* __restrict__ out,
+                                               uint8_t* __restrict__ tok_out, WarpScratch& W) {
   const int lane = threadIdx.x & 31;
   // ---- greedy tokens: argmax per position, lowest index on ties.  The 7
   //      positions of an action slice are loaded before any is reduced (7 KB
@@ -113,7 +113,9 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
   //      result is the exact sum rounded once, so the order is free and
   //      kFeatUnroll float4 pairs per lane are loaded before they are accumulated)
   double cosv = -2.0;
-  if (need_cos && fnE && fpE) {
+  if (need_cos && cos_in) {
+    cosv = cos_in[e];  // computed by cos_kernel (off the critical path in the engine step)
+  } else if (need_cos && fnE && fpE) {
     const float4* a4 = reinterpret_cast<const float4*>(fnE);
     const float4* b4 = reinterpret_cast<const float4*>(fpE);
     const int n4 = d_f / 4;
@@ -335,7 +337,7 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __restrict__ ids, int E, int k, int L,
+__global__ void __launch_bounds__(kThreads, 1024 / kThreads) verify_kernel(const int32_t* __restrict__ ids, int E, int k, int L,
                                                              const uint8_t* __restrict__ tokens,
                                                              const uint8_t* __restrict__ cand_tokens,
                                                              const float* __restrict__ logits,
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
                                                              const float* __restrict__ feat_prev, int d_f,
                                                              const int32_t* __restrict__ history, int gap_d,
                                                              const hsd_verify_params* __restrict__ params, int P,
-                                                             int need_cos, hsd_outcome* __restrict__ out,
+                                                             int need_cos, const double* __restrict__ cos_in,
+                                                             hsd_outcome* __restrict__ out,
                                                              uint8_t* __restrict__ tok_out) {
   __shared__ WarpScratch sw[kWarps];
   const int warp = threadIdx.x >> 5;
@@ -351,19 +354,93 @@ __global__ void __launch_bounds__(kThreads, 4) verify_kernel(const int32_t* __re
   if (e >= E) return;
   verify_episode(e, E, k, L, ids, tokens, cand_tokens, logits + (size_t)e * L * 256,
                  feat_now ? feat_now + (size_t)e * d_f : nullptr, feat_prev ? feat_prev + (size_t)e * d_f : nullptr,
-                 d_f, history, gap_d, params, P, need_cos, out, tok_out, sw[warp]);
+                 d_f, history, gap_d, params, P, need_cos, cos_in, out, tok_out, sw[warp]);
+}
+
+// should_skip's similarity for every episode as its own pass: one CTA per
+// episode, all 2 x d_f x 4 bytes in flight at once (8 float4 pairs per thread
+// at d_f = 4096) instead of one warp's serial round trips.  Same exactly
+// rounded double-double sum as verify_episode, so either path gives the same
+// bits.
+constexpr int kCosThreads = 128;
+constexpr int kCosUnroll = 8;
+
+__global__ void __launch_bounds__(kCosThreads) cos_kernel(const float* __restrict__ feat_now,
+                                                          const float* __restrict__ feat_prev, int d_f,
+                                                          double* __restrict__ cos_out) {
+  const int e = blockIdx.x;
+  const float4* a4 = reinterpret_cast<const float4*>(feat_now + (size_t)e * d_f);
+  const float4* b4 = reinterpret_cast<const float4*>(feat_prev + (size_t)e * d_f);
+  const int n4 = d_f / 4;
+  double hi = 0.0, lo = 0.0;
+  for (int t0 = threadIdx.x; t0 < n4; t0 += kCosThreads * kCosUnroll) {
+    float4 xa[kCosUnroll], yb[kCosUnroll];
+#pragma unroll
+    for (int u = 0; u < kCosUnroll; ++u) {
+      const int t = t0 + kCosThreads * u;
+      xa[u] = t < n4 ? __ldcs(a4 + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+      yb[u] = t < n4 ? __ldcs(b4 + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kCosUnroll; ++u) {
+      const double pr[4] = {(double)xa[u].x * (double)yb[u].x, (double)xa[u].y * (double)yb[u].y,
+                            (double)xa[u].z * (double)yb[u].z, (double)xa[u].w * (double)yb[u].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double sm, er;
+        dev::two_sum(hi, pr[i], sm, er);
+        hi = sm;
+        lo = __dadd_rn(lo, er);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+    const double olo = __shfl_xor_sync(0xffffffffu, lo, o);
+    double sm, er;
+    dev::two_sum(hi, ohi, sm, er);
+    hi = sm;
+    lo = __dadd_rn(__dadd_rn(lo, olo), er);
+  }
+  __shared__ double rh[kCosThreads / 32], rl[kCosThreads / 32];
+  if ((threadIdx.x & 31) == 0) {
+    rh[threadIdx.x >> 5] = hi;
+    rl[threadIdx.x >> 5] = lo;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    hi = rh[0];
+    lo = rl[0];
+    for (int w = 1; w < kCosThreads / 32; ++w) {
+      double sm, er;
+      dev::two_sum(hi, rh[w], sm, er);
+      hi = sm;
+      lo = __dadd_rn(__dadd_rn(lo, rl[w]), er);
+    }
+    double sm, er;
+    dev::two_sum(hi, lo, sm, er);
+    cos_out[e] = sm;
+  }
 }
 
 }  // namespace
 
+cudaError_t launch_cos(const float* feat_now, const float* feat_prev, int E, int d_f, double* cos_out,
+                       cudaStream_t s) {
+  if (E <= 0) return cudaSuccess;
+  cos_kernel<<<E, kCosThreads, 0, s>>>(feat_now, feat_prev, d_f, cos_out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_verify(const int32_t* ids, int E, int k, int L, const uint8_t* tokens, const uint8_t* cand_tokens,
                           const float* logits, const float* feat_now, const float* feat_prev, int d_f,
                           const int32_t* history, int gap_d, const hsd_verify_params* params_dev, int P, int need_cos,
-                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s) {
+                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s, const double* cos_in) {
   if (E <= 0) return cudaSuccess;
   verify_kernel<<<(E + kWarps - 1) / kWarps, kThreads, 0, s>>>(ids, E, k, L, tokens, cand_tokens, logits, feat_now,
                                                                 feat_prev, d_f, history, gap_d, params_dev, P, need_cos,
-                                                                out, tok_out);
+                                                                cos_in, out, tok_out);
   return cudaGetLastError();
 }
 

@@ -117,7 +117,10 @@ cudaError_t launch_p2p_merge(const P2PWindows& w, int rank, int G, int B, int k,
 cudaError_t launch_verify(const int32_t* ids, int E, int k, int L, const uint8_t* tokens, const uint8_t* cand_tokens,
                           const float* logits, const float* feat_now, const float* feat_prev, int d_f,
                           const int32_t* history, int gap_d, const hsd_verify_params* params_dev, int P, int need_cos,
-                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s);
+                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s, const double* cos_in = nullptr);
+// should_skip similarity [E] (exactly rounded, same bits as K4's in-kernel dot) as a separate pass
+cudaError_t launch_cos(const float* feat_now, const float* feat_prev, int E, int d_f, double* cos_out,
+                       cudaStream_t s);
 cudaError_t launch_gather_tokens(const uint8_t* tokens, const int32_t* ids, int n, uint8_t* out, cudaStream_t s);
 
 // ---- K5 kinematics -------------------------------------------------------------
