@@ -85,6 +85,41 @@ struct __align__(1024) WideSmem {
   uint32_t tmem_base;
 };
 
+// One staging round of the epilogue: the 32 staged queries x 128 key rows in
+// `stg` are merged into the register-resident per-query top-32 lists (a warp
+// owns 4 queries; lane l holds rank l of each list, ascending keys).
+template <int kMyQ>
+__device__ __forceinline__ void epi_insert_round(const float* stg, int ew, int lane, int j, int q_valid,
+                                                 int64_t base, int64_t row_hi, uint64_t (&top)[kMyQ]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int ql = ew * 4 + i;
+    if (j * kStgQ + ql < q_valid) {
+      uint64_t& tp = top[j * 4 + i];
+      uint64_t key[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = lane + 32 * u;
+        key[u] = base + rr < row_hi ? cand_key(stg[rr * kStg + ql], (uint32_t)(base + rr)) : kEmpty;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t mask = __ballot_sync(0xffffffffu, key[u] < dev::shfl_u64(tp, 31));
+        while (mask) {
+          const int src = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const uint64_t x = dev::shfl_u64(key[u], src);
+          const int pos = __popc(__ballot_sync(0xffffffffu, tp < x));
+          if (pos < 32) {
+            const uint64_t up = dev::shfl_u64(tp, (lane + 31) & 31);
+            tp = lane < pos ? tp : (lane == pos ? x : up);
+          }
+        }
+      }
+    }
+  }
+}
+
 // kMC > 1: a cluster of kMC CTAs shares one key range; CTA rank r holds query
 // group r (256 queries each) and issues every kMC-th key tile with a TMA
 // multicast into all kMC CTAs, so the keys cross HBM once for up to 1024
@@ -280,33 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int t = 0; t < 16; ++t) S.stg[r * kStg + half * 16 + t] = __uint_as_float(acc[t]);
             named_sync(1, 32 * kEpiWarps);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int ql = ew * 4 + i;
-              if (q_base + j * kStgQ + ql < B) {
-                uint64_t& tp = top[j * 4 + i];
-                uint64_t key[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  const int rr = lane + 32 * u;
-                  key[u] = base + rr < row_end ? cand_key(S.stg[rr * kStg + ql], (uint32_t)(base + rr)) : kEmpty;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                  uint32_t mask = __ballot_sync(0xffffffffu, key[u] < dev::shfl_u64(tp, 31));
-                  while (mask) {
-                    const int src = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    const uint64_t x = dev::shfl_u64(key[u], src);
-                    const int pos = __popc(__ballot_sync(0xffffffffu, tp < x));
-                    if (pos < 32) {
-                      const uint64_t up = dev::shfl_u64(tp, (lane + 31) & 31);
-                      tp = lane < pos ? tp : (lane == pos ? x : up);
-                    }
-                  }
-                }
-              }
-            }
+            epi_insert_round(S.stg, ew, lane, j, B - q_base, base, row_end, top);
             named_sync(1, 32 * kEpiWarps);
           }
         }
@@ -328,6 +337,219 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant for one group of 129..256 queries (NS = 4).  Why: at
+// N = 256 the single-CTA kernel re-streams the 32-KB query tile of every
+// k-chunk from L2 into shared memory for ONE 16-KB key tile (the two
+// 256-column accumulator buffers leave no room to reuse it), and the MMA reads
+// both back: ~96 KB of shared-memory traffic per key tile, more than the
+// 128 B/clk port sustains at the UMMA rate.  With cta_group::2 the pair runs
+// one M = 256 UMMA per k-step: each CTA stages its own key block (A half) and
+// HALF of the query tile (B half, 128 queries), so per CTA and key tile the
+// traffic drops to 16 + 16 KB written and 16 + 16 KB read, and the L2 query
+// stream halves.
+//   pair rank 0 (leader): key TMA, query TMA, MMA issue, TMEM alloc, epilogue
+//   pair rank 1:          key TMA, query TMA,            TMEM alloc, epilogue
+// Every full barrier lives in the leader (both CTAs' TMA bytes complete on it);
+// the leader's commits multicast into both CTAs' empty / acc_full barriers; the
+// peer's epilogue arrives remotely on the leader's acc_empty.
+// Accumulator rows: leader TMEM = its key block, peer TMEM = the next block.
+constexpr int kPairQ = 256;                 // UMMA N (queries per pass)
+constexpr int kPairHalfQ = kPairQ / 2;      // B rows staged per CTA
+constexpr int kPairQTile = kPairHalfQ * 128;
+constexpr int kPairKS = 8, kPairQS = 4;
+
+struct __align__(1024) PairSmem {
+  uint8_t kbuf[kPairKS][kKeyTile];
+  uint8_t qbuf[kPairQS][kPairQTile];
+  float stg[kBM * kStg];
+  uint64_t k_full[kPairKS], k_empty[kPairKS];
+  uint64_t q_full[kPairQS], q_empty[kPairQS];
+  uint64_t acc_full[2], acc_empty[2];
+  uint32_t tmem_base;
+};
+
+template <bool kBf16>
+__global__ void __launch_bounds__(kThreads, 1)
+    sim_pair_kernel(const __grid_constant__ CUtensorMap keys_map, const __grid_constant__ CUtensorMap q_map,
+                    int64_t row_begin, int64_t row_end, int dim, int B, int64_t blocks_per_pair,
+                    uint64_t* __restrict__ partial) {
+  constexpr int kBK = kBf16 ? 64 : 32;
+  constexpr int kMyQ = kPairQ / kEpiWarps;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = (int)cluster_ctarank();  // 0 = leader
+  const int unit = (int)cluster_id_x(), n_units = (int)n_clusters_x();
+  const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
+  const int64_t blk0 = (int64_t)unit * blocks_per_pair;
+  const int64_t blk1 = std::min<int64_t>(blk0 + blocks_per_pair, n_blocks);
+  const int64_t steps = blk1 > blk0 ? (blk1 - blk0 + 1) / 2 : 0;  // key-block pairs
+  const int64_t row_hi = std::min<int64_t>(row_end, row_begin + blk1 * kBM);
+  const int nk = (dim + kBK - 1) / kBK;
+  const int kc0 = (int)(((int64_t)unit * nk) / n_units);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPairKS; ++i) {
+      mbar_init(&S.k_full[i], 1);
+      mbar_init(&S.k_empty[i], 1);
+    }
+    for (int i = 0; i < kPairQS; ++i) {
+      mbar_init(&S.q_full[i], 1);
+      mbar_init(&S.q_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&S.acc_full[i], 1);
+      mbar_init(&S.acc_empty[i], 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the leader's barriers exist before any peer TMA / remote arrive
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    // ======================= key stream: this CTA's block of each pair step
+    if (lane == 0 && steps > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&keys_map) : "memory");
+      const uint64_t pol = policy_evict_first();
+      int ks = 0;
+      uint32_t kph = 0;
+      for (int64_t st = 0; st < steps; ++st) {
+        const int row = (int)(row_begin + (blk0 + 2 * st + rank) * kBM);
+        for (int kc = 0; kc < nk; ++kc) {
+          mbar_wait(&S.k_empty[ks], kph ^ 1);
+          if (rank == 0) mbar_expect_tx(&S.k_full[ks], 2 * kKeyTile);
+          const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
+          tma_load_2d_pair(&S.kbuf[ks][0], &keys_map, mapa_shared(smem_u32(&S.k_full[ks]), 0), c * kBK, row, pol);
+          if (++ks == kPairKS) {
+            ks = 0;
+            kph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ======================= query half tiles (L2-resident)
+    if (lane == 0 && steps > 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&q_map) : "memory");
+      const uint64_t pol = policy_evict_last();
+      int qs = 0;
+      uint32_t qph = 0;
+      for (int64_t st = 0; st < steps; ++st)
+        for (int kc = 0; kc < nk; ++kc) {
+          mbar_wait(&S.q_empty[qs], qph ^ 1);
+          if (rank == 0) mbar_expect_tx(&S.q_full[qs], 2 * kPairQTile);
+          const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
+          tma_load_2d_pair(&S.qbuf[qs][0], &q_map, mapa_shared(smem_u32(&S.q_full[qs]), 0), c * kBK,
+                           rank * kPairHalfQ, pol);
+          if (++qs == kPairQS) {
+            qs = 0;
+            qph ^= 1;
+          }
+        }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer (leader only)
+    if (rank == 0) {
+      constexpr uint32_t idesc = kBf16 ? bf16_idesc(2 * kBM, kPairQ) : tf32_idesc(2 * kBM, kPairQ);
+      const uint64_t adesc0 = sw128_desc(&S.kbuf[0][0]);
+      const uint64_t bdesc0 = sw128_desc(&S.qbuf[0][0]);
+      int ks = 0, qs = 0;
+      uint32_t kph = 0, qph = 0;
+      for (int64_t gi = 0; gi < steps; ++gi) {
+        const int buf = (int)(gi & 1);
+        if (gi >= 2) {  // both CTAs' epilogues drained this buffer
+          mbar_wait(&S.acc_empty[buf], (uint32_t)((gi / 2) - 1) & 1);
+          tc_fence_after();
+        }
+        for (int kc = 0; kc < nk; ++kc) {
+          mbar_wait(&S.q_full[qs], qph);
+          mbar_wait(&S.k_full[ks], kph);
+          tc_fence_after();
+          const uint64_t adesc = adesc0 + (uint64_t)(ks * (kKeyTile >> 4));
+          const uint64_t bdesc = bdesc0 + (uint64_t)(qs * (kPairQTile >> 4));
+          const uint32_t d = tmem + buf * kPairQ;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            if (kBf16)
+              mma2_ss_f16(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
+            else
+              mma2_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit2_mc(&S.k_empty[ks], 3);
+          tc_commit2_mc(&S.q_empty[qs], 3);
+          if (++ks == kPairKS) {
+            ks = 0;
+            kph ^= 1;
+          }
+          if (++qs == kPairQS) {
+            qs = 0;
+            qph ^= 1;
+          }
+        }
+        tc_commit2_mc(&S.acc_full[buf], 3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ======================= epilogue (8 warps per CTA, its own key block)
+    const int ew = warp - 4;
+    const int quad = warp & 3;
+    const int half = ew >> 2;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    const uint32_t leader_empty0 = mapa_shared(smem_u32(&S.acc_empty[0]), 0);
+    const uint32_t leader_empty1 = mapa_shared(smem_u32(&S.acc_empty[1]), 0);
+    uint64_t top[kMyQ];
+#pragma unroll
+    for (int i = 0; i < kMyQ; ++i) top[i] = kEmpty;
+    for (int64_t gi = 0; gi < steps; ++gi) {
+      const int buf = (int)(gi & 1);
+      mbar_wait(&S.acc_full[buf], (uint32_t)(gi / 2) & 1);
+      tc_fence_after();
+      const int64_t base = row_begin + (blk0 + 2 * gi + rank) * kBM;
+#pragma unroll
+      for (int j = 0; j < kPairQ / kStgQ; ++j) {
+        uint32_t acc[16];
+        TMEM_LD16(tmem + lane_addr + buf * kPairQ + j * kStgQ + half * 16, acc);
+        tmem_ld_wait();
+        if (j == kPairQ / kStgQ - 1) {  // buffer drained
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(buf ? leader_empty1 : leader_empty0);
+        }
+#pragma unroll
+        for (int t = 0; t < 16; ++t) S.stg[r * kStg + half * 16 + t] = __uint_as_float(acc[t]);
+        named_sync(1, 32 * kEpiWarps);
+        epi_insert_round(S.stg, ew, lane, j, B, base, row_hi, top);
+        named_sync(1, 32 * kEpiWarps);
+      }
+    }
+    const int cta = unit * 2 + rank;
+#pragma unroll
+    for (int j = 0; j < kPairQ / kStgQ; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int q = j * kStgQ + ew * 4 + i;
+        if (q < B) partial[((size_t)cta * B + q) * kCandLocal + lane] = top[j * 4 + i];
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // no CTA leaves while its peer's MMAs / commits may still touch it
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
@@ -369,6 +591,41 @@ cudaError_t launch_ns(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, 
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
+}
+
+template <bool kBf16>
+cudaError_t launch_pair(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, int64_t re, int dim, int B,
+                        int lists, int64_t per_pair, uint64_t* partial, cudaStream_t s) {
+  const size_t smem = sizeof(PairSmem) + 1024;
+  auto kern = sim_pair_kernel<kBf16>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)lists);  // lists = 2 x pairs
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, km, qm, rb, re, dim, B, per_pair, partial);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// CTA-pair kernel for a single group of 129..256 queries; HSD_WIDE_PAIR=0
+// selects the single-CTA kernel instead (ablation).
+bool pair_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HSD_WIDE_PAIR");
+    v = (e && !strcmp(e, "0")) ? 0 : 1;
+  }
+  return v == 1;
 }
 
 // Accumulator layout per NS: "db" = double-buffered (256 columns per buffer;
@@ -453,9 +710,15 @@ static int max_active_clusters(int G, int num_sms) {
   return cache[G];
 }
 
+static bool use_pair(int B) { return B > 128 && B <= 256 && pair_enabled(); }
+
 int sim_wide_lists(int B, int64_t rows, int num_sms) {
   const int g = wide_groups(B);
   const int64_t blocks = (rows + kBM - 1) / kBM;
+  if (use_pair(B)) {  // CTA pairs: lists = 2 x pairs, each pair walks >= 2 key blocks
+    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>((blocks + 1) / 2, num_sms / 2));
+    return (int)(2 * pairs);
+  }
   return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, max_active_clusters(g, num_sms)));
 }
 
@@ -490,22 +753,30 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
   const int rows = box * groups;    // padded query slab
   const bool bf16 = key_dtype == HSD_DTYPE_BF16;
   if (bf16 && dim % 8) return cudaErrorInvalidValue;  // TMA row stride must be a multiple of 16 B
+  const bool pair = use_pair(B) && !dump && lists % 2 == 0;
+  const uint32_t qbox = pair ? (uint32_t)kPairHalfQ : (uint32_t)box;  // a pair CTA stages half the queries
   CUtensorMap km, qm;
   if (bf16) {
     pad_queries_bf16_kernel<<<rows, 256, 0, s>>>(queries, B, dim, (uint16_t*)scratch);
     if (!tc_make_map_bf16(&km, keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
-        !tc_make_map_bf16(&qm, scratch, (uint64_t)rows, (uint64_t)dim, (uint32_t)box))
+        !tc_make_map_bf16(&qm, scratch, (uint64_t)rows, (uint64_t)dim, qbox))
       return cudaErrorInvalidValue;
   } else {
     pad_queries_f32_kernel<<<rows, 256, 0, s>>>(queries, B, dim, (float*)scratch);
     if (!tc_make_map(&km, (const float*)keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
-        !tc_make_map(&qm, (const float*)scratch, (uint64_t)rows, (uint64_t)dim, (uint32_t)box))
+        !tc_make_map(&qm, (const float*)scratch, (uint64_t)rows, (uint64_t)dim, qbox))
       return cudaErrorInvalidValue;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
   const int64_t per = (n_blocks + lists - 1) / lists;
+  if (pair) {
+    const int64_t pairs = lists / 2;
+    const int64_t per_pair = ((n_blocks + pairs - 1) / pairs + 1) & ~(int64_t)1;  // even: whole block pairs
+    return bf16 ? launch_pair<true>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s)
+                : launch_pair<false>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s);
+  }
   if (groups > 1) {
     if (dump) return cudaErrorInvalidValue;  // the debug dump covers single-group passes
     switch (groups) {

@@ -249,7 +249,7 @@ def test_edge_shapes_all_kernels(torch, dtype, filt):
             if filt == "bf16_copy":
                 col.set_filter("bf16_copy")
             stored = emb if dtype == "f32" else torch.as_tensor(emb).bfloat16().float().numpy()
-            for B in (1, 3, 70, 300, 1030):
+            for B in (1, 3, 70, 200, 300, 1030):
                 q = torch.as_tensor(rng.standard_normal((B, dim)).astype(np.float32), device="cuda")
                 for k, rg in ((1, (0, n)), (9, (0, n)), (4, (n // 3, n))):
                     if rg[0] >= rg[1]:
