@@ -357,6 +357,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // the leader's commits multicast into both CTAs' empty / acc_full barriers; the
 // peer's epilogue arrives remotely on the leader's acc_empty.
 // Accumulator rows: leader TMEM = its key block, peer TMEM = the next block.
+// kG > 1 (257..1024 queries): a cluster of kG pairs, pair g holding query
+// group g; the key tile of pair-half h is issued by CTA 2 (t mod kG) + h and
+// multicast into the kG CTAs of half h (keys cross HBM once per pass), and a
+// key slot is refilled only after all kG pair leaders released it.
 constexpr int kPairQ = 256;                 // UMMA N (queries per pass)
 constexpr int kPairHalfQ = kPairQ / 2;      // B rows staged per CTA
 constexpr int kPairQTile = kPairHalfQ * 128;
@@ -372,7 +376,7 @@ struct __align__(1024) PairSmem {
   uint32_t tmem_base;
 };
 
-template <bool kBf16>
+template <bool kBf16, int kG>
 __global__ void __launch_bounds__(kThreads, 1)
     sim_pair_kernel(const __grid_constant__ CUtensorMap keys_map, const __grid_constant__ CUtensorMap q_map,
                     int64_t row_begin, int64_t row_end, int dim, int B, int64_t blocks_per_pair,
@@ -382,7 +386,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = (int)cluster_ctarank();  // 0 = leader
+  const int cr = (int)cluster_ctarank();
+  const int rank = cr & 1;           // 0 = pair leader
+  const int grp = cr >> 1;           // query group of this pair
+  const uint32_t leader = (uint32_t)(cr & ~1);
+  const int q_base = grp * kPairQ;
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * grp));
+  const uint16_t all_mask = (uint16_t)((1u << (2 * kG)) - 1);
+  uint16_t half_mask = 0;  // the kG CTAs holding the same key half
+#pragma unroll
+  for (int g = 0; g < kG; ++g) half_mask |= (uint16_t)(1u << (2 * g + rank));
   const int unit = (int)cluster_id_x(), n_units = (int)n_clusters_x();
   const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
   const int64_t blk0 = (int64_t)unit * blocks_per_pair;
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kPairKS; ++i) {
       mbar_init(&S.k_full[i], 1);
-      mbar_init(&S.k_empty[i], 1);
+      mbar_init(&S.k_empty[i], kG);
     }
     for (int i = 0; i < kPairQS; ++i) {
       mbar_init(&S.q_full[i], 1);
@@ -425,13 +438,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol = policy_evict_first();
       int ks = 0;
       uint32_t kph = 0;
+      uint32_t tile = 0;
       for (int64_t st = 0; st < steps; ++st) {
         const int row = (int)(row_begin + (blk0 + 2 * st + rank) * kBM);
-        for (int kc = 0; kc < nk; ++kc) {
+        for (int kc = 0; kc < nk; ++kc, ++tile) {
           mbar_wait(&S.k_empty[ks], kph ^ 1);
           if (rank == 0) mbar_expect_tx(&S.k_full[ks], 2 * kKeyTile);
           const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
-          tma_load_2d_pair(&S.kbuf[ks][0], &keys_map, mapa_shared(smem_u32(&S.k_full[ks]), 0), c * kBK, row, pol);
+          const uint32_t bar = mapa_shared(smem_u32(&S.k_full[ks]), leader);
+          if constexpr (kG > 1) {
+            if ((int)(tile % kG) == grp)
+              tma_load_2d_pair_mc(&S.kbuf[ks][0], &keys_map, bar, c * kBK, row, half_mask, pol);
+          } else {
+            tma_load_2d_pair(&S.kbuf[ks][0], &keys_map, bar, c * kBK, row, pol);
+          }
           if (++ks == kPairKS) {
             ks = 0;
             kph ^= 1;
@@ -451,8 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&S.q_empty[qs], qph ^ 1);
           if (rank == 0) mbar_expect_tx(&S.q_full[qs], 2 * kPairQTile);
           const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
-          tma_load_2d_pair(&S.qbuf[qs][0], &q_map, mapa_shared(smem_u32(&S.q_full[qs]), 0), c * kBK,
-                           rank * kPairHalfQ, pol);
+          tma_load_2d_pair(&S.qbuf[qs][0], &q_map, mapa_shared(smem_u32(&S.q_full[qs]), leader), c * kBK,
+                           q_base + rank * kPairHalfQ, pol);
           if (++qs == kPairQS) {
             qs = 0;
             qph ^= 1;
@@ -487,8 +507,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
               mma2_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
           }
-          tc_commit2_mc(&S.k_empty[ks], 3);
-          tc_commit2_mc(&S.q_empty[qs], 3);
+          tc_commit2_mc(&S.k_empty[ks], all_mask);  // every CTA's slot ks: kG releases complete it
+          tc_commit2_mc(&S.q_empty[qs], pair_mask);
           if (++ks == kPairKS) {
             ks = 0;
             kph ^= 1;
@@ -498,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             qph ^= 1;
           }
         }
-        tc_commit2_mc(&S.acc_full[buf], 3);
+        tc_commit2_mc(&S.acc_full[buf], pair_mask);
       }
     }
   } else if (warp >= 4) {
@@ -508,8 +528,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;
     const int r = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    const uint32_t leader_empty0 = mapa_shared(smem_u32(&S.acc_empty[0]), 0);
-    const uint32_t leader_empty1 = mapa_shared(smem_u32(&S.acc_empty[1]), 0);
+    const uint32_t leader_empty0 = mapa_shared(smem_u32(&S.acc_empty[0]), leader);
+    const uint32_t leader_empty1 = mapa_shared(smem_u32(&S.acc_empty[1]), leader);
     uint64_t top[kMyQ];
 #pragma unroll
     for (int i = 0; i < kMyQ; ++i) top[i] = kEmpty;
@@ -531,17 +551,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < 16; ++t) S.stg[r * kStg + half * 16 + t] = __uint_as_float(acc[t]);
         named_sync(1, 32 * kEpiWarps);
-        epi_insert_round(S.stg, ew, lane, j, B, base, row_hi, top);
+        epi_insert_round(S.stg, ew, lane, j, B - q_base, base, row_hi, top);
         named_sync(1, 32 * kEpiWarps);
       }
     }
-    const int cta = unit * 2 + rank;
+    const int list = unit * 2 + rank;  // one list per key half of the cluster's range
 #pragma unroll
     for (int j = 0; j < kPairQ / kStgQ; ++j)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int q = j * kStgQ + ew * 4 + i;
-        if (q < B) partial[((size_t)cta * B + q) * kCandLocal + lane] = top[j * 4 + i];
+        const int q = q_base + j * kStgQ + ew * 4 + i;
+        if (q < B) partial[((size_t)list * B + q) * kCandLocal + lane] = top[j * 4 + i];
       }
   }
   tc_fence_before();
@@ -593,21 +613,21 @@ cudaError_t launch_ns(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, 
   return cudaGetLastError();
 }
 
-template <bool kBf16>
+template <bool kBf16, int kG>
 cudaError_t launch_pair(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, int64_t re, int dim, int B,
                         int lists, int64_t per_pair, uint64_t* partial, cudaStream_t s) {
   const size_t smem = sizeof(PairSmem) + 1024;
-  auto kern = sim_pair_kernel<kBf16>;
+  auto kern = sim_pair_kernel<kBf16, kG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)lists);  // lists = 2 x pairs
+  cfg.gridDim = dim3((unsigned)(lists * kG));  // lists = 2 x clusters; a cluster is kG pairs
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = 2 * kG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -710,14 +730,50 @@ static int max_active_clusters(int G, int num_sms) {
   return cache[G];
 }
 
-static bool use_pair(int B) { return B > 128 && B <= 256 && pair_enabled(); }
+static bool use_pair(int B) { return B > 128 && pair_enabled(); }
+
+// Clusters of G CTA pairs (2G CTAs) resident at once, cached per G.
+static int max_active_pair_clusters(int G, int num_sms) {
+  static int cache[5] = {0, 0, 0, 0, 0};
+  if (!cache[G]) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * G * (num_sms / (2 * G))));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sizeof(PairSmem) + 1024;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)(2 * G);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t e = cudaSuccess;
+    auto q = [&](auto kern) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
+    };
+    switch (G) {
+      case 1: q(sim_pair_kernel<false, 1>); break;
+      case 2: q(sim_pair_kernel<false, 2>); break;
+      case 3: q(sim_pair_kernel<false, 3>); break;
+      default: q(sim_pair_kernel<false, 4>); break;
+    }
+    if (e != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = num_sms / (2 * G);
+    }
+    cache[G] = std::max(1, n);
+  }
+  return std::max(1, std::min(cache[G], num_sms / (2 * G)));
+}
 
 int sim_wide_lists(int B, int64_t rows, int num_sms) {
   const int g = wide_groups(B);
   const int64_t blocks = (rows + kBM - 1) / kBM;
-  if (use_pair(B)) {  // CTA pairs: lists = 2 x pairs, each pair walks >= 2 key blocks
-    const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>((blocks + 1) / 2, num_sms / 2));
-    return (int)(2 * pairs);
+  if (use_pair(B)) {  // clusters of g CTA pairs: lists = 2 x clusters, each walks >= 2 key blocks
+    const int64_t cl = std::max<int64_t>(1, std::min<int64_t>((blocks + 1) / 2, max_active_pair_clusters(g, num_sms)));
+    return (int)(2 * cl);
   }
   return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, max_active_clusters(g, num_sms)));
 }
@@ -774,8 +830,18 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
   if (pair) {
     const int64_t pairs = lists / 2;
     const int64_t per_pair = ((n_blocks + pairs - 1) / pairs + 1) & ~(int64_t)1;  // even: whole block pairs
-    return bf16 ? launch_pair<true>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s)
-                : launch_pair<false>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s);
+    switch (groups) {
+#define HSD_PAIR(G)                                                                                        \
+  case G:                                                                                                  \
+    return bf16 ? launch_pair<true, G>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s)    \
+                : launch_pair<false, G>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s);
+      HSD_PAIR(1)
+      HSD_PAIR(2)
+      HSD_PAIR(3)
+      HSD_PAIR(4)
+#undef HSD_PAIR
+      default: return cudaErrorInvalidValue;
+    }
   }
   if (groups > 1) {
     if (dump) return cudaErrorInvalidValue;  // the debug dump covers single-group passes

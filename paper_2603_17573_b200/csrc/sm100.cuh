@@ -151,6 +151,16 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar_cluster), "l"(policy)
       : "memory");
 }
+// ... multicast into the same offset of every CTA in cta_mask; the completion
+// goes to each destination's pair leader (bar_cluster names the issuer's leader).
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int x,
+                                                    int y, uint16_t cta_mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(x), "r"(y), "r"(bar_cluster), "h"(cta_mask), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tc_commit2_mc(uint64_t* b, uint16_t cta_mask) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
