@@ -25,4 +25,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --cache-co
   --log-file $OUT/launches_warm.csv $ARGS > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:sim_wide|rescore" -s 6 -c 2 \
   -o $OUT/full_c2 $ARGS > /dev/null 2>&1
+# config-4 shape (B = 256, CTA-pair filter) on a 2M-row DB to bound the replay time
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:sim_pair|verify" -s 2 -c 2 \
+  -o $OUT/full_c4 python bench.py --config c4 --n 2000000 --filter native --steps 2 --warmup 1 --no-cpu-baseline \
+  --e2e-steps 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:verify" -s 2 -c 1 \
+  -o $OUT/full_c3 python bench.py --config c3 --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 ls -la $OUT

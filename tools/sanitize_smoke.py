@@ -16,7 +16,7 @@ for dtype in ("f32", "bf16"):
     col.generate(H.REAL, 3, n)
     for path in (["tc", "rows", "tile", "tc1", "tc3"] if dtype == "f32" else ["tc"]):
         H.set_sim_path(path)
-        for B in (1, 5, 64, 300):
+        for B in (1, 5, 64, 200, 300):
             if path in ("tc1", "tc3", "rows", "tile") and B > 64:
                 continue
             q = H.gen_queries(H.REAL, 4, 3, n, 0, B, dim)
@@ -35,6 +35,24 @@ for dtype in ("f32", "bf16"):
                      feat_now=fn, feat_prev=fp)
 xyz = torch.as_tensor(synth.trajectory_windows(64, 15, seed=3)[0], device="cuda")
 H.window_features(xyz, derivatives=True)
+# engine step: K5 + the skip similarity on the side stream, K1 / K2 / K4 on the main stream
+col = H.Collection(dim, capacity=n)
+col.generate(H.REAL, 3, n)
+eng = H.Engine(col, 64, 8, 7, 64, 15)
+rows = H.query_rows(4, H.REAL, n, 0, 64)
+fn, fp = H.gen_features(5, 64, 64)
+dev = "cuda"
+buf = H.StepBuffers(queries=H.gen_queries(H.REAL, 4, 3, n, 0, 64, dim), logits=H.gen_logits(col, 3, rows, 7),
+                    feat_now=fn, feat_prev=fp, xyz=xyz, history=torch.full((64,), 100, dtype=torch.int32, device=dev),
+                    scores=torch.empty((64, 8), dtype=torch.float64, device=dev),
+                    ids=torch.empty((64, 8), dtype=torch.int32, device=dev),
+                    out=torch.empty((64, 20), dtype=torch.uint8, device=dev),
+                    tokens=torch.empty((64, 7), dtype=torch.uint8, device=dev),
+                    R=torch.empty(64, dtype=torch.float64, device=dev), D=torch.empty(64, dtype=torch.float64, device=dev),
+                    F=torch.empty(64, dtype=torch.float64, device=dev),
+                    decision=torch.empty(64, dtype=torch.int32, device=dev))
+eng.step(64, buf, H.VerifyParams.make(skip_enabled=True, min_S=0.95, O_dist=5), gap_d=1)
+torch.cuda.synchronize()
 col = H.Collection(64, capacity=64 * 40, dtype="bf16")
 col.generate(H.REAL, 7, 64 * 40, payload=H.PAYLOAD_TRAJ, traj_T=64)
 loop = H.HybridLoop(col, H.hybrid_params(40, traj_T=64, d_f=64, seed=5, db_seed=7), max_rounds=20)
