@@ -127,6 +127,8 @@ hsd_status hsd_collection_generate_rows(hsd_collection* c, int kind, uint64_t db
  * dot product of the (fp32-widened) query and key, bit for bit.
  * k < 1 -> HSD_ERR_INVALID_INPUT (store.cpp:60); k > HSD_K_MAX ->
  * HSD_ERR_INVALID_INPUT.  An empty collection yields all -1 (no error).
+ * `queries` is a device pointer, 16-byte aligned (HSD_ERR_INVALID_INPUT
+ * otherwise; rows are dim * 4 bytes apart with dim % 4 == 0).
  * ---------------------------------------------------------------------- */
 hsd_status hsd_search_topk_exact(hsd_collection* c, const float* queries, int B, int k, double* scores,
                                  int32_t* ids, void* stream);

@@ -259,6 +259,8 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   if (B < 0) return fail(HSD_ERR_INVALID_INPUT, "negative batch");
   if (B == 0) return HSD_OK;
   if (!queries || !scores || !ids) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (reinterpret_cast<uintptr_t>(queries) % 16)  // 128-bit / cp.async / TMA staging of query rows
+    return fail(HSD_ERR_INVALID_INPUT, "queries must be 16-byte aligned");
   hsd_status st = require_device(c->device);
   if (st != HSD_OK) return st;
   rb = std::max<int64_t>(rb, 0);

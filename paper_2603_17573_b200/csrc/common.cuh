@@ -112,5 +112,15 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
   e = __dadd_rn(__dsub_rn(a, av), __dsub_rn(b, bv));
 }
 
+// Order key of an exact fp64 score for (score desc) ranking with integer
+// compares: a larger score gives a smaller key; -0.0 and +0.0 share a key
+// (they compare equal, so the id decides, as with the reference's
+// std::sort comparator).  Scores are finite.
+__device__ __forceinline__ uint64_t score_desc_key(double d) {
+  uint64_t u = (uint64_t)__double_as_longlong(d == 0.0 ? 0.0 : d);
+  u = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+  return ~u;
+}
+
 }  // namespace dev
 }  // namespace hsd

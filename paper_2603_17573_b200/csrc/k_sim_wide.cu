@@ -575,14 +575,47 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Zero-padded copy of the query slab to `rows` rows (the TMA box); bf16 mode
 // rounds to bf16 (RN-even, hsd_bf16_bits) on the way.
-__global__ void pad_queries_f32_kernel(const float* __restrict__ q, int B, int dim, float* __restrict__ out) {
-  const int row = blockIdx.x;
-  for (int c = threadIdx.x; c < dim; c += blockDim.x) out[(size_t)row * dim + c] = row < B ? q[(size_t)row * dim + c] : 0.f;
+// One CTA per padded row; dim % 4 == 0 (the collection's contract), rows are
+// 16-B aligned.  Each thread moves kPadVec float4 with all loads issued before
+// any store: a scalar load->store loop serialises one L2/DRAM round trip per
+// iteration (measured 11 us for a 64 x 4096 slab, ~1 us vectorised).
+constexpr int kPadThreads = 256, kPadVec = 4;
+__global__ void __launch_bounds__(kPadThreads) pad_queries_f32_kernel(const float* __restrict__ q, int B, int dim,
+                                                                      float* __restrict__ out) {
+  const int row = blockIdx.x, n4 = dim / 4;
+  const float4* src = reinterpret_cast<const float4*>(q + (size_t)row * dim);
+  float4* dst = reinterpret_cast<float4*>(out + (size_t)row * dim);
+  for (int c0 = threadIdx.x; c0 < n4; c0 += kPadThreads * kPadVec) {
+    float4 v[kPadVec];
+#pragma unroll
+    for (int u = 0; u < kPadVec; ++u) {
+      const int c = c0 + u * kPadThreads;
+      v[u] = (row < B && c < n4) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kPadVec; ++u)
+      if (c0 + u * kPadThreads < n4) dst[c0 + u * kPadThreads] = v[u];
+  }
 }
-__global__ void pad_queries_bf16_kernel(const float* __restrict__ q, int B, int dim, uint16_t* __restrict__ out) {
-  const int row = blockIdx.x;
-  for (int c = threadIdx.x; c < dim; c += blockDim.x)
-    out[(size_t)row * dim + c] = row < B ? hsd_bf16_bits(q[(size_t)row * dim + c]) : (uint16_t)0;
+__global__ void __launch_bounds__(kPadThreads) pad_queries_bf16_kernel(const float* __restrict__ q, int B, int dim,
+                                                                       uint16_t* __restrict__ out) {
+  const int row = blockIdx.x, n4 = dim / 4;
+  const float4* src = reinterpret_cast<const float4*>(q + (size_t)row * dim);
+  uint2* dst = reinterpret_cast<uint2*>(out + (size_t)row * dim);
+  for (int c0 = threadIdx.x; c0 < n4; c0 += kPadThreads * kPadVec) {
+    float4 v[kPadVec];
+#pragma unroll
+    for (int u = 0; u < kPadVec; ++u) {
+      const int c = c0 + u * kPadThreads;
+      v[u] = (row < B && c < n4) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kPadVec; ++u)
+      if (c0 + u * kPadThreads < n4)
+        dst[c0 + u * kPadThreads] =
+            make_uint2((uint32_t)hsd_bf16_bits(v[u].x) | ((uint32_t)hsd_bf16_bits(v[u].y) << 16),
+                       (uint32_t)hsd_bf16_bits(v[u].z) | ((uint32_t)hsd_bf16_bits(v[u].w) << 16));
+  }
 }
 
 template <bool kBf16, int NS, int GB, bool kDump, int kMC = 1>
@@ -813,12 +846,12 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
   const uint32_t qbox = pair ? (uint32_t)kPairHalfQ : (uint32_t)box;  // a pair CTA stages half the queries
   CUtensorMap km, qm;
   if (bf16) {
-    pad_queries_bf16_kernel<<<rows, 256, 0, s>>>(queries, B, dim, (uint16_t*)scratch);
+    pad_queries_bf16_kernel<<<rows, kPadThreads, 0, s>>>(queries, B, dim, (uint16_t*)scratch);
     if (!tc_make_map_bf16(&km, keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
         !tc_make_map_bf16(&qm, scratch, (uint64_t)rows, (uint64_t)dim, qbox))
       return cudaErrorInvalidValue;
   } else {
-    pad_queries_f32_kernel<<<rows, 256, 0, s>>>(queries, B, dim, (float*)scratch);
+    pad_queries_f32_kernel<<<rows, kPadThreads, 0, s>>>(queries, B, dim, (float*)scratch);
     if (!tc_make_map(&km, (const float*)keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
         !tc_make_map(&qm, (const float*)scratch, (uint64_t)rows, (uint64_t)dim, qbox))
       return cudaErrorInvalidValue;

@@ -6,6 +6,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/rl tools/rescore_lab.cu && /tmp/rl
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 #include <random>
 #include <cuda_runtime.h>
@@ -62,7 +63,30 @@ __global__ void __launch_bounds__(kThr) v_ring(const float* __restrict__ keys, i
     if (kMode == 2) { if (tid < n) acc += rows[ch & 1][tid][ch]; }
     else if (tid < n) {
       const float* r = rows[ch & 1][tid];
-      if (kPipe > 0 && w == kW) {
+      if (kMode == 5 && w == kW) {
+#pragma unroll 16
+        for (int j = 0; j < kW; ++j) {
+          const uint32_t u = __float_as_uint(r[j]);
+          const uint32_t a = u & 0x7fffffffu;
+          const uint32_t hi = (u & 0x80000000u) | (a ? (a >> 3) + 0x38000000u : 0u);
+          acc = __fma_rn(qd[j], __hiloint2double((int)hi, (int)(u << 29)), acc);
+        }
+      } else if (kMode == 3 && w == kW) {
+        constexpr int P = kPipe > 0 ? kPipe : 1;
+        double qa[P], ra[P];
+#pragma unroll
+        for (int u = 0; u < P; ++u) { qa[u] = qd[u]; asm volatile("cvt.f64.f32 %0, %1;" : "=d"(ra[u]) : "f"(r[u])); }
+        for (int j = 0; j < kW; j += P) {
+          double qb[P], rb[P];
+          const int jn = j + P < kW ? j + P : j;
+#pragma unroll
+          for (int u = 0; u < P; ++u) { qb[u] = qd[jn + u]; asm volatile("cvt.f64.f32 %0, %1;" : "=d"(rb[u]) : "f"(r[jn + u])); }
+#pragma unroll
+          for (int u = 0; u < P; ++u) asm volatile("fma.rn.f64 %0, %1, %2, %0;" : "+d"(acc) : "d"(qa[u]), "d"(ra[u]));
+#pragma unroll
+          for (int u = 0; u < P; ++u) { qa[u] = qb[u]; ra[u] = rb[u]; }
+        }
+      } else if (kPipe > 0 && w == kW) {
         constexpr int P = kPipe > 0 ? kPipe : 1;
         double qa[P], ra[P];
 #pragma unroll
@@ -251,12 +275,90 @@ __global__ void __launch_bounds__(128) v_int(const float* __restrict__ keys, int
   if (tid < n) o.exact[c0 + tid] = acc;
 }
 
+
+// replica of k_select.cu rank_kernel (no publish) to time it alone
+__global__ void __launch_bounds__(256) v_rank(const Scr* __restrict__ scr, int k, double* __restrict__ scores,
+                                              int32_t* __restrict__ ids, int* __restrict__ overflow) {
+  __shared__ double ex[kCandMax];
+  __shared__ uint32_t id[kCandMax];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const Scr& o = scr[b];
+  const int n = o.n;
+  if (tid < n) {
+    ex[tid] = o.exact[tid];
+    id[tid] = o.id[tid];
+  }
+  __syncthreads();
+  if (tid < n) {
+    const double s = ex[tid];
+    const uint32_t me = id[tid];
+    int rank = 0;
+    for (int c = 0; c < n; ++c) {
+      const double x = ex[c];
+      rank += (x > s) || (x == s && id[c] < me);
+    }
+    if (rank < k) {
+      scores[(size_t)b * k + rank] = s;
+      ids[(size_t)b * k + rank] = (int32_t)me;
+    }
+  }
+  for (int r = n + tid; r < k; r += 256) {
+    scores[(size_t)b * k + r] = -INFINITY;
+    ids[(size_t)b * k + r] = -1;
+  }
+  if (tid == 0 && o.over) atomicAdd(overflow, 1);
+}
+
+__device__ __forceinline__ uint64_t ord_desc(double d) {
+  // larger double -> smaller key (ascending key order = descending score); -0.0 == +0.0 like ==
+  uint64_t u = (uint64_t)__double_as_longlong(d == 0.0 ? 0.0 : d);
+  u = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+  return ~u;
+}
+__global__ void __launch_bounds__(256) v_rank2(const Scr* __restrict__ scr, int k, double* __restrict__ scores,
+                                               int32_t* __restrict__ ids, int* __restrict__ overflow) {
+  __shared__ uint64_t key[kCandMax];
+  __shared__ uint32_t id[kCandMax];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const Scr& o = scr[b];
+  const int n = o.n;
+  double s = 0.0;
+  uint32_t me = 0;
+  uint64_t mk = 0;
+  if (tid < n) {
+    s = o.exact[tid];
+    me = o.id[tid];
+    mk = ord_desc(s);
+    key[tid] = mk;
+    id[tid] = me;
+  }
+  __syncthreads();
+  if (tid < n) {
+    int rank = 0;
+#pragma unroll 8
+    for (int c = 0; c < n; ++c) {
+      const uint64_t x = key[c];
+      rank += (x < mk) | ((x == mk) & (id[c] < me));
+    }
+    if (rank < k) {
+      scores[(size_t)b * k + rank] = s;
+      ids[(size_t)b * k + rank] = (int32_t)me;
+    }
+  }
+  for (int r = n + tid; r < k; r += 256) {
+    scores[(size_t)b * k + r] = -INFINITY;
+    ids[(size_t)b * k + r] = -1;
+  }
+  if (tid == 0 && o.over) atomicAdd(overflow, 1);
+}
+__global__ void v_empty() {}
+
 __global__ void flush(float* p, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] += 1.f;
 }
 
 int main(int argc, char** argv) {
-  const int B = 64, dim = 4096;
+  const int B = argc > 1 ? atoi(argv[1]) : 64, dim = 4096;
   const size_t N = 250000;  // 4.1 GB of fp32 rows
   std::mt19937_64 rng(7);
   std::vector<float> hk(N * dim);
@@ -265,7 +367,7 @@ int main(int argc, char** argv) {
   std::vector<float> hq((size_t)B * dim);
   for (auto& x : hq) x = nd(rng);
   std::vector<Scr> hs(B);
-  std::uniform_int_distribution<int> nc(40, 163);
+  std::uniform_int_distribution<int> nc(argc > 2 ? atoi(argv[2]) : 40, argc > 3 ? atoi(argv[3]) : 163);
   for (int b = 0; b < B; ++b) {
     hs[b].n = nc(rng);
     for (int c = 0; c < hs[b].n; ++c) hs[b].id[c] = (uint32_t)(rng() % N);
@@ -321,13 +423,46 @@ int main(int argc, char** argv) {
     run("v_ring<" #P "," #W ",pipe" #PIPE ",thr" #T ">", [&] { k<<<dim3(B, kCandMax / P), T, sm>>>(dk, dim, dq, ds); }); \
   }
   RING(32, 256, 8, 128)
-  RINGM(32, 256, 8, 128, 1)
-  RINGM(32, 256, 8, 128, 2)
-  RINGM(8, 512, 0, 128, 1)
-  RINGM(8, 512, 0, 128, 2)
-  RING(24, 256, 8, 128)
-  RING(24, 256, 4, 128)
-  RING(24, 256, 4, 256)
+  RINGM(32, 256, 16, 128, 3)
+  RINGM(32, 256, 8, 128, 5)
+  RINGM(32, 128, 8, 128, 5)
+  RINGM(16, 256, 8, 128, 5)
+  {
+    double* dsc; int32_t* did; int* dov;
+    CK(cudaMalloc(&dsc, B * 8 * 8)); CK(cudaMalloc(&did, B * 8 * 4)); CK(cudaMalloc(&dov, 4));
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int rep = 0; rep < 2; ++rep) {
+      float ms;
+      cudaEventRecord(e0);
+      for (int i = 0; i < 100; ++i) v_rank<<<B, 256>>>(ds, 8, dsc, did, dov);
+      cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+      printf("rank kernel alone (x100 back to back): %.2f us each\n", ms * 10.f);
+      {
+        double* dsc2; int32_t* did2;
+        CK(cudaMalloc(&dsc2, B * 8 * 8)); CK(cudaMalloc(&did2, B * 8 * 4));
+        cudaEventRecord(e0);
+        for (int i = 0; i < 100; ++i) v_rank2<<<B, 256>>>(ds, 8, dsc2, did2, dov);
+        cudaEventRecord(e1); cudaEventSynchronize(e1); float m2; cudaEventElapsedTime(&m2, e0, e1);
+        std::vector<double> a(B * 8), b2(B * 8); std::vector<int32_t> ia(B * 8), ib(B * 8);
+        cudaMemcpy(a.data(), dsc, B * 64, cudaMemcpyDeviceToHost); cudaMemcpy(b2.data(), dsc2, B * 64, cudaMemcpyDeviceToHost);
+        cudaMemcpy(ia.data(), did, B * 32, cudaMemcpyDeviceToHost); cudaMemcpy(ib.data(), did2, B * 32, cudaMemcpyDeviceToHost);
+        bool same = true; for (int i = 0; i < B * 8; ++i) same &= (a[i] == b2[i]) && (ia[i] == ib[i]);
+        printf("rank2 (integer keys): %.2f us each, %s\n", m2 * 10.f, same ? "same output" : "DIFFERENT");
+      }
+      cudaEventRecord(e0);
+      for (int i = 0; i < 100; ++i) v_empty<<<B, 256>>>();
+      cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+      printf("empty kernel (x100): %.2f us each\n", ms * 10.f);
+      cudaEventRecord(e0);
+      for (int i = 0; i < 100; ++i) { flush<<<1184, 256>>>(dfl, nfl); v_rank<<<B, 256>>>(ds, 8, dsc, did, dov); }
+      cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+      float ms2;
+      cudaEventRecord(e0);
+      for (int i = 0; i < 100; ++i) flush<<<1184, 256>>>(dfl, nfl);
+      cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms2, e0, e1);
+      printf("rank after an L2 flush: %.2f us each\n", (ms - ms2) * 10.f);
+    }
+  }
   run("v_int<32,128>", [&] { v_int<32, 128><<<dim3(B, kCandMax / 32), 128>>>(dk, dim, dq, ds); });
 #define WS(P, T, W, PIPE, S)                                                                                     \
   {                                                                                                              \
