@@ -237,7 +237,11 @@ int choose_path(int B, int dtype, bool shadow = false) {
   if (o == kPathRows) return B <= 8 ? kPathRows : kPathTile;
   if (o == kPathTile) return B <= 8 ? kPathRows : kPathTile;  // launch_sim picks rows for B <= 8
   if (o == kPathTc || o == kPathTc3 || o == kPathTc1) return o;
-  return B <= 4 ? kPathRows : kPathTc;
+  // the wide tcgen05 filter for every batch: at 1M x 4096 fp32 it streams at
+  // 6.9 TB/s for B = 1..64, where the SIMT rows kernel reached 2.3 TB/s at
+  // B = 1 and 6.6 TB/s at B = 4 (tools/bench_search.py); rows stays an ablation
+  (void)B;
+  return kPathTc;
 }
 bool is_tc(int p) { return p == kPathTc || p == kPathTc3 || p == kPathTc1; }
 int pass_width(int p) { return p == kPathTc ? hsd::sim_wide_max_batch() : kSlab; }

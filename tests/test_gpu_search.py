@@ -88,6 +88,9 @@ def test_search_edge_cases(torch):
         col.search_topk_exact(q, 33)
     with pytest.raises(H.InvalidInputError):
         col.search_topk_exact(torch.zeros((2, 32), device="cuda"), 3)  # dim mismatch (store.cpp:30)
+    misaligned = torch.zeros(3 * 64 + 1, device="cuda")[1:].view(3, 64)  # 4-byte offset view
+    with pytest.raises(H.InvalidInputError):
+        col.search_topk_exact(misaligned, 3)
 
 
 def test_range_search_is_a_task_shard(torch):
