@@ -40,7 +40,18 @@ def oracle_round(drafts, greedy, cosv, hist, gap_d, p):
 @pytest.mark.parametrize("L", [7, 21])
 @pytest.mark.parametrize("k", [1, 3, 8, 12])
 def test_verify_parity(torch, L, k):
-    n, E, d_f = 400, 512, 256
+    _parity(torch, L, k, 512)
+
+
+@pytest.mark.parametrize("L", [7, 21])
+def test_verify_parity_large_round(torch, L):
+    """A round of 1100 episodes (more CTAs than one wave of the 2-episode K4
+    CTAs on some SM counts); the reported skip similarity matches too."""
+    _parity(torch, L, 8, 1100)
+
+
+def _parity(torch, L, k, E):
+    n, d_f = 400, 256
     db_seed, lseed, fseed = 21, 5, 9
     col = H.Collection(64, capacity=n)
     col.generate(O.REAL, db_seed, n)
@@ -77,6 +88,8 @@ def test_verify_parity(torch, L, k):
                 assert (g["win_a"], g["win_b"]) == (o.win_a, o.win_b), (e, pi)
             np.testing.assert_array_equal(toks[pi, e, :o.n_emit], np.array(o.tokens[:o.n_emit]))
             assert g["greedy0"] == greedy[0]
+            if p.skip_enabled:
+                assert g["cos_sim"] == np.float32(cosv), (e, pi)
             stats["skipped"] += o.skipped
             stats["fallback"] += o.fallback
             stats["partial"] += 0 < o.accept_len < L
