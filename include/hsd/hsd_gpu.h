@@ -152,10 +152,12 @@ hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count
 hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
                                 void* stream);
 /* Similarity-path override for ablations/tests (fp32 collections): 0 auto
- * (SIMT for B <= 4, wide tcgen05 TF32 otherwise), 1 SIMT rows/tile, 2 SIMT
- * tile, 3 wide tcgen05 TF32 (256 queries per pass), 4 tcgen05 3xTF32, 5
- * 64-query tcgen05 TF32.  Process-wide; also HSD_SIM_PATH=rows|tile|tc|tc3|tc1.
- * bf16 collections always use the wide kernel. */
+ * (the wide tcgen05 filter for every batch, CTA pairs above 128 queries),
+ * 1 SIMT rows/tile, 2 SIMT tile, 3 wide tcgen05 TF32, 4 tcgen05 3xTF32,
+ * 5 64-query tcgen05 TF32, 6 wide kernels without CTA pairs (also applies to
+ * bf16 collections).  Process-wide; also
+ * HSD_SIM_PATH=rows|tile|tc|tc3|tc1|tc_single.  bf16 collections otherwise
+ * always use the wide kernels. */
 hsd_status hsd_set_sim_path(int path);
 
 /* ------------------------------------------------------------------------

@@ -600,12 +600,12 @@ def quantize(actions, lo=-1.0, hi=1.0, k_bins=256, stream=None):
     return bins
 
 
-SIM_PATHS = {"auto": 0, "rows": 1, "tile": 2, "tc": 3, "tc3": 4, "tc1": 5}
+SIM_PATHS = {"auto": 0, "rows": 1, "tile": 2, "tc": 3, "tc3": 4, "tc1": 5, "tc_single": 6}
 
 
 def set_sim_path(name: str) -> None:
     """Similarity kernel override (ablations / tests): auto | rows | tile | tc (wide TF32, default) | tc1 (64-query
-    TF32) | tc3 (3xTF32)."""
+    TF32) | tc3 (3xTF32) | tc_single (wide kernels without CTA pairs)."""
     check(lib().hsd_set_sim_path(SIM_PATHS[name]))
 
 

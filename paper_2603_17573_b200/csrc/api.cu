@@ -213,7 +213,7 @@ constexpr int kSlab = 64;  // queries per similarity launch of the 64-wide paths
 // (TF32 over fp32 keys, bf16 over bf16 keys; up to 256 queries per pass).
 // HSD_SIM_PATH=rows|tile|tc|tc1|tc3 or hsd_set_sim_path override it for fp32
 // collections (tests and ablations: tc1 = 64-query TF32 kernel, tc3 = 3xTF32).
-enum { kPathAuto = 0, kPathRows = 1, kPathTile = 2, kPathTc = 3, kPathTc3 = 4, kPathTc1 = 5 };
+enum { kPathAuto = 0, kPathRows = 1, kPathTile = 2, kPathTc = 3, kPathTc3 = 4, kPathTc1 = 5, kPathTcSingle = 6 };
 int g_path = -1;
 int path_override() {
   int& v = g_path;
@@ -225,6 +225,7 @@ int path_override() {
     if (e && !strcmp(e, "tc")) v = kPathTc;
     if (e && !strcmp(e, "tc3")) v = kPathTc3;
     if (e && !strcmp(e, "tc1")) v = kPathTc1;
+    if (e && !strcmp(e, "tc_single")) v = kPathTcSingle;
   }
   return v;
 }
@@ -237,6 +238,7 @@ int choose_path(int B, int dtype, bool shadow = false) {
   if (o == kPathRows) return B <= 8 ? kPathRows : kPathTile;
   if (o == kPathTile) return B <= 8 ? kPathRows : kPathTile;  // launch_sim picks rows for B <= 8
   if (o == kPathTc || o == kPathTc3 || o == kPathTc1) return o;
+  if (o == kPathTcSingle) return kPathTc;  // the wide kernels without CTA pairs (sim_wide_set_single)
   // the wide tcgen05 filter for every batch: at 1M x 4096 fp32 it streams at
   // 6.9 TB/s for B = 1..64, where the SIMT rows kernel reached 2.3 TB/s at
   // B = 1 and 6.6 TB/s at B = 4 (tools/bench_search.py); rows stays an ablation
@@ -576,10 +578,12 @@ hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B,
 }
 
 hsd_status hsd_set_sim_path(int path) {
-  if (path < 0 || path > 5)
+  if (path < 0 || path > 6)
     return fail(HSD_ERR_INVALID_INPUT,
-                "path must be 0 auto, 1 rows, 2 tile, 3 tc (wide TF32), 4 tc3 (3xTF32), 5 tc1 (64-query TF32)");
+                "path must be 0 auto, 1 rows, 2 tile, 3 tc (wide TF32), 4 tc3 (3xTF32), 5 tc1 (64-query TF32), "
+                "6 tc_single (wide kernels without CTA pairs)");
   g_path = path;
+  hsd::sim_wide_set_single(path == kPathTcSingle);
   return HSD_OK;
 }
 

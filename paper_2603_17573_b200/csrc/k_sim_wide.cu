@@ -670,15 +670,16 @@ cudaError_t launch_pair(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb
   return cudaGetLastError();
 }
 
-// CTA-pair kernel for a single group of 129..256 queries; HSD_WIDE_PAIR=0
-// selects the single-CTA kernel instead (ablation).
+// CTA-pair kernels above 128 queries; HSD_WIDE_PAIR=0 or the tc_single path
+// override (hsd_set_sim_path) select the single-CTA kernels (ablation).
+int g_force_single = 0;
 bool pair_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HSD_WIDE_PAIR");
     v = (e && !strcmp(e, "0")) ? 0 : 1;
   }
-  return v == 1;
+  return v == 1 && !g_force_single;
 }
 
 // Accumulator layout per NS: "db" = double-buffered (256 columns per buffer;
@@ -713,6 +714,7 @@ cudaError_t launch_dispatch(int NS, const CUtensorMap& km, const CUtensorMap& qm
 }  // namespace
 
 int sim_wide_max_batch() { return 1024; }
+void sim_wide_set_single(bool single) { g_force_single = single ? 1 : 0; }
 
 // Query groups (cluster size) of one pass: B <= 256 -> 1 CTA per key range;
 // more -> ceil(B / 256) CTAs per cluster sharing each key tile by multicast.

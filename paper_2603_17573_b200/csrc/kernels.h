@@ -60,6 +60,7 @@ cudaError_t launch_sim_tc1(const float* keys, int64_t n_keys_total, int64_t row_
 // N = 64/128/256), fp32 keys read as TF32 or bf16 keys (kind::f16); same
 // partial-list contract.  scratch: sim_wide_scratch_bytes(dim).
 int sim_wide_max_batch();
+void sim_wide_set_single(bool single);  // ablation: no CTA-pair kernels
 // partial lists (= persistent CTAs, or clusters when B > 256) of a wide pass
 int sim_wide_lists(int B, int64_t rows, int num_sms);
 double sim_wide_gamma(int dim, int key_dtype);

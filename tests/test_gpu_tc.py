@@ -115,19 +115,25 @@ def test_wide_scores_within_bound(torch, kind, dim, n, B, dtype):
         assert np.array_equal(approx, exact)
 
 
+@pytest.mark.parametrize("path", ["auto", "tc_single"])
 @pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
-def test_wide_batches_bit_identical(torch, kind):
-    """One pass serves up to 256 queries; B > 256 takes several passes."""
-    for dim, n in ((64, 4000), (4096, 1800)):
-        col = H.Collection(dim, capacity=n)
-        col.generate(kind, 21, n)
-        for B in (5, 65, 127, 128, 129, 200, 256, 300, 513, 700, 1024, 1100):
-            q = H.gen_queries(kind, 22, 21, n, 1, B, dim)
-            sc, ids = col.search_topk_exact(q, 8)
-            osc, oid = O.search_synth(kind, 21, n, q.cpu().numpy(), 8)
-            np.testing.assert_array_equal(ids.cpu().numpy(), oid, err_msg=f"dim={dim} B={B}")
-            np.testing.assert_array_equal(sc.cpu().numpy(), osc)
-        assert col.overflow_count() == 0
+def test_wide_batches_bit_identical(torch, kind, path):
+    """One pass serves up to 1024 queries (CTA pairs above 128, clusters of
+    query groups above 256); tc_single = the single-CTA kernels (ablation)."""
+    H.set_sim_path(path)
+    try:
+        for dim, n in ((64, 4000), (4096, 1800)):
+            col = H.Collection(dim, capacity=n)
+            col.generate(kind, 21, n)
+            for B in (5, 65, 127, 128, 129, 200, 256, 300, 513, 700, 1024, 1100):
+                q = H.gen_queries(kind, 22, 21, n, 1, B, dim)
+                sc, ids = col.search_topk_exact(q, 8)
+                osc, oid = O.search_synth(kind, 21, n, q.cpu().numpy(), 8)
+                np.testing.assert_array_equal(ids.cpu().numpy(), oid, err_msg=f"dim={dim} B={B}")
+                np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+            assert col.overflow_count() == 0
+    finally:
+        H.set_sim_path("auto")
 
 
 @pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
