@@ -50,7 +50,22 @@ def test_verify_parity_large_round(torch, L):
     _parity(torch, L, 8, 1100)
 
 
-def _parity(torch, L, k, E):
+def test_verify_skip_threshold_at_the_exact_similarity(torch):
+    """min_S equal to an episode's exactly rounded similarity (R >= min_S holds
+    with equality) and one ulp above it: only an exactly rounded dot decides
+    these like the oracle."""
+    E, d_f = 64, 256
+    now, prev = O.gen_features(9, 0, E, d_f)
+    cos = [O.feature_cos(now[e], prev[e]) for e in range(4)]
+    sweep = [H.VerifyParams.make(relaxed=True, skip_enabled=True, min_S=c, O_dist=8) for c in cos]
+    sweep += [H.VerifyParams.make(relaxed=True, skip_enabled=True, min_S=float(np.nextafter(c, 2.0)), O_dist=8)
+              for c in cos]
+    stats = _parity(torch, 7, 8, E, sweep=sweep, feats=(now, prev))
+    assert stats["skipped"] > 0
+
+
+def _parity(torch, L, k, E, sweep=None, feats=None):
+    sweep = SWEEP if sweep is None else sweep
     n, d_f = 400, 256
     db_seed, lseed, fseed = 21, 5, 9
     col = H.Collection(64, capacity=n)
@@ -64,11 +79,11 @@ def _parity(torch, L, k, E):
     src = np.where(rng.random(E) < 0.7, ids[:, 0], -1).astype(np.int64)
     src[ids[:, 0] < 0] = -1
     logits = O.gen_logits(db_seed, lseed, src, 0, L)
-    now, prev = O.gen_features(fseed, 0, E, d_f)
+    now, prev = O.gen_features(fseed, 0, E, d_f) if feats is None else feats
     hist = rng.integers(0, 8, size=E).astype(np.int32)
     gap_d = 2
     t = lambda a: torch.as_tensor(a, device="cuda")
-    out, toks = col.verify_round(t(ids), t(logits), SWEEP, feat_now=t(now), feat_prev=t(prev), history=t(hist),
+    out, toks = col.verify_round(t(ids), t(logits), sweep, feat_now=t(now), feat_prev=t(prev), history=t(hist),
                                  gap_d=gap_d)
     toks = toks.cpu().numpy()
     tok_db = O.synth_tokens(db_seed, np.arange(n))[:, :L].astype(np.int32)
@@ -78,7 +93,7 @@ def _parity(torch, L, k, E):
         drafts = tok_db[valid]
         greedy = np.array([O.argmax(logits[e, p]) for p in range(L)], np.int32)
         cosv = O.feature_cos(now[e], prev[e])
-        for pi, p in enumerate(SWEEP):
+        for pi, p in enumerate(sweep):
             o = oracle_round(drafts, greedy, cosv, int(hist[e]), gap_d, p)
             g = out[pi, e]
             got = (g["accept_len"], g["fallback"], g["skipped"], g["calls"], g["n_emit"])
@@ -94,7 +109,9 @@ def _parity(torch, L, k, E):
             stats["fallback"] += o.fallback
             stats["partial"] += 0 < o.accept_len < L
     # every branch is exercised
-    assert all(v > 0 for v in stats.values()), stats
+    if sweep is SWEEP:
+        assert all(v > 0 for v in stats.values()), stats
+    return stats
 
 
 def test_verify_validation(torch):
