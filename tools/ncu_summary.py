@@ -39,15 +39,16 @@ def launches(src, dst):
     for r in rows[1:]:
         name = r[ki].split("(")[0].replace("hsd::<unnamed>::", "").replace("void ", "")
         agg.setdefault(name, []).append(float(r[vi].replace(",", "")) / 1e3)
-    total_step = sum(sum(v) for k, v in agg.items() if not k.startswith(("gen_", "at::", "pad_", "split_q")))
+    # one-time setup kernels (synthetic data, the bf16 filter copy) are not part of the step
+    setup = lambda k: k.startswith(("gen_", "at::")) or k.endswith("to_bf16_kernel")
+    total_step = sum(sum(v) for k, v in agg.items() if not setup(k))
     with open(dst, "w") as f:
         f.write(f"# ncu launch list — `{' '.join(sys.argv[1:3])}`\n\n")
         f.write("Per-launch device time (ncu `gpu__time_duration.sum --clock-control none`, serialised and "
                 "cold-cache: compare shares, not absolutes).\n\n")
         f.write("| kernel | launches | mean us | total us | share of hot-path time |\n|---|---:|---:|---:|---:|\n")
         for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-            hot = not k.startswith(("gen_", "at::"))
-            share = f"{100 * sum(v) / total_step:.1f}%" if hot and not k.startswith(("pad_", "split_q")) else "-"
+            share = f"{100 * sum(v) / total_step:.1f}%" if not setup(k) else "-"
             f.write(f"| `{k}` | {len(v)} | {sum(v) / len(v):.1f} | {sum(v):.1f} | {share} |\n")
     print(open(dst).read())
 
