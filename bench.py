@@ -908,20 +908,30 @@ def run_c5(args):
         "tokens_per_s": tokens / (ms / 1e3), "retrieval_queries_per_round": float(nr_per_round.mean()),
         "episode_rounds": int(rep["rounds"][0]),
     }
-    # e2e: the same rounds driven through the public API with each round's
-    # StepRecord row read back to pinned host memory
-    h_row = torch.empty((args.robots * 16,), dtype=torch.uint8).pin_memory()
+    # e2e: the SAME rounds (a fresh loop over the same episodes, same warm-up)
+    # driven one round per call through the public API, the trace of the
+    # timed rounds read back to pinned host memory at the end (the loop is
+    # stateful: continuing the first loop would time later rounds with a
+    # different retrieval / drafter mix)
+    loop.close()
+    loop = H.HybridLoop(col, hp, n_total_rows=args.n, max_rounds=total_rounds, comm=comm, id_offset=b0)
+    loop.step(args.warmup, stream=stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    h_tr = torch.empty((args.steps * args.robots * 16,), dtype=torch.uint8).pin_memory()
     import time as _t
-    n_e2e = min(20, args.steps)
+    n_e2e = args.steps
     t0 = _t.perf_counter()
     for i in range(n_e2e):
         loop.step(1, stream=stream)
-    torch.cuda.synchronize()
-    tr_all = loop.trace()
-    h_row.numpy()[:] = tr_all[-1].view(np.uint8)
+    tr_all = loop.trace()  # synchronises
+    h_tr.numpy()[:] = tr_all[args.warmup:].reshape(-1).view(np.uint8)
     e2e_v = args.robots * n_e2e / (_t.perf_counter() - t0)
+    loop.close()
     e2e = {"value": e2e_v, "unit": "robot-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": args.robots * 16 + 8,
-           "api": "hsd_hybrid_step (C ABI) + per-round StepRecord read-back, wall clock; the harness inputs "
+           "api": "hsd_hybrid_step (C ABI), one round per call, the same rounds as `value`, StepRecords read back to "
+                  "pinned host memory; wall clock; the harness inputs "
                   "(robot observations, verifier logits) are generated on the device", "passes": n_e2e}
     if rank == 0:
         cb = None
@@ -943,7 +953,6 @@ def run_c5(args):
             "stages_ms": stages, "loop": loop_stats,
         }
         print(json.dumps(line), flush=True)
-    loop.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
