@@ -391,6 +391,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int grp = cr >> 1;           // query group of this pair
   const uint32_t leader = (uint32_t)(cr & ~1);
   const int q_base = grp * kPairQ;
+  // UMMA N of this pair: its group's queries rounded up to 32 (the last group
+  // of a pass is usually partial; the MMA work scales with N).  The leader
+  // stages queries [0, N/2) of the group, the peer [N/2, N).
+  const int n_grp = B - q_base < kPairQ ? B - q_base : kPairQ;
+  const int n_mma = (n_grp + 31) & ~31;
+  const int n_half = n_mma / 2;
   const uint16_t pair_mask = (uint16_t)(3u << (2 * grp));
   const uint16_t all_mask = (uint16_t)((1u << (2 * kG)) - 1);
   uint16_t half_mask = 0;  // the kG CTAs holding the same key half
@@ -472,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (rank == 0) mbar_expect_tx(&S.q_full[qs], 2 * kPairQTile);
           const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
           tma_load_2d_pair(&S.qbuf[qs][0], &q_map, mapa_shared(smem_u32(&S.q_full[qs]), leader), c * kBK,
-                           q_base + rank * kPairHalfQ, pol);
+                           q_base + rank * n_half, pol);
           if (++qs == kPairQS) {
             qs = 0;
             qph ^= 1;
@@ -482,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ======================= MMA issuer (leader only)
     if (rank == 0) {
-      constexpr uint32_t idesc = kBf16 ? bf16_idesc(2 * kBM, kPairQ) : tf32_idesc(2 * kBM, kPairQ);
+      const uint32_t idesc = kBf16 ? bf16_idesc(2 * kBM, n_mma) : tf32_idesc(2 * kBM, n_mma);
       const uint64_t adesc0 = sw128_desc(&S.kbuf[0][0]);
       const uint64_t bdesc0 = sw128_desc(&S.qbuf[0][0]);
       int ks = 0, qs = 0;
@@ -538,12 +544,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&S.acc_full[buf], (uint32_t)(gi / 2) & 1);
       tc_fence_after();
       const int64_t base = row_begin + (blk0 + 2 * gi + rank) * kBM;
+      const int nj = n_mma / kStgQ;  // staging rounds holding this pair's columns
 #pragma unroll
       for (int j = 0; j < kPairQ / kStgQ; ++j) {
+        if (j >= nj) break;
         uint32_t acc[16];
         TMEM_LD16(tmem + lane_addr + buf * kPairQ + j * kStgQ + half * 16, acc);
         tmem_ld_wait();
-        if (j == kPairQ / kStgQ - 1) {  // buffer drained
+        if (j == nj - 1) {  // buffer drained
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(buf ? leader_empty1 : leader_empty0);
