@@ -380,7 +380,7 @@ template <bool kBf16, int kG>
 __global__ void __launch_bounds__(kThreads, 1)
     sim_pair_kernel(const __grid_constant__ CUtensorMap keys_map, const __grid_constant__ CUtensorMap q_map,
                     int64_t row_begin, int64_t row_end, int dim, int B, int64_t blocks_per_pair,
-                    uint64_t* __restrict__ partial) {
+                    int per_group, uint64_t* __restrict__ partial) {
   constexpr int kBK = kBf16 ? 64 : 32;
   constexpr int kMyQ = kPairQ / kEpiWarps;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -390,12 +390,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int rank = cr & 1;           // 0 = pair leader
   const int grp = cr >> 1;           // query group of this pair
   const uint32_t leader = (uint32_t)(cr & ~1);
-  const int q_base = grp * kPairQ;
-  // UMMA N of this pair: its group's queries rounded up to 32 (the last group
-  // of a pass is usually partial; the MMA work scales with N).  The leader
-  // stages queries [0, N/2) of the group, the peer [N/2, N).
-  const int n_grp = B - q_base < kPairQ ? B - q_base : kPairQ;
-  const int n_mma = (n_grp + 31) & ~31;
+  // The pass's B queries are split evenly over the kG pairs (per_group, a
+  // multiple of 16, <= 256): the pairs of a cluster run in lockstep on shared
+  // key tiles, so the widest group sets the pace.  UMMA N of this pair = its
+  // group's queries rounded up to 16; the leader stages queries [0, N/2) of
+  // the group, the peer [N/2, N).
+  const int q_base = grp * per_group;
+  const int n_grp = B - q_base < per_group ? (B - q_base > 0 ? B - q_base : 0) : per_group;
+  const int n_mma = (n_grp + 15) & ~15;
   const int n_half = n_mma / 2;
   const uint16_t pair_mask = (uint16_t)(3u << (2 * grp));
   const uint16_t all_mask = (uint16_t)((1u << (2 * kG)) - 1);
@@ -544,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&S.acc_full[buf], (uint32_t)(gi / 2) & 1);
       tc_fence_after();
       const int64_t base = row_begin + (blk0 + 2 * gi + rank) * kBM;
-      const int nj = n_mma / kStgQ;  // staging rounds holding this pair's columns
+      const int nj = (n_mma + kStgQ - 1) / kStgQ;  // staging rounds holding this pair's columns
 #pragma unroll
       for (int j = 0; j < kPairQ / kStgQ; ++j) {
         if (j >= nj) break;
@@ -559,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int t = 0; t < 16; ++t) S.stg[r * kStg + half * 16 + t] = __uint_as_float(acc[t]);
         named_sync(1, 32 * kEpiWarps);
-        epi_insert_round(S.stg, ew, lane, j, B - q_base, base, row_hi, top);
+        epi_insert_round(S.stg, ew, lane, j, n_grp, base, row_hi, top);
         named_sync(1, 32 * kEpiWarps);
       }
     }
@@ -568,8 +570,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < kPairQ / kStgQ; ++j)
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int q = q_base + j * kStgQ + ew * 4 + i;
-        if (q < B) partial[((size_t)list * B + q) * kCandLocal + lane] = top[j * 4 + i];
+        const int ql = j * kStgQ + ew * 4 + i;
+        if (ql < n_grp) partial[((size_t)list * B + q_base + ql) * kCandLocal + lane] = top[j * 4 + i];
       }
   }
   tc_fence_before();
@@ -657,6 +659,7 @@ cudaError_t launch_ns(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, 
 template <bool kBf16, int kG>
 cudaError_t launch_pair(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, int64_t re, int dim, int B,
                         int lists, int64_t per_pair, uint64_t* partial, cudaStream_t s) {
+  const int per_group = (((B + kG - 1) / kG) + 15) & ~15;  // <= 256: kG = ceil(B / 256)
   const size_t smem = sizeof(PairSmem) + 1024;
   auto kern = sim_pair_kernel<kBf16, kG>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -673,7 +676,7 @@ cudaError_t launch_pair(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, km, qm, rb, re, dim, B, per_pair, partial);
+  e = cudaLaunchKernelEx(&cfg, kern, km, qm, rb, re, dim, B, per_pair, per_group, partial);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
