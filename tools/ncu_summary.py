@@ -19,7 +19,7 @@ FULL_METRICS = [
     ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("dram__bytes.sum.per_second", "DRAM bandwidth"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
