@@ -7,6 +7,15 @@
 namespace hsd {
 namespace dev {
 
+// ---- programmatic dependent launch (PDL) -------------------------------------
+// The small kernels of the step (K2's three launches, K4) are launched with
+// programmatic stream serialization: a kernel lets its dependent launch as
+// soon as all its CTAs are resident (pdl_trigger at entry), and the dependent
+// blocks in pdl_wait until the predecessor grid has completed and its memory
+// is visible.  Every dependent calls pdl_wait before touching any input.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 constexpr int kWarp = 32;
 constexpr int kCandLocal = 32;     // candidates kept per (CTA, query) by the similarity kernels
 constexpr uint64_t kEmpty = ~0ull; // empty candidate slot (sorts last)
@@ -123,4 +132,22 @@ __device__ __forceinline__ uint64_t score_desc_key(double d) {
 }
 
 }  // namespace dev
+}  // namespace hsd
+
+namespace hsd {
+// Launch `kern` as a programmatic dependent of the previous kernel on `s`.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 }  // namespace hsd

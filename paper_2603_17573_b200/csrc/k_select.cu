@@ -64,6 +64,8 @@ __global__ void __launch_bounds__(kThreads) select_cand_kernel(const uint64_t* _
                                                                const unsigned long long* __restrict__ maxnorm_bits,
                                                                double gamma, SelScratch* __restrict__ scr) {
   __shared__ CandSmem S;
+  dev::pdl_wait();  // K1's partial lists
+  dev::pdl_trigger();
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* qrow = queries + (size_t)b * dim;
@@ -175,6 +177,8 @@ __global__ void __launch_bounds__(kRThreads) rescore_kernel(const KT* __restrict
   auto& qs = *reinterpret_cast<float(*)[2][kW]>(smem_raw + sizeof(KT) * 2 * kPer * kStride);
   auto& qd = *reinterpret_cast<double(*)[kW]>(smem_raw + sizeof(KT) * 2 * kPer * kStride + sizeof(float) * 2 * kW);
   __shared__ uint32_t ids[kPer];
+  dev::pdl_wait();  // the candidate lists
+  dev::pdl_trigger();
   const int b = blockIdx.x, c0 = blockIdx.y * kPer;
   SelScratch& o = scr[b];
   const int n = min(o.n - c0, kPer);
@@ -265,6 +269,8 @@ __global__ void __launch_bounds__(kThreads) rank_kernel(const SelScratch* __rest
   // time of the fp64 (x > s) || (x == s && ...) form (6 vs 12 us at n ~ 100)
   __shared__ uint64_t key[kCandMax];
   __shared__ uint32_t id[kCandMax];
+  dev::pdl_wait();  // the exact scores
+  dev::pdl_trigger();
   const int b = blockIdx.x, tid = threadIdx.x;
   const SelScratch& o = scr[b];
   const int n = o.n;
@@ -367,8 +373,8 @@ cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, cons
   if (B <= 0) return cudaSuccess;
   if (key_dtype == HSD_DTYPE_BF16 && dim % 8) return cudaErrorInvalidValue;
   SelScratch* scr = reinterpret_cast<SelScratch*>(scratch);
-  select_cand_kernel<<<B, kThreads, 0, s>>>(partial, lists, B, k, dim, queries, maxnorm_bits, gamma, scr);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(select_cand_kernel, dim3(B), dim3(kThreads), 0, s, partial, lists, B, k, dim, queries,
+                             maxnorm_bits, gamma, scr);
   if (e != cudaSuccess) return e;
   const dim3 grid(B, kCandMax / kPer);
   // the kernel's occupancy is set by shared memory: ask for the full carveout
@@ -389,15 +395,13 @@ cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, cons
     configured.fetch_or(1ull << dev);
   }
   if (key_dtype == HSD_DTYPE_BF16)
-    rescore_kernel<uint16_t><<<grid, kRThreads, sm16, s>>>((const uint16_t*)keys, dim, queries, scr);
+    e = launch_pdl(rescore_kernel<uint16_t>, grid, dim3(kRThreads), sm16, s, (const uint16_t*)keys, dim, queries, scr);
   else
-    rescore_kernel<float><<<grid, kRThreads, sm32, s>>>((const float*)keys, dim, queries, scr);
-  e = cudaGetLastError();
+    e = launch_pdl(rescore_kernel<float>, grid, dim3(kRThreads), sm32, s, (const float*)keys, dim, queries, scr);
   if (e != cudaSuccess) return e;
   P2PPublish pb{};
   if (pub) pb = *pub;
-  rank_kernel<<<B, kThreads, 0, s>>>(scr, k, scores, ids, overflow, pb, pub ? 1 : 0);
-  return cudaGetLastError();
+  return launch_pdl(rank_kernel, dim3(B), dim3(kThreads), 0, s, scr, k, scores, ids, overflow, pb, pub ? 1 : 0);
 }
 
 cudaError_t launch_merge_ranks(const double* g_scores, const int32_t* g_ids, const uint8_t* g_tok, int G, int B, int k,

@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (kMC > 1) cluster_sync_all();  // peers' barriers exist before any multicast / remote arrive
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
+  dev::pdl_trigger();  // K2's first kernel may launch onto free SM resources and wait there
 
   if (warp == 0) {
     // ======================= key stream (HBM)
@@ -438,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync_all();  // the leader's barriers exist before any peer TMA / remote arrive
   tc_fence_after();
   const uint32_t tmem = S.tmem_base;
+  dev::pdl_trigger();  // K2's first kernel may launch onto free SM resources and wait there
 
   if (warp == 0) {
     // ======================= key stream: this CTA's block of each pair step

@@ -349,6 +349,8 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) verify_kernel(const
                                                              hsd_outcome* __restrict__ out,
                                                              uint8_t* __restrict__ tok_out) {
   __shared__ WarpScratch sw[kWarps];
+  dev::pdl_wait();  // the retrieved ids (K2)
+  dev::pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const int e = blockIdx.x * kWarps + warp;
   if (e >= E) return;
@@ -438,10 +440,9 @@ cudaError_t launch_verify(const int32_t* ids, int E, int k, int L, const uint8_t
                           const int32_t* history, int gap_d, const hsd_verify_params* params_dev, int P, int need_cos,
                           hsd_outcome* out, uint8_t* tok_out, cudaStream_t s, const double* cos_in) {
   if (E <= 0) return cudaSuccess;
-  verify_kernel<<<(E + kWarps - 1) / kWarps, kThreads, 0, s>>>(ids, E, k, L, tokens, cand_tokens, logits, feat_now,
-                                                                feat_prev, d_f, history, gap_d, params_dev, P, need_cos,
-                                                                cos_in, out, tok_out);
-  return cudaGetLastError();
+  return launch_pdl(verify_kernel, dim3((E + kWarps - 1) / kWarps), dim3(kThreads), 0, s, ids, E, k, L, tokens,
+                    cand_tokens, logits, feat_now, feat_prev, d_f, history, gap_d, params_dev, P, need_cos, cos_in, out,
+                    tok_out);
 }
 
 // Pre-gather the payload tokens of a [n] id list (sharded search records).
