@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 3) {
     // ======================= query tiles (L2-resident, reused by gb key tiles)
     if (lane == 0 && blk0 < blk1) {
+      dev::pdl_wait();  // the padded query slab (the key stream above does not need it)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&q_map) : "memory");
       const uint64_t pol = policy_evict_last();
       int qs = 0;
@@ -472,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 3) {
     // ======================= query half tiles (L2-resident)
     if (lane == 0 && steps > 0) {
+      dev::pdl_wait();  // the padded query slab
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&q_map) : "memory");
       const uint64_t pol = policy_evict_last();
       int qs = 0;
@@ -594,6 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kPadThreads = 256, kPadVec = 4;
 __global__ void __launch_bounds__(kPadThreads) pad_queries_f32_kernel(const float* __restrict__ q, int B, int dim,
                                                                       float* __restrict__ out) {
+  dev::pdl_trigger();  // K1 may launch and start its key stream now
   const int row = blockIdx.x, n4 = dim / 4;
   const float4* src = reinterpret_cast<const float4*>(q + (size_t)row * dim);
   float4* dst = reinterpret_cast<float4*>(out + (size_t)row * dim);
@@ -611,6 +614,7 @@ __global__ void __launch_bounds__(kPadThreads) pad_queries_f32_kernel(const floa
 }
 __global__ void __launch_bounds__(kPadThreads) pad_queries_bf16_kernel(const float* __restrict__ q, int B, int dim,
                                                                        uint16_t* __restrict__ out) {
+  dev::pdl_trigger();  // K1 may launch and start its key stream now
   const int row = blockIdx.x, n4 = dim / 4;
   const float4* src = reinterpret_cast<const float4*>(q + (size_t)row * dim);
   uint2* dst = reinterpret_cast<uint2*>(out + (size_t)row * dim);
@@ -637,24 +641,24 @@ cudaError_t launch_ns(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, 
   auto kern = sim_wide_kernel<kBf16, NS, GB, kDump, kMC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if constexpr (kMC == 1) {
-    kern<<<lists, kThreads, smem, s>>>(km, qm, rb, re, dim, B, per, partial, dump);
-  } else {  // `lists` clusters of kMC CTAs
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(lists * kMC));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kMC;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, km, qm, rb, re, dim, B, per, partial, dump);
-    if (e != cudaSuccess) return e;
-  }
+  // programmatic dependent of the query-slab kernel: the CTAs set up and start
+  // the key stream while the slab is written (only the query producer waits)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(lists * kMC));  // kMC > 1: `lists` clusters of kMC CTAs
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = kMC;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kMC > 1 ? 2 : 1;
+  e = cudaLaunchKernelEx(&cfg, kern, km, qm, rb, re, dim, B, per, partial, dump);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -671,13 +675,15 @@ cudaError_t launch_pair(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2 * kG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // after the query-slab kernel
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   e = cudaLaunchKernelEx(&cfg, kern, km, qm, rb, re, dim, B, per_pair, per_group, partial);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
