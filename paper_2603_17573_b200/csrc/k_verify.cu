@@ -74,6 +74,11 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
                                                const double* __restrict__ cos_in, hsd_outcome* __restrict__ out,
                                                uint8_t* __restrict__ tok_out, WarpScratch& W) {
   const int lane = threadIdx.x & 31;
+  // The candidate ids (and then their token rows) do not depend on the logits
+  // or the features: issue them first so their round trips overlap the
+  // logits / feature phases instead of following them.
+  const int32_t* my_ids = ids + (size_t)e * k;
+  const int id = lane < k ? my_ids[lane] : -1;
   // ---- greedy tokens: argmax per position, lowest index on ties.  The 7
   //      positions of an action slice are loaded before any is reduced (7 KB
   //      in flight per warp) — the kernel is HBM-bound at C3's 4096 episodes.
@@ -108,6 +113,19 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
       if (lane == 0) W.greedy[p0 + u] = bi;
     }
   }
+
+  // ---- the candidates' draft tokens: cp.async into this warp's staging rows
+  //      (completes under the feature stream; waited for before the dedup)
+  if (id >= 0) {
+    const uint8_t* row = cand_tokens ? cand_tokens + ((size_t)e * k + lane) * HSD_TOKENS_STRIDE
+                                     : tokens + (size_t)id * HSD_TOKENS_STRIDE;
+#pragma unroll
+    for (int i = 0; i < kTokStride / 4; ++i) {
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&W.tok[lane][4 * i]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(row + 4 * i) : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 
   // ---- verify-skip similarity: exactly rounded dot (double-double; the
   //      result is the exact sum rounded once, so the order is free and
@@ -165,22 +183,9 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
     cosv = s;
   }
 
-  // ---- gather the candidates' draft tokens
-  const int32_t* my_ids = ids + (size_t)e * k;
-  int n_cand = 0;
-  {
-    const int id = lane < k ? my_ids[lane] : -1;
-    const unsigned m = __ballot_sync(0xffffffffu, id >= 0);
-    n_cand = __popc(m);  // ids are rank-ordered with -1 padding at the end
-    if (id >= 0) {
-      const uint8_t* row = cand_tokens ? cand_tokens + ((size_t)e * k + lane) * HSD_TOKENS_STRIDE
-                                       : tokens + (size_t)id * HSD_TOKENS_STRIDE;
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(row);
-      uint32_t* dst = reinterpret_cast<uint32_t*>(W.tok[lane]);
-#pragma unroll
-      for (int i = 0; i < kTokStride / 4; ++i) dst[i] = __ldg(src + i);
-    }
-  }
+  // ---- the gathered draft tokens have landed
+  const int n_cand = __popc(__ballot_sync(0xffffffffu, id >= 0));  // ids are rank-ordered, -1 padding last
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
   const int* greedy = W.greedy;  // positions < L (shared memory, no per-thread copy)
   const int hist = history ? history[e] : 0x7fffffff;
