@@ -81,6 +81,9 @@ def parse():
                         "query searches all shards (local top-k + NCCL all-gather + merge, strong scaling)")
     p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "bf16", "c5"])
     p.add_argument("--graph", action="store_true", help="replay each decode round from a captured CUDA graph")
+    p.add_argument("--pipeline", type=int, default=0,
+                   help="engines (one stream each) the steps alternate over; 0 = auto (2 when the scanned DB "
+                        "exceeds L2, else 1)")
     p.add_argument("--robots", type=int, default=1024, help="C5 robots")
     p.add_argument("--traj-T", type=int, default=500, help="C5 demonstration length (actions) per DB episode")
     p.add_argument("--k-top", type=int, default=3, help="C5 K_top (SPEC default 3)")
@@ -378,6 +381,9 @@ def config_of(args, world):
               f"inputs larger than L2 ({args.n * args.dim * (2 if args.dtype == 'bf16' or args.filter == 'bf16_copy' else 4) / 1e9:.1f} GB of keys "
               f"streamed per pass)",
         "verify": "relaxed 30/15, verify-skip min_S=0.95 O_dist=5 d=1, chain cap 64",
+        "pipeline": (f"{getattr(args, 'pipe', 1)} engine(s) on as many streams, steps alternating: step i+1's "
+                     f"similarity scan runs while step i's select / verify finish"
+                     if getattr(args, "pipe", 1) > 1 else "1 engine, steps back to back on one stream"),
     }
 
 
@@ -426,22 +432,51 @@ def run_ours(args):
     hist = torch.full((B,), 100, dtype=torch.int32, device=dev)
     vp = H.VerifyParams.make(relaxed=True, bias_seq_max=30, bias_token_max=15, skip_enabled=True, min_S=0.95, O_dist=5)
 
+    post_steps = None
+    engs, strs = [], []
     if (world == 1 or replicas) and not args.force_sharded:
-        eng = H.Engine(col, B, k, L, d_f, 15)
-        outs = dict(scores=torch.empty((B, k), dtype=torch.float64, device=dev),
-                    ids=torch.empty((B, k), dtype=torch.int32, device=dev),
-                    out=torch.empty((B, 20), dtype=torch.uint8, device=dev),
-                    tokens=torch.empty((B, L), dtype=torch.uint8, device=dev),
-                    R=torch.empty(B, dtype=torch.float64, device=dev), D=torch.empty(B, dtype=torch.float64, device=dev),
-                    F=torch.empty(B, dtype=torch.float64, device=dev),
-                    decision=torch.empty(B, dtype=torch.int32, device=dev))
-        bufs = [H.StepBuffers(queries=qs[s], logits=lg[s], feat_now=feats[s][0], feat_prev=feats[s][1], xyz=xyz[s],
-                              history=hist, **outs) for s in range(S)]
+        # Steps are independent batches of episodes.  With `pipe` engines on
+        # `pipe` streams (steps alternating), step i+1's K1 streams the DB while
+        # step i's K2 / K4 finish: the small latency-bound kernels leave the
+        # HBM-bound K1 back to back.  Config 1 (L2 flushed around every step's
+        # event bracket) keeps one engine.
+        scanned = (b1 - b0) * dim * (2 if (args.dtype == "bf16" or args.filter == "bf16_copy") else 4)
+        pipe = args.pipeline if args.pipeline > 0 else (1 if scanned < 2 * 126e6 else 2)
+        args.pipe = pipe
+        engs = [H.Engine(col, B, k, L, d_f, 15) for _ in range(pipe)]
+        strs = [stream] + [torch.cuda.Stream(device=dev) for _ in range(pipe - 1)]
+
+        def mk_outs():
+            return dict(scores=torch.empty((B, k), dtype=torch.float64, device=dev),
+                        ids=torch.empty((B, k), dtype=torch.int32, device=dev),
+                        out=torch.empty((B, 20), dtype=torch.uint8, device=dev),
+                        tokens=torch.empty((B, L), dtype=torch.uint8, device=dev),
+                        R=torch.empty(B, dtype=torch.float64, device=dev),
+                        D=torch.empty(B, dtype=torch.float64, device=dev),
+                        F=torch.empty(B, dtype=torch.float64, device=dev),
+                        decision=torch.empty(B, dtype=torch.int32, device=dev))
+        outs = [mk_outs() for _ in range(pipe)]
+        bufs = [[H.StepBuffers(queries=qs[s], logits=lg[s], feat_now=feats[s][0], feat_prev=feats[s][1], xyz=xyz[s],
+                               history=hist, **outs[j]) for s in range(S)] for j in range(pipe)]
+        ev_fork = torch.cuda.Event()
 
         def step(i):
-            eng.step(B, bufs[i % S], vp, gap_d=1, stream=stream, graph=args.graph)
-        # K5 + skip similarity (side stream), pad queries, K1, K2 (3 kernels), K4 — eager or as one graph's nodes
+            j = i % pipe
+            if i == 0 and pipe > 1:  # the other streams start after everything before on the main stream
+                ev_fork.record(stream)
+                for t in strs[1:]:
+                    t.wait_event(ev_fork)
+            engs[j].step(B, bufs[j][i % S], vp, gap_d=1, stream=strs[j], graph=args.graph)
+
+        def join():  # the main stream's next event covers every stream's steps
+            for t in strs[1:]:
+                e = torch.cuda.Event()
+                e.record(t)
+                stream.wait_event(e)
+        post_steps = join if pipe > 1 else None
+        # K5 + skip similarity (side stream), query slab, K1, K2 (3 kernels), K4 — eager or as one graph's nodes
         launches_per_step = 8
+        eng = engs[0]
     else:
         comm = setup_comm(H, dist, world, rank, local, args.exchange, max_B=B, k_max=k)
         lo, hi = H.shard_range(B, world, rank)  # this rank's episodes
@@ -472,8 +507,8 @@ def run_ours(args):
     for i in range(args.warmup):
         step(i)
     barrier()
-    if eng is not None:
-        eng.enable_timing(args.steps)
+    for en in engs:
+        en.enable_timing(args.steps)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     # A DB that fits in L2 (config 1: 82 MB scanned per step) would stay cached
@@ -494,6 +529,8 @@ def run_ours(args):
             step(i)
             if flush:
                 evs[i][1].record(stream)
+        if post_steps is not None:
+            post_steps()
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1) if not flush else sum(a.elapsed_time(b) for a, b in evs)
@@ -506,11 +543,14 @@ def run_ours(args):
 
     stages = None
     roof = None
-    if eng is not None and args.graph:  # graph replays carry no stage events: time eager rounds of the same shape
+    if eng is not None and (args.graph or getattr(args, "pipe", 1) > 1):
+        # graph replays carry no stage events, and with steps in flight on several
+        # streams a stage's events also cover the wait for the other steps'
+        # kernels: time eager back-to-back steps of the same shape on one engine
         eng.stage_times()
         eng.enable_timing(min(args.steps, 50))
         for i in range(min(args.steps, 50)):
-            eng.step(B, bufs[i % S], vp, gap_d=1, stream=stream)
+            eng.step(B, bufs[0][i % S], vp, gap_d=1, stream=stream)
         torch.cuda.synchronize()
     if eng is not None:
         n_rec, st = eng.stage_times()
@@ -539,7 +579,7 @@ def run_ours(args):
     # ---- e2e through the public host-buffer API (hsd_step_host_async)
     e2e = None
     if eng is not None:
-        e2e = run_e2e(H, torch, eng, args, qs, lg, feats, xyz_np, vp, stream)
+        e2e = run_e2e(H, torch, engs, args, qs, lg, feats, xyz_np, vp, strs)
         if replicas:  # whole job: the slowest rank's rate x ranks
             e2e["value"] = reduce_scalar(dist, torch, e2e["value"], "min") * world
             e2e["note"] = "min over ranks x ranks (each rank its own episodes)"
@@ -619,7 +659,7 @@ def setup_comm(H, dist, world, rank, local, exchange="p2p", max_B=1024, k_max=32
     return H.Comm(obj[0], world, rank, local)
 
 
-def run_e2e(H, torch, eng, args, qs, lg, feats, xyz_np, vp, stream):
+def run_e2e(H, torch, engs, args, qs, lg, feats, xyz_np, vp, strs):
     B, k, L, d_f, dim = args.batch, args.k, args.L, args.d_f, args.dim
     pin = lambda t: t.cpu().pin_memory()
     S = len(qs)
@@ -634,27 +674,35 @@ def run_e2e(H, torch, eng, args, qs, lg, feats, xyz_np, vp, stream):
                     D=torch.empty(B, dtype=torch.float64).pin_memory(),
                     F=torch.empty(B, dtype=torch.float64).pin_memory(),
                     decision=torch.empty(B, dtype=torch.int32).pin_memory())
-    bufs = [H.StepBuffers(**host_in[s], **host_out) for s in range(S)]
+    pipe = len(engs)
+    # per engine its own pinned outputs (steps in flight on different engines)
+    host_outs = [host_out] + [{kk: torch.empty_like(v).pin_memory() for kk, v in host_out.items()}
+                              for _ in range(pipe - 1)]
+    bufs = [[H.StepBuffers(**host_in[s], **host_outs[j]) for s in range(S)] for j in range(pipe)]
     h2d = sum(v.numel() * v.element_size() for v in host_in[0].values())
     d2h = sum(v.numel() * v.element_size() for v in host_out.values())
-    for i in range(3):
-        eng.step_host(B, bufs[i % S], vp, gap_d=1, stream=stream)
+    for j in range(pipe):
+        for i in range(3):
+            engs[j].step_host(B, bufs[j][i % S], vp, gap_d=1, stream=strs[j])
     torch.cuda.synchronize()
     n = args.e2e_steps
     # the public async host-buffer API: pass i+1's uploads and pass i-1's
-    # downloads run on the engine's copy streams under pass i's kernels
+    # downloads run on each engine's copy streams under the kernels; with
+    # pipe > 1 engines on their own streams, passes alternate between them
     t0 = time.perf_counter()
     for i in range(n):
-        eng.step_host_async(B, bufs[i % S], vp, gap_d=1, stream=stream)
-    eng.sync()
+        engs[i % pipe].step_host_async(B, bufs[i % pipe][i % S], vp, gap_d=1, stream=strs[i % pipe])
+    for en in engs:
+        en.sync()
     dt = time.perf_counter() - t0
-    # the synchronous call (one pass at a time), for reference
+    # the synchronous call (one pass at a time, one engine), for reference
     t1 = time.perf_counter()
     for i in range(n):
-        eng.step_host(B, bufs[i % S], vp, gap_d=1, stream=stream)
+        engs[0].step_host(B, bufs[0][i % S], vp, gap_d=1, stream=strs[0])
     dt_sync = time.perf_counter() - t1
     return {"value": B * n / dt, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "api": "hsd_step_host_async + hsd_engine_sync (C ABI), pinned host buffers, wall clock",
+            "api": f"hsd_step_host_async + hsd_engine_sync (C ABI), pinned host buffers, wall clock; "
+                   f"{pipe} engine(s) on {pipe} stream(s), passes alternating",
             "passes": n, "sync_api_value": B * n / dt_sync}
 
 
