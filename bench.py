@@ -381,8 +381,9 @@ def config_of(args, world):
               f"inputs larger than L2 ({args.n * args.dim * (2 if args.dtype == 'bf16' or args.filter == 'bf16_copy' else 4) / 1e9:.1f} GB of keys "
               f"streamed per pass)",
         "verify": "relaxed 30/15, verify-skip min_S=0.95 O_dist=5 d=1, chain cap 64",
-        "pipeline": (f"{getattr(args, 'pipe', 1)} engine(s) on as many streams, steps alternating: step i+1's "
-                     f"similarity scan runs while step i's select / verify finish"
+        "pipeline": (f"{getattr(args, 'pipe', 1)} cohorts of {args.batch} episodes, one engine + stream each, "
+                     f"their steps interleaved (each cohort's steps stay in order): one cohort's similarity scan "
+                     f"runs while the other's select / verify finish"
                      if getattr(args, "pipe", 1) > 1 else "1 engine, steps back to back on one stream"),
     }
 
