@@ -789,8 +789,9 @@ def run_c3(args):
                                          H._ptr(feats[s][1]), d_f, H._ptr(hist), 1, H.C.cast(arr, H.C.c_void_p), P,
                                          H._ptr(o), H._ptr(t), H._stream(st)))
 
-    # rounds are independent: with `pipe` streams (rounds alternating, outputs per
-    # stream) one round's latency-bound tail overlaps the next round's loads
+    # `pipe` cohorts of E episodes, one stream each (outputs per stream), their
+    # rounds interleaved: one round's latency-bound tail overlaps the other
+    # cohort's loads (each cohort's rounds stay in order)
     pipe = args.pipeline if args.pipeline > 0 else 2
     strs = [stream] + [torch.cuda.Stream(device=dev) for _ in range(pipe - 1)]
     outs = [(out, toks)] + [(torch.empty_like(out), torch.empty_like(toks)) for _ in range(pipe - 1)]
