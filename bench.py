@@ -877,7 +877,9 @@ def run_c3(args):
         "data": "synthetic (counter-generated logits/features/drafts)",
         "config": {"workload": f"C3: {E} episodes x {P} parameter sets (acceptance tolerance x skip threshold), "
                                f"k={k}, L={L}, d_f={d_f}", "episodes": E, "param_sets": P, "sweep": C3_SWEEP,
-                   "l2": "two resident input sets of 164 MB alternate (> L2)"},
+                   "l2": "two resident input sets of 164 MB alternate (> L2)",
+                   "pipeline": (f"{pipe} cohorts of {E} episodes, one stream each, their rounds interleaved"
+                                if pipe > 1 else "one round at a time")},
         "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
