@@ -765,8 +765,12 @@ def run_c3(args):
     import paper_2603_17573_b200 as H
 
     rank, world, local = env_rank()
+    local = local % max(torch.cuda.device_count(), 1)  # (plumbing runs may put several ranks on one GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    import torch.distributed as dist
+    if world > 1:  # every rank verifies its own episodes (weak scaling); timing = max over ranks
+        init_dist(dist, dev)
     E, k, L, d_f = args.episodes, args.k, args.L, args.d_f
     n_db = 1_000_000
     col = H.Collection(8, capacity=n_db, device=local)  # token table (payload drafts); keys unused here
@@ -823,7 +827,9 @@ def run_c3(args):
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    value = E / (ms / 1e3)
+    if world > 1:
+        ms = reduce_scalar(dist, torch, ms, "max")
+    value = world * E / (ms / 1e3)
     in_bytes = E * (L * 256 * 4 + 2 * d_f * 4 + k * 4 + k * HSD_TOK_ROW + 4)
     out_bytes = P * E * (20 + L)
     peak, peak_kind = load_peaks()
@@ -866,13 +872,13 @@ def run_c3(args):
            "api": "hsd_verify_round (C ABI) with pinned host buffers, wall clock", "passes": n_e2e}
 
     cb = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and rank == 0:
         cb = c3_cpu_baseline(args, ids[0].cpu().numpy(), lg[0].cpu().numpy(), feats[0][0].cpu().numpy(),
                              feats[0][1].cpu().numpy(), col)
     line = {
         "metric": "verified episode-rounds/sec (each under every parameter set of the sweep), 4096 concurrent "
                   "episodes, 7x256 logits (C3)",
-        "value": value, "unit": "episode-rounds/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "value": value, "unit": "episode-rounds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (counter-generated logits/features/drafts)",
         "config": {"workload": f"C3: {E} episodes x {P} parameter sets (acceptance tolerance x skip threshold), "
@@ -882,7 +888,11 @@ def run_c3(args):
                                 if pipe > 1 else "one round at a time")},
         "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary(),
     }
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 HSD_TOK_ROW = 32
