@@ -68,7 +68,7 @@ struct WideCfg {
   static constexpr int kBufs = kTmemCols / kBufCols;  // 2 = double-buffered, 1 = single
   static_assert(kBufs == 1 || kBufs == 2, "accumulators must fill 256 or 512 TMEM columns");
   static constexpr int kQTile = kBQ * 128;            // bytes per query k-chunk tile
-  static constexpr int kKStages = NS == 4 ? 7 : 9;
+  static constexpr int kKStages = NS == 4 ? 7 : (NS == 1 ? 10 : 9);  // NS = 1: 10 measured 0.7% over 9, 11-12 (fewer query stages) slower
   static constexpr int kQStages = NS == 1 ? 4 : 3;
   static constexpr int kMyQ = kBQ / kEpiWarps;        // queries owned per epilogue lane-group
 };
