@@ -1,6 +1,17 @@
-// k_sim_wide.cu — K1 (tensor cores, default path for B > 4): similarity FILTER
-// on tcgen05 + TMA for up to 256 queries per pass, fused with the per-CTA
-// top-32 candidate filter.  Two operand types share the kernel:
+// k_sim_wide.cu — K1 (tensor cores, the default for every batch): similarity
+// FILTER on tcgen05 + TMA for up to 1024 queries per pass, fused with the
+// per-CTA top-32 candidate filter.  Kernels in this file:
+//
+//   sim_wide_kernel  one CTA per SM, up to 128 queries per pass (NS = 1, 2);
+//                    with kMC > 1 clusters of query groups share multicast key
+//                    tiles (the single-CTA ablation above 128 queries)
+//   sim_pair_kernel  above 128 queries: CTA pairs (tcgen05.mma.cta_group::2,
+//                    M = 256), clusters of up to 4 pairs with multicast key
+//                    halves, queries balanced over the pairs (see below)
+//   pad_queries_*    the zero-padded query slab; K1 is its programmatic
+//                    dependent (only the query producer waits for it)
+//
+// Two operand types share the kernels:
 //
 //   TF32  fp32 collections: keys and queries are read as TF32 straight from
 //         the fp32 tiles (kind::tf32, 32 fp32 = one 128-B atom per k-chunk);
