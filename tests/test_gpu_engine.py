@@ -94,3 +94,34 @@ def test_graph_replay_matches_eager(torch):
             for s in range(3):
                 for kk in bufs[s]:
                     assert torch.equal(bufs[s][kk], ref[s][kk]), (rep, s, kk)
+
+
+@pytest.mark.parametrize("B", [48, 200])
+def test_cohorts_on_two_streams_match_serial_steps(torch, B):
+    """Two engines over one collection, each on its own stream, their steps
+    interleaved with no synchronisation between them (the bench's cohort
+    pipelining; B = 200 runs the CTA-pair filter): every step's outputs equal
+    the same step run alone."""
+    n, dim, k, L, d_f = 20000, 256, 8, 7, 256
+    col = H.Collection(dim, capacity=n)
+    col.generate(H.REAL, 5, n)
+    vp = H.VerifyParams.make(skip_enabled=True, min_S=0.95, O_dist=5)
+    S = 6
+    ins = [make_inputs(torch, col, n, dim, B, L, d_f, s) for s in range(S)]
+    solo = H.Engine(col, B, k, L, d_f, 15)
+    ref = []
+    for s in range(S):
+        o = outputs(torch, B, k, L, "cuda")
+        solo.step(B, H.StepBuffers(**ins[s], **o), vp)
+        torch.cuda.synchronize()
+        ref.append({kk: v.cpu() for kk, v in o.items()})
+    engs = [H.Engine(col, B, k, L, d_f, 15) for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [outputs(torch, B, k, L, "cuda") for _ in range(S)]
+    for rep in range(3):  # repeat: the interleaving differs run to run
+        for s in range(S):
+            engs[s % 2].step(B, H.StepBuffers(**ins[s], **outs[s]), vp, stream=streams[s % 2])
+        torch.cuda.synchronize()
+        for s in range(S):
+            for kk in outs[s]:
+                assert torch.equal(outs[s][kk].cpu(), ref[s][kk]), (rep, s, kk)
