@@ -353,6 +353,62 @@ __global__ void __launch_bounds__(256) v_rank2(const Scr* __restrict__ scr, int 
 }
 __global__ void v_empty() {}
 
+
+// fp64 rows in HBM (a hypothetical fp64 rescoring copy of the keys): the chain
+// is LDS + DFMA only, no F2F widening
+template <int kPer, int kW, int kThr = 128>
+__global__ void __launch_bounds__(kThr) v_ring64(const double* __restrict__ keys, int dim,
+                                                 const float* __restrict__ queries, Scr* scr) {
+  constexpr int kStride = kW + 2;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  auto& rows = *reinterpret_cast<double(*)[2][kPer][kStride]>(smem_raw);
+  auto& qs = *reinterpret_cast<float(*)[2][kW]>(smem_raw + 8 * 2 * kPer * kStride);
+  auto& qd = *reinterpret_cast<double(*)[kW]>(smem_raw + 8 * 2 * kPer * kStride + 4 * 2 * kW);
+  __shared__ uint32_t ids[kPer];
+  const int b = blockIdx.x, c0 = blockIdx.y * kPer;
+  Scr& o = scr[b];
+  const int n = min(o.n - c0, kPer);
+  if (n <= 0) return;
+  const int tid = threadIdx.x;
+  if (tid < n) ids[tid] = o.id[c0 + tid];
+  __syncthreads();
+  const float* qrow = queries + (size_t)b * dim;
+  const int nchunk = (dim + kW - 1) / kW;
+  constexpr int v16 = kW / 2;
+  auto issue = [&](int ch) {
+    const int cbase = ch * kW;
+    for (int i = tid; i < n * v16; i += kThr) {
+      const int c = i / v16, j16 = i - c * v16;
+      const int col = cbase + j16 * 2;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&rows[ch & 1][c][j16 * 2]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(keys + (size_t)ids[c] * dim + col), "r"(col < dim ? 16 : 0) : "memory");
+    }
+    for (int j4 = tid; j4 < kW / 4; j4 += kThr) {
+      const int col = cbase + j4 * 4;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&qs[ch & 1][j4 * 4]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(qrow + col), "r"(col < dim ? 16 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc = 0.0;
+  issue(0);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    if (ch + 1 < nchunk) { issue(ch + 1); asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    for (int j = tid; j < kW; j += kThr) qd[j] = (double)qs[ch & 1][j];
+    __syncthreads();
+    const int w = min(dim - ch * kW, kW);
+    if (tid < n) {
+      const double* r = rows[ch & 1][tid];
+#pragma unroll 16
+      for (int j = 0; j < w; ++j) acc = __fma_rn(qd[j], r[j], acc);
+    }
+    __syncthreads();
+  }
+  if (tid < n) o.exact[c0 + tid] = acc;
+}
+
 __global__ void flush(float* p, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] += 1.f;
 }
@@ -462,6 +518,23 @@ int main(int argc, char** argv) {
       cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms2, e0, e1);
       printf("rank after an L2 flush: %.2f us each\n", (ms - ms2) * 10.f);
     }
+  }
+  {
+    double* dk64;
+    CK(cudaMalloc(&dk64, N * dim * 8));
+    std::vector<double> hk64(hk.begin(), hk.end());
+    CK(cudaMemcpy(dk64, hk64.data(), N * dim * 8, cudaMemcpyHostToDevice));
+#define RING64(P, W)                                                                                       \
+    {                                                                                                      \
+      auto k = v_ring64<P, W>;                                                                             \
+      const int sm = 8 * 2 * P * (W + 2) + 4 * 2 * W + 8 * W;                                              \
+      CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                        \
+      run("v_ring64<" #P "," #W "> (fp64 rows)", [&] { k<<<dim3(B, kCandMax / P), 128, sm>>>(dk64, dim, dq, ds); }); \
+    }
+    RING64(32, 128)
+    RING64(32, 256)
+    RING64(16, 256)
+    cudaFree(dk64);
   }
   run("v_int<32,128>", [&] { v_int<32, 128><<<dim3(B, kCandMax / 32), 128>>>(dk, dim, dq, ds); });
 #define WS(P, T, W, PIPE, S)                                                                                     \
