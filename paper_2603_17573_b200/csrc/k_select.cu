@@ -32,7 +32,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kPool = 512;
 constexpr int kCandMax = 256;   // rescored candidates per query
-constexpr int kPer = 32;        // candidates rescored per CTA of the rescoring kernel (lanes of warp 0)
+constexpr int kPerWide = 32;    // candidates rescored per CTA (lanes of warp 0) from 9 queries up
+constexpr int kPerNarrow = 8;   // ... and for 1-8 queries (more CTAs, more rows in flight)
 constexpr int kRThreads = 128;  // rescoring CTA: all threads stage rows, warp 0 runs the fp64 chains
 
 __device__ __forceinline__ double widen(float x) { return (double)x; }
@@ -157,16 +158,18 @@ __global__ void __launch_bounds__(kThreads) select_cand_kernel(const uint64_t* _
 // Shape (tools/rescore_lab.cu, config-2 shape, L2 flushed): 32 chains per CTA
 // run at 52 us where 8 chains per CTA took 90-110 us — the chain's per-step
 // F2F widening and DFMA are issued per warp instruction, so full warps of
-// chains cost 4x fewer issue slots per SM than quarter-filled ones.
+// chains cost 4x fewer issue slots per SM than quarter-filled ones.  At 1-8
+// queries the SMs are idle anyway, and 8 chains per CTA (more CTAs, more rows
+// in flight) measured 41.5 us against 47.5 us for 32 (100 candidates).
 constexpr int kW = 256;    // elements per chunk
 constexpr int kPipe = 8;   // chain steps whose operands are loaded ahead
 
-template <typename KT>
+template <typename KT, int kPer>
 constexpr size_t rescore_smem() {
   return sizeof(KT) * 2 * kPer * (kW + 16 / sizeof(KT)) + sizeof(float) * 2 * kW + sizeof(double) * kW;
 }
 
-template <typename KT>
+template <typename KT, int kPer>
 __global__ void __launch_bounds__(kRThreads) rescore_kernel(const KT* __restrict__ keys, int dim,
                                                             const float* __restrict__ queries,
                                                             SelScratch* __restrict__ scr) {
@@ -376,28 +379,37 @@ cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, cons
   cudaError_t e = launch_pdl(select_cand_kernel, dim3(B), dim3(kThreads), 0, s, partial, lists, B, k, dim, queries,
                              maxnorm_bits, gamma, scr);
   if (e != cudaSuccess) return e;
-  const dim3 grid(B, kCandMax / kPer);
-  // the kernel's occupancy is set by shared memory: ask for the full carveout
-  const size_t sm16 = rescore_smem<uint16_t>(), sm32 = rescore_smem<float>();
   // function attributes are per device: set them once for each device used
+  // (the kernels' occupancy is set by shared memory: ask for the full carveout)
   static std::atomic<uint64_t> configured{0};
   int dev = 0;
   cudaGetDevice(&dev);
+  auto attrs = [](auto kern, size_t smem) {
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return r;
+  };
   if (dev < 64 && !(configured.load() >> dev & 1)) {
-    e = cudaFuncSetAttribute(rescore_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm16);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(rescore_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm32);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(rescore_kernel<uint16_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(rescore_kernel<float>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = attrs(rescore_kernel<uint16_t, kPerWide>, rescore_smem<uint16_t, kPerWide>());
+    if (e == cudaSuccess) e = attrs(rescore_kernel<float, kPerWide>, rescore_smem<float, kPerWide>());
+    if (e == cudaSuccess) e = attrs(rescore_kernel<uint16_t, kPerNarrow>, rescore_smem<uint16_t, kPerNarrow>());
+    if (e == cudaSuccess) e = attrs(rescore_kernel<float, kPerNarrow>, rescore_smem<float, kPerNarrow>());
     if (e != cudaSuccess) return e;
     configured.fetch_or(1ull << dev);
   }
+  auto go = [&](auto kern, size_t smem, int per, const auto* kp) {
+    return launch_pdl(kern, dim3(B, kCandMax / per), dim3(kRThreads), smem, s, kp, dim, queries, scr);
+  };
+  const bool narrow = B <= 8;
   if (key_dtype == HSD_DTYPE_BF16)
-    e = launch_pdl(rescore_kernel<uint16_t>, grid, dim3(kRThreads), sm16, s, (const uint16_t*)keys, dim, queries, scr);
+    e = narrow ? go(rescore_kernel<uint16_t, kPerNarrow>, rescore_smem<uint16_t, kPerNarrow>(), kPerNarrow,
+                    (const uint16_t*)keys)
+               : go(rescore_kernel<uint16_t, kPerWide>, rescore_smem<uint16_t, kPerWide>(), kPerWide,
+                    (const uint16_t*)keys);
   else
-    e = launch_pdl(rescore_kernel<float>, grid, dim3(kRThreads), sm32, s, (const float*)keys, dim, queries, scr);
+    e = narrow ? go(rescore_kernel<float, kPerNarrow>, rescore_smem<float, kPerNarrow>(), kPerNarrow,
+                    (const float*)keys)
+               : go(rescore_kernel<float, kPerWide>, rescore_smem<float, kPerWide>(), kPerWide, (const float*)keys);
   if (e != cudaSuccess) return e;
   P2PPublish pb{};
   if (pub) pb = *pub;

@@ -479,10 +479,10 @@ int main(int argc, char** argv) {
     run("v_ring<" #P "," #W ",pipe" #PIPE ",thr" #T ">", [&] { k<<<dim3(B, kCandMax / P), T, sm>>>(dk, dim, dq, ds); }); \
   }
   RING(32, 256, 8, 128)
-  RINGM(32, 256, 16, 128, 3)
-  RINGM(32, 256, 8, 128, 5)
-  RINGM(32, 128, 8, 128, 5)
-  RINGM(16, 256, 8, 128, 5)
+  RING(16, 256, 8, 128)
+  RING(8, 256, 8, 128)
+  RING(16, 128, 8, 128)
+  RING(8, 512, 8, 128)
   {
     double* dsc; int32_t* did; int* dov;
     CK(cudaMalloc(&dsc, B * 8 * 8)); CK(cudaMalloc(&did, B * 8 * 4)); CK(cudaMalloc(&dov, 4));
