@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ C
   }
 }
 
-int main() {
-  const long N = 1000064, dim = 4096;
+int main(int argc, char** argv) {
+  const long N = argc > 1 ? atol(argv[1]) : 1000064, dim = 4096;  // N: a multiple of 128
   const int nblocks = N / 128, nk = dim / 32;
   float* d;
   cudaMalloc(&d, N * dim * 4);
