@@ -138,26 +138,26 @@ hsd_status hsd_search_topk_exact(hsd_collection* c, const float* queries, int B,
 hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B, int k, int64_t row_begin,
                                  int64_t row_end, double* scores, int32_t* ids, void* stream);
 
-/* Number of queries whose exact-rescoring candidate window overflowed in the
- * last search on `stream` (0 in every tested configuration; non-zero means
- * the result may be inexact).  Synchronizes `stream`. */
+/* Search statistics of `stream`, accumulated since the last reset:
+ *   stats3[0] queries that needed the exact range fallback (a filter list
+ *             could not bound its rows: runs of near-duplicate records);
+ *   stats3[1] pooled candidates rescored exactly;
+ *   stats3[2] filter lists rescanned by the fallback.
+ * Results are exact either way; the fallback only costs time.  Synchronizes
+ * `stream`; reset != 0 zeroes the counters afterwards. */
+hsd_status hsd_search_stats(hsd_collection* c, void* stream, int reset, int* stats3);
+/* stats3[0] of hsd_search_stats (kept for ABI version 1 callers). */
 hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count);
 
-/* Diagnostics: a tcgen05 similarity kernel's approximate (filter) scores of
- * B queries against every record, fp32 [B][size] (device); variant 1 = the
- * wide filter of the default path (TF32 over fp32 keys, bf16 over bf16 keys;
- * B <= 256), 2 = 64-query TF32 kernel, 3 = 3xTF32 filter (B <= 64), 4 = the
- * bf16 filter copy of an fp32 collection (B <= 256).  Used by
- * the tests to check the error bounds the exact rescoring relies on. */
+/* Diagnostics: the tcgen05 filter's approximate scores of B <= 256 queries
+ * against every record, fp32 [B][size] (device); variant 1 = the stored keys
+ * (TF32 over fp32 keys, bf16 over bf16 keys), 4 = the bf16 filter copy of an
+ * fp32 collection.  Used by the tests to check the error bounds the exact
+ * rescoring relies on. */
 hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
                                 void* stream);
-/* Similarity-path override for ablations/tests (fp32 collections): 0 auto
- * (the wide tcgen05 filter for every batch, CTA pairs above 128 queries),
- * 1 SIMT rows/tile, 2 SIMT tile, 3 wide tcgen05 TF32, 4 tcgen05 3xTF32,
- * 5 64-query tcgen05 TF32, 6 wide kernels without CTA pairs (also applies to
- * bf16 collections).  Process-wide; also
- * HSD_SIM_PATH=rows|tile|tc|tc3|tc1|tc_single.  bf16 collections otherwise
- * always use the wide kernels. */
+/* Ablation switch, process-wide: 0 auto (CTA-pair kernels above 128 queries),
+ * 1 single-CTA wide kernels only (also HSD_WIDE_PAIR=0). */
 hsd_status hsd_set_sim_path(int path);
 
 /* ------------------------------------------------------------------------
@@ -291,6 +291,9 @@ hsd_status hsd_step_graph(hsd_engine* e, int B, const hsd_step_io* io, const hsd
  * over the recorded steps, then resets the recorder. */
 hsd_status hsd_engine_enable_timing(hsd_engine* e, int max_steps);
 hsd_status hsd_engine_stage_times(hsd_engine* e, int* n_steps, double ms[5]);
+/* The engine's search statistics (as hsd_search_stats; the engine owns its
+ * scratch).  Synchronizes the device. */
+hsd_status hsd_engine_stats(hsd_engine* e, int reset, int* stats3);
 
 /* Same with HOST buffers: H2D of the inputs and D2H of the outputs happen
  * inside the call (device staging owned by the engine); synchronous. */

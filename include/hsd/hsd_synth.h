@@ -19,6 +19,13 @@
  *   HSD_SYNTH_REAL  : Irwin-Hall(4) integer vector, L2-normalised exactly:
  *                     sum of squares in int64 (order-independent), sqrt and the
  *                     divide in fp64, then rounded once to fp32.
+ *   HSD_SYNTH_CLUSTER: REAL rows, except that each 512-row block may open with
+ *                     a run of 64-512 consecutive rows around one centre: a
+ *                     near-duplicate run (64 * centre + noise, pairwise cosine
+ *                     ~0.9999: the steps of a demonstration, SPEC.md:602,
+ *                     608-613) or a run of identical rows (a stationary
+ *                     segment).  Queries near such a run see hundreds of rows
+ *                     within the filter's error window of the k-th score.
  *
  * This header is plain C99 and compiles as CUDA (__host__ __device__).
  */
@@ -41,6 +48,7 @@ extern "C" {
 enum {
   HSD_SYNTH_EXACT = 0,
   HSD_SYNTH_REAL = 1,
+  HSD_SYNTH_CLUSTER = 2,
 };
 
 /* stream tags */
@@ -99,6 +107,36 @@ HSD_HD int32_t hsd_key_raw(uint64_t kbase, int64_t src_row, int dim, int col) {
   return hsd_ih4(hsd_hash_at(kbase, (uint64_t)src_row * (uint64_t)dim + (uint64_t)col));
 }
 
+/* CLUSTER family: block g = row / HSD_CLUSTER_BLOCK opens with a run of
+ * hsd_cluster_len rows of kind hsd_cluster_type (0 none, 1 near-duplicate,
+ * 2 identical). */
+#define HSD_CLUSTER_BLOCK 512
+HSD_HD uint64_t hsd_cluster_hash(uint64_t kbase, int64_t g) {
+  return hsd_hash_at(kbase ^ 0xC2B2AE3D27D4EB4Full, (uint64_t)g);
+}
+HSD_HD int hsd_cluster_type(uint64_t kbase, int64_t g) {
+  const uint32_t t = (uint32_t)(hsd_cluster_hash(kbase, g) & 3u);
+  return t <= 1u ? 1 : (t == 2u ? 2 : 0);
+}
+HSD_HD int hsd_cluster_len(uint64_t kbase, int64_t g) {
+  return 64 + (int)((hsd_cluster_hash(kbase, g) >> 8) % 449u);
+}
+/* Raw (un-normalised) integer of key (row, col) of family `kind` (REAL or
+ * CLUSTER; |raw| < 2^24, so dim * raw^2 fits int64 for dim < 2^14). */
+HSD_HD int64_t hsd_key_raw_kind(int kind, uint64_t kbase, int64_t row, int dim, int col) {
+  if (kind == HSD_SYNTH_CLUSTER) {
+    const int64_t g = row / HSD_CLUSTER_BLOCK, p = row % HSD_CLUSTER_BLOCK;
+    const int type = hsd_cluster_type(kbase, g);
+    if (type != 0 && p < hsd_cluster_len(kbase, g)) {
+      const int64_t centre =
+          hsd_ih4(hsd_hash_at(kbase ^ 0x165667B19E3779F9ull, (uint64_t)g * (uint64_t)dim + (uint64_t)col));
+      if (type == 2) return centre;
+      return 64 * centre + hsd_key_raw(kbase, row, dim, col);
+    }
+  }
+  return hsd_key_raw(kbase, row, dim, col);
+}
+
 /* Exactly-rounded normalisation of one raw element given the int64 sum of squares. */
 HSD_HD float hsd_norm_val(int64_t raw, int64_t sumsq) {
   double n = sqrt((double)sumsq);
@@ -142,12 +180,22 @@ HSD_HD int64_t hsd_query_row(uint64_t seed, int kind, int64_t q, int64_t n_rows)
   return (int64_t)((h >> 8) % (uint64_t)n_rows);
 }
 
-/* REAL-family raw query element (needs the picked row). */
-HSD_HD int64_t hsd_query_raw(uint64_t seed, uint64_t db_seed, int64_t q, int64_t row, int dim, int col) {
+/* REAL / CLUSTER raw query element (needs the picked row).  Near-duplicate
+ * queries of CLUSTER rows scale the noise like the row (64x inside a run). */
+HSD_HD int64_t hsd_query_raw_kind(int kind, uint64_t seed, uint64_t db_seed, int64_t q, int64_t row, int dim,
+                                  int col) {
   int64_t noise = hsd_ih4(hsd_hash_at(hsd_stream_base(seed, HSD_TAG_QNOISE), (uint64_t)q * (uint64_t)dim + col));
   if (row < 0) return noise;
-  int64_t k = hsd_key_raw(hsd_stream_base(db_seed, HSD_TAG_KEYS), hsd_key_src_row(HSD_SYNTH_REAL, row), dim, col);
+  const uint64_t kbase = hsd_stream_base(db_seed, HSD_TAG_KEYS);
+  int64_t k = hsd_key_raw_kind(kind, kbase, hsd_key_src_row(kind, row), dim, col);
+  if (kind == HSD_SYNTH_CLUSTER) {
+    const int64_t g = row / HSD_CLUSTER_BLOCK;
+    if (hsd_cluster_type(kbase, g) == 1 && row % HSD_CLUSTER_BLOCK < hsd_cluster_len(kbase, g)) noise *= 64;
+  }
   return 3 * k + noise;
+}
+HSD_HD int64_t hsd_query_raw(uint64_t seed, uint64_t db_seed, int64_t q, int64_t row, int dim, int col) {
+  return hsd_query_raw_kind(HSD_SYNTH_REAL, seed, db_seed, q, row, dim, col);
 }
 
 /* EXACT-family query element. */

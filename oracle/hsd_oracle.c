@@ -63,7 +63,7 @@ int hsdo_search_topk_exact(const float* keys, int64_t n, int dim, const float* q
 
 /* `kind` may carry HSDO_KEYS_BF16: the stored key is the bf16 rounding
  * (RN-even) of the fp32 key, widened back to fp32 (bf16 collections). */
-static void gen_key_row(int kind, uint64_t kbase, int64_t row, int dim, float* out, int32_t* scratch) {
+static void gen_key_row(int kind, uint64_t kbase, int64_t row, int dim, float* out, int64_t* scratch) {
   const int bf16 = (kind & HSDO_KEYS_BF16) != 0;
   kind &= ~HSDO_KEYS_BF16;
   int64_t src = hsd_key_src_row(kind, row);
@@ -72,8 +72,8 @@ static void gen_key_row(int kind, uint64_t kbase, int64_t row, int dim, float* o
   } else {
     int64_t ss = 0;
     for (int c = 0; c < dim; ++c) {
-      scratch[c] = hsd_key_raw(kbase, src, dim, c);
-      ss += (int64_t)scratch[c] * scratch[c];
+      scratch[c] = hsd_key_raw_kind(kind, kbase, src, dim, c);
+      ss += scratch[c] * scratch[c];
     }
     for (int c = 0; c < dim; ++c) out[c] = hsd_norm_val(scratch[c], ss);
   }
@@ -83,7 +83,7 @@ static void gen_key_row(int kind, uint64_t kbase, int64_t row, int dim, float* o
 
 void hsdo_gen_keys(int kind, uint64_t db_seed, int64_t row0, int64_t n, int dim, float* out) {
   uint64_t kbase = hsd_stream_base(db_seed, HSD_TAG_KEYS);
-  int32_t* scratch = (int32_t*)malloc(sizeof(int32_t) * (size_t)dim);
+  int64_t* scratch = (int64_t*)malloc(sizeof(int64_t) * (size_t)dim);
   for (int64_t r = 0; r < n; ++r) gen_key_row(kind, kbase, row0 + r, dim, out + (size_t)r * dim, scratch);
   free(scratch);
 }
@@ -101,7 +101,7 @@ void hsdo_gen_queries(int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_row
     }
     int64_t ss = 0;
     for (int c = 0; c < dim; ++c) {
-      raw[c] = hsd_query_raw(q_seed, db_seed, q, row, dim, c);
+      raw[c] = hsd_query_raw_kind(kind, q_seed, db_seed, q, row, dim, c);
       ss += raw[c] * raw[c];
     }
     for (int c = 0; c < dim; ++c) o[c] = hsd_norm_val(raw[c], ss);
@@ -131,7 +131,7 @@ int hsdo_search_synth(int kind, uint64_t db_seed, int64_t n, int dim, const floa
     t = omp_get_thread_num();
 #endif
     float* row = (float*)malloc(sizeof(float) * (size_t)dim);
-    int32_t* scratch = (int32_t*)malloc(sizeof(int32_t) * (size_t)dim);
+    int64_t* scratch = (int64_t*)malloc(sizeof(int64_t) * (size_t)dim);
     int64_t chunk = (n + nt - 1) / nt;
     int64_t r0 = chunk * t, r1 = r0 + chunk < n ? r0 + chunk : n;
     for (int64_t r = r0; r < r1; ++r) {

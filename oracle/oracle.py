@@ -231,7 +231,7 @@ def ref_save(loaded: dict, path: str) -> int:
 
 
 # ---------------------------------------------------------------- helpers
-EXACT, REAL = 0, 1
+EXACT, REAL, CLUSTER = 0, 1, 2
 KEYS_BF16 = 0x100  # OR into `kind`: the DB stores bf16-rounded keys (hsd_oracle.h HSDO_KEYS_BF16)
 
 

@@ -25,7 +25,7 @@ LIB_PATH = os.path.join(_HERE, "libhsd_gpu.so")
 
 HSD_K_MAX = 32
 TOKENS_STRIDE = 32
-EXACT, REAL = 0, 1
+EXACT, REAL, CLUSTER = 0, 1, 2
 F32, BF16 = 0, 1  # hsd_dtype (key storage)
 _DTYPES = {"f32": F32, "fp32": F32, "float32": F32, F32: F32, "bf16": BF16, "bfloat16": BF16, BF16: BF16}
 
@@ -183,6 +183,8 @@ def lib():
         "hsd_search_topk_exact": [_vp, _vp, C.c_int, C.c_int, _vp, _vp, _vp],
         "hsd_search_topk_range": [_vp, _vp, C.c_int, C.c_int, C.c_int64, C.c_int64, _vp, _vp, _vp],
         "hsd_search_overflow_count": [_vp, _vp, C.POINTER(C.c_int)],
+        "hsd_search_stats": [_vp, _vp, C.c_int, C.POINTER(C.c_int * 3)],
+        "hsd_engine_stats": [_vp, C.c_int, C.POINTER(C.c_int * 3)],
         "hsd_verify_round": [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, _vp, C.c_int,
                              _vp, _vp, _vp],
         "hsd_window_features": [C.c_int, _vp, C.c_int, C.POINTER(MetricParams), C.POINTER(NormBounds), _vp, _vp, _vp,
@@ -419,9 +421,14 @@ class Collection:
         check(lib().hsd_collection_save_image(self._h, os.fsencode(path)))
 
     def overflow_count(self, stream=None) -> int:
-        c = C.c_int()
-        check(lib().hsd_search_overflow_count(self._h, _stream(stream), C.byref(c)))
-        return c.value
+        """Queries that needed the exact range fallback on `stream` (results are exact either way)."""
+        return self.search_stats(stream)["fallback_queries"]
+
+    def search_stats(self, stream=None, reset=False) -> dict:
+        """Accumulated search statistics of `stream` (hsd_search_stats; synchronizes)."""
+        v = (C.c_int * 3)()
+        check(lib().hsd_search_stats(self._h, _stream(stream), int(reset), C.byref(v)))
+        return {"fallback_queries": v[0], "candidates": v[1], "fallback_lists": v[2]}
 
     def verify_round(self, ids, logits, params, feat_now=None, feat_prev=None, history=None, gap_d=1, stream=None):
         """Fused gather + verify-skip + relaxed acceptance.
@@ -600,12 +607,12 @@ def quantize(actions, lo=-1.0, hi=1.0, k_bins=256, stream=None):
     return bins
 
 
-SIM_PATHS = {"auto": 0, "rows": 1, "tile": 2, "tc": 3, "tc3": 4, "tc1": 5, "tc_single": 6}
+SIM_PATHS = {"auto": 0, "tc_single": 1}
 
 
 def set_sim_path(name: str) -> None:
-    """Similarity kernel override (ablations / tests): auto | rows | tile | tc (wide TF32, default) | tc1 (64-query
-    TF32) | tc3 (3xTF32) | tc_single (wide kernels without CTA pairs)."""
+    """Filter kernel ablation switch: auto (CTA-pair kernels above 128 queries) | tc_single (single-CTA wide
+    kernels only)."""
     check(lib().hsd_set_sim_path(SIM_PATHS[name]))
 
 
@@ -731,6 +738,12 @@ class Engine:
 
     def sync(self):
         check(lib().hsd_engine_sync(self._h))
+
+    def search_stats(self, reset=False) -> dict:
+        """The engine's accumulated search statistics (hsd_engine_stats; synchronizes the device)."""
+        v = (C.c_int * 3)()
+        check(lib().hsd_engine_stats(self._h, int(reset), C.byref(v)))
+        return {"fallback_queries": v[0], "candidates": v[1], "fallback_lists": v[2]}
 
 
 # --------------------------------------------------------------------------- hybrid loop (config 5)

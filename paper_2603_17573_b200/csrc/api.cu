@@ -100,14 +100,17 @@ __global__ void offset_ids_kernel(int32_t* ids, int n, int64_t off) {
   if (i < n && ids[i] >= 0) ids[i] = (int32_t)(ids[i] + off);
 }
 
+// Device scratch of one search stream (or one engine): K1's filter lists, the
+// padded query slab, K2's per-query state and the search statistics.
 struct Scratch {
   uint64_t* partial = nullptr;
   size_t partial_cap = 0;  // bytes
   void* sel = nullptr;     // K2 per-query candidate / exact-score scratch
   size_t sel_cap = 0;
-  float* qsplit = nullptr;  // Qh | Ql of the tcgen05 path
-  size_t qsplit_cap = 0;
-  int* overflow = nullptr;
+  void* qslab = nullptr;   // K1's padded query slab (TMA source)
+  size_t qslab_cap = 0;
+  int* stats = nullptr;    // [0] fallback queries, [1] pooled candidates, [2] fallback lists (accumulated)
+  bool fixed = false;      // engine-owned: never reallocated (captured graphs hold its pointers)
 };
 
 }  // namespace
@@ -176,77 +179,64 @@ hsd_status refresh_shadow(hsd_collection* c, int64_t row0, int64_t n) {
   return HSD_OK;
 }
 
-hsd_status get_scratch(hsd_collection* c, cudaStream_t s, size_t partial_bytes, size_t qsplit_bytes, Scratch** out) {
-  std::lock_guard<std::mutex> lk(c->mu);
-  Scratch& sc = c->scratch[s];
-  if (!sc.overflow) CU(cudaMalloc(&sc.overflow, sizeof(int)));
-  if (sc.partial_cap < partial_bytes) {
-    cudaFree(sc.partial);
-    sc.partial = nullptr;
-    sc.partial_cap = 0;
-    CU(cudaMalloc(&sc.partial, partial_bytes));
-    sc.partial_cap = partial_bytes;
+// Scratch bytes of one search of B queries over `rows` rows on `nsm` SMs
+// (all_sizes: of ANY search of up to B queries — an engine's fixed scratch).
+// Every pass may use a different list count (pair clusters, the tail pass):
+// the lists are sized for the largest lists(Bs) * Bs.
+void scratch_need(int B, int64_t rows, int nsm, int dim, bool all_sizes, size_t* partial, size_t* sel,
+                  size_t* qslab) {
+  const int W = hsd::kMaxBatchPass;
+  size_t p = 0;
+  if (all_sizes) {
+    for (int t = 1; t <= std::min(B, W); ++t) p = std::max(p, (size_t)hsd::sim_wide_lists(t, rows, nsm) * t);
+  } else {
+    for (int b0 = 0; b0 < B; b0 += W) {
+      const int Bs = std::min(W, B - b0);
+      p = std::max(p, (size_t)hsd::sim_wide_lists(Bs, rows, nsm) * Bs);
+    }
   }
-  const size_t sel_bytes = hsd::select_scratch_bytes(1024);
-  if (sc.sel_cap < sel_bytes) {
-    cudaFree(sc.sel);
-    sc.sel = nullptr;
-    sc.sel_cap = 0;
-    CU(cudaMalloc(&sc.sel, sel_bytes));
-    sc.sel_cap = sel_bytes;
+  *partial = p * hsd::dev::kCandLocal * sizeof(uint64_t);
+  *sel = hsd::select_scratch_bytes(std::min(B, W));
+  *qslab = hsd::sim_wide_scratch_bytes(dim);
+}
+
+hsd_status alloc_scratch(Scratch& sc, size_t partial_bytes, size_t sel_bytes, size_t qslab_bytes) {
+  if (!sc.stats) {
+    CU(cudaMalloc(&sc.stats, 4 * sizeof(int)));
+    CU(cudaMemset(sc.stats, 0, 4 * sizeof(int)));
   }
-  if (sc.qsplit_cap < qsplit_bytes) {
-    cudaFree(sc.qsplit);
-    sc.qsplit = nullptr;
-    sc.qsplit_cap = 0;
-    CU(cudaMalloc(&sc.qsplit, qsplit_bytes));
-    sc.qsplit_cap = qsplit_bytes;
-  }
-  *out = &sc;
+  auto grow = [&](void** p, size_t* cap, size_t need) -> cudaError_t {
+    if (*cap >= need) return cudaSuccess;
+    cudaFree(*p);  // implicit device synchronisation: no kernel still reads the old buffer
+    *p = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(p, need);
+    if (e == cudaSuccess) *cap = need;
+    return e;
+  };
+  CU(grow((void**)&sc.partial, &sc.partial_cap, partial_bytes));
+  CU(grow(&sc.sel, &sc.sel_cap, sel_bytes));
+  CU(grow(&sc.qslab, &sc.qslab_cap, qslab_bytes));
   return HSD_OK;
 }
 
-constexpr int kSlab = 64;  // queries per similarity launch of the 64-wide paths
-
-// Similarity path per query pass: SIMT GEMV for tiny batches on fp32
-// collections (HBM-bound on CUDA cores), the wide tcgen05 filter otherwise
-// (TF32 over fp32 keys, bf16 over bf16 keys; up to 256 queries per pass).
-// HSD_SIM_PATH=rows|tile|tc|tc1|tc3 or hsd_set_sim_path override it for fp32
-// collections (tests and ablations: tc1 = 64-query TF32 kernel, tc3 = 3xTF32).
-enum { kPathAuto = 0, kPathRows = 1, kPathTile = 2, kPathTc = 3, kPathTc3 = 4, kPathTc1 = 5, kPathTcSingle = 6 };
-int g_path = -1;
-int path_override() {
-  int& v = g_path;
-  if (v < 0) {
-    const char* e = getenv("HSD_SIM_PATH");
-    v = kPathAuto;
-    if (e && !strcmp(e, "rows")) v = kPathRows;
-    if (e && !strcmp(e, "tile")) v = kPathTile;
-    if (e && !strcmp(e, "tc")) v = kPathTc;
-    if (e && !strcmp(e, "tc3")) v = kPathTc3;
-    if (e && !strcmp(e, "tc1")) v = kPathTc1;
-    if (e && !strcmp(e, "tc_single")) v = kPathTcSingle;
-  }
-  return v;
+void free_scratch(Scratch& sc) {
+  cudaFree(sc.partial);
+  cudaFree(sc.sel);
+  cudaFree(sc.qslab);
+  cudaFree(sc.stats);
+  sc = Scratch{};
 }
-constexpr int kShadowGamma = 0x100;  // sim_wide_gamma flag: bf16-rounded keys (filter shadow)
 
-int choose_path(int B, int dtype, bool shadow = false) {
-  if (dtype == HSD_DTYPE_BF16) return kPathTc;  // the only bf16 similarity kernel
-  if (shadow && path_override() == kPathAuto) return kPathTc;  // the bf16 copy halves the scan for every B
-  const int o = path_override();
-  if (o == kPathRows) return B <= 8 ? kPathRows : kPathTile;
-  if (o == kPathTile) return B <= 8 ? kPathRows : kPathTile;  // launch_sim picks rows for B <= 8
-  if (o == kPathTc || o == kPathTc3 || o == kPathTc1) return o;
-  if (o == kPathTcSingle) return kPathTc;  // the wide kernels without CTA pairs (sim_wide_set_single)
-  // the wide tcgen05 filter for every batch: at 1M x 4096 fp32 it streams at
-  // 6.9 TB/s for B = 1..64, where the SIMT rows kernel reached 2.3 TB/s at
-  // B = 1 and 6.6 TB/s at B = 4 (tools/bench_search.py); rows stays an ablation
-  (void)B;
-  return kPathTc;
+hsd_status get_scratch(hsd_collection* c, cudaStream_t s, size_t partial_bytes, size_t sel_bytes, size_t qslab_bytes,
+                       Scratch** out) {
+  std::lock_guard<std::mutex> lk(c->mu);
+  Scratch& sc = c->scratch[s];
+  hsd_status st = alloc_scratch(sc, partial_bytes, sel_bytes, qslab_bytes);
+  if (st != HSD_OK) return st;
+  *out = &sc;
+  return HSD_OK;
 }
-bool is_tc(int p) { return p == kPathTc || p == kPathTc3 || p == kPathTc1; }
-int pass_width(int p) { return p == kPathTc ? hsd::sim_wide_max_batch() : kSlab; }
 
 // Optional stage events (engine timing): marks[i] is recorded after stage i.
 struct StageMarks {
@@ -254,12 +244,16 @@ struct StageMarks {
   cudaEvent_t after_select = nullptr;
 };
 
+constexpr int kShadowGamma = 0x100;  // sim_wide_gamma flag: bf16-rounded keys (filter shadow)
+
+// K1 + K2 over rows [rb, re) in passes of up to 1024 queries.
+// own != nullptr: the engine's fixed scratch (sized at engine creation).
 // pub != nullptr: sharded search over peer memory — the final per-query
 // top-k records are published into the peers' windows by K2 (scores / ids
 // are then scratch for an empty shard only).
 hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, int64_t rb, int64_t re, double* scores,
                        int32_t* ids, cudaStream_t s, const StageMarks* marks = nullptr, int reserve_sms = 0,
-                       const hsd::P2PPublish* pub = nullptr) {
+                       const hsd::P2PPublish* pub = nullptr, Scratch* own = nullptr) {
   if (k < 1) return fail(HSD_ERR_INVALID_INPUT, "k must be >= 1");  // store.cpp:60
   if (k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k = %d exceeds HSD_K_MAX = %d", k, HSD_K_MAX);
   if (B < 0) return fail(HSD_ERR_INVALID_INPUT, "negative batch");
@@ -283,60 +277,39 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   // (the engine's kinematics); the persistent tcgen05 kernel sizes its grid to
   // the rest so neither waits for the other's CTAs to retire.
   const int nsm = std::max(1, num_sms(c->device) - std::max(0, reserve_sms));
-  const int path = choose_path(B, c->dtype, c->shadow != nullptr);
-  const int W = pass_width(path);
-  const int Bs0 = std::min(B, W);
-  const int lists0 = path == kPathTc ? hsd::sim_wide_lists(Bs0, rows, nsm)
-                     : is_tc(path)    ? hsd::sim_tc_lists(rows, nsm)
-                                      : hsd::sim_plan(Bs0, rows, c->dim, nsm).lists;
-  const size_t qscratch = path == kPathTc    ? hsd::sim_wide_scratch_bytes(c->dim)
-                          : path == kPathTc1 ? hsd::sim_tc1_scratch_bytes(c->dim)
-                          : path == kPathTc3 ? hsd::sim_tc_scratch_bytes(c->dim)
-                                             : 0;
-  Scratch* sc = nullptr;
-  // partial lists: the tcgen05 paths write exactly lists0 per pass; the SIMT plan may use up to 4 per SM
-  const size_t n_lists = is_tc(path) ? (size_t)lists0 : (size_t)std::max(lists0, 4 * nsm);
-  st = get_scratch(c, s, n_lists * Bs0 * hsd::dev::kCandLocal * sizeof(uint64_t), qscratch, &sc);
-  if (st != HSD_OK) return st;
-  CU(cudaMemsetAsync(sc->overflow, 0, sizeof(int), s));
+  size_t need_p = 0, need_s = 0, need_q = 0;
+  scratch_need(B, rows, nsm, c->dim, false, &need_p, &need_s, &need_q);
+  Scratch* sc = own;
+  if (own) {
+    if (own->partial_cap < need_p || own->sel_cap < need_s || own->qslab_cap < need_q)
+      return fail(HSD_ERR_INVALID_INPUT, "engine scratch too small for this step (batch %d)", B);
+  } else {
+    st = get_scratch(c, s, need_p, need_s, need_q, &sc);
+    if (st != HSD_OK) return st;
+  }
+  // the filter: the bf16 copy of an fp32 collection when present (half the
+  // bytes; both operands bf16-rounded), else the stored keys (TF32 / bf16)
+  const void* fkeys = c->shadow ? (const void*)c->shadow : c->keys;
+  const int fdtype = c->shadow ? HSD_DTYPE_BF16 : c->dtype;
+  const double gamma = c->shadow ? hsd::sim_wide_gamma(c->dim, HSD_DTYPE_BF16 | kShadowGamma)
+                                 : hsd::sim_wide_gamma(c->dim, c->dtype);
+  const int W = hsd::kMaxBatchPass;
   for (int b0 = 0; b0 < B; b0 += W) {
     const int Bs = std::min(W, B - b0);
-    // the SIMT paths pick rows vs tile per pass; the tcgen05 paths are fixed
-    const int p = is_tc(path) ? path : choose_path(Bs, c->dtype, c->shadow != nullptr);
-    hsd::SimPlan plan = hsd::sim_plan(Bs, rows, c->dim, nsm);
+    const int lists = hsd::sim_wide_lists(Bs, rows, nsm);
+    if (lists > hsd::select_max_lists()) return fail(HSD_ERR_CONFIG, "%d filter lists exceed the select kernel", lists);
     const float* q = queries + (size_t)b0 * c->dim;
-    if (p == kPathTc) {
-      plan.lists = hsd::sim_wide_lists(Bs, rows, nsm);
-      if (c->shadow) {  // bf16 filter copy of fp32 keys: both operands rounded
-        plan.gamma = hsd::sim_wide_gamma(c->dim, HSD_DTYPE_BF16 | kShadowGamma);
-        CU(hsd::launch_sim_wide(c->shadow, HSD_DTYPE_BF16, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit,
-                                sc->partial, nullptr, s));
-      } else {
-        plan.gamma = hsd::sim_wide_gamma(c->dim, c->dtype);
-        CU(hsd::launch_sim_wide(c->keys, c->dtype, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial,
-                                nullptr, s));
-      }
-    } else if (p == kPathTc1) {
-      plan.lists = hsd::sim_tc_lists(rows, nsm);
-      plan.gamma = hsd::sim_tc1_gamma(c->dim);
-      CU(hsd::launch_sim_tc1((const float*)c->keys, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial,
-                             nullptr, s));
-    } else if (p == kPathTc3) {
-      plan.lists = hsd::sim_tc_lists(rows, nsm);
-      plan.gamma = hsd::sim_tc_gamma(c->dim);
-      CU(hsd::launch_sim_tc((const float*)c->keys, c->n, rb, re, c->dim, q, Bs, plan.lists, sc->qsplit, sc->partial,
-                            nullptr, s));
-    } else {
-      CU(hsd::launch_sim((const float*)c->keys, rb, re, c->dim, q, Bs, plan, sc->partial, s));
-    }
+    hsd::ListGeom geom{};
+    CU(hsd::launch_sim_wide(fkeys, fdtype, c->n, rb, re, c->dim, q, Bs, lists, sc->qslab, sc->partial, nullptr, s,
+                            &geom));
     if (marks && marks->after_sim && b0 + W >= B) CU(cudaEventRecord(marks->after_sim, s));
     hsd::P2PPublish pb{};
     if (pub) {
       pb = *pub;
       pb.q_offset = b0;
     }
-    CU(hsd::launch_select(sc->partial, plan.lists, Bs, k, c->keys, c->dtype, c->dim, q, c->maxnorm, plan.gamma,
-                          scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->overflow, sc->sel, s,
+    CU(hsd::launch_select(sc->partial, lists, Bs, k, c->keys, c->dtype, c->dim, q, c->maxnorm, gamma, geom,
+                          scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->stats, sc->sel, nsm, s,
                           pub ? &pb : nullptr));
   }
   if (marks && marks->after_select) CU(cudaEventRecord(marks->after_select, s));
@@ -403,12 +376,7 @@ hsd_status hsd_collection_create_ex(int device, int dim, int64_t capacity, int d
 hsd_status hsd_collection_destroy(hsd_collection* c) {
   if (!c) return HSD_OK;
   cudaSetDevice(c->device);
-  for (auto& kv : c->scratch) {
-    cudaFree(kv.second.partial);
-    cudaFree(kv.second.sel);
-    cudaFree(kv.second.qsplit);
-    cudaFree(kv.second.overflow);
-  }
+  for (auto& kv : c->scratch) free_scratch(kv.second);
   cudaFree(c->keys);
   cudaFree(c->tokens);
   cudaFree(c->shadow);
@@ -548,7 +516,7 @@ hsd_status hsd_collection_generate_ex(hsd_collection* c, int kind, uint64_t db_s
     return fail(HSD_ERR_CONFIG, "unknown payload family %d", payload);
   if (payload == HSD_PAYLOAD_TRAJ && traj_T < 1) return fail(HSD_ERR_CONFIG, "traj_T must be >= 1");
   if (row0 < 0) return fail(HSD_ERR_INVALID_INPUT, "negative row offset");
-  if (kind != 0 && kind != 1) return fail(HSD_ERR_CONFIG, "unknown synthetic family %d", kind);
+  if (kind < HSD_SYNTH_EXACT || kind > HSD_SYNTH_CLUSTER) return fail(HSD_ERR_CONFIG, "unknown synthetic family %d", kind);
   if (n < 0) return fail(HSD_ERR_INVALID_INPUT, "negative record count");
   if (n == 0) return HSD_OK;
   hsd_status st = require_device(c->device);
@@ -578,65 +546,62 @@ hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B,
 }
 
 hsd_status hsd_set_sim_path(int path) {
-  if (path < 0 || path > 6)
-    return fail(HSD_ERR_INVALID_INPUT,
-                "path must be 0 auto, 1 rows, 2 tile, 3 tc (wide TF32), 4 tc3 (3xTF32), 5 tc1 (64-query TF32), "
-                "6 tc_single (wide kernels without CTA pairs)");
-  g_path = path;
-  hsd::sim_wide_set_single(path == kPathTcSingle);
+  if (path != 0 && path != 1)
+    return fail(HSD_ERR_INVALID_INPUT, "path must be 0 (auto) or 1 (single-CTA wide kernels, no CTA pairs)");
+  hsd::sim_wide_set_single(path == 1);
   return HSD_OK;
 }
 
 hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
                                 void* stream) {
   if (!c || !queries || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
-  if (variant < 1 || variant > 4)
-    return fail(HSD_ERR_INVALID_INPUT,
-                "variant must be 1 (wide TF32/bf16), 2 (64-query TF32), 3 (3xTF32) or 4 (bf16 filter copy)");
+  if (variant != 1 && variant != 4)
+    return fail(HSD_ERR_INVALID_INPUT, "variant must be 1 (stored keys: TF32 / bf16) or 4 (bf16 filter copy)");
   if (variant == 4 && !c->shadow) return fail(HSD_ERR_INVALID_INPUT, "collection has no bf16 filter copy");
-  const int maxB = (variant == 1 || variant == 4) ? 256 : kSlab;
-  if (B < 1 || B > maxB) return fail(HSD_ERR_INVALID_INPUT, "debug dump supports 1 <= B <= %d", maxB);
-  if (variant != 1 && variant != 4 && c->dtype != HSD_DTYPE_F32)
-    return fail(HSD_ERR_INVALID_INPUT, "variant needs fp32 keys");
+  if (B < 1 || B > 256) return fail(HSD_ERR_INVALID_INPUT, "debug dump supports 1 <= B <= 256");
   hsd_status st = require_device(c->device);
   if (st != HSD_OK) return st;
   if (c->n == 0) return HSD_OK;
-  if (variant == 1 && B > 256) return fail(HSD_ERR_INVALID_INPUT, "debug dump supports B <= 256");
-  const int lists = hsd::sim_tc_lists(c->n, num_sms(c->device));
+  const int nsm = num_sms(c->device);
+  size_t need_p = 0, need_s = 0, need_q = 0;
+  scratch_need(B, c->n, nsm, c->dim, false, &need_p, &need_s, &need_q);
+  const int lists = hsd::sim_wide_lists(B, c->n, nsm);
   Scratch* sc = nullptr;
-  st = get_scratch(c, (cudaStream_t)stream, (size_t)lists * B * hsd::dev::kCandLocal * 8,
-                   std::max(hsd::sim_tc_scratch_bytes(c->dim), hsd::sim_wide_scratch_bytes(c->dim)), &sc);
+  st = get_scratch(c, (cudaStream_t)stream, need_p, need_s, need_q, &sc);
   if (st != HSD_OK) return st;
-  if (variant == 3)
-    CU(hsd::launch_sim_tc((const float*)c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial,
-                          out, (cudaStream_t)stream));
-  else if (variant == 2)
-    CU(hsd::launch_sim_tc1((const float*)c->keys, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial,
-                           out, (cudaStream_t)stream));
-  else if (variant == 4)
-    CU(hsd::launch_sim_wide(c->shadow, HSD_DTYPE_BF16, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit,
+  if (variant == 4)
+    CU(hsd::launch_sim_wide(c->shadow, HSD_DTYPE_BF16, c->n, 0, c->n, c->dim, queries, B, lists, sc->qslab,
                             sc->partial, out, (cudaStream_t)stream));
   else
-    CU(hsd::launch_sim_wide(c->keys, c->dtype, c->n, 0, c->n, c->dim, queries, B, lists, sc->qsplit, sc->partial, out,
+    CU(hsd::launch_sim_wide(c->keys, c->dtype, c->n, 0, c->n, c->dim, queries, B, lists, sc->qslab, sc->partial, out,
                             (cudaStream_t)stream));
   return HSD_OK;
 }
 
-hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count) {
-  if (!c || !count) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+hsd_status hsd_search_stats(hsd_collection* c, void* stream, int reset, int* stats3) {
+  if (!c || !stats3) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   hsd_status st = require_device(c->device);
   if (st != HSD_OK) return st;
-  *count = 0;
-  int* ov = nullptr;
+  stats3[0] = stats3[1] = stats3[2] = 0;
+  int* dv = nullptr;
   {
     std::lock_guard<std::mutex> lk(c->mu);
     auto it = c->scratch.find((cudaStream_t)stream);
     if (it == c->scratch.end()) return HSD_OK;
-    ov = it->second.overflow;
+    dv = it->second.stats;
   }
   CU(cudaStreamSynchronize((cudaStream_t)stream));
-  CU(cudaMemcpy(count, ov, sizeof(int), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(stats3, dv, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  if (reset) CU(cudaMemset(dv, 0, 4 * sizeof(int)));
   return HSD_OK;
+}
+
+hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count) {
+  if (!count) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  int v[3];
+  hsd_status st = hsd_search_stats(c, stream, 0, v);
+  *count = v[0];
+  return st;
 }
 
 static hsd_status check_verify_params(const hsd_verify_params* params, int P) {
@@ -686,7 +651,8 @@ hsd_status device_params(int device, const hsd_verify_params* params, int P, cud
 static hsd_status verify_impl(int device, hsd_collection* c, const uint8_t* drafts, const int32_t* ids, int E, int k,
                               int L, const float* logits, const float* feat_now, const float* feat_prev, int d_f,
                               const int32_t* history, int gap_d, const hsd_verify_params* params, int P,
-                              hsd_outcome* out, uint8_t* tokens, void* stream, const double* cos_in = nullptr) {
+                              hsd_outcome* out, uint8_t* tokens, void* stream, const double* cos_in = nullptr,
+                              const hsd_verify_params* params_dev = nullptr) {
   if (L != 7 && L != 21) return fail(HSD_ERR_INVALID_INPUT, "draft length must be 7 or 21, got %d", L);
   if (k < 1 || k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k must be in [1, %d]", HSD_K_MAX);
   if (E < 0) return fail(HSD_ERR_INVALID_INPUT, "negative episode count");
@@ -700,9 +666,11 @@ static hsd_status verify_impl(int device, hsd_collection* c, const uint8_t* draf
     return fail(HSD_ERR_INVALID_INPUT, "verify-skip needs fp32 features with d_f a multiple of 4");
   st = require_device(device);
   if (st != HSD_OK) return st;
-  const hsd_verify_params* dp = nullptr;
-  st = device_params(device, params, P, (cudaStream_t)stream, &dp);
-  if (st != HSD_OK) return st;
+  const hsd_verify_params* dp = params_dev;  // an engine's own copy (stream-ordered / per captured graph)
+  if (!dp) {
+    st = device_params(device, params, P, (cudaStream_t)stream, &dp);
+    if (st != HSD_OK) return st;
+  }
   CU(hsd::launch_verify(ids, E, k, L, c ? c->tokens : nullptr, drafts, logits, feat_now, feat_prev, d_f, history, gap_d, dp, P,
                         need_cos, out, tokens, (cudaStream_t)stream, cos_in));
   return HSD_OK;
@@ -819,6 +787,7 @@ struct StageSlot {
 struct StepGraph {
   std::vector<uint8_t> key;
   cudaGraphExec_t exec = nullptr;
+  hsd_verify_params* vp = nullptr;  // private device copy of the captured parameters
 };
 
 struct hsd_engine {
@@ -835,6 +804,12 @@ struct hsd_engine {
   cudaStream_t side = nullptr;  // K5 and the verify-skip similarity run concurrently with K1
   cudaEvent_t fork = nullptr, join = nullptr;
   double* cos = nullptr;  // [max_B] should_skip similarity, computed on the side stream
+  // Fixed device state of the engine's steps: K1/K2 scratch sized for max_B
+  // at creation and never reallocated, and the eager steps' parameter copy
+  // (updated stream-ordered).  Captured graphs hold these pointers, so one
+  // engine issues its steps on one stream at a time.
+  Scratch scr;
+  hsd_verify_params* vp = nullptr;
 };
 
 static constexpr int kStepEvents = 6;
@@ -878,6 +853,13 @@ hsd_status hsd_engine_create(hsd_collection* c, int max_B, int k, int L, int d_f
       if (r == cudaSuccess) r = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
   }
   alloc(&e->cos, (size_t)max_B * 8);
+  alloc(&e->vp, sizeof(hsd_verify_params));
+  if (r == cudaSuccess) {
+    size_t need_p = 0, need_s = 0, need_q = 0;
+    scratch_need(max_B, INT64_MAX / 4, num_sms(c->device), c->dim, true, &need_p, &need_s, &need_q);
+    if (alloc_scratch(e->scr, need_p, need_s, need_q) != HSD_OK) r = cudaErrorMemoryAllocation;
+    e->scr.fixed = true;
+  }
   if (r == cudaSuccess) r = cudaStreamCreateWithFlags(&e->up, cudaStreamNonBlocking);
   if (r == cudaSuccess) r = cudaStreamCreateWithFlags(&e->down, cudaStreamNonBlocking);
   if (r != cudaSuccess) {
@@ -929,6 +911,7 @@ hsd_status hsd_engine_destroy(hsd_engine* e) {
   if (!e) return HSD_OK;
   cudaSetDevice(e->c->device);
   for (cudaEvent_t x : e->ev) cudaEventDestroy(x);
+  cudaDeviceSynchronize();  // no step still reads the engine's buffers
   cudaFree(e->cos);
   if (e->side) {
     cudaStreamSynchronize(e->side);
@@ -946,18 +929,24 @@ hsd_status hsd_engine_destroy(hsd_engine* e) {
   }
   if (e->up) cudaStreamDestroy(e->up);
   if (e->down) cudaStreamDestroy(e->down);
-  for (StepGraph& g : e->graphs) cudaGraphExecDestroy(g.exec);
+  for (StepGraph& g : e->graphs) {
+    cudaGraphExecDestroy(g.exec);
+    cudaFree(g.vp);
+  }
+  free_scratch(e->scr);
+  cudaFree(e->vp);
   delete e;
   return HSD_OK;
 }
 
-hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
-                    const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream) {
-  if (!e || !io || !vp) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
-  if (B < 0 || B > e->max_B) return fail(HSD_ERR_INVALID_INPUT, "batch %d outside [0, %d]", B, e->max_B);
-  if (B == 0) return HSD_OK;
-  hsd_status st = require_device(e->c->device);
-  if (st != HSD_OK) return st;
+}  // extern "C"
+
+// One decode round on `stream`; vp_dev: the device copy of *vp the verify
+// kernel reads (the engine's eager copy, or a captured graph's own).
+static hsd_status step_impl(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                            const hsd_verify_params* vp_dev, const hsd_metric_params* mp, const hsd_norm_bounds* nb,
+                            int gap_d, void* stream) {
+  hsd_status st = HSD_OK;
   cudaStream_t s = (cudaStream_t)stream;
   cudaEvent_t* ev = (e->recorded < e->max_steps) ? &e->ev[(size_t)e->recorded * kStepEvents] : nullptr;
   if (ev) CU(cudaEventRecord(ev[0], s));
@@ -992,12 +981,12 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
   }
   const int k5_blocks = io->xyz ? (B + 15) / 16 : 0;  // K5 runs 16 windows per CTA
   st = search_impl(e->c, io->queries, B, e->k, 0, e->c->n, io->scores, io->ids, s, ev ? &marks : nullptr,
-                   k5_blocks);  // K1+K2
+                   k5_blocks, nullptr, &e->scr);  // K1+K2
   if (st != HSD_OK) return st;
   if (use_side) CU(cudaStreamWaitEvent(s, e->join, 0));
   st = verify_impl(e->c->device, e->c, nullptr, io->ids, B, e->k, e->L, io->logits, io->feat_now, io->feat_prev,
-                   e->d_f, io->history, gap_d, vp, 1, io->out, io->tokens, stream,
-                   cos_side ? e->cos : nullptr);  // K4
+                   e->d_f, io->history, gap_d, vp, 1, io->out, io->tokens, stream, cos_side ? e->cos : nullptr,
+                   vp_dev);  // K4
   if (st != HSD_OK) return st;
   if (ev) {
     if (!use_side) {
@@ -1007,6 +996,32 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
     CU(cudaEventRecord(ev[3], s));
     ++e->recorded;
   }
+  return HSD_OK;
+}
+
+extern "C" {
+
+hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verify_params* vp,
+                    const hsd_metric_params* mp, const hsd_norm_bounds* nb, int gap_d, void* stream) {
+  if (!e || !io || !vp) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (B < 0 || B > e->max_B) return fail(HSD_ERR_INVALID_INPUT, "batch %d outside [0, %d]", B, e->max_B);
+  if (B == 0) return HSD_OK;
+  hsd_status st = require_device(e->c->device);
+  if (st != HSD_OK) return st;
+  st = check_verify_params(vp, 1);
+  if (st != HSD_OK) return st;
+  // stream-ordered copy: the previous steps' verify kernels read their own values first
+  CU(cudaMemcpyAsync(e->vp, vp, sizeof *vp, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return step_impl(e, B, io, vp, e->vp, mp, nb, gap_d, stream);
+}
+
+hsd_status hsd_engine_stats(hsd_engine* e, int reset, int* stats3) {
+  if (!e || !stats3) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(e->c->device);
+  if (st != HSD_OK) return st;
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(stats3, e->scr.stats, 3 * sizeof(int), cudaMemcpyDeviceToHost));
+  if (reset) CU(cudaMemset(e->scr.stats, 0, 4 * sizeof(int)));
   return HSD_OK;
 }
 
@@ -1042,14 +1057,19 @@ hsd_status hsd_step_graph(hsd_engine* e, int B, const hsd_step_io* io, const hsd
       return HSD_OK;
     }
   // miss: run the round eagerly (warms every per-stream cache), then capture
-  // the same launch sequence for the next calls
+  // the same launch sequence for the next calls, reading a private copy of
+  // the parameters (the engine's scratch is fixed, so the graph's other
+  // pointers stay valid)
   const int saved = e->max_steps;
   e->max_steps = 0;  // no stage-timing events inside graphs
   st = hsd_step(e, B, io, vp, mp, nb, gap_d, stream);
+  hsd_verify_params* gvp = nullptr;
   if (st == HSD_OK) {
+    CU(cudaMalloc(&gvp, sizeof *vp));
+    CU(cudaMemcpy(gvp, vp, sizeof *vp, cudaMemcpyHostToDevice));
     cudaGraph_t g = nullptr;
     CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
-    st = hsd_step(e, B, io, vp, mp, nb, gap_d, stream);
+    st = step_impl(e, B, io, vp, gvp, mp, nb, gap_d, stream);
     cudaError_t ce = cudaStreamEndCapture(s, &g);
     if (st == HSD_OK && ce != cudaSuccess) st = cuda_fail(ce, "cudaStreamEndCapture");
     if (st == HSD_OK) {
@@ -1059,14 +1079,20 @@ hsd_status hsd_step_graph(hsd_engine* e, int B, const hsd_step_io* io, const hsd
         st = cuda_fail(ce, "cudaGraphInstantiate");
       } else {
         if (e->graphs.size() >= 16) {
-          for (StepGraph& old : e->graphs) cudaGraphExecDestroy(old.exec);
+          CU(cudaStreamSynchronize(s));  // replays of the old graphs may still read their parameters
+          for (StepGraph& old : e->graphs) {
+            cudaGraphExecDestroy(old.exec);
+            cudaFree(old.vp);
+          }
           e->graphs.clear();
         }
-        e->graphs.push_back({std::move(key), x});
+        e->graphs.push_back({std::move(key), x, gvp});
+        gvp = nullptr;
       }
     }
     if (g) cudaGraphDestroy(g);
   }
+  if (gvp) cudaFree(gvp);
   e->max_steps = saved;
   return st;
 }
@@ -1364,7 +1390,7 @@ hsd_status hsd_merge_topk(int device, const double* g_scores, const int32_t* g_i
 // ------------------------------------------------------------------ generators
 hsd_status hsd_gen_queries(int device, int kind, uint64_t q_seed, uint64_t db_seed, int64_t n_rows, int64_t q0, int B,
                            int dim, float* out, void* stream) {
-  if (kind != 0 && kind != 1) return fail(HSD_ERR_CONFIG, "unknown synthetic family %d", kind);
+  if (kind < HSD_SYNTH_EXACT || kind > HSD_SYNTH_CLUSTER) return fail(HSD_ERR_CONFIG, "unknown synthetic family %d", kind);
   if (B < 0 || dim < 1) return fail(HSD_ERR_INVALID_INPUT, "bad shape");
   hsd_status st = require_device(device);
   if (st != HSD_OK) return st;

@@ -844,30 +844,36 @@ int sim_wide_lists(int B, int64_t rows, int num_sms) {
 }
 
 double sim_wide_gamma(int dim, int key_dtype) {
-  // Accumulation: fp32 tensor-core accumulator (not round-to-nearest) over dim
-  // products, <= (dim + 16) 2^-23 relative to sum|k_i q_i| (as for TF32).
-  const double acc = (dim + 16.0) / 8388608.0;
+  // Relative forward error of the filter score S~ against the real dot S of
+  // the stored keys and the fp32 query: |S - S~| <= gamma * sum|k_i q_i|.
+  // (k_select.cu adds the absolute underflow / flush-to-zero slack.)
+  // Products: with operands rounded to k' = k(1 + a), q' = q(1 + b),
+  // |k'q' - kq| <= (|a| + |b| + |ab|) |kq|; bf16 x bf16 and tf32 x tf32
+  // products are exact in fp32.  Accumulation: the fp32 tensor-core
+  // accumulator (not round-to-nearest) over dim products, <= (dim + 16) 2^-23
+  // relative to sum|k'q'| <= (1 + u)^2 sum|kq|; 2^-22 per product covers
+  // truncation of every addend to the running exponent.
+  const double acc = (dim + 16.0) * 0x1p-22 * 1.02;
   if (key_dtype & 0x100) {
-    // bf16 filter copy of fp32 keys: both operands rounded (RN, 2^-9 each):
-    // |kq - k'q'| <= (2^-9 + 2^-9 + 2^-18) |k||q| per product.
-    return (1.0 / 256.0 + 1.0 / 262144.0) * 1.0001 + acc;
+    // bf16 filter copy of fp32 keys: both operands rounded to bf16, RN-even,
+    // unit roundoff u = 2^-8 (8-bit significand): a = b = 2^-8.
+    return (0x1p-7 + 0x1p-16) * 1.0001 + acc;
   }
   if (key_dtype == HSD_DTYPE_BF16) {
-    // bf16 keys are exact; queries rounded to bf16 (RN): |q - bf16(q)| <= 2^-9 |q|;
-    // bf16 x bf16 products are exact in fp32.
-    return 1.0 / 512.0 * 1.0001 + acc;
+    // bf16 keys are exact; queries rounded to bf16 (RN-even): b = 2^-8.
+    return 0x1p-8 * 1.0001 + acc;
   }
-  // TF32 operands: |x - tf32(x)| <= 2^-10 |x| (truncation), so
-  // |kq - k'q'| <= (2^-10 + 2^-10 (1 + 2^-10)) |k||q| per product.
-  return (2.0 + 1.0 / 1024.0) / 1024.0 * 1.0001 + acc;
+  // TF32 operands (fp32 tiles read as tf32: the low 13 mantissa bits are
+  // dropped, |x - tf32(x)| < 2^-10 |x|): a = b = 2^-10.
+  return (0x1p-9 + 0x1p-20) * 1.0001 + acc;
 }
 
 size_t sim_wide_scratch_bytes(int dim) { return (size_t)1024 * dim * sizeof(float); }
 
 cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin, int64_t row_end,
                             int dim, const float* queries, int B, int lists, void* scratch, uint64_t* partial,
-                            float* dump, cudaStream_t s) {
-  if (B < 1 || B > 1024) return cudaErrorInvalidValue;
+                            float* dump, cudaStream_t s, ListGeom* geom) {
+  if (B < 1 || B > kMaxBatchPass) return cudaErrorInvalidValue;
   const int groups = wide_groups(B);
   const int NS = groups > 1 ? 4 : (B <= 64 ? 1 : (B <= 128 ? 2 : 4));
   const int box = 64 * NS;          // query rows per CTA
@@ -892,9 +898,11 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
   if (e != cudaSuccess) return e;
   const int64_t n_blocks = (row_end - row_begin + kBM - 1) / kBM;
   const int64_t per = (n_blocks + lists - 1) / lists;
+  if (geom) *geom = ListGeom{row_begin, row_end, per, 1};
   if (pair) {
     const int64_t pairs = lists / 2;
     const int64_t per_pair = ((n_blocks + pairs - 1) / pairs + 1) & ~(int64_t)1;  // even: whole block pairs
+    if (geom) *geom = ListGeom{row_begin, row_end, per_pair, 2};
     switch (groups) {
 #define HSD_PAIR(G)                                                                                        \
   case G:                                                                                                  \

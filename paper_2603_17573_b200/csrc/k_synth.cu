@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_keys_kernel(int kind, uint64_
   } else {
     long long ss = 0;
     for (int c = threadIdx.x; c < dim; c += kGenThreads) {
-      long long r = hsd_key_raw(kbase, src, dim, c);
+      long long r = hsd_key_raw_kind(kind, kbase, src, dim, c);
       ss += r * r;
     }
     ss = BR(tmp.i).Sum(ss);
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_keys_kernel(int kind, uint64_
     __syncthreads();
     ss = s_ss;
     for (int c = threadIdx.x; c < dim; c += kGenThreads) {
-      const float v = store_key(out + c, hsd_norm_val(hsd_key_raw(kbase, src, dim, c), ss));
+      const float v = store_key(out + c, hsd_norm_val(hsd_key_raw_kind(kind, kbase, src, dim, c), ss));
       nrm2 += (double)v * (double)v;
     }
     __syncthreads();
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_queries_kernel(int kind, uint
   }
   long long ss = 0;
   for (int c = threadIdx.x; c < dim; c += kGenThreads) {
-    long long r = hsd_query_raw(q_seed, db_seed, q, row, dim, c);
+    long long r = hsd_query_raw_kind(kind, q_seed, db_seed, q, row, dim, c);
     ss += r * r;
   }
   ss = BR(tmp).Sum(ss);
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kGenThreads) gen_queries_kernel(int kind, uint
   __syncthreads();
   ss = s_ss;
   for (int c = threadIdx.x; c < dim; c += kGenThreads)
-    o[c] = hsd_norm_val(hsd_query_raw(q_seed, db_seed, q, row, dim, c), ss);
+    o[c] = hsd_norm_val(hsd_query_raw_kind(kind, q_seed, db_seed, q, row, dim, c), ss);
 }
 
 // One CTA per (episode, position): 256 threads = 256 bins.

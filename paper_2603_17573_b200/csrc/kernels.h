@@ -28,33 +28,20 @@ cudaError_t launch_quantize(const double* actions, int64_t n, const double* lohi
 cudaError_t launch_quantize_tokens(const double* actions /*[n][21]*/, int64_t n, uint8_t* tokens /*[n][32]*/,
                                    int32_t* bad, cudaStream_t s);
 
-// ---- K1 similarity + per-CTA candidate lists ---------------------------------
-// partial: [grid][B][kCandLocal] u64 candidate keys; returns grid in *lists.
-struct SimPlan {
-  int lists;      // number of candidate lists per query (= grid of the sim kernel)
-  double gamma;   // relative error bound of the approximate score path
+// ---- K1 similarity + per-list candidate lists --------------------------------
+// partial: [lists][B][kCandLocal] u64 candidate keys (the filter's top-32 of
+// each list's rows per query).
+constexpr int kMaxBatchPass = 1024;  // queries per K1 pass
+
+// Rows covered by filter list l of a pass (what the exact fallback rescans):
+// blocks first + j * stride (j < count) of 128 rows, clipped to row_end, with
+//   stride 1 (one CTA / cluster per list): first = l * per, count = min(per, nb - first)
+//   stride 2 (CTA pairs, list 2u + h):     blocks u*per + h, u*per + h + 2, ... < min((u+1)*per, nb)
+struct ListGeom {
+  int64_t row_begin, row_end;
+  int64_t per;
+  int stride;
 };
-SimPlan sim_plan(int B, int64_t rows, int dim, int num_sms);
-cudaError_t launch_sim(const float* keys, int64_t row_begin, int64_t row_end, int dim, const float* queries, int B,
-                       const SimPlan& plan, uint64_t* partial, cudaStream_t s);
-
-// K1' tcgen05 3xTF32 path (k_sim_tc.cu): B <= 64 queries per launch, one
-// persistent CTA per SM.  scratch: sim_tc_scratch_bytes(dim) (Qh/Ql split).
-// dump != nullptr -> debug mode writing every approximate score [B][rows].
-size_t sim_tc_scratch_bytes(int dim);
-double sim_tc_gamma(int dim);
-int sim_tc_lists(int64_t rows, int num_sms);
-cudaError_t launch_sim_tc(const float* keys, int64_t n_keys_total, int64_t row_begin, int64_t row_end, int dim,
-                          const float* queries, int B, int lists, float* scratch, uint64_t* partial, float* dump,
-                          cudaStream_t s);
-
-// K1 tcgen05 TF32 filter path (k_sim_tc1.cu, default for B > 4): same
-// contract; scratch sim_tc1_scratch_bytes(dim) (64-row padded query slab).
-double sim_tc1_gamma(int dim);
-size_t sim_tc1_scratch_bytes(int dim);
-cudaError_t launch_sim_tc1(const float* keys, int64_t n_keys_total, int64_t row_begin, int64_t row_end, int dim,
-                           const float* queries, int B, int lists, float* scratch, uint64_t* partial, float* dump,
-                           cudaStream_t s);
 
 // K1 wide tcgen05 filter (k_sim_wide.cu): up to 256 queries per pass (UMMA
 // N = 64/128/256), fp32 keys read as TF32 or bf16 keys (kind::f16); same
@@ -67,18 +54,22 @@ double sim_wide_gamma(int dim, int key_dtype);
 size_t sim_wide_scratch_bytes(int dim);
 cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin, int64_t row_end,
                             int dim, const float* queries, int B, int lists, void* scratch, uint64_t* partial,
-                            float* dump, cudaStream_t s);
+                            float* dump, cudaStream_t s, ListGeom* geom = nullptr);
 
-// ---- K2 select: margin candidates + exact fp64 rescoring + final top-k -------
-// Three launches (candidates, rescoring over (query, 8-candidate) CTAs, rank);
-// scratch: select_scratch_bytes(B).
+// ---- K2 select: exact top-k from the filter lists -----------------------------
+// Four launches (candidates + threshold, pooled rescoring, exact range
+// fallback, rank; k_select.cu); scratch: select_scratch_bytes(B), B <= kMaxBatchPass.
+// stats (device, accumulated): [0] queries that needed the range fallback,
+// [1] pooled candidates rescored, [2] fallback lists rescanned.
 size_t select_scratch_bytes(int B);
+int select_max_lists();
 // pub != nullptr: the rank kernel publishes the top-k records (global ids +
 // draft tokens) into every peer's window instead of writing scores / ids.
 struct P2PPublish;
 cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, const void* keys, int key_dtype, int dim,
-                          const float* queries, const unsigned long long* maxnorm_bits, double gamma, double* scores,
-                          int32_t* ids, int* overflow, void* scratch, cudaStream_t s, const P2PPublish* pub = nullptr);
+                          const float* queries, const unsigned long long* maxnorm_bits, double gamma,
+                          const ListGeom& geom, double* scores, int32_t* ids, int* stats, void* scratch, int num_sms,
+                          cudaStream_t s, const P2PPublish* pub = nullptr);
 
 // K3 merge of G gathered per-rank top-k records (sharded search); tokens
 // [G][B][k][32] are permuted alongside when non-null.

@@ -125,3 +125,58 @@ def test_cohorts_on_two_streams_match_serial_steps(torch, B):
         for s in range(S):
             for kk in outs[s]:
                 assert torch.equal(outs[s][kk].cpu(), ref[s][kk]), (rep, s, kk)
+
+
+def test_graphs_alternating_batch_and_params(torch):
+    """Cached graphs keep their own parameters and the engine's fixed scratch:
+    graphs captured for (B = 8, strict), (B = 160, relaxed + skip) and
+    (B = 40, tight caps) replayed in alternation equal the eager steps (a
+    larger B used to reallocate the scratch an older graph still pointed at,
+    and every graph read the last parameters copied)."""
+    n, dim, k, L, d_f = 30000, 256, 8, 7, 256
+    col = H.Collection(dim, capacity=n)
+    col.generate(H.REAL, 5, n)
+    col.set_filter("bf16_copy")
+    eng = H.Engine(col, 160, k, L, d_f, 15)
+    cases = [(8, H.VerifyParams.make(relaxed=False)),
+             (160, H.VerifyParams.make(skip_enabled=True, min_S=0.9, O_dist=5)),
+             (40, H.VerifyParams.make(bias_seq_max=4, bias_token_max=2))]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        ins = [make_inputs(torch, col, n, dim, B, L, d_f, i) for i, (B, _) in enumerate(cases)]
+        ref = []
+        for i, (B, vp) in enumerate(cases):
+            o = outputs(torch, B, k, L, "cuda")
+            eng.step(B, H.StepBuffers(**ins[i], **o), vp, stream=st)
+            st.synchronize()
+            ref.append({kk: v.clone() for kk, v in o.items()})
+        bufs = [outputs(torch, B, k, L, "cuda") for B, _ in cases]
+        for rep in range(4):
+            order = [0, 1, 2] if rep % 2 == 0 else [2, 0, 1]
+            for i in order:
+                B, vp = cases[i]
+                for v in bufs[i].values():
+                    v.zero_()
+                eng.step(B, H.StepBuffers(**ins[i], **bufs[i]), vp, stream=st, graph=True)
+                # an eager step in between with other parameters must not leak into the graphs
+                eng.step(B, H.StepBuffers(**ins[i], **outputs(torch, B, k, L, "cuda")),
+                         H.VerifyParams.make(relaxed=True, bias_seq_max=0, bias_token_max=0), stream=st)
+            st.synchronize()
+            for i in range(3):
+                for kk in bufs[i]:
+                    assert torch.equal(bufs[i][kk], ref[i][kk]), (rep, i, kk)
+
+
+def test_multi_pass_batch_scratch(torch):
+    """B = 1280 over 24k rows: two passes with different filter-list counts
+    (1024-query clusters, then a 256-query pair pass) share one scratch."""
+    from oracle import oracle as O
+    n, dim = 24_000, 64
+    col = H.Collection(dim, capacity=n)
+    col.generate(O.REAL, 3, n)
+    for B in (1280, 1100, 2100):
+        q = H.gen_queries(O.REAL, 4, 3, n, 0, B, dim)
+        sc, ids = col.search_topk_exact(q, 8)
+        osc, oid = O.search_synth(O.REAL, 3, n, q.cpu().numpy(), 8, threads=0)
+        np.testing.assert_array_equal(ids.cpu().numpy(), oid)
+        np.testing.assert_array_equal(sc.cpu().numpy(), osc)

@@ -1,6 +1,7 @@
-"""tcgen05 3xTF32 similarity kernel (K1'): its approximate filter scores stay
-inside the error bound the exact rescoring relies on (k_sim_tc.cu,
-sim_tc_gamma), and every similarity path gives bit-identical top-k results."""
+"""tcgen05 filter kernels (K1, k_sim_wide.cu): the approximate filter scores
+stay inside the forward error bound the exact selection relies on
+(sim_wide_gamma), including on rounding-adversarial inputs, and every kernel
+variant gives bit-identical top-k results."""
 import numpy as np
 import pytest
 
@@ -17,81 +18,14 @@ def torch():
     return torch
 
 
-def gamma_tc(dim, variant):
-    if variant == 3:  # 3xTF32 (k_sim_tc.cu sim_tc_gamma)
-        return 3.0 / 2**20 + (3.0 * dim + 16.0) / 2**23
-    return (2.0 + 1.0 / 1024) / 1024 * 1.0001 + (dim + 16.0) / 2**23  # TF32 (k_sim_tc1.cu)
-
-
-@pytest.mark.parametrize("variant", [1, 2, 3])
-@pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
-@pytest.mark.parametrize("dim,n,B", [(64, 3000, 64), (4096, 3000, 64), (4096, 1000, 13), (256, 777, 1)])
-def test_tc_scores_within_bound(torch, kind, dim, n, B, variant):
-    col = H.Collection(dim, capacity=n)
-    col.generate(kind, 5, n)
-    q = H.gen_queries(kind, 6, 5, n, 0, B, dim)
-    approx = col.debug_sim_scores(q, variant=variant).cpu().numpy().astype(np.float64)
-    keys = O.gen_keys(kind, 5, 0, n, dim).astype(np.float64)
-    qq = q.cpu().numpy().astype(np.float64)
-    exact = qq @ keys.T
-    bound = gamma_tc(dim, variant) * (np.abs(qq) @ np.abs(keys).T)
-    err = np.abs(approx - exact)
-    assert np.all(err <= bound), float((err / np.maximum(bound, 1e-300)).max())
-    scale = np.linalg.norm(qq, axis=1, keepdims=True) * np.linalg.norm(keys, axis=1)[None, :]
-    rel = float((err / scale).max())
-    if variant == 3:
-        # all three split terms reach the accumulator: the residual is the
-        # tensor core's (truncating) fp32 accumulation, far inside the bound
-        assert rel < 1e-4
-    else:
-        assert rel < 2e-3
-    if kind == O.EXACT:  # k/16 values are exact in TF32 -> exact scores
-        assert np.array_equal(approx, exact)
-
-
-@pytest.mark.parametrize("path", ["rows", "tile", "tc", "tc1", "tc3"])
-@pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
-def test_paths_bit_identical(torch, path, kind):
-    try:
-        H.set_sim_path(path)
-        for dim, n in ((64, 5000), (4096, 2500), (4352, 1200)):
-            col = H.Collection(dim, capacity=n)
-            col.generate(kind, 17, n)
-            for B in (1, 4, 8, 13, 64, 70):
-                q = H.gen_queries(kind, 18, 17, n, 3, B, dim)
-                sc, ids = col.search_topk_exact(q, 8)
-                osc, oid = O.search_synth(kind, 17, n, q.cpu().numpy(), 8)
-                np.testing.assert_array_equal(ids.cpu().numpy(), oid, err_msg=f"{path} dim={dim} B={B}")
-                np.testing.assert_array_equal(sc.cpu().numpy(), osc)
-            assert col.overflow_count() == 0
-    finally:
-        H.set_sim_path("auto")
-
-
-@pytest.mark.parametrize("path", ["tc", "tc1", "tc3"])
-def test_tc_ragged_tail_and_range(torch, path):
-    """Row counts that are not multiples of the 128-key block, and sub-ranges."""
-    H.set_sim_path(path)
-    try:
-        n, dim = 1000 * 3 + 77, 128
-        col = H.Collection(dim, capacity=n)
-        col.generate(O.REAL, 9, n)
-        q = H.gen_queries(O.REAL, 10, 9, n, 0, 32, dim)
-        for rng in ((0, n), (5, 133), (1000, 2999), (n - 1, n)):
-            sc, ids = col.search_topk_exact(q, 5, row_range=rng)
-            keys = O.gen_keys(O.REAL, 9, rng[0], rng[1] - rng[0], dim)
-            osc, oid = O.search_topk(keys, q.cpu().numpy(), 5)
-            kk = oid.shape[1]
-            np.testing.assert_array_equal(ids.cpu().numpy()[:, :kk], oid + rng[0])
-            np.testing.assert_array_equal(sc.cpu().numpy()[:, :kk], osc)
-    finally:
-        H.set_sim_path("auto")
-
-
 # ----------------------------------------------------------------------------- wide kernel (k_sim_wide.cu)
+def acc_term(dim):
+    return (dim + 16.0) * 2.0**-22 * 1.02  # fp32 tensor-core accumulation (sim_wide_gamma)
+
+
 def gamma_wide(dim, bf16):
-    acc = (dim + 16.0) / 2**23
-    return (1.0 / 512 * 1.0001 + acc) if bf16 else ((2.0 + 1.0 / 1024) / 1024 * 1.0001 + acc)
+    """bf16 keys: query rounded to bf16, u = 2^-8; fp32 keys: TF32 truncation 2^-10 per operand."""
+    return (2.0**-8 * 1.0001 + acc_term(dim)) if bf16 else ((2.0**-9 + 2.0**-20) * 1.0001 + acc_term(dim))
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -183,7 +117,87 @@ def test_bf16_config_errors(torch):
 
 
 # ----------------------------------------------------------------------------- bf16 filter copy of fp32 keys
-GAMMA_COPY = lambda dim: (1.0 / 256 + 1.0 / 262144) * 1.0001 + (dim + 16.0) / 2**23  # noqa: E731
+def GAMMA_COPY(dim):
+    """bf16 copy of fp32 keys: both operands RN-even to bf16 (u = 2^-8 each)."""
+    return (2.0**-7 + 2.0**-16) * 1.0001 + acc_term(dim)
+
+
+# round-1 constants (unit roundoff taken as 2^-9): the adversarial inputs below must violate them
+OLD_GAMMA_COPY = lambda dim: (1.0 / 256 + 1.0 / 262144) * 1.0001 + (dim + 16.0) / 2**23  # noqa: E731
+OLD_GAMMA_BF16 = lambda dim: 1.0 / 512 * 1.0001 + (dim + 16.0) / 2**23  # noqa: E731
+
+
+def midpoint_vectors(rows, dim, seed):
+    """fp32 vectors whose every component sits just below a bf16 rounding
+    midpoint (1 + 2^-8 - 2^-20 times a power of two, random sign), so RN-even
+    rounds every one DOWN in magnitude by ~2^-8 relative."""
+    rng = np.random.default_rng(seed)
+    mant = np.float32(1.0 + 2.0**-8 - 2.0**-20)
+    scale = np.float32(2.0) ** (-5 - rng.integers(0, 3, size=(rows, dim))).astype(np.float32)
+    sign = np.where(rng.random((rows, dim)) < 0.5, -1, 1).astype(np.float32)
+    return (mant * scale * sign).astype(np.float32), sign
+
+
+@pytest.mark.parametrize("dim", [64, 4096])
+def test_filter_bound_midpoint_adversarial(torch, dim):
+    """Every product rounded the same way: the bf16 filter copy errs by ~2^-7
+    relative (both operands) and bf16 keys by ~2^-8 (query only).  The errors
+    exceed the round-1 constants and stay inside sim_wide_gamma."""
+    n, B = 300, 8
+    keys, sign = midpoint_vectors(n, dim, 1)
+    q = (np.abs(midpoint_vectors(B, dim, 2)[0]) * sign[:B]).astype(np.float32)  # same signs: products all > 0
+    qd = torch.as_tensor(q, device="cuda")
+    acts = np.zeros((n, 3, 7))
+    exact = q.astype(np.float64) @ keys.astype(np.float64).T
+    absum = np.abs(q.astype(np.float64)) @ np.abs(keys.astype(np.float64)).T
+    # bf16 filter copy of fp32 keys
+    col = H.Collection(dim, capacity=n)
+    col.insert(keys, acts)
+    col.set_filter("bf16_copy")
+    approx = col.debug_sim_scores(qd, variant=4).cpu().numpy().astype(np.float64)
+    rel = np.abs(approx - exact) / absum
+    assert rel[np.arange(B), np.arange(B)].min() > OLD_GAMMA_COPY(dim), rel.max()
+    assert np.all(rel <= GAMMA_COPY(dim)), rel.max()
+    sc, ids = col.search_topk_exact(qd, 8)
+    osc, oid = O.search_topk(keys, q, 8)
+    np.testing.assert_array_equal(ids.cpu().numpy(), oid)
+    np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+    # bf16 collection: the stored keys are exact, the query is rounded
+    colb = H.Collection(dim, capacity=n, dtype="bf16")
+    stored = torch.as_tensor(keys).bfloat16().float().numpy().astype(np.float64)
+    colb.insert(keys, acts)
+    approx = colb.debug_sim_scores(qd, variant=1).cpu().numpy().astype(np.float64)
+    ex_b = q.astype(np.float64) @ stored.T
+    ab_b = np.abs(q.astype(np.float64)) @ np.abs(stored).T
+    rel = np.abs(approx - ex_b) / ab_b
+    assert rel.max() > OLD_GAMMA_BF16(dim), rel.max()
+    assert np.all(rel <= gamma_wide(dim, True)), rel.max()
+    # TF32 over the fp32 keys (truncation), inside its own bound
+    col.set_filter("native")
+    approx = col.debug_sim_scores(qd, variant=1).cpu().numpy().astype(np.float64)
+    rel = np.abs(approx - exact) / absum
+    assert np.all(rel <= gamma_wide(dim, False)), rel.max()
+
+
+@pytest.mark.parametrize("path", ["auto", "tc_single"])
+def test_ragged_tail_and_range(torch, path):
+    """Row counts that are not multiples of the 128-key block, and sub-ranges."""
+    H.set_sim_path(path)
+    try:
+        n, dim = 1000 * 3 + 77, 128
+        col = H.Collection(dim, capacity=n)
+        col.generate(O.REAL, 9, n)
+        for B in (32, 200):
+            q = H.gen_queries(O.REAL, 10, 9, n, 0, B, dim)
+            for rng in ((0, n), (5, 133), (1000, 2999), (n - 1, n)):
+                sc, ids = col.search_topk_exact(q, 5, row_range=rng)
+                keys = O.gen_keys(O.REAL, 9, rng[0], rng[1] - rng[0], dim)
+                osc, oid = O.search_topk(keys, q.cpu().numpy(), 5)
+                kk = oid.shape[1]
+                np.testing.assert_array_equal(ids.cpu().numpy()[:, :kk], oid + rng[0])
+                np.testing.assert_array_equal(sc.cpu().numpy()[:, :kk], osc)
+    finally:
+        H.set_sim_path("auto")
 
 
 @pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
@@ -267,4 +281,3 @@ def test_edge_shapes_all_kernels(torch, dtype, filt):
                                                   err_msg=f"dim={dim} n={n} B={B} k={k} rg={rg}")
                     np.testing.assert_array_equal(sc.cpu().numpy()[:, :kk], osc)
                     assert np.all(ids.cpu().numpy()[:, kk:] == -1)
-            assert col.overflow_count() == 0
