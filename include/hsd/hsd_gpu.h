@@ -209,6 +209,34 @@ hsd_status hsd_verify_round_drafts(int device, const int32_t* ids, const uint8_t
                                    hsd_outcome* out, uint8_t* tokens, void* stream);
 
 /* ------------------------------------------------------------------------
+ * verify_tree with a real verifier: VerifierModel::verify_chain returns, per
+ * chain, greedy tokens TEACHER-FORCED on that chain (models.hpp:34-37), so
+ * every chain has its own greedy tokens.  Two calls:
+ *
+ * 1. hsd_enumerate_chains: the chains verify_tree visits (
+ *    unique token sequences "pos0 of candidate a + later groups
+ *    of candidate b" in DFS = lexicographic (a, b) order, at most `cap`).
+ *    Outputs (device): n_chains int32 [E]; chain_ab int16 [E][cap][2] (a, b);
+ *    chain_tokens uint8 [E][cap][L] — the inputs of the caller's verifier.
+ * 2. hsd_verify_round_chains: the verifier's output for those chains, either
+ *    chain_greedy uint8 [E][cap][L] (verify_chain's tokens) or chain_logits
+ *    fp32 [E][cap][L][256] (greedy = std::max_element over the bins), plus
+ *    greedy_ctx int32 [E] = greedy_next(context) (models.hpp:38-39), the token
+ *    emitted on fallback / for an empty shard.  Verify-skip as in
+ *    hsd_verify_round; one parameter set (its chain_cap must equal `cap`).
+ *    Outputs: out [E] and tokens [E][L] as hsd_verify_round.
+ * Candidates come from the collection's token table by id (c != NULL) or
+ * from pre-gathered drafts uint8 [E][k][32] (then `device` names the GPU). */
+hsd_status hsd_enumerate_chains(hsd_collection* c, int device, const int32_t* ids, const uint8_t* drafts, int E,
+                                int k, int L, int cap, int32_t* n_chains, int16_t* chain_ab, uint8_t* chain_tokens,
+                                void* stream);
+hsd_status hsd_verify_round_chains(hsd_collection* c, int device, const int32_t* ids, const uint8_t* drafts, int E,
+                                   int k, int L, int cap, const uint8_t* chain_greedy, const float* chain_logits,
+                                   const int32_t* greedy_ctx, const float* feat_now, const float* feat_prev, int d_f,
+                                   const int32_t* history, int gap_d, const hsd_verify_params* params,
+                                   hsd_outcome* out, uint8_t* tokens, void* stream);
+
+/* ------------------------------------------------------------------------
  * Kinematic fused metric — window_features + classify_segment + decide_sd
  * (kinematics.cpp:38-273) for W windows of w points.
  * ---------------------------------------------------------------------- */
@@ -231,6 +259,18 @@ typedef struct hsd_norm_bounds {
 hsd_status hsd_window_features(int device, const double* xyz, int W, const hsd_metric_params* params,
                                const hsd_norm_bounds* bounds, const int32_t* history, double* R, double* D, double* F,
                                int32_t* decision, void* stream);
+
+/* compute_percentile_bounds (kinematics.cpp:238-247): (min, nearest-rank
+ * 95th percentile) of n > 0 DEVICE fp64 samples, returned to the HOST.
+ * n < 1 or a non-finite sample -> HSD_ERR_INVALID_INPUT.  Synchronizes `stream`. */
+hsd_status hsd_percentile_bounds(int device, const double* samples, int64_t n, double* min_out, double* p95_out,
+                                 void* stream);
+/* NormalizationBounds of a task suite (the norm-bounds computation, SPEC.md:205,
+ * Appendix D): R and D of every window xyz fp64 [W][w][3] (device), then
+ * (r_min, r_max95) and (d_min, d_max95) with hsd_percentile_bounds.  HOST
+ * output.  Synchronizes `stream`. */
+hsd_status hsd_norm_bounds_from_windows(int device, const double* xyz, int W, const hsd_metric_params* params,
+                                        hsd_norm_bounds* out, void* stream);
 
 /* Same, plus the windowed finite-difference kinematics of each window in the
  * same pass: vaj fp64 [W][3] (may be NULL) = mean |velocity|, mean

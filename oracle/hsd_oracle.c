@@ -385,6 +385,58 @@ void hsdo_verify_round(const int* drafts, int n_cand, int L, const int* greedy, 
   free(bs);
 }
 
+/* verify_tree with teacher-forced per-chain verifier output
+ * (VerifierModel::verify_chain, models.hpp:34-37): chain c of the brute-force
+ * enumeration above is compared with its own greedy tokens
+ * chain_greedy[c][0..L); the fallback / empty-shard token is greedy_ctx =
+ * greedy_next(context) (models.hpp:38-39).  Otherwise as hsdo_verify_round. */
+void hsdo_verify_round_chains(const int* drafts, int n_cand, int L, const int* chain_greedy, int greedy_ctx, int skip,
+                              int cap, const hsdo_accept_params* p, hsdo_outcome* out) {
+  memset(out, 0, sizeof(*out));
+  if (n_cand <= 0) {
+    out->fallback = 1;
+    out->calls = 1;
+    out->n_emit = 1;
+    out->tokens[0] = greedy_ctx;
+    out->win_a = out->win_b = -1;
+    return;
+  }
+  if (skip) {
+    out->skipped = 1;
+    out->accept_len = L;
+    out->n_emit = L;
+    for (int t = 0; t < L; ++t) out->tokens[t] = drafts[t];
+    return;
+  }
+  int* chains = (int*)malloc(sizeof(int) * (size_t)cap * L);
+  int* as = (int*)malloc(sizeof(int) * (size_t)cap);
+  int* bs = (int*)malloc(sizeof(int) * (size_t)cap);
+  int n = hsdo_enumerate_chains(drafts, n_cand, L, cap, chains, as, bs);
+  int best = -1, best_len = -1;
+  for (int c = 0; c < n; ++c) {
+    int len = chain_prefix(chains + (size_t)c * L, L, chain_greedy + (size_t)c * L, p);
+    if (len > best_len) {
+      best_len = len;
+      best = c;
+    }
+  }
+  out->calls = n;
+  out->win_a = as[best];
+  out->win_b = bs[best];
+  out->accept_len = best_len;
+  if (best_len == 0) {
+    out->fallback = 1;
+    out->n_emit = 1;
+    out->tokens[0] = greedy_ctx;
+  } else {
+    out->n_emit = best_len;
+    for (int t = 0; t < best_len; ++t) out->tokens[t] = chains[(size_t)best * L + t];
+  }
+  free(chains);
+  free(as);
+  free(bs);
+}
+
 void hsdo_calibrate_init(hsdo_calib* c) {
   c->min_S = INFINITY;
   c->O_dist = 0;

@@ -117,6 +117,8 @@ void hsdo_verify_round(const int* drafts, int n_cand, int L, const int* greedy, 
                        const hsdo_accept_params* p, hsdo_outcome* out);
 
 /* Brute-force DFS enumerator used to pin the fast path above. */
+void hsdo_verify_round_chains(const int* drafts, int n_cand, int L, const int* chain_greedy /* cap x L */,
+                              int greedy_ctx, int skip, int cap, const hsdo_accept_params* p, hsdo_outcome* out);
 int hsdo_enumerate_chains(const int* drafts, int n_cand, int L, int cap, int* chains_out /* cap x L */,
                           int* a_out, int* b_out);
 

@@ -141,6 +141,8 @@ def lib():
         L.hsdo_verify_round.argtypes = [_i, C.c_int, C.c_int, _i, C.c_int, C.c_int, C.POINTER(AcceptParams),
                                         C.POINTER(Outcome)]
         L.hsdo_enumerate_chains.argtypes = [_i, C.c_int, C.c_int, C.c_int, _i, _i, _i]
+        L.hsdo_verify_round_chains.argtypes = [_i, C.c_int, C.c_int, _i, C.c_int, C.c_int, C.c_int,
+                                               C.POINTER(AcceptParams), C.POINTER(Outcome)]
         L.hsdo_calibrate_init.argtypes = [C.POINTER(Calib)]
         L.hsdo_calibrate_accumulate.argtypes = [C.POINTER(Calib), _d, C.c_int, C.c_double]
         L.hsdo_calibrate_finish.argtypes = [C.POINTER(Calib), C.POINTER(C.c_double), C.POINTER(C.c_int)]
@@ -340,6 +342,18 @@ def verify_round(drafts, greedy, skip=False, cap=64, enabled=True, seq_max=30, t
     out = Outcome()
     p = AcceptParams(int(enabled), seq_max, tok_max)
     lib().hsdo_verify_round(drafts, n_cand, L, greedy, int(skip), cap, C.byref(p), C.byref(out))
+    return out
+
+
+def verify_round_chains(drafts, chain_greedy, greedy_ctx, skip=False, cap=64, enabled=True, seq_max=30,
+                        tok_max=15) -> Outcome:
+    """verify_tree with per-chain (teacher-forced) greedy tokens chain_greedy [cap][L] (hsdo_verify_round_chains)."""
+    drafts = np.ascontiguousarray(np.atleast_2d(drafts), np.int32)
+    n_cand, L = drafts.shape if drafts.size else (0, np.asarray(chain_greedy).shape[-1])
+    cg = np.ascontiguousarray(np.asarray(chain_greedy).reshape(-1, L), np.int32)
+    out = Outcome()
+    p = AcceptParams(int(enabled), seq_max, tok_max)
+    lib().hsdo_verify_round_chains(drafts, n_cand, L, cg, int(greedy_ctx), int(skip), cap, C.byref(p), C.byref(out))
     return out
 
 

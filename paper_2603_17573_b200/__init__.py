@@ -185,6 +185,11 @@ def lib():
         "hsd_search_overflow_count": [_vp, _vp, C.POINTER(C.c_int)],
         "hsd_search_stats": [_vp, _vp, C.c_int, C.POINTER(C.c_int * 3)],
         "hsd_engine_stats": [_vp, C.c_int, C.POINTER(C.c_int * 3)],
+        "hsd_enumerate_chains": [_vp, C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
+        "hsd_verify_round_chains": [_vp, C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
+                                    _vp, C.c_int, _vp, C.c_int, C.POINTER(VerifyParams), _vp, _vp, _vp],
+        "hsd_percentile_bounds": [C.c_int, _vp, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double), _vp],
+        "hsd_norm_bounds_from_windows": [C.c_int, _vp, C.c_int, C.POINTER(MetricParams), C.POINTER(NormBounds), _vp],
         "hsd_verify_round": [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, _vp, C.c_int,
                              _vp, _vp, _vp],
         "hsd_window_features": [C.c_int, _vp, C.c_int, C.POINTER(MetricParams), C.POINTER(NormBounds), _vp, _vp, _vp,
@@ -473,6 +478,59 @@ def verify_round_drafts(ids, drafts, logits, params, feat_now=None, feat_prev=No
                                         _ptr(feat_now), _ptr(feat_prev), d_f, _ptr(history), gap_d,
                                         C.cast(arr, C.c_void_p), P, _ptr(out), _ptr(toks), _stream(stream)))
     return out.cpu().numpy().view(OUTCOME_DTYPE).reshape(P, E), toks
+
+
+def enumerate_chains(ids, L, cap=64, col=None, drafts=None, stream=None):
+    """The chains verify_tree visits (hsd_enumerate_chains): (n_chains int32 [E], chain_ab int16 [E, cap, 2],
+    chain_tokens uint8 [E, cap, L]) — what a real verifier is run on."""
+    torch = _torch()
+    ids = ids.contiguous()
+    E, k = ids.shape
+    dev = ids.device
+    n = torch.empty(E, dtype=torch.int32, device=dev)
+    ab = torch.empty((E, cap, 2), dtype=torch.int16, device=dev)
+    tok = torch.empty((E, cap, L), dtype=torch.uint8, device=dev)
+    check(lib().hsd_enumerate_chains(col.handle if col is not None else None, dev.index or 0, _ptr(ids), _ptr(drafts),
+                                     E, k, L, cap, _ptr(n), _ptr(ab), _ptr(tok), _stream(stream)))
+    return n, ab, tok
+
+
+def verify_round_chains(ids, params, greedy_ctx, chain_greedy=None, chain_logits=None, col=None, drafts=None,
+                        feat_now=None, feat_prev=None, history=None, gap_d=1, stream=None):
+    """verify_tree with per-chain teacher-forced verifier output (hsd_verify_round_chains): chain_greedy uint8
+    [E, cap, L] or chain_logits float32 [E, cap, L, 256]; greedy_ctx int32 [E].  Returns (outcomes [E], tokens)."""
+    torch = _torch()
+    ids = ids.contiguous()
+    E, k = ids.shape
+    src = chain_greedy if chain_greedy is not None else chain_logits
+    cap, L = src.shape[1], src.shape[2]
+    d_f = 0 if feat_now is None else feat_now.shape[1]
+    out = torch.empty((E, C.sizeof(Outcome)), dtype=torch.uint8, device=ids.device)
+    toks = torch.empty((E, L), dtype=torch.uint8, device=ids.device)
+    check(lib().hsd_verify_round_chains(col.handle if col is not None else None, ids.device.index or 0, _ptr(ids),
+                                        _ptr(drafts), E, k, L, cap, _ptr(chain_greedy), _ptr(chain_logits),
+                                        _ptr(greedy_ctx), _ptr(feat_now), _ptr(feat_prev), d_f, _ptr(history), gap_d,
+                                        C.byref(params), _ptr(out), _ptr(toks), _stream(stream)))
+    return out.cpu().numpy().view(OUTCOME_DTYPE).reshape(E), toks
+
+
+def percentile_bounds(samples, stream=None):
+    """compute_percentile_bounds (kinematics.cpp:238-247) of device fp64 samples -> (min, p95)."""
+    samples = samples.contiguous()
+    lo, hi = C.c_double(), C.c_double()
+    check(lib().hsd_percentile_bounds(samples.device.index or 0, _ptr(samples), samples.numel(), C.byref(lo),
+                                      C.byref(hi), _stream(stream)))
+    return lo.value, hi.value
+
+
+def norm_bounds_from_windows(xyz, params=None, stream=None) -> "NormBounds":
+    """NormalizationBounds of a suite from its windows xyz fp64 [W, w, 3] (hsd_norm_bounds_from_windows)."""
+    xyz = xyz.contiguous()
+    mp = params if params is not None else DEFAULT_METRIC
+    nb = NormBounds()
+    check(lib().hsd_norm_bounds_from_windows(xyz.device.index or 0, _ptr(xyz), xyz.shape[0], C.byref(mp),
+                                             C.byref(nb), _stream(stream)))
+    return nb
 
 
 class Comm:

@@ -693,6 +693,67 @@ hsd_status hsd_verify_round_drafts(int device, const int32_t* ids, const uint8_t
                      P, out, tokens, stream);
 }
 
+static hsd_status chains_common(hsd_collection* c, int* device, const int32_t* ids, const uint8_t* drafts, int E,
+                                int k, int L, int cap) {
+  if (c) *device = c->device;
+  if (L != 7 && L != 21) return fail(HSD_ERR_INVALID_INPUT, "draft length must be 7 or 21, got %d", L);
+  if (k < 1 || k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k must be in [1, %d]", HSD_K_MAX);
+  if (cap < 1 || cap > HSD_K_MAX * HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "chain cap must be in [1, 1024]");
+  if (E < 0) return fail(HSD_ERR_INVALID_INPUT, "negative episode count");
+  if (E > 0 && !ids) return fail(HSD_ERR_INVALID_INPUT, "null ids");
+  if (!c && !drafts) return fail(HSD_ERR_INVALID_INPUT, "need a collection or pre-gathered drafts");
+  return require_device(*device);
+}
+
+hsd_status hsd_enumerate_chains(hsd_collection* c, int device, const int32_t* ids, const uint8_t* drafts, int E,
+                                int k, int L, int cap, int32_t* n_chains, int16_t* chain_ab, uint8_t* chain_tokens,
+                                void* stream) {
+  hsd_status st = chains_common(c, &device, ids, drafts, E, k, L, cap);
+  if (st != HSD_OK || E == 0) return st;
+  if (!n_chains || !chain_ab || !chain_tokens) return fail(HSD_ERR_INVALID_INPUT, "null output");
+  CU(hsd::launch_enumerate_chains(ids, E, k, L, c ? c->tokens : nullptr, drafts, cap, n_chains, chain_ab,
+                                  chain_tokens, (cudaStream_t)stream));
+  return HSD_OK;
+}
+
+hsd_status hsd_verify_round_chains(hsd_collection* c, int device, const int32_t* ids, const uint8_t* drafts, int E,
+                                   int k, int L, int cap, const uint8_t* chain_greedy, const float* chain_logits,
+                                   const int32_t* greedy_ctx, const float* feat_now, const float* feat_prev, int d_f,
+                                   const int32_t* history, int gap_d, const hsd_verify_params* params,
+                                   hsd_outcome* out, uint8_t* tokens, void* stream) {
+  hsd_status st = chains_common(c, &device, ids, drafts, E, k, L, cap);
+  if (st != HSD_OK) return st;
+  st = check_verify_params(params, 1);
+  if (st != HSD_OK) return st;
+  if ((params->chain_cap > 0 ? params->chain_cap : 64) != cap)
+    return fail(HSD_ERR_CONFIG, "params.chain_cap (%d) must equal the enumeration cap (%d)", params->chain_cap, cap);
+  if (E == 0) return HSD_OK;
+  if (!!chain_greedy == !!chain_logits)
+    return fail(HSD_ERR_INVALID_INPUT, "pass exactly one of chain_greedy / chain_logits");
+  if (!greedy_ctx || !out || !tokens) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (params->skip_enabled && (!feat_now || !feat_prev || d_f < 4 || d_f % 4))
+    return fail(HSD_ERR_INVALID_INPUT, "verify-skip needs fp32 features with d_f a multiple of 4");
+  cudaStream_t s = (cudaStream_t)stream;
+  const hsd_verify_params* dp = nullptr;
+  st = device_params(device, params, 1, s, &dp);
+  if (st != HSD_OK) return st;
+  uint8_t* g = const_cast<uint8_t*>(chain_greedy);
+  if (chain_logits) {  // greedy tokens of every (episode, chain, position), stream-ordered scratch
+    const int64_t rows = (int64_t)E * cap * L;
+    CU(cudaMallocAsync((void**)&g, (size_t)rows, s));
+    cudaError_t e = hsd::launch_chain_argmax(chain_logits, rows, g, s);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(g, s);
+      return cuda_fail(e, "chain_argmax");
+    }
+  }
+  cudaError_t e = hsd::launch_verify_chains(ids, E, k, L, c ? c->tokens : nullptr, drafts, cap, g, greedy_ctx,
+                                            feat_now, feat_prev, d_f, history, gap_d, dp, out, tokens, s);
+  if (chain_logits) cudaFreeAsync(g, s);
+  CU(e);
+  return HSD_OK;
+}
+
 static hsd_status check_metric(const hsd_metric_params* mp, const hsd_norm_bounds* nb) {
   if (!mp || !nb) return fail(HSD_ERR_INVALID_INPUT, "null parameters");
   // FusedMetricParams::validate (kinematics.cpp:19-24)
@@ -733,6 +794,57 @@ hsd_status hsd_window_features_ex(int device, const double* xyz, int W, const hs
   st = require_device(device);
   if (st != HSD_OK) return st;
   CU(hsd::launch_kinematics(xyz, W, *params, *bounds, history, R, D, F, decision, (cudaStream_t)stream, vaj));
+  return HSD_OK;
+}
+
+hsd_status hsd_percentile_bounds(int device, const double* samples, int64_t n, double* min_out, double* p95_out,
+                                 void* stream) {
+  if (n < 1) return fail(HSD_ERR_INVALID_INPUT, "percentile of empty sample set");  // kinematics.cpp:239
+  if (!samples || !min_out || !p95_out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  hsd_status st = require_device(device);
+  if (st != HSD_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  void* buf = nullptr;  // [2] fp64 result + int non-finite count
+  CU(cudaMallocAsync(&buf, 24, s));
+  CU(cudaMemsetAsync((uint8_t*)buf + 16, 0, 4, s));
+  cudaError_t e = hsd::launch_percentile_bounds(samples, n, (double*)buf, (int*)((uint8_t*)buf + 16), s);
+  uint8_t host[24];
+  if (e == cudaSuccess) e = cudaMemcpyAsync(host, buf, 24, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(buf, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  CU(e);
+  int bad;
+  std::memcpy(&bad, host + 16, 4);
+  if (bad) return fail(HSD_ERR_INVALID_INPUT, "%d non-finite samples", bad);
+  std::memcpy(min_out, host, 8);
+  std::memcpy(p95_out, host + 8, 8);
+  return HSD_OK;
+}
+
+hsd_status hsd_norm_bounds_from_windows(int device, const double* xyz, int W, const hsd_metric_params* params,
+                                        hsd_norm_bounds* out, void* stream) {
+  if (!out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (W < 1) return fail(HSD_ERR_INVALID_INPUT, "percentile of empty sample set");
+  const hsd_norm_bounds unit{0.0, 1.0, 0.0, 1.0};
+  hsd_status st = check_metric(params, &unit);
+  if (st != HSD_OK) return st;
+  st = require_device(device);
+  if (st != HSD_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* rd = nullptr;  // R [W], D [W], F [W], decision [W]
+  CU(cudaMallocAsync((void**)&rd, (size_t)W * 32, s));
+  cudaError_t e = hsd::launch_kinematics(xyz, W, *params, unit, nullptr, rd, rd + W, rd + 2 * W,
+                                         (int32_t*)(rd + 3 * W), s);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(rd, s);
+    return cuda_fail(e, "kinematics");
+  }
+  hsd_norm_bounds b{};
+  st = hsd_percentile_bounds(device, rd, W, &b.r_min, &b.r_max95, stream);
+  if (st == HSD_OK) st = hsd_percentile_bounds(device, rd + W, W, &b.d_min, &b.d_max95, stream);
+  cudaFreeAsync(rd, s);
+  if (st != HSD_OK) return st;
+  *out = b;
   return HSD_OK;
 }
 

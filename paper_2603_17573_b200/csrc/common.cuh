@@ -121,6 +121,68 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
   e = __dadd_rn(__dsub_rn(a, av), __dsub_rn(b, bv));
 }
 
+// Greedy verifier token over 256 bins held 8 per lane (lane l: bins 8l..8l+7
+// in a, c): std::max_element's result (the reference's greedy rule, PAPER.md
+// Eq. 2-1), i.e. the sequential scan `if (v[b] > v[best]) best = b`: the
+// lowest index among equal maxima; a NaN is never selected after bin 0, and a
+// NaN in bin 0 is never replaced (every comparison with it is false).
+__device__ __forceinline__ int warp_argmax256(const float4& a, const float4& c, int lane) {
+  const float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+  constexpr int kNone = 0x7fffffff;
+  float best = -INFINITY;
+  int bi = kNone;  // no non-NaN value seen yet
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (v[i] > best || (bi == kNone && v[i] == v[i])) {
+      best = v[i];
+      bi = lane * 8 + i;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  const float v0 = __shfl_sync(0xffffffffu, a.x, 0);
+  return (v0 != v0 || bi == kNone) ? 0 : bi;
+}
+
+// should_skip's similarity over one warp: the double-double sum of the exact
+// fp64 products of two fp32 vectors (d % 4 == 0), i.e. the exact dot rounded
+// once (except within ~2^-100): the same bits as cos_kernel / K4.
+__device__ __forceinline__ double warp_dd_dot(const float* a, const float* b, int d, int lane) {
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  double hi = 0.0, lo = 0.0;
+  for (int t = lane; t < d / 4; t += 32) {
+    const float4 x = a4[t], y = b4[t];
+    const double pr[4] = {(double)x.x * (double)y.x, (double)x.y * (double)y.y, (double)x.z * (double)y.z,
+                          (double)x.w * (double)y.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double s, e;
+      two_sum(hi, pr[i], s, e);
+      hi = s;
+      lo = __dadd_rn(lo, e);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+    const double olo = __shfl_xor_sync(0xffffffffu, lo, o);
+    double s, e;
+    two_sum(hi, ohi, s, e);
+    hi = s;
+    lo = __dadd_rn(__dadd_rn(lo, olo), e);
+  }
+  double s, e;
+  two_sum(hi, lo, s, e);
+  return s;
+}
+
 // Order key of an exact fp64 score for (score desc) ranking with integer
 // compares: a larger score gives a smaller key; -0.0 and +0.0 share a key
 // (they compare equal, so the id decides, as with the reference's

@@ -92,24 +92,7 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
     }
 #pragma unroll
     for (int u = 0; u < 7; ++u) {
-      const float v[8] = {a[u].x, a[u].y, a[u].z, a[u].w, c[u].x, c[u].y, c[u].z, c[u].w};
-      float best = v[0];
-      int bi = lane * 8;
-#pragma unroll
-      for (int i = 1; i < 8; ++i)
-        if (v[i] > best) {
-          best = v[i];
-          bi = lane * 8 + i;
-        }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
+      const int bi = dev::warp_argmax256(a[u], c[u], lane);
       if (lane == 0) W.greedy[p0 + u] = bi;
     }
   }

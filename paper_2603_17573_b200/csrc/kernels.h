@@ -115,11 +115,25 @@ cudaError_t launch_cos(const float* feat_now, const float* feat_prev, int E, int
                        cudaStream_t s);
 cudaError_t launch_gather_tokens(const uint8_t* tokens, const int32_t* ids, int n, uint8_t* out, cudaStream_t s);
 
+// ---- verify_tree with per-chain (teacher-forced) verifier output (k_chains.cu)
+cudaError_t launch_chain_argmax(const float* logits, int64_t rows, uint8_t* greedy, cudaStream_t s);
+cudaError_t launch_enumerate_chains(const int32_t* ids, int E, int k, int L, const uint8_t* tokens,
+                                    const uint8_t* cand_tokens, int cap, int32_t* n_chains, int16_t* chain_ab,
+                                    uint8_t* chain_tokens, cudaStream_t s);
+cudaError_t launch_verify_chains(const int32_t* ids, int E, int k, int L, const uint8_t* tokens,
+                                 const uint8_t* cand_tokens, int cap, const uint8_t* chain_greedy,
+                                 const int32_t* greedy_ctx, const float* feat_now, const float* feat_prev, int d_f,
+                                 const int32_t* history, int gap_d, const hsd_verify_params* params_dev,
+                                 hsd_outcome* out, uint8_t* tok_out, cudaStream_t s);
+
 // ---- K5 kinematics -------------------------------------------------------------
 // vaj (optional) [W][3]: mean |velocity|, |acceleration|, |jerk| per step over the window
 cudaError_t launch_kinematics(const double* xyz, int W, const hsd_metric_params& mp, const hsd_norm_bounds& nb,
                               const int32_t* history, double* R, double* D, double* F, int32_t* decision,
                               cudaStream_t s, double* vaj = nullptr);
+
+// compute_percentile_bounds (k_bounds.cu): out2 (device) <- (min, p95); bad (device) += non-finite count
+cudaError_t launch_percentile_bounds(const double* samples, int64_t n, double* out2, int* bad, cudaStream_t s);
 
 // ---- verify-skip offline calibration (k_calib.cu) --------------------------------
 size_t calib_scratch_bytes(int n_traj, int max_tiles);
