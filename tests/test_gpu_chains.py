@@ -93,6 +93,10 @@ def test_verify_round_chains_parity(torch, L, k, variant, pset):
     n, _, chain_tok = H.enumerate_chains(t(torch, ids), L, cap=cap, drafts=t(torch, drafts))
     chain_tok = chain_tok.cpu().numpy()
     greedy = perturb(rng, chain_tok, L)  # [E][cap][L] (rows >= n_chains unused)
+    # every 3rd episode: the verifier departs from every chain after pos0 (partial prefixes)
+    g2 = greedy.astype(np.int64)
+    g2[::3, :, 3:6] = (g2[::3, :, 3:6] + 40 + rng.integers(0, 40, g2[::3, :, 3:6].shape)) % 256
+    greedy = g2.astype(np.uint8)
     g_ctx = rng.integers(0, 256, size=E).astype(np.int32)
     now, prev = O.gen_features(7, 0, E, d_f)
     hist = rng.integers(0, 6, size=E).astype(np.int32)
