@@ -15,7 +15,11 @@
 // for bit, what store.cpp:59-73 returns for the fp32-rounded embeddings and
 // query (the fp64 scores are the reference's sequential dot of the widened
 // values); inputs that are already fp32-representable (the usual case: model
-// activations) are therefore bit-identical end to end.  See INTEGRATION.md.
+// activations) are therefore bit-identical end to end.  Any dim >= 1 is
+// accepted: rows are zero-padded to a multiple of 8 on the device, and the
+// trailing fma(0, 0, s) steps leave the sequential sum's bits unchanged (s
+// starts at +0.0 and a sum of an +0.0 product never produces -0.0).  See
+// INTEGRATION.md.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -64,6 +68,11 @@ class DeviceBuffer {
   DeviceBuffer(const DeviceBuffer&) = delete;
   DeviceBuffer& operator=(const DeviceBuffer&) = delete;
   DeviceBuffer(DeviceBuffer&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)) {}
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    return *this;
+  }
   ~DeviceBuffer() { cudaFree(p_); }
   void resize(size_t n) {
     if (n <= n_) return;
@@ -95,18 +104,23 @@ class DeviceBuffer {
 class Collection {
  public:
   Collection() = default;
-  Collection(std::string name, int dim, int device = 0, int64_t capacity = 1024) : name_(std::move(name)), dim_(dim) {
+  Collection(std::string name, int dim, int device = 0, int64_t capacity = 1024)
+      : name_(std::move(name)), dim_(dim), pdim_((dim + 7) / 8 * 8) {
     if (dim < 1) throw ConfigError("collection dim must be >= 1");  // store.cpp:37
-    check(hsd_collection_create(device, dim, capacity, &h_));
+    check(hsd_collection_create(device, pdim_, capacity, &h_));
     device_ = device;
   }
   Collection(Collection&& o) noexcept { *this = std::move(o); }
   Collection& operator=(Collection&& o) noexcept {
     std::swap(name_, o.name_);
     std::swap(dim_, o.dim_);
+    std::swap(pdim_, o.pdim_);
     std::swap(device_, o.device_);
     std::swap(h_, o.h_);
     std::swap(records_, o.records_);
+    std::swap(q_, o.q_);
+    std::swap(s_, o.s_);
+    std::swap(i_, o.i_);
     return *this;
   }
   ~Collection() { hsd_collection_destroy(h_); }
@@ -137,24 +151,77 @@ class Collection {
   // Bulk insert; returns the id of the first record.
   int insert_batch(const std::vector<Record>& recs) {
     const int64_t n = (int64_t)recs.size();
-    std::vector<float> emb((size_t)n * dim_);
+    std::vector<float> emb((size_t)n * pdim_, 0.0f);
     std::vector<double> act((size_t)n * 21);
     std::vector<int32_t> ep((size_t)n), st((size_t)n);
+    int d_f = 0;
     for (int64_t i = 0; i < n; ++i) {
       const Record& r = recs[(size_t)i];
       if ((int)r.embedding.size() != dim_)
         throw SchemaError("embedding dim " + std::to_string(r.embedding.size()) + " does not match collection dim " +
                           std::to_string(dim_));
-      for (int c = 0; c < dim_; ++c) emb[(size_t)i * dim_ + c] = (float)r.embedding[(size_t)c];
+      for (int c = 0; c < dim_; ++c) emb[(size_t)i * pdim_ + c] = (float)r.embedding[(size_t)c];
       for (int s = 0; s < 3; ++s)
         for (int j = 0; j < 7; ++j) act[(size_t)i * 21 + s * 7 + j] = r.payload.next_actions[(size_t)s][(size_t)j];
       ep[(size_t)i] = r.payload.episode_idx;
       st[(size_t)i] = r.payload.step_idx;
+      if (r.feature && !d_f) d_f = (int)r.feature->size();
     }
     int64_t first = 0;
     check(hsd_collection_insert(h_, emb.data(), act.data(), ep.data(), st.data(), n, &first));
+    if (d_f) {  // Record::feature -> the device feature table (feeds calibrate_skip)
+      std::vector<float> f((size_t)n * d_f, 0.0f);
+      std::vector<uint8_t> has((size_t)n, 0);
+      for (int64_t i = 0; i < n; ++i) {
+        const auto& rf = recs[(size_t)i].feature;
+        if (!rf) continue;
+        if ((int)rf->size() != d_f) throw SchemaError("feature length differs from the collection's first feature");
+        for (int c = 0; c < d_f; ++c) f[(size_t)i * d_f + c] = (float)(*rf)[(size_t)c];
+        has[(size_t)i] = 1;
+      }
+      check(hsd_collection_set_features(h_, first, n, d_f, f.data(), has.data()));
+    }
     records_.insert(records_.end(), recs.begin(), recs.end());
     return (int)first;
+  }
+
+  // offline_calibrate_skip over the collection's own
+  // recorded features: a trajectory is a run of consecutive records with one
+  // episode_idx (records without a feature stand alone and add no pair).
+  // Returns (min_S, O_dist); CalibrationError when no pair exceeds T.
+  std::pair<double, int> calibrate_skip(double T) const {
+    const float* feat = nullptr;
+    int d_f = 0;
+    check(hsd_collection_features(h_, &feat, nullptr, &d_f));
+    if (!d_f) throw CalibrationError("no record carries a verifier feature");
+    std::vector<int64_t> off{0};
+    for (size_t i = 1; i < records_.size(); ++i)
+      if (records_[i].payload.episode_idx != records_[i - 1].payload.episode_idx || !records_[i].feature ||
+          !records_[i - 1].feature)
+        off.push_back((int64_t)i);
+    off.push_back((int64_t)records_.size());
+    double best = INFINITY;
+    int best_d = 0;
+    bool found = false;
+    for (size_t t0 = 0; t0 + 1 < off.size(); t0 += 65535) {  // hsd_calibrate_skip's batch limit
+      const size_t nt = std::min<size_t>(65535, off.size() - 1 - t0);
+      std::vector<int64_t> o(off.begin() + (long)t0, off.begin() + (long)(t0 + nt + 1));
+      const int64_t base = o.front();
+      for (auto& v : o) v -= base;
+      double m = 0.0;
+      int d = 0;
+      const hsd_status st =
+          hsd_calibrate_skip(device_, feat + (size_t)base * d_f, d_f, o.data(), (int)nt, T, &m, &d, nullptr);
+      if (st == HSD_ERR_CALIBRATION) continue;
+      check(st);
+      if (!found || m < best) {  // first strict minimum in trajectory order
+        best = m;
+        best_d = d;
+        found = true;
+      }
+    }
+    if (!found) throw CalibrationError("no feature pair exceeds the similarity boundary T");
+    return {best, best_d};
   }
 
   // Collection::search_topk_exact (store.cpp:59-73).
@@ -171,20 +238,20 @@ class Collection {
     const int B = (int)queries.size();
     std::vector<std::vector<SearchHit>> out((size_t)B);
     if (records_.empty() || B == 0) return out;  // empty collection -> empty result
-    std::vector<float> q((size_t)B * dim_);
+    std::vector<float> q((size_t)B * pdim_, 0.0f);
     for (int b = 0; b < B; ++b) {
       if ((int)queries[(size_t)b].size() != dim_) throw InvalidInputError("embedding dim mismatch in cosine");
-      for (int c = 0; c < dim_; ++c) q[(size_t)b * dim_ + c] = (float)queries[(size_t)b][(size_t)c];
+      for (int c = 0; c < dim_; ++c) q[(size_t)b * pdim_ + c] = (float)queries[(size_t)b][(size_t)c];
     }
-    DeviceBuffer<float> dq;
-    DeviceBuffer<double> ds((size_t)B * k);
-    DeviceBuffer<int32_t> di((size_t)B * k);
-    dq.upload(q.data(), q.size());
-    check(hsd_search_topk_exact(h_, dq.get(), B, k, ds.get(), di.get(), nullptr));
+    // device buffers persist across calls (grown on demand): no allocation per query
+    s_.resize((size_t)B * k);
+    i_.resize((size_t)B * k);
+    q_.upload(q.data(), q.size());
+    check(hsd_search_topk_exact(h_, q_.get(), B, k, s_.get(), i_.get(), nullptr));
     std::vector<double> sc((size_t)B * k);
     std::vector<int32_t> id((size_t)B * k);
-    ds.download(sc.data(), sc.size());
-    di.download(id.data(), id.size());
+    s_.download(sc.data(), sc.size());
+    i_.download(id.data(), id.size());
     for (int b = 0; b < B; ++b)
       for (int j = 0; j < k; ++j) {
         const int32_t r = id[(size_t)b * k + j];
@@ -197,9 +264,13 @@ class Collection {
  private:
   std::string name_;
   int dim_ = 0;
+  int pdim_ = 0;  // device row length: dim rounded up to 8 (zero padding)
   int device_ = 0;
   hsd_collection* h_ = nullptr;
   std::vector<Record> records_;
+  mutable DeviceBuffer<float> q_;
+  mutable DeviceBuffer<double> s_;
+  mutable DeviceBuffer<int32_t> i_;
 };
 
 // ---------------------------------------------------------------- kinematics

@@ -111,6 +111,16 @@ hsd_status hsd_collection_data(const hsd_collection* c, const void** keys, const
 hsd_status hsd_collection_insert(hsd_collection* c, const float* emb, const double* next_actions,
                                  const int32_t* episode_idx, const int32_t* step_idx, int64_t n, int64_t* first_id);
 
+/* Record::feature (store.hpp:40-42) of records [row0, row0 + n): fp32 HOST
+ * [n][d_f], has uint8 [n] (NULL = all present; absent rows stay zero).  The
+ * first call fixes d_f; another length -> HSD_ERR_SCHEMA.  Synchronous.  The
+ * device table feeds hsd_calibrate_skip (offline Alg. 1) directly. */
+hsd_status hsd_collection_set_features(hsd_collection* c, int64_t row0, int64_t n, int d_f, const float* feat,
+                                       const uint8_t* has);
+/* Device view of the feature table: fp32 [capacity][d_f], presence [capacity]
+ * (NULL / d_f = 0 when no record carries a feature). */
+hsd_status hsd_collection_features(const hsd_collection* c, const float** feat, const uint8_t** has, int* d_f);
+
 /* Append n counter-generated records (include/hsd/hsd_synth.h, family
  * `kind`) generated on the device; synchronous.  Record i of the collection
  * holds synthetic row i. */

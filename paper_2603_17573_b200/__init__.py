@@ -185,6 +185,8 @@ def lib():
         "hsd_search_overflow_count": [_vp, _vp, C.POINTER(C.c_int)],
         "hsd_search_stats": [_vp, _vp, C.c_int, C.POINTER(C.c_int * 3)],
         "hsd_engine_stats": [_vp, C.c_int, C.POINTER(C.c_int * 3)],
+        "hsd_collection_set_features": [_vp, C.c_int64, C.c_int64, C.c_int, _vp, _vp],
+        "hsd_collection_features": [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(C.c_int)],
         "hsd_enumerate_chains": [_vp, C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
         "hsd_verify_round_chains": [_vp, C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
                                     _vp, C.c_int, _vp, C.c_int, C.POINTER(VerifyParams), _vp, _vp, _vp],
@@ -428,6 +430,23 @@ class Collection:
     def overflow_count(self, stream=None) -> int:
         """Queries that needed the exact range fallback on `stream` (results are exact either way)."""
         return self.search_stats(stream)["fallback_queries"]
+
+    def set_features(self, features, has=None, row0=0) -> None:
+        """Record::feature of records [row0, row0 + n) (host fp32 [n, d_f]; has uint8 [n] or None = all)."""
+        f = np.ascontiguousarray(features, np.float32)
+        h = None if has is None else np.ascontiguousarray(has, np.uint8)
+        check(lib().hsd_collection_set_features(self._h, row0, f.shape[0], f.shape[1], f.ctypes.data_as(_vp),
+                                                None if h is None else h.ctypes.data_as(_vp)))
+
+    def features(self):
+        """(features float32 [size, d_f], has uint8 [size]) device views, or None when no record carries one."""
+        fp, hp, d = _vp(), _vp(), C.c_int()
+        check(lib().hsd_collection_features(self._h, C.byref(fp), C.byref(hp), C.byref(d)))
+        if not d.value:
+            return None
+        torch = _torch()
+        n, dev = self.size(), self.device
+        return (_from_ptr(fp.value, (n, d.value), torch.float32, dev), _from_ptr(hp.value, (n,), torch.uint8, dev))
 
     def search_stats(self, stream=None, reset=False) -> dict:
         """Accumulated search statistics of `stream` (hsd_search_stats; synchronizes)."""

@@ -128,6 +128,11 @@ struct hsd_collection {
   uint16_t* shadow = nullptr;
   uint8_t* tokens = nullptr;
   unsigned long long* maxnorm = nullptr;  // fp64 bits of max row norm
+  // Record::feature (store.hpp:40-42): verifier features captured at recording
+  // time, fp32 [cap][d_f] + presence [cap] (allocated on first use; d_f fixed)
+  float* feat = nullptr;
+  uint8_t* has_feat = nullptr;
+  int d_f = 0;
   std::mutex mu;
   std::unordered_map<cudaStream_t, Scratch> scratch;
 };
@@ -162,6 +167,28 @@ hsd_status ensure_capacity(hsd_collection* c, int64_t need) {
     if (c->n > 0) CU(cudaMemcpy(ns, c->shadow, (size_t)c->n * c->dim * 2, cudaMemcpyDeviceToDevice));
     cudaFree(c->shadow);
     c->shadow = ns;
+  }
+  if (c->feat) {
+    float* nf = nullptr;
+    uint8_t* nh = nullptr;
+    cudaError_t e2 = cudaMalloc(&nf, (size_t)ncap * c->d_f * 4);
+    if (e2 == cudaSuccess) e2 = cudaMalloc(&nh, (size_t)ncap);
+    if (e2 != cudaSuccess) {
+      cudaFree(nk);
+      cudaFree(nt);
+      cudaFree(nf);
+      return cuda_fail(e2, "cudaMalloc(features)");
+    }
+    CU(cudaMemset(nf, 0, (size_t)ncap * c->d_f * 4));
+    CU(cudaMemset(nh, 0, (size_t)ncap));
+    if (c->n > 0) {
+      CU(cudaMemcpy(nf, c->feat, (size_t)c->n * c->d_f * 4, cudaMemcpyDeviceToDevice));
+      CU(cudaMemcpy(nh, c->has_feat, (size_t)c->n, cudaMemcpyDeviceToDevice));
+    }
+    cudaFree(c->feat);
+    cudaFree(c->has_feat);
+    c->feat = nf;
+    c->has_feat = nh;
   }
   cudaFree(c->keys);
   cudaFree(c->tokens);
@@ -381,6 +408,8 @@ hsd_status hsd_collection_destroy(hsd_collection* c) {
   cudaFree(c->tokens);
   cudaFree(c->shadow);
   cudaFree(c->maxnorm);
+  cudaFree(c->feat);
+  cudaFree(c->has_feat);
   delete c;
   return HSD_OK;
 }
@@ -497,6 +526,41 @@ hsd_status hsd_collection_insert(hsd_collection* c, const float* emb, const doub
   if (st != HSD_OK) return st;
   CU(cudaDeviceSynchronize());
   c->n += n;
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_set_features(hsd_collection* c, int64_t row0, int64_t n, int d_f, const float* feat,
+                                       const uint8_t* has) {
+  if (!c) return fail(HSD_ERR_INVALID_INPUT, "null collection");
+  if (n < 0 || row0 < 0 || row0 + n > c->n) return fail(HSD_ERR_INVALID_INPUT, "feature rows outside the collection");
+  if (d_f < 1) return fail(HSD_ERR_INVALID_INPUT, "feature dim must be >= 1");
+  if (c->d_f && c->d_f != d_f)
+    return fail(HSD_ERR_SCHEMA, "feature length %d differs from the collection's first feature (%d)", d_f, c->d_f);
+  if (n > 0 && !feat) return fail(HSD_ERR_INVALID_INPUT, "null features");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  if (!c->feat) {
+    CU(cudaMalloc(&c->feat, (size_t)c->cap * d_f * 4));
+    CU(cudaMalloc(&c->has_feat, (size_t)c->cap));
+    CU(cudaMemset(c->feat, 0, (size_t)c->cap * d_f * 4));
+    CU(cudaMemset(c->has_feat, 0, (size_t)c->cap));
+    c->d_f = d_f;
+  }
+  if (n == 0) return HSD_OK;
+  CU(cudaMemcpy(c->feat + (size_t)row0 * d_f, feat, (size_t)n * d_f * 4, cudaMemcpyHostToDevice));
+  if (has) {
+    CU(cudaMemcpy(c->has_feat + row0, has, (size_t)n, cudaMemcpyHostToDevice));
+  } else {
+    CU(cudaMemset(c->has_feat + row0, 1, (size_t)n));
+  }
+  return HSD_OK;
+}
+
+hsd_status hsd_collection_features(const hsd_collection* c, const float** feat, const uint8_t** has, int* d_f) {
+  if (!c || !feat || !d_f) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *feat = c->feat;
+  if (has) *has = c->has_feat;
+  *d_f = c->d_f;
   return HSD_OK;
 }
 
@@ -1307,7 +1371,8 @@ struct hsd_comm {
   hsd::P2PWindows win{};
   bool p2p = false;
   uint64_t epoch = 0;
-  int* err = nullptr;
+  int* err = nullptr;    // device view of h_err (mapped pinned host memory)
+  int* h_err = nullptr;  // set by the merge when a peer never published
 };
 
 extern "C" {
@@ -1348,8 +1413,9 @@ hsd_status hsd_comm_destroy(hsd_comm* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   for (int g = 0; g < c->world && g < hsd::kMaxP2P; ++g)
     if (c->p2p && g != c->rank && c->win.base[g]) cudaIpcCloseMemHandle(c->win.base[g]);
-  void* ps[] = {c->gs, c->gi, c->ls, c->li, c->gt, c->lt, c->window, c->err};
+  void* ps[] = {c->gs, c->gi, c->ls, c->li, c->gt, c->lt, c->window};
   for (void* p : ps) cudaFree(p);
+  if (c->h_err) cudaFreeHost(c->h_err);
   delete c;
   return HSD_OK;
 }
@@ -1379,8 +1445,11 @@ hsd_status hsd_comm_p2p_export(hsd_comm* c, int max_B, int k_max, uint8_t handle
     const size_t bytes = hsd::p2p_window_bytes(c->world, max_B, k_max, &c->win);
     CU(cudaMalloc(&c->window, bytes));
     CU(cudaMemset(c->window, 0, bytes));  // flags start at epoch 0
-    CU(cudaMalloc(&c->err, sizeof(int)));
-    CU(cudaMemset(c->err, 0, sizeof(int)));
+    // the merge's timeout flag lives in mapped host memory: the next call reads
+    // it without synchronising and fails instead of returning empty results
+    CU(cudaHostAlloc((void**)&c->h_err, sizeof(int), cudaHostAllocMapped));
+    *(volatile int*)c->h_err = 0;
+    CU(cudaHostGetDevicePointer((void**)&c->err, c->h_err, 0));
     c->win.base[c->rank] = c->window;
   }
   cudaIpcMemHandle_t h;
@@ -1410,10 +1479,11 @@ hsd_status hsd_comm_p2p_import(hsd_comm* c, const uint8_t* handles) {
 hsd_status hsd_comm_p2p_status(hsd_comm* c, int* peer_timeout) {
   if (!c || !peer_timeout) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   *peer_timeout = 0;
-  if (!c->err) return HSD_OK;
+  if (!c->h_err) return HSD_OK;
   hsd_status st = require_device(c->device);
   if (st != HSD_OK) return st;
-  CU(cudaMemcpy(peer_timeout, c->err, sizeof(int), cudaMemcpyDeviceToHost));
+  CU(cudaDeviceSynchronize());
+  *peer_timeout = *(volatile int*)c->h_err;
   return HSD_OK;
 }
 
@@ -1453,6 +1523,9 @@ hsd_status hsd_search_topk_sharded(hsd_collection* col, hsd_comm* cm, int64_t id
     CU(cudaMalloc(&cm->lt, need * HSD_TOKENS_STRIDE));
     cm->cap = need;
   }
+  if (cm->p2p && cm->h_err && *(volatile int*)cm->h_err)  // a previous round's merge timed out
+    return fail(HSD_ERR_NCCL, "peer exchange: a peer never published its records (merge timed out); the "
+                              "communicator is unusable");
   if (cm->p2p) {  // local top-k whose K2 epilogue publishes into every peer's window, then the merge
     if (B > cm->win.Bmax || k > cm->win.kmax)
       return fail(HSD_ERR_INVALID_INPUT, "batch %d / k %d exceed the peer window (%d, %d)", B, k, cm->win.Bmax,

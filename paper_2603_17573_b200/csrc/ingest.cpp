@@ -497,6 +497,8 @@ hsd_status hsd_collection_from_jsonl(const hsd_jsonl_db* db, int device, int dty
   if (db->n == 0) return HSD_OK;
   int64_t first = 0;
   st = hsd_collection_insert(*out, db->emb.data(), db->next.data(), db->ep.data(), db->st.data(), db->n, &first);
+  if (st == HSD_OK && db->d_f)  // Record::feature rows (store.cpp:184-188) travel to the device too
+    st = hsd_collection_set_features(*out, 0, db->n, db->d_f, db->feat.data(), db->has_feat.data());
   if (st != HSD_OK) {
     hsd_collection_destroy(*out);
     *out = nullptr;

@@ -86,6 +86,88 @@ int main() {
   CHECK(empty.search_topk_exact(queries[0], 5).empty(), "empty collection -> empty result");
   CHECK(throws<hsd::ConfigError>([&] { hsd::gpu::Collection bad("b", 0); }), "dim 0 -> ConfigError");
 
+  // ---- any dim: rows zero-padded to a multiple of 8 on the device, scores unchanged bit for bit
+  for (int odd : {1, 3, 61, 130}) {
+    hsd::Collection r2("odd", odd);
+    std::mt19937_64 g((uint64_t)odd);
+    std::normal_distribution<float> Nf(0.0f, 1.0f);
+    for (int i = 0; i < 700; ++i) {
+      hsd::Embedding e((size_t)odd);
+      for (auto& v : e) v = (double)Nf(g);
+      hsd::Payload p;
+      p.episode_idx = i;
+      r2.insert(std::move(e), p);
+    }
+    auto g2 = hsd::gpu::Collection::from(r2, 0);
+    for (int t = 0; t < 5; ++t) {
+      hsd::Embedding qq((size_t)odd);
+      for (auto& v : qq) v = (double)Nf(g);
+      auto want = r2.search_topk_exact(qq, 9);
+      auto got = g2.search_topk_exact(qq, 9);
+      CHECK(got.size() == want.size(), "odd dim %d hit count", odd);
+      for (size_t i = 0; i < std::min(got.size(), want.size()); ++i) {
+        CHECK(got[i].record_id == want[i].record_id, "odd dim %d id rank=%zu", odd, i);
+        CHECK(std::memcmp(&got[i].score, &want[i].score, sizeof(double)) == 0, "odd dim %d score bits", odd);
+      }
+    }
+  }
+
+  // ---- Record::feature on the device -> offline calibration from the collection itself
+  {
+    const int df = 64, per_ep = 20, n_ep = 6;
+    hsd::gpu::Collection fc("feat", 16);
+    std::vector<hsd::Record> recs;
+    std::vector<float> fall;
+    std::mt19937_64 g(11);
+    std::normal_distribution<double> Nd(0.0, 1.0);
+    for (int e = 0; e < n_ep; ++e) {
+      std::vector<double> base((size_t)df);
+      for (auto& v : base) v = Nd(g);
+      for (int i = 0; i < per_ep; ++i) {
+        std::vector<double> f((size_t)df);
+        double nn = 0.0;
+        for (int c = 0; c < df; ++c) {
+          f[(size_t)c] = base[(size_t)c] + 0.02 * i * Nd(g);
+          nn += f[(size_t)c] * f[(size_t)c];
+        }
+        for (auto& v : f) v /= std::sqrt(nn);
+        for (double v : f) fall.push_back((float)v);
+        hsd::Payload p;
+        p.episode_idx = e;
+        p.step_idx = i;
+        recs.push_back({hsd::Embedding(16, 0.25), p, (e == 3 && i == 7) ? std::nullopt : std::optional(f)});
+      }
+    }
+    fc.insert_batch(recs);
+    const double T = 0.9;
+    auto got = fc.calibrate_skip(T);
+    // oracle: exactly rounded dots of the stored fp32 features, trajectories split at the featureless record
+    hsdo_calib cal;
+    hsdo_calibrate_init(&cal);
+    std::vector<std::pair<int, int>> runs;
+    for (int e = 0; e < n_ep; ++e) {
+      if (e == 3) {
+        runs.push_back({e * per_ep, e * per_ep + 7});
+        runs.push_back({e * per_ep + 8, (e + 1) * per_ep});
+      } else {
+        runs.push_back({e * per_ep, (e + 1) * per_ep});
+      }
+    }
+    for (auto [a, b] : runs) {
+      const int m = b - a;
+      std::vector<double> sims((size_t)m * m, 0.0);
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j)
+          sims[(size_t)i * m + j] = hsdo_feature_cos(&fall[(size_t)(a + i) * df], &fall[(size_t)(a + j) * df], df);
+      hsdo_calibrate_accumulate(&cal, sims.data(), m, T);
+    }
+    double mS = 0.0;
+    int od = 0;
+    CHECK(hsdo_calibrate_finish(&cal, &mS, &od) == 0, "oracle calibration");
+    CHECK(got.first == mS && got.second == od, "calibrate_skip %.17g/%d vs %.17g/%d", got.first, got.second, mS, od);
+    CHECK(throws<hsd::CalibrationError>([&] { fc.calibrate_skip(1.0); }), "T = 1 -> CalibrationError");
+  }
+
   // ---- quantize parity against the reference
   std::mt19937_64 rng(5);
   std::uniform_real_distribution<double> U(-1.4, 1.4);

@@ -74,3 +74,37 @@ def test_image_errors(torch, tmp_path):
         H.load_image(str(bad))
     with pytest.raises(H.IoError):
         H.load_image(str(tmp_path / "missing.img"))
+
+
+def test_jsonl_features_reach_the_device_and_calibrate(torch, tmp_path):
+    """Record::feature (store.hpp:40-42) travels with the records: the device feature table equals the file's
+    features (fp32), absent features stay zero, and offline Alg. 1 runs on it."""
+    rng = np.random.default_rng(6)
+    n, dim, d_f = 120, 16, 32
+    path = str(tmp_path / "f.jsonl")
+    feats = rng.standard_normal((n, d_f))
+    feats /= np.linalg.norm(feats, axis=1, keepdims=True)
+    with open(path, "w") as f:
+        f.write(json.dumps({"version": 1, "name": "t", "dim": dim, "metric": "cosine"}) + "\n")
+        for i in range(n):
+            rec = {"embedding": [float(x) for x in rng.standard_normal(dim)],
+                   "payload": {"dataset_name": "d", "episode_idx": i // 40, "step_idx": i % 40,
+                               "current_action": [0.0] * 7, "next_actions": [[0.0] * 7] * 3,
+                               "language_instruction": "x"},
+                   "feature": None if i == 5 else [float(x) for x in feats[i]]}
+            f.write(json.dumps(rec) + "\n")
+    col = H.load_jsonl(path)
+    fv = col.features()
+    assert fv is not None
+    ft, has = fv[0].cpu().numpy(), fv[1].cpu().numpy()
+    want = feats.astype(np.float32)
+    want[5] = 0
+    np.testing.assert_array_equal(ft, want)
+    assert has[5] == 0 and has.sum() == n - 1
+    off = np.array([0, 40, 80, 120], np.int64)
+    got = H.calibrate_skip(fv[0], off, T=-1.0)
+    sims = [np.array([[O.feature_cos(want[a + i], want[a + j]) for j in range(40)] for i in range(40)])
+            for a in (0, 40, 80)]
+    assert got == O.calibrate(sims, -1.0)
+    with pytest.raises(H.SchemaError):
+        col.set_features(np.zeros((1, d_f + 1), np.float32), row0=0)
