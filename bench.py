@@ -75,10 +75,11 @@ def parse():
                    help="use the sharded (NCCL all-gather + merge) step even at world size 1")
     p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                    help="row-sharded DB: top-k records exchanged through peer memory (default) or an NCCL all-gather")
-    p.add_argument("--shard", default="episodes", choices=["episodes", "db"],
-                   help="N > 1: 'episodes' = every rank holds the DB and runs its own batch of independent episodes "
-                        "(weak scaling, no collective on the data path); 'db' = the DB is row-sharded and every "
-                        "query searches all shards (local top-k + NCCL all-gather + merge, strong scaling)")
+    p.add_argument("--shard", default=None, choices=["episodes", "db"],
+                   help="N > 1: 'db' (default) = the DB is row-sharded and every query searches all shards (local "
+                        "top-k + exchange + merge, strong scaling: the north-star path); 'episodes' = every rank "
+                        "holds the DB and runs its own batch of independent episodes (weak scaling, no collective on "
+                        "the data path)")
     p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "bf16", "c5"])
     p.add_argument("--graph", action="store_true", help="replay each decode round from a captured CUDA graph")
     p.add_argument("--pipeline", type=int, default=0,
@@ -246,20 +247,44 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ CPU reference arm
-def cpu_reference_setup(args, n_sample):
-    """Reference Collection (store.cpp, compiled in place into oracle/_ref) holding
-    n_sample rows of the same synthetic DB, and the step inputs."""
+def mem_available_bytes():
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except Exception:
+        pass
+    return 0
+
+
+def cpu_rows(args):
+    """Rows the CPU arm's reference Collection holds: the whole DB when the host
+    can hold it (fp64 embeddings + payloads, ~33 GB at 1M x 4096, plus 8 GB of
+    headroom), else a 1/16 sample whose per-query time is scaled by N / rows
+    (reported as `extrapolation`; the search is linear in N, SURVEY §6 probe)."""
+    need = args.n * (args.dim * 8 + 512) * 1.1 + 8e9
+    if mem_available_bytes() >= need or args.n <= 20_000:
+        return args.n
+    return max(1000, min(args.n, args.n // 16, 62_500))
+
+
+def cpu_reference_setup(args, n_rows, threads):
+    """Reference Collection (store.cpp, compiled in place into oracle/_ref)
+    holding rows [0, n_rows) of the synthetic DB, and the episodes' inputs."""
     from oracle import oracle as O
 
     kind = "reference" if O.ref_available() else "port"
     q = O.gen_queries(args.kind, 7, 2026, args.n, 0, args.batch, args.dim)
     state = {"kind": kind, "q": q}
+    t0 = time.perf_counter()
     if kind == "reference":
         R = O.ref()
         col = R.hsdref_collection_new(args.dim)
-        rc = R.hsdref_insert_synth(col, args.kind, 2026, 0, n_sample, args.dim)
+        rc = R.hsdref_insert_synth_mt(col, args.kind, 2026, 0, n_rows, args.dim, threads)
         assert rc == 0, rc
         state["col"] = col
+    state["build_s"] = time.perf_counter() - t0
     from paper_2603_17573_b200 import synth
 
     rows = synth.query_rows(7, args.kind, args.n, 0, args.batch)
@@ -270,85 +295,83 @@ def cpu_reference_setup(args, n_sample):
     return state
 
 
-def cpu_reference_step(args, state, n_sample, threads):
-    """One pass of the reference CPU path over B episodes on an n_sample-row
-    sample of the DB: Collection::search_topk_exact per query (threads in
-    parallel, one query per thread), quantize of the hit payloads (inside the
-    reference call), then should_skip + verify_tree + window_features per
-    episode with the oracle port (spec-only / Eigen-dependent in the reference)."""
+def cpu_reference_step(args, state, n_rows, threads, eps):
+    """One round of the reference CPU path over the episodes `eps` (one per
+    host thread): Collection::search_topk_exact per query on the n_rows-row
+    Collection (one query per thread, SPEC.md:297 allows concurrent const
+    searches), quantize of the hit payloads (inside the reference call), then
+    should_skip + verify_tree + window_features per episode with the oracle
+    port (spec-only / Eigen-dependent in the reference)."""
     from oracle import oracle as O
 
+    q = state["q"][eps]
     if state["kind"] == "reference":
-        sc, ids, tok = O.ref_search(state["col"], state["q"], args.k, threads=threads)
+        sc, ids, tok = O.ref_search(state["col"], q, args.k, threads=threads)
         tok = tok.astype(np.int32)
     else:
-        sc, ids = O.search_synth(args.kind, 2026, n_sample, state["q"], args.k, threads=threads)
+        sc, ids = O.search_synth(args.kind, 2026, n_rows, q, args.k, threads=threads)
         tok = O.synth_tokens(2026, ids.ravel()).reshape(ids.shape[0], ids.shape[1], 21).astype(np.int32)
     now, prev = state["feat"]
     mp = O.MetricParams(0.5, 15, 0.5, 1.0)
     nb = O.NormBounds(0.000009, 0.123381, 0.000001, 0.014989)
     st = O.SkipState(0.9, 0.95, 5, 0.1, 0)
-    for e in range(args.batch):
+    for j, e in enumerate(eps):
         O.window_features(state["xyz"][e], mp, nb)
         greedy = np.array([O.argmax(state["logits"][e, p]) for p in range(args.L)], np.int32)
         skip = O.should_skip(O.feature_cos(now[e], prev[e]), st, 1, 1 << 30)
-        O.verify_round(tok[e, :, :args.L], greedy, skip=skip)
+        O.verify_round(tok[j, :, :args.L], greedy, skip=skip)
 
 
-def cpu_sample_rows(args):
-    """Rows of the DB sample the CPU arm searches: ~1-2 s of CPU work per pass
-    (1/16 of the 1M DB; capped so a 10M DB does not need 20 GB of host fp64;
-    config 1's 10k-row DB is searched whole)."""
-    if args.n <= 20_000:
-        return args.n
-    return max(1000, min(args.n, args.n // 16, 62_500))
-
-
-def cpu_baseline(args, seconds_budget=20.0, steps=None, warmup=0):
+def cpu_baseline(args, steps=2, warmup=0):
+    """The reference CPU path on the box's host cores.  A step is a round of
+    `threads` episodes (one query per thread over the whole DB when it fits in
+    host RAM); value = episodes / s.  Returns (cpu_baseline dict, per-round
+    seconds, extrapolation factor)."""
     threads = os.cpu_count() or 1
-    n_sample = cpu_sample_rows(args)
-    state = cpu_reference_setup(args, n_sample)
-    for _ in range(warmup):
-        cpu_reference_step(args, state, n_sample, threads)
+    n_rows = cpu_rows(args)
+    state = cpu_reference_setup(args, n_rows, threads)
+    T = min(threads, args.batch)
+    rounds = lambda i: [(i * T + j) % args.batch for j in range(T)]  # noqa: E731
+    for i in range(warmup):
+        cpu_reference_step(args, state, n_rows, threads, rounds(i))
     times = []
-    t_start = time.perf_counter()
-    while True:
+    for i in range(steps):
         t0 = time.perf_counter()
-        cpu_reference_step(args, state, n_sample, threads)
+        cpu_reference_step(args, state, n_rows, threads, rounds(warmup + i))
         times.append(time.perf_counter() - t0)
-        if steps is not None:
-            if len(times) >= steps:
-                break
-        elif time.perf_counter() - t_start > seconds_budget or len(times) >= 50:
-            break
     t = statistics.mean(times)
-    scale = args.n / n_sample  # search cost is linear in N (SURVEY.md §6 probe: 58 ms -> 674 ms -> 6.07 s)
-    value = args.batch / (t * scale)
+    scale = args.n / n_rows
+    value = T / (t * scale)
     if state["kind"] == "reference":
         from oracle import oracle as O
 
         O.ref().hsdref_collection_free(state["col"])
-    sample = (f"{args.batch} episodes/pass, search on an {n_sample}-row sample of the {args.n}-row DB "
-              f"(x{scale:.0f} linear extrapolation), {threads} threads, {len(times)} passes, "
-              f"{t:.3f} s/pass")
-    return {"value": value, "unit": "steps/s", "cores": threads, "kind": state["kind"], "sample": sample}, times
+    where = (f"the full {args.n}-row DB" if n_rows == args.n else
+             f"a {n_rows}-row sample of the {args.n}-row DB (per-query time x{scale:.0f}, linear in N)")
+    sample = (f"{len(times)} rounds of {T} episodes (one query per thread) searched on {where}, {threads} threads, "
+              f"{t:.2f} s/round; reference Collection built in {state['build_s']:.0f} s")
+    cb = {"value": value, "unit": "steps/s", "cores": threads, "kind": state["kind"], "sample": sample}
+    if n_rows != args.n:
+        cb["extrapolation"] = scale
+    return cb, times, scale, T
 
 
 def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    cb, times = cpu_baseline(args, steps=args.steps, warmup=args.warmup)
-    t = statistics.mean(times) * (args.n / cpu_sample_rows(args))
+    cb, times, scale, T = cpu_baseline(args, steps=args.steps, warmup=args.warmup)
     line = {
         "metric": metric_of(args), "value": cb["value"], "unit": "steps/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 * t, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": config_of(args, world),
-        "cpu_baseline": cb,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.mean(times), "episodes_per_step": T,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference", "config": config_of(args, world), "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    if scale != 1:
+        line["extrapolation"] = {"factor": scale, "note": "ms_per_step is the measured sample round; value scales "
+                                                          "the per-query time by N / sampled rows"}
     print(json.dumps(line), flush=True)
 
 
@@ -417,7 +440,10 @@ def run_ours(args):
     if world > 1:
         init_dist(dist, dev)
     B, k, L, d_f, dim = args.batch, args.k, args.L, args.d_f, args.dim
+    if args.shard is None:  # N > 1: the north-star path, a row-sharded DB
+        args.shard = "db"
     replicas = world > 1 and args.shard == "episodes" and not args.force_sharded
+    sharded = (world > 1 and not replicas) or args.force_sharded
     b0, b1 = (0, args.n) if replicas else H.shard_range(args.n, world, rank)
     col = H.Collection(dim, capacity=b1 - b0, device=local, dtype=args.dtype)
     col.generate(args.kind, 2026, b1 - b0, row0=b0)
@@ -437,9 +463,8 @@ def run_ours(args):
     e0_rank = rank * S * B if replicas else 0  # replicas: each rank runs its own episodes
     rows = [synth.query_rows(7, args.kind, args.n, e0_rank + s * B, B) for s in range(S)]
     qs = [H.gen_queries(args.kind, 7, 2026, args.n, e0_rank + s * B, B, dim, device=local) for s in range(S)]
-    # logits are generated from global rows; with a sharded DB use the token view of rank-local rows only when
-    # available: generate them on the host oracle-free path -> device generator needs the row's tokens, so we
-    # build them from a full-token collection of the rows we need (tokens are tiny).
+    # logits whose greedy tokens follow each query's source record (device generator; on a sharded DB the
+    # records of other shards fall back to random drafts)
     lg = [gen_logits_global(H, args, r, local, col, b0, b1) for r in rows]
     feats = [H.gen_features(5 + s, B, d_f, device=local) for s in range(S)]
     xyz_np = [synth.trajectory_windows(B, 15, seed=4 + s)[0] for s in range(S)]
@@ -447,19 +472,31 @@ def run_ours(args):
     hist = torch.full((B,), 100, dtype=torch.int32, device=dev)
     vp = H.VerifyParams.make(relaxed=True, bias_seq_max=30, bias_token_max=15, skip_enabled=True, min_S=0.95, O_dist=5)
 
-    post_steps = None
-    engs, strs = [], []
-    if (world == 1 or replicas) and not args.force_sharded:
-        # Steps are independent batches of episodes.  With `pipe` engines on
-        # `pipe` streams (steps alternating), step i+1's K1 streams the DB while
-        # step i's K2 / K4 finish: the small latency-bound kernels leave the
-        # HBM-bound K1 back to back.  Config 1 (L2 flushed around every step's
-        # event bracket) keeps one engine.
-        scanned = (b1 - b0) * dim * (2 if (args.dtype == "bf16" or args.filter == "bf16_copy") else 4)
-        pipe = args.pipeline if args.pipeline > 0 else (1 if scanned < 2 * 126e6 else 2)
-        args.pipe = pipe
+    # Steps are independent batches of episodes.  With `pipe` cohorts on `pipe`
+    # streams (steps alternating), step i+1's K1 streams the DB while step i's
+    # K2 / K4 finish: the small latency-bound kernels leave the HBM-bound K1
+    # back to back.  A DB that fits in L2 (config 1) keeps one cohort.
+    scanned = (b1 - b0) * dim * (2 if (args.dtype == "bf16" or args.filter == "bf16_copy") else 4)
+    pipe = args.pipeline if args.pipeline > 0 else (1 if scanned < 2 * 126e6 else 2)
+    args.pipe = pipe
+    strs = [stream] + [torch.cuda.Stream(device=dev) for _ in range(pipe - 1)]
+    ev_fork = torch.cuda.Event()
+
+    def fork(i):
+        if i == 0 and pipe > 1:  # the other streams start after everything before on the main stream
+            ev_fork.record(stream)
+            for t in strs[1:]:
+                t.wait_event(ev_fork)
+
+    def join():  # the main stream's next event covers every stream's steps
+        for t in strs[1:]:
+            e = torch.cuda.Event()
+            e.record(t)
+            stream.wait_event(e)
+
+    engs, comms, exchange = [], [], None
+    if not sharded:
         engs = [H.Engine(col, B, k, L, d_f, 15) for _ in range(pipe)]
-        strs = [stream] + [torch.cuda.Stream(device=dev) for _ in range(pipe - 1)]
 
         def mk_outs():
             return dict(scores=torch.empty((B, k), dtype=torch.float64, device=dev),
@@ -473,45 +510,28 @@ def run_ours(args):
         outs = [mk_outs() for _ in range(pipe)]
         bufs = [[H.StepBuffers(queries=qs[s], logits=lg[s], feat_now=feats[s][0], feat_prev=feats[s][1], xyz=xyz[s],
                                history=hist, **outs[j]) for s in range(S)] for j in range(pipe)]
-        ev_fork = torch.cuda.Event()
 
         def step(i):
+            fork(i)
             j = i % pipe
-            if i == 0 and pipe > 1:  # the other streams start after everything before on the main stream
-                ev_fork.record(stream)
-                for t in strs[1:]:
-                    t.wait_event(ev_fork)
             engs[j].step(B, bufs[j][i % S], vp, gap_d=1, stream=strs[j], graph=args.graph)
-
-        def join():  # the main stream's next event covers every stream's steps
-            for t in strs[1:]:
-                e = torch.cuda.Event()
-                e.record(t)
-                stream.wait_event(e)
-        post_steps = join if pipe > 1 else None
-        # K5 + skip similarity (side stream), query slab, K1, K2 (3 kernels), K4 — eager or as one graph's nodes
-        launches_per_step = 8
-        eng = engs[0]
+        # K5 + skip similarity (side stream), query slab, K1, K2 (4 kernels), K4 — eager or as one graph's nodes
+        launches_per_step = 9
     else:
-        comm = setup_comm(H, dist, world, rank, local, args.exchange, max_B=B, k_max=k)
-        lo, hi = H.shard_range(B, world, rank)  # this rank's episodes
-        sc = torch.empty((B, k), dtype=torch.float64, device=dev)
-        Bl = hi - lo
-        R = torch.empty(max(Bl, 1), dtype=torch.float64, device=dev)
-        D, F = torch.empty_like(R), torch.empty_like(R)
-        dec = torch.empty(max(Bl, 1), dtype=torch.int32, device=dev)
+        # one communicator (receive window / NCCL comm) per cohort: the cohorts' exchanges are independent
+        comms = [setup_comm(H, dist, world, rank, local, args.exchange, max_B=B, k_max=k) for _ in range(pipe)]
+        exchange = {"kind": "peer-memory (CUDA IPC windows, publish fused into K2)" if args.exchange == "p2p"
+                    else "NCCL all-gather", "ranks": comms[0].world, "communicators": pipe}
+        lo, hi = H.shard_range(B, world, rank)  # this rank verifies episodes [lo, hi)
+        sh = [ShardedCohort(H, torch, dev, B, k, L, lo, hi) for _ in range(pipe)]
 
         def step(i):
+            fork(i)
+            j = i % pipe
             s = i % S
-            if Bl > 0:
-                H.window_features(xyz[s][lo:hi], H.DEFAULT_METRIC, H.LIBERO_GOAL, history=hist[lo:hi], stream=stream)
-            _, ids, drafts = comm.search_topk(col, b0, qs[s], k, stream=stream)
-            if Bl > 0:
-                H.verify_round_drafts(ids[lo:hi].contiguous(), drafts[lo:hi].contiguous(), lg[s][lo:hi], vp,
-                                      feat_now=feats[s][0][lo:hi], feat_prev=feats[s][1][lo:hi], history=hist[lo:hi],
-                                      gap_d=1, stream=stream)
-        launches_per_step = 8
-        eng = None
+            sh[j].run(comms[j], col, b0, qs[s], lg[s], feats[s], xyz[s], hist, vp, strs[j])
+        launches_per_step = 10  # K5 (side stream), slab, K1, K2 (4 kernels, publish fused), merge, K4
+    post_steps = join if pipe > 1 else None
 
     def barrier():
         torch.cuda.synchronize()
@@ -521,18 +541,20 @@ def run_ours(args):
 
     for i in range(args.warmup):
         step(i)
+    if post_steps is not None:
+        post_steps()
     barrier()
     for en in engs:
         en.enable_timing(args.steps)
+        en.search_stats(reset=True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     # A DB that fits in L2 (config 1: 82 MB scanned per step) would stay cached
     # across steps: flush L2 between timed steps (a 512 MB write, outside the
     # per-step CUDA-event brackets) and sum the per-step device times.
-    scanned = (b1 - b0) * dim * (2 if (args.dtype == "bf16" or args.filter == "bf16_copy") else 4)
     flush = scanned < 2 * 126e6
+    l2buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
     if flush:
-        l2buf = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
@@ -554,57 +576,82 @@ def run_ours(args):
     ms_per_step = ms / args.steps
     value = (world if replicas else 1) * B * args.steps / (ms / 1e3)  # whole-job steps/s
 
-    stages = None
-    roof = None
-    if eng is not None and (args.graph or getattr(args, "pipe", 1) > 1):
-        # graph replays carry no stage events, and with steps in flight on several
-        # streams a stage's events also cover the wait for the other steps'
-        # kernels: time eager back-to-back steps of the same shape on one engine
-        eng.stage_times()
-        eng.enable_timing(min(args.steps, 50))
+    esz = 2 if (args.dtype == "bf16" or args.filter == "bf16_copy") else 4
+    passes = (B + 1023) // 1024  # up to 1024 queries share one key stream (cluster multicast)
+    alg_bytes = passes * (b1 - b0) * dim * esz + B * dim * 4
+    peak, peak_kind = load_peaks()
+    stages = roof = select = None
+    if engs:
+        # K1 inside the timed region: the similarity kernels' completion-to-completion
+        # interval (steps of all cohorts merged in issue order).  Graph replays carry
+        # no stage events; config 1 re-times eager steps with the L2 flushed.
+        k1_ms = None
+        if not args.graph:
+            marks = [en.stage_marks(engs[0]) for en in engs]
+            ends = sorted(m[1] for mk in marks for m in mk)
+            if len(ends) >= 2:
+                k1_ms = (ends[-1] - ends[0]) / (len(ends) - 1)
+        st_stats = engs[0].search_stats()
+        n_rec, st = engs[0].stage_times()
+        stages_timed = {kname: v / max(n_rec, 1) for kname, v in st.items()}
+        # isolated kernel times: eager back-to-back steps on one engine (L2 flushed first when it would hold the DB)
+        engs[0].enable_timing(min(args.steps, 50))
         for i in range(min(args.steps, 50)):
-            eng.step(B, bufs[0][i % S], vp, gap_d=1, stream=stream)
+            if flush:
+                l2buf.fill_(i & 0xFF)
+            engs[0].step(B, bufs[0][i % S], vp, gap_d=1, stream=stream)
         torch.cuda.synchronize()
-    if eng is not None:
-        n_rec, st = eng.stage_times()
+        n_rec, st = engs[0].stage_times()
         stages = {kname: v / max(n_rec, 1) for kname, v in st.items()}
-        sim_ms = stages["similarity"]
-        esz = 2 if (args.dtype == "bf16" or args.filter == "bf16_copy") else 4
-        passes = (B + 1023) // 1024  # up to 1024 queries share one key stream (cluster multicast)
-        alg_bytes = passes * (b1 - b0) * dim * esz + B * dim * 4
-        peak, peak_kind = load_peaks()
-        achieved = alg_bytes / (sim_ms / 1e3) / 1e9
+        if k1_ms is None:
+            k1_ms = stages["similarity"]
+            k1_src = "eager steps of the same shape" + (", L2 flushed before each" if flush else "")
+        else:
+            k1_src = "timed region: K1 completion-to-completion interval over the interleaved cohorts"
+        achieved = alg_bytes / (k1_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": load_traffic(traffic_key(args)),
                 "kernel": f"similarity (K1, {'kind::tf32' if esz == 4 else 'kind::f16'} filter"
-                          f"{' over the bf16 key copy' if args.filter == 'bf16_copy' else ''})",
-                "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": sim_ms, "peak_source": peak_kind,
-                "share_of_step": sim_ms / stages["total"]}
-        # tensor-pipe side of the same kernel (the filter's MMA work)
-        tflops = 2.0 * B * (b1 - b0) * dim / (sim_ms / 1e3) / 1e12
+                          f"{' over the bf16 key copy' if args.filter == 'bf16_copy' and esz == 2 else ''})",
+                "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": k1_ms, "avg_launch_source": k1_src,
+                "isolated_launch_ms": stages["similarity"], "peak_source": peak_kind,
+                "share_of_step": min(1.0, k1_ms / ms_per_step) if not flush else stages["similarity"] / stages["total"]}
+        tflops = 2.0 * B * (b1 - b0) * dim / (k1_ms / 1e3) / 1e12
         bf16_peak = load_peak_key("bf16_tflops")
         if bf16_peak:
             tpk = bf16_peak if esz == 2 else bf16_peak / 2.0
             roof["tensor"] = {"achieved_tflops": tflops, "peak_tflops": tpk, "frac": tflops / tpk,
                               "peak_source": "measured bf16" if esz == 2
                               else "measured bf16 / 2 (nominal TF32:BF16 dense ratio)"}
+        select = {"candidates_per_query": st_stats["candidates"] / max(1, B * args.steps),
+                  "fallback_queries": st_stats["fallback_queries"], "fallback_lists": st_stats["fallback_lists"],
+                  "select_ms": stages["select"], "timed_region_stage_ms": stages_timed}
+    else:
+        # sharded: per rank, the shard's algorithmic bytes over the whole step time (a lower bound on K1's rate)
+        achieved = alg_bytes / (ms_per_step / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "similarity (K1) of one shard; bytes per rank / step time (max over ranks)",
+                "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": ms_per_step,
+                "avg_launch_source": "timed region (whole step: an upper bound on K1's time)",
+                "peak_source": peak_kind, "per_rank": True}
 
-    # ---- e2e through the public host-buffer API (hsd_step_host_async)
+    # ---- e2e through the public host-buffer API
     e2e = None
-    if eng is not None:
+    if engs:
         e2e = run_e2e(H, torch, engs, args, qs, lg, feats, xyz_np, vp, strs)
-        if replicas:  # whole job: the slowest rank's rate x ranks
-            e2e["value"] = reduce_scalar(dist, torch, e2e["value"], "min") * world
-            e2e["note"] = "min over ranks x ranks (each rank its own episodes)"
+    else:
+        e2e = run_e2e_sharded(torch, dist, world, sh, comms, col, b0, args, qs, lg, feats, xyz_np, hist, vp, strs)
+    if replicas:  # whole job: the slowest rank's rate x ranks
+        e2e["value"] = reduce_scalar(dist, torch, e2e["value"], "min") * world
+        e2e["note"] = "min over ranks x ranks (each rank its own episodes)"
 
-    overflow = col.overflow_count(stream)
     recall = None
     if args.dtype == "bf16" and world == 1 and args.n <= 4_000_000:
         recall = bf16_recall(H, torch, args, col, qs, local)
     if rank == 0:
         cb = None
         if world == 1 and not args.no_cpu_baseline and not args.force_sharded:
-            cb, _ = cpu_baseline(args, seconds_budget=args.cpu_seconds)
+            cb, _, _, _ = cpu_baseline(args, steps=2)
         line = {
             "metric": metric_of(args), "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -612,14 +659,63 @@ def run_ours(args):
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (counter-generated DB/queries/logits/features)",
             "config": config_of(args, world), "pipeline": pipeline_of(args), "roofline": roof, "cpu_baseline": cb,
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "stages_ms": stages,
-            "search_overflow": overflow,
+            "select": select,
         }
+        if exchange is not None:
+            line["exchange"] = exchange
         if recall is not None:
             line["recall_at_k"] = recall
         print(json.dumps(line), flush=True)
+    for c in comms:
+        c.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+class ShardedCohort:
+    """One cohort's decode round on a row-sharded DB (preallocated buffers, no
+    host synchronisation): K5 for this rank's episodes on a side stream,
+    the sharded exact top-k (local K1 + K2 whose rank kernel publishes the
+    records into every peer's window, then the merge; or the NCCL all-gather
+    + merge), and K4 over the exchanged draft records of this rank's episodes."""
+
+    def __init__(self, H, torch, dev, B, k, L, lo, hi):
+        self.H, self.torch, self.lo, self.hi, self.k, self.L = H, torch, lo, hi, k, L
+        Bl = max(hi - lo, 1)
+        self.out = (torch.empty((B, k), dtype=torch.float64, device=dev),
+                    torch.empty((B, k), dtype=torch.int32, device=dev),
+                    torch.empty((B, k, H.TOKENS_STRIDE), dtype=torch.uint8, device=dev))
+        self.R = torch.empty(Bl, dtype=torch.float64, device=dev)
+        self.D, self.F = torch.empty_like(self.R), torch.empty_like(self.R)
+        self.dec = torch.empty(Bl, dtype=torch.int32, device=dev)
+        self.o = torch.empty((Bl, 20), dtype=torch.uint8, device=dev)
+        self.tok = torch.empty((Bl, L), dtype=torch.uint8, device=dev)
+        self.side = torch.cuda.Stream(device=dev)
+        self.fork_ev, self.join_ev = torch.cuda.Event(), torch.cuda.Event()
+        self.arr = (H.VerifyParams * 1)()
+
+    def run(self, comm, col, b0, q, lg, feat, xyz, hist, vp, stream):
+        H, lo, hi = self.H, self.lo, self.hi
+        lib, P = H.lib(), H._ptr
+        Bl = hi - lo
+        if Bl > 0:  # K5 beside the scan, on SMs the search leaves free
+            self.fork_ev.record(stream)
+            self.side.wait_event(self.fork_ev)
+            H.check(lib.hsd_window_features(xyz.device.index or 0, P(xyz[lo:hi]), Bl, H.C.byref(H.DEFAULT_METRIC),
+                                            H.C.byref(H.LIBERO_GOAL), P(hist[lo:hi]), P(self.R), P(self.D),
+                                            P(self.F), P(self.dec), H._stream(self.side)))
+            self.join_ev.record(self.side)
+        comm.search_topk(col, b0, q, self.k, stream=stream, out=self.out, reserve_sms=(Bl + 15) // 16 if Bl else 0)
+        if Bl > 0:
+            stream.wait_event(self.join_ev)
+            _, ids, drafts = self.out
+            self.arr[0] = vp
+            fn, fp = feat
+            H.check(lib.hsd_verify_round_drafts(ids.device.index or 0, P(ids[lo:hi]), P(drafts[lo:hi]), Bl, self.k,
+                                                self.L, P(lg[lo:hi]), P(fn[lo:hi]), P(fp[lo:hi]), fn.shape[1],
+                                                P(hist[lo:hi]), 1, H.C.cast(self.arr, H.C.c_void_p), 1, P(self.o),
+                                                P(self.tok), H._stream(stream)))
 
 
 def init_dist(dist, dev):
@@ -717,6 +813,62 @@ def run_e2e(H, torch, engs, args, qs, lg, feats, xyz_np, vp, strs):
             "api": f"hsd_step_host_async + hsd_engine_sync (C ABI), pinned host buffers, wall clock; "
                    f"{pipe} engine(s) on {pipe} stream(s), passes alternating",
             "passes": n, "sync_api_value": B * n / dt_sync}
+
+
+def run_e2e_sharded(torch, dist, world, sh, comms, col, b0, args, qs, lg, feats, xyz_np, hist, vp, strs):
+    """e2e of the row-sharded path through the public C ABI (hsd_window_features,
+    hsd_search_topk_sharded_ex, hsd_verify_round_drafts): every pass copies
+    its queries (all ranks search every query) and this rank's episodes'
+    logits / features / windows from pinned host memory, and reads the
+    outcomes and emitted tokens back; wall clock, max over ranks."""
+    B = args.batch
+    lo, hi = sh[0].lo, sh[0].hi
+    pipe = len(sh)
+    S = len(qs)
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    h_in = [dict(q=pin(qs[s]), lg=pin(lg[s][lo:hi]), fn=pin(feats[s][0][lo:hi]), fp=pin(feats[s][1][lo:hi]),
+                 xyz=torch.as_tensor(xyz_np[s][lo:hi]).pin_memory()) for s in range(S)]
+    d_in = [dict(q=torch.empty_like(qs[0]), lg=torch.empty_like(lg[0]), fn=torch.empty_like(feats[0][0]),
+                 fp=torch.empty_like(feats[0][1]), xyz=torch.empty_like(torch.as_tensor(xyz_np[0], device=qs[0].device)))
+            for _ in range(pipe)]
+    h_out = [dict(o=torch.empty_like(c.o, device="cpu").pin_memory(), tok=torch.empty_like(c.tok, device="cpu").pin_memory())
+             for c in sh]
+    h2d = sum(v.numel() * v.element_size() for v in h_in[0].values())
+    d2h = sum(v.numel() * v.element_size() for v in h_out[0].values()) if hi > lo else 0
+
+    def one(i):
+        j, s = i % pipe, i % S
+        st = strs[j]
+        with torch.cuda.stream(st):
+            d = d_in[j]
+            d["q"].copy_(h_in[s]["q"], non_blocking=True)
+            if hi > lo:
+                d["lg"][lo:hi].copy_(h_in[s]["lg"], non_blocking=True)
+                d["fn"][lo:hi].copy_(h_in[s]["fn"], non_blocking=True)
+                d["fp"][lo:hi].copy_(h_in[s]["fp"], non_blocking=True)
+                d["xyz"][lo:hi].copy_(h_in[s]["xyz"], non_blocking=True)
+            sh[j].run(comms[j], col, b0, d["q"], d["lg"], (d["fn"], d["fp"]), d["xyz"], hist, vp, st)
+            if hi > lo:
+                h_out[j]["o"].copy_(sh[j].o, non_blocking=True)
+                h_out[j]["tok"].copy_(sh[j].tok, non_blocking=True)
+
+    for i in range(2 * pipe):
+        one(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n = args.e2e_steps
+    t0 = time.perf_counter()
+    for i in range(n):
+        one(i)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        dt = reduce_scalar(dist, torch, dt, "max")
+    return {"value": B * n / dt, "unit": "steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "api": "hsd_window_features + hsd_search_topk_sharded_ex + hsd_verify_round_drafts (C ABI), pinned host "
+                   f"buffers, wall clock, max over ranks; {pipe} cohort(s) on {pipe} stream(s); bytes per rank",
+            "passes": n}
 
 
 def traffic_key(args):

@@ -341,6 +341,13 @@ hsd_status hsd_step_graph(hsd_engine* e, int B, const hsd_step_io* io, const hsd
  * over the recorded steps, then resets the recorder. */
 hsd_status hsd_engine_enable_timing(hsd_engine* e, int max_steps);
 hsd_status hsd_engine_stage_times(hsd_engine* e, int* n_steps, double ms[5]);
+/* Per recorded step of `e`: the times (ms) of its [start, after similarity,
+ * after select, end] events relative to the first recorded start event of
+ * `ref` (another engine on the same device, or e itself) — marks [n][4].
+ * With steps of several engines interleaved this gives the similarity
+ * kernel's completion-to-completion interval inside a timed region.  Call
+ * before hsd_engine_stage_times (which resets the recorder); synchronizes. */
+hsd_status hsd_engine_stage_marks(hsd_engine* e, const hsd_engine* ref, int max_n, double* marks, int* n);
 /* The engine's search statistics (as hsd_search_stats; the engine owns its
  * scratch).  Synchronizes the device. */
 hsd_status hsd_engine_stats(hsd_engine* e, int reset, int* stats3);
@@ -376,6 +383,11 @@ hsd_status hsd_shard_range(int64_t n_total, int world, int rank, int64_t* begin,
  * records' drafts travel with them, so verification needs no remote lookup). */
 hsd_status hsd_search_topk_sharded(hsd_collection* c, hsd_comm* comm, int64_t id_offset, const float* queries, int B,
                                    int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream);
+/* Same; reserve_sms SMs are left to work running concurrently on another
+ * stream (e.g. the kinematic metric of the rank's episodes). */
+hsd_status hsd_search_topk_sharded_ex(hsd_collection* c, hsd_comm* comm, int64_t id_offset, const float* queries,
+                                      int B, int k, double* scores, int32_t* ids, uint8_t* drafts, int reserve_sms,
+                                      void* stream);
 
 /* Peer-memory exchange instead of the NCCL all-gather: every rank exports the
  * CUDA IPC handle of its receive window (sized for up to max_B queries and

@@ -190,6 +190,7 @@ def ref():
         R.hsdref_collection_size.argtypes = [C.c_void_p]
         R.hsdref_insert.argtypes = [C.c_void_p, _f, _d, C.c_int64, C.c_int, C.c_int]
         R.hsdref_insert_synth.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_int]
+        R.hsdref_insert_synth_mt.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int]
         R.hsdref_search.argtypes = [C.c_void_p, _d, C.c_int, C.c_int, _d, _i, C.c_void_p]
         R.hsdref_search_batch.argtypes = [C.c_void_p, _f, C.c_int, C.c_int, C.c_int, C.c_int, _d, _i, C.c_void_p]
         R.hsdref_quantize.argtypes = [_d, _d, _d, C.c_int, _i]

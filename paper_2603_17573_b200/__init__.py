@@ -185,6 +185,7 @@ def lib():
         "hsd_search_overflow_count": [_vp, _vp, C.POINTER(C.c_int)],
         "hsd_search_stats": [_vp, _vp, C.c_int, C.POINTER(C.c_int * 3)],
         "hsd_engine_stats": [_vp, C.c_int, C.POINTER(C.c_int * 3)],
+        "hsd_engine_stage_marks": [_vp, _vp, C.c_int, _vp, C.POINTER(C.c_int)],
         "hsd_collection_set_features": [_vp, C.c_int64, C.c_int64, C.c_int, _vp, _vp],
         "hsd_collection_features": [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(C.c_int)],
         "hsd_enumerate_chains": [_vp, C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
@@ -221,6 +222,7 @@ def lib():
         "hsd_comm_p2p_status": [_vp, C.POINTER(C.c_int)],
         "hsd_shard_range": [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
         "hsd_search_topk_sharded": [_vp, _vp, C.c_int64, _vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
+        "hsd_search_topk_sharded_ex": [_vp, _vp, C.c_int64, _vp, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp],
         "hsd_verify_round_drafts": [C.c_int, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp,
                                     C.c_int, _vp, C.c_int, _vp, _vp, _vp],
         "hsd_collection_generate_rows": [_vp, C.c_int, C.c_uint64, C.c_int64, C.c_int64],
@@ -594,15 +596,18 @@ class Comm:
             lib().hsd_comm_destroy(self._h)
             self._h = C.c_void_p()
 
-    def search_topk(self, col: Collection, id_offset: int, queries, k: int, stream=None):
-        """Sharded search: local top-k + all-gather + merge -> (scores, ids, drafts [B, k, 32])."""
+    def search_topk(self, col: Collection, id_offset: int, queries, k: int, stream=None, out=None, reserve_sms=0):
+        """Sharded search: local top-k + exchange + merge -> (scores, ids, drafts [B, k, 32]); `out` = preallocated
+        (scores, ids, drafts); reserve_sms SMs are left to concurrent work on another stream."""
         torch = _torch()
         B = queries.shape[0]
-        scores = torch.empty((B, k), dtype=torch.float64, device=queries.device)
-        ids = torch.empty((B, k), dtype=torch.int32, device=queries.device)
-        drafts = torch.empty((B, k, TOKENS_STRIDE), dtype=torch.uint8, device=queries.device)
-        check(lib().hsd_search_topk_sharded(col.handle, self._h, id_offset, _ptr(queries), B, k, _ptr(scores),
-                                            _ptr(ids), _ptr(drafts), _stream(stream)))
+        if out is None:
+            out = (torch.empty((B, k), dtype=torch.float64, device=queries.device),
+                   torch.empty((B, k), dtype=torch.int32, device=queries.device),
+                   torch.empty((B, k, TOKENS_STRIDE), dtype=torch.uint8, device=queries.device))
+        scores, ids, drafts = out
+        check(lib().hsd_search_topk_sharded_ex(col.handle, self._h, id_offset, _ptr(queries), B, k, _ptr(scores),
+                                               _ptr(ids), _ptr(drafts), reserve_sms, _stream(stream)))
         return scores, ids, drafts
 
 
@@ -769,6 +774,7 @@ class Engine:
         self._h = C.c_void_p()
         check(lib().hsd_engine_create(col.handle, max_B, k, L, d_f, w, C.byref(self._h)))
         self.col, self.max_B, self.k, self.L, self.d_f, self.w = col, max_B, k, L, d_f, w
+        self._max_steps = 0
 
     def close(self):
         if self._h:
@@ -783,6 +789,15 @@ class Engine:
 
     def enable_timing(self, max_steps: int) -> None:
         check(lib().hsd_engine_enable_timing(self._h, max_steps))
+        self._max_steps = max_steps
+
+    def stage_marks(self, ref=None):
+        """[n, 4] event times (ms) of the recorded steps (start, after similarity, after select, end) relative to
+        the first recorded step of engine `ref` (default self)."""
+        m = np.zeros((max(self._max_steps, 1), 4), np.float64)
+        n = C.c_int()
+        check(lib().hsd_engine_stage_marks(self._h, (ref or self)._h, m.shape[0], m.ctypes.data_as(_vp), C.byref(n)))
+        return m[:n.value]
 
     def stage_times(self):
         """(steps, {stage: summed ms}) of the recorded steps (synchronizes)."""

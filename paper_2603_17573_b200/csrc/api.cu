@@ -1083,6 +1083,26 @@ hsd_status hsd_engine_stage_times(hsd_engine* e, int* n_steps, double* ms) {
   return HSD_OK;
 }
 
+hsd_status hsd_engine_stage_marks(hsd_engine* e, const hsd_engine* ref, int max_n, double* marks, int* n) {
+  if (!e || !ref || !marks || !n) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (ref->recorded < 1) return fail(HSD_ERR_INVALID_INPUT, "reference engine has no recorded step");
+  hsd_status st = require_device(e->c->device);
+  if (st != HSD_OK) return st;
+  const int m = std::min(max_n, e->recorded);
+  cudaEvent_t r0 = ref->ev[0];
+  for (int s = 0; s < m; ++s) {
+    const cudaEvent_t* v = &e->ev[(size_t)s * kStepEvents];
+    CU(cudaEventSynchronize(v[3]));
+    for (int j = 0; j < 4; ++j) {
+      float t = 0.f;
+      CU(cudaEventElapsedTime(&t, r0, v[j]));
+      marks[(size_t)s * 4 + j] = t;
+    }
+  }
+  *n = m;
+  return HSD_OK;
+}
+
 hsd_status hsd_engine_destroy(hsd_engine* e) {
   if (!e) return HSD_OK;
   cudaSetDevice(e->c->device);
@@ -1498,6 +1518,12 @@ hsd_status hsd_shard_range(int64_t n_total, int world, int rank, int64_t* begin,
 
 hsd_status hsd_search_topk_sharded(hsd_collection* col, hsd_comm* cm, int64_t id_offset, const float* queries, int B,
                                    int k, double* scores, int32_t* ids, uint8_t* drafts, void* stream) {
+  return hsd_search_topk_sharded_ex(col, cm, id_offset, queries, B, k, scores, ids, drafts, 0, stream);
+}
+
+hsd_status hsd_search_topk_sharded_ex(hsd_collection* col, hsd_comm* cm, int64_t id_offset, const float* queries,
+                                      int B, int k, double* scores, int32_t* ids, uint8_t* drafts, int reserve_sms,
+                                      void* stream) {
   if (!col || !cm) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   if (k < 1 || k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k must be in [1, %d]", HSD_K_MAX);
   if (B <= 0) return B == 0 ? HSD_OK : fail(HSD_ERR_INVALID_INPUT, "negative batch");
@@ -1538,13 +1564,13 @@ hsd_status hsd_search_topk_sharded(hsd_collection* col, hsd_comm* cm, int64_t id
     pub.epoch = cm->epoch;
     pub.id_offset = id_offset;
     pub.tokens = col->tokens;
-    st = search_impl(col, queries, B, k, 0, col->n, cm->ls, cm->li, s, nullptr, 0, &pub);
+    st = search_impl(col, queries, B, k, 0, col->n, cm->ls, cm->li, s, nullptr, reserve_sms, &pub);
     if (st != HSD_OK) return st;
     CU(hsd::launch_p2p_merge(cm->win, cm->rank, cm->world, B, k, cm->epoch, scores, ids, drafts, cm->err, s));
     return HSD_OK;
   }
   // local top-k over this rank's shard (K1 + K2), then the 32-B draft record
-  st = search_impl(col, queries, B, k, 0, col->n, cm->ls, cm->li, s);
+  st = search_impl(col, queries, B, k, 0, col->n, cm->ls, cm->li, s, nullptr, reserve_sms);
   if (st != HSD_OK) return st;
   CU(hsd::launch_gather_tokens(col->tokens, cm->li, (int)need, cm->lt, s));
   offset_ids_kernel<<<(int)((need + 255) / 256), 256, 0, s>>>(cm->li, (int)need, id_offset);
