@@ -166,8 +166,12 @@ hsd_status hsd_search_overflow_count(hsd_collection* c, void* stream, int* count
  * rescoring relies on. */
 hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
                                 void* stream);
-/* Ablation switch, process-wide: 0 auto (CTA-pair kernels above 128 queries),
- * 1 single-CTA wide kernels only (also HSD_WIDE_PAIR=0). */
+/* Search path switch, process-wide: 0 auto (exact scan of every row when the
+ * cost model prefers it — small rows x batch, B <= 4 — else the tensor-core
+ * filter + exact rescoring, CTA-pair kernels above 128 queries), 1 filter with
+ * single-CTA wide kernels only (also HSD_WIDE_PAIR=0), 2 filter + rescoring
+ * only, 3 exact scan wherever it applies (B <= 4, k <= 32).  Every path
+ * returns the same bits. */
 hsd_status hsd_set_sim_path(int path);
 
 /* ------------------------------------------------------------------------

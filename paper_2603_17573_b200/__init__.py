@@ -689,12 +689,13 @@ def quantize(actions, lo=-1.0, hi=1.0, k_bins=256, stream=None):
     return bins
 
 
-SIM_PATHS = {"auto": 0, "tc_single": 1}
+SIM_PATHS = {"auto": 0, "tc_single": 1, "filter": 2, "scan": 3}
 
 
 def set_sim_path(name: str) -> None:
-    """Filter kernel ablation switch: auto (CTA-pair kernels above 128 queries) | tc_single (single-CTA wide
-    kernels only)."""
+    """Search path switch: auto (cost model: exact scan of every row for small rows x batch, else the
+    tensor-core filter + exact rescoring, CTA pairs above 128 queries) | tc_single (filter, single-CTA wide
+    kernels only) | filter (filter + rescoring only) | scan (exact scan wherever it applies: B <= 4, k <= 32)."""
     check(lib().hsd_set_sim_path(SIM_PATHS[name]))
 
 

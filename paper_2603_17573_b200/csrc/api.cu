@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -78,6 +79,8 @@ hsd_status require_device(int device) {
   return HSD_OK;
 }
 
+constexpr int kMaxSms = 256;  // sizing bound of per-SM scratch
+
 int num_sms(int device) {
   static int cache[64] = {0};
   if (device >= 0 && device < 64 && cache[device]) return cache[device];
@@ -110,6 +113,7 @@ struct Scratch {
   void* qslab = nullptr;   // K1's padded query slab (TMA source)
   size_t qslab_cap = 0;
   int* stats = nullptr;    // [0] fallback queries, [1] pooled candidates, [2] fallback lists (accumulated)
+  void* scan = nullptr;    // K1x exact scan: ticket + per-CTA lists (zeroed once; the ticket self-resets)
   bool fixed = false;      // engine-owned: never reallocated (captured graphs hold its pointers)
 };
 
@@ -232,6 +236,11 @@ hsd_status alloc_scratch(Scratch& sc, size_t partial_bytes, size_t sel_bytes, si
     CU(cudaMalloc(&sc.stats, 4 * sizeof(int)));
     CU(cudaMemset(sc.stats, 0, 4 * sizeof(int)));
   }
+  if (!sc.scan) {
+    const size_t b = hsd::exact_scan_scratch_bytes(hsd::kScanMaxBatch, kMaxSms);
+    CU(cudaMalloc(&sc.scan, b));
+    CU(cudaMemset(sc.scan, 0, b));
+  }
   auto grow = [&](void** p, size_t* cap, size_t need) -> cudaError_t {
     if (*cap >= need) return cudaSuccess;
     cudaFree(*p);  // implicit device synchronisation: no kernel still reads the old buffer
@@ -252,6 +261,7 @@ void free_scratch(Scratch& sc) {
   cudaFree(sc.sel);
   cudaFree(sc.qslab);
   cudaFree(sc.stats);
+  cudaFree(sc.scan);
   sc = Scratch{};
 }
 
@@ -270,6 +280,24 @@ struct StageMarks {
   cudaEvent_t after_sim = nullptr;
   cudaEvent_t after_select = nullptr;
 };
+
+// Search path override (hsd_set_sim_path): 0 auto, 1 single-CTA wide
+// kernels, 2 filter + rescoring only, 3 exact scan wherever it applies.
+std::atomic<int> g_search_path{0};
+
+// K1x (exact scan of every row) or K1 + K2 (filter + exact rescoring): the
+// cheaper by the measured cost model.  The filter streams the
+// bf16 copy (or the stored keys), then pays K2's chain after the scan; the
+// exact scan streams the stored keys with the chains running underneath.
+bool use_exact_scan(const hsd_collection* c, int B, int k, int64_t rows) {
+  const int mode = g_search_path.load();
+  if (mode == 1 || mode == 2) return false;
+  if (!hsd::exact_scan_supported(B, c->dim, c->dtype, k)) return false;
+  if (mode == 3) return true;
+  const double fbytes = (double)rows * c->dim * (c->shadow ? 2 : (int)key_bytes(c));
+  const double filter_us = fbytes / 6.5e6 + 12.0 + c->dim * 0.0095;
+  return hsd::exact_scan_cost_us(rows, c->dim, c->dtype, B) < filter_us;
+}
 
 constexpr int kShadowGamma = 0x100;  // sim_wide_gamma flag: bf16-rounded keys (filter shadow)
 
@@ -320,6 +348,14 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   const int fdtype = c->shadow ? HSD_DTYPE_BF16 : c->dtype;
   const double gamma = c->shadow ? hsd::sim_wide_gamma(c->dim, HSD_DTYPE_BF16 | kShadowGamma)
                                  : hsd::sim_wide_gamma(c->dim, c->dtype);
+  if (!pub && use_exact_scan(c, B, k, rows)) {
+    // K1x: every row's exact chain while the keys stream (small rows x batch)
+    CU(hsd::launch_exact_scan(c->keys, c->dtype, c->n, rb, re, c->dim, queries, B, k, sc->scan,
+                              std::min(nsm, kMaxSms), scores, ids, s));
+    if (marks && marks->after_sim) CU(cudaEventRecord(marks->after_sim, s));
+    if (marks && marks->after_select) CU(cudaEventRecord(marks->after_select, s));
+    return HSD_OK;
+  }
   const int W = hsd::kMaxBatchPass;
   for (int b0 = 0; b0 < B; b0 += W) {
     const int Bs = std::min(W, B - b0);
@@ -610,9 +646,12 @@ hsd_status hsd_search_topk_range(hsd_collection* c, const float* queries, int B,
 }
 
 hsd_status hsd_set_sim_path(int path) {
-  if (path != 0 && path != 1)
-    return fail(HSD_ERR_INVALID_INPUT, "path must be 0 (auto) or 1 (single-CTA wide kernels, no CTA pairs)");
+  if (path < 0 || path > 3)
+    return fail(HSD_ERR_INVALID_INPUT,
+                "path must be 0 (auto), 1 (single-CTA wide kernels, no CTA pairs), 2 (filter + rescoring only) "
+                "or 3 (exact scan wherever it applies)");
   hsd::sim_wide_set_single(path == 1);
+  g_search_path.store(path);
   return HSD_OK;
 }
 

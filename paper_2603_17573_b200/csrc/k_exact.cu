@@ -1,0 +1,557 @@
+// k_exact.cu — K1x exact scan: every row scored with the reference's own
+// arithmetic, for searches whose (rows x queries) is small.
+//
+// Collection::search_topk_exact (store.cpp:59-73) scores every record with
+// cosine_similarity (store.cpp:29-34): s += a[i] * b[i] sequentially in fp64,
+// then orders by (score desc, id asc) and keeps k.  The default path (K1
+// tensor-core filter + K2 exact rescoring of the candidates) pays K2's
+// dim-step dependent fp64 chain AFTER the filter's scan.  For a small DB at
+// batch 1..4 (config 1: 10k rows x 4096, one query) streaming the fp32 keys
+// once costs about as much as that one chain, so this kernel runs the chain of
+// EVERY row while the keys stream in, and the filter, the candidate pooling
+// and the rescoring all disappear:
+//
+//   * one thread per row (lanes 0..lpw-1 of 4 compute warps, a tile of
+//     R = 4 lpw rows per CTA, persistent over tiles), each running NQ <= 4
+//     independent chains (one per query: NQ-way ILP on the DFMA latency);
+//   * warp 4 streams the tile's 128-B row segments (32 fp32 or 64 bf16
+//     columns) by TMA into an S-stage SWIZZLE_128B ring; a thread's 16-B
+//     shared loads of its own row hit 8 distinct bank groups per 8 rows
+//     (conflict-free);
+//   * the queries are widened to fp64 once per CTA into shared memory
+//     (zero-padded to the chunk width: fma(0, 0, s) == s, and s is never
+//     -0.0 since the chain starts at +0.0);
+//   * acc = fma(q_i, k_i, acc), i ascending: the fp32 (or bf16) x fp32
+//     product is exact in fp64, so this is bit-identical to s += a[i]*b[i];
+//   * each warp keeps a sorted (order key, id) top-k per query in registers
+//     (bitonic sort + merge; a batch that cannot enter is rejected with one
+//     ballot), the CTA's 4 warp lists merge in shared memory, and the last
+//     CTA to finish (ticket) merges the CTAs' lists into the final top-k.
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace hsd {
+namespace {
+
+using dev::kEmpty;
+using namespace sm100;
+
+// compute warps: one per scheduler.  (Two per scheduler with half the rows
+// each measured 16% slower at config 1: the per-step instruction stream is
+// issued per warp, so it doubles, while a chain's latency stays.)
+__host__ __device__ constexpr int compute_warps(int) { return 4; }
+constexpr uint32_t kNoId = 0xFFFFFFFFu;
+constexpr int kSmemBudget = 225 * 1024;
+
+// (order key, id): ascending = the reference's (score desc, id asc).
+__device__ __forceinline__ bool lt(uint64_t ak, uint32_t ai, uint64_t bk, uint32_t bi) {
+  return ak < bk || (ak == bk && ai < bi);
+}
+
+// Bitonic sort of 32 (key, id) pairs, one per lane, ascending.
+__device__ __forceinline__ void warp_sort_ki(uint64_t& k, uint32_t& i) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint64_t ok = dev::shfl_xor_u64(k, stride);
+      const uint32_t oi = __shfl_xor_sync(0xffffffffu, i, stride);
+      const bool asc = (lane & size) == 0 || size == 32;
+      const bool lower = (lane & stride) == 0;
+      const bool other_less = lt(ok, oi, k, i);
+      // ascending region: the lower lane keeps the smaller element
+      if ((lower == asc) ? other_less : !other_less) {
+        k = ok;
+        i = oi;
+      }
+    }
+  }
+}
+
+// Merge a sorted-ascending batch (b) into the sorted list (l): keeps the 32
+// smallest of the union, sorted.
+__device__ __forceinline__ void warp_merge_ki(uint64_t& lk, uint32_t& li, uint64_t bk, uint32_t bi) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t rk = dev::shfl_u64(bk, 31 - lane);
+  const uint32_t ri = __shfl_sync(0xffffffffu, bi, 31 - lane);
+  if (lt(rk, ri, lk, li)) {
+    lk = rk;
+    li = ri;
+  }
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) {
+    const uint64_t ok = dev::shfl_xor_u64(lk, stride);
+    const uint32_t oi = __shfl_xor_sync(0xffffffffu, li, stride);
+    const bool lower = (lane & stride) == 0;
+    const bool other_less = lt(ok, oi, lk, li);
+    if (lower ? other_less : !other_less) {
+      lk = ok;
+      li = oi;
+    }
+  }
+}
+
+// Offer one unsorted batch (one entry per lane) to the warp's top-k list.
+__device__ __forceinline__ void warp_offer(uint64_t& lk, uint32_t& li, uint64_t ck, uint32_t ci, int k) {
+  const uint64_t kk = dev::shfl_u64(lk, k - 1);
+  const uint32_t ki = __shfl_sync(0xffffffffu, li, k - 1);
+  if (!__any_sync(0xffffffffu, lt(ck, ci, kk, ki))) return;
+  warp_sort_ki(ck, ci);
+  warp_merge_ki(lk, li, ck, ci);
+}
+
+// Offer a sorted list (entries 0..k-1 valid, one per lane) to the warp's list.
+__device__ __forceinline__ void warp_offer_sorted(uint64_t& lk, uint32_t& li, uint64_t ck, uint32_t ci, int k) {
+  const uint64_t kk = dev::shfl_u64(lk, k - 1);
+  const uint32_t ki = __shfl_sync(0xffffffffu, li, k - 1);
+  const uint64_t hk = dev::shfl_u64(ck, 0);
+  const uint32_t hi = __shfl_sync(0xffffffffu, ci, 0);
+  if (!lt(hk, hi, kk, ki)) return;
+  warp_merge_ki(lk, li, ck, ci);
+}
+
+__device__ __forceinline__ double key_score(uint64_t key) {  // inverse of score_desc_key (scores are never -0.0)
+  uint64_t u = ~key;
+  u = (u >> 63) ? (u & 0x7FFFFFFFFFFFFFFFull) : ~u;
+  return __longlong_as_double((long long)u);
+}
+
+// The chain is latency-bound: one dependent DFMA per step (~8.6 cycles on
+// sm_100) with one warp per scheduler.  So nothing else may sit on its
+// critical path: the 32 keys of the NEXT 32-column sub-segment are loaded
+// from shared memory and widened (F2F) while the current sub's 32 DFMAs
+// run, and each group of 4 steps has its query operands loaded one group
+// ahead (NQ <= 2; from 3 queries up the NQ independent chains hide them).
+constexpr int kSub = 32;  // columns per sub-segment (one 128-B fp32 segment, half a bf16 one)
+
+template <typename KT>
+struct SubRaw {
+  static constexpr int kVec = kSub * (int)sizeof(KT) / 16;  // 16-B loads per sub: 8 fp32, 4 bf16
+  uint4 v[kVec];
+};
+
+// widen elements [4g, 4g + 4) of a sub (F2F: exact)
+template <typename KT>
+__device__ __forceinline__ void widen4(const SubRaw<KT>& r, int g, double* out) {
+  if constexpr (sizeof(KT) == 4) {
+    const uint4 x = r.v[g];
+    out[0] = (double)__uint_as_float(x.x);
+    out[1] = (double)__uint_as_float(x.y);
+    out[2] = (double)__uint_as_float(x.z);
+    out[3] = (double)__uint_as_float(x.w);
+  } else {
+    const uint4 x = r.v[g >> 1];
+    const uint32_t w0 = (g & 1) ? x.z : x.x, w1 = (g & 1) ? x.w : x.y;
+    out[0] = (double)__uint_as_float(w0 << 16);  // element 2i: the low half
+    out[1] = (double)__uint_as_float(w0 & 0xFFFF0000u);
+    out[2] = (double)__uint_as_float(w1 << 16);
+    out[3] = (double)__uint_as_float(w1 & 0xFFFF0000u);
+  }
+}
+
+// 32 chain steps on the widened sub `kc` (columns col0..col0+31 of the
+// queries in q64) while the next sub `rn` is widened into `kn`.
+template <typename KT, int NQ, bool kNext>
+__device__ __forceinline__ void chain_sub(const double (&kc)[kSub], double (&kn)[kSub], const SubRaw<KT>& rn,
+                                          const double* __restrict__ q64, int qlen, int col0, double (&acc)[NQ]) {
+  constexpr bool kQPre = NQ <= 2;
+  double2 qa[NQ][2], qb[NQ][2];
+  if constexpr (kQPre) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      qa[q][0] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0);
+      qa[q][1] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 2);
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < kSub / 4; ++g) {
+    if constexpr (kQPre) {
+      if (g + 1 < kSub / 4) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          qb[q][0] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 4 * g + 4);
+          qb[q][1] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 4 * g + 6);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        qa[q][0] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 4 * g);
+        qa[q][1] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 4 * g + 2);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      acc[q] = __fma_rn(qa[q][0].x, kc[4 * g + 0], acc[q]);
+      acc[q] = __fma_rn(qa[q][0].y, kc[4 * g + 1], acc[q]);
+      acc[q] = __fma_rn(qa[q][1].x, kc[4 * g + 2], acc[q]);
+      acc[q] = __fma_rn(qa[q][1].y, kc[4 * g + 3], acc[q]);
+    }
+    if constexpr (kNext) widen4<KT>(rn, g, &kn[4 * g]);
+    if constexpr (kQPre) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        qa[q][0] = qb[q][0];
+        qa[q][1] = qb[q][1];
+      }
+    }
+  }
+}
+
+struct ScanArgs {
+  int dim, nchunk;               // 128-B row segments per row
+  int64_t row_begin, row_end;    // rows scored
+  int R, lpw, S;                 // tile rows (4 lpw), rows per warp, ring stages
+  int64_t ntiles;
+  int k;
+  const float* queries;          // [NQ][dim]
+  uint64_t* lkey;                // [gridDim][NQ][32]
+  uint32_t* lid;
+  unsigned* ticket;              // zero between launches (the last CTA resets it)
+  double* scores;                // [NQ][k]
+  int32_t* ids;
+};
+
+template <typename KT, int NQ, int kCW = compute_warps(NQ)>
+__global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __grid_constant__ CUtensorMap km, ScanArgs a) {
+  constexpr int CPC = 128 / (int)sizeof(KT);  // columns per 128-B segment
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // SWIZZLE_128B stages must sit on 1-KB boundaries (the plan reserves the slack)
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int stage_bytes = a.R * 128;
+  const int qlen = a.nchunk * CPC;
+  uint8_t* ring = smem;
+  double* q64 = reinterpret_cast<double*>(smem + (size_t)a.S * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(q64 + (size_t)NQ * qlen);
+  uint64_t* empty = full + a.S;
+  uint64_t* ck = empty + a.S;                          // [kCW][NQ][32] CTA merge staging
+  uint32_t* ci = reinterpret_cast<uint32_t*>(ck + kCW * NQ * 32);
+  __shared__ int s_last;
+
+  if (tid == 0) {
+    for (int s = 0; s < a.S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  dev::pdl_wait();  // the queries may come from the previous kernel
+
+  if (warp == kCW) {
+    // ---- TMA producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int slot = 0, n = 0;
+      uint32_t ph = 0;
+      for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const int y = (int)(a.row_begin + t * a.R);
+        for (int j = 0; j < a.nchunk; ++j) {
+          if (n >= a.S) mbar_wait(&empty[slot], ph ^ 1);
+          ++n;
+          mbar_expect_tx(&full[slot], (uint32_t)stage_bytes);
+          tma_load_2d(ring + (size_t)slot * stage_bytes, &km, &full[slot], j * CPC, y, pol);
+          if (++slot == a.S) slot = 0, ph ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---- compute warps: queries -> fp64 (zero-padded), then the chains
+    {
+      // all of a thread's 16-B query loads in flight at once (one L2 round
+      // trip, not one per element), then the widened stores
+      constexpr int kLd = 8;
+      const int d4 = a.dim / 4, n4 = NQ * d4;
+      const float4* q4 = reinterpret_cast<const float4*>(a.queries);
+      for (int b0 = tid; b0 < n4; b0 += kCW * 32 * kLd) {
+        float4 v[kLd];
+#pragma unroll
+        for (int u = 0; u < kLd; ++u) {
+          const int x = b0 + u * kCW * 32;
+          v[u] = x < n4 ? __ldg(q4 + x) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kLd; ++u) {
+          const int x = b0 + u * kCW * 32;
+          if (x < n4) {
+            const int q = x / d4, c = (x - q * d4) * 4;
+            double* o = q64 + (size_t)q * qlen + c;
+            o[0] = (double)v[u].x;
+            o[1] = (double)v[u].y;
+            o[2] = (double)v[u].z;
+            o[3] = (double)v[u].w;
+          }
+        }
+      }
+      for (int x = tid; x < NQ * (qlen - a.dim); x += kCW * 32) {  // zero tail of the last segment
+        const int q = x / (qlen - a.dim);
+        q64[(size_t)q * qlen + a.dim + (x - q * (qlen - a.dim))] = 0.0;
+      }
+    }
+    named_sync(1, kCW * 32);
+    uint64_t lk[NQ];
+    uint32_t li[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      lk[q] = kEmpty;
+      li[q] = kNoId;
+    }
+    const int rr = warp * a.lpw + lane;
+    const int swz = rr & 7;
+    // ring positions: the next segment to wait for, the next to release
+    int wslot = 0, rslot = 0;
+    uint32_t wph = 0;
+    constexpr int SUBS = CPC / kSub;  // subs per 128-B segment
+    const uint8_t* rowbase = ring + (size_t)(lane < a.lpw ? rr : 0) * 128;
+    // sub u of the tile: segment u / SUBS, 16-B chunks [h kVec, (h + 1) kVec)
+    auto load_sub = [&](int u, SubRaw<KT>& r) {
+      const int h = u % SUBS;
+      if (h == 0) mbar_wait(&full[wslot], wph);
+      const uint8_t* rowp = rowbase + (size_t)wslot * stage_bytes;
+#pragma unroll
+      for (int c = 0; c < SubRaw<KT>::kVec; ++c)
+        r.v[c] = *reinterpret_cast<const uint4*>(rowp + (((h * SubRaw<KT>::kVec + c) ^ swz) << 4));
+      if (h == SUBS - 1 && ++wslot == a.S) wslot = 0, wph ^= 1;
+    };
+    // after the last sub of a segment is widened, its slot is free
+    auto release_if_last = [&](int u) {
+      if (u % SUBS == SUBS - 1) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rslot]);
+        if (++rslot == a.S) rslot = 0;
+      }
+    };
+    const int U = a.nchunk * SUBS;
+    for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+      const int64_t row = a.row_begin + t * a.R + rr;
+      const bool active = lane < a.lpw && row < a.row_end;
+      double acc[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+      double ka[kSub], kb[kSub];
+      SubRaw<KT> raw;
+      load_sub(0, raw);
+#pragma unroll
+      for (int g = 0; g < kSub / 4; ++g) widen4<KT>(raw, g, &ka[4 * g]);
+      release_if_last(0);
+      // ping-pong over (ka, kb): sub u runs on one while sub u + 1 is widened into the other
+      for (int u = 0; u < U; u += 2) {
+        if (u + 1 < U) {
+          load_sub(u + 1, raw);
+          chain_sub<KT, NQ, true>(ka, kb, raw, q64, qlen, u * kSub, acc);
+          release_if_last(u + 1);
+        } else {
+          chain_sub<KT, NQ, false>(ka, kb, raw, q64, qlen, u * kSub, acc);
+          break;
+        }
+        if (u + 2 < U) {
+          load_sub(u + 2, raw);
+          chain_sub<KT, NQ, true>(kb, ka, raw, q64, qlen, (u + 1) * kSub, acc);
+          release_if_last(u + 2);
+        } else {
+          chain_sub<KT, NQ, false>(kb, ka, raw, q64, qlen, (u + 1) * kSub, acc);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        warp_offer(lk[q], li[q], active ? dev::score_desc_key(acc[q]) : kEmpty, active ? (uint32_t)row : kNoId, a.k);
+    }
+    // the CTA's list: warps 1..3 stage theirs, warp 0 merges
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      ck[(warp * NQ + q) * 32 + lane] = lk[q];
+      ci[(warp * NQ + q) * 32 + lane] = li[q];
+    }
+    named_sync(1, kCW * 32);
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        for (int w = 1; w < kCW; ++w)
+          warp_offer_sorted(lk[q], li[q], ck[(w * NQ + q) * 32 + lane], ci[(w * NQ + q) * 32 + lane], a.k);
+        a.lkey[((size_t)blockIdx.x * NQ + q) * 32 + lane] = lk[q];
+        a.lid[((size_t)blockIdx.x * NQ + q) * 32 + lane] = li[q];
+      }
+    }
+  }
+  // ---- the last CTA merges every CTA's list
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  constexpr int kWarps = kCW + 1;
+  uint64_t lk[NQ];
+  uint32_t li[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    lk[q] = kEmpty;
+    li[q] = kNoId;
+  }
+  // every CTA's first k entries into shared memory at once (the ring is
+  // free; one L2 round trip, not one per list), then each warp merges its
+  // share from shared memory (a list whose head cannot enter costs one test)
+  const int G = gridDim.x;
+  const int per_list = NQ * a.k;
+  const int chunk = (int)((size_t)a.S * stage_bytes / ((size_t)per_list * 12));
+  uint64_t* sk = reinterpret_cast<uint64_t*>(ring);
+  uint32_t* si = reinterpret_cast<uint32_t*>(ring + (size_t)chunk * per_list * 8);
+  for (int c0 = 0; c0 < G; c0 += chunk) {
+    const int n = min(chunk, G - c0);
+#pragma unroll 8
+    for (int x = tid; x < n * per_list; x += kWarps * 32) {
+      const int g = x / per_list, r = x - g * per_list, q = r / a.k, j = r - q * a.k;
+      const size_t src = ((size_t)(c0 + g) * NQ + q) * 32 + j;
+      sk[x] = __ldcg(&a.lkey[src]);
+      si[x] = __ldcg(&a.lid[src]);
+    }
+    __syncthreads();
+    for (int g = warp; g < n; g += kWarps) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int x = (g * NQ + q) * a.k + lane;
+        warp_offer_sorted(lk[q], li[q], lane < a.k ? sk[x] : kEmpty, lane < a.k ? si[x] : kNoId, a.k);
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();  // the CTA merge staging is free again
+  if (warp > 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      ck[((warp - 1) * NQ + q) * 32 + lane] = lk[q];
+      ci[((warp - 1) * NQ + q) * 32 + lane] = li[q];
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      for (int w = 0; w < kWarps - 1; ++w)
+        warp_offer_sorted(lk[q], li[q], ck[(w * NQ + q) * 32 + lane], ci[(w * NQ + q) * 32 + lane], a.k);
+      if (lane < a.k) {
+        const bool ok = lk[q] != kEmpty;
+        a.scores[(size_t)q * a.k + lane] = ok ? key_score(lk[q]) : -INFINITY;
+        a.ids[(size_t)q * a.k + lane] = ok ? (int32_t)li[q] : -1;
+      }
+    }
+    if (lane == 0) *a.ticket = 0u;
+  }
+}
+
+struct ScanPlan {
+  int lpw, R, S, grid;
+  int64_t ntiles;
+  size_t smem;
+};
+
+template <typename KT>
+ScanPlan scan_plan(int64_t rows, int dim, int NQ, int nsm) {
+  constexpr int CPC = 128 / (int)sizeof(KT);
+  const int kCW = compute_warps(NQ);
+  ScanPlan p{};
+  const int nchunk = (dim + CPC - 1) / CPC;
+  int lpw = (int)std::min<int64_t>(32, (((rows + nsm - 1) / nsm) + kCW - 1) / kCW);
+  while ((kCW * lpw) % 8) ++lpw;  // a stage is a whole number of 1-KB swizzle atoms
+  p.lpw = lpw;
+  p.R = kCW * lpw;
+  p.ntiles = (rows + p.R - 1) / p.R;
+  p.grid = (int)std::min<int64_t>(p.ntiles, nsm);
+  const size_t fixed = (size_t)NQ * nchunk * CPC * sizeof(double) + 64 * 16 +
+                       (size_t)kCW * NQ * 32 * (sizeof(uint64_t) + sizeof(uint32_t)) + 1024;
+  const size_t stage = (size_t)p.R * 128;
+  const int S = (int)std::min<size_t>(16, (kSmemBudget - fixed) / stage);
+  p.S = S;
+  p.smem = (size_t)S * stage + fixed;
+  return p;
+}
+
+template <typename KT, int NQ>
+cudaError_t launch_scan_t(const CUtensorMap& km, const ScanPlan& p, const ScanArgs& a, cudaStream_t s) {
+  auto kern = exact_scan_kernel<KT, NQ>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)p.grid);
+  cfg.blockDim = dim3((compute_warps(NQ) + 1) * 32);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, km, a);
+}
+
+}  // namespace
+
+bool exact_scan_supported(int B, int dim, int key_dtype, int k) {
+  if (B < 1 || B > kScanMaxBatch || k < 1 || k > 32) return false;
+  if (key_dtype == HSD_DTYPE_BF16 ? dim % 8 : dim % 4) return false;  // TMA row stride: 16-B multiple
+  const size_t q = (size_t)B * (size_t)(dim + 63) * sizeof(double);
+  return q <= 136 * 1024;  // leaves room for a >= 4-stage ring of the widest tile
+}
+
+size_t exact_scan_scratch_bytes(int B, int num_sms) {
+  const int nq = std::max(1, B);
+  return (size_t)num_sms * nq * 32 * (sizeof(uint64_t) + sizeof(uint32_t)) + 256;
+}
+
+double exact_scan_cost_us(int64_t rows, int dim, int key_dtype, int B) {
+  // streaming bound (fp32 / bf16 keys at ~6 TB/s) vs the dim-step DFMA chain
+  // (~4.6 ns per step) + launch / merge overhead; measured on B200
+  const double bytes = (double)rows * dim * (key_dtype == HSD_DTYPE_BF16 ? 2 : 4);
+  const double stream = bytes / 6.0e6;
+  const double chain = dim * 4.6e-3 * (B > 2 ? 1.15 : 1.0);
+  return std::max(stream, chain) + 6.0;
+}
+
+cudaError_t launch_exact_scan(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin,
+                              int64_t row_end, int dim, const float* queries, int B, int k,
+                              void* scratch, int num_sms, double* scores,
+                              int32_t* ids, cudaStream_t s) {
+  if (!exact_scan_supported(B, dim, key_dtype, k) || row_end <= row_begin) return cudaErrorInvalidValue;
+  const bool bf16 = key_dtype == HSD_DTYPE_BF16;
+  const int NQ = B;
+  const int64_t rows = row_end - row_begin;
+  const ScanPlan p = bf16 ? scan_plan<uint16_t>(rows, dim, NQ, num_sms) : scan_plan<float>(rows, dim, NQ, num_sms);
+  if (p.S < 2) return cudaErrorInvalidValue;
+  CUtensorMap km;
+  const bool ok = bf16 ? tc_make_map_bf16(&km, keys, (uint64_t)n_keys_total, (uint64_t)dim, (uint32_t)p.R)
+                       : tc_make_map(&km, (const float*)keys, (uint64_t)n_keys_total, (uint64_t)dim, (uint32_t)p.R);
+  if (!ok) return cudaErrorInvalidValue;
+  uint8_t* sc = static_cast<uint8_t*>(scratch);
+  ScanArgs a{};
+  a.dim = dim;
+  a.nchunk = bf16 ? (dim + 63) / 64 : (dim + 31) / 32;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  a.R = p.R;
+  a.lpw = p.lpw;
+  a.S = p.S;
+  a.ntiles = p.ntiles;
+  a.k = k;
+  a.queries = queries;
+  a.ticket = reinterpret_cast<unsigned*>(sc);
+  a.lkey = reinterpret_cast<uint64_t*>(sc + 256);
+  a.lid = reinterpret_cast<uint32_t*>(sc + 256 + (size_t)num_sms * NQ * 32 * sizeof(uint64_t));
+  a.scores = scores;
+  a.ids = ids;
+  switch (NQ) {
+#define HSD_SCAN(N)                                                                      \
+  case N:                                                                                \
+    return bf16 ? launch_scan_t<uint16_t, N>(km, p, a, s) : launch_scan_t<float, N>(km, p, a, s);
+    HSD_SCAN(1)
+    HSD_SCAN(2)
+    HSD_SCAN(3)
+    HSD_SCAN(4)
+#undef HSD_SCAN
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace hsd

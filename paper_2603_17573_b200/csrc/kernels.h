@@ -56,6 +56,17 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
                             int dim, const float* queries, int B, int lists, void* scratch, uint64_t* partial,
                             float* dump, cudaStream_t s, ListGeom* geom = nullptr);
 
+// ---- K1x exact scan (k_exact.cu): every row's reference fp64 chain + top-k ----
+// For small (rows x batch): replaces K1 + K2.  scratch: exact_scan_scratch_bytes,
+// zeroed once at allocation (a ticket the last CTA resets).
+constexpr int kScanMaxBatch = 4;
+bool exact_scan_supported(int B, int dim, int key_dtype, int k);
+size_t exact_scan_scratch_bytes(int B, int num_sms);
+double exact_scan_cost_us(int64_t rows, int dim, int key_dtype, int B);
+cudaError_t launch_exact_scan(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin,
+                              int64_t row_end, int dim, const float* queries, int B, int k, void* scratch,
+                              int num_sms, double* scores, int32_t* ids, cudaStream_t s);
+
 // ---- K2 select: exact top-k from the filter lists -----------------------------
 // Four launches (candidates + threshold, pooled rescoring, exact range
 // fallback, rank; k_select.cu); scratch: select_scratch_bytes(B), B <= kMaxBatchPass.

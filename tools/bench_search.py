@@ -1,8 +1,10 @@
-"""Micro-benchmark of the batched exact search (K1 similarity + K2 select) per
-path / key dtype / batch, device-timed with CUDA events on the launching
-stream.  Prints one JSON line per configuration.
+"""Micro-benchmark of the batched exact search per search path / key dtype /
+batch, device-timed with CUDA events on the launching stream (L2 flushed
+before every timed search with --flush).  Prints one JSON line per
+configuration.
 
-  python tools/bench_search.py --n 1000000 --dim 4096 --batches 64,128,256 --dtypes f32,bf16
+  python tools/bench_search.py --n 10000 --dim 4096 --batches 1,2,4 --paths filter,scan --flush
+  python tools/bench_search.py --n 1000000 --dim 4096 --batches 64,256 --dtypes f32,bf16
 """
 import argparse
 import json
@@ -19,9 +21,11 @@ def main():
     ap.add_argument("--dim", type=int, default=4096)
     ap.add_argument("--batches", default="64,128,256")
     ap.add_argument("--dtypes", default="f32,bf16")
-    ap.add_argument("--paths", default="tc")
+    ap.add_argument("--paths", default="auto", help="comma list of auto | filter | scan | tc_single")
+    ap.add_argument("--shadow", action="store_true", help="fp32 collections keep the bf16 filter copy")
+    ap.add_argument("--flush", action="store_true", help="write 512 MB between timed searches (cold L2)")
     ap.add_argument("--k", type=int, default=8)
-    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--iters", type=int, default=20)
     a = ap.parse_args()
     import torch
 
@@ -29,30 +33,34 @@ def main():
 
     torch.cuda.set_device(0)
     s = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if a.flush else None
     for dt in a.dtypes.split(","):
         col = H.Collection(a.dim, capacity=a.n, dtype=dt)
         col.generate(H.REAL, 2026, a.n)
-        esz = 2 if dt == "bf16" else 4
+        if a.shadow and dt == "f32":
+            col.set_filter("bf16_copy")
         for path in a.paths.split(","):
-            if dt == "bf16" and path != "tc":
-                continue
             H.set_sim_path(path)
             for B in [int(x) for x in a.batches.split(",")]:
                 q = H.gen_queries(H.REAL, 7, 2026, a.n, 0, B, a.dim)
                 for _ in range(3):
                     col.search_topk_exact(q, a.k)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                      for _ in range(a.iters)]
                 torch.cuda.synchronize()
-                e0.record(s)
-                for _ in range(a.iters):
+                for e0, e1 in ev:
+                    if flush is not None:
+                        flush.fill_(1)
+                    e0.record(s)
                     col.search_topk_exact(q, a.k)
-                e1.record(s)
+                    e1.record(s)
                 torch.cuda.synchronize()
-                ms = e0.elapsed_time(e1) / a.iters
-                gbs = a.n * a.dim * esz * ((B + 1023) // 1024 if path == "tc" else (B + 63) // 64) / (ms / 1e3) / 1e9
-                print(json.dumps({"dtype": dt, "path": path, "B": B, "n": a.n, "dim": a.dim, "ms": ms,
-                                  "queries_per_s": B / (ms / 1e3), "key_stream_GBps": gbs,
-                                  "overflow": col.overflow_count()}), flush=True)
+                t = sorted(e0.elapsed_time(e1) for e0, e1 in ev)
+                ms = sum(t) / len(t)
+                print(json.dumps({"dtype": dt, "path": path, "shadow": bool(a.shadow), "B": B, "n": a.n,
+                                  "dim": a.dim, "ms": ms, "ms_min": t[0], "ms_median": t[len(t) // 2],
+                                  "queries_per_s": B / (ms / 1e3), "l2_flushed": bool(a.flush),
+                                  "stats": col.search_stats(reset=True)}), flush=True)
             H.set_sim_path("auto")
         col.close()
         del col
