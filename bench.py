@@ -61,7 +61,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=1_000_000)
+    p.add_argument("--n", "--rows", dest="n", type=int, default=1_000_000)
     p.add_argument("--dim", type=int, default=4096)
     p.add_argument("--batch", type=int, default=64)
     p.add_argument("--k", type=int, default=8)
@@ -95,6 +95,8 @@ def parse():
     p.add_argument("--episodes", type=int, default=4096, help="C3 episodes per round")
     a = p.parse_args()
     given = {x.split("=")[0] for x in sys.argv[1:] if x.startswith("--")}
+    if "--rows" in given:
+        given.add("--n")
     if a.config == "c4":
         if "--n" not in given:
             a.n = 10_000_000
@@ -389,10 +391,6 @@ def config_of(args, world):
                      f"k={args.k}, draft len {args.L}, 7x256 verifier logits, {args.d_f}-d skip features, "
                      f"15-pt windows"),
         "key_dtype": args.dtype,
-        "filter": ("bf16 copy of the fp32 keys (+50% HBM) streamed by the tensor-core filter; exact fp64 rescoring "
-                   "from the fp32 keys (results bit-identical to the fp32 reference)"
-                   if args.filter == "bf16_copy" and args.dtype == "f32"
-                   else getattr(args, "filter_note", "native (filter reads the stored keys)")),
         "n_rows": args.n, "dim": args.dim, "batch": args.batch, "k": args.k, "draft_len": args.L, "d_f": args.d_f,
         "synthetic_family": "REAL" if args.kind == 1 else "EXACT",
         "parallelism": ("single" if world == 1 else
@@ -405,9 +403,21 @@ def config_of(args, world):
     }
 
 
+def search_of(args):
+    """How our arm searches (a top-level key: `config` stays the workload both arms share)."""
+    if getattr(args, "search_path", "filter") == "scan":
+        return ("exact scan (K1x) of the stored keys: every row scored with the reference's sequential fp64 sum, no "
+                "filter (the library's cost model picks it for this rows x batch)")
+    if args.filter == "bf16_copy" and args.dtype == "f32":
+        return ("bf16 copy of the fp32 keys (+50% HBM) streamed by the tensor-core filter; exact fp64 rescoring from "
+                "the fp32 keys (results bit-identical to the fp32 reference)")
+    return getattr(args, "filter_note", "tensor-core filter over the stored keys + exact fp64 rescoring")
+
+
 def l2_of(args):
     """The L2 rule as this workload meets it (the same text in both arms' config)."""
-    scanned = args.n * args.dim * (2 if args.dtype == "bf16" or args.filter == "bf16_copy" else 4)
+    scanned = args.n * args.dim * (2 if args.dtype == "bf16" or (args.filter == "bf16_copy" and getattr(
+        args, "search_path", "filter") != "scan") else 4)
     if scanned < 2 * 126e6:
         return ("L2 flushed between timed steps (512 MB write outside the per-step CUDA-event brackets; the "
                 "per-step device times are summed)")
@@ -453,6 +463,9 @@ def run_ours(args):
         except H.OutOfMemoryError:  # e.g. C4's 164 GB of fp32 keys on one GPU: no room for the copy
             args.filter = "native"
             args.filter_note = "bf16 copy does not fit next to the fp32 keys on this GPU; native TF32 filter"
+    # the search path the library picks for this shape (the peer-memory exchange publishes from K2)
+    args.search_path = ("filter" if sharded and args.exchange == "p2p"
+                        else col.search_plan(B, args.k, b1 - b0))
     if args.graph:  # graph capture needs a non-legacy stream
         gstream = torch.cuda.Stream(device=dev)
         torch.cuda.set_stream(gstream)
@@ -515,8 +528,9 @@ def run_ours(args):
             fork(i)
             j = i % pipe
             engs[j].step(B, bufs[j][i % S], vp, gap_d=1, stream=strs[j], graph=args.graph)
-        # K5 + skip similarity (side stream), query slab, K1, K2 (4 kernels), K4 — eager or as one graph's nodes
-        launches_per_step = 9
+        # K5 + skip similarity (side stream), query slab, K1, K2 (4 kernels), K4 — eager or as one graph's nodes;
+        # the exact-scan path: K5 + skip similarity, K1x, K4
+        launches_per_step = 4 if args.search_path == "scan" else 9
     else:
         # one communicator (receive window / NCCL comm) per cohort: the cohorts' exchanges are independent
         comms = [setup_comm(H, dist, world, rank, local, args.exchange, max_B=B, k_max=k) for _ in range(pipe)]
@@ -576,8 +590,13 @@ def run_ours(args):
     ms_per_step = ms / args.steps
     value = (world if replicas else 1) * B * args.steps / (ms / 1e3)  # whole-job steps/s
 
-    esz = 2 if (args.dtype == "bf16" or args.filter == "bf16_copy") else 4
-    passes = (B + 1023) // 1024  # up to 1024 queries share one key stream (cluster multicast)
+    scan = getattr(args, "search_path", "filter") == "scan"
+    if scan:  # K1x reads the stored keys once (fp32: 4 B per element), all B <= 4 queries per row
+        esz = 2 if args.dtype == "bf16" else 4
+        passes = 1
+    else:
+        esz = 2 if (args.dtype == "bf16" or args.filter == "bf16_copy") else 4
+        passes = (B + 1023) // 1024  # up to 1024 queries share one key stream (cluster multicast)
     alg_bytes = passes * (b1 - b0) * dim * esz + B * dim * 4
     peak, peak_kind = load_peaks()
     stages = roof = select = None
@@ -611,14 +630,21 @@ def run_ours(args):
         achieved = alg_bytes / (k1_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": load_traffic(traffic_key(args)),
-                "kernel": f"similarity (K1, {'kind::tf32' if esz == 4 else 'kind::f16'} filter"
-                          f"{' over the bf16 key copy' if args.filter == 'bf16_copy' and esz == 2 else ''})",
+                "kernel": ("similarity (K1x exact scan: every row's sequential fp64 chain over the stored keys + "
+                           "top-k; no filter, no rescoring)" if scan else
+                           f"similarity (K1, {'kind::tf32' if esz == 4 else 'kind::f16'} filter"
+                           f"{' over the bf16 key copy' if args.filter == 'bf16_copy' and esz == 2 else ''})"),
                 "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": k1_ms, "avg_launch_source": k1_src,
                 "isolated_launch_ms": stages["similarity"], "peak_source": peak_kind,
                 "share_of_step": min(1.0, k1_ms / ms_per_step) if not flush else stages["similarity"] / stages["total"]}
         tflops = 2.0 * B * (b1 - b0) * dim / (k1_ms / 1e3) / 1e12
         bf16_peak = load_peak_key("bf16_tflops")
-        if bf16_peak:
+        if scan:  # fp64 CUDA-core chains: the DFMA latency of one dim-step chain is the compute floor
+            roof["chain"] = {"steps_per_row": dim, "ns_per_step": k1_ms * 1e6 / dim,
+                             "dfma_latency_floor_ns": 8.6 / 1.965,
+                             "note": "each row's score is one dependent chain of dim fp64 FMAs (the reference's "
+                                     "sequential sum); rows run in parallel, one per thread"}
+        elif bf16_peak:
             tpk = bf16_peak if esz == 2 else bf16_peak / 2.0
             roof["tensor"] = {"achieved_tflops": tflops, "peak_tflops": tpk, "frac": tflops / tpk,
                               "peak_source": "measured bf16" if esz == 2
@@ -657,7 +683,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak" if (replicas or world == 1) else "strong",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (counter-generated DB/queries/logits/features)",
-            "config": config_of(args, world), "pipeline": pipeline_of(args), "roofline": roof, "cpu_baseline": cb,
+            "config": config_of(args, world), "pipeline": pipeline_of(args), "search": search_of(args),
+            "roofline": roof, "cpu_baseline": cb,
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(), "stages_ms": stages,
             "select": select,
         }
@@ -721,7 +748,12 @@ class ShardedCohort:
 def init_dist(dist, dev):
     """NCCL (one process per GPU); HSD_BENCH_BACKEND=gloo for plumbing runs with
     several ranks on one GPU (the timing reductions use CPU tensors)."""
-    backend = os.environ.get("HSD_BENCH_BACKEND", "nccl")
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    import torch
+
+    # ranks sharing a GPU (plumbing runs): NCCL refuses two ranks on one device
+    default = "nccl" if torch.cuda.device_count() >= world else "gloo"
+    backend = os.environ.get("HSD_BENCH_BACKEND", default)
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=dev)
     else:

@@ -173,6 +173,10 @@ hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, 
  * only, 3 exact scan wherever it applies (B <= 4, k <= 32).  Every path
  * returns the same bits. */
 hsd_status hsd_set_sim_path(int path);
+/* The path a search of B queries (top-k) over `rows` rows (-1: the whole
+ * collection) takes under the current switch: *exact_scan = 1 for the exact
+ * scan (K1x), 0 for the tensor-core filter + exact rescoring (K1 + K2). */
+hsd_status hsd_search_plan(hsd_collection* c, int B, int k, int64_t rows, int* exact_scan);
 
 /* ------------------------------------------------------------------------
  * Verification — fused gather + verify-skip + sequence-wise relaxed

@@ -228,6 +228,7 @@ def lib():
         "hsd_collection_generate_rows": [_vp, C.c_int, C.c_uint64, C.c_int64, C.c_int64],
         "hsd_debug_sim_scores": [_vp, _vp, C.c_int, C.c_int, _vp, _vp],
         "hsd_set_sim_path": [C.c_int],
+        "hsd_search_plan": [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p],
         "hsd_merge_topk": [C.c_int, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
         "hsd_gen_queries": [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, _vp,
                             _vp],
@@ -449,6 +450,12 @@ class Collection:
         torch = _torch()
         n, dev = self.size(), self.device
         return (_from_ptr(fp.value, (n, d.value), torch.float32, dev), _from_ptr(hp.value, (n,), torch.uint8, dev))
+
+    def search_plan(self, B: int, k: int, rows: int = -1) -> str:
+        """The search path a batch of B queries takes: "scan" (K1x exact scan) or "filter" (K1 + K2)."""
+        v = C.c_int()
+        check(lib().hsd_search_plan(self._h, int(B), int(k), int(rows), C.byref(v)))
+        return "scan" if v.value else "filter"
 
     def search_stats(self, stream=None, reset=False) -> dict:
         """Accumulated search statistics of `stream` (hsd_search_stats; synchronizes)."""

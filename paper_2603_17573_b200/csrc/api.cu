@@ -655,6 +655,12 @@ hsd_status hsd_set_sim_path(int path) {
   return HSD_OK;
 }
 
+hsd_status hsd_search_plan(hsd_collection* c, int B, int k, int64_t rows, int* exact_scan) {
+  if (!c || !exact_scan) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *exact_scan = use_exact_scan(c, B, k, rows < 0 ? c->n : rows) ? 1 : 0;
+  return HSD_OK;
+}
+
 hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, int variant, float* out,
                                 void* stream) {
   if (!c || !queries || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");

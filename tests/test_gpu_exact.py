@@ -25,6 +25,16 @@ def torch():
     return torch
 
 
+@pytest.fixture(autouse=True)
+def filter_path():
+    """This module covers the filter + rescoring path's exactness machinery (the
+    candidate margin and the range fallback): small batches would otherwise take
+    the exact scan (tests/test_gpu_scan.py covers that path on these families)."""
+    H.set_sim_path("filter")
+    yield
+    H.set_sim_path("auto")
+
+
 def check(col, kind, seed, n, q, k, row_range=None):
     sc, ids = col.search_topk_exact(q, k, row_range=row_range)
     if row_range is None:
@@ -88,7 +98,7 @@ def test_cluster_dim4096_and_ranges(torch, B):
 
 @pytest.mark.parametrize("path", ["auto", "tc_single"])
 def test_cluster_all_pass_widths(torch, path):
-    H.set_sim_path(path)
+    H.set_sim_path("filter" if path == "auto" else path)
     try:
         n, dim = 12_000, 64
         col = H.Collection(dim, capacity=n)

@@ -57,18 +57,26 @@ def test_search_matches_reference_fixture(torch, name):
     assert col.overflow_count() == 0
 
 
+@pytest.mark.parametrize("path", ["auto", "filter"])
 @pytest.mark.parametrize("kind", [O.EXACT, O.REAL])
 @pytest.mark.parametrize("B", [1, 2, 3, 5, 8, 9, 24, 64, 100])
 @pytest.mark.parametrize("dim", [64, 4096])
-def test_search_parity_vs_oracle(torch, kind, B, dim):
+def test_search_parity_vs_oracle(torch, kind, B, dim, path):
+    """auto: the exact scan for small rows x batch (B <= 4), else the filter; filter: K1 + K2 always."""
+    if path == "filter" and B > 4:
+        pytest.skip("auto already takes the filter path")
     n = 20_000 if dim == 64 else 6000
     col = make_db(kind, 100 + B, n, dim)
     q = H.gen_queries(kind, 200 + B, 100 + B, n, 0, B, dim)
-    for k in (1, 8, 32):
-        sc, ids = col.search_topk_exact(q, k)
-        osc, oid = O.search_synth(kind, 100 + B, n, q.cpu().numpy(), k, threads=0)
-        np.testing.assert_array_equal(ids.cpu().numpy(), oid)
-        np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+    H.set_sim_path(path)
+    try:
+        for k in (1, 8, 32):
+            sc, ids = col.search_topk_exact(q, k)
+            osc, oid = O.search_synth(kind, 100 + B, n, q.cpu().numpy(), k, threads=0)
+            np.testing.assert_array_equal(ids.cpu().numpy(), oid)
+            np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+    finally:
+        H.set_sim_path("auto")
     assert col.overflow_count() == 0
 
 

@@ -144,16 +144,32 @@ def test_p2p_sharded_search_single_rank():
         comm.close()
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_p2p_exchange_multi_process(world):
-    """G processes exchange their top-k records through each other's IPC-mapped windows (one GPU)."""
+def _run_workers(world, exchange, port):
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    port = 29600 + world
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "tests", "p2p_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root)
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(root, "tests", "p2p_worker.py"),
+           "--exchange", exchange]
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_exchange_multi_process(world):
+    """G processes exchange their top-k records through each other's IPC-mapped windows (one GPU)."""
+    r = _run_workers(world, "p2p", 29600 + world)
     assert "P2P_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+@pytest.mark.gpu
+def test_nccl_exchange_world2():
+    """The product's NCCL all-gather exchange at world 2 (hsd_search_topk_sharded over a 2-rank data-path
+    communicator), checked against the single-collection search; needs two GPUs (NCCL refuses two ranks on one
+    device)."""
+    r = _run_workers(2, "nccl", 29611)
+    if "NCCL_SAME_DEVICE" in r.stdout:
+        pytest.skip("one GPU on this box: NCCL needs a device per rank")
+    assert "NCCL_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "data-path NCCL communicator with 2 ranks" in r.stdout
