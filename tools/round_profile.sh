@@ -8,6 +8,7 @@
 #   full_c4.ncu-rep    the CTA-pair filter at B = 256 (fp32, TF32) + K4
 #   full_c5.ncu-rep    the CTA-pair filter at B = 683 (3 pairs per cluster, bf16)
 #   full_c3.ncu-rep    K4 at config 3 (4096 episodes x 12 parameter sets)
+#   full_c1.ncu-rep    K1x exact scan at config 1 (10k rows, batch 1)
 # Usage: gpurun --timeout 3000 -- bash tools/round_profile.sh [quick]
 set -u
 OUT=gpurun_out
@@ -37,6 +38,9 @@ timeout 900 ncu --set full --clock-control none --import-source on -k "regex:sim
   -o $OUT/full_c5 python tools/bench_search.py --n 1000000 --batches 683 --dtypes bf16 --iters 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:verify" -s 2 -c 1 \
   -o $OUT/full_c3 python bench.py --config c3 --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+# config-1 shape: the K1x exact scan (10k rows, batch 1)
+timeout 600 ncu --set full --clock-control none --import-source on -k "regex:exact_scan" -s 4 -c 1 \
+  -o $OUT/full_c1 python bench.py --config c1 --steps 3 --warmup 1 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 timeout 600 python bench.py --impl reference > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 # summaries on the box (gpurun returns at most 64 MiB): launch lists, full captures, DRAM traffic
 cp profiles/traffic.json $OUT/traffic.json
@@ -50,6 +54,8 @@ python tools/ncu_summary.py full $OUT/full_c5.ncu-rep $OUT/ncu_full_c5.md --traf
   --key similarity_pair_c5 --match sim_pair > /dev/null
 python tools/ncu_summary.py full $OUT/full_c3.ncu-rep $OUT/ncu_full_c3.md --traffic $OUT/traffic.json \
   --key verify_c3 --match verify > /dev/null
+python tools/ncu_summary.py full $OUT/full_c1.ncu-rep $OUT/ncu_full_c1.md --traffic $OUT/traffic.json \
+  --key exact_scan_c1 --match exact_scan > /dev/null
 # keep the config-2 report (source-level reading here); drop the rest to stay under the size cap
-rm -f $OUT/full_c3.ncu-rep $OUT/full_c4.ncu-rep $OUT/full_c5.ncu-rep
+rm -f $OUT/full_c1.ncu-rep $OUT/full_c3.ncu-rep $OUT/full_c4.ncu-rep $OUT/full_c5.ncu-rep
 ls -la $OUT
