@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -117,13 +118,18 @@ class Collection {
     std::swap(pdim_, o.pdim_);
     std::swap(device_, o.device_);
     std::swap(h_, o.h_);
+    std::swap(index_, o.index_);
+    std::swap(nprobe_, o.nprobe_);
     std::swap(records_, o.records_);
     std::swap(q_, o.q_);
     std::swap(s_, o.s_);
     std::swap(i_, o.i_);
     return *this;
   }
-  ~Collection() { hsd_collection_destroy(h_); }
+  ~Collection() {
+    drop_index();
+    hsd_collection_destroy(h_);
+  }
 
   // Upload an existing reference collection (e.g. one built by load_collection).
   static Collection from(const hsd::Collection& c, int device = 0) {
@@ -169,6 +175,7 @@ class Collection {
     }
     int64_t first = 0;
     check(hsd_collection_insert(h_, emb.data(), act.data(), ep.data(), st.data(), n, &first));
+    if (n) drop_index();  // stale after mutation (store.cpp:55)
     if (d_f) {  // Record::feature -> the device feature table (feeds calibrate_skip)
       std::vector<float> f((size_t)n * d_f, 0.0f);
       std::vector<uint8_t> has((size_t)n, 0);
@@ -228,9 +235,45 @@ class Collection {
   std::vector<SearchHit> search_topk_exact(const Embedding& query, int k) const {
     return search_topk_exact_batch(std::vector<Embedding>{query}, k).front();
   }
-  // Collection::search_topk (store.cpp:82-92): the device search is exact at
-  // every size, so no approximate index is involved.
-  std::vector<SearchHit> search_topk(const Embedding& query, int k) const { return search_topk_exact(query, k); }
+  // Collection::build_hnsw (store.cpp:75-80): the device's approximate index
+  // is an inverted file (IVF-flat, hsd_index_*), not a graph.  HnswParams map
+  // to it as  nlist = ceil(sqrt(N)) (<= 16384),  Lloyd iterations =
+  // clamp(ef_construct / 10, 1, 20),  nprobe = clamp(ef_search / 4, 1, 32);
+  // m (graph degree) has no IVF meaning.
+  void build_hnsw(const HnswParams& params) {
+    if (records_.empty()) throw InvalidInputError("cannot index an empty collection");  // store.cpp:76
+    if (params.m < 2 || params.ef_construct < 1) throw ConfigError("invalid hnsw parameters");  // hnsw.cpp:42
+    drop_index();
+    const double n = (double)records_.size();
+    hsd_ivf_params p{(int)std::min(16384.0, std::ceil(std::sqrt(n))), std::clamp(params.ef_construct / 10, 1, 20)};
+    check(hsd_index_build(h_, &p, &index_));
+    nprobe_ = std::clamp(params.ef_search / 4, 1, 32);
+  }
+  bool has_hnsw() const { return index_ != nullptr; }
+
+  // Collection::search_topk (store.cpp:82-92): the index when built (the
+  // returned scores are still cosine_similarity of the returned ids, :86-90),
+  // else the exact search.
+  std::vector<SearchHit> search_topk(const Embedding& query, int k) const {
+    if (!index_) return search_topk_exact(query, k);
+    if (k < 1) return {};  // HnswIndex::search returns no ids (hnsw.cpp:160)
+    if ((int)query.size() != dim_) throw InvalidInputError("embedding dim mismatch in cosine");
+    if (k > HSD_K_MAX) throw InvalidInputError("k exceeds the device top-k limit HSD_K_MAX");
+    std::vector<float> q((size_t)pdim_, 0.0f);
+    for (int c = 0; c < dim_; ++c) q[(size_t)c] = (float)query[(size_t)c];
+    s_.resize((size_t)k);
+    i_.resize((size_t)k);
+    q_.upload(q.data(), q.size());
+    check(hsd_search_topk_index(index_, q_.get(), 1, k, nprobe_, s_.get(), i_.get(), nullptr, nullptr));
+    std::vector<double> sc((size_t)k);
+    std::vector<int32_t> id((size_t)k);
+    s_.download(sc.data(), sc.size());
+    i_.download(id.data(), id.size());
+    std::vector<SearchHit> out;
+    for (int j = 0; j < k && id[(size_t)j] >= 0; ++j)
+      out.push_back({sc[(size_t)j], id[(size_t)j], records_[(size_t)id[(size_t)j]].payload});
+    return out;
+  }
 
   // Batched search: one pass over the DB for all queries.
   std::vector<std::vector<SearchHit>> search_topk_exact_batch(const std::vector<Embedding>& queries, int k) const {
@@ -262,11 +305,18 @@ class Collection {
   }
 
  private:
+  void drop_index() {
+    hsd_index_destroy(index_);
+    index_ = nullptr;
+  }
+
   std::string name_;
   int dim_ = 0;
   int pdim_ = 0;  // device row length: dim rounded up to 8 (zero padding)
   int device_ = 0;
   hsd_collection* h_ = nullptr;
+  hsd_index* index_ = nullptr;  // approximate index (build_hnsw), dropped on insert
+  int nprobe_ = 25;
   std::vector<Record> records_;
   mutable DeviceBuffer<float> q_;
   mutable DeviceBuffer<double> s_;

@@ -179,6 +179,48 @@ hsd_status hsd_set_sim_path(int path);
 hsd_status hsd_search_plan(hsd_collection* c, int B, int k, int64_t rows, int* exact_scan);
 
 /* ------------------------------------------------------------------------
+ * Approximate index — the device stand-in for the reference's HNSW index:
+ * Collection::build_hnsw(HnswParams) (store.cpp:75-80, hnsw.cpp:58-169) and
+ * the index branch of Collection::search_topk (store.cpp:82-92).
+ *
+ * An inverted file (IVF-flat): nlist unit-norm centroids (spherical k-means,
+ * n_iter Lloyd iterations whose assignment is the collection's own exact
+ * search; deterministic), each record in the list of its best centroid
+ * (score desc, id asc), the lists read in place from the keys.  A search
+ * scores every centroid, scans the rows of the nprobe best lists, keeps the
+ * 32 best candidates by their fp32-accumulated scores (over the stored keys,
+ * or the bf16 filter copy when the collection keeps one) and returns
+ * the top k of those by the EXACT score: every returned score is the
+ * reference's cosine_similarity of the returned id (store.cpp:86-90), ranked
+ * (score desc, id asc).  Recall against search_topk_exact is reported by the
+ * tests and the bench, not guaranteed.
+ *
+ * hsd_index_build: empty collection -> HSD_ERR_INVALID_INPUT ("cannot index
+ * an empty collection", store.cpp:76); nlist is clamped to the row count.
+ * The index holds the collection (which must outlive it); a later insert or
+ * generate makes it stale, and a stale index searches exactly (the reference
+ * drops the index on insert and search_topk falls back to the exact scan).
+ * ---------------------------------------------------------------------- */
+typedef struct hsd_ivf_params {
+  int nlist;  /* inverted lists, 1..16384 (clamped to the row count) */
+  int n_iter; /* Lloyd iterations after the strided seeds, 0..1000 */
+} hsd_ivf_params;
+typedef struct hsd_index hsd_index;
+hsd_status hsd_index_build(hsd_collection* c, const hsd_ivf_params* params, hsd_index** out);
+hsd_status hsd_index_destroy(hsd_index* x);
+/* nlist, indexed rows, longest list, stale (1 when the collection changed) */
+hsd_status hsd_index_info(const hsd_index* x, int* nlist, int64_t* n_rows, int* max_list, int* stale);
+/* Host copies (any may be NULL): offs [nlist + 1], perm [n_rows] (list
+ * order -> record id, ascending within each list), centroids fp32 [nlist][dim]. */
+hsd_status hsd_index_lists(const hsd_index* x, int32_t* offs, int32_t* perm, float* centroids);
+/* Approximate top-k of B queries (device, 16-byte aligned) over the nprobe
+ * (1..32, clamped to nlist) best lists; scores / ids as
+ * hsd_search_topk_exact (-inf / -1 past the candidates found).  probes
+ * (device [B][nprobe], optional) receives the probed list ids. */
+hsd_status hsd_search_topk_index(hsd_index* x, const float* queries, int B, int k, int nprobe, double* scores,
+                                 int32_t* ids, int32_t* probes, void* stream);
+
+/* ------------------------------------------------------------------------
  * Verification — fused gather + verify-skip + sequence-wise relaxed
  * acceptance + accepted length (spec-only in the reference).
  * ---------------------------------------------------------------------- */

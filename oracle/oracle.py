@@ -473,3 +473,83 @@ def window_derivatives(xyz) -> np.ndarray:
     out = np.zeros(3, np.float64)
     lib().hsdo_window_derivatives(x.ctypes.data_as(C.c_void_p), x.shape[0], out.ctypes.data_as(C.c_void_p))
     return out
+
+
+# ---- approximate index (IVF-flat) restatement ----------------------------------
+# The product's device index (paper_2603_17573_b200/csrc/k_ivf.cu) stands in for
+# the reference's HNSW behind Collection::build_hnsw / search_topk
+# (store.cpp:75-92).  HNSW's graph has no bit-level counterpart, so the oracle
+# pins the index's own definition: exact assignment of every record to its best
+# centroid (the reference's score and (score desc, id asc) order, store.cpp:59-73),
+# the stable list order, normalized list means, and search_topk's contract that
+# returned scores are the reference's cosine_similarity of the returned ids
+# (store.cpp:86-90).
+
+def ivf_seed_rows(n: int, nlist: int) -> np.ndarray:
+    """Row floor((2l + 1) n / (2 nlist)) of each of nlist strata (k_ivf.cu ivf_seed_kernel)."""
+    l = np.arange(nlist, dtype=np.float64)
+    return ((2.0 * l + 1.0) * float(n) / (2.0 * nlist)).astype(np.int64)
+
+
+def ivf_assign(keys: np.ndarray, cent: np.ndarray) -> np.ndarray:
+    """Best centroid of every row by the reference's exact search (row = query)."""
+    _, ids = search_topk(cent, keys, 1)
+    return ids[:, 0].astype(np.int32)
+
+
+def ivf_lists(assign: np.ndarray, nlist: int):
+    """Stable counting sort: offs [nlist + 1], perm (record ids, ascending within a list)."""
+    counts = np.bincount(assign, minlength=nlist)
+    offs = np.zeros(nlist + 1, np.int32)
+    offs[1:] = np.cumsum(counts)
+    perm = np.argsort(assign, kind="stable").astype(np.int32)
+    return offs, perm
+
+
+def ivf_centroids(keys: np.ndarray, offs: np.ndarray, perm: np.ndarray, old: np.ndarray) -> np.ndarray:
+    """List means normalized to unit length (fp64 sums, fp32 result); empty lists keep the old centroid."""
+    out = old.astype(np.float32).copy()
+    for l in range(len(offs) - 1):
+        rows = perm[offs[l]:offs[l + 1]]
+        if len(rows) == 0:
+            continue
+        s = keys[rows].astype(np.float64).sum(axis=0)
+        nrm = np.sqrt((s * s).sum())
+        if nrm > 0 and np.isfinite(nrm):
+            out[l] = (s / nrm).astype(np.float32)
+    return out
+
+
+def ivf_build(keys: np.ndarray, nlist: int, n_iter: int):
+    """The whole build on the CPU (small cases): (centroids, offs, perm)."""
+    keys = np.ascontiguousarray(keys, np.float32)
+    n = keys.shape[0]
+    nlist = min(nlist, n)
+    seeds = keys[ivf_seed_rows(n, nlist)].astype(np.float64)
+    nrm = np.sqrt((seeds * seeds).sum(axis=1, keepdims=True))
+    cent = np.where(nrm > 0, seeds / np.where(nrm > 0, nrm, 1.0), 0.0).astype(np.float32)
+    for it in range(n_iter + 1):
+        offs, perm = ivf_lists(ivf_assign(keys, cent), nlist)
+        if it == n_iter:
+            break
+        cent = ivf_centroids(keys, offs, perm, cent)
+    return cent, offs, perm
+
+
+def ivf_search_lists(keys: np.ndarray, offs: np.ndarray, perm: np.ndarray, probes: np.ndarray,
+                     queries: np.ndarray, k: int):
+    """Exact top-k of each query over the rows of its probed lists: ids are
+    record ids, scores the reference's sequential fp64 sum (store.cpp:29-34)."""
+    queries = np.ascontiguousarray(np.atleast_2d(queries), np.float32)
+    B = queries.shape[0]
+    sc = np.full((B, k), -np.inf, np.float64)
+    ids = np.full((B, k), -1, np.int64)
+    for b in range(B):
+        rows = np.sort(np.concatenate([perm[offs[l]:offs[l + 1]] for l in set(int(p) for p in probes[b])]))
+        if len(rows) == 0:
+            continue
+        s, i = search_topk(keys[rows], queries[b:b + 1], k)
+        m = s.shape[1]
+        sc[b, :m] = s[0]
+        ids[b, :m] = rows[i[0]]
+    return sc, ids

@@ -132,6 +132,10 @@ MODE_HYBRID, MODE_PURE_RETRIEVAL, MODE_PURE_DRAFTER, MODE_AUTOREGRESSIVE = 0, 1,
 PAYLOAD_RANDOM, PAYLOAD_TRAJ = 0, 1
 
 
+class IvfParams(C.Structure):
+    _fields_ = [("nlist", C.c_int), ("n_iter", C.c_int)]
+
+
 class SkipState(C.Structure):
     """hsd_skip_state: VerifySkipState (SPEC.md:411-414)."""
     _fields_ = [("T", C.c_double), ("min_S", C.c_double), ("O_dist", C.c_int32), ("delta", C.c_double),
@@ -254,6 +258,11 @@ def lib():
                                C.POINTER(C.c_int), _vp],
         "hsd_update_skip_state": [C.POINTER(SkipState), C.c_int, C.c_double, C.c_double],
         "hsd_collection_load_image": [C.c_char_p, C.c_int, C.POINTER(_vp)],
+        "hsd_index_build": [_vp, C.POINTER(IvfParams), C.POINTER(_vp)],
+        "hsd_index_destroy": [_vp],
+        "hsd_index_info": [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "hsd_index_lists": [_vp, _vp, _vp, _vp],
+        "hsd_search_topk_index": [_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -322,6 +331,10 @@ class Collection:
         self._dim = dim
 
     def close(self):
+        idx = getattr(self, "_index", None)
+        if idx is not None:  # the index refers to this collection's rows
+            idx.close()
+            self._index = None
         if self._h:
             lib().hsd_collection_destroy(self._h)
             self._h = C.c_void_p()
@@ -407,6 +420,26 @@ class Collection:
                                               _ptr(scores), _ptr(ids), _stream(stream)))
         return scores, ids
 
+    # ---- approximate index (Collection::build_hnsw / search_topk, store.cpp:75-92) ----
+    def build_hnsw(self, nlist: int = 1024, n_iter: int = 10, nprobe: int = 16) -> "Index":
+        """Build the device approximate index (IVF-flat; the stand-in for the
+        reference's HNSW) over the current records; search_topk then uses it
+        until the next insert / generate (which makes it stale: exact again)."""
+        self._index = Index(self, nlist=nlist, n_iter=n_iter)
+        self._nprobe = int(nprobe)
+        return self._index
+
+    def has_hnsw(self) -> bool:
+        idx = getattr(self, "_index", None)
+        return idx is not None and not idx.info()["stale"]
+
+    def search_topk(self, queries, k: int, stream=None):
+        """Collection::search_topk (store.cpp:82-92): the index when built and
+        current, else search_topk_exact."""
+        if not self.has_hnsw():
+            return self.search_topk_exact(queries, k, stream=stream)
+        return self._index.search_topk(queries, k, nprobe=self._nprobe, stream=stream)
+
     def debug_sim_scores(self, queries, variant=1, stream=None):
         """Approximate tcgen05 filter scores float32 [B, size] (diagnostics; variant 1 = wide TF32/bf16
         filter of the default path, 2 = 64-query TF32, 3 = 3xTF32, 4 = the bf16 filter copy)."""
@@ -487,6 +520,62 @@ class Collection:
                                      _stream(stream)))
         o = out.cpu().numpy().view(OUTCOME_DTYPE).reshape(P, E)
         return o, toks
+
+
+class Index:
+    """IVF-flat approximate index over a Collection (hsd_index_*)."""
+
+    def __init__(self, col: "Collection", nlist: int = 1024, n_iter: int = 10):
+        self._col = col
+        h = _vp()
+        p = IvfParams(int(nlist), int(n_iter))
+        check(lib().hsd_index_build(col.handle, C.byref(p), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hsd_index_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        nl, n, ml, st = C.c_int(), C.c_int64(), C.c_int(), C.c_int()
+        check(lib().hsd_index_info(self._h, C.byref(nl), C.byref(n), C.byref(ml), C.byref(st)))
+        return {"nlist": nl.value, "n_rows": n.value, "max_list": ml.value, "stale": bool(st.value)}
+
+    def lists(self):
+        """(offs int32 [nlist+1], perm int32 [n], centroids float32 [nlist, dim]) on the host."""
+        inf = self.info()
+        offs = np.empty(inf["nlist"] + 1, np.int32)
+        perm = np.empty(inf["n_rows"], np.int32)
+        cent = np.empty((inf["nlist"], self._col._dim), np.float32)
+        check(lib().hsd_index_lists(self._h, offs.ctypes.data, perm.ctypes.data, cent.ctypes.data))
+        return offs, perm, cent
+
+    def search_topk(self, queries, k: int, nprobe: int = 16, stream=None, return_probes=False):
+        torch = _torch()
+        q = queries.contiguous()
+        if q.dtype != torch.float32 or not q.is_cuda:
+            raise InvalidInputError("queries must be a CUDA float32 tensor")
+        if q.dim() == 1:
+            q = q[None]
+        if q.shape[1] != self._col._dim:
+            raise InvalidInputError("embedding dim mismatch in cosine")  # store.cpp:30
+        B = q.shape[0]
+        kk = max(int(k), 1)
+        scores = torch.empty((B, kk), dtype=torch.float64, device=q.device)
+        ids = torch.empty((B, kk), dtype=torch.int32, device=q.device)
+        probes = torch.full((B, max(int(nprobe), 1)), -1, dtype=torch.int32, device=q.device) if return_probes else None
+        check(lib().hsd_search_topk_index(self._h, _ptr(q), B, int(k), int(nprobe), _ptr(scores), _ptr(ids),
+                                          _ptr(probes) if probes is not None else None, _stream(stream)))
+        if return_probes:
+            return scores, ids, probes
+        return scores, ids
 
 
 def verify_round_drafts(ids, drafts, logits, params, feat_now=None, feat_prev=None, history=None, gap_d=1,

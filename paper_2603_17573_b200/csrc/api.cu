@@ -137,6 +137,9 @@ struct hsd_collection {
   float* feat = nullptr;
   uint8_t* has_feat = nullptr;
   int d_f = 0;
+  // bumped by every row mutation: an approximate index built at an older
+  // generation is stale (the reference drops its HNSW index on insert)
+  uint64_t gen = 0;
   std::mutex mu;
   std::unordered_map<cudaStream_t, Scratch> scratch;
 };
@@ -562,6 +565,7 @@ hsd_status hsd_collection_insert(hsd_collection* c, const float* emb, const doub
   if (st != HSD_OK) return st;
   CU(cudaDeviceSynchronize());
   c->n += n;
+  ++c->gen;
   return HSD_OK;
 }
 
@@ -629,6 +633,7 @@ hsd_status hsd_collection_generate_ex(hsd_collection* c, int kind, uint64_t db_s
   if (st != HSD_OK) return st;
   CU(cudaDeviceSynchronize());
   c->n += n;
+  ++c->gen;
   return HSD_OK;
 }
 
@@ -2129,6 +2134,273 @@ hsd_status hsd_update_skip_state(hsd_skip_state* s, int success, double S_c, dou
     s->O_dist = s->O_dist - 1 < 1 ? 1 : s->O_dist - 1;
   if (s->min_S < s->T) s->min_S = s->T;
   if (s->min_S > 1.0) s->min_S = 1.0;
+  return HSD_OK;
+}
+
+}  // extern "C"
+
+// ---- approximate index (IVF-flat; k_ivf.cu) ------------------------------------
+// Collection::build_hnsw / search_topk (store.cpp:75-92), SURVEY §8(f) rank 4.
+
+namespace {
+struct IvfScratch {
+  uint64_t* part = nullptr;  // per-unit top-32 lists (coarse and fine passes share it)
+  size_t part_cap = 0;
+  uint64_t* pool = nullptr;  // [kMaxBatchPass][32]
+  int32_t* probe = nullptr;  // [kMaxBatchPass * 32]
+  int32_t* upre = nullptr;   // [kMaxBatchPass * 32 + 1]
+  void* sel = nullptr;       // k_select's per-query scratch
+  int* stats = nullptr;
+};
+}  // namespace
+
+struct hsd_index {
+  hsd_collection* col = nullptr;  // indexed collection (not owned)
+  uint64_t gen = 0;               // the collection's generation at build
+  int64_t n = 0;
+  int nlist = 0, dim = 0, max_list = 0;
+  hsd_collection* cent = nullptr;  // owned: the centroids as an fp32 collection (the build's exact assignment)
+  int32_t* offs = nullptr;
+  int32_t* perm = nullptr;
+  std::mutex mu;
+  std::unordered_map<cudaStream_t, IvfScratch> scratch;
+};
+
+namespace {
+
+void free_ivf_scratch(IvfScratch& s) {
+  cudaFree(s.part);
+  cudaFree(s.pool);
+  cudaFree(s.probe);
+  cudaFree(s.upre);
+  cudaFree(s.sel);
+  cudaFree(s.stats);
+  s = IvfScratch{};
+}
+
+// Rows per scan unit: 128, or 32 when 128-row units would leave SMs idle.
+int ivf_unit_rows(double units128, int nsm) { return units128 >= 2.0 * nsm ? 128 : 32; }
+
+// Exact assignment of every row to its best centroid (score desc, id asc):
+// the collection's own search over the centroid set, rows as queries.
+hsd_status ivf_assign(hsd_collection* c, hsd_collection* cent, float* qtmp, int64_t qtmp_rows, double* sc,
+                      int32_t* assign) {
+  for (int64_t r0 = 0; r0 < c->n; r0 += qtmp_rows) {
+    const int64_t m = std::min(qtmp_rows, c->n - r0);
+    const float* q = nullptr;
+    if (c->dtype == HSD_DTYPE_BF16) {
+      CU(hsd::launch_ivf_widen((const uint16_t*)c->keys + (size_t)r0 * c->dim, m * c->dim, qtmp, 0));
+      q = qtmp;
+    } else {
+      q = (const float*)c->keys + (size_t)r0 * c->dim;
+    }
+    hsd_status st = search_impl(cent, q, (int)m, 1, 0, cent->n, sc, assign + r0, 0);
+    if (st != HSD_OK) return st;
+  }
+  return HSD_OK;
+}
+
+hsd_status ivf_set_centroid_rows(hsd_collection* cent) {
+  CU(cudaMemsetAsync(cent->maxnorm, 0, sizeof(unsigned long long), 0));
+  CU(hsd::launch_row_norms(cent->keys, HSD_DTYPE_F32, 0, cent->n, cent->dim, cent->maxnorm, 0));
+  ++cent->gen;
+  return HSD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hsd_status hsd_index_destroy(hsd_index* x) {
+  if (!x) return HSD_OK;
+  cudaSetDevice(x->col ? x->col->device : 0);
+  for (auto& kv : x->scratch) free_ivf_scratch(kv.second);
+  cudaFree(x->offs);
+  cudaFree(x->perm);
+  hsd_collection_destroy(x->cent);
+  delete x;
+  return HSD_OK;
+}
+
+hsd_status hsd_index_build(hsd_collection* c, const hsd_ivf_params* p, hsd_index** out) {
+  if (!c || !p || !out) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  *out = nullptr;
+  if (c->n == 0) return fail(HSD_ERR_INVALID_INPUT, "cannot index an empty collection");  // store.cpp:76
+  if (p->nlist < 1 || p->nlist > hsd::kIvfMaxLists)
+    return fail(HSD_ERR_CONFIG, "nlist must be in [1, %d], got %d", hsd::kIvfMaxLists, p->nlist);
+  if (p->n_iter < 0 || p->n_iter > 1000) return fail(HSD_ERR_CONFIG, "n_iter must be in [0, 1000], got %d", p->n_iter);
+  if (c->n > INT32_MAX) return fail(HSD_ERR_CONFIG, "the index addresses at most 2^31 - 1 rows");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  auto* x = new hsd_index();
+  x->col = c;
+  x->gen = c->gen;
+  x->n = c->n;
+  x->dim = c->dim;
+  x->nlist = (int)std::min<int64_t>(p->nlist, c->n);
+  const int L = x->nlist, dim = c->dim;
+  const int64_t n = c->n;
+  double* sum = nullptr;
+  double* sc = nullptr;
+  int32_t* assign = nullptr;
+  int32_t* bh = nullptr;
+  float* qtmp = nullptr;
+  int64_t chunk = 0;
+  const int64_t G = hsd::ivf_sort_blocks(n, &chunk);
+  const int64_t qrows = std::min<int64_t>(n, 1 << 16);
+  auto done = [&](hsd_status r) {
+    cudaFree(sum);
+    cudaFree(sc);
+    cudaFree(assign);
+    cudaFree(bh);
+    cudaFree(qtmp);
+    if (r != HSD_OK) hsd_index_destroy(x);
+    return r;
+  };
+#define IVF_CU(expr)                                     \
+  do {                                                   \
+    cudaError_t e_ = (expr);                             \
+    if (e_ != cudaSuccess) return done(cuda_fail(e_, #expr)); \
+  } while (0)
+  st = hsd_collection_create_ex(c->device, dim, L, HSD_DTYPE_F32, &x->cent);
+  if (st != HSD_OK) return done(st);
+  IVF_CU(cudaMalloc(&sum, (size_t)L * dim * sizeof(double)));
+  IVF_CU(cudaMalloc(&sc, (size_t)qrows * sizeof(double)));
+  IVF_CU(cudaMalloc(&assign, (size_t)n * sizeof(int32_t)));
+  IVF_CU(cudaMalloc(&bh, (size_t)G * L * sizeof(int32_t)));
+  IVF_CU(cudaMalloc(&x->offs, (size_t)(L + 1) * sizeof(int32_t)));
+  IVF_CU(cudaMalloc(&x->perm, (size_t)n * sizeof(int32_t)));
+  if (c->dtype == HSD_DTYPE_BF16) IVF_CU(cudaMalloc(&qtmp, (size_t)qrows * dim * sizeof(float)));
+  float* cent = (float*)x->cent->keys;
+  IVF_CU(cudaMemset(cent, 0, (size_t)L * dim * sizeof(float)));
+  x->cent->n = L;
+  // seeds: one row per stratum, normalized
+  IVF_CU(hsd::launch_ivf_seed(c->keys, c->dtype, dim, n, L, sum, 0));
+  IVF_CU(hsd::launch_ivf_centroids(nullptr, c->dtype, dim, L, nullptr, nullptr, sum, cent, 0));
+  st = ivf_set_centroid_rows(x->cent);
+  if (st != HSD_OK) return done(st);
+  for (int it = 0; it <= p->n_iter; ++it) {
+    st = ivf_assign(c, x->cent, qtmp, qrows, sc, assign);
+    if (st != HSD_OK) return done(st);
+    IVF_CU(hsd::launch_ivf_sort(assign, n, L, bh, x->offs, x->perm, 0));
+    if (it == p->n_iter) break;  // the lists match the final centroids
+    IVF_CU(hsd::launch_ivf_centroids(c->keys, c->dtype, dim, L, x->perm, x->offs, sum, cent, 0));
+    st = ivf_set_centroid_rows(x->cent);
+    if (st != HSD_OK) return done(st);
+  }
+  std::vector<int32_t> offs(L + 1);
+  IVF_CU(cudaMemcpy(offs.data(), x->offs, (L + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  for (int l = 0; l < L; ++l) x->max_list = std::max(x->max_list, offs[l + 1] - offs[l]);
+  if (offs[L] != n) return done(fail(HSD_ERR_CUDA, "index build: %d of %lld rows placed", offs[L], (long long)n));
+  IVF_CU(cudaDeviceSynchronize());
+#undef IVF_CU
+  *out = x;
+  return done(HSD_OK);
+}
+
+hsd_status hsd_index_info(const hsd_index* x, int* nlist, int64_t* n_rows, int* max_list, int* stale) {
+  if (!x) return fail(HSD_ERR_INVALID_INPUT, "null index");
+  if (nlist) *nlist = x->nlist;
+  if (n_rows) *n_rows = x->n;
+  if (max_list) *max_list = x->max_list;
+  if (stale) *stale = x->gen != x->col->gen;
+  return HSD_OK;
+}
+
+hsd_status hsd_index_lists(const hsd_index* x, int32_t* offs, int32_t* perm, float* centroids) {
+  if (!x) return fail(HSD_ERR_INVALID_INPUT, "null index");
+  hsd_status st = require_device(x->col->device);
+  if (st != HSD_OK) return st;
+  if (offs) CU(cudaMemcpy(offs, x->offs, (x->nlist + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (perm) CU(cudaMemcpy(perm, x->perm, x->n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (centroids)
+    CU(cudaMemcpy(centroids, x->cent->keys, (size_t)x->nlist * x->dim * sizeof(float), cudaMemcpyDeviceToHost));
+  return HSD_OK;
+}
+
+hsd_status hsd_search_topk_index(hsd_index* x, const float* queries, int B, int k, int nprobe, double* scores,
+                                 int32_t* ids, int32_t* probes, void* stream) {
+  if (!x) return fail(HSD_ERR_INVALID_INPUT, "null index");
+  hsd_collection* c = x->col;
+  cudaStream_t s = (cudaStream_t)stream;
+  // an index older than the rows is dropped, as insert drops the HNSW index
+  // (store.cpp:44-57): search_topk falls back to the exact search (:83)
+  if (x->gen != c->gen) return search_impl(c, queries, B, k, 0, c->n, scores, ids, s);
+  if (k < 1) return fail(HSD_ERR_INVALID_INPUT, "k must be >= 1");  // store.cpp:60
+  if (k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k = %d exceeds HSD_K_MAX = %d", k, HSD_K_MAX);
+  if (nprobe < 1 || nprobe > 32) return fail(HSD_ERR_INVALID_INPUT, "nprobe must be in [1, 32], got %d", nprobe);
+  if (B < 0) return fail(HSD_ERR_INVALID_INPUT, "negative batch");
+  if (B == 0) return HSD_OK;
+  if (!queries || !scores || !ids) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
+  if (reinterpret_cast<uintptr_t>(queries) % 16) return fail(HSD_ERR_INVALID_INPUT, "queries must be 16-byte aligned");
+  hsd_status st = require_device(c->device);
+  if (st != HSD_OK) return st;
+  const int np = std::min(nprobe, x->nlist);
+  const int nsm = num_sms(c->device);
+  const int W = hsd::kMaxBatchPass;
+  const int Bp = std::min(B, W);
+  // rows per unit, coarse and fine, and the unit bounds of one pass
+  const int ur_c = ivf_unit_rows((double)Bp * ((x->nlist + 127) / 128), nsm);
+  const int per_q = (x->nlist + ur_c - 1) / ur_c;
+  const double avg = (double)x->n / x->nlist;
+  const int ur_f = ivf_unit_rows((double)Bp * np * std::ceil(avg / 128.0), nsm);
+  const int64_t fine_max = (int64_t)Bp * np * ((x->max_list + ur_f - 1) / ur_f);
+  const int64_t units_max = std::max<int64_t>((int64_t)Bp * per_q, fine_max);
+  IvfScratch* sc = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(x->mu);
+    sc = &x->scratch[s];
+    if (!sc->pool) {
+      CU(cudaMalloc(&sc->pool, (size_t)W * 32 * sizeof(uint64_t)));
+      CU(cudaMalloc(&sc->probe, (size_t)W * 32 * sizeof(int32_t)));
+      CU(cudaMalloc(&sc->upre, ((size_t)W * 32 + 1) * sizeof(int32_t)));
+      CU(cudaMalloc(&sc->sel, hsd::select_scratch_bytes(W)));
+      CU(cudaMalloc(&sc->stats, 4 * sizeof(int)));
+      CU(cudaMemset(sc->stats, 0, 4 * sizeof(int)));
+    }
+    const size_t need = hsd::ivf_part_bytes(units_max);
+    if (sc->part_cap < need) {
+      cudaFree(sc->part);  // implicit synchronisation: no kernel still reads it
+      sc->part = nullptr;
+      sc->part_cap = 0;
+      CU(cudaMalloc(&sc->part, need));
+      sc->part_cap = need;
+    }
+  }
+  const int grid = nsm * 8;
+  for (int b0 = 0; b0 < B; b0 += W) {
+    const int Bs = std::min(W, B - b0);
+    const float* q = queries + (size_t)b0 * c->dim;
+    hsd::IvfUnits cu{};
+    cu.mode = 0;
+    cu.ur = ur_c;
+    cu.per_q = per_q;
+    cu.n_q = Bs;
+    cu.n_rows = x->nlist;
+    CU(hsd::launch_ivf_scan(x->cent->keys, 0, x->dim, nullptr, x->dim, q, cu, (int64_t)Bs * per_q, grid, sc->part, s));
+    CU(hsd::launch_ivf_merge(sc->part, cu, Bs, sc->pool, s));
+    CU(hsd::launch_ivf_probe(sc->pool, Bs, np, x->offs, ur_f, sc->probe, sc->upre, s));
+    if (probes) {
+      CU(cudaMemcpy2DAsync(probes + (size_t)b0 * nprobe, nprobe * sizeof(int32_t), sc->probe, np * sizeof(int32_t),
+                           np * sizeof(int32_t), Bs, cudaMemcpyDeviceToDevice, s));
+    }
+    hsd::IvfUnits fu{};
+    fu.mode = 1;
+    fu.ur = ur_f;
+    fu.n_pairs = Bs * np;
+    fu.nprobe = np;
+    fu.upre = sc->upre;
+    fu.probe = sc->probe;
+    fu.offs = x->offs;
+    const int64_t fmax = (int64_t)Bs * np * ((x->max_list + ur_f - 1) / ur_f);
+    // the fine scan streams the filter copy when the collection keeps one (half the bytes)
+    const void* frows = c->shadow ? (const void*)c->shadow : c->keys;
+    const int fbf16 = c->shadow || c->dtype == HSD_DTYPE_BF16;
+    CU(hsd::launch_ivf_scan(frows, fbf16, x->dim, x->perm, x->dim, q, fu, fmax, grid, sc->part, s));
+    CU(hsd::launch_ivf_merge(sc->part, fu, Bs, sc->pool, s));
+    CU(hsd::launch_rescore_pool(sc->pool, 32, Bs, k, c->keys, c->dtype, c->dim, q, scores + (size_t)b0 * k,
+                                ids + (size_t)b0 * k, sc->stats, sc->sel, s));
+  }
   return HSD_OK;
 }
 

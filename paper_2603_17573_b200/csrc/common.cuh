@@ -113,6 +113,14 @@ __device__ __forceinline__ float4 ldg_stream(const float4* p) {
   return r;
 }
 
+__device__ __forceinline__ uint4 ldg_stream_u4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 // Knuth TwoSum (error-free transformation).
 __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
   s = __dadd_rn(a, b);

@@ -670,6 +670,52 @@ cudaError_t select_typed(const uint64_t* partial, int lists, int B, int k, const
   return launch_pdl(rank_kernel, dim3(B), dim3(kThreads), 0, s, scr, k, scores, ids, stats, pb, pub ? 1 : 0);
 }
 
+// Pooled candidates from an external filter (the IVF index, k_ivf.cu): one
+// CTA per query copies the valid entries of pool[b][0..C) (u64 candidate
+// keys: the filter's approximate order, global row ids) into the per-query
+// scratch the rescoring and rank kernels read; no fallback lists.
+__global__ void __launch_bounds__(kThreads) pool_kernel(const uint64_t* __restrict__ pool, int C,
+                                                        SelScratch* __restrict__ scr) {
+  __shared__ int n;
+  dev::pdl_wait();
+  dev::pdl_trigger();
+  const int b = blockIdx.x, tid = threadIdx.x;
+  SelScratch& o = scr[b];
+  if (tid == 0) n = 0;
+  __syncthreads();
+  for (int i = tid; i < C; i += kThreads) {
+    const uint64_t key = pool[(size_t)b * C + i];
+    if (key != kEmpty) o.id[atomicAdd(&n, 1)] = cand_id(key);
+  }
+  if (tid < dev::kCandLocal) {
+    o.fb_key[tid] = kEmpty;
+    o.fb_id[tid] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    o.n = n;
+    o.n_fb = 0;
+    o.lock = 0;
+  }
+}
+
+template <typename KT>
+cudaError_t rescore_pool_typed(const uint64_t* pool, int C, int B, int k, const KT* keys, int dim,
+                               const float* queries, double* scores, int32_t* ids, int* stats, SelScratch* scr,
+                               cudaStream_t s) {
+  cudaError_t e = launch_pdl(pool_kernel, dim3(B), dim3(kThreads), 0, s, pool, C, scr);
+  if (e != cudaSuccess) return e;
+  const size_t smem = rescore_smem<KT, kPerNarrow>();
+  e = cudaFuncSetAttribute(rescore_kernel<KT, kPerNarrow>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  // C <= 32 candidates per query: (C / 8) CTAs of 8 chains each
+  e = launch_pdl(rescore_kernel<KT, kPerNarrow>, dim3(B, (C + kPerNarrow - 1) / kPerNarrow), dim3(kRThreads), smem, s,
+                 keys, dim, queries, scr);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(rank_kernel, dim3(B), dim3(kThreads), 0, s, (const SelScratch*)scr, k, scores, ids, stats,
+                    P2PPublish{}, 0);
+}
+
 }  // namespace
 
 size_t select_scratch_bytes(int B) { return (size_t)B * sizeof(SelScratch); }
@@ -689,6 +735,18 @@ cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, cons
                         ids, stats, scr, fb_grid, s, pub);
   return select_typed(partial, lists, B, k, (const float*)keys, dim, queries, maxnorm_bits, gamma, geom, scores, ids,
                       stats, scr, fb_grid, s, pub);
+}
+
+cudaError_t launch_rescore_pool(const uint64_t* pool, int C, int B, int k, const void* keys, int key_dtype, int dim,
+                                const float* queries, double* scores, int32_t* ids, int* stats, void* scratch,
+                                cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  if (B > kMaxBatchPass || C < 1 || C > dev::kCandLocal || k > dev::kCandLocal) return cudaErrorInvalidValue;
+  if (key_dtype == HSD_DTYPE_BF16 && dim % 8) return cudaErrorInvalidValue;
+  SelScratch* scr = reinterpret_cast<SelScratch*>(scratch);
+  if (key_dtype == HSD_DTYPE_BF16)
+    return rescore_pool_typed(pool, C, B, k, (const uint16_t*)keys, dim, queries, scores, ids, stats, scr, s);
+  return rescore_pool_typed(pool, C, B, k, (const float*)keys, dim, queries, scores, ids, stats, scr, s);
 }
 
 cudaError_t launch_merge_ranks(const double* g_scores, const int32_t* g_ids, const uint8_t* g_tok, int G, int B, int k,

@@ -82,6 +82,13 @@ cudaError_t launch_select(const uint64_t* partial, int lists, int B, int k, cons
                           const ListGeom& geom, double* scores, int32_t* ids, int* stats, void* scratch, int num_sms,
                           cudaStream_t s, const P2PPublish* pub = nullptr);
 
+// Exact rescoring + rank of externally pooled candidates (the IVF index):
+// pool [B][C] u64 candidate keys (kEmpty = none, ids = rows of `keys`),
+// C <= 32; scratch: select_scratch_bytes(B), B <= kMaxBatchPass.
+cudaError_t launch_rescore_pool(const uint64_t* pool, int C, int B, int k, const void* keys, int key_dtype, int dim,
+                                const float* queries, double* scores, int32_t* ids, int* stats, void* scratch,
+                                cudaStream_t s);
+
 // K3 merge of G gathered per-rank top-k records (sharded search); tokens
 // [G][B][k][32] are permuted alongside when non-null.
 cudaError_t launch_merge_ranks(const double* g_scores, const int32_t* g_ids, const uint8_t* g_tok, int G, int B, int k,
@@ -114,6 +121,39 @@ cudaError_t launch_p2p_publish(const P2PWindows& w, int rank, int G, int B, int 
 cudaError_t launch_p2p_merge(const P2PWindows& w, int rank, int G, int B, int k, uint64_t epoch, double* scores,
                              int32_t* ids, uint8_t* tok, int* err, cudaStream_t s);
 
+// ---- approximate index: IVF-flat (k_ivf.cu; host side in api.cu) ---------------
+// Scan units: mode 0 (coarse) unit u = (query u / per_q, rows [(u % per_q) ur, +ur)
+// of [0, n_rows)); mode 1 (fine) pairs p = b * nprobe + j own units
+// [upre[p], upre[p + 1]), chunks of ur rows of list probe[p] = [offs[l], offs[l+1]).
+struct IvfUnits {
+  int mode;
+  int ur;  // rows per unit: 32 or 128
+  int per_q, n_q;
+  int64_t n_rows;
+  int n_pairs, nprobe;
+  const int32_t* upre;
+  const int32_t* probe;
+  const int32_t* offs;
+};
+constexpr int kIvfMaxLists = 16384;
+size_t ivf_part_bytes(int64_t units);
+// per-unit top-32 (u64 candidate keys; ids = row_id[pos] or pos) of bf16 (rows_bf16) or fp32 rows
+cudaError_t launch_ivf_scan(const void* rows, int rows_bf16, int64_t stride, const int32_t* row_id, int dim,
+                            const float* queries, const IvfUnits& su, int64_t max_units, int grid, uint64_t* part,
+                            cudaStream_t s);
+cudaError_t launch_ivf_merge(const uint64_t* part, const IvfUnits& su, int B, uint64_t* pool, cudaStream_t s);
+cudaError_t launch_ivf_probe(const uint64_t* pool, int B, int nprobe, const int32_t* offs, int ur, int32_t* probe,
+                             int32_t* upre, cudaStream_t s);
+// build: seeds (sum <- seed rows), centroids (sum <- list sums when perm; cent <- sum / |sum|)
+cudaError_t launch_ivf_seed(const void* keys, int key_dtype, int dim, int64_t n, int nlist, double* sum,
+                            cudaStream_t s);
+cudaError_t launch_ivf_centroids(const void* keys, int key_dtype, int dim, int nlist, const int32_t* perm,
+                                 const int32_t* offs, double* sum, float* cent, cudaStream_t s);
+cudaError_t launch_ivf_widen(const uint16_t* in, int64_t n, float* out, cudaStream_t s);
+// stable counting sort of rows by list: bh scratch [ivf_sort_blocks(n)][nlist]
+int64_t ivf_sort_blocks(int64_t n, int64_t* chunk);
+cudaError_t launch_ivf_sort(const int32_t* assign, int64_t n, int nlist, int32_t* bh, int32_t* offs, int32_t* perm,
+                            cudaStream_t s);
 // ---- K4 gather + verify-skip + relaxed acceptance ----------------------------
 // Draft tokens come from the collection's table by id, or pre-gathered
 // cand_tokens [E][k][32] when non-null (sharded search records).

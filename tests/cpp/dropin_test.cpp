@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <random>
 #include <vector>
 
@@ -85,6 +86,48 @@ int main() {
   hsd::gpu::Collection empty("e", dim);
   CHECK(empty.search_topk_exact(queries[0], 5).empty(), "empty collection -> empty result");
   CHECK(throws<hsd::ConfigError>([&] { hsd::gpu::Collection bad("b", 0); }), "dim 0 -> ConfigError");
+
+  // ---- approximate index: build_hnsw / has_hnsw / search_topk (store.cpp:75-92)
+  {
+    hsd::HnswParams hp;  // m 16, ef_construct 100, ef_search 100
+    ref.build_hnsw(hp);
+    gpu.build_hnsw(hp);
+    CHECK(gpu.has_hnsw(), "has_hnsw after build");
+    int common = 0, total = 0;
+    for (int b = 0; b < B; ++b) {
+      auto got = gpu.search_topk(queries[(size_t)b], k);
+      auto hn = ref.search_topk(queries[(size_t)b], k);  // the reference's HNSW
+      auto ex = ref.search_topk_exact(queries[(size_t)b], k);
+      CHECK(!got.empty() && got.size() <= (size_t)k, "index hit count q=%d", b);
+      for (size_t i = 0; i < got.size(); ++i) {
+        // every score is the reference's cosine_similarity of the returned id (store.cpp:86-90)
+        const double want = hsd::cosine_similarity(queries[(size_t)b], ref.record(got[i].record_id).embedding);
+        CHECK(std::memcmp(&got[i].score, &want, sizeof(double)) == 0, "index score bits q=%d rank=%zu", b, i);
+        CHECK(got[i].payload == ref.record(got[i].record_id).payload, "index payload q=%d", b);
+        if (i) CHECK(got[i - 1].score > got[i].score || (got[i - 1].score == got[i].score &&
+                                                          got[i - 1].record_id < got[i].record_id),
+                     "index order q=%d rank=%zu", b, i);
+      }
+      // near-duplicate queries (the first half of a REAL batch) find their row at rank 0, as HNSW does
+      if (hsd_query_row(78, HSD_SYNTH_REAL, b, n) >= 0) {
+        CHECK(got[0].record_id == ex[0].record_id, "index top-1 q=%d", b);
+        CHECK(hn.empty() || hn[0].record_id == ex[0].record_id, "reference hnsw top-1 q=%d", b);
+      }
+      for (const auto& h : got)
+        for (const auto& e : ex) common += h.record_id == e.record_id;
+      total += (int)ex.size();
+    }
+    std::printf("index recall@%d vs exact: %.3f\n", k, (double)common / total);
+    CHECK(gpu.search_topk(queries[0], 0).empty(), "index k = 0 -> no hits (hnsw.cpp:160)");
+    hsd::Payload p;
+    gpu.insert(queries[0], p);  // mutation drops the index (store.cpp:55)
+    CHECK(!gpu.has_hnsw(), "insert drops the index");
+    auto after = gpu.search_topk(queries[1], k);
+    auto exact = gpu.search_topk_exact(queries[1], k);
+    CHECK(after.size() == exact.size() && after[0].record_id == exact[0].record_id, "no index -> exact search");
+    hsd::gpu::Collection e2("e2", dim);
+    CHECK(throws<hsd::InvalidInputError>([&] { e2.build_hnsw(hp); }), "empty collection -> InvalidInputError");
+  }
 
   // ---- any dim: rows zero-padded to a multiple of 8 on the device, scores unchanged bit for bit
   for (int odd : {1, 3, 61, 130}) {
