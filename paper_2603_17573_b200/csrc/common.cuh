@@ -136,26 +136,19 @@ __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e
 // NaN in bin 0 is never replaced (every comparison with it is false).
 __device__ __forceinline__ int warp_argmax256(const float4& a, const float4& c, int lane) {
   const float v[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-  constexpr int kNone = 0x7fffffff;
-  float best = -INFINITY;
-  int bi = kNone;  // no non-NaN value seen yet
+  // the largest non-NaN value (fmaxf drops a NaN operand; NaN only if all are)
+  float m = fmaxf(fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3])), fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7])));
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if (v[i] > best || (bi == kNone && v[i] == v[i])) {
-      best = v[i];
-      bi = lane * 8 + i;
-    }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  // the lowest bin holding it (-0.0 == +0.0, as the sequential > scan sees them)
+  int first = 8;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ob > best || (ob == best && oi < bi)) {
-      best = ob;
-      bi = oi;
-    }
-  }
+  for (int i = 7; i >= 0; --i) first = v[i] == m ? i : first;
+  const unsigned hit = __ballot_sync(0xffffffffu, first < 8);
+  const int src = hit ? __ffs(hit) - 1 : 0;
+  const int fi = __shfl_sync(0xffffffffu, first, src);
   const float v0 = __shfl_sync(0xffffffffu, a.x, 0);
-  return (v0 != v0 || bi == kNone) ? 0 : bi;
+  return (v0 != v0 || hit == 0) ? 0 : src * 8 + fi;
 }
 
 // should_skip's similarity over one warp: the double-double sum of the exact

@@ -56,15 +56,191 @@ struct WarpScratch {
   int greedy[32];
   uint8_t pair[kPairs];  // per (set, candidate): rest | pos0-accepted << 7
   int8_t len[kPairs], bb[kPairs];
-  int canA[HSD_K_MAX], canB[HSD_K_MAX];
   int rankA[HSD_K_MAX], rankB[HSD_K_MAX];
 };
 
+// verify-skip similarity of one episode on one warp: exactly rounded dot
+// (double-double; the result is the exact sum rounded once, so the order is
+// free).  kFeatUnroll float4 pairs per lane are requested (volatile loads,
+// all issued) before any is accumulated.
+__device__ __forceinline__ double episode_cos(const float* fnE, const float* fpE, int d_f, int lane) {
+  const float4* a4 = reinterpret_cast<const float4*>(fnE);
+  const float4* b4 = reinterpret_cast<const float4*>(fpE);
+  const int n4 = d_f / 4;
+  // two independent double-double accumulators (x / z and y / w components)
+  double hv[2] = {0.0, 0.0}, lv[2] = {0.0, 0.0};
+  for (int t0 = lane; t0 < n4; t0 += 32 * kFeatUnroll) {
+    float4 xa[kFeatUnroll], yb[kFeatUnroll];
+#pragma unroll
+    for (int u = 0; u < kFeatUnroll; ++u) {
+      const int t = min(t0 + 32 * u, n4 - 1);
+      xa[u] = dev::ldg_stream(a4 + t);
+      yb[u] = dev::ldg_stream(b4 + t);
+    }
+#pragma unroll
+    for (int u = 0; u < kFeatUnroll; ++u) {
+      if (t0 + 32 * u >= n4) {
+        xa[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        yb[u] = xa[u];
+      }
+      const double pr[4] = {(double)xa[u].x * (double)yb[u].x, (double)xa[u].y * (double)yb[u].y,
+                            (double)xa[u].z * (double)yb[u].z, (double)xa[u].w * (double)yb[u].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double s, er;
+        dev::two_sum(hv[i & 1], pr[i], s, er);
+        hv[i & 1] = s;
+        lv[i & 1] = __dadd_rn(lv[i & 1], er);
+      }
+    }
+  }
+  double hi = hv[0], lo = lv[0];
+  {
+    double s, er;
+    dev::two_sum(hi, hv[1], s, er);
+    hi = s;
+    lo = __dadd_rn(__dadd_rn(lo, lv[1]), er);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+    const double olo = __shfl_xor_sync(0xffffffffu, lo, o);
+    double s, er;
+    dev::two_sum(hi, ohi, s, er);
+    hi = s;
+    lo = __dadd_rn(__dadd_rn(lo, olo), er);
+  }
+  double s, er;
+  dev::two_sum(hi, lo, s, er);
+  return s;
+}
+
+// The same similarity, fast: plain fp64 sums (every fp32 x fp32 product is
+// exact in fp64; two FMA chains per lane, then the butterfly) plus a
+// rigorous bound on their error, from an fp32 sum of |products|.  Whenever
+// the bound cannot settle the result — the float cos_sim output or any
+// enabled set's `cos >= min_S` decision could differ from the exactly
+// rounded similarity's — the exact double-double pass (episode_cos) decides
+// instead.  The returned value is then only used through those two, so it is
+// interchangeable with the exact one.  Half the fp64 instructions of the
+// double-double loop on the common path.
+__device__ __forceinline__ void cos_accum(const float4 (&xa)[kFeatUnroll], const float4 (&yb)[kFeatUnroll],
+                                          double& s0, double& s1, float& ab) {
+#pragma unroll
+  for (int u = 0; u < kFeatUnroll; ++u) {
+    s0 = fma((double)xa[u].x, (double)yb[u].x, s0);
+    s1 = fma((double)xa[u].y, (double)yb[u].y, s1);
+    s0 = fma((double)xa[u].z, (double)yb[u].z, s0);
+    s1 = fma((double)xa[u].w, (double)yb[u].w, s1);
+    ab = fmaf(fabsf(xa[u].x), fabsf(yb[u].x), ab);
+    ab = fmaf(fabsf(xa[u].y), fabsf(yb[u].y), ab);
+    ab = fmaf(fabsf(xa[u].z), fabsf(yb[u].z), ab);
+    ab = fmaf(fabsf(xa[u].w), fabsf(yb[u].w), ab);
+  }
+}
+
+// Chunk c of a lane's feature elements: float4 index c * 32U + 32u + lane
+// (volatile loads: every load of the chunk is issued before any is used).
+__device__ __forceinline__ void cos_load_regs(const float4* a4, const float4* b4, int n4, int c, int lane,
+                                              float4 (&xa)[kFeatUnroll], float4 (&yb)[kFeatUnroll]) {
+#pragma unroll
+  for (int u = 0; u < kFeatUnroll; ++u) {
+    const int t = min(c * 32 * kFeatUnroll + 32 * u + lane, n4 - 1);
+    xa[u] = dev::ldg_stream(a4 + t);
+    yb[u] = dev::ldg_stream(b4 + t);
+  }
+#pragma unroll
+  for (int u = 0; u < kFeatUnroll; ++u)
+    if (c * 32 * kFeatUnroll + 32 * u + lane >= n4) {
+      xa[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      yb[u] = xa[u];
+    }
+}
+
+__device__ __forceinline__ double episode_cos_fast(const float* fnE, const float* fpE, int d_f, int lane,
+                                                   const hsd_verify_params* __restrict__ params, int P) {
+  const float4* a4 = reinterpret_cast<const float4*>(fnE);
+  const float4* b4 = reinterpret_cast<const float4*>(fpE);
+  const int n4 = d_f / 4;
+  const int nch = (n4 + 32 * kFeatUnroll - 1) / (32 * kFeatUnroll);
+  double s0 = 0.0, s1 = 0.0;
+  float ab = 0.f;
+  for (int c = 0; c < nch; ++c) {
+    float4 xa[kFeatUnroll], yb[kFeatUnroll];
+    cos_load_regs(a4, b4, n4, c, lane, xa, yb);
+    cos_accum(xa, yb, s0, s1, ab);
+  }
+  double sv = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {  // butterfly: every lane ends with the same bits
+    sv += __shfl_xor_sync(0xffffffffu, sv, o);
+    ab += __shfl_xor_sync(0xffffffffu, ab, o);
+  }
+  // A term passes through <= d_f / 32 + 8 roundings (its chain, the join, 5
+  // butterfly levels): |sv - S| <= m u sum|p| (1 + O(mu)).  The fp32 sum of
+  // |p| (m_f roundings, every term rounded at most once more) is a lower
+  // estimate within m_f 2^-24; fp32 underflow loses < 2^-149 per term.
+  const double m = (double)(d_f / 32 + 8);
+  const double abs_sum = (double)ab * (1.0 + (m + 2.0) * 0x1p-23) + (double)d_f * 0x1p-148;
+  const double err = abs_sum * m * 0x1p-53 * (1.0 + 0x1p-30) + (double)d_f * 0x1p-1074;
+  const double e2 = err * (1.0 + 0x1p-50) + fabs(sv) * 0x1p-51;  // + the final rounding of the exact value
+  bool amb = !isfinite(sv) || !isfinite(e2) || (float)(sv - e2) != (float)(sv + e2);
+  for (int p = 0; p < P; ++p)
+    if (params[p].skip_enabled) amb |= fabs(sv - params[p].min_S) <= e2 + fabs(params[p].min_S) * 0x1p-51;
+  return amb ? episode_cos(fnE, fpE, d_f, lane) : sv;
+}
+
+// Candidate dedup (chain language): lane c < n_cand gets the
+// first candidate with its pos0 group (bytes 0-2) and the first with its
+// later groups (bytes 3..L-1).  Token rows live in registers (NW words) and
+// are compared through shuffles, all lanes in step.
+template <int NW>
+__device__ __forceinline__ void dedup_rows(const WarpScratch& W, int n_cand, int L, int lane, int& ca, int& cb) {
+  uint32_t w[NW], mk[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    w[i] = lane < n_cand ? reinterpret_cast<const uint32_t*>(W.tok[lane])[i] : 0u;
+    uint32_t m = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int t = 4 * i + b;
+      if (t >= 3 && t < L) m |= 0xFFu << (8 * b);
+    }
+    mk[i] = m;
+  }
+  ca = lane;
+  cb = lane;
+  for (int c = 0; c < n_cand; ++c) {
+    uint32_t dA = 0, dB = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const uint32_t x = __shfl_sync(0xffffffffu, w[i], c) ^ w[i];
+      if (i == 0) dA = x & 0xFFFFFFu;
+      dB |= x & mk[i];
+    }
+    if (c < lane) {
+      if (ca == lane && dA == 0) ca = c;
+      if (cb == lane && dB == 0) cb = c;
+    }
+  }
+}
+
 // One episode's decode round on one warp.  lgE: its logits [L][256]; fnE /
-// fpE: its features [d_f] (or null).  (A persistent variant streaming the next
-// episode into shared memory with bulk copies measured 3.7x slower at C3: with
-// 2 warps per SM the short dependent global reads of ids / tokens / params are
-// no longer hidden; one warp per episode at full occupancy is faster.)
+// fpE: its features [d_f] (or null).
+//
+// Phase order.  C3's 4096 episodes fit in one wave of warps (32 per SM), so
+// the kernel lasts as long as one warp's whole round.  The two halves of the
+// round — streaming the 32-KB feature pair (HBM-bound) and the logits +
+// dedup + acceptance sweep (latency-bound, little traffic) — are independent
+// until the outcome step needs the similarity.  Even warps stream their
+// features first, odd warps last, so on every SM half the warps keep HBM busy
+// while the other half run their sweeps, instead of every warp reaching the
+// feature phase at the same time.  (A persistent variant streaming the next
+// episode into shared memory with bulk copies measured 3.7x slower: with 2
+// warps per SM the short dependent global reads of ids / tokens / params are
+// no longer hidden.  One CTA of 4 warps per episode with every load issued up
+// front measured 1.7x slower: its 128 registers left 4 episodes per SM, each
+// serialising its sweep on one warp.)
 __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const int32_t* __restrict__ ids,
                                                const uint8_t* __restrict__ tokens,
                                                const uint8_t* __restrict__ cand_tokens, const float* lgE,
@@ -74,126 +250,67 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
                                                const double* __restrict__ cos_in, hsd_outcome* __restrict__ out,
                                                uint8_t* __restrict__ tok_out, WarpScratch& W) {
   const int lane = threadIdx.x & 31;
+  const bool feat_first = ((threadIdx.x >> 5) & 1) == 0;
+  const bool own_cos = need_cos && !cos_in && fnE && fpE;
   // The candidate ids (and then their token rows) do not depend on the logits
   // or the features: issue them first so their round trips overlap the
   // logits / feature phases instead of following them.
   const int32_t* my_ids = ids + (size_t)e * k;
   const int id = lane < k ? my_ids[lane] : -1;
-  // ---- greedy tokens: argmax per position, lowest index on ties.  The 7
-  //      positions of an action slice are loaded before any is reduced (7 KB
-  //      in flight per warp) — the kernel is HBM-bound at C3's 4096 episodes.
-  const float4* lg = reinterpret_cast<const float4*>(lgE);
-  for (int p0 = 0; p0 < L; p0 += 7) {
-    float4 a[7], c[7];
-#pragma unroll
-    for (int u = 0; u < 7; ++u) {
-      a[u] = lg[(p0 + u) * 64 + lane * 2];
-      c[u] = lg[(p0 + u) * 64 + lane * 2 + 1];
-    }
-#pragma unroll
-    for (int u = 0; u < 7; ++u) {
-      const int bi = dev::warp_argmax256(a[u], c[u], lane);
-      if (lane == 0) W.greedy[p0 + u] = bi;
-    }
-  }
-
-  // ---- the candidates' draft tokens: cp.async into this warp's staging rows
-  //      (completes under the feature stream; waited for before the dedup)
-  if (id >= 0) {
-    const uint8_t* row = cand_tokens ? cand_tokens + ((size_t)e * k + lane) * HSD_TOKENS_STRIDE
-                                     : tokens + (size_t)id * HSD_TOKENS_STRIDE;
-#pragma unroll
-    for (int i = 0; i < kTokStride / 4; ++i) {
-      const uint32_t d = (uint32_t)__cvta_generic_to_shared(&W.tok[lane][4 * i]);
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(row + 4 * i) : "memory");
-    }
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-
-  // ---- verify-skip similarity: exactly rounded dot (double-double; the
-  //      result is the exact sum rounded once, so the order is free and
-  //      kFeatUnroll float4 pairs per lane are loaded before they are accumulated)
   double cosv = -2.0;
-  if (need_cos && cos_in) {
-    cosv = cos_in[e];  // computed by cos_kernel (off the critical path in the engine step)
-  } else if (need_cos && fnE && fpE) {
-    const float4* a4 = reinterpret_cast<const float4*>(fnE);
-    const float4* b4 = reinterpret_cast<const float4*>(fpE);
-    const int n4 = d_f / 4;
-    // four independent double-double accumulators (one per float4 component)
-    // keep four dependent chains in flight instead of one
-    double hv[4] = {0.0, 0.0, 0.0, 0.0}, lv[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int t0 = lane; t0 < n4; t0 += 32 * kFeatUnroll) {
-      float4 xa[kFeatUnroll], yb[kFeatUnroll];
+  if (need_cos && cos_in) cosv = cos_in[e];  // cos_kernel's pass (off the critical path in the engine step)
+  // ---- the candidates' draft tokens: cp.async into this warp's staging rows
+  //      (waited for before the dedup)
+  auto stage_tokens = [&]() {
+    if (id >= 0) {
+      const uint8_t* row = cand_tokens ? cand_tokens + ((size_t)e * k + lane) * HSD_TOKENS_STRIDE
+                                       : tokens + (size_t)id * HSD_TOKENS_STRIDE;
 #pragma unroll
-      for (int u = 0; u < kFeatUnroll; ++u) {
-        const int t = t0 + 32 * u;
-        xa[u] = t < n4 ? a4[t] : make_float4(0.f, 0.f, 0.f, 0.f);
-        yb[u] = t < n4 ? b4[t] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < kFeatUnroll; ++u) {
-        const double pr[4] = {(double)xa[u].x * (double)yb[u].x, (double)xa[u].y * (double)yb[u].y,
-                              (double)xa[u].z * (double)yb[u].z, (double)xa[u].w * (double)yb[u].w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          double s, er;
-          dev::two_sum(hv[i], pr[i], s, er);
-          hv[i] = s;
-          lv[i] = __dadd_rn(lv[i], er);
-        }
+      for (int i = 0; i < kTokStride / 4; ++i) {
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(&W.tok[lane][4 * i]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(row + 4 * i) : "memory");
       }
     }
-    double hi = hv[0], lo = lv[0];
-#pragma unroll
-    for (int i = 1; i < 4; ++i) {
-      double s, er;
-      dev::two_sum(hi, hv[i], s, er);
-      hi = s;
-      lo = __dadd_rn(__dadd_rn(lo, lv[i]), er);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // Two phases in parity order (see above): the feature stream, and the
+  // logits + token gather + dedup.  One code site each.
+  int n_cand = 0, nA = 0, nB = 0;
+  for (int ph = 0; ph < 2; ++ph) {
+    if ((ph == 0) == feat_first) {
+      if (ph == 0) stage_tokens();  // even warps: the token rows land under the feature stream
+      if (own_cos) cosv = episode_cos_fast(fnE, fpE, d_f, lane, params, P);
+      continue;
     }
+    // ---- greedy tokens: argmax per position, lowest index on ties.  Four
+    //      positions are loaded before any is reduced (4 KB in flight per warp).
+    const float4* lg = reinterpret_cast<const float4*>(lgE);
+    for (int p0 = 0; p0 < L; p0 += 4) {
+      float4 a[4], c[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ohi = __shfl_xor_sync(0xffffffffu, hi, o);
-      const double olo = __shfl_xor_sync(0xffffffffu, lo, o);
-      double s, er;
-      dev::two_sum(hi, ohi, s, er);
-      hi = s;
-      lo = __dadd_rn(__dadd_rn(lo, olo), er);
-    }
-    double s, er;
-    dev::two_sum(hi, lo, s, er);
-    cosv = s;
-  }
-
-  // ---- the gathered draft tokens have landed
-  const int n_cand = __popc(__ballot_sync(0xffffffffu, id >= 0));  // ids are rank-ordered, -1 padding last
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-  const int* greedy = W.greedy;  // positions < L (shared memory, no per-thread copy)
-  const int hist = history ? history[e] : 0x7fffffff;
-
-  // ---- candidate dedup (chain language) — independent of params
-  if (lane < n_cand) {
-    const uint8_t* me = W.tok[lane];
-    int ca = lane, cb = lane;
-    for (int c = 0; c < lane; ++c) {
-      const uint8_t* o = W.tok[c];
-      if (ca == lane && o[0] == me[0] && o[1] == me[1] && o[2] == me[2]) ca = c;
-      if (cb == lane) {
-        bool same = true;
-        for (int t = 3; t < L; ++t) same &= (o[t] == me[t]);
-        if (same) cb = c;
+      for (int u = 0; u < 4; ++u) {
+        const int p = min(p0 + u, L - 1);
+        a[u] = lg[p * 64 + lane * 2];
+        c[u] = lg[p * 64 + lane * 2 + 1];
+      }
+      if (ph == 0 && p0 == 0) stage_tokens();  // odd warps: the id has arrived under the logit loads
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int bi = dev::warp_argmax256(a[u], c[u], lane);
+        if (lane == 0 && p0 + u < L) W.greedy[p0 + u] = bi;
       }
     }
-    W.canA[lane] = ca;
-    W.canB[lane] = cb;
-  }
-  __syncwarp();
-  int nA = 0, nB = 0;
-  {
-    const bool isA = lane < n_cand && W.canA[lane] == lane;
-    const bool isB = lane < n_cand && W.canB[lane] == lane;
+    // ---- the gathered draft tokens have landed: dedup (independent of params)
+    n_cand = __popc(__ballot_sync(0xffffffffu, id >= 0));  // ids are rank-ordered, -1 padding last
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    int ca, cb;
+    if (L <= 8)
+      dedup_rows<2>(W, n_cand, L, lane, ca, cb);
+    else
+      dedup_rows<6>(W, n_cand, L, lane, ca, cb);
+    const bool isA = lane < n_cand && ca == lane;
+    const bool isB = lane < n_cand && cb == lane;
     const unsigned mA = __ballot_sync(0xffffffffu, isA), mB = __ballot_sync(0xffffffffu, isB);
     nA = __popc(mA);
     nB = __popc(mB);
@@ -201,8 +318,10 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
       W.rankA[lane] = isA ? __popc(mA & ((1u << lane) - 1)) : -1;
       W.rankB[lane] = isB ? __popc(mB & ((1u << lane) - 1)) : -1;
     }
+    __syncwarp();
   }
-  __syncwarp();
+  const int* greedy = W.greedy;  // positions < L (shared memory, no per-thread copy)
+  const int hist = history ? history[e] : 0x7fffffff;
 
   // ---- per parameter set (a tolerance / threshold sweep): lane-parallel over
   //      (set, candidate) pairs, processed in chunks of kPairs pairs.
