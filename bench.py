@@ -18,15 +18,15 @@ fp32 keys (16.4 GB resident in HBM), batch 64 queries, k = 8, draft length 7,
   cpu_baseline  the reference's own search (oracle/_ref, store.cpp compiled
              in place) + oracle port of verify/kinematics on the host cores
 
---gpus N (torchrun), --shard episodes (default): every GPU holds the 1M DB
-(+ its bf16 filter copy) and runs its own batches of independent episodes —
-the episodes are the independent units, so there is no collective on the data
-path (weak scaling; value = all ranks' steps / the slowest rank's time).
---shard db: the 1M DB is row-sharded over N GPUs (strong scaling); each pass
-searches all 64 queries on every shard, exchanges the B x k draft records with
-an NCCL all-gather and merges them; verification of the 64 episodes is split
-across ranks (the path C4 / C5 use for DBs that do not fit one GPU).
-
+--gpus N (torchrun), --shard db (default for N > 1, the north-star path): the
+1M DB is row-sharded over N GPUs (strong scaling); each pass searches all 64
+queries on every shard, exchanges the B x k draft records (peer memory, or an
+NCCL all-gather with --exchange nccl) and merges them; verification of the 64
+episodes is split across ranks (the path C4 / C5 use for DBs that do not fit
+one GPU).
+--shard episodes: every GPU holds the 1M DB (+ its bf16 filter copy) and runs
+its own batches of independent episodes — no collective on the data path (weak
+scaling; value = all ranks' steps / the slowest rank's time).
 --impl reference: the reference CPU path alone (see cpu_reference_step).
 
 --config selects the workload (default c2, the BASELINE.json headline):
