@@ -276,6 +276,14 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
   // Two phases in parity order (see above): the feature stream, and the
   // logits + token gather + dedup.  One code site each.
   int n_cand = 0, nA = 0, nB = 0;
+  // odd warps run the sweep before their features: skip decisions are deferred
+  const bool defer = own_cos && !feat_first;
+  const int hist = history ? history[e] : 0x7fffffff;
+  const int hist_ok = gap_d >= 1 && hist >= gap_d;
+  auto skip_cond = [&](const hsd_verify_params& pp) {  // should_skip without the similarity test
+    return pp.skip_enabled && n_cand > 0 && hist_ok && gap_d <= pp.O_dist;
+  };
+  const int* greedy = W.greedy;  // positions < L (shared memory, no per-thread copy)
   for (int ph = 0; ph < 2; ++ph) {
     if ((ph == 0) == feat_first) {
       if (ph == 0) stage_tokens();  // even warps: the token rows land under the feature stream
@@ -319,9 +327,6 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
       W.rankB[lane] = isB ? __popc(mB & ((1u << lane) - 1)) : -1;
     }
     __syncwarp();
-  }
-  const int* greedy = W.greedy;  // positions < L (shared memory, no per-thread copy)
-  const int hist = history ? history[e] : 0x7fffffff;
 
   // ---- per parameter set (a tolerance / threshold sweep): lane-parallel over
   //      (set, candidate) pairs, processed in chunks of kPairs pairs.
@@ -331,7 +336,6 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
   //         among the enumerated chains (DFS order: rank_a * nB + rank_b < cap);
   //      C: one lane per set: longest chain, earliest on ties -> outcome.
   const int G = group_count(L);
-  const int hist_ok = gap_d >= 1 && hist >= gap_d;
   const int nc = n_cand > 0 ? n_cand : 1;
   const int chunk = kPairs / nc;  // sets per chunk (>= 1: n_cand <= 32)
   for (int p0 = 0; p0 < P; p0 += chunk) {
@@ -393,7 +397,7 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
       o.greedy0 = (int16_t)greedy[0];
       o.cos_sim = (float)cosv;
       uint8_t* my_tok = tok_out + ((size_t)pi * E + e) * L;
-      const bool skip = pp.skip_enabled && n_cand > 0 && hist_ok && gap_d <= pp.O_dist && cosv >= pp.min_S;
+      const bool skip = !defer && skip_cond(pp) && cosv >= pp.min_S;
       if (skip) {  // the retrieved draft is emitted as fully accepted
         o.accept_len = L;
         o.win_a = 0;
@@ -441,6 +445,33 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
       out[(size_t)pi * E + e] = o;
     }
     __syncwarp();
+  }
+  }  // the logits / logic phase
+  // ---- odd warps streamed their features after the sweep: apply the skip
+  //      decisions now (a skipped set's outcome is replaced) and the similarity
+  if (defer) {
+    __syncwarp();
+    for (int q = lane; q < P; q += 32) {
+      const hsd_verify_params& pp = params[q];
+      hsd_outcome* op = out + (size_t)q * E + e;
+      if (skip_cond(pp) && cosv >= pp.min_S) {
+        hsd_outcome o;
+        o.accept_len = L;
+        o.win_a = 0;
+        o.win_b = 0;
+        o.calls = 0;
+        o.fallback = 0;
+        o.skipped = 1;
+        o.n_emit = (int16_t)L;
+        o.greedy0 = (int16_t)W.greedy[0];
+        o.cos_sim = (float)cosv;
+        *op = o;
+        uint8_t* my_tok = tok_out + ((size_t)q * E + e) * L;
+        for (int t = 0; t < L; ++t) my_tok[t] = W.tok[0][t];
+      } else {
+        op->cos_sim = (float)cosv;
+      }
+    }
   }
 }
 
