@@ -14,11 +14,9 @@ n, dim = 3000, 128
 for dtype in ("f32", "bf16"):
     col = H.Collection(dim, capacity=n, dtype=dtype)
     col.generate(H.REAL, 3, n)
-    for path in (["tc", "rows", "tile", "tc1", "tc3"] if dtype == "f32" else ["tc"]):
+    for path in ("auto", "filter", "scan", "tc_single"):
         H.set_sim_path(path)
         for B in (1, 5, 64, 200, 300):
-            if path in ("tc1", "tc3", "rows", "tile") and B > 64:
-                continue
             q = H.gen_queries(H.REAL, 4, 3, n, 0, B, dim)
             sc, ids = col.search_topk_exact(q, 8)
     H.set_sim_path("auto")
@@ -26,6 +24,12 @@ for dtype in ("f32", "bf16"):
         col.set_filter("bf16_copy")
         q = H.gen_queries(H.REAL, 4, 3, n, 0, 700, dim)
         col.search_topk_exact(q, 8)
+    # the approximate index: build (exact assignment, counting sort, centroids) and search
+    idx = H.Index(col, nlist=24, n_iter=2)
+    for B in (1, 70, 1100):
+        q = H.gen_queries(H.REAL, 6, 3, n, 0, B, dim)
+        idx.search_topk(q, 8, nprobe=3, return_probes=True)
+    idx.close()
     rows = H.query_rows(4, H.REAL, n, 0, 64)
     lg = H.gen_logits(col, 3, rows, 7)
     fn, fp = H.gen_features(5, 64, 64)
@@ -33,6 +37,17 @@ for dtype in ("f32", "bf16"):
     sc, ids = col.search_topk_exact(q, 8)
     col.verify_round(ids, lg, [H.VerifyParams.make(skip_enabled=True), H.VerifyParams.make(relaxed=False)],
                      feat_now=fn, feat_prev=fp)
+# the range fallback: runs of near-duplicate rows
+cl = H.Collection(dim, capacity=4096)
+cl.generate(H.CLUSTER, 9, 4096)
+for B in (1, 64):
+    cl.search_topk_exact(H.gen_queries(H.CLUSTER, 4, 9, 4096, 0, B, dim), 8)
+# per-chain verification and percentile bounds
+ids8 = ids[:16].contiguous()
+nch, ab, ctoks = H.enumerate_chains(ids8, 7, col=col)
+H.verify_round_chains(ids8, H.VerifyParams.make(), torch.zeros(16, dtype=torch.int32, device="cuda"),
+                      chain_greedy=ctoks, col=col)
+H.percentile_bounds(torch.rand(1000, dtype=torch.float64, device="cuda"))
 xyz = torch.as_tensor(synth.trajectory_windows(64, 15, seed=3)[0], device="cuda")
 H.window_features(xyz, derivatives=True)
 # engine step: K5 + the skip similarity on the side stream, K1 / K2 / K4 on the main stream
