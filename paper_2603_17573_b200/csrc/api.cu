@@ -2339,12 +2339,19 @@ hsd_status hsd_search_topk_index(hsd_index* x, const float* queries, int B, int 
   const int nsm = num_sms(c->device);
   const int W = hsd::kMaxBatchPass;
   const int Bp = std::min(B, W);
-  // rows per unit, coarse and fine, and the unit bounds of one pass
+  // rows per scoring chunk (ur) and per unit (span), coarse and fine, and the
+  // unit bounds of one pass: spans grow so a pass has at most ~kUnitCap units
+  // (the per-unit top-32 lists stay small whatever nlist / nprobe / B are)
+  const int64_t kUnitCap = std::max<int64_t>(256LL * nsm, (int64_t)Bp * np);
   const int ur_c = ivf_unit_rows((double)Bp * ((x->nlist + 127) / 128), nsm);
-  const int per_q = (x->nlist + ur_c - 1) / ur_c;
+  int span_c = ur_c;
+  while ((int64_t)Bp * ((x->nlist + span_c - 1) / span_c) > kUnitCap) span_c *= 2;
+  const int per_q = (x->nlist + span_c - 1) / span_c;
   const double avg = (double)x->n / x->nlist;
   const int ur_f = ivf_unit_rows((double)Bp * np * std::ceil(avg / 128.0), nsm);
-  const int64_t fine_max = (int64_t)Bp * np * ((x->max_list + ur_f - 1) / ur_f);
+  int span_f = ur_f;
+  while ((int64_t)Bp * np * ((x->max_list + span_f - 1) / span_f) > kUnitCap) span_f *= 2;
+  const int64_t fine_max = (int64_t)Bp * np * ((x->max_list + span_f - 1) / span_f);
   const int64_t units_max = std::max<int64_t>((int64_t)Bp * per_q, fine_max);
   IvfScratch* sc = nullptr;
   {
@@ -2374,12 +2381,13 @@ hsd_status hsd_search_topk_index(hsd_index* x, const float* queries, int B, int 
     hsd::IvfUnits cu{};
     cu.mode = 0;
     cu.ur = ur_c;
+    cu.span = span_c;
     cu.per_q = per_q;
     cu.n_q = Bs;
     cu.n_rows = x->nlist;
     CU(hsd::launch_ivf_scan(x->cent->keys, 0, x->dim, nullptr, x->dim, q, cu, (int64_t)Bs * per_q, grid, sc->part, s));
     CU(hsd::launch_ivf_merge(sc->part, cu, Bs, sc->pool, s));
-    CU(hsd::launch_ivf_probe(sc->pool, Bs, np, x->offs, ur_f, sc->probe, sc->upre, s));
+    CU(hsd::launch_ivf_probe(sc->pool, Bs, np, x->offs, span_f, sc->probe, sc->upre, s));
     if (probes) {
       CU(cudaMemcpy2DAsync(probes + (size_t)b0 * nprobe, nprobe * sizeof(int32_t), sc->probe, np * sizeof(int32_t),
                            np * sizeof(int32_t), Bs, cudaMemcpyDeviceToDevice, s));
@@ -2387,12 +2395,13 @@ hsd_status hsd_search_topk_index(hsd_index* x, const float* queries, int B, int 
     hsd::IvfUnits fu{};
     fu.mode = 1;
     fu.ur = ur_f;
+    fu.span = span_f;
     fu.n_pairs = Bs * np;
     fu.nprobe = np;
     fu.upre = sc->upre;
     fu.probe = sc->probe;
     fu.offs = x->offs;
-    const int64_t fmax = (int64_t)Bs * np * ((x->max_list + ur_f - 1) / ur_f);
+    const int64_t fmax = (int64_t)Bs * np * ((x->max_list + span_f - 1) / span_f);
     // the fine scan streams the filter copy when the collection keeps one (half the bytes)
     const void* frows = c->shadow ? (const void*)c->shadow : c->keys;
     const int fbf16 = c->shadow || c->dtype == HSD_DTYPE_BF16;

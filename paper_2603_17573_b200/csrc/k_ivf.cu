@@ -19,9 +19,10 @@
 //
 // Search (B queries, nprobe lists each):
 //   1. coarse scan: every centroid scored (fp32 SIMT over the fp32 centroids),
-//      units of `ur` rows -> per-unit top-32 -> per-query merge -> the nprobe
+//      units of `span` rows (chunks of `ur`) -> per-unit top-32 -> per-query merge -> the nprobe
 //      best lists (approximate order; ties by list id);
-//   2. probe prefix: units of the probed lists (ceil(len / ur) each);
+//   2. probe prefix: units of the probed lists (ceil(len / span) each; the
+//      span bounds the unit count, so the per-unit lists stay small);
 //   3. fine scan: the probed lists' rows (the stored keys, or the bf16 filter
 //      copy of an fp32 collection when it keeps one) x the fp32 query, fp32
 //      accumulation; per-unit top-32 keyed by RECORD id;
@@ -148,8 +149,8 @@ __device__ __forceinline__ Unit unit_of(const IvfUnits& su, int64_t u) {
   Unit x;
   if (su.mode == 0) {
     x.b = (int)(u / su.per_q);
-    x.r0 = (u - (int64_t)x.b * su.per_q) * su.ur;
-    x.r1 = min(x.r0 + su.ur, su.n_rows);
+    x.r0 = (u - (int64_t)x.b * su.per_q) * su.span;
+    x.r1 = min(x.r0 + su.span, su.n_rows);
     return x;
   }
   int lo = 0, hi = su.n_pairs;  // largest p with upre[p] <= u
@@ -159,8 +160,8 @@ __device__ __forceinline__ Unit unit_of(const IvfUnits& su, int64_t u) {
   }
   const int l = su.probe[lo];
   x.b = lo / su.nprobe;
-  x.r0 = su.offs[l] + (u - su.upre[lo]) * (int64_t)su.ur;
-  x.r1 = min(x.r0 + su.ur, (int64_t)su.offs[l + 1]);
+  x.r0 = su.offs[l] + (u - su.upre[lo]) * (int64_t)su.span;
+  x.r1 = min(x.r0 + su.span, (int64_t)su.offs[l + 1]);
   return x;
 }
 
@@ -180,28 +181,32 @@ __global__ void __launch_bounds__(kIThreads) ivf_scan_kernel(const KT* __restric
   for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
     const Unit x = unit_of(su, u);
     const float* q = queries + (size_t)x.b * dim;
-    for (int rr = warp; rr < su.ur; rr += 2 * kIWarps) {
-      const int64_t pa = x.r0 + rr, pb = pa + kIWarps;
-      const bool va = pa < x.r1, vb = pb < x.r1;
-      // the record behind each list position: its id and its stored key row
-      const int64_t ia = va ? (row_id ? (int64_t)row_id[pa] : pa) : 0;
-      const int64_t ib = vb ? (row_id ? (int64_t)row_id[pb] : pb) : ia;
-      float sa = 0.f, sb = 0.f;
-      if (va) dot2(rows + ia * stride, rows + ib * stride, vb, q, dim, lane, sa, sb);
-      if (lane == 0) {
-        sk[rr] = va ? dev::cand_key(sa, (uint32_t)ia) : kEmpty;
-        sk[rr + kIWarps] = vb ? dev::cand_key(sb, (uint32_t)ib) : kEmpty;
+    uint64_t top = kEmpty;  // warp 0: the unit's running top-32 over its chunks of ur rows
+    for (int64_t c0 = x.r0; c0 < x.r1; c0 += su.ur) {
+      for (int rr = warp; rr < su.ur; rr += 2 * kIWarps) {
+        const int64_t pa = c0 + rr, pb = pa + kIWarps;
+        const bool va = pa < x.r1, vb = pb < x.r1;
+        // the record behind each list position: its id and its stored key row
+        const int64_t ia = va ? (row_id ? (int64_t)row_id[pa] : pa) : 0;
+        const int64_t ib = vb ? (row_id ? (int64_t)row_id[pb] : pb) : ia;
+        float sa = 0.f, sb = 0.f;
+        if (va) dot2(rows + ia * stride, rows + ib * stride, vb, q, dim, lane, sa, sb);
+        if (lane == 0) {
+          sk[rr] = va ? dev::cand_key(sa, (uint32_t)ia) : kEmpty;
+          sk[rr + kIWarps] = vb ? dev::cand_key(sb, (uint32_t)ib) : kEmpty;
+        }
       }
-    }
-    __syncthreads();
-    if (warp == 0) {
-      uint64_t v[4];
+      __syncthreads();
+      if (warp == 0) {
+        uint64_t v[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) v[t] = t * 32 + lane < su.ur ? sk[t * 32 + lane] : kEmpty;
-      dev::warp_sort<4>(v);
-      out[(size_t)u * 32 + lane] = v[0];
+        for (int t = 0; t < 4; ++t) v[t] = t * 32 + lane < su.ur ? sk[t * 32 + lane] : kEmpty;
+        dev::warp_sort<4>(v);
+        top = dev::warp_merge_top32(top, v[0]);
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    if (warp == 0) out[(size_t)u * 32 + lane] = top;
   }
 }
 
@@ -231,10 +236,10 @@ __global__ void __launch_bounds__(kIThreads) ivf_merge_kernel(const uint64_t* __
 }
 
 // Probe lists (the first nprobe of each query's coarse pool) and the fine
-// scan's unit prefix upre[p] (ceil(len / ur) units per probed list).  One CTA.
+// scan's unit prefix upre[p] (ceil(len / span) units per probed list).  One CTA.
 constexpr int kPThreads = 1024;
 __global__ void __launch_bounds__(kPThreads) ivf_probe_kernel(const uint64_t* __restrict__ pool, int B, int nprobe,
-                                                              const int32_t* __restrict__ offs, int ur,
+                                                              const int32_t* __restrict__ offs, int span,
                                                               int32_t* __restrict__ probe,
                                                               int32_t* __restrict__ upre) {
   __shared__ int wsum[kPThreads / 32];
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(kPThreads) ivf_probe_kernel(const uint64_t* __
     const uint64_t key = pool[(size_t)(p / nprobe) * 32 + (p % nprobe)];
     const int l = key == kEmpty ? -1 : (int)dev::cand_id(key);
     probe[p] = l < 0 ? 0 : l;
-    run += l < 0 ? 0 : (offs[l + 1] - offs[l] + ur - 1) / ur;
+    run += l < 0 ? 0 : (offs[l + 1] - offs[l] + span - 1) / span;
   }
   int incl = run;
 #pragma unroll
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(kPThreads) ivf_probe_kernel(const uint64_t* __
     const uint64_t key = pool[(size_t)(p / nprobe) * 32 + (p % nprobe)];
     const int l = key == kEmpty ? -1 : (int)dev::cand_id(key);
     upre[p] = base;
-    base += l < 0 ? 0 : (offs[l + 1] - offs[l] + ur - 1) / ur;
+    base += l < 0 ? 0 : (offs[l + 1] - offs[l] + span - 1) / span;
   }
   if (tid == kPThreads - 1) upre[n] = base;
 }
@@ -421,7 +426,7 @@ size_t ivf_part_bytes(int64_t units) { return (size_t)units * 32 * sizeof(uint64
 cudaError_t launch_ivf_scan(const void* rows, int rows_bf16, int64_t stride, const int32_t* row_id, int dim,
                             const float* queries, const IvfUnits& su, int64_t max_units, int grid, uint64_t* part,
                             cudaStream_t s) {
-  if (su.ur != 32 && su.ur != kUnitMax) return cudaErrorInvalidValue;
+  if ((su.ur != 32 && su.ur != kUnitMax) || su.span < su.ur || su.span % su.ur) return cudaErrorInvalidValue;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(max_units, grid));
   if (rows_bf16)
     ivf_scan_kernel<uint16_t><<<g, kIThreads, 0, s>>>((const uint16_t*)rows, stride, row_id, dim, queries, su, part);
@@ -436,11 +441,11 @@ cudaError_t launch_ivf_merge(const uint64_t* part, const IvfUnits& su, int B, ui
   return cudaGetLastError();
 }
 
-cudaError_t launch_ivf_probe(const uint64_t* pool, int B, int nprobe, const int32_t* offs, int ur, int32_t* probe,
+cudaError_t launch_ivf_probe(const uint64_t* pool, int B, int nprobe, const int32_t* offs, int span, int32_t* probe,
                              int32_t* upre, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   if (nprobe < 1 || nprobe > 32) return cudaErrorInvalidValue;
-  ivf_probe_kernel<<<1, kPThreads, 0, s>>>(pool, B, nprobe, offs, ur, probe, upre);
+  ivf_probe_kernel<<<1, kPThreads, 0, s>>>(pool, B, nprobe, offs, span, probe, upre);
   return cudaGetLastError();
 }
 

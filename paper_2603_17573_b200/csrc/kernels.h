@@ -122,12 +122,13 @@ cudaError_t launch_p2p_merge(const P2PWindows& w, int rank, int G, int B, int k,
                              int32_t* ids, uint8_t* tok, int* err, cudaStream_t s);
 
 // ---- approximate index: IVF-flat (k_ivf.cu; host side in api.cu) ---------------
-// Scan units: mode 0 (coarse) unit u = (query u / per_q, rows [(u % per_q) ur, +ur)
+// Scan units: mode 0 (coarse) unit u = (query u / per_q, rows [(u % per_q) span, +span)
 // of [0, n_rows)); mode 1 (fine) pairs p = b * nprobe + j own units
-// [upre[p], upre[p + 1]), chunks of ur rows of list probe[p] = [offs[l], offs[l+1]).
+// [upre[p], upre[p + 1]), spans of list probe[p] = [offs[l], offs[l+1]).
 struct IvfUnits {
   int mode;
-  int ur;  // rows per unit: 32 or 128
+  int ur;    // rows per scoring chunk: 32 or 128
+  int span;  // rows per unit: a multiple of ur (a unit loops over its chunks)
   int per_q, n_q;
   int64_t n_rows;
   int n_pairs, nprobe;
@@ -142,7 +143,7 @@ cudaError_t launch_ivf_scan(const void* rows, int rows_bf16, int64_t stride, con
                             const float* queries, const IvfUnits& su, int64_t max_units, int grid, uint64_t* part,
                             cudaStream_t s);
 cudaError_t launch_ivf_merge(const uint64_t* part, const IvfUnits& su, int B, uint64_t* pool, cudaStream_t s);
-cudaError_t launch_ivf_probe(const uint64_t* pool, int B, int nprobe, const int32_t* offs, int ur, int32_t* probe,
+cudaError_t launch_ivf_probe(const uint64_t* pool, int B, int nprobe, const int32_t* offs, int span, int32_t* probe,
                              int32_t* upre, cudaStream_t s);
 // build: seeds (sum <- seed rows), centroids (sum <- list sums when perm; cent <- sum / |sum|)
 cudaError_t launch_ivf_seed(const void* keys, int key_dtype, int dim, int64_t n, int nlist, double* sum,

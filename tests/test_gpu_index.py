@@ -113,6 +113,24 @@ def test_search_is_exact_over_probed_lists(torch, dtype, B, nprobe):
     np.testing.assert_array_equal(sc, rs)
 
 
+@pytest.mark.parametrize("nlist,nprobe,B", [(1, 1, 1100), (2, 2, 300), (3, 1, 1)])
+def test_few_long_lists(torch, nlist, nprobe, B):
+    # a handful of huge lists: units span many 32/128-row chunks (the per-pass unit cap)
+    n, dim, k = 20000, 64, 8
+    col = make_db(O.REAL, 31, n, dim)
+    idx = H.Index(col, nlist=nlist, n_iter=1)
+    offs, perm, cent = idx.lists()
+    q = H.gen_queries(O.REAL, 2, 31, n, 0, B, dim)
+    sc, ids, probes = idx.search_topk(q, k, nprobe=nprobe, return_probes=True)
+    rs, ri = O.ivf_search_lists(O.gen_keys(O.REAL, 31, 0, n, dim), offs, perm, probes.cpu().numpy(),
+                                q.cpu().numpy(), k)
+    np.testing.assert_array_equal(ids.cpu().numpy(), ri)
+    np.testing.assert_array_equal(sc.cpu().numpy(), rs)
+    if nprobe == nlist:  # every list probed: the exact search
+        es, ei = col.search_topk_exact(q, k)
+        np.testing.assert_array_equal(ids.cpu().numpy(), ei.cpu().numpy())
+
+
 def test_recall_and_full_probe(torch):
     n, dim, k = 20000, 256, 8
     col = make_db(O.REAL, 2, n, dim)
