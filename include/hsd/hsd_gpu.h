@@ -172,6 +172,10 @@ hsd_status hsd_debug_sim_scores(hsd_collection* c, const float* queries, int B, 
  * single-CTA wide kernels only (also HSD_WIDE_PAIR=0), 2 filter + rescoring
  * only, 3 exact scan wherever it applies (B <= 4, k <= 32).  Every path
  * returns the same bits. */
+/* Diagnostics: returns and clears the CUDA runtime's pending (non-sticky)
+ * error of the calling thread — the tests check that no entry point, destroy
+ * included, leaves one behind. */
+int hsd_debug_last_cuda_error(void);
 hsd_status hsd_set_sim_path(int path);
 /* The path a search of B queries (top-k) over `rows` rows (-1: the whole
  * collection) takes under the current switch: *exact_scan = 1 for the exact

@@ -258,6 +258,7 @@ def lib():
                                C.POINTER(C.c_int), _vp],
         "hsd_update_skip_state": [C.POINTER(SkipState), C.c_int, C.c_double, C.c_double],
         "hsd_collection_load_image": [C.c_char_p, C.c_int, C.POINTER(_vp)],
+        "hsd_debug_last_cuda_error": [],
         "hsd_index_build": [_vp, C.POINTER(IvfParams), C.POINTER(_vp)],
         "hsd_index_destroy": [_vp],
         "hsd_index_info": [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int), C.POINTER(C.c_int)],
@@ -558,6 +559,8 @@ class Index:
         return offs, perm, cent
 
     def search_topk(self, queries, k: int, nprobe: int = 16, stream=None, return_probes=False):
+        if not getattr(self, "_h", None) or not self._col._h:
+            raise InvalidInputError("the index or its collection has been closed")
         torch = _torch()
         q = queries.contiguous()
         if q.dtype != torch.float32 or not q.is_cuda:

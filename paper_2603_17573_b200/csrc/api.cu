@@ -450,6 +450,7 @@ hsd_status hsd_collection_destroy(hsd_collection* c) {
   cudaFree(c->feat);
   cudaFree(c->has_feat);
   delete c;
+  cudaGetLastError();
   return HSD_OK;
 }
 
@@ -1018,6 +1019,7 @@ struct StepGraph {
 
 struct hsd_engine {
   hsd_collection* c = nullptr;
+  int device = 0;  // the collection's device (destroy never dereferences c: it may be gone)
   int max_B = 0, k = 0, L = 0, d_f = 0, w = 0;
   std::vector<StepGraph> graphs;  // small LRU-less cache (cleared when full)
   StageSlot slot[2];
@@ -1051,6 +1053,7 @@ hsd_status hsd_engine_create(hsd_collection* c, int max_B, int k, int L, int d_f
   if (st != HSD_OK) return st;
   auto* e = new hsd_engine();
   e->c = c;
+  e->device = c->device;
   e->max_B = max_B;
   e->k = k;
   e->L = L;
@@ -1155,7 +1158,7 @@ hsd_status hsd_engine_stage_marks(hsd_engine* e, const hsd_engine* ref, int max_
 
 hsd_status hsd_engine_destroy(hsd_engine* e) {
   if (!e) return HSD_OK;
-  cudaSetDevice(e->c->device);
+  cudaSetDevice(e->device);
   for (cudaEvent_t x : e->ev) cudaEventDestroy(x);
   cudaDeviceSynchronize();  // no step still reads the engine's buffers
   cudaFree(e->cos);
@@ -1182,6 +1185,7 @@ hsd_status hsd_engine_destroy(hsd_engine* e) {
   free_scratch(e->scr);
   cudaFree(e->vp);
   delete e;
+  cudaGetLastError();  // a destroy leaves no pending error behind
   return HSD_OK;
 }
 
@@ -1682,6 +1686,7 @@ hsd_status hsd_gen_features(int device, uint64_t seed, int E, int d_f, float* no
 // ------------------------------------------------------------------ hybrid loop (config 5)
 struct hsd_hybrid {
   hsd_collection* c = nullptr;
+  int device = 0;  // the collection's device (destroy never dereferences c)
   hsd_comm* comm = nullptr;
   int64_t id_offset = 0, n_total = 0;
   hsd_hybrid_params p{};
@@ -1721,7 +1726,7 @@ extern "C" {
 
 hsd_status hsd_hybrid_destroy(hsd_hybrid* h) {
   if (!h) return HSD_OK;
-  cudaSetDevice(h->c->device);
+  cudaSetDevice(h->device);
   cudaDeviceSynchronize();
   for (void* p : h->allocs) cudaFree(p);
   if (h->h_counts) cudaFreeHost(h->h_counts);
@@ -1729,6 +1734,7 @@ hsd_status hsd_hybrid_destroy(hsd_hybrid* h) {
     for (cudaEvent_t e : set)
       if (e) cudaEventDestroy(e);
   delete h;
+  cudaGetLastError();
   return HSD_OK;
 }
 
@@ -1756,6 +1762,7 @@ hsd_status hsd_hybrid_create(hsd_collection* c, hsd_comm* comm, int64_t id_offse
   if (st != HSD_OK) return st;
   auto* h = new hsd_hybrid();
   h->c = c;
+  h->device = c->device;
   h->comm = comm;
   h->id_offset = id_offset;
   h->n_total = n_total_rows;
@@ -2155,7 +2162,8 @@ struct IvfScratch {
 }  // namespace
 
 struct hsd_index {
-  hsd_collection* col = nullptr;  // indexed collection (not owned)
+  hsd_collection* col = nullptr;  // indexed collection (not owned; destroy never dereferences it)
+  int device = 0;
   uint64_t gen = 0;               // the collection's generation at build
   int64_t n = 0;
   int nlist = 0, dim = 0, max_list = 0;
@@ -2213,12 +2221,13 @@ extern "C" {
 
 hsd_status hsd_index_destroy(hsd_index* x) {
   if (!x) return HSD_OK;
-  cudaSetDevice(x->col ? x->col->device : 0);
+  cudaSetDevice(x->device);
   for (auto& kv : x->scratch) free_ivf_scratch(kv.second);
   cudaFree(x->offs);
   cudaFree(x->perm);
   hsd_collection_destroy(x->cent);
   delete x;
+  cudaGetLastError();
   return HSD_OK;
 }
 
@@ -2234,6 +2243,7 @@ hsd_status hsd_index_build(hsd_collection* c, const hsd_ivf_params* p, hsd_index
   if (st != HSD_OK) return st;
   auto* x = new hsd_index();
   x->col = c;
+  x->device = c->device;
   x->gen = c->gen;
   x->n = c->n;
   x->dim = c->dim;
@@ -2414,3 +2424,6 @@ hsd_status hsd_search_topk_index(hsd_index* x, const float* queries, int B, int 
 }
 
 }  // extern "C"
+
+extern "C" int hsd_debug_last_cuda_error(void) { return (int)cudaGetLastError(); }
+

@@ -233,3 +233,20 @@ def test_small_lists_pad_and_errors(torch):
         H.Index(empty, nlist=4)
     with pytest.raises(H.ConfigError):
         H.Index(col, nlist=0)
+
+
+def test_destroy_order_leaves_no_error(torch):
+    # a reference cycle (Collection <-> its build_hnsw index) is finalized in any
+    # order by Python's GC: an index outliving its collection must destroy cleanly
+    import ctypes as C
+    col = make_db(O.REAL, 8, 500, 64)
+    idx = H.Index(col, nlist=8, n_iter=1)
+    L = H.lib()
+    L.hsd_debug_last_cuda_error()
+    assert L.hsd_collection_destroy(col.handle) == 0
+    col._h = C.c_void_p()  # closed
+    with pytest.raises(H.InvalidInputError, match="closed"):
+        idx.search_topk(H.gen_queries(O.REAL, 1, 8, 500, 0, 2, 64), 4)
+    idx.close()
+    assert L.hsd_debug_last_cuda_error() == 0
+
