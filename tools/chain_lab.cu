@@ -1,0 +1,134 @@
+// chain_lab.cu — K1x's consumer loop (k_exact.cu) without TMA or barriers, to
+// find what makes its fp64 chain slower in the kernel (~15 cycles per step)
+// than the same chain_sub code alone (9.3, tools/fp64_rate.cu).  The ring is a
+// static shared-memory tile; the grid is config 1's (139 CTAs x (4 + 1) warps,
+// 18 active lanes per compute warp, 4096 steps).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/bin/chain_lab tools/chain_lab.cu
+//   MODE 0  replica: ring slot rotation, swizzled 16-B row loads, ping-pong widening
+//   MODE 1  fixed ring slot (no slot arithmetic)
+//   MODE 2  no widening of the next sub (keys reused): the DFMA chain + q loads only
+//   MODE 3  replica with every lane active (lpw = 32)
+//   MODE 4  replica, query operands two groups ahead
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+constexpr int kSub = 32;
+struct Raw {
+  uint4 v[8];
+};
+
+__device__ __forceinline__ void widen4(const Raw& r, int g, double* out) {
+  const uint4 x = r.v[g];
+  out[0] = (double)__uint_as_float(x.x);
+  out[1] = (double)__uint_as_float(x.y);
+  out[2] = (double)__uint_as_float(x.z);
+  out[3] = (double)__uint_as_float(x.w);
+}
+
+template <bool kNext, int kAhead>
+__device__ __forceinline__ void chain_sub(const double (&kc)[kSub], double (&kn)[kSub], const Raw& rn,
+                                          const double* __restrict__ q64, int col0, double& acc) {
+  double2 qa[kAhead][2];
+#pragma unroll
+  for (int a = 0; a < kAhead; ++a) {
+    qa[a][0] = *reinterpret_cast<const double2*>(q64 + col0 + 4 * a);
+    qa[a][1] = *reinterpret_cast<const double2*>(q64 + col0 + 4 * a + 2);
+  }
+#pragma unroll
+  for (int g = 0; g < kSub / 4; ++g) {
+    double2 nb0, nb1;
+    if (g + kAhead < kSub / 4) {
+      nb0 = *reinterpret_cast<const double2*>(q64 + col0 + 4 * (g + kAhead));
+      nb1 = *reinterpret_cast<const double2*>(q64 + col0 + 4 * (g + kAhead) + 2);
+    }
+    acc = __fma_rn(qa[0][0].x, kc[4 * g + 0], acc);
+    acc = __fma_rn(qa[0][0].y, kc[4 * g + 1], acc);
+    acc = __fma_rn(qa[0][1].x, kc[4 * g + 2], acc);
+    acc = __fma_rn(qa[0][1].y, kc[4 * g + 3], acc);
+    if (kNext) widen4(rn, g, &kn[4 * g]);
+#pragma unroll
+    for (int a = 0; a + 1 < kAhead; ++a) {
+      qa[a][0] = qa[a + 1][0];
+      qa[a][1] = qa[a + 1][1];
+    }
+    qa[kAhead - 1][0] = nb0;
+    qa[kAhead - 1][1] = nb1;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int R = 4 * lpw;
+  const int stage_bytes = R * 128;
+  double* q64 = reinterpret_cast<double*>(smem + (size_t)S * stage_bytes);
+  for (int i = threadIdx.x; i < S * stage_bytes / 4; i += blockDim.x)
+    reinterpret_cast<float*>(smem)[i] = 1.0f + 1e-7f * (i & 1023);
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) q64[i] = 1.0 - 1e-9 * i;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 4) return;
+  const int rr = warp * lpw + lane;
+  const int swz = rr & 7;
+  const unsigned char* rowbase = smem + (size_t)(lane < lpw ? rr : 0) * 128;
+  int wslot = 0;
+  auto load_sub = [&](int u, Raw& r) {
+    const unsigned char* rowp = rowbase + (size_t)(MODE == 1 ? 0 : wslot) * stage_bytes;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) r.v[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
+    if (MODE != 1 && ++wslot == S) wslot = 0;
+  };
+  constexpr int kAhead = MODE == 4 ? 2 : 1;
+  double acc = 0.0;
+  double ka[kSub], kb[kSub];
+  Raw raw;
+  load_sub(0, raw);
+#pragma unroll
+  for (int g = 0; g < kSub / 4; ++g) widen4(raw, g, &ka[4 * g]);
+  for (int u = 0; u < U; u += 2) {
+    if (MODE != 2) load_sub(u + 1, raw);
+    chain_sub<MODE != 2, kAhead>(ka, kb, raw, q64, (u * kSub) & 4095, acc);
+    if (MODE != 2) load_sub(u + 2, raw);
+    if (MODE == 2)
+      chain_sub<false, kAhead>(ka, kb, raw, q64, ((u + 1) * kSub) & 4095, acc);
+    else
+      chain_sub<true, kAhead>(kb, ka, raw, q64, ((u + 1) * kSub) & 4095, acc);
+  }
+  if (acc == 1.2345) out[0] = acc;
+}
+
+template <int MODE>
+void run(const char* name, int lpw) {
+  double* out;
+  cudaMalloc(&out, 8);
+  const int U = 128, S = (180 * 1024) / (4 * lpw * 128) < 20 ? (180 * 1024) / (4 * lpw * 128) : 20;
+  const size_t smem = (size_t)S * 4 * lpw * 128 + 4096 * 8;
+  cudaFuncSetAttribute(lab<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  lab<MODE><<<139, 160, smem>>>(out, U, S, lpw);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e9;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    lab<MODE><<<139, 160, smem>>>(out, U, S, lpw);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  const double steps = (double)U * kSub;
+  printf("%-44s lpw %2d: %.1f us, %.2f ns/step, %.1f cycles/step @1965 MHz  err=%s\n", name, lpw, best * 1e3,
+         best * 1e6 / steps, best * 1e6 / steps * 1.965, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  run<0>("replica", 18);
+  run<1>("fixed ring slot", 18);
+  run<2>("no next-sub widening", 18);
+  run<3>("replica, every lane", 32);
+  run<4>("replica, q two groups ahead", 18);
+  return 0;
+}
