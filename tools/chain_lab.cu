@@ -9,6 +9,7 @@
 //   MODE 2  no widening of the next sub (keys reused): the DFMA chain + q loads only
 //   MODE 3  replica with every lane active (lpw = 32)
 //   MODE 4  replica, query operands two groups ahead
+//   MODE 5  replica, the next sub widened in the second half of the current one
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -26,7 +27,7 @@ __device__ __forceinline__ void widen4(const Raw& r, int g, double* out) {
   out[3] = (double)__uint_as_float(x.w);
 }
 
-template <bool kNext, int kAhead>
+template <bool kNext, int kAhead, bool kLate = false>
 __device__ __forceinline__ void chain_sub(const double (&kc)[kSub], double (&kn)[kSub], const Raw& rn,
                                           const double* __restrict__ q64, int col0, double& acc) {
   double2 qa[kAhead][2];
@@ -46,7 +47,11 @@ __device__ __forceinline__ void chain_sub(const double (&kc)[kSub], double (&kn)
     acc = __fma_rn(qa[0][0].y, kc[4 * g + 1], acc);
     acc = __fma_rn(qa[0][1].x, kc[4 * g + 2], acc);
     acc = __fma_rn(qa[0][1].y, kc[4 * g + 3], acc);
-    if (kNext) widen4(rn, g, &kn[4 * g]);
+    if (kNext && !kLate) widen4(rn, g, &kn[4 * g]);
+    if (kNext && kLate && g >= 4) {  // the next sub's rows: widened in the second half (its loads have landed)
+      widen4(rn, 2 * (g - 4), &kn[8 * (g - 4)]);
+      widen4(rn, 2 * (g - 4) + 1, &kn[8 * (g - 4) + 4]);
+    }
 #pragma unroll
     for (int a = 0; a + 1 < kAhead; ++a) {
       qa[a][0] = qa[a + 1][0];
@@ -80,6 +85,7 @@ __global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw
     if (MODE != 1 && ++wslot == S) wslot = 0;
   };
   constexpr int kAhead = MODE == 4 ? 2 : 1;
+  constexpr bool kLate = MODE == 5;
   double acc = 0.0;
   double ka[kSub], kb[kSub];
   Raw raw;
@@ -88,12 +94,12 @@ __global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw
   for (int g = 0; g < kSub / 4; ++g) widen4(raw, g, &ka[4 * g]);
   for (int u = 0; u < U; u += 2) {
     if (MODE != 2) load_sub(u + 1, raw);
-    chain_sub<MODE != 2, kAhead>(ka, kb, raw, q64, (u * kSub) & 4095, acc);
+    chain_sub<MODE != 2, kAhead, kLate>(ka, kb, raw, q64, (u * kSub) & 4095, acc);
     if (MODE != 2) load_sub(u + 2, raw);
     if (MODE == 2)
       chain_sub<false, kAhead>(ka, kb, raw, q64, ((u + 1) * kSub) & 4095, acc);
     else
-      chain_sub<true, kAhead>(kb, ka, raw, q64, ((u + 1) * kSub) & 4095, acc);
+      chain_sub<true, kAhead, kLate>(kb, ka, raw, q64, ((u + 1) * kSub) & 4095, acc);
   }
   if (acc == 1.2345) out[0] = acc;
 }
@@ -130,5 +136,6 @@ int main() {
   run<2>("no next-sub widening", 18);
   run<3>("replica, every lane", 32);
   run<4>("replica, q two groups ahead", 18);
+  run<5>("replica, next sub widened in the second half", 18);
   return 0;
 }
