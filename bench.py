@@ -1206,6 +1206,12 @@ def run_c5(args):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": peak_kind, **common, "tensor": tensor}
     value = args.robots * args.steps / (ms / 1e3)
+    # our kernels per round (hsd_hybrid_step): windows + K5 + compaction + emit, then for a
+    # retrieval cohort query/logit prep + per 1024-query pass (slab, K1, K2 x 4) + K4, and for a
+    # drafter cohort drafts + logits + K4
+    nd_per_round = (tr["mode"] == 0).sum(axis=1)
+    launches = int(sum(4 + (3 + 6 * int(np.ceil(r / 1024.0)) if r > 0 else 0) + (3 if d > 0 else 0)
+                       for r, d in zip(nr_per_round, nd_per_round)))
     tokens = int(tr["n_emit"].sum())
     loop_stats = {
         "decision_mix": {"retrieval": float((tr["mode"] == 1).mean()), "drafter": float((tr["mode"] == 0).mean()),
@@ -1256,7 +1262,7 @@ def run_c5(args):
                        "robots": args.robots, "n_rows": args.n, "rows_per_gpu": rows_local, "dim": args.dim,
                        "k_top": args.k_top, "traj_T": args.traj_T, "parallelism": f"db-shard{world}",
                        "l2": "DB far larger than L2 (streamed every round)"},
-            "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": None, "clocks": clk.summary(),
+            "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "stages_ms": stages, "loop": loop_stats,
         }
         print(json.dumps(line), flush=True)
