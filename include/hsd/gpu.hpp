@@ -258,7 +258,6 @@ class Collection {
     if (!index_) return search_topk_exact(query, k);
     if (k < 1) return {};  // HnswIndex::search returns no ids (hnsw.cpp:160)
     if ((int)query.size() != dim_) throw InvalidInputError("embedding dim mismatch in cosine");
-    if (k > HSD_K_MAX) throw InvalidInputError("k exceeds the device top-k limit HSD_K_MAX");
     std::vector<float> q((size_t)pdim_, 0.0f);
     for (int c = 0; c < dim_; ++c) q[(size_t)c] = (float)query[(size_t)c];
     s_.resize((size_t)k);

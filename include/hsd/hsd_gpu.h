@@ -135,8 +135,10 @@ hsd_status hsd_collection_generate_rows(hsd_collection* c, int kind, uint64_t db
  * record ids, ordered (score desc, id asc); when k > size the trailing
  * entries are id -1 / score -inf.  Scores are the reference's sequential fp64
  * dot product of the (fp32-widened) query and key, bit for bit.
- * k < 1 -> HSD_ERR_INVALID_INPUT (store.cpp:60); k > HSD_K_MAX ->
- * HSD_ERR_INVALID_INPUT.  An empty collection yields all -1 (no error).
+ * k < 1 -> HSD_ERR_INVALID_INPUT (store.cpp:60).  k > HSD_K_MAX is served
+ * by a separate exact path (every row's score, then a stable radix sort per
+ * query; stream-ordered scratch of ~24 bytes per row) and needs dim <= ~17000.
+ * An empty collection yields all -1 (no error).
  * `queries` is a device pointer, 16-byte aligned (HSD_ERR_INVALID_INPUT
  * otherwise; rows are dim * 4 bytes apart with dim % 4 == 0).
  * ---------------------------------------------------------------------- */
@@ -220,7 +222,8 @@ hsd_status hsd_index_lists(const hsd_index* x, int32_t* offs, int32_t* perm, flo
 /* Approximate top-k of B queries (device, 16-byte aligned) over the nprobe
  * (1..32, clamped to nlist) best lists; scores / ids as
  * hsd_search_topk_exact (-inf / -1 past the candidates found).  probes
- * (device [B][nprobe], optional) receives the probed list ids. */
+ * (device [B][nprobe], optional) receives the probed list ids.  k >
+ * HSD_K_MAX answers with the exact top-k (probes untouched). */
 hsd_status hsd_search_topk_index(hsd_index* x, const float* queries, int B, int k, int nprobe, double* scores,
                                  int32_t* ids, int32_t* probes, void* stream);
 

@@ -90,9 +90,8 @@ int num_sms(int device) {
   return v;
 }
 
-__global__ void fill_empty_kernel(double* scores, int32_t* ids, int n) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
+__global__ void fill_empty_kernel(double* scores, int32_t* ids, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     scores[i] = -INFINITY;
     ids[i] = -1;
   }
@@ -313,7 +312,11 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
                        int32_t* ids, cudaStream_t s, const StageMarks* marks = nullptr, int reserve_sms = 0,
                        const hsd::P2PPublish* pub = nullptr, Scratch* own = nullptr) {
   if (k < 1) return fail(HSD_ERR_INVALID_INPUT, "k must be >= 1");  // store.cpp:60
-  if (k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k = %d exceeds HSD_K_MAX = %d", k, HSD_K_MAX);
+  // k > HSD_K_MAX: the exact scan of every row + a stable radix sort (a
+  // plain search only; the engine, sharded and index paths keep k <= 32)
+  const bool large_k = k > HSD_K_MAX;
+  if (large_k && (pub || own || marks))
+    return fail(HSD_ERR_INVALID_INPUT, "k = %d exceeds HSD_K_MAX = %d", k, HSD_K_MAX);
   if (B < 0) return fail(HSD_ERR_INVALID_INPUT, "negative batch");
   if (B == 0) return HSD_OK;
   if (!queries || !scores || !ids) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
@@ -325,10 +328,17 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
   re = std::min<int64_t>(re, c->n);
   const int64_t rows = re - rb;
   if (rows <= 0) {  // empty collection -> empty result, no error (store.cpp:62-72)
-    const int n = B * k;
-    fill_empty_kernel<<<(n + 255) / 256, 256, 0, s>>>(scores, ids, n);
+    const int64_t n = (int64_t)B * k;
+    fill_empty_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 64), 256, 0, s>>>(scores, ids, n);
     CU(cudaGetLastError());
     if (pub) CU(hsd::launch_p2p_publish(pub->w, pub->rank, pub->G, B, k, pub->epoch, scores, ids, nullptr, s));
+    return HSD_OK;
+  }
+  if (large_k) {
+    if (!hsd::exact_topk_large_supported(c->dim, c->dtype))
+      return fail(HSD_ERR_INVALID_INPUT, "k = %d > HSD_K_MAX needs dim <= ~17000 (fp64 query slab), got %d", k, c->dim);
+    CU(hsd::launch_exact_topk_large(c->keys, c->dtype, c->n, rb, re, c->dim, queries, B, k,
+                                    std::min(num_sms(c->device), kMaxSms), scores, ids, s));
     return HSD_OK;
   }
   // reserve_sms: SMs left free for work running concurrently on another stream
@@ -2337,7 +2347,9 @@ hsd_status hsd_search_topk_index(hsd_index* x, const float* queries, int B, int 
   // (store.cpp:44-57): search_topk falls back to the exact search (:83)
   if (x->gen != c->gen) return search_impl(c, queries, B, k, 0, c->n, scores, ids, s);
   if (k < 1) return fail(HSD_ERR_INVALID_INPUT, "k must be >= 1");  // store.cpp:60
-  if (k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k = %d exceeds HSD_K_MAX = %d", k, HSD_K_MAX);
+  // k > HSD_K_MAX: the exact top-k (the probed-list lists hold 32 entries);
+  // the exact answer is also the best one an index can return
+  if (k > HSD_K_MAX) return search_impl(c, queries, B, k, 0, c->n, scores, ids, s);
   if (nprobe < 1 || nprobe > 32) return fail(HSD_ERR_INVALID_INPUT, "nprobe must be in [1, 32], got %d", nprobe);
   if (B < 0) return fail(HSD_ERR_INVALID_INPUT, "negative batch");
   if (B == 0) return HSD_OK;

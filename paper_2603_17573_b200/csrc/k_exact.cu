@@ -27,6 +27,8 @@
 //     (bitonic sort + merge; a batch that cannot enter is rejected with one
 //     ballot), the CTA's 4 warp lists merge in shared memory, and the last
 //     CTA to finish (ticket) merges the CTAs' lists into the final top-k.
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "sm100.cuh"
@@ -212,6 +214,7 @@ struct ScanArgs {
   unsigned* ticket;              // zero between launches (the last CTA resets it)
   double* scores;                // [NQ][k]
   int32_t* ids;
+  uint64_t* allkey;              // != nullptr: every row's order key [NQ][rows], no top-k (large k)
 };
 
 template <typename KT, int NQ, int kCW = compute_warps(NQ)>
@@ -355,10 +358,19 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
           chain_sub<KT, NQ, false>(kb, ka, raw, q64, qlen, (u + 1) * kSub, acc);
         }
       }
+      if (a.allkey) {  // large k: the keys go to the radix sort (coalesced: consecutive rows per lane)
+        if (active) {
+          const int64_t rows = a.row_end - a.row_begin;
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) a.allkey[(size_t)q * rows + (row - a.row_begin)] = dev::score_desc_key(acc[q]);
+        }
+        continue;
+      }
 #pragma unroll
       for (int q = 0; q < NQ; ++q)
         warp_offer(lk[q], li[q], active ? dev::score_desc_key(acc[q]) : kEmpty, active ? (uint32_t)row : kNoId, a.k);
     }
+    if (a.allkey) return;  // uniform over the compute warps; the producer's loads were all consumed
     // the CTA's list: warps 1..3 stage theirs, warp 0 merges
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -376,6 +388,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
       }
     }
   }
+  if (a.allkey) return;  // the producer warp (large k: no merge)
   // ---- the last CTA merges every CTA's list
   __threadfence();
   __syncthreads();
@@ -552,6 +565,113 @@ cudaError_t launch_exact_scan(const void* keys, int key_dtype, int64_t n_keys_to
 #undef HSD_SCAN
     default: return cudaErrorInvalidValue;
   }
+}
+
+// ---- large k (k > HSD_K_MAX): every row's key, then a stable radix sort ----
+//
+// The register top-k lists hold 32 entries.  For larger k the scan above
+// writes every row's order key (its exact fp64 chain, bit-identical to
+// cosine_similarity) and a stable LSD radix sort of (key, row id) with the
+// ids in ascending order yields exactly the reference's (score desc, id asc)
+// order (store.cpp:66-69); the first k entries are the result.
+namespace {
+
+__global__ void iota_ids_kernel(uint32_t* __restrict__ v, int64_t n, int64_t base) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (uint32_t)(base + i);
+}
+
+__global__ void emit_topk_kernel(const uint64_t* __restrict__ key, const uint32_t* __restrict__ id, int64_t rows,
+                                 int k, double* __restrict__ scores, int32_t* __restrict__ ids) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+    const bool ok = j < rows;
+    scores[j] = ok ? key_score(key[j]) : -INFINITY;
+    ids[j] = ok ? (int32_t)id[j] : -1;
+  }
+}
+
+}  // namespace
+
+bool exact_topk_large_supported(int dim, int key_dtype) { return exact_scan_supported(1, dim, key_dtype, 1); }
+
+cudaError_t launch_exact_topk_large(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin,
+                                    int64_t row_end, int dim, const float* queries, int B, int k, int num_sms,
+                                    double* scores, int32_t* ids, cudaStream_t s) {
+  const int64_t rows = row_end - row_begin;
+  if (B < 1 || k < 1 || rows < 1 || rows > INT32_MAX || !exact_topk_large_supported(dim, key_dtype))
+    return cudaErrorInvalidValue;
+  const bool bf16 = key_dtype == HSD_DTYPE_BF16;
+  int G = kScanMaxBatch;  // queries per scan: the widest group whose fp64 query slab fits
+  while (G > 1 && !exact_scan_supported(G, dim, key_dtype, 1)) --G;
+  G = std::min(G, B);
+  uint64_t *kin = nullptr, *kout = nullptr;
+  uint32_t *vin = nullptr, *vout = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, kout, vin, vout, rows, 0, 64, s);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&kin, (size_t)G * rows * 8, s);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&kout, (size_t)rows * 8, s);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&vin, (size_t)rows * 4, s);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&vout, (size_t)rows * 4, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&tmp, tmp_bytes, s);
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, (int64_t)num_sms * 8);
+  for (int b0 = 0; e == cudaSuccess && b0 < B; b0 += G) {
+    const int nq = std::min(G, B - b0);
+    const ScanPlan p = bf16 ? scan_plan<uint16_t>(rows, dim, nq, num_sms) : scan_plan<float>(rows, dim, nq, num_sms);
+    if (p.S < 2) {
+      e = cudaErrorInvalidValue;
+      break;
+    }
+    CUtensorMap km;
+    const bool ok = bf16 ? tc_make_map_bf16(&km, keys, (uint64_t)n_keys_total, (uint64_t)dim, (uint32_t)p.R)
+                         : tc_make_map(&km, (const float*)keys, (uint64_t)n_keys_total, (uint64_t)dim, (uint32_t)p.R);
+    if (!ok) {
+      e = cudaErrorInvalidValue;
+      break;
+    }
+    ScanArgs a{};
+    a.dim = dim;
+    a.nchunk = bf16 ? (dim + 63) / 64 : (dim + 31) / 32;
+    a.row_begin = row_begin;
+    a.row_end = row_end;
+    a.R = p.R;
+    a.lpw = p.lpw;
+    a.S = p.S;
+    a.ntiles = p.ntiles;
+    a.k = 1;
+    a.queries = queries + (size_t)b0 * dim;
+    a.allkey = kin;
+    switch (nq) {
+#define HSD_SCAN(N)                                                                                  \
+  case N:                                                                                            \
+    e = bf16 ? launch_scan_t<uint16_t, N>(km, p, a, s) : launch_scan_t<float, N>(km, p, a, s);       \
+    break;
+      HSD_SCAN(1)
+      HSD_SCAN(2)
+      HSD_SCAN(3)
+      HSD_SCAN(4)
+#undef HSD_SCAN
+      default: e = cudaErrorInvalidValue;
+    }
+    for (int q = 0; e == cudaSuccess && q < nq; ++q) {
+      iota_ids_kernel<<<blocks, 256, 0, s>>>(vin, rows, row_begin);
+      e = cudaGetLastError();
+      if (e == cudaSuccess)
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, kin + (size_t)q * rows, kout, vin, vout, rows, 0, 64, s);
+      if (e == cudaSuccess) {
+        const size_t o = (size_t)(b0 + q) * k;
+        emit_topk_kernel<<<(int)std::min<int64_t>((k + 255) / 256, (int64_t)num_sms * 8), 256, 0, s>>>(
+            kout, vout, rows, k, scores + o, ids + o);
+        e = cudaGetLastError();
+      }
+    }
+  }
+  if (kin) cudaFreeAsync(kin, s);
+  if (kout) cudaFreeAsync(kout, s);
+  if (vin) cudaFreeAsync(vin, s);
+  if (vout) cudaFreeAsync(vout, s);
+  if (tmp) cudaFreeAsync(tmp, s);
+  return e;
 }
 
 }  // namespace hsd

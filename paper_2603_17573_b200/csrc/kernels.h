@@ -66,6 +66,12 @@ double exact_scan_cost_us(int64_t rows, int dim, int key_dtype, int B);
 cudaError_t launch_exact_scan(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin,
                               int64_t row_end, int dim, const float* queries, int B, int k, void* scratch,
                               int num_sms, double* scores, int32_t* ids, cudaStream_t s);
+// k > HSD_K_MAX: the same scan writes every row's order key, a stable radix
+// sort per query orders (key, id); stream-ordered allocations (cudaMallocAsync).
+bool exact_topk_large_supported(int dim, int key_dtype);
+cudaError_t launch_exact_topk_large(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin,
+                                    int64_t row_end, int dim, const float* queries, int B, int k, int num_sms,
+                                    double* scores, int32_t* ids, cudaStream_t s);
 
 // ---- K2 select: exact top-k from the filter lists -----------------------------
 // Four launches (candidates + threshold, pooled rescoring, exact range

@@ -79,8 +79,21 @@ int main() {
     }
   }
   CHECK(gpu.search_topk(queries[0], HSD_K_MAX).size() == HSD_K_MAX, "k = HSD_K_MAX");
-  CHECK(throws<hsd::InvalidInputError>([&] { gpu.search_topk(queries[0], HSD_K_MAX + 1); }),
-        "k > HSD_K_MAX -> InvalidInputError (documented device limit, no CPU fallback)");
+  // k > HSD_K_MAX: the large-k path (every row's score + a stable radix sort), any k as in store.cpp
+  for (int kk : {HSD_K_MAX + 1, 500, n, n + 3}) {
+    std::vector<hsd::Embedding> q3(queries.begin(), queries.begin() + 5);
+    auto lb = gpu.search_topk_exact_batch(q3, kk);
+    for (int b = 0; b < 5; ++b) {
+      auto want = ref.search_topk_exact(queries[(size_t)b], kk);
+      auto got = b == 0 ? gpu.search_topk_exact(queries[0], kk) : lb[(size_t)b];
+      CHECK(got.size() == want.size(), "large-k hit count k=%d q=%d", kk, b);
+      bool same = got.size() == want.size();
+      for (size_t i = 0; same && i < got.size(); ++i)
+        same = got[i].record_id == want[i].record_id &&
+               std::memcmp(&got[i].score, &want[i].score, sizeof(double)) == 0 && got[i].payload == want[i].payload;
+      CHECK(same, "large-k hits k=%d q=%d", kk, b);
+    }
+  }
   CHECK(throws<hsd::InvalidInputError>([&] { gpu.search_topk_exact(queries[0], 0); }), "k < 1 -> InvalidInputError");
   CHECK(throws<hsd::SchemaError>([&] { gpu.insert(hsd::Embedding(3, 0.0), hsd::Payload{}); }), "dim -> SchemaError");
   hsd::gpu::Collection empty("e", dim);
@@ -119,6 +132,14 @@ int main() {
     }
     std::printf("index recall@%d vs exact: %.3f\n", k, (double)common / total);
     CHECK(gpu.search_topk(queries[0], 0).empty(), "index k = 0 -> no hits (hnsw.cpp:160)");
+    {  // k > HSD_K_MAX through the index: the exact top-k
+      auto got = gpu.search_topk(queries[2], 100);
+      auto want = ref.search_topk_exact(queries[2], 100);
+      bool same = got.size() == want.size();
+      for (size_t i = 0; same && i < got.size(); ++i)
+        same = got[i].record_id == want[i].record_id && std::memcmp(&got[i].score, &want[i].score, 8) == 0;
+      CHECK(same, "index k = 100 -> the exact top-100");
+    }
     hsd::Payload p;
     gpu.insert(queries[0], p);  // mutation drops the index (store.cpp:55)
     CHECK(!gpu.has_hnsw(), "insert drops the index");

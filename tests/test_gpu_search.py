@@ -92,8 +92,10 @@ def test_search_edge_cases(torch):
     assert (ids[:, 10:] == -1).all()
     with pytest.raises(H.InvalidInputError):
         col.search_topk_exact(q, 0)  # store.cpp:60
-    with pytest.raises(H.InvalidInputError):
-        col.search_topk_exact(q, 33)
+    sc, ids = col.search_topk_exact(q, 33)  # k > HSD_K_MAX: the large-k path, same contract
+    np.testing.assert_array_equal(ids[:, :10].cpu().numpy(), oid)
+    np.testing.assert_array_equal(sc[:, :10].cpu().numpy(), osc)
+    assert (ids[:, 10:] == -1).all() and torch.isinf(sc[:, 10:]).all()
     with pytest.raises(H.InvalidInputError):
         col.search_topk_exact(torch.zeros((2, 32), device="cuda"), 3)  # dim mismatch (store.cpp:30)
     misaligned = torch.zeros(3 * 64 + 1, device="cuda")[1:].view(3, 64)  # 4-byte offset view
