@@ -777,7 +777,7 @@ static hsd_status verify_impl(int device, hsd_collection* c, const uint8_t* draf
                               int L, const float* logits, const float* feat_now, const float* feat_prev, int d_f,
                               const int32_t* history, int gap_d, const hsd_verify_params* params, int P,
                               hsd_outcome* out, uint8_t* tokens, void* stream, const double* cos_in = nullptr,
-                              const hsd_verify_params* params_dev = nullptr) {
+                              const hsd_verify_params* params_dev = nullptr, bool early = false) {
   if (L != 7 && L != 21) return fail(HSD_ERR_INVALID_INPUT, "draft length must be 7 or 21, got %d", L);
   if (k < 1 || k > HSD_K_MAX) return fail(HSD_ERR_INVALID_INPUT, "k must be in [1, %d]", HSD_K_MAX);
   if (E < 0) return fail(HSD_ERR_INVALID_INPUT, "negative episode count");
@@ -797,7 +797,7 @@ static hsd_status verify_impl(int device, hsd_collection* c, const uint8_t* draf
     if (st != HSD_OK) return st;
   }
   CU(hsd::launch_verify(ids, E, k, L, c ? c->tokens : nullptr, drafts, logits, feat_now, feat_prev, d_f, history, gap_d, dp, P,
-                        need_cos, out, tokens, (cudaStream_t)stream, cos_in));
+                        need_cos, out, tokens, (cudaStream_t)stream, cos_in, early));
   return HSD_OK;
 }
 
@@ -1048,6 +1048,8 @@ struct hsd_engine {
   // engine issues its steps on one stream at a time.
   Scratch scr;
   hsd_verify_params* vp = nullptr;
+  hsd_verify_params vp_last{};  // the values *vp holds (stream-ordered), valid when vp_set
+  bool vp_set = false;
 };
 
 static constexpr int kStepEvents = 6;
@@ -1214,7 +1216,13 @@ static hsd_status step_impl(hsd_engine* e, int B, const hsd_step_io* io, const h
   // on the retrieval: run them on a side stream so they hide under K1 (K5's
   // Gauss-Newton loop is latency-bound; the similarity would otherwise be a
   // serial feature stream inside K4 after K2).
-  const bool cos_side = vp->skip_enabled && e->d_f > 0 && io->feat_now && io->feat_prev;
+  // Small batches on the exact scan (K1x, config 1): K4 is launched as K1x's
+  // programmatic dependent and runs its feature / logits phases while K1x
+  // scans (the similarity in K4 itself), so only the ids -> sweep tail follows
+  // the scan; K5 alone takes the side stream, joined after K4.
+  static const bool no_early = getenv("HSD_NO_EARLY_VERIFY") != nullptr;  // A/B measurements only
+  const bool early = !no_early && B <= hsd::kScanMaxBatch && use_exact_scan(e->c, B, e->k, e->c->n);
+  const bool cos_side = !early && vp->skip_enabled && e->d_f > 0 && io->feat_now && io->feat_prev;
   const bool use_side = io->xyz || cos_side;
   if (use_side) {
     if (!e->side) {
@@ -1243,11 +1251,12 @@ static hsd_status step_impl(hsd_engine* e, int B, const hsd_step_io* io, const h
   st = search_impl(e->c, io->queries, B, e->k, 0, e->c->n, io->scores, io->ids, s, ev ? &marks : nullptr,
                    k5_blocks, nullptr, &e->scr);  // K1+K2
   if (st != HSD_OK) return st;
-  if (use_side) CU(cudaStreamWaitEvent(s, e->join, 0));
+  if (use_side && !early) CU(cudaStreamWaitEvent(s, e->join, 0));
   st = verify_impl(e->c->device, e->c, nullptr, io->ids, B, e->k, e->L, io->logits, io->feat_now, io->feat_prev,
                    e->d_f, io->history, gap_d, vp, 1, io->out, io->tokens, stream, cos_side ? e->cos : nullptr,
-                   vp_dev);  // K4
+                   vp_dev, early);  // K4
   if (st != HSD_OK) return st;
+  if (use_side && early) CU(cudaStreamWaitEvent(s, e->join, 0));
   if (ev) {
     if (!use_side) {
       CU(cudaEventRecord(ev[4], s));
@@ -1270,8 +1279,14 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
   if (st != HSD_OK) return st;
   st = check_verify_params(vp, 1);
   if (st != HSD_OK) return st;
-  // stream-ordered copy: the previous steps' verify kernels read their own values first
-  CU(cudaMemcpyAsync(e->vp, vp, sizeof *vp, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  // stream-ordered copy: the previous steps' verify kernels read their own
+  // values first.  Unchanged parameters (every step of a run) skip it: a
+  // pageable 64-B copy costs ~1.4 us of stream time at config 1.
+  if (!e->vp_set || std::memcmp(&e->vp_last, vp, sizeof *vp) != 0) {
+    CU(cudaMemcpyAsync(e->vp, vp, sizeof *vp, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    e->vp_last = *vp;
+    e->vp_set = true;
+  }
   return step_impl(e, B, io, vp, e->vp, mp, nb, gap_d, stream);
 }
 

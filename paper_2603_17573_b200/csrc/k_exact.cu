@@ -243,6 +243,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
   }
   __syncthreads();
   dev::pdl_wait();  // the queries may come from the previous kernel
+  dev::pdl_trigger();  // an early K4 (engine step) may start its logits / feature phases under the scan
 
   if (warp == kCW) {
     // ---- TMA producer

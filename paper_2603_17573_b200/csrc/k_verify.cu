@@ -248,15 +248,19 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
                                                const int32_t* __restrict__ history, int gap_d,
                                                const hsd_verify_params* __restrict__ params, int P, int need_cos,
                                                const double* __restrict__ cos_in, hsd_outcome* __restrict__ out,
-                                               uint8_t* __restrict__ tok_out, WarpScratch& W) {
+                                               uint8_t* __restrict__ tok_out, WarpScratch& W, bool early) {
   const int lane = threadIdx.x & 31;
-  const bool feat_first = ((threadIdx.x >> 5) & 1) == 0;
+  // early: launched (PDL) while the search still runs — the features and
+  // logits (inputs of the step) are reduced first, then the warp waits for
+  // the search grid and only the ids -> token rows -> sweep remain after it
+  const bool feat_first = early || ((threadIdx.x >> 5) & 1) == 0;
   const bool own_cos = need_cos && !cos_in && fnE && fpE;
   // The candidate ids (and then their token rows) do not depend on the logits
   // or the features: issue them first so their round trips overlap the
   // logits / feature phases instead of following them.
   const int32_t* my_ids = ids + (size_t)e * k;
-  const int id = lane < k ? my_ids[lane] : -1;
+  int id = -1;
+  if (!early) id = lane < k ? my_ids[lane] : -1;
   double cosv = -2.0;
   if (need_cos && cos_in) cosv = cos_in[e];  // cos_kernel's pass (off the critical path in the engine step)
   // ---- the candidates' draft tokens: cp.async into this warp's staging rows
@@ -286,7 +290,7 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
   const int* greedy = W.greedy;  // positions < L (shared memory, no per-thread copy)
   for (int ph = 0; ph < 2; ++ph) {
     if ((ph == 0) == feat_first) {
-      if (ph == 0) stage_tokens();  // even warps: the token rows land under the feature stream
+      if (ph == 0 && !early) stage_tokens();  // even warps: the token rows land under the feature stream
       if (own_cos) cosv = episode_cos_fast(fnE, fpE, d_f, lane, params, P);
       continue;
     }
@@ -307,6 +311,11 @@ __device__ __forceinline__ void verify_episode(int e, int E, int k, int L, const
         const int bi = dev::warp_argmax256(a[u], c[u], lane);
         if (lane == 0 && p0 + u < L) W.greedy[p0 + u] = bi;
       }
+    }
+    if (early) {  // the search's ids are complete and visible past this point
+      dev::pdl_wait();
+      id = lane < k ? my_ids[lane] : -1;
+      stage_tokens();
     }
     // ---- the gathered draft tokens have landed: dedup (independent of params)
     n_cand = __popc(__ballot_sync(0xffffffffu, id >= 0));  // ids are rank-ordered, -1 padding last
@@ -485,16 +494,22 @@ __global__ void __launch_bounds__(kThreads, 1024 / kThreads) verify_kernel(const
                                                              const hsd_verify_params* __restrict__ params, int P,
                                                              int need_cos, const double* __restrict__ cos_in,
                                                              hsd_outcome* __restrict__ out,
-                                                             uint8_t* __restrict__ tok_out) {
+                                                             uint8_t* __restrict__ tok_out, int early) {
   __shared__ WarpScratch sw[kWarps];
-  dev::pdl_wait();  // the retrieved ids (K2)
+  // early != 0: every input but the ids predates the previous kernel, so
+  // verify_episode waits only before the ids (see there); the PDL trigger of
+  // the previous grid then lets the logits / feature phases run under it
+  if (!early) dev::pdl_wait();  // the retrieved ids (K2)
   dev::pdl_trigger();
   const int warp = threadIdx.x >> 5;
   const int e = blockIdx.x * kWarps + warp;
-  if (e >= E) return;
+  if (e >= E) {
+    if (early) dev::pdl_wait();  // no access, but no grid outlives its predecessor's inputs either
+    return;
+  }
   verify_episode(e, E, k, L, ids, tokens, cand_tokens, logits + (size_t)e * L * 256,
                  feat_now ? feat_now + (size_t)e * d_f : nullptr, feat_prev ? feat_prev + (size_t)e * d_f : nullptr,
-                 d_f, history, gap_d, params, P, need_cos, cos_in, out, tok_out, sw[warp]);
+                 d_f, history, gap_d, params, P, need_cos, cos_in, out, tok_out, sw[warp], early != 0);
 }
 
 // should_skip's similarity for every episode as its own pass: one CTA per
@@ -576,11 +591,11 @@ cudaError_t launch_cos(const float* feat_now, const float* feat_prev, int E, int
 cudaError_t launch_verify(const int32_t* ids, int E, int k, int L, const uint8_t* tokens, const uint8_t* cand_tokens,
                           const float* logits, const float* feat_now, const float* feat_prev, int d_f,
                           const int32_t* history, int gap_d, const hsd_verify_params* params_dev, int P, int need_cos,
-                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s, const double* cos_in) {
+                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s, const double* cos_in, bool early) {
   if (E <= 0) return cudaSuccess;
   return launch_pdl(verify_kernel, dim3((E + kWarps - 1) / kWarps), dim3(kThreads), 0, s, ids, E, k, L, tokens,
                     cand_tokens, logits, feat_now, feat_prev, d_f, history, gap_d, params_dev, P, need_cos, cos_in, out,
-                    tok_out);
+                    tok_out, early ? 1 : 0);
 }
 
 // Pre-gather the payload tokens of a [n] id list (sharded search records).

@@ -167,7 +167,11 @@ cudaError_t launch_ivf_sort(const int32_t* assign, int64_t n, int nlist, int32_t
 cudaError_t launch_verify(const int32_t* ids, int E, int k, int L, const uint8_t* tokens, const uint8_t* cand_tokens,
                           const float* logits, const float* feat_now, const float* feat_prev, int d_f,
                           const int32_t* history, int gap_d, const hsd_verify_params* params_dev, int P, int need_cos,
-                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s, const double* cos_in = nullptr);
+                          hsd_outcome* out, uint8_t* tok_out, cudaStream_t s, const double* cos_in = nullptr,
+                          bool early = false);
+// early: K4 is the programmatic dependent of the search's last kernel and
+// reduces its logits / features (inputs of the step) before it waits for the
+// search grid; only the ids -> token rows -> acceptance sweep follow it.
 // should_skip similarity [E] (exactly rounded, same bits as K4's in-kernel dot) as a separate pass
 cudaError_t launch_cos(const float* feat_now, const float* feat_prev, int E, int d_f, double* cos_out,
                        cudaStream_t s);
