@@ -111,6 +111,8 @@ def parse():
             a.batch = 1
         if "--steps" not in given:
             a.steps = 200
+        if "--e2e-steps" not in given:
+            a.e2e_steps = 200  # one 200-step episode through the host-buffer API
     if a.config == "c5":
         world = int(os.environ.get("WORLD_SIZE", 1))
         if "--n" not in given:

@@ -110,6 +110,29 @@ def main():
         ts = np.array([x.elapsed_time(y) * 1e3 for x, y in evs])
         res[f"bench-like 200 steps{' + NVML poller' if poll else ''}"] = (
             float(np.median(ts)), float(ts.min()), float(ts.mean()), float(np.percentile(ts, 90)))
+    # host cost per call (wall clock of the enqueue loop, then the total with the sync)
+    import time
+    pin = lambda t: t.cpu().pin_memory()  # noqa: E731
+    hin = dict(queries=pin(q), logits=pin(lg), feat_now=pin(now), feat_prev=pin(prev), xyz=pin(xyz),
+               history=pin(hist))
+    hout = {kk: torch.empty_like(v, device="cpu").pin_memory() for kk, v in outs.items()}
+    hb = H.StepBuffers(**hin, **hout)
+    host = {}
+    for name, fn in (("eng.step (device buffers)", lambda: eng.step(B, full, vp_skip, gap_d=1)),
+                     ("eng.step_host_async (pinned host buffers)", lambda: eng.step_host_async(B, hb, vp_skip, gap_d=1))):
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(200):
+            fn()
+        t1 = time.perf_counter()
+        eng.sync()
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        host[name] = ((t1 - t0) / 200 * 1e6, (t2 - t0) / 200 * 1e6)
+    for name, (enq, tot) in host.items():
+        print(f"host   {name:42s} enqueue {enq:7.2f} us/call   with sync {tot:7.2f} us/call")
     tag = "base" if os.environ.get("HSD_NO_EARLY_VERIFY") else "early"
     for name, (med, mn, mean, p90) in res.items():
         print(f"{tag:5s}  {name:42s} median {med:7.2f}  min {mn:7.2f}  mean {mean:7.2f}  p90 {p90:7.2f} us")
