@@ -384,7 +384,11 @@ hsd_status search_impl(hsd_collection* c, const float* queries, int B, int k, in
       pb = *pub;
       pb.q_offset = b0;
     }
-    CU(hsd::launch_select(sc->partial, lists, Bs, k, c->keys, c->dtype, c->dim, q, c->maxnorm, gamma, geom,
+    // fp32 keys converted to bf16 on chip (CTA-pair passes): the bf16-copy bound
+    const double g = !c->shadow && hsd::sim_wide_converts(fdtype, Bs, c->dim)
+                         ? hsd::sim_wide_gamma(c->dim, HSD_DTYPE_BF16 | kShadowGamma)
+                         : gamma;
+    CU(hsd::launch_select(sc->partial, lists, Bs, k, c->keys, c->dtype, c->dim, q, c->maxnorm, g, geom,
                           scores + (size_t)b0 * k, ids + (size_t)b0 * k, sc->stats, sc->sel, nsm, s,
                           pub ? &pb : nullptr));
   }

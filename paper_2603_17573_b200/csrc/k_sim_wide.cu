@@ -379,25 +379,62 @@ constexpr int kPairHalfQ = kPairQ / 2;      // B rows staged per CTA
 constexpr int kPairQTile = kPairHalfQ * 128;
 constexpr int kPairKS = 8, kPairQS = 4;
 
-struct __align__(1024) PairSmem {
-  uint8_t kbuf[kPairKS][kKeyTile];
-  uint8_t qbuf[kPairQS][kPairQTile];
+// kConv: fp32 keys converted to bf16 on chip.  Per 64-column k-chunk the key
+// producer TMA-loads two fp32 boxes (128 rows x 32 columns each, 32 KB) into
+// a raw ring; four converter warps round them to bf16 (RN-even, the same
+// rounding as the bf16 filter copy) into the SWIZZLE_128B K-major tile that
+// kind::f16 reads, so the pair runs bf16 MMAs (half the tensor work of TF32)
+// while HBM still carries each fp32 key once.  Queries: the bf16 slab.  The
+// filter bound is the bf16-copy one (both operands bf16-rounded).
+constexpr int kConvRawS = 3, kConvKS = 3, kConvQS = 3;
+constexpr int kConvWarps = 4;
+constexpr int kConvThreads = kThreads + 32 * kConvWarps;
+
+template <bool kConv>
+struct __align__(1024) PairSmemT {
+  static constexpr int KS = kConv ? kConvKS : kPairKS;
+  static constexpr int QS = kConv ? kConvQS : kPairQS;
+  static constexpr int RS = kConv ? kConvRawS : 0;
+  uint8_t kbuf[KS][kKeyTile];
+  uint8_t qbuf[QS][kPairQTile];
+  uint8_t raw[RS > 0 ? RS : 1][kConv ? 2 * kKeyTile : 16];  // 1-KB aligned (after whole 16-KB tiles)
   float stg[kBM * kStg];
-  uint64_t k_full[kPairKS], k_empty[kPairKS];
-  uint64_t q_full[kPairQS], q_empty[kPairQS];
+  uint64_t k_full[KS], k_empty[KS];
+  uint64_t q_full[QS], q_empty[QS];
+  uint64_t raw_full[RS > 0 ? RS : 1], raw_empty[RS > 0 ? RS : 1];
   uint64_t acc_full[2], acc_empty[2];
   uint32_t tmem_base;
 };
+using PairSmem = PairSmemT<false>;
+static_assert(sizeof(PairSmemT<true>) + 1024 <= 227 * 1024, "conversion pair kernel exceeds shared memory");
 
-template <bool kBf16, int kG>
-__global__ void __launch_bounds__(kThreads, 1)
+// Arrive on the pair leader's barrier without a cluster-scope release (no
+// MEMBAR.GPU): the converter's generic stores are ordered for the tensor
+// cores by fence.proxy.async, and the arrive / wait pair at the default
+// (CTA) scope then orders them for the MMA issue — the remote-arrive form of
+// CUTLASS's ClusterBarrier.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x (low half) = lo
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+template <bool kBf16, int kG, bool kConv = false>
+__global__ void __launch_bounds__(kConv ? kConvThreads : kThreads, 1)
     sim_pair_kernel(const __grid_constant__ CUtensorMap keys_map, const __grid_constant__ CUtensorMap q_map,
                     int64_t row_begin, int64_t row_end, int dim, int B, int64_t blocks_per_pair,
                     int per_group, uint64_t* __restrict__ partial) {
-  constexpr int kBK = kBf16 ? 64 : 32;
+  static_assert(!kConv || (!kBf16 && kG == 1), "on-chip conversion: fp32 keys, one pair per cluster");
+  constexpr bool kF16 = kBf16 || kConv;  // kind::f16 MMAs
+  constexpr int kBK = kF16 ? 64 : 32;
+  constexpr int KS = PairSmemT<kConv>::KS, QS = PairSmemT<kConv>::QS;
   constexpr int kMyQ = kPairQ / kEpiWarps;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  PairSmemT<kConv>& S =
+      *reinterpret_cast<PairSmemT<kConv>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cr = (int)cluster_ctarank();
   const int rank = cr & 1;           // 0 = pair leader
@@ -427,13 +464,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kc0 = (int)(((int64_t)unit * nk) / n_units);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kPairKS; ++i) {
-      mbar_init(&S.k_full[i], 1);
+    for (int i = 0; i < KS; ++i) {
+      // kConv: both CTAs' converter warps arrive on the leader's k_full
+      mbar_init(&S.k_full[i], kConv ? 2 * kConvWarps : 1);
       mbar_init(&S.k_empty[i], kG);
     }
-    for (int i = 0; i < kPairQS; ++i) {
+    for (int i = 0; i < QS; ++i) {
       mbar_init(&S.q_full[i], 1);
       mbar_init(&S.q_empty[i], 1);
+    }
+    if constexpr (kConv) {
+      for (int i = 0; i < kConvRawS; ++i) {
+        mbar_init(&S.raw_full[i], 1);
+        mbar_init(&S.raw_empty[i], kConvWarps);
+      }
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&S.acc_full[i], 1);
@@ -464,9 +508,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t st = 0; st < steps; ++st) {
         const int row = (int)(row_begin + (blk0 + 2 * st + rank) * kBM);
         for (int kc = 0; kc < nk; ++kc, ++tile) {
+          const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
+          if constexpr (kConv) {
+            // raw fp32 halves of the chunk into this CTA's own ring
+            mbar_wait(&S.raw_empty[ks], kph ^ 1);
+            mbar_expect_tx(&S.raw_full[ks], 2 * kKeyTile);
+            tma_load_2d(&S.raw[ks][0], &keys_map, &S.raw_full[ks], c * kBK, row, pol);
+            tma_load_2d(&S.raw[ks][kKeyTile], &keys_map, &S.raw_full[ks], c * kBK + 32, row, pol);
+            if (++ks == kConvRawS) {
+              ks = 0;
+              kph ^= 1;
+            }
+            continue;
+          }
           mbar_wait(&S.k_empty[ks], kph ^ 1);
           if (rank == 0) mbar_expect_tx(&S.k_full[ks], 2 * kKeyTile);
-          const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
           const uint32_t bar = mapa_shared(smem_u32(&S.k_full[ks]), leader);
           if constexpr (kG > 1) {
             if ((int)(tile % kG) == grp)
@@ -474,7 +530,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             tma_load_2d_pair(&S.kbuf[ks][0], &keys_map, bar, c * kBK, row, pol);
           }
-          if (++ks == kPairKS) {
+          if (++ks == KS) {
             ks = 0;
             kph ^= 1;
           }
@@ -496,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int c = kc + kc0 < nk ? kc + kc0 : kc + kc0 - nk;
           tma_load_2d_pair(&S.qbuf[qs][0], &q_map, mapa_shared(smem_u32(&S.q_full[qs]), leader), c * kBK,
                            q_base + rank * n_half, pol);
-          if (++qs == kPairQS) {
+          if (++qs == QS) {
             qs = 0;
             qph ^= 1;
           }
@@ -505,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ======================= MMA issuer (leader only)
     if (rank == 0) {
-      const uint32_t idesc = kBf16 ? bf16_idesc(2 * kBM, n_mma) : tf32_idesc(2 * kBM, n_mma);
+      const uint32_t idesc = kF16 ? bf16_idesc(2 * kBM, n_mma) : tf32_idesc(2 * kBM, n_mma);
       const uint64_t adesc0 = sw128_desc(&S.kbuf[0][0]);
       const uint64_t bdesc0 = sw128_desc(&S.qbuf[0][0]);
       int ks = 0, qs = 0;
@@ -525,24 +581,68 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d = tmem + buf * kPairQ;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            if (kBf16)
+            if (kF16)
               mma2_ss_f16(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
             else
               mma2_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
           }
           tc_commit2_mc(&S.k_empty[ks], all_mask);  // every CTA's slot ks: kG releases complete it
           tc_commit2_mc(&S.q_empty[qs], pair_mask);
-          if (++ks == kPairKS) {
+          if (++ks == KS) {
             ks = 0;
             kph ^= 1;
           }
-          if (++qs == kPairQS) {
+          if (++qs == QS) {
             qs = 0;
             qph ^= 1;
           }
         }
         tc_commit2_mc(&S.acc_full[buf], pair_mask);
       }
+    }
+  } else if (kConv && warp >= 4 + kEpiWarps) {
+    // ======================= converters: raw fp32 halves -> bf16 K-major SW128 tile
+    if constexpr (kConv) {
+      int rs = 0, ks = 0;
+      uint32_t rph = 0, kph = 0;
+      for (int64_t st = 0; st < steps; ++st)
+        for (int kc = 0; kc < nk; ++kc) {
+          mbar_wait(&S.raw_full[rs], rph);
+          mbar_wait(&S.k_empty[ks], kph ^ 1);  // the MMAs have read this bf16 stage
+          const uint8_t* raw = &S.raw[rs][0];
+          uint8_t* dst = &S.kbuf[ks][0];
+          // lane = (row parity rsel, fp32 box h, fp32 16-B chunk x): one 16-B
+          // load of 4 keys, 8 B of bf16 out — the half (x & 1) of bf16 chunk
+          // j = 4h + x / 2.  SWIZZLE_128B puts 16-B chunk c of row r at
+          // c ^ (r & 7) in both tiles, so every 8-lane load phase reads 8
+          // distinct chunks of one row and every 16-lane store phase writes
+          // one whole 128-B bf16 row: no bank conflicts either way.
+          const int x = lane & 7, h = (lane >> 3) & 1, rsel = lane >> 4;
+          const int cw = warp - 4 - kEpiWarps;
+#pragma unroll 8
+          for (int i = 0; i < kBM / (2 * kConvWarps); ++i) {
+            const int r = (i * kConvWarps + cw) * 2 + rsel, sw = r & 7;
+            const float4 a = *reinterpret_cast<const float4*>(raw + h * kKeyTile + r * 128 + ((x ^ sw) << 4));
+            const int j = 4 * h + (x >> 1);
+            *reinterpret_cast<uint2*>(dst + r * 128 + ((j ^ sw) << 4) + (x & 1) * 8) =
+                make_uint2(bf16x2_rn(a.x, a.y), bf16x2_rn(a.z, a.w));
+          }
+          // the tile's generic stores -> visible to the tensor cores (async proxy)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&S.raw_empty[rs]);
+            mbar_arrive_remote(mapa_shared(smem_u32(&S.k_full[ks]), leader));
+          }
+          if (++rs == kConvRawS) {
+            rs = 0;
+            rph ^= 1;
+          }
+          if (++ks == KS) {
+            ks = 0;
+            kph ^= 1;
+          }
+        }
     }
   } else if (warp >= 4) {
     // ======================= epilogue (8 warps per CTA, its own key block)
@@ -673,17 +773,17 @@ cudaError_t launch_ns(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, 
   return cudaGetLastError();
 }
 
-template <bool kBf16, int kG>
+template <bool kBf16, int kG, bool kConv = false>
 cudaError_t launch_pair(const CUtensorMap& km, const CUtensorMap& qm, int64_t rb, int64_t re, int dim, int B,
                         int lists, int64_t per_pair, uint64_t* partial, cudaStream_t s) {
   const int per_group = (((B + kG - 1) / kG) + 15) & ~15;  // <= 256: kG = ceil(B / 256)
-  const size_t smem = sizeof(PairSmem) + 1024;
-  auto kern = sim_pair_kernel<kBf16, kG>;
+  const size_t smem = sizeof(PairSmemT<kConv>) + 1024;
+  auto kern = sim_pair_kernel<kBf16, kG, kConv>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)(lists * kG));  // lists = 2 x clusters; a cluster is kG pairs
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kConv ? kConvThreads : kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
@@ -797,6 +897,17 @@ static int max_active_clusters(int G, int num_sms) {
 
 static bool use_pair(int B) { return B > 128 && pair_enabled(); }
 
+// fp32 keys in the pair kernel (one pair per cluster, 129..256 queries):
+// converted to bf16 on chip (kind::f16) unless HSD_PAIR_CONVERT=0 (TF32).
+static bool pair_convert_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HSD_PAIR_CONVERT");
+    v = (e && !strcmp(e, "0")) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // Clusters of G CTA pairs (2G CTAs) resident at once, cached per G.
 static int max_active_pair_clusters(int G, int num_sms) {
   static int cache[5] = {0, 0, 0, 0, 0};
@@ -843,6 +954,11 @@ int sim_wide_lists(int B, int64_t rows, int num_sms) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(blocks, max_active_clusters(g, num_sms)));
 }
 
+bool sim_wide_converts(int key_dtype, int B, int dim) {
+  // dim % 8: the bf16 query slab's rows must be 16-B multiples (TMA stride)
+  return key_dtype == HSD_DTYPE_F32 && dim % 8 == 0 && use_pair(B) && wide_groups(B) == 1 && pair_convert_enabled();
+}
+
 double sim_wide_gamma(int dim, int key_dtype) {
   // Relative forward error of the filter score S~ against the real dot S of
   // the stored keys and the fp32 query: |S - S~| <= gamma * sum|k_i q_i|.
@@ -881,9 +997,15 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
   const bool bf16 = key_dtype == HSD_DTYPE_BF16;
   if (bf16 && dim % 8) return cudaErrorInvalidValue;  // TMA row stride must be a multiple of 16 B
   const bool pair = use_pair(B) && !dump && lists % 2 == 0;
+  const bool conv = pair && sim_wide_converts(key_dtype, B, dim);
   const uint32_t qbox = pair ? (uint32_t)kPairHalfQ : (uint32_t)box;  // a pair CTA stages half the queries
   CUtensorMap km, qm;
-  if (bf16) {
+  if (conv) {  // fp32 key tiles (converted on chip), bf16 query slab
+    pad_queries_bf16_kernel<<<rows, kPadThreads, 0, s>>>(queries, B, dim, (uint16_t*)scratch);
+    if (!tc_make_map(&km, (const float*)keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
+        !tc_make_map_bf16(&qm, scratch, (uint64_t)rows, (uint64_t)dim, qbox))
+      return cudaErrorInvalidValue;
+  } else if (bf16) {
     pad_queries_bf16_kernel<<<rows, kPadThreads, 0, s>>>(queries, B, dim, (uint16_t*)scratch);
     if (!tc_make_map_bf16(&km, keys, (uint64_t)n_keys_total, (uint64_t)dim, kBM) ||
         !tc_make_map_bf16(&qm, scratch, (uint64_t)rows, (uint64_t)dim, qbox))
@@ -903,6 +1025,7 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
     const int64_t pairs = lists / 2;
     const int64_t per_pair = ((n_blocks + pairs - 1) / pairs + 1) & ~(int64_t)1;  // even: whole block pairs
     if (geom) *geom = ListGeom{row_begin, row_end, per_pair, 2};
+    if (conv) return launch_pair<false, 1, true>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s);
     switch (groups) {
 #define HSD_PAIR(G)                                                                                        \
   case G:                                                                                                  \

@@ -51,6 +51,9 @@ void sim_wide_set_single(bool single);  // ablation: no CTA-pair kernels
 // partial lists (= persistent CTAs, or clusters when B > 256) of a wide pass
 int sim_wide_lists(int B, int64_t rows, int num_sms);
 double sim_wide_gamma(int dim, int key_dtype);
+// true when a pass of B queries over fp32 keys converts the key tiles to bf16
+// on chip (the CTA-pair kernel): its filter bound is the bf16-copy one
+bool sim_wide_converts(int key_dtype, int B, int dim);
 size_t sim_wide_scratch_bytes(int dim);
 cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_total, int64_t row_begin, int64_t row_end,
                             int dim, const float* queries, int B, int lists, void* scratch, uint64_t* partial,

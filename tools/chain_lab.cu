@@ -10,8 +10,12 @@
 //   MODE 3  replica with every lane active (lpw = 32)
 //   MODE 4  replica, query operands two groups ahead
 //   MODE 5  replica, the next sub widened in the second half of the current one
+//   MODE 6  replica, widening by integer bit moves (x * 2^-896 exactly; the
+//           queries carry the 2^896) instead of F2F on the fp64 pipe
+//   MODE 7  MODE 6 with a fixed ring slot
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdio>
 
 constexpr int kSub = 32;
@@ -27,7 +31,22 @@ __device__ __forceinline__ void widen4(const Raw& r, int g, double* out) {
   out[3] = (double)__uint_as_float(x.w);
 }
 
-template <bool kNext, int kAhead, bool kLate = false>
+// fp32 x -> the double x * 2^-896, exactly, for every finite x (zero and
+// subnormals included): the fp32 exponent / fraction fields move into the
+// double's unchanged, so only the bias differs.  Integer ops, not the fp64 pipe.
+__device__ __forceinline__ double widen_bits(uint32_t u) {
+  const uint32_t hi = (uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu;
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+__device__ __forceinline__ void widen4b(const Raw& r, int g, double* out) {
+  const uint4 x = r.v[g];
+  out[0] = widen_bits(x.x);
+  out[1] = widen_bits(x.y);
+  out[2] = widen_bits(x.z);
+  out[3] = widen_bits(x.w);
+}
+
+template <bool kNext, int kAhead, bool kLate = false, bool kBits = false>
 __device__ __forceinline__ void chain_sub(const double (&kc)[kSub], double (&kn)[kSub], const Raw& rn,
                                           const double* __restrict__ q64, int col0, double& acc) {
   double2 qa[kAhead][2];
@@ -47,7 +66,12 @@ __device__ __forceinline__ void chain_sub(const double (&kc)[kSub], double (&kn)
     acc = __fma_rn(qa[0][0].y, kc[4 * g + 1], acc);
     acc = __fma_rn(qa[0][1].x, kc[4 * g + 2], acc);
     acc = __fma_rn(qa[0][1].y, kc[4 * g + 3], acc);
-    if (kNext && !kLate) widen4(rn, g, &kn[4 * g]);
+    if (kNext && !kLate) {
+      if (kBits)
+        widen4b(rn, g, &kn[4 * g]);
+      else
+        widen4(rn, g, &kn[4 * g]);
+    }
     if (kNext && kLate && g >= 4) {  // the next sub's rows: widened in the second half (its loads have landed)
       widen4(rn, 2 * (g - 4), &kn[8 * (g - 4)]);
       widen4(rn, 2 * (g - 4) + 1, &kn[8 * (g - 4) + 4]);
@@ -79,13 +103,14 @@ __global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw
   const unsigned char* rowbase = smem + (size_t)(lane < lpw ? rr : 0) * 128;
   int wslot = 0;
   auto load_sub = [&](int u, Raw& r) {
-    const unsigned char* rowp = rowbase + (size_t)(MODE == 1 ? 0 : wslot) * stage_bytes;
+    const unsigned char* rowp = rowbase + (size_t)(MODE == 1 || MODE == 7 ? 0 : wslot) * stage_bytes;
 #pragma unroll
     for (int c = 0; c < 8; ++c) r.v[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
-    if (MODE != 1 && ++wslot == S) wslot = 0;
+    if (MODE != 1 && MODE != 7 && ++wslot == S) wslot = 0;
   };
   constexpr int kAhead = MODE == 4 ? 2 : 1;
   constexpr bool kLate = MODE == 5;
+  constexpr bool kBits = MODE == 6 || MODE == 7;
   double acc = 0.0;
   double ka[kSub], kb[kSub];
   Raw raw;
@@ -94,12 +119,12 @@ __global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw
   for (int g = 0; g < kSub / 4; ++g) widen4(raw, g, &ka[4 * g]);
   for (int u = 0; u < U; u += 2) {
     if (MODE != 2) load_sub(u + 1, raw);
-    chain_sub<MODE != 2, kAhead, kLate>(ka, kb, raw, q64, (u * kSub) & 4095, acc);
+    chain_sub<MODE != 2, kAhead, kLate, kBits>(ka, kb, raw, q64, (u * kSub) & 4095, acc);
     if (MODE != 2) load_sub(u + 2, raw);
     if (MODE == 2)
       chain_sub<false, kAhead>(ka, kb, raw, q64, ((u + 1) * kSub) & 4095, acc);
     else
-      chain_sub<true, kAhead, kLate>(kb, ka, raw, q64, ((u + 1) * kSub) & 4095, acc);
+      chain_sub<true, kAhead, kLate, kBits>(kb, ka, raw, q64, ((u + 1) * kSub) & 4095, acc);
   }
   if (acc == 1.2345) out[0] = acc;
 }
@@ -137,5 +162,7 @@ int main() {
   run<3>("replica, every lane", 32);
   run<4>("replica, q two groups ahead", 18);
   run<5>("replica, next sub widened in the second half", 18);
+  run<6>("replica, integer widening (no F2F)", 18);
+  run<7>("integer widening, fixed ring slot", 18);
   return 0;
 }
