@@ -486,10 +486,11 @@ class Collection:
         return (_from_ptr(fp.value, (n, d.value), torch.float32, dev), _from_ptr(hp.value, (n,), torch.uint8, dev))
 
     def search_plan(self, B: int, k: int, rows: int = -1) -> str:
-        """The search path a batch of B queries takes: "scan" (K1x exact scan) or "filter" (K1 + K2)."""
+        """The search path a batch of B queries takes: "scan" (K1x exact scan), "filter" (K1 + K2) or
+        "filter_bf16_onchip" (K1 + K2, fp32 key tiles converted to bf16 on chip by the CTA-pair filter)."""
         v = C.c_int()
         check(lib().hsd_search_plan(self._h, int(B), int(k), int(rows), C.byref(v)))
-        return "scan" if v.value else "filter"
+        return {1: "scan", 2: "filter_bf16_onchip"}.get(v.value, "filter")
 
     def search_stats(self, stream=None, reset=False) -> dict:
         """Accumulated search statistics of `stream` (hsd_search_stats; synchronizes)."""

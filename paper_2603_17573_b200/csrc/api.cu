@@ -678,6 +678,8 @@ hsd_status hsd_set_sim_path(int path) {
 hsd_status hsd_search_plan(hsd_collection* c, int B, int k, int64_t rows, int* exact_scan) {
   if (!c || !exact_scan) return fail(HSD_ERR_INVALID_INPUT, "null pointer");
   *exact_scan = use_exact_scan(c, B, k, rows < 0 ? c->n : rows) ? 1 : 0;
+  const int Bs = std::min(B, hsd::kMaxBatchPass);
+  if (!*exact_scan && !c->shadow && hsd::sim_wide_converts(c->dtype, Bs, c->dim)) *exact_scan = 2;
   return HSD_OK;
 }
 
