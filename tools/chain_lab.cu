@@ -13,6 +13,10 @@
 //   MODE 6  replica, widening by integer bit moves (x * 2^-896 exactly; the
 //           queries carry the 2^896) instead of F2F on the fp64 pipe
 //   MODE 7  MODE 6 with a fixed ring slot
+//   MODE 8  simple loop: per 4 steps one 16-B row load + two broadcast query
+//           loads + 4 F2F + 4 DFMA, straight from the ring slot (the compiler
+//           schedules; no ping-pong widening)
+//   MODE 9  MODE 8 with the segment loop unrolled by 2
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -108,6 +112,28 @@ __global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw
     for (int c = 0; c < 8; ++c) r.v[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
     if (MODE != 1 && MODE != 7 && ++wslot == S) wslot = 0;
   };
+  if constexpr (MODE >= 8) {
+    double acc8 = 0.0;
+    int slot = 0;
+#pragma unroll (MODE == 9 ? 2 : 1)
+    for (int u = 0; u < U; ++u) {
+      const unsigned char* rowp = rowbase + (size_t)slot * stage_bytes;
+      const double* q = q64 + ((u * kSub) & 4095);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(rowp + ((g ^ swz) << 4));
+        const double2 q0 = *reinterpret_cast<const double2*>(q + 4 * g);
+        const double2 q1 = *reinterpret_cast<const double2*>(q + 4 * g + 2);
+        acc8 = __fma_rn(q0.x, (double)v.x, acc8);
+        acc8 = __fma_rn(q0.y, (double)v.y, acc8);
+        acc8 = __fma_rn(q1.x, (double)v.z, acc8);
+        acc8 = __fma_rn(q1.y, (double)v.w, acc8);
+      }
+      if (++slot == S) slot = 0;
+    }
+    if (acc8 == 1.2345) out[0] = acc8;
+    return;
+  }
   constexpr int kAhead = MODE == 4 ? 2 : 1;
   constexpr bool kLate = MODE == 5;
   constexpr bool kBits = MODE == 6 || MODE == 7;
@@ -164,5 +190,7 @@ int main() {
   run<5>("replica, next sub widened in the second half", 18);
   run<6>("replica, integer widening (no F2F)", 18);
   run<7>("integer widening, fixed ring slot", 18);
+  run<8>("simple loop (row LDS + q LDS + F2F + DFMA)", 18);
+  run<9>("simple loop, segments unrolled by 2", 18);
   return 0;
 }

@@ -68,6 +68,16 @@ buf = H.StepBuffers(queries=H.gen_queries(H.REAL, 4, 3, n, 0, 64, dim), logits=H
                     decision=torch.empty(64, dtype=torch.int32, device=dev))
 eng.step(64, buf, H.VerifyParams.make(skip_enabled=True, min_S=0.95, O_dist=5), gap_d=1)
 torch.cuda.synchronize()
+# batch 1 on the exact scan: K4 launched early (PDL) under K1x, its own skip similarity
+eng1 = H.Engine(col, 1, 8, 7, 64, 15)
+b1 = H.StepBuffers(**{kk: (v[:1] if hasattr(v, "shape") else v) for kk, v in buf.__dict__.items()})
+for _ in range(3):
+    eng1.step(1, b1, H.VerifyParams.make(skip_enabled=True, min_S=0.95, O_dist=5), gap_d=1)
+torch.cuda.synchronize()
+# k > 32: every row's chain + radix sort; index search with k > 32
+q = H.gen_queries(H.REAL, 4, 3, n, 0, 5, dim)
+col.search_topk_exact(q, 100)
+col.search_topk_exact(q, n + 3, row_range=(10, 400))
 col = H.Collection(64, capacity=64 * 40, dtype="bf16")
 col.generate(H.REAL, 7, 64 * 40, payload=H.PAYLOAD_TRAJ, traj_T=64)
 loop = H.HybridLoop(col, H.hybrid_params(40, traj_T=64, d_f=64, seed=5, db_seed=7), max_rounds=20)
