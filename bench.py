@@ -694,6 +694,9 @@ def run_ours(args):
     e2e = None
     if engs:
         e2e = run_e2e(H, torch, engs, args, qs, lg, feats, xyz_np, vp, strs)
+        if flush:
+            e2e["note"] = ("an episode's steps back to back through the host API, without the L2 flush the device-"
+                           "timed value applies between steps: part of the DB stays in the 126 MB L2")
     else:
         e2e = run_e2e_sharded(torch, dist, world, sh, comms, col, b0, args, qs, lg, feats, xyz_np, hist, vp, strs)
     if replicas:  # whole job: the slowest rank's rate x ranks

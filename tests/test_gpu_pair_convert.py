@@ -87,3 +87,15 @@ def test_converted_pair_ragged_ranges(torch):
         kk = oid.shape[1]
         np.testing.assert_array_equal(ids[:, :kk].cpu().numpy(), oid + rb, err_msg=f"{rb}:{re}")
         np.testing.assert_array_equal(sc[:, :kk].cpu().numpy(), osc, err_msg=f"{rb}:{re}")
+
+
+def test_search_plan_reports_the_conversion(torch):
+    col = H.Collection(256, capacity=5000)
+    col.generate(O.REAL, 1, 5000)
+    assert col.search_plan(200, 8) == "filter_bf16_onchip"
+    assert col.search_plan(100, 8) == "filter"  # one CTA per key range: TF32
+    col.set_filter("bf16_copy")
+    assert col.search_plan(200, 8) == "filter"  # the copy is streamed instead
+    odd = H.Collection(100, capacity=3000)
+    odd.generate(O.REAL, 1, 3000)
+    assert odd.search_plan(200, 8) == "filter"  # dim % 8: no bf16 slab, TF32 pair kernel
