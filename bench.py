@@ -653,7 +653,7 @@ def run_ours(args):
             k1_src = "timed region: K1 completion-to-completion interval over the interleaved cohorts"
         achieved = alg_bytes / (k1_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": load_traffic(traffic_key(args)),
+                "traffic": traffic_of(args, b1 - b0),
                 "kernel": ("similarity (K1x exact scan: every row's sequential fp64 chain over the stored keys + "
                            "top-k; no filter, no rescoring)" if scan else
                            "similarity (K1 CTA-pair filter, fp32 key tiles converted to bf16 on chip, kind::f16)"
@@ -942,6 +942,16 @@ def traffic_key(args):
     if args.config == "c2":
         return "similarity" if args.filter == "bf16_copy" else "similarity_native"
     return f"similarity_{args.config}"
+
+
+def traffic_of(args, rows):
+    """ncu dram bytes per launch of this run's dominant kernel.  Config 4's
+    capture (tools/round_profile.sh) runs the same CTA-pair kernel on a 2M-row
+    DB to bound the replay time; its bytes scale with the rows streamed."""
+    if args.config == "c4":
+        t = load_traffic("similarity_pair")
+        return None if t is None else t * rows / 2_000_000
+    return load_traffic(traffic_key(args))
 
 
 def load_peak_key(key):

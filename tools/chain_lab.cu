@@ -17,6 +17,9 @@
 //           loads + 4 F2F + 4 DFMA, straight from the ring slot (the compiler
 //           schedules; no ping-pong widening)
 //   MODE 9  MODE 8 with the segment loop unrolled by 2
+//   MODE 10 the next sub's 8 row loads issued one sub ahead (raw registers),
+//           widened just in time per group of 4 steps
+//   MODE 11 MODE 10 with the query operands loaded one group ahead
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -112,6 +115,49 @@ __global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw
     for (int c = 0; c < 8; ++c) r.v[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
     if (MODE != 1 && MODE != 7 && ++wslot == S) wslot = 0;
   };
+  if constexpr (MODE == 10 || MODE == 11) {
+    double acc10 = 0.0;
+    int slot = 0;
+    Raw cur, nxt;
+    const uint32_t ofs0 = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cur.v[c] = *reinterpret_cast<const uint4*>(rowbase + ofs0 + ((c ^ swz) << 4));
+    for (int u = 0; u < U; ++u) {
+      if (++slot == S) slot = 0;
+      const unsigned char* rowp = rowbase + (size_t)slot * stage_bytes;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) nxt.v[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
+      const double* q = q64 + ((u * kSub) & 4095);
+      double2 qa0 = *reinterpret_cast<const double2*>(q), qa1 = *reinterpret_cast<const double2*>(q + 2);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        double2 q0, q1, qn0, qn1;
+        if constexpr (MODE == 11) {
+          q0 = qa0;
+          q1 = qa1;
+          if (g + 1 < 8) {
+            qn0 = *reinterpret_cast<const double2*>(q + 4 * g + 4);
+            qn1 = *reinterpret_cast<const double2*>(q + 4 * g + 6);
+          }
+        } else {
+          q0 = *reinterpret_cast<const double2*>(q + 4 * g);
+          q1 = *reinterpret_cast<const double2*>(q + 4 * g + 2);
+        }
+        const uint4 x = cur.v[g];
+        acc10 = __fma_rn(q0.x, (double)__uint_as_float(x.x), acc10);
+        acc10 = __fma_rn(q0.y, (double)__uint_as_float(x.y), acc10);
+        acc10 = __fma_rn(q1.x, (double)__uint_as_float(x.z), acc10);
+        acc10 = __fma_rn(q1.y, (double)__uint_as_float(x.w), acc10);
+        if constexpr (MODE == 11) {
+          qa0 = qn0;
+          qa1 = qn1;
+        }
+      }
+      cur = nxt;
+    }
+    if (acc10 == 1.2345) out[0] = acc10;
+    return;
+  }
   if constexpr (MODE >= 8) {
     double acc8 = 0.0;
     int slot = 0;
@@ -192,5 +238,7 @@ int main() {
   run<7>("integer widening, fixed ring slot", 18);
   run<8>("simple loop (row LDS + q LDS + F2F + DFMA)", 18);
   run<9>("simple loop, segments unrolled by 2", 18);
+  run<10>("raw one sub ahead, widened just in time", 18);
+  run<11>("raw one sub ahead, JIT widening, q one group ahead", 18);
   return 0;
 }
