@@ -13,7 +13,8 @@
 //
 //   * one thread per row (lanes 0..lpw-1 of 4 compute warps, a tile of
 //     R = 4 lpw rows per CTA, persistent over tiles), each running NQ <= 4
-//     independent chains (one per query: NQ-way ILP on the DFMA latency);
+//     independent chains (one per query: NQ-way ILP on the DFMA latency),
+//     16 B of its row per shared load, widened just before its DFMAs;
 //   * warp 4 streams the tile's 128-B row segments (32 fp32 or 64 bf16
 //     columns) by TMA into an S-stage SWIZZLE_128B ring; a thread's 16-B
 //     shared loads of its own row hit 8 distinct bank groups per 8 rows
@@ -121,86 +122,15 @@ __device__ __forceinline__ double key_score(uint64_t key) {  // inverse of score
 }
 
 // The chain is latency-bound: one dependent DFMA per step (~8.6 cycles on
-// sm_100) with one warp per scheduler.  So nothing else may sit on its
-// critical path: the 32 keys of the NEXT 32-column sub-segment are loaded
-// from shared memory and widened (F2F) while the current sub's 32 DFMAs
-// run, and each group of 4 steps has its query operands loaded one group
-// ahead (NQ <= 2; from 3 queries up the NQ independent chains hide them).
+// sm_100) with one warp per scheduler.  The consumer loop is the plain one:
+// per 16-B chunk of a thread's row segment one shared load, the widening and
+// the chunk's DFMAs per query, with the broadcast query operands loaded
+// beside them; the compiler schedules the loads a group ahead.  (A ping-pong
+// variant that widened the whole next 32-column sub into fp64 registers while
+// the current sub's chain ran used 190 registers and measured ~1 us slower per
+// scan at config 1, r02q: 55.3 vs 54.4 us.)
 constexpr int kSub = 32;  // columns per sub-segment (one 128-B fp32 segment, half a bf16 one)
-
-template <typename KT>
-struct SubRaw {
-  static constexpr int kVec = kSub * (int)sizeof(KT) / 16;  // 16-B loads per sub: 8 fp32, 4 bf16
-  uint4 v[kVec];
-};
-
-// widen elements [4g, 4g + 4) of a sub (F2F: exact)
-template <typename KT>
-__device__ __forceinline__ void widen4(const SubRaw<KT>& r, int g, double* out) {
-  if constexpr (sizeof(KT) == 4) {
-    const uint4 x = r.v[g];
-    out[0] = (double)__uint_as_float(x.x);
-    out[1] = (double)__uint_as_float(x.y);
-    out[2] = (double)__uint_as_float(x.z);
-    out[3] = (double)__uint_as_float(x.w);
-  } else {
-    const uint4 x = r.v[g >> 1];
-    const uint32_t w0 = (g & 1) ? x.z : x.x, w1 = (g & 1) ? x.w : x.y;
-    out[0] = (double)__uint_as_float(w0 << 16);  // element 2i: the low half
-    out[1] = (double)__uint_as_float(w0 & 0xFFFF0000u);
-    out[2] = (double)__uint_as_float(w1 << 16);
-    out[3] = (double)__uint_as_float(w1 & 0xFFFF0000u);
-  }
-}
-
-// 32 chain steps on the widened sub `kc` (columns col0..col0+31 of the
-// queries in q64) while the next sub `rn` is widened into `kn`.
-template <typename KT, int NQ, bool kNext>
-__device__ __forceinline__ void chain_sub(const double (&kc)[kSub], double (&kn)[kSub], const SubRaw<KT>& rn,
-                                          const double* __restrict__ q64, int qlen, int col0, double (&acc)[NQ]) {
-  constexpr bool kQPre = NQ <= 2;
-  double2 qa[NQ][2], qb[NQ][2];
-  if constexpr (kQPre) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      qa[q][0] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0);
-      qa[q][1] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 2);
-    }
-  }
-#pragma unroll
-  for (int g = 0; g < kSub / 4; ++g) {
-    if constexpr (kQPre) {
-      if (g + 1 < kSub / 4) {
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          qb[q][0] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 4 * g + 4);
-          qb[q][1] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 4 * g + 6);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        qa[q][0] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 4 * g);
-        qa[q][1] = *reinterpret_cast<const double2*>(q64 + (size_t)q * qlen + col0 + 4 * g + 2);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      acc[q] = __fma_rn(qa[q][0].x, kc[4 * g + 0], acc[q]);
-      acc[q] = __fma_rn(qa[q][0].y, kc[4 * g + 1], acc[q]);
-      acc[q] = __fma_rn(qa[q][1].x, kc[4 * g + 2], acc[q]);
-      acc[q] = __fma_rn(qa[q][1].y, kc[4 * g + 3], acc[q]);
-    }
-    if constexpr (kNext) widen4<KT>(rn, g, &kn[4 * g]);
-    if constexpr (kQPre) {
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        qa[q][0] = qb[q][0];
-        qa[q][1] = qb[q][1];
-      }
-    }
-  }
-}
+constexpr int kVecPerSub(int key_bytes) { return kSub * key_bytes / 16; }  // 16-B loads per sub: 8 fp32, 4 bf16
 
 struct ScanArgs {
   int dim, nchunk;               // 128-B row segments per row
@@ -310,24 +240,6 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
     uint32_t wph = 0;
     constexpr int SUBS = CPC / kSub;  // subs per 128-B segment
     const uint8_t* rowbase = ring + (size_t)(lane < a.lpw ? rr : 0) * 128;
-    // sub u of the tile: segment u / SUBS, 16-B chunks [h kVec, (h + 1) kVec)
-    auto load_sub = [&](int u, SubRaw<KT>& r) {
-      const int h = u % SUBS;
-      if (h == 0) mbar_wait(&full[wslot], wph);
-      const uint8_t* rowp = rowbase + (size_t)wslot * stage_bytes;
-#pragma unroll
-      for (int c = 0; c < SubRaw<KT>::kVec; ++c)
-        r.v[c] = *reinterpret_cast<const uint4*>(rowp + (((h * SubRaw<KT>::kVec + c) ^ swz) << 4));
-      if (h == SUBS - 1 && ++wslot == a.S) wslot = 0, wph ^= 1;
-    };
-    // after the last sub of a segment is widened, its slot is free
-    auto release_if_last = [&](int u) {
-      if (u % SUBS == SUBS - 1) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[rslot]);
-        if (++rslot == a.S) rslot = 0;
-      }
-    };
     const int U = a.nchunk * SUBS;
     for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
       const int64_t row = a.row_begin + t * a.R + rr;
@@ -335,28 +247,49 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
       double acc[NQ];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
-      double ka[kSub], kb[kSub];
-      SubRaw<KT> raw;
-      load_sub(0, raw);
+      // per 16-B chunk of the row segment: one shared load, widen, the
+      // chunk's DFMAs per query (broadcast query operands); the compiler
+      // schedules the loads a group ahead.  The slot is released after its
+      // last sub.
+      constexpr int E = 16 / (int)sizeof(KT);  // keys per 16-B chunk
+      constexpr int kVec = kVecPerSub((int)sizeof(KT));
+      for (int u = 0; u < U; ++u) {
+        const int h = u % SUBS;
+        if (h == 0) mbar_wait(&full[wslot], wph);
+        const uint8_t* rowp = rowbase + (size_t)wslot * stage_bytes;
+        const double* qc = q64 + (size_t)u * kSub;
 #pragma unroll
-      for (int g = 0; g < kSub / 4; ++g) widen4<KT>(raw, g, &ka[4 * g]);
-      release_if_last(0);
-      // ping-pong over (ka, kb): sub u runs on one while sub u + 1 is widened into the other
-      for (int u = 0; u < U; u += 2) {
-        if (u + 1 < U) {
-          load_sub(u + 1, raw);
-          chain_sub<KT, NQ, true>(ka, kb, raw, q64, qlen, u * kSub, acc);
-          release_if_last(u + 1);
-        } else {
-          chain_sub<KT, NQ, false>(ka, kb, raw, q64, qlen, u * kSub, acc);
-          break;
+        for (int c = 0; c < kVec; ++c) {
+          const uint4 x = *reinterpret_cast<const uint4*>(rowp + (((h * kVec + c) ^ swz) << 4));
+          double kv[E];
+          if constexpr (sizeof(KT) == 4) {
+            kv[0] = (double)__uint_as_float(x.x);
+            kv[1] = (double)__uint_as_float(x.y);
+            kv[2] = (double)__uint_as_float(x.z);
+            kv[3] = (double)__uint_as_float(x.w);
+          } else {
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              kv[2 * i] = (double)__uint_as_float(w[i] << 16);
+              kv[2 * i + 1] = (double)__uint_as_float(w[i] & 0xFFFF0000u);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+            for (int e = 0; e < E; e += 2) {
+              const double2 qq = *reinterpret_cast<const double2*>(qc + (size_t)q * qlen + c * E + e);
+              acc[q] = __fma_rn(qq.x, kv[e], acc[q]);
+              acc[q] = __fma_rn(qq.y, kv[e + 1], acc[q]);
+            }
+          }
         }
-        if (u + 2 < U) {
-          load_sub(u + 2, raw);
-          chain_sub<KT, NQ, true>(kb, ka, raw, q64, qlen, (u + 1) * kSub, acc);
-          release_if_last(u + 2);
-        } else {
-          chain_sub<KT, NQ, false>(kb, ka, raw, q64, qlen, (u + 1) * kSub, acc);
+        if (h == SUBS - 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[rslot]);
+          if (++rslot == a.S) rslot = 0;
+          if (++wslot == a.S) wslot = 0, wph ^= 1;
         }
       }
       if (a.allkey) {  // large k: the keys go to the radix sort (coalesced: consecutive rows per lane)
