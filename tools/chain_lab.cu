@@ -20,6 +20,10 @@
 //   MODE 10 the next sub's 8 row loads issued one sub ahead (raw registers),
 //           widened just in time per group of 4 steps
 //   MODE 11 MODE 10 with the query operands loaded one group ahead
+//   MODE 12 tools/fp64_rate.cu's "K1x shape" loop (padded 36-float rows, one
+//           fixed row per thread, q index i & 4095) inside this harness
+//   MODE 13 the same flat loop over steps (i += 4) reading the ring: slot
+//           (i / 32) mod S (S a power of two), chunk (i / 4) mod 8, swizzled
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -115,6 +119,37 @@ __global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw
     for (int c = 0; c < 8; ++c) r.v[c] = *reinterpret_cast<const uint4*>(rowp + ((c ^ swz) << 4));
     if (MODE != 1 && MODE != 7 && ++wslot == S) wslot = 0;
   };
+  if constexpr (MODE == 13) {
+    double a13 = 0.0;
+    const int smask = S - 1;  // S rounded down to a power of two by the caller
+    for (int i = 0; i < U * kSub; i += 4) {
+      const unsigned char* p = rowbase + (size_t)((i >> 5) & smask) * stage_bytes + ((((i >> 2) & 7) ^ swz) << 4);
+      const float4 v = *reinterpret_cast<const float4*>(p);
+      const double2 x0 = *reinterpret_cast<const double2*>(q64 + (i & 4095));
+      const double2 x1 = *reinterpret_cast<const double2*>(q64 + ((i + 2) & 4095));
+      a13 = __fma_rn(x0.x, (double)v.x, a13);
+      a13 = __fma_rn(x0.y, (double)v.y, a13);
+      a13 = __fma_rn(x1.x, (double)v.z, a13);
+      a13 = __fma_rn(x1.y, (double)v.w, a13);
+    }
+    if (a13 == 1.2345) out[0] = a13;
+    return;
+  }
+  if constexpr (MODE == 12) {
+    const float* kr = reinterpret_cast<const float*>(smem) + (size_t)(lane < lpw ? rr : 0) * 36;
+    double a12 = 0.0;
+    for (int i = 0; i < U * kSub; i += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(kr + (i & 31));
+      const double2 x0 = *reinterpret_cast<const double2*>(q64 + (i & 4095));
+      const double2 x1 = *reinterpret_cast<const double2*>(q64 + ((i + 2) & 4095));
+      a12 = __fma_rn(x0.x, (double)v.x, a12);
+      a12 = __fma_rn(x0.y, (double)v.y, a12);
+      a12 = __fma_rn(x1.x, (double)v.z, a12);
+      a12 = __fma_rn(x1.y, (double)v.w, a12);
+    }
+    if (a12 == 1.2345) out[0] = a12;
+    return;
+  }
   if constexpr (MODE == 10 || MODE == 11) {
     double acc10 = 0.0;
     int slot = 0;
@@ -205,26 +240,37 @@ template <int MODE>
 void run(const char* name, int lpw) {
   double* out;
   cudaMalloc(&out, 8);
-  const int U = 128, S = (180 * 1024) / (4 * lpw * 128) < 20 ? (180 * 1024) / (4 * lpw * 128) : 20;
+  int S = (180 * 1024) / (4 * lpw * 128) < 20 ? (180 * 1024) / (4 * lpw * 128) : 20;
+  if (MODE == 13)
+    while (S & (S - 1)) --S;  // a power of two: the slot is a mask
+  const int U = 128;
   const size_t smem = (size_t)S * 4 * lpw * 128 + 4096 * 8;
   cudaFuncSetAttribute(lab<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   lab<MODE><<<139, 160, smem>>>(out, U, S, lpw);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  float best = 1e9;
-  for (int rep = 0; rep < 5; ++rep) {
-    cudaEventRecord(e0);
-    lab<MODE><<<139, 160, smem>>>(out, U, S, lpw);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
-    float ms;
-    cudaEventElapsedTime(&ms, e0, e1);
-    best = ms < best ? ms : best;
-  }
-  const double steps = (double)U * kSub;
-  printf("%-44s lpw %2d: %.1f us, %.2f ns/step, %.1f cycles/step @1965 MHz  err=%s\n", name, lpw, best * 1e3,
-         best * 1e6 / steps, best * 1e6 / steps * 1.965, cudaGetErrorString(cudaGetLastError()));
+  // time U = 1024 subs (32768 steps) minus U = 0 (the shared-memory setup),
+  // so the per-step figure is the loop's alone
+  auto best_of = [&](int u) {
+    float best = 1e9;
+    for (int rep = 0; rep < 5; ++rep) {
+      cudaEventRecord(e0);
+      lab<MODE><<<139, 160, smem>>>(out, u, S, lpw);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      best = ms < best ? ms : best;
+    }
+    return best;
+  };
+  const int UL = 8 * U;
+  const float t0 = best_of(0), t1 = best_of(UL);
+  const double steps = (double)UL * kSub;
+  const double ns = (t1 - t0) * 1e6 / steps;
+  printf("%-50s lpw %2d: setup %.1f us, %.2f ns/step, %.1f cycles/step @1965 MHz  err=%s\n", name, lpw, t0 * 1e3, ns,
+         ns * 1.965, cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
@@ -240,5 +286,7 @@ int main() {
   run<9>("simple loop, segments unrolled by 2", 18);
   run<10>("raw one sub ahead, widened just in time", 18);
   run<11>("raw one sub ahead, JIT widening, q one group ahead", 18);
+  run<12>("fp64_rate K1x-shape loop in this harness", 18);
+  run<13>("flat step loop over the swizzled ring", 18);
   return 0;
 }
