@@ -96,12 +96,12 @@ def test_graph_replay_matches_eager(torch):
                     assert torch.equal(bufs[s][kk], ref[s][kk]), (rep, s, kk)
 
 
-@pytest.mark.parametrize("B", [48, 200])
+@pytest.mark.parametrize("B", [1, 3, 48, 200])
 def test_cohorts_on_two_streams_match_serial_steps(torch, B):
     """Two engines over one collection, each on its own stream, their steps
     interleaved with no synchronisation between them (the bench's cohort
-    pipelining; B = 200 runs the CTA-pair filter): every step's outputs equal
-    the same step run alone."""
+    pipelining; B = 200 runs the CTA-pair filter, B <= 4 the exact scan with
+    K4 launched under it): every step's outputs equal the same step run alone."""
     n, dim, k, L, d_f = 20000, 256, 8, 7, 256
     col = H.Collection(dim, capacity=n)
     col.generate(H.REAL, 5, n)
