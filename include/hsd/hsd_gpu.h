@@ -183,7 +183,7 @@ hsd_status hsd_set_sim_path(int path);
  * collection) takes under the current switch: *exact_scan = 1 for the exact
  * scan (K1x), 0 for the tensor-core filter + exact rescoring (K1 + K2), 2 for
  * the same filter whose fp32 key tiles are converted to bf16 on chip (CTA
- * pairs, 129..256 queries over fp32 keys without the bf16 filter copy). */
+ * pairs, 129..1024 queries over fp32 keys without the bf16 filter copy). */
 hsd_status hsd_search_plan(hsd_collection* c, int B, int k, int64_t rows, int* exact_scan);
 
 /* ------------------------------------------------------------------------

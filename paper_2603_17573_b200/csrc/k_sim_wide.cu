@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kConv ? kConvThreads : kThreads, 1)
     sim_pair_kernel(const __grid_constant__ CUtensorMap keys_map, const __grid_constant__ CUtensorMap q_map,
                     int64_t row_begin, int64_t row_end, int dim, int B, int64_t blocks_per_pair,
                     int per_group, uint64_t* __restrict__ partial) {
-  static_assert(!kConv || (!kBf16 && kG == 1), "on-chip conversion: fp32 keys, one pair per cluster");
+  static_assert(!kConv || !kBf16, "on-chip conversion: fp32 keys");
   constexpr bool kF16 = kBf16 || kConv;  // kind::f16 MMAs
   constexpr int kBK = kF16 ? 64 : 32;
   constexpr int KS = PairSmemT<kConv>::KS, QS = PairSmemT<kConv>::QS;
@@ -467,7 +467,8 @@ __global__ void __launch_bounds__(kConv ? kConvThreads : kThreads, 1)
     for (int i = 0; i < KS; ++i) {
       // kConv: both CTAs' converter warps arrive on the leader's k_full
       mbar_init(&S.k_full[i], kConv ? 2 * kConvWarps : 1);
-      mbar_init(&S.k_empty[i], kG);
+      // kConv: the bf16 stage is this CTA's own (only its pair's MMAs read it)
+      mbar_init(&S.k_empty[i], kConv ? 1 : kG);
     }
     for (int i = 0; i < QS; ++i) {
       mbar_init(&S.q_full[i], 1);
@@ -476,7 +477,9 @@ __global__ void __launch_bounds__(kConv ? kConvThreads : kThreads, 1)
     if constexpr (kConv) {
       for (int i = 0; i < kConvRawS; ++i) {
         mbar_init(&S.raw_full[i], 1);
-        mbar_init(&S.raw_empty[i], kConvWarps);
+        // kG > 1: the raw slot is a multicast target of the kG CTAs of this
+        // pair-half, so every one of their converters releases it here
+        mbar_init(&S.raw_empty[i], kConvWarps * kG);
       }
     }
     for (int i = 0; i < 2; ++i) {
@@ -513,8 +516,15 @@ __global__ void __launch_bounds__(kConv ? kConvThreads : kThreads, 1)
             // raw fp32 halves of the chunk into this CTA's own ring
             mbar_wait(&S.raw_empty[ks], kph ^ 1);
             mbar_expect_tx(&S.raw_full[ks], 2 * kKeyTile);
-            tma_load_2d(&S.raw[ks][0], &keys_map, &S.raw_full[ks], c * kBK, row, pol);
-            tma_load_2d(&S.raw[ks][kKeyTile], &keys_map, &S.raw_full[ks], c * kBK + 32, row, pol);
+            if constexpr (kG > 1) {  // tile t: issued by pair t mod kG into the kG CTAs of this half
+              if ((int)(tile % kG) == grp) {
+                tma_load_2d_mc(&S.raw[ks][0], &keys_map, &S.raw_full[ks], c * kBK, row, half_mask, pol);
+                tma_load_2d_mc(&S.raw[ks][kKeyTile], &keys_map, &S.raw_full[ks], c * kBK + 32, row, half_mask, pol);
+              }
+            } else {
+              tma_load_2d(&S.raw[ks][0], &keys_map, &S.raw_full[ks], c * kBK, row, pol);
+              tma_load_2d(&S.raw[ks][kKeyTile], &keys_map, &S.raw_full[ks], c * kBK + 32, row, pol);
+            }
             if (++ks == kConvRawS) {
               ks = 0;
               kph ^= 1;
@@ -586,7 +596,8 @@ __global__ void __launch_bounds__(kConv ? kConvThreads : kThreads, 1)
             else
               mma2_ss(d, adesc + 2 * kk, bdesc + 2 * kk, idesc, (kc > 0 || kk > 0) ? 1u : 0u);
           }
-          tc_commit2_mc(&S.k_empty[ks], all_mask);  // every CTA's slot ks: kG releases complete it
+          // every CTA's slot ks: kG releases complete it (kConv: the pair's own bf16 stage)
+          tc_commit2_mc(&S.k_empty[ks], kConv ? pair_mask : all_mask);
           tc_commit2_mc(&S.q_empty[qs], pair_mask);
           if (++ks == KS) {
             ks = 0;
@@ -631,7 +642,13 @@ __global__ void __launch_bounds__(kConv ? kConvThreads : kThreads, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive(&S.raw_empty[rs]);
+            if constexpr (kG > 1) {
+#pragma unroll
+              for (int g = 0; g < kG; ++g)
+                mbar_arrive_remote(mapa_shared(smem_u32(&S.raw_empty[rs]), (uint32_t)(2 * g + rank)));
+            } else {
+              mbar_arrive(&S.raw_empty[rs]);
+            }
             mbar_arrive_remote(mapa_shared(smem_u32(&S.k_full[ks]), leader));
           }
           if (++rs == kConvRawS) {
@@ -956,7 +973,7 @@ int sim_wide_lists(int B, int64_t rows, int num_sms) {
 
 bool sim_wide_converts(int key_dtype, int B, int dim) {
   // dim % 8: the bf16 query slab's rows must be 16-B multiples (TMA stride)
-  return key_dtype == HSD_DTYPE_F32 && dim % 8 == 0 && use_pair(B) && wide_groups(B) == 1 && pair_convert_enabled();
+  return key_dtype == HSD_DTYPE_F32 && dim % 8 == 0 && use_pair(B) && pair_convert_enabled();
 }
 
 double sim_wide_gamma(int dim, int key_dtype) {
@@ -1025,7 +1042,15 @@ cudaError_t launch_sim_wide(const void* keys, int key_dtype, int64_t n_keys_tota
     const int64_t pairs = lists / 2;
     const int64_t per_pair = ((n_blocks + pairs - 1) / pairs + 1) & ~(int64_t)1;  // even: whole block pairs
     if (geom) *geom = ListGeom{row_begin, row_end, per_pair, 2};
-    if (conv) return launch_pair<false, 1, true>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s);
+    if (conv) {
+      switch (groups) {
+        case 1: return launch_pair<false, 1, true>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s);
+        case 2: return launch_pair<false, 2, true>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s);
+        case 3: return launch_pair<false, 3, true>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s);
+        case 4: return launch_pair<false, 4, true>(km, qm, row_begin, row_end, dim, B, lists, per_pair, partial, s);
+        default: return cudaErrorInvalidValue;
+      }
+    }
     switch (groups) {
 #define HSD_PAIR(G)                                                                                        \
   case G:                                                                                                  \

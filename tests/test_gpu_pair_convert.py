@@ -1,6 +1,7 @@
 """CTA-pair filter over fp32 keys with on-chip bf16 conversion (k_sim_wide.cu,
-sim_pair_kernel<false, 1, true>; passes of 129..256 queries over an fp32
-collection without the bf16 filter copy).
+sim_pair_kernel<false, G, true>; passes of 129..1024 queries over an fp32
+collection without the bf16 filter copy; above 256 queries clusters of G
+pairs share multicast raw key tiles).
 
 The converter warps round every fp32 key to bf16 RN-even — the rounding the
 bf16 filter copy stores — and the queries go through the same bf16 slab, so
@@ -33,7 +34,8 @@ def _run(col, q, k):
 
 @pytest.mark.parametrize("kind", [O.EXACT, O.REAL, O.CLUSTER])
 @pytest.mark.parametrize("dim,n,B", [(64, 6000, 256), (4096, 2500, 200), (100, 3000, 129), (4352, 1500, 160),
-                                     (136, 4000, 250)])
+                                     (136, 4000, 250), (256, 5000, 300), (4096, 1200, 513), (64, 9000, 700),
+                                     (512, 3000, 1024)])
 def test_converted_pair_matches_oracle_and_copy_path(torch, kind, dim, n, B):
     col = H.Collection(dim, capacity=n)
     col.generate(kind, 11, n)
@@ -94,6 +96,7 @@ def test_search_plan_reports_the_conversion(torch):
     col.generate(O.REAL, 1, 5000)
     assert col.search_plan(200, 8) == "filter_bf16_onchip"
     assert col.search_plan(100, 8) == "filter"  # one CTA per key range: TF32
+    assert col.search_plan(700, 8) == "filter_bf16_onchip"  # clusters of 3 pairs
     col.set_filter("bf16_copy")
     assert col.search_plan(200, 8) == "filter"  # the copy is streamed instead
     odd = H.Collection(100, capacity=3000)
