@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--paths", default="auto", help="comma list of auto | filter | scan | tc_single")
     ap.add_argument("--shadow", action="store_true", help="fp32 collections keep the bf16 filter copy")
     ap.add_argument("--flush", action="store_true", help="write 512 MB between timed searches (cold L2)")
+    ap.add_argument("--flush-read", action="store_true",
+                    help="with --flush: then read 256 MB, so the write's dirty lines drain outside the timing")
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--iters", type=int, default=20)
     a = ap.parse_args()
@@ -34,6 +36,7 @@ def main():
     torch.cuda.set_device(0)
     s = torch.cuda.current_stream()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if a.flush else None
+    rd = torch.zeros(64 << 20, dtype=torch.int32, device="cuda") if a.flush and a.flush_read else None
     for dt in a.dtypes.split(","):
         col = H.Collection(a.dim, capacity=a.n, dtype=dt)
         col.generate(H.REAL, 2026, a.n)
@@ -51,6 +54,8 @@ def main():
                 for e0, e1 in ev:
                     if flush is not None:
                         flush.fill_(1)
+                        if rd is not None:
+                            rd.sum()
                     e0.record(s)
                     col.search_topk_exact(q, a.k)
                     e1.record(s)
