@@ -941,6 +941,8 @@ def traffic_key(args):
     """profiles/traffic.json entry of this run's dominant kernel (ncu dram bytes per launch)."""
     if args.config == "c2":
         return "similarity" if args.filter == "bf16_copy" else "similarity_native"
+    if args.config == "c1" and getattr(args, "search_path", "filter") == "scan":
+        return "exact_scan_c1"  # tools/round_profile.sh: K1x at the config-1 shape
     return f"similarity_{args.config}"
 
 
