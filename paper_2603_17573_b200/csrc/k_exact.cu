@@ -46,6 +46,7 @@ using namespace sm100;
 __host__ __device__ constexpr int compute_warps(int) { return 4; }
 constexpr uint32_t kNoId = 0xFFFFFFFFu;
 constexpr int kSmemBudget = 225 * 1024;
+constexpr int kSegPerStage = 4;
 
 // (order key, id): ascending = the reference's (score desc, id asc).
 __device__ __forceinline__ bool lt(uint64_t ak, uint32_t ai, uint64_t bk, uint32_t bi) {
@@ -136,6 +137,7 @@ struct ScanArgs {
   int dim, nchunk;               // 128-B row segments per row
   int64_t row_begin, row_end;    // rows scored
   int R, lpw, S;                 // tile rows (4 lpw), rows per warp, ring stages
+  int seg;                       // 128-B row segments per stage (one barrier handshake each)
   int64_t ntiles;
   int k;
   const float* queries;          // [NQ][dim]
@@ -154,7 +156,8 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
   // SWIZZLE_128B stages must sit on 1-KB boundaries (the plan reserves the slack)
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int stage_bytes = a.R * 128;
+  const int seg_bytes = a.R * 128;
+  const int stage_bytes = seg_bytes * a.seg;
   const int qlen = a.nchunk * CPC;
   uint8_t* ring = smem;
   double* q64 = reinterpret_cast<double*>(smem + (size_t)a.S * stage_bytes);
@@ -183,11 +186,14 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
       uint32_t ph = 0;
       for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
         const int y = (int)(a.row_begin + t * a.R);
-        for (int j = 0; j < a.nchunk; ++j) {
+        for (int j = 0; j < a.nchunk; j += a.seg) {
+          const int nseg = min(a.seg, a.nchunk - j);
           if (n >= a.S) mbar_wait(&empty[slot], ph ^ 1);
           ++n;
-          mbar_expect_tx(&full[slot], (uint32_t)stage_bytes);
-          tma_load_2d(ring + (size_t)slot * stage_bytes, &km, &full[slot], j * CPC, y, pol);
+          mbar_expect_tx(&full[slot], (uint32_t)(nseg * seg_bytes));
+          for (int s2 = 0; s2 < nseg; ++s2)
+            tma_load_2d(ring + (size_t)slot * stage_bytes + (size_t)s2 * seg_bytes, &km, &full[slot], (j + s2) * CPC,
+                        y, pol);
           if (++slot == a.S) slot = 0, ph ^= 1;
         }
       }
@@ -240,7 +246,6 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
     uint32_t wph = 0;
     constexpr int SUBS = CPC / kSub;  // subs per 128-B segment
     const uint8_t* rowbase = ring + (size_t)(lane < a.lpw ? rr : 0) * 128;
-    const int U = a.nchunk * SUBS;
     for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
       const int64_t row = a.row_begin + t * a.R + rr;
       const bool active = lane < a.lpw && row < a.row_end;
@@ -249,48 +254,52 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
       for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
       // per 16-B chunk of the row segment: one shared load, widen, the
       // chunk's DFMAs per query (broadcast query operands); the compiler
-      // schedules the loads a group ahead.  The slot is released after its
-      // last sub.
+      // schedules the loads a group ahead.  A stage holds up to 4 segments
+      // (128 fp32 columns) behind one barrier wait and one release: 47 vs
+      // 49 us at 2.5k rows, 51 vs 53 us at config 1 (same box, r02q).
       constexpr int E = 16 / (int)sizeof(KT);  // keys per 16-B chunk
       constexpr int kVec = kVecPerSub((int)sizeof(KT));
-      for (int u = 0; u < U; ++u) {
-        const int h = u % SUBS;
-        if (h == 0) mbar_wait(&full[wslot], wph);
-        const uint8_t* rowp = rowbase + (size_t)wslot * stage_bytes;
-        const double* qc = q64 + (size_t)u * kSub;
+      for (int j = 0; j < a.nchunk; j += a.seg) {  // one ring stage: nseg row segments, one handshake
+        const int nseg = min(a.seg, a.nchunk - j);
+        mbar_wait(&full[wslot], wph);
+        for (int sg = 0; sg < nseg; ++sg) {
+          const uint8_t* rowp = rowbase + (size_t)wslot * stage_bytes + (size_t)sg * seg_bytes;
 #pragma unroll
-        for (int c = 0; c < kVec; ++c) {
-          const uint4 x = *reinterpret_cast<const uint4*>(rowp + (((h * kVec + c) ^ swz) << 4));
-          double kv[E];
-          if constexpr (sizeof(KT) == 4) {
-            kv[0] = (double)__uint_as_float(x.x);
-            kv[1] = (double)__uint_as_float(x.y);
-            kv[2] = (double)__uint_as_float(x.z);
-            kv[3] = (double)__uint_as_float(x.w);
-          } else {
-            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+          for (int h = 0; h < SUBS; ++h) {
+            const double* qc = q64 + (size_t)((j + sg) * SUBS + h) * kSub;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              kv[2 * i] = (double)__uint_as_float(w[i] << 16);
-              kv[2 * i + 1] = (double)__uint_as_float(w[i] & 0xFFFF0000u);
-            }
-          }
+            for (int c = 0; c < kVec; ++c) {
+              const uint4 x = *reinterpret_cast<const uint4*>(rowp + (((h * kVec + c) ^ swz) << 4));
+              double kv[E];
+              if constexpr (sizeof(KT) == 4) {
+                kv[0] = (double)__uint_as_float(x.x);
+                kv[1] = (double)__uint_as_float(x.y);
+                kv[2] = (double)__uint_as_float(x.z);
+                kv[3] = (double)__uint_as_float(x.w);
+              } else {
+                const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) {
+                for (int i = 0; i < 4; ++i) {
+                  kv[2 * i] = (double)__uint_as_float(w[i] << 16);
+                  kv[2 * i + 1] = (double)__uint_as_float(w[i] & 0xFFFF0000u);
+                }
+              }
 #pragma unroll
-            for (int e = 0; e < E; e += 2) {
-              const double2 qq = *reinterpret_cast<const double2*>(qc + (size_t)q * qlen + c * E + e);
-              acc[q] = __fma_rn(qq.x, kv[e], acc[q]);
-              acc[q] = __fma_rn(qq.y, kv[e + 1], acc[q]);
+              for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+                for (int e = 0; e < E; e += 2) {
+                  const double2 qq = *reinterpret_cast<const double2*>(qc + (size_t)q * qlen + c * E + e);
+                  acc[q] = __fma_rn(qq.x, kv[e], acc[q]);
+                  acc[q] = __fma_rn(qq.y, kv[e + 1], acc[q]);
+                }
+              }
             }
           }
         }
-        if (h == SUBS - 1) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[rslot]);
-          if (++rslot == a.S) rslot = 0;
-          if (++wslot == a.S) wslot = 0, wph ^= 1;
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rslot]);
+        if (++rslot == a.S) rslot = 0;
+        if (++wslot == a.S) wslot = 0, wph ^= 1;
       }
       if (a.allkey) {  // large k: the keys go to the radix sort (coalesced: consecutive rows per lane)
         if (active) {
@@ -390,7 +399,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
 }
 
 struct ScanPlan {
-  int lpw, R, S, grid;
+  int lpw, R, S, grid, seg;
   int64_t ntiles;
   size_t smem;
 };
@@ -409,8 +418,19 @@ ScanPlan scan_plan(int64_t rows, int dim, int NQ, int nsm) {
   p.grid = (int)std::min<int64_t>(p.ntiles, nsm);
   const size_t fixed = (size_t)NQ * nchunk * CPC * sizeof(double) + 64 * 16 +
                        (size_t)kCW * NQ * 32 * (sizeof(uint64_t) + sizeof(uint32_t)) + 1024;
-  const size_t stage = (size_t)p.R * 128;
-  const int S = (int)std::min<size_t>(16, (kSmemBudget - fixed) / stage);
+  // Stages of up to kSegPerStage row segments: the consumers' barrier wait and
+  // release (~120 cycles per handshake, tools/chain_lab.cu mode 14) are paid
+  // once per stage; the ring keeps >= 4 stages.
+  int seg = kSegPerStage;
+  size_t stage = 0;
+  int S = 0;
+  for (;; seg >>= 1) {
+    seg = std::max(1, std::min(seg, nchunk));
+    stage = (size_t)p.R * 128 * seg;
+    S = (int)std::min<size_t>(16, (kSmemBudget - fixed) / stage);
+    if (S >= 4 || seg == 1) break;
+  }
+  p.seg = seg;
   p.S = S;
   p.smem = (size_t)S * stage + fixed;
   return p;
@@ -480,6 +500,7 @@ cudaError_t launch_exact_scan(const void* keys, int key_dtype, int64_t n_keys_to
   a.R = p.R;
   a.lpw = p.lpw;
   a.S = p.S;
+  a.seg = p.seg;
   a.ntiles = p.ntiles;
   a.k = k;
   a.queries = queries;
@@ -571,6 +592,7 @@ cudaError_t launch_exact_topk_large(const void* keys, int key_dtype, int64_t n_k
     a.R = p.R;
     a.lpw = p.lpw;
     a.S = p.S;
+    a.seg = p.seg;
     a.ntiles = p.ntiles;
     a.k = 1;
     a.queries = queries + (size_t)b0 * dim;

@@ -22,6 +22,9 @@
 //   MODE 11 MODE 10 with the query operands loaded one group ahead
 //   MODE 12 tools/fp64_rate.cu's "K1x shape" loop (padded 36-float rows, one
 //           fixed row per thread, q index i & 4095) inside this harness
+//   MODE 14 MODE 8 plus K1x's per-segment handshake: an mbarrier wait (on an
+//           already completed phase) before each sub, __syncwarp + lane-0
+//           arrive on an "empty" barrier after it
 //   MODE 13 the same flat loop over steps (i += 4) reading the ring: slot
 //           (i / 32) mod S (S a power of two), chunk (i / 4) mod 8, swizzled
 #include <cuda_runtime.h>
@@ -196,8 +199,23 @@ __global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw
   if constexpr (MODE >= 8) {
     double acc8 = 0.0;
     int slot = 0;
+    __shared__ uint64_t bars[2];
+    if constexpr (MODE == 14) {
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bars[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"((uint32_t)__cvta_generic_to_shared(&bars[1])));
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(&bars[0])) : "memory");
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
 #pragma unroll (MODE == 9 ? 2 : 1)
     for (int u = 0; u < U; ++u) {
+      if constexpr (MODE == 14) {  // phase 0 of bars[0] is complete: the wait returns at once
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tW14:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+            "@p bra.uni D14;\n\tbra.uni W14;\n\tD14:\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(&bars[0]))
+            : "memory");
+      }
       const unsigned char* rowp = rowbase + (size_t)slot * stage_bytes;
       const double* q = q64 + ((u * kSub) & 4095);
 #pragma unroll
@@ -209,6 +227,12 @@ __global__ void __launch_bounds__(160, 1) lab(double* out, int U, int S, int lpw
         acc8 = __fma_rn(q0.y, (double)v.y, acc8);
         acc8 = __fma_rn(q1.x, (double)v.z, acc8);
         acc8 = __fma_rn(q1.y, (double)v.w, acc8);
+      }
+      if constexpr (MODE == 14) {
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(&bars[1]))
+                       : "memory");
       }
       if (++slot == S) slot = 0;
     }
@@ -288,5 +312,6 @@ int main() {
   run<11>("raw one sub ahead, JIT widening, q one group ahead", 18);
   run<12>("fp64_rate K1x-shape loop in this harness", 18);
   run<13>("flat step loop over the swizzled ring", 18);
+  run<14>("simple loop + per-sub mbarrier wait / arrive", 18);
   return 0;
 }
