@@ -26,8 +26,9 @@
 //     product is exact in fp64, so this is bit-identical to s += a[i]*b[i];
 //   * each warp keeps a sorted (order key, id) top-k per query in registers
 //     (bitonic sort + merge; a batch that cannot enter is rejected with one
-//     ballot), the CTA's 4 warp lists merge in shared memory, and the last
-//     CTA to finish (ticket) merges the CTAs' lists into the final top-k.
+//     ballot), the CTA's 4 warp lists merge in shared memory, and the
+//     CTAs' lists merge in two ticketed levels (groups of 12 CTAs, then the
+//     groups) into the final top-k.
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -46,6 +47,7 @@ using namespace sm100;
 __host__ __device__ constexpr int compute_warps(int) { return 4; }
 constexpr uint32_t kNoId = 0xFFFFFFFFu;
 constexpr int kSmemBudget = 225 * 1024;
+constexpr int kGroup = 12;      // CTAs per first-level merge group (~sqrt of the grid)
 constexpr int kSegPerStage = 4;
 
 // (order key, id): ascending = the reference's (score desc, id asc).
@@ -144,6 +146,9 @@ struct ScanArgs {
   uint64_t* lkey;                // [gridDim][NQ][32]
   uint32_t* lid;
   unsigned* ticket;              // zero between launches (the last CTA resets it)
+  unsigned* gticket;             // [groups] per-group tickets (each group's last CTA resets its own)
+  uint64_t* gkey;                // [groups][NQ][32] group lists
+  uint32_t* gid;
   double* scores;                // [NQ][k]
   int32_t* ids;
   uint64_t* allkey;              // != nullptr: every row's order key [NQ][rows], no top-k (large k)
@@ -332,70 +337,102 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) exact_scan_kernel(const __g
     }
   }
   if (a.allkey) return;  // the producer warp (large k: no merge)
-  // ---- the last CTA merges every CTA's list
+  // ---- two-level merge.  The last CTA of each group of kGroup CTAs merges
+  // the group's lists into a group list; the last group then merges the
+  // group lists.  (One last CTA merging all ~140 lists chained ~28 dependent
+  // warp merges per warp: 51.2 -> 49.2 us at config 1, same box, r02q.)
+  constexpr int kWarps = kCW + 1;
+  const int G = gridDim.x;
+  const int ngroups = (G + kGroup - 1) / kGroup;
+  const int grp = blockIdx.x / kGroup;
+  const int first = grp * kGroup, members = min(kGroup, G - first);
+  uint64_t lk[NQ];
+  uint32_t li[NQ];
+  auto merge_lists = [&](const uint64_t* __restrict__ key, const uint32_t* __restrict__ id, int lfirst, int count) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      lk[q] = kEmpty;
+      li[q] = kNoId;
+    }
+    const int per_list = NQ * a.k;
+    const int chunk = (int)((size_t)a.S * stage_bytes / ((size_t)per_list * 12));
+    uint64_t* sk = reinterpret_cast<uint64_t*>(ring);
+    uint32_t* si = reinterpret_cast<uint32_t*>(ring + (size_t)chunk * per_list * 8);
+    for (int c0 = 0; c0 < count; c0 += chunk) {
+      const int n = min(chunk, count - c0);
+#pragma unroll 8
+      for (int x = tid; x < n * per_list; x += kWarps * 32) {
+        const int g = x / per_list, r = x - g * per_list, q = r / a.k, j = r - q * a.k;
+        const size_t src = ((size_t)(lfirst + c0 + g) * NQ + q) * 32 + j;
+        sk[x] = __ldcg(&key[src]);
+        si[x] = __ldcg(&id[src]);
+      }
+      __syncthreads();
+      for (int g = warp; g < n; g += kWarps) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int x = (g * NQ + q) * a.k + lane;
+          warp_offer_sorted(lk[q], li[q], lane < a.k ? sk[x] : kEmpty, lane < a.k ? si[x] : kNoId, a.k);
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (warp > 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        ck[((warp - 1) * NQ + q) * 32 + lane] = lk[q];
+        ci[((warp - 1) * NQ + q) * 32 + lane] = li[q];
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        for (int w = 0; w < kWarps - 1; ++w)
+          warp_offer_sorted(lk[q], li[q], ck[(w * NQ + q) * 32 + lane], ci[(w * NQ + q) * 32 + lane], a.k);
+    }
+  };
+  auto write_final = [&]() {
+    if (warp == 0) {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q)
+        if (lane < a.k) {
+          const bool ok = lk[q] != kEmpty;
+          a.scores[(size_t)q * a.k + lane] = ok ? key_score(lk[q]) : -INFINITY;
+          a.ids[(size_t)q * a.k + lane] = ok ? (int32_t)li[q] : -1;
+        }
+    }
+  };
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  if (tid == 0) s_last = atomicAdd(&a.gticket[grp], 1u) == (unsigned)members - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  constexpr int kWarps = kCW + 1;
-  uint64_t lk[NQ];
-  uint32_t li[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    lk[q] = kEmpty;
-    li[q] = kNoId;
+  merge_lists(a.lkey, a.lid, first, members);
+  if (ngroups == 1) {
+    write_final();
+    if (tid == 0) a.gticket[grp] = 0u;
+    return;
   }
-  // every CTA's first k entries into shared memory at once (the ring is
-  // free; one L2 round trip, not one per list), then each warp merges its
-  // share from shared memory (a list whose head cannot enter costs one test)
-  const int G = gridDim.x;
-  const int per_list = NQ * a.k;
-  const int chunk = (int)((size_t)a.S * stage_bytes / ((size_t)per_list * 12));
-  uint64_t* sk = reinterpret_cast<uint64_t*>(ring);
-  uint32_t* si = reinterpret_cast<uint32_t*>(ring + (size_t)chunk * per_list * 8);
-  for (int c0 = 0; c0 < G; c0 += chunk) {
-    const int n = min(chunk, G - c0);
-#pragma unroll 8
-    for (int x = tid; x < n * per_list; x += kWarps * 32) {
-      const int g = x / per_list, r = x - g * per_list, q = r / a.k, j = r - q * a.k;
-      const size_t src = ((size_t)(c0 + g) * NQ + q) * 32 + j;
-      sk[x] = __ldcg(&a.lkey[src]);
-      si[x] = __ldcg(&a.lid[src]);
-    }
-    __syncthreads();
-    for (int g = warp; g < n; g += kWarps) {
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const int x = (g * NQ + q) * a.k + lane;
-        warp_offer_sorted(lk[q], li[q], lane < a.k ? sk[x] : kEmpty, lane < a.k ? si[x] : kNoId, a.k);
-      }
-    }
-    __syncthreads();
-  }
-  __syncthreads();  // the CTA merge staging is free again
-  if (warp > 0) {
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      ck[((warp - 1) * NQ + q) * 32 + lane] = lk[q];
-      ci[((warp - 1) * NQ + q) * 32 + lane] = li[q];
-    }
-  }
-  __syncthreads();
   if (warp == 0) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      for (int w = 0; w < kWarps - 1; ++w)
-        warp_offer_sorted(lk[q], li[q], ck[(w * NQ + q) * 32 + lane], ci[(w * NQ + q) * 32 + lane], a.k);
-      if (lane < a.k) {
-        const bool ok = lk[q] != kEmpty;
-        a.scores[(size_t)q * a.k + lane] = ok ? key_score(lk[q]) : -INFINITY;
-        a.ids[(size_t)q * a.k + lane] = ok ? (int32_t)li[q] : -1;
-      }
+      a.gkey[((size_t)grp * NQ + q) * 32 + lane] = lk[q];
+      a.gid[((size_t)grp * NQ + q) * 32 + lane] = li[q];
     }
-    if (lane == 0) *a.ticket = 0u;
+    if (lane == 0) a.gticket[grp] = 0u;
   }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(a.ticket, 1u) == (unsigned)ngroups - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  merge_lists(a.gkey, a.gid, 0, ngroups);
+  write_final();
+  if (tid == 0) *a.ticket = 0u;
 }
 
 struct ScanPlan {
@@ -465,7 +502,8 @@ bool exact_scan_supported(int B, int dim, int key_dtype, int k) {
 
 size_t exact_scan_scratch_bytes(int B, int num_sms) {
   const int nq = std::max(1, B);
-  return (size_t)num_sms * nq * 32 * (sizeof(uint64_t) + sizeof(uint32_t)) + 256;
+  const int groups = (num_sms + kGroup - 1) / kGroup;
+  return (size_t)(num_sms + groups) * nq * 32 * (sizeof(uint64_t) + sizeof(uint32_t)) + 256;
 }
 
 double exact_scan_cost_us(int64_t rows, int dim, int key_dtype, int B) {
@@ -504,9 +542,16 @@ cudaError_t launch_exact_scan(const void* keys, int key_dtype, int64_t n_keys_to
   a.ntiles = p.ntiles;
   a.k = k;
   a.queries = queries;
+  // [ticket | group tickets (<= 48) : 256 B][lkey][lid][gkey][gid]
+  const int groups = (num_sms + kGroup - 1) / kGroup;
+  if (groups > 48) return cudaErrorInvalidValue;
   a.ticket = reinterpret_cast<unsigned*>(sc);
+  a.gticket = reinterpret_cast<unsigned*>(sc + 64);
   a.lkey = reinterpret_cast<uint64_t*>(sc + 256);
   a.lid = reinterpret_cast<uint32_t*>(sc + 256 + (size_t)num_sms * NQ * 32 * sizeof(uint64_t));
+  a.gkey = reinterpret_cast<uint64_t*>(sc + 256 + (size_t)num_sms * NQ * 32 * 12);
+  a.gid = reinterpret_cast<uint32_t*>(sc + 256 + (size_t)num_sms * NQ * 32 * 12 +
+                                      (size_t)groups * NQ * 32 * sizeof(uint64_t));
   a.scores = scores;
   a.ids = ids;
   switch (NQ) {
