@@ -1056,6 +1056,7 @@ struct hsd_engine {
   hsd_verify_params* vp = nullptr;
   hsd_verify_params vp_last{};  // the values *vp holds (stream-ordered), valid when vp_set
   bool vp_set = false;
+  void* vp_stream = nullptr;     // the stream that copied them
 };
 
 static constexpr int kStepEvents = 6;
@@ -1288,10 +1289,12 @@ hsd_status hsd_step(hsd_engine* e, int B, const hsd_step_io* io, const hsd_verif
   // stream-ordered copy: the previous steps' verify kernels read their own
   // values first.  Unchanged parameters (every step of a run) skip it: a
   // pageable 64-B copy costs ~1.4 us of stream time at config 1.
-  if (!e->vp_set || std::memcmp(&e->vp_last, vp, sizeof *vp) != 0) {
+  // (only on the stream that made the copy: another stream is not ordered after it)
+  if (!e->vp_set || e->vp_stream != stream || std::memcmp(&e->vp_last, vp, sizeof *vp) != 0) {
     CU(cudaMemcpyAsync(e->vp, vp, sizeof *vp, cudaMemcpyHostToDevice, (cudaStream_t)stream));
     e->vp_last = *vp;
     e->vp_set = true;
+    e->vp_stream = stream;
   }
   return step_impl(e, B, io, vp, e->vp, mp, nb, gap_d, stream);
 }
