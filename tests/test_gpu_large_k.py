@@ -90,3 +90,24 @@ def test_large_k_empty_and_errors(torch):
     col.generate(O.REAL, 1, 10)
     with pytest.raises(H.InvalidInputError):
         col.search_topk_exact(q, 0)
+
+
+def test_large_k_wide_rows_and_limit(torch):
+    """Wide rows: the fp64 query slab of the scan bounds the dim (one query per pass near the
+    limit); beyond it k > 32 is rejected with InvalidInput, k <= 32 still searches."""
+    n, dim = 400, 16384
+    col = H.Collection(dim, capacity=n)
+    col.generate(O.REAL, 12, n)
+    q = H.gen_queries(O.REAL, 13, 12, n, 0, 3, dim)
+    sc, ids = col.search_topk_exact(q, 50)
+    osc, oid = O.search_synth(O.REAL, 12, n, q.cpu().numpy(), 50)
+    np.testing.assert_array_equal(ids.cpu().numpy(), oid)
+    np.testing.assert_array_equal(sc.cpu().numpy(), osc)
+    big = H.Collection(20480, capacity=64)
+    big.generate(O.REAL, 14, 64)
+    qb = H.gen_queries(O.REAL, 15, 14, 64, 0, 1, 20480)
+    with pytest.raises(H.InvalidInputError):
+        big.search_topk_exact(qb, 40)
+    sc, ids = big.search_topk_exact(qb, 8)
+    osc, oid = O.search_synth(O.REAL, 14, 64, qb.cpu().numpy(), 8)
+    np.testing.assert_array_equal(ids.cpu().numpy(), oid)
