@@ -381,13 +381,13 @@ constexpr int kPairKS = 8, kPairQS = 4;
 
 // kConv: fp32 keys converted to bf16 on chip.  Per 64-column k-chunk the key
 // producer TMA-loads two fp32 boxes (128 rows x 32 columns each, 32 KB) into
-// a raw ring; four converter warps round them to bf16 (RN-even, the same
+// a raw ring; eight converter warps round them to bf16 (RN-even, the same
 // rounding as the bf16 filter copy) into the SWIZZLE_128B K-major tile that
 // kind::f16 reads, so the pair runs bf16 MMAs (half the tensor work of TF32)
 // while HBM still carries each fp32 key once.  Queries: the bf16 slab.  The
 // filter bound is the bf16-copy one (both operands bf16-rounded).
 constexpr int kConvRawS = 3, kConvKS = 3, kConvQS = 3;
-constexpr int kConvWarps = 4;
+constexpr int kConvWarps = 8;
 constexpr int kConvThreads = kThreads + 32 * kConvWarps;
 
 template <bool kConv>
